@@ -1,0 +1,315 @@
+"""TEST INFRASTRUCTURE — numpy restatement of the reference plan executor.
+
+This is the CHECKER, never the product: only tests/, ``__graft_entry__.smoke()``
+and bench.py's ``cpu_baseline`` leg may import it. It restates, in float64
+numpy, the reference's CPU executor ``planc::run_plan`` and its helpers:
+
+* ``reconstruct``      — reference proj/src/refexec.cpp:102-140
+* ``eval_compute``     — refexec.cpp:142-257 (matmul 142-168, elementwise
+                         178-193, reduce-sum 194-215, embedding 216-250,
+                         identity 251-252)
+* ``run_plan``         — refexec.cpp:361-557 (lane cursor loop 483-522,
+                         collective rendezvous 459-481, reassembly 532-556)
+* ``compare_outputs``  — refexec.cpp:604-631
+
+Two deliberate extensions over the reference, both
+off by default so the restatement is bit-compatible with the reference:
+
+* ``vv=True``: a piece whose value_count is a multiple m of the target's
+  contributes (summed) to target value index vi when piece_vi // m == vi —
+  the multi-step V(4)->V(2)->V(1) reductions the reference throws on
+  (slot arithmetic of rvd.cpp:226-251).
+* ``return_vtensors=True`` additionally returns every produced vTensor's
+  value (the reference only returns reassembled pTensors).
+
+Parity pinning: tests/test_oracle.py checks this module against the compiled
+reference (oracle/_ref) and the golden fixtures in tests/golden/.
+"""
+from __future__ import annotations
+
+import json
+
+import numpy as np
+
+
+class UsageError(RuntimeError):
+    pass
+
+
+class InternalError(RuntimeError):
+    pass
+
+
+def _region_intersect(a, b):
+    out = []
+    for (alo, ahi), (blo, bhi) in zip(a, b):
+        lo, hi = max(alo, blo), min(ahi, bhi)
+        if lo >= hi:
+            return None
+        out.append((lo, hi))
+    return out
+
+
+def _vol(region):
+    v = 1
+    for lo, hi in region:
+        v *= hi - lo
+    return v
+
+
+def _sl(region, origin):
+    return tuple(slice(lo - o[0], hi - o[0]) for (lo, hi), o in zip(region, origin))
+
+
+def reconstruct(target, pieces, ctx="", vv=False):
+    """refexec.cpp:102-140. target/pieces masks are dicts with region, vi, vc."""
+    treg = target["region"]
+    out = np.zeros([hi - lo for lo, hi in treg], dtype=np.float64)
+    touched = 0
+    for mask, value in pieces:
+        if mask["vc"] == target["vc"] and mask["vi"] == target["vi"]:
+            copy = True
+        elif target["vc"] == 1 and mask["vc"] > 1:
+            copy = False
+        elif (vv and mask["vc"] > target["vc"] and mask["vc"] % target["vc"] == 0
+              and mask["vi"] // (mask["vc"] // target["vc"]) == target["vi"]):
+            copy = False
+        else:
+            continue
+        ov = _region_intersect(mask["region"], treg)
+        if ov is None:
+            continue
+        dst = _sl(ov, treg)
+        src = value[_sl(ov, mask["region"])]
+        if copy:
+            out[dst] = src
+        else:
+            out[dst] += src
+        touched += _vol(ov)
+    if touched < _vol(treg):
+        raise InternalError(f"reconstruct: region {treg} not fully covered ({ctx})")
+    return out
+
+
+def eval_compute(op, ins, in_masks, out_masks):
+    """refexec.cpp:172-257."""
+    kind = op["kind"]
+    if kind == "matmul":
+        a, b = ins[0], ins[1]
+        a = a.T if op.get("transpose_a") else a
+        b = b.T if op.get("transpose_b") else b
+        if a.shape[1] != b.shape[0]:
+            raise InternalError("matmul operand inner extents differ in " + op["id"])
+        return [a @ b]
+    if kind in ("add", "mul", "max"):
+        out = ins[0].copy()
+        for x in ins[1:]:
+            if x.shape != out.shape:
+                raise InternalError("elementwise shape mismatch in " + op["id"])
+            if kind == "add":
+                out = out + x
+            elif kind == "mul":
+                out = out * x
+            else:
+                out = np.maximum(out, x)
+        return [out]
+    if kind == "reduce-sum":
+        axis = op.get("axis", 0)
+        out = ins[0].sum(axis=axis)
+        if out.ndim == 0:
+            out = out.reshape(1)
+        return [out]
+    if kind == "embedding-lookup":
+        idx, table = ins[0], ins[1]
+        lo = in_masks[1]["region"][0][0]
+        rows, h = table.shape
+        ids = idx.astype(np.int64)
+        out = np.zeros((idx.shape[0], h))
+        ok = (ids >= lo) & (ids < lo + rows)
+        out[ok] = table[ids[ok] - lo]
+        return [out]
+    if kind == "embedding-grad":
+        idx, gout = ins[0], ins[1]
+        (lo, hi) = out_masks[0]["region"][0]
+        rows = hi - lo
+        out = np.zeros((rows, gout.shape[1]))
+        ids = idx.astype(np.int64)
+        for j in range(ids.shape[0]):
+            if lo <= ids[j] < lo + rows:
+                out[ids[j] - lo] += gout[j]
+        return [out]
+    if kind == "identity":
+        return [ins[0].copy()]
+    raise UsageError(f"refexec: unsupported op kind {kind} ({op['id']})")
+
+
+class Plan:
+    """Parsed plan.json (wire form of ExecutionPlan, simulate.cpp:492-602)."""
+
+    def __init__(self, doc):
+        j = json.loads(doc) if isinstance(doc, str) else doc
+        self.ptensors = {p["id"]: p for p in j["ptensors"]}
+        self.vtensors = {}
+        for v in j["vtensors"]:
+            self.vtensors[v["id"]] = {
+                "id": v["id"], "pt": v["ptensor"],
+                "region": [tuple(iv) for iv in v["region"]],
+                "vi": v["value"][0], "vc": v["value"][1], "owner": v["owner"],
+            }
+        self.ops = j["ops"]
+        self.op = {o["id"]: o for o in self.ops}
+        self.assignment = j["assignment"]
+        self.feeds = {c: p for c, p in j["feeds"]}
+        self.coll_groups = {g["id"]: g for g in j["coll_groups"]}
+        self.lanes = j["lanes"]
+        self.sync_edges = j.get("sync_edges", [])
+        produced = set()
+        for o in self.ops:
+            for v in o["outputs"]:
+                produced.add(self.vtensors[v]["pt"])
+        self.graph_inputs = {p for p in self.ptensors if p not in produced}
+
+
+def run_plan(plan, inputs, vv=False, return_vtensors=False):
+    """refexec.cpp:361-557 restated. ``plan`` is a Plan or plan.json text."""
+    if not isinstance(plan, Plan):
+        plan = Plan(plan)
+    g = plan
+    vt_values = {}
+    channel_values = {}
+
+    def input_value(vt):
+        if vt["pt"] not in inputs:
+            raise UsageError(f"run_plan: missing input tensor {vt['pt']}")
+        if vt["vc"] != 1:
+            raise UsageError("run_plan: graph input consumed as partial value")
+        return np.asarray(inputs[vt["pt"]], dtype=np.float64)[_sl(vt["region"], [(0, 0)] * len(vt["region"]))].copy()
+
+    def feed_ready(cvt):
+        vt = g.vtensors[cvt]
+        if vt["pt"] in g.graph_inputs:
+            return True
+        if cvt not in g.feeds:
+            raise InternalError(f"run_plan: consumer view {cvt} of op {vt['owner']} has no feed")
+        return g.feeds[cvt] in vt_values
+
+    def feed_value(cvt):
+        if cvt in g.feeds:
+            return vt_values[g.feeds[cvt]]
+        return input_value(g.vtensors[cvt])
+
+    def mask(v):
+        return g.vtensors[v]
+
+    members = {gid: set(grp["ops"]) for gid, grp in g.coll_groups.items()}
+    cursor = [0] * len(g.lanes)
+    op_pos = {}
+    for l, lane in enumerate(g.lanes):
+        for t, task in enumerate(lane["tasks"]):
+            op_pos[task["op"]] = (l, t)
+
+    def arrived(oid):
+        l, t = op_pos[oid]
+        return cursor[l] == t
+
+    def exec_op(op):
+        k = op["kind"]
+        if k == "free":
+            return
+        if k == "send":
+            channel_values[op["channel"]] = feed_value(op["inputs"][0])
+            return
+        if k == "recv":
+            vt_values[op["outputs"][0]] = channel_values[op["channel"]]
+            return
+        if k in ("split", "concat", "reduce-assemble"):
+            pieces = [(mask(v), feed_value(v)) for v in op["inputs"]]
+            for out in op["outputs"]:
+                vt_values[out] = reconstruct(mask(out), pieces, "op " + op["id"], vv)
+            return
+        ins = [feed_value(v) for v in op["inputs"]]
+        outs = eval_compute(op, ins, [mask(v) for v in op["inputs"]], [mask(v) for v in op["outputs"]])
+        for v, val in zip(op["outputs"], outs):
+            vt_values[v] = val
+
+    def exec_collective(grp):
+        pieces = []
+        for oid in grp["ops"]:
+            for v in g.op[oid]["inputs"]:
+                pieces.append((mask(v), feed_value(v)))
+        for oid in grp["ops"]:
+            for out in g.op[oid]["outputs"]:
+                vt_values[out] = reconstruct(mask(out), pieces, "collective " + oid, vv)
+
+    progress = True
+    while progress:
+        progress = False
+        for l, lane in enumerate(g.lanes):
+            tasks = lane["tasks"]
+            while cursor[l] < len(tasks):
+                op = g.op[tasks[cursor[l]]["op"]]
+                if op["kind"] == "recv":
+                    ready = op["channel"] in channel_values
+                elif op["kind"] == "collective":
+                    ready = all(arrived(m) for m in members[op["coll_group"]])
+                    if ready:
+                        ready = all(feed_ready(v) for m in members[op["coll_group"]] for v in g.op[m]["inputs"])
+                else:
+                    ready = all(feed_ready(v) for v in op["inputs"])
+                if not ready:
+                    break
+                if op["kind"] == "collective":
+                    exec_collective(g.coll_groups[op["coll_group"]])
+                    for m in members[op["coll_group"]]:
+                        ml, mt = op_pos[m]
+                        cursor[ml] = mt + 1
+                else:
+                    exec_op(op)
+                    cursor[l] += 1
+                progress = True
+    for l, lane in enumerate(g.lanes):
+        if cursor[l] < len(lane["tasks"]):
+            raise InternalError(f"run_plan: pairing deadlock at task {lane['tasks'][cursor[l]]['op']} "
+                                f"on device {lane['device']}")
+
+    outputs = {}
+    piece_vts = {}
+    for op in g.ops:
+        if op["inserted"]:
+            continue
+        for v in op["outputs"]:
+            piece_vts.setdefault(mask(v)["pt"], []).append(v)
+    for pt_id, vts in sorted(piece_vts.items()):
+        seen = set()
+        pieces = []
+        for v in vts:
+            m = mask(v)
+            key = (tuple(m["region"]), m["vi"], m["vc"])
+            if key in seen:
+                continue
+            seen.add(key)
+            pieces.append((m, vt_values[v]))
+        shape = g.ptensors[pt_id]["shape"]
+        full = {"region": [(0, e) for e in shape], "vi": 0, "vc": 1}
+        outputs[pt_id] = reconstruct(full, pieces, f"output {pt_id}", vv)
+    if return_vtensors:
+        return outputs, vt_values
+    return outputs
+
+
+def compare_outputs(expected, actual, rel_tol=0.0):
+    """refexec.cpp:604-631: |e-a| <= tol*max(1,|e|), exact when tol == 0."""
+    for pid in sorted(expected):
+        e = np.asarray(expected[pid])
+        if pid not in actual or tuple(np.shape(actual[pid])) != tuple(e.shape):
+            return False, f"mismatch on tensor {pid} (missing or shape)"
+        a = np.asarray(actual[pid], dtype=np.float64)
+        if rel_tol == 0.0:
+            bad = e != a
+        else:
+            bad = np.abs(e - a) > rel_tol * np.maximum(1.0, np.abs(e))
+        if bad.any():
+            idx = np.unravel_index(int(np.argmax(bad)), e.shape)
+            return False, (f"mismatch on tensor {pid} at {list(map(int, idx))}: "
+                           f"expected {e[idx]}, got {a[idx]}")
+    return True, "ok"

@@ -1,0 +1,357 @@
+// TEST INFRASTRUCTURE — the reference-side checker, never the product.
+//
+// A thin extern "C" shim over the UNMODIFIED reference planc library, built
+// from /root/reference/proj sources into oracle/_ref/libplanc_ref.so by
+// oracle/Makefile. Only tests/, __graft_entry__.smoke() and bench.py's
+// cpu_baseline / --impl reference legs load it. It exposes:
+//   * the reference front end (load_graph -> strategy -> compile -> save_plan),
+//     reference proj/src/compile.cpp:7-67, strategies.cpp:679-712;
+//   * the reference fixtures' graph documents (proj/tests/testutil.cpp:28-368);
+//   * the oracle (run_reference, refexec.cpp:264-350), the CPU plan executor
+//     the product replaces (run_plan, refexec.cpp:361-557), seeded inputs
+//     (random_integer_inputs, refexec.cpp:559-590) and compare_outputs.
+// Tensor maps cross the ABI as a flat int64/double blob:
+//   int64 count; per tensor: int64 id, int64 rank, int64 shape[rank],
+//   double data[volume].
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "planc/compile.hpp"
+#include "planc/refexec.hpp"
+#include "planc/simulate.hpp"
+#include "planc/strategies.hpp"
+#include "planc/transform.hpp"
+#include "testutil.hpp"
+
+using namespace planc;
+
+namespace {
+
+thread_local std::string g_err;
+
+char* dup_string(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+std::map<std::string, std::string> parse_kv(const char* spec) {
+  std::map<std::string, std::string> kv;
+  std::stringstream ss(spec ? spec : "");
+  std::string item;
+  while (std::getline(ss, item, ';')) {
+    auto eq = item.find('=');
+    if (eq == std::string::npos) continue;
+    kv[item.substr(0, eq)] = item.substr(eq + 1);
+  }
+  return kv;
+}
+
+std::vector<std::string> split_csv(const std::string& s) {
+  std::vector<std::string> out;
+  std::stringstream ss(s);
+  std::string item;
+  while (std::getline(ss, item, ',')) {
+    if (!item.empty()) out.push_back(item);
+  }
+  return out;
+}
+
+std::vector<char> encode(const TensorMap& m) {
+  std::vector<char> out;
+  auto put = [&](const void* p, std::size_t n) {
+    out.insert(out.end(), static_cast<const char*>(p),
+               static_cast<const char*>(p) + n);
+  };
+  std::int64_t count = static_cast<std::int64_t>(m.size());
+  put(&count, 8);
+  for (const auto& [id, t] : m) {
+    std::int64_t i = id, r = static_cast<std::int64_t>(t.shape.size());
+    put(&i, 8);
+    put(&r, 8);
+    put(t.shape.data(), 8 * t.shape.size());
+    put(t.data.data(), 8 * t.data.size());
+  }
+  return out;
+}
+
+TensorMap decode(const char* blob) {
+  TensorMap m;
+  const char* p = blob;
+  auto get = [&](void* dst, std::size_t n) {
+    std::memcpy(dst, p, n);
+    p += n;
+  };
+  std::int64_t count = 0;
+  get(&count, 8);
+  for (std::int64_t c = 0; c < count; ++c) {
+    std::int64_t id = 0, rank = 0;
+    get(&id, 8);
+    get(&rank, 8);
+    ConcreteTensor t;
+    t.shape.resize(static_cast<std::size_t>(rank));
+    get(t.shape.data(), 8 * rank);
+    t.data.resize(static_cast<std::size_t>(t.volume()));
+    get(t.data.data(), 8 * t.data.size());
+    m[static_cast<int>(id)] = std::move(t);
+  }
+  return m;
+}
+
+char* blob_out(const TensorMap& m, std::int64_t* nbytes) {
+  auto v = encode(m);
+  char* p = static_cast<char*>(std::malloc(v.size()));
+  std::memcpy(p, v.data(), v.size());
+  if (nbytes) *nbytes = static_cast<std::int64_t>(v.size());
+  return p;
+}
+
+// Megatron-style tensor parallelism written as an sProgram over op_trans, the
+// way the reference's own TP test does it (proj/tests/test_refexec.cpp:100-140):
+// forward ops whose id starts with "col" split output dim 1 (column-parallel
+// GEMM), "row" value-split (row-parallel GEMM -> partial sums), "tp" split
+// output dim 1 (elementwise ops between the column- and row-parallel GEMMs),
+// everything else is replicated. Backward ops follow their forward op through
+// adapt_backward (transform.cpp:503); optimizer ops "optc" / "optr" split like
+// their column- / row-parallel weight (dim 1 / dim 0), others are replicated.
+StrategyInfo megatron_tp(PlanGraph& g, const ClusterSpec& env,
+                         const StrategyConfig& cfg) {
+  int n = cfg.devices;
+  std::vector<std::string> snapshot;
+  for (const auto& op : g.ops) snapshot.push_back(op.id);
+  auto has_backward = [&](const std::string& fwd) {
+    for (const auto& o : g.ops) {
+      if (o.backward_of && *o.backward_of == fwd) return true;
+    }
+    return false;
+  };
+  for (const auto& oid : snapshot) {
+    if (!g.has_op(oid)) continue;
+    const OpNode& op = g.op(oid);
+    if (op.direction == OpDirection::backward) continue;
+    TransformAlgo algo = replica_algo(n);
+    // Role prefix of the op id's last '.'-separated component.
+    std::string role = oid.substr(oid.rfind('.') == std::string::npos
+                                      ? 0
+                                      : oid.rfind('.') + 1);
+    auto is = [&](const char* p) { return role.rfind(p, 0) == 0; };
+    if (op.direction == OpDirection::forward) {
+      if (is("col") || is("tp")) {
+        algo = split_algo(1, n);
+      } else if (is("row")) {
+        algo = value_split_algo(n);
+      }
+    } else if (op.direction == OpDirection::optimizer) {
+      if (is("optc")) algo = split_algo(1, n);
+      if (is("optr")) algo = split_algo(0, n);
+    }
+    std::vector<std::string> bwd;
+    if (has_backward(oid)) bwd = adapt_backward(g, oid, algo);
+    auto ids = op_trans(g, oid, algo);
+    for (std::size_t i = 0; i < ids.size(); ++i) {
+      op_assign(g, env, ids[i], static_cast<int>(i % n));
+    }
+    for (std::size_t i = 0; i < bwd.size(); ++i) {
+      op_assign(g, env, bwd[i], static_cast<int>(i % n));
+    }
+  }
+  return {};
+}
+
+// Hand-written sProgram in the style of the reference's adapter tests
+// (test_refexec.cpp:100-140, test_commplan.cpp:303-366): target_ops lists
+// "op@algo" with algo v (value split), sD (split output dim D), r (replica)
+// or e (vocabulary-sharded embedding); replacement i goes to device i.
+// Paired backward ops follow through adapt_backward. Unlisted ops stay whole
+// on device 0.
+StrategyInfo manual(PlanGraph& g, const ClusterSpec& env,
+                    const StrategyConfig& cfg) {
+  int n = cfg.devices;
+  std::map<std::string, std::string> algo_of;
+  for (const auto& t : cfg.target_ops) {
+    auto at = t.find('@');
+    if (at == std::string::npos) throw UsageError("manual: bad target " + t);
+    algo_of[t.substr(0, at)] = t.substr(at + 1);
+  }
+  std::vector<std::string> snapshot;
+  for (const auto& op : g.ops) snapshot.push_back(op.id);
+  for (const auto& oid : snapshot) {
+    if (!g.has_op(oid)) continue;
+    auto it = algo_of.find(oid);
+    if (it == algo_of.end()) continue;
+    const std::string& a = it->second;
+    TransformAlgo algo = replica_algo(n);
+    if (a == "v") algo = value_split_algo(n);
+    else if (a == "e") algo = shard_embed_algo(n);
+    else if (a[0] == 's') algo = split_algo(std::stoi(a.substr(1)), n);
+    bool paired = false;
+    for (const auto& o : g.ops) {
+      if (o.backward_of && *o.backward_of == oid) paired = true;
+    }
+    std::vector<std::string> bwd;
+    if (paired) bwd = adapt_backward(g, oid, algo);
+    auto ids = op_trans(g, oid, algo);
+    for (std::size_t i = 0; i < ids.size(); ++i) {
+      op_assign(g, env, ids[i], static_cast<int>(i % n));
+    }
+    for (std::size_t i = 0; i < bwd.size(); ++i) {
+      op_assign(g, env, bwd[i], static_cast<int>(i % n));
+    }
+  }
+  for (const auto& op : g.ops) {
+    if (!g.assignment.count(op.id)) op_assign(g, env, op.id, 0);
+  }
+  return {};
+}
+
+struct Registrar {
+  Registrar() {
+    register_strategy("megatron_tp", megatron_tp);
+    register_strategy("manual", manual);
+  }
+} registrar;
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+void ref_free(void* p) { std::free(p); }
+
+char* ref_mlp_doc(int layers, std::int64_t batch, std::int64_t hidden,
+                  int optimizer, int bias, int weight_grads) {
+  testutil::MlpSpec s;
+  s.layers = layers;
+  s.batch = batch;
+  s.hidden = hidden;
+  s.optimizer = optimizer != 0;
+  s.bias = bias != 0;
+  s.weight_grads = weight_grads != 0;
+  return dup_string(testutil::mlp_doc(s));
+}
+
+char* ref_coshard_doc(std::int64_t b, std::int64_t h, std::int64_t m) {
+  return dup_string(testutil::coshard_doc({b, h, m}));
+}
+
+char* ref_embed_doc(int stage_layers, std::int64_t b, std::int64_t v,
+                    std::int64_t h) {
+  return dup_string(testutil::embed_doc({stage_layers, b, v, h}));
+}
+
+char* ref_three_pass_doc(int layers, std::int64_t b, std::int64_t h) {
+  return dup_string(testutil::three_pass_doc({layers, b, h}));
+}
+
+char* ref_chain_doc() { return dup_string(testutil::chain_doc()); }
+
+// spec: "strategy=...;devices=N;micro_batches=K;stages=S;shards=n;
+//        target_ops=a,b;inner_dp=d;pattern_match=0|1;cluster_devices=N;
+//        group_size=G;intra_bw=..;intra_lat=..;inter_bw=..;inter_lat=..;
+//        throughput=..;testutil_cluster=0|1"
+char* ref_compile(const char* graph_doc, const char* spec) {
+  try {
+    auto kv = parse_kv(spec);
+    auto geti = [&](const char* k, int d) {
+      return kv.count(k) ? std::stoi(kv[k]) : d;
+    };
+    auto getd = [&](const char* k, double d) {
+      return kv.count(k) ? std::stod(kv[k]) : d;
+    };
+    StrategyConfig c;
+    c.strategy = kv.count("strategy") ? kv["strategy"] : "none";
+    c.devices = geti("devices", 1);
+    c.micro_batches = geti("micro_batches", 1);
+    c.stages = geti("stages", 1);
+    c.shards = geti("shards", 1);
+    c.inner_dp = geti("inner_dp", 1);
+    if (kv.count("target_ops")) c.target_ops = split_csv(kv["target_ops"]);
+    int ndev = geti("cluster_devices", c.devices);
+    ClusterSpec cluster;
+    if (geti("testutil_cluster", 0)) {
+      cluster = testutil::make_cluster(ndev, geti("group_size", 0));
+    } else {
+      cluster = ClusterSpec::uniform(
+          ndev, geti("group_size", ndev), std::int64_t{180} << 30,
+          {getd("intra_bw", 900e9), getd("intra_lat", 3e-6)},
+          {getd("inter_bw", 50e9), getd("inter_lat", 10e-6)},
+          getd("throughput", 1.39e15));
+    }
+    auto result = compile(load_graph(graph_doc), cluster, c,
+                          geti("pattern_match", 1) != 0);
+    return dup_string(save_plan(result.plan));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+char* ref_random_inputs(const char* graph_doc, std::uint64_t seed,
+                        int magnitude, std::int64_t* nbytes) {
+  try {
+    auto g = load_graph(graph_doc);
+    return blob_out(random_integer_inputs(g, seed, magnitude), nbytes);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+char* ref_run_reference(const char* graph_doc, const char* inputs,
+                        std::int64_t* nbytes) {
+  try {
+    auto g = load_graph(graph_doc);
+    return blob_out(run_reference(g, decode(inputs)), nbytes);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// Runs the reference CPU plan executor `iters` times; reports mean seconds
+// per run_plan call (plan parsing excluded) and returns the last outputs.
+char* ref_run_plan(const char* plan_json, const char* inputs, int iters,
+                   double* seconds_per_iter, std::int64_t* nbytes) {
+  try {
+    auto plan = load_plan(plan_json);
+    auto in = decode(inputs);
+    TensorMap out;
+    if (iters < 1) iters = 1;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < iters; ++i) out = run_plan(plan, in);
+    auto t1 = std::chrono::steady_clock::now();
+    if (seconds_per_iter) {
+      *seconds_per_iter =
+          std::chrono::duration<double>(t1 - t0).count() / iters;
+    }
+    return blob_out(out, nbytes);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// Re-serializes a plan through the reference's own load_plan/save_plan.
+char* ref_roundtrip_plan(const char* plan_json) {
+  try {
+    return dup_string(save_plan(load_plan(plan_json)));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// 0 = equal (within rel_tol), 1 = mismatch (message in ref_last_error()).
+int ref_compare(const char* expected, const char* actual, double rel_tol) {
+  auto r = compare_outputs(decode(expected), decode(actual), rel_tol);
+  g_err = r.to_string();
+  return r.ok ? 0 : 1;
+}
+
+}  // extern "C"
