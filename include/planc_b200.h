@@ -1,0 +1,126 @@
+/*
+ * planc_b200 — C ABI of the B200-native SuperScaler plan executor.
+ *
+ * Drop-in boundary for the reference's plan-execution path:
+ *
+ *   TensorMap planc::run_plan(const ExecutionPlan& plan, const TensorMap& inputs)
+ *     reference /root/reference/proj/include/planc/refexec.hpp:43,
+ *     implementation proj/src/refexec.cpp:361-557
+ *
+ * The plan crosses the ABI in its wire form, the plan.json text produced by
+ * planc::save_plan (proj/src/simulate.cpp:492-602) and read with the same keys
+ * as planc::load_plan (simulate.cpp:604-739). TensorMap values cross as
+ * dense row-major double arrays keyed by pTensor id, exactly the
+ * ConcreteTensor{shape, data} layout (refexec.hpp:19-32).
+ *
+ * Error behaviour mirrors the reference's exception classes
+ * (proj/include/planc/util.hpp:17-29) as return codes; the message is
+ * available from planc_b200_last_error():
+ *   PLANC_B200_OK        0
+ *   PLANC_B200_EINTERNAL 1  InternalError (no feed, pairing deadlock,
+ *                            uncovered reconstruct region, ...)
+ *   PLANC_B200_ECUDA     2  CUDA runtime / device failure
+ *   PLANC_B200_EUSAGE    4  SchemaError / UsageError (malformed plan, missing
+ *                            input, partial-value graph input, unsupported op
+ *                            kind) — the CLI's exit code 4 (tools/planc.cpp:18-20)
+ * No exception crosses the ABI. One handle is used from one host thread.
+ */
+#ifndef PLANC_B200_H_
+#define PLANC_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PLANC_B200_OK 0
+#define PLANC_B200_EINTERNAL 1
+#define PLANC_B200_ECUDA 2
+#define PLANC_B200_EUSAGE 4
+
+/* Open flags. */
+#define PLANC_B200_NO_GRAPH 0x1u        /* issue eagerly instead of replaying a CUDA graph */
+#define PLANC_B200_NO_TENSOR_CORES 0x2u /* force the SIMT GEMM (debug / A-B checks) */
+#define PLANC_B200_STRICT_VALUE 0x4u    /* reference value-part rule only: V(m*v)->V(v) pieces are
+                                           skipped like refexec.cpp:110-117 instead of summed */
+
+typedef struct planc_b200_exec planc_b200_exec;
+
+/* Last error of the calling thread (handle-less calls) or of any handle. */
+const char* planc_b200_last_error(void);
+
+/* Compiles a plan for the GPU: buffers, kernels, cross-lane events, box
+ * programs. lane_gpu[i] is the CUDA device ordinal that runs plan lane i
+ * (lanes are the plan's DeviceLanes in document order, simulate.hpp:32-35);
+ * NULL or num_lane_gpu == 0 maps every lane to device 0, fewer entries than
+ * lanes wrap around. Replaces load_plan + the set-up half of run_plan. */
+int planc_b200_open(const char* plan_json, const int* lane_gpu, int num_lane_gpu, uint32_t flags,
+                    planc_b200_exec** out);
+void planc_b200_close(planc_b200_exec* h);
+
+/* Binds one graph-input pTensor (refexec.cpp:366-376); `data` is dense
+ * row-major with `rank` extents `shape`. Copied; placed on the GPU at the
+ * next run. */
+int planc_b200_set_input(planc_b200_exec* h, int ptensor, const double* data, const int64_t* shape, int rank);
+
+/* Executes the plan `iters` times (>= 1) back to back; *ms_per_step receives
+ * the mean device time per step (CUDA events, origin stream). iters == 0
+ * runs one untimed step (verification). */
+int planc_b200_run(planc_b200_exec* h, int iters, double* ms_per_step);
+
+/* End-to-end steps: per step H2D of every non-weight graph input from
+ * pinned host memory, the plan step, D2H of every terminal non-weight
+ * output piece. */
+int planc_b200_run_e2e(planc_b200_exec* h, int iters, double* ms_per_step, int64_t* h2d_bytes_per_step,
+                       int64_t* d2h_bytes_per_step);
+
+/* Produced pTensors (refexec.cpp:532-556), ascending id. Returns the count;
+ * writes up to `cap` ids. */
+int planc_b200_num_outputs(planc_b200_exec* h);
+int planc_b200_output_ids(planc_b200_exec* h, int* ids, int cap);
+/* Rank / shape of a pTensor. */
+int planc_b200_ptensor_shape(planc_b200_exec* h, int ptensor, int64_t* shape, int cap, int* rank);
+/* Reassembled value of a produced pTensor as doubles (volume elements). */
+int planc_b200_get_output(planc_b200_exec* h, int ptensor, double* out, int64_t capacity);
+
+/* Graph-input pTensors the plan places (ascending id). */
+int planc_b200_num_inputs(planc_b200_exec* h);
+int planc_b200_input_ids(planc_b200_exec* h, int* ids, int cap);
+
+/* Step accounting (algorithmic, from task masks). */
+typedef struct planc_b200_stats {
+  int num_lanes;
+  int num_tasks;
+  int num_instructions;
+  int kernels_per_step;   /* kernel launches of one step */
+  int gemm_tc_per_step;   /* of which tcgen05 GEMMs */
+  int graph_captured;     /* 1 when steps replay one CUDA graph */
+  double flops;           /* total GEMM + elementwise FLOPs of one step */
+  double hbm_bytes;       /* memory-bound kernels' bytes (reads + writes) */
+  double wire_bytes;      /* adapter bytes by NCCL bus-bandwidth convention */
+  double max_lane_gemm_flops;
+  double max_lane_hbm_bytes;
+  double max_lane_wire_bytes;
+  int64_t device_bytes;   /* arena bytes over all lanes */
+} planc_b200_stats;
+int planc_b200_get_stats(planc_b200_exec* h, planc_b200_stats* out);
+
+/* Per-kernel-family timing of one eagerly issued, serialised step.
+ * Returns a JSON array [{"kind","launches","ms","flops","bytes","wire_bytes"}]
+ * (caller frees with planc_b200_free). */
+int planc_b200_profile(planc_b200_exec* h, char** json_out);
+
+/* Host-only lowering (no GPU needed): the executor's device program for a
+ * plan as JSON — buffers, instructions, box cells, issue order. */
+int planc_b200_describe(const char* plan_json, uint32_t flags, char** json_out);
+void planc_b200_free(void* p);
+
+/* Library identity: "planc_b200 <version> sm_100a". */
+const char* planc_b200_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PLANC_B200_H_ */

@@ -166,18 +166,29 @@ StrategyInfo megatron_tp(PlanGraph& g, const ClusterSpec& env,
 
 // Hand-written sProgram in the style of the reference's adapter tests
 // (test_refexec.cpp:100-140, test_commplan.cpp:303-366): target_ops lists
-// "op@algo" with algo v (value split), sD (split output dim D), r (replica)
-// or e (vocabulary-sharded embedding); replacement i goes to device i.
+// "op@algo[@offset[@count]]" with algo v (value split), sD (split output dim
+// D), r (replica) or e (vocabulary-sharded embedding), fanned out `count`
+// ways (default: devices); replacement i goes to device offset + i.
 // Paired backward ops follow through adapt_backward. Unlisted ops stay whole
 // on device 0.
 StrategyInfo manual(PlanGraph& g, const ClusterSpec& env,
                     const StrategyConfig& cfg) {
   int n = cfg.devices;
-  std::map<std::string, std::string> algo_of;
+  struct Target {
+    std::string algo;
+    int offset = 0;
+    int count = 0;
+  };
+  std::map<std::string, Target> algo_of;
   for (const auto& t : cfg.target_ops) {
-    auto at = t.find('@');
-    if (at == std::string::npos) throw UsageError("manual: bad target " + t);
-    algo_of[t.substr(0, at)] = t.substr(at + 1);
+    std::vector<std::string> f;
+    std::stringstream ss(t);
+    std::string item;
+    while (std::getline(ss, item, '@')) f.push_back(item);
+    if (f.size() < 2) throw UsageError("manual: bad target " + t);
+    Target tg{f[1], f.size() > 2 ? std::stoi(f[2]) : 0,
+              f.size() > 3 ? std::stoi(f[3]) : n};
+    algo_of[f[0]] = tg;
   }
   std::vector<std::string> snapshot;
   for (const auto& op : g.ops) snapshot.push_back(op.id);
@@ -185,11 +196,12 @@ StrategyInfo manual(PlanGraph& g, const ClusterSpec& env,
     if (!g.has_op(oid)) continue;
     auto it = algo_of.find(oid);
     if (it == algo_of.end()) continue;
-    const std::string& a = it->second;
-    TransformAlgo algo = replica_algo(n);
-    if (a == "v") algo = value_split_algo(n);
-    else if (a == "e") algo = shard_embed_algo(n);
-    else if (a[0] == 's') algo = split_algo(std::stoi(a.substr(1)), n);
+    const std::string& a = it->second.algo;
+    int cnt = it->second.count, off = it->second.offset;
+    TransformAlgo algo = replica_algo(cnt);
+    if (a == "v") algo = value_split_algo(cnt);
+    else if (a == "e") algo = shard_embed_algo(cnt);
+    else if (a[0] == 's') algo = split_algo(std::stoi(a.substr(1)), cnt);
     bool paired = false;
     for (const auto& o : g.ops) {
       if (o.backward_of && *o.backward_of == oid) paired = true;
@@ -198,10 +210,10 @@ StrategyInfo manual(PlanGraph& g, const ClusterSpec& env,
     if (paired) bwd = adapt_backward(g, oid, algo);
     auto ids = op_trans(g, oid, algo);
     for (std::size_t i = 0; i < ids.size(); ++i) {
-      op_assign(g, env, ids[i], static_cast<int>(i % n));
+      op_assign(g, env, ids[i], off + static_cast<int>(i % cnt));
     }
     for (std::size_t i = 0; i < bwd.size(); ++i) {
-      op_assign(g, env, bwd[i], static_cast<int>(i % n));
+      op_assign(g, env, bwd[i], off + static_cast<int>(i % cnt));
     }
   }
   for (const auto& op : g.ops) {

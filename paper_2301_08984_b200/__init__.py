@@ -1,0 +1,248 @@
+"""planc_b200 — B200-native executor for SuperScaler parallelization plans.
+
+Python face of the C ABI in ``include/planc_b200.h`` (the product is the
+C++/CUDA library ``_lib/libplanc_b200.so``; this module only binds it).
+The API mirrors the reference's plan-execution interface
+(reference proj/include/planc/refexec.hpp:38-60):
+
+    run_plan(plan_json, inputs) -> outputs      # refexec.hpp:43
+    compare_outputs(expected, actual, rel_tol)  # refexec.hpp:58 (pure host)
+
+``inputs`` / ``outputs`` are TensorMaps: ``dict[int, numpy.ndarray]`` keyed
+by pTensor id (refexec.hpp:34), values dense row-major float64 like
+ConcreteTensor. Errors raise the reference's exception classes
+(SchemaError / UsageError / InternalError, util.hpp:17-29); device failures
+raise CudaError. There is no CPU fallback: without the built library or a
+GPU every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+import numpy as np
+
+__all__ = [
+    "Executor", "run_plan", "describe", "compare_outputs", "library_path",
+    "SchemaError", "UsageError", "InternalError", "CudaError",
+    "NO_GRAPH", "NO_TENSOR_CORES", "STRICT_VALUE",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_lib", "libplanc_b200.so")
+
+NO_GRAPH = 0x1
+NO_TENSOR_CORES = 0x2
+STRICT_VALUE = 0x4
+
+
+class PlancError(RuntimeError):
+    pass
+
+
+class SchemaError(PlancError):
+    pass
+
+
+class UsageError(PlancError):
+    pass
+
+
+class InternalError(PlancError):
+    pass
+
+
+class CudaError(PlancError):
+    pass
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [
+        ("num_lanes", ctypes.c_int), ("num_tasks", ctypes.c_int), ("num_instructions", ctypes.c_int),
+        ("kernels_per_step", ctypes.c_int), ("gemm_tc_per_step", ctypes.c_int), ("graph_captured", ctypes.c_int),
+        ("flops", ctypes.c_double), ("hbm_bytes", ctypes.c_double), ("wire_bytes", ctypes.c_double),
+        ("max_lane_gemm_flops", ctypes.c_double), ("max_lane_hbm_bytes", ctypes.c_double),
+        ("max_lane_wire_bytes", ctypes.c_double), ("device_bytes", ctypes.c_int64),
+    ]
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise RuntimeError(
+            f"planc_b200: native library missing ({_LIB_PATH}); build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` — there is no CPU fallback")
+    L = ctypes.CDLL(_LIB_PATH)
+    c_int, c_i64, c_dbl, vp = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+    P = ctypes.POINTER
+    L.planc_b200_last_error.restype = ctypes.c_char_p
+    L.planc_b200_version.restype = ctypes.c_char_p
+    L.planc_b200_open.argtypes = [ctypes.c_char_p, P(c_int), c_int, ctypes.c_uint32, P(vp)]
+    L.planc_b200_close.argtypes = [vp]
+    L.planc_b200_set_input.argtypes = [vp, c_int, P(c_dbl), P(c_i64), c_int]
+    L.planc_b200_run.argtypes = [vp, c_int, P(c_dbl)]
+    L.planc_b200_run_e2e.argtypes = [vp, c_int, P(c_dbl), P(c_i64), P(c_i64)]
+    L.planc_b200_num_outputs.argtypes = [vp]
+    L.planc_b200_output_ids.argtypes = [vp, P(c_int), c_int]
+    L.planc_b200_num_inputs.argtypes = [vp]
+    L.planc_b200_input_ids.argtypes = [vp, P(c_int), c_int]
+    L.planc_b200_ptensor_shape.argtypes = [vp, c_int, P(c_i64), c_int, P(c_int)]
+    L.planc_b200_get_output.argtypes = [vp, c_int, P(c_dbl), c_i64]
+    L.planc_b200_get_stats.argtypes = [vp, P(_Stats)]
+    L.planc_b200_profile.argtypes = [vp, P(ctypes.c_char_p)]
+    L.planc_b200_describe.argtypes = [ctypes.c_char_p, ctypes.c_uint32, P(vp)]
+    L.planc_b200_free.argtypes = [vp]
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc == 0:
+        return
+    msg = _load().planc_b200_last_error().decode()
+    if rc == 4:
+        raise (SchemaError if msg.startswith("SchemaError") else UsageError)(msg)
+    if rc == 2:
+        raise CudaError(msg)
+    raise InternalError(msg)
+
+
+def version() -> str:
+    return _load().planc_b200_version().decode()
+
+
+def describe(plan_json: str, strict_value: bool = False) -> dict:
+    """Host-only lowering of a plan (no GPU): buffers, instructions, cells."""
+    L = _load()
+    out = ctypes.c_void_p()
+    _check(L.planc_b200_describe(plan_json.encode(), STRICT_VALUE if strict_value else 0, ctypes.byref(out)))
+    s = ctypes.string_at(out.value).decode()
+    L.planc_b200_free(out)
+    return json.loads(s)
+
+
+class Executor:
+    """One compiled plan on the GPU(s). ``lane_gpus[i]`` runs plan lane i."""
+
+    def __init__(self, plan_json: str, lane_gpus=None, flags: int = 0):
+        L = _load()
+        self._h = ctypes.c_void_p()
+        arr, n = None, 0
+        if lane_gpus:
+            n = len(lane_gpus)
+            arr = (ctypes.c_int * n)(*lane_gpus)
+        _check(L.planc_b200_open(plan_json.encode(), arr, n, flags, ctypes.byref(self._h)))
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _load().planc_b200_close(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- inputs / outputs ------------------------------------------------
+    def input_ids(self):
+        L = _load()
+        n = L.planc_b200_num_inputs(self._h)
+        ids = (ctypes.c_int * max(n, 1))()
+        L.planc_b200_input_ids(self._h, ids, n)
+        return list(ids[:n])
+
+    def output_ids(self):
+        L = _load()
+        n = L.planc_b200_num_outputs(self._h)
+        ids = (ctypes.c_int * max(n, 1))()
+        L.planc_b200_output_ids(self._h, ids, n)
+        return list(ids[:n])
+
+    def shape(self, ptensor: int):
+        shp = (ctypes.c_int64 * 16)()
+        rank = ctypes.c_int()
+        _check(_load().planc_b200_ptensor_shape(self._h, ptensor, shp, 16, ctypes.byref(rank)))
+        return tuple(shp[: rank.value])
+
+    def set_input(self, ptensor: int, value):
+        a = np.ascontiguousarray(value, dtype=np.float64)
+        shp = (ctypes.c_int64 * max(a.ndim, 1))(*a.shape)
+        _check(_load().planc_b200_set_input(self._h, ptensor, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                            shp, a.ndim))
+
+    def set_inputs(self, inputs: dict):
+        for pid, v in inputs.items():
+            self.set_input(int(pid), v)
+
+    def get_output(self, ptensor: int) -> np.ndarray:
+        shp = self.shape(ptensor)
+        out = np.empty(shp, dtype=np.float64)
+        _check(_load().planc_b200_get_output(self._h, ptensor, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                             out.size))
+        return out
+
+    def outputs(self) -> dict:
+        return {pid: self.get_output(pid) for pid in self.output_ids()}
+
+    # -- execution --------------------------------------------------------
+    def run(self, iters: int = 0) -> float:
+        ms = ctypes.c_double()
+        _check(_load().planc_b200_run(self._h, iters, ctypes.byref(ms)))
+        return ms.value
+
+    def run_e2e(self, iters: int):
+        ms = ctypes.c_double()
+        hb, db = ctypes.c_int64(), ctypes.c_int64()
+        _check(_load().planc_b200_run_e2e(self._h, iters, ctypes.byref(ms), ctypes.byref(hb), ctypes.byref(db)))
+        return ms.value, hb.value, db.value
+
+    def stats(self) -> dict:
+        s = _Stats()
+        _check(_load().planc_b200_get_stats(self._h, ctypes.byref(s)))
+        return {k: getattr(s, k) for k, _ in _Stats._fields_}
+
+    def profile(self):
+        out = ctypes.c_char_p()
+        L = _load()
+        _check(L.planc_b200_profile(self._h, ctypes.byref(out)))
+        return json.loads(out.value.decode())
+
+
+def run_plan(plan_json: str, inputs: dict, lane_gpus=None, flags: int = 0) -> dict:
+    """Drop-in for ``planc::run_plan(plan, inputs)`` (refexec.hpp:43)."""
+    with Executor(plan_json, lane_gpus, flags) as ex:
+        ex.set_inputs(inputs)
+        ex.run(0)
+        return ex.outputs()
+
+
+def compare_outputs(expected: dict, actual: dict, rel_tol: float = 0.0):
+    """``planc::compare_outputs`` (refexec.cpp:604-631): |e-a| <= tol*max(1,|e|)."""
+    for pid in sorted(expected):
+        e = np.asarray(expected[pid], dtype=np.float64)
+        if pid not in actual or tuple(np.shape(actual[pid])) != e.shape:
+            return False, f"mismatch on tensor {pid} (missing or shape)"
+        a = np.asarray(actual[pid], dtype=np.float64)
+        bad = (e != a) if rel_tol == 0.0 else (np.abs(e - a) > rel_tol * np.maximum(1.0, np.abs(e)))
+        if bad.any():
+            idx = np.unravel_index(int(np.argmax(bad)), e.shape)
+            return False, (f"mismatch on tensor {pid} at {list(map(int, idx))}: "
+                           f"expected {e[idx]}, got {a[idx]}")
+    return True, "ok"

@@ -1,0 +1,208 @@
+// extern "C" boundary (include/planc_b200.h): exceptions become return
+// codes, mirroring the reference's error classes (util.hpp:17-29).
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+#include <string>
+
+#include "../../include/planc_b200.h"
+#include "runtime.hpp"
+
+using namespace planc_b200;
+
+struct planc_b200_exec {
+  Executor* ex = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return PLANC_B200_OK;
+  } catch (const SchemaError& e) {
+    g_last_error = std::string("SchemaError: ") + e.what();
+    return PLANC_B200_EUSAGE;
+  } catch (const UsageError& e) {
+    g_last_error = std::string("UsageError: ") + e.what();
+    return PLANC_B200_EUSAGE;
+  } catch (const InternalError& e) {
+    g_last_error = std::string("InternalError: ") + e.what();
+    return PLANC_B200_EINTERNAL;
+  } catch (const std::exception& e) {
+    g_last_error = std::string("CudaError: ") + e.what();
+    return PLANC_B200_ECUDA;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return PLANC_B200_EINTERNAL;
+  }
+}
+
+char* dup(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* planc_b200_last_error(void) { return g_last_error.c_str(); }
+
+const char* planc_b200_version(void) { return "planc_b200 0.1.0 sm_100a"; }
+
+void planc_b200_free(void* p) { std::free(p); }
+
+int planc_b200_open(const char* plan_json, const int* lane_gpu, int num_lane_gpu, uint32_t flags,
+                    planc_b200_exec** out) {
+  return guarded([&] {
+    if (!plan_json || !out) throw UsageError("planc_b200_open: null argument");
+    ExecOptions opt;
+    opt.use_graph = (flags & PLANC_B200_NO_GRAPH) == 0;
+    opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
+    opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
+    std::vector<int> lanes;
+    for (int i = 0; lane_gpu && i < num_lane_gpu; ++i) lanes.push_back(lane_gpu[i]);
+    auto* h = new planc_b200_exec;
+    try {
+      h->ex = new Executor(plan_json, lanes, opt);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void planc_b200_close(planc_b200_exec* h) {
+  if (!h) return;
+  delete h->ex;
+  delete h;
+}
+
+int planc_b200_set_input(planc_b200_exec* h, int ptensor, const double* data, const int64_t* shape, int rank) {
+  return guarded([&] {
+    if (!h || !data || (rank > 0 && !shape)) throw UsageError("planc_b200_set_input: null argument");
+    std::vector<std::int64_t> s(shape, shape + rank);
+    h->ex->set_input(ptensor, data, s);
+  });
+}
+
+int planc_b200_run(planc_b200_exec* h, int iters, double* ms_per_step) {
+  return guarded([&] {
+    if (!h) throw UsageError("planc_b200_run: null handle");
+    double ms = h->ex->run(iters);
+    if (ms_per_step) *ms_per_step = ms;
+  });
+}
+
+int planc_b200_run_e2e(planc_b200_exec* h, int iters, double* ms_per_step, int64_t* h2d, int64_t* d2h) {
+  return guarded([&] {
+    if (!h) throw UsageError("planc_b200_run_e2e: null handle");
+    std::int64_t a = 0, b = 0;
+    double ms = h->ex->run_e2e(iters, &a, &b);
+    if (ms_per_step) *ms_per_step = ms;
+    if (h2d) *h2d = a;
+    if (d2h) *d2h = b;
+  });
+}
+
+int planc_b200_num_outputs(planc_b200_exec* h) { return h ? static_cast<int>(h->ex->output_ids().size()) : -1; }
+
+int planc_b200_output_ids(planc_b200_exec* h, int* ids, int cap) {
+  if (!h) return -1;
+  auto v = h->ex->output_ids();
+  for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i) ids[i] = v[i];
+  return static_cast<int>(v.size());
+}
+
+int planc_b200_num_inputs(planc_b200_exec* h) {
+  return h ? static_cast<int>(h->ex->program().graph_inputs.size()) : -1;
+}
+
+int planc_b200_input_ids(planc_b200_exec* h, int* ids, int cap) {
+  if (!h) return -1;
+  const auto& v = h->ex->program().graph_inputs;
+  for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i) ids[i] = v[i];
+  return static_cast<int>(v.size());
+}
+
+int planc_b200_ptensor_shape(planc_b200_exec* h, int ptensor, int64_t* shape, int cap, int* rank) {
+  return guarded([&] {
+    if (!h) throw UsageError("null handle");
+    const PTensor& pt = h->ex->plan().pt(ptensor);
+    if (rank) *rank = static_cast<int>(pt.shape.size());
+    for (int i = 0; i < cap && i < static_cast<int>(pt.shape.size()); ++i) shape[i] = pt.shape[i];
+  });
+}
+
+int planc_b200_get_output(planc_b200_exec* h, int ptensor, double* out, int64_t capacity) {
+  return guarded([&] {
+    if (!h || !out) throw UsageError("planc_b200_get_output: null argument");
+    HostTensor t = h->ex->get_output(ptensor);
+    if (static_cast<std::int64_t>(t.data.size()) > capacity) throw UsageError("output buffer too small");
+    std::memcpy(out, t.data.data(), t.data.size() * sizeof(double));
+  });
+}
+
+int planc_b200_get_stats(planc_b200_exec* h, planc_b200_stats* s) {
+  return guarded([&] {
+    if (!h || !s) throw UsageError("null argument");
+    const Program& p = h->ex->program();
+    const ExecutionPlan& pl = h->ex->plan();
+    std::memset(s, 0, sizeof(*s));
+    s->num_lanes = p.num_lanes;
+    for (const auto& l : pl.lanes) s->num_tasks += static_cast<int>(l.tasks.size());
+    s->num_instructions = static_cast<int>(p.instrs.size());
+    s->kernels_per_step = h->ex->kernels_per_step();
+    s->gemm_tc_per_step = h->ex->gemm_tc_launches();
+    s->graph_captured = h->ex->graph_captured() ? 1 : 0;
+    s->flops = p.total_flops;
+    s->hbm_bytes = p.total_bytes;
+    s->wire_bytes = p.total_wire_bytes;
+    std::vector<double> gf(p.num_lanes, 0);
+    for (const auto& in : p.instrs)
+      if (in.kind == InstrKind::gemm) gf[in.lane] += in.flops;
+    for (int l = 0; l < p.num_lanes; ++l) {
+      s->max_lane_gemm_flops = std::max(s->max_lane_gemm_flops, gf[l]);
+      s->max_lane_hbm_bytes = std::max(s->max_lane_hbm_bytes, p.lane_bytes[l]);
+      s->max_lane_wire_bytes = std::max(s->max_lane_wire_bytes, p.lane_wire_bytes[l]);
+      s->device_bytes += p.lane_arena_bytes[l];
+    }
+  });
+}
+
+int planc_b200_profile(planc_b200_exec* h, char** json_out) {
+  return guarded([&] {
+    if (!h || !json_out) throw UsageError("null argument");
+    auto st = h->ex->profile();
+    std::ostringstream os;
+    os.precision(17);
+    os << "[";
+    for (std::size_t i = 0; i < st.size(); ++i) {
+      os << (i ? "," : "") << "{\"kind\":\"" << st[i].kind << "\",\"launches\":" << st[i].launches
+         << ",\"ms\":" << st[i].ms << ",\"flops\":" << st[i].flops << ",\"bytes\":" << st[i].bytes
+         << ",\"wire_bytes\":" << st[i].wire_bytes << "}";
+    }
+    os << "]";
+    *json_out = dup(os.str());
+  });
+}
+
+int planc_b200_describe(const char* plan_json, uint32_t flags, char** json_out) {
+  return guarded([&] {
+    if (!plan_json || !json_out) throw UsageError("null argument");
+    ProgramOptions po;
+    po.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
+    ExecutionPlan plan = load_plan(plan_json);
+    Program p = build_program(plan, po);
+    *json_out = dup(p.describe_json());
+  });
+}
+
+}  // extern "C"

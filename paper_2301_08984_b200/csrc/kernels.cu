@@ -1,0 +1,482 @@
+// Memory-bound sub-operator kernels, the fused adapter (box) kernel and the
+// SIMT GEMM used for shapes the tcgen05 path does not take. sm_100a only.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace planc_b200 {
+
+namespace {
+
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+inline int grid_for(std::int64_t work, int per_block, int cap = 148 * 32) {
+  std::int64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<int>(g);
+}
+
+// ---- element access --------------------------------------------------------
+
+template <typename T>
+struct Acc {
+  using type = float;
+};
+template <>
+struct Acc<int> {
+  using type = int;
+};
+
+template <typename T>
+__device__ __forceinline__ typename Acc<T>::type to_acc(T v) {
+  return static_cast<typename Acc<T>::type>(v);
+}
+template <>
+__device__ __forceinline__ float to_acc<__nv_bfloat16>(__nv_bfloat16 v) {
+  return __bfloat162float(v);
+}
+template <typename T>
+__device__ __forceinline__ T from_acc(typename Acc<T>::type v) {
+  return static_cast<T>(v);
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+// V consecutive elements (V*sizeof(T) = 16 bytes when V > 1).
+template <typename T, int V>
+__device__ __forceinline__ void load_vec(const T* p, typename Acc<T>::type (&o)[V]) {
+  if constexpr (V == 1) {
+    o[0] = to_acc<T>(*p);
+  } else {
+    uint4 raw = __ldg(reinterpret_cast<const uint4*>(p));
+    const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int i = 0; i < V; ++i) o[i] = to_acc<T>(e[i]);
+  }
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void store_vec(T* p, const typename Acc<T>::type (&v)[V]) {
+  if constexpr (V == 1) {
+    *p = from_acc<T>(v[0]);
+  } else {
+    uint4 raw;
+    T* e = reinterpret_cast<T*>(&raw);
+#pragma unroll
+    for (int i = 0; i < V; ++i) e[i] = from_acc<T>(v[i]);
+    *reinterpret_cast<uint4*>(p) = raw;
+  }
+}
+
+__device__ __forceinline__ float load_any(const void* p, int dt, std::int64_t i) {
+  if (dt == DT_BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+  if (dt == DT_I32) return static_cast<float>(reinterpret_cast<const int*>(p)[i]);
+  return reinterpret_cast<const float*>(p)[i];
+}
+
+__device__ __forceinline__ void store_any(void* p, int dt, std::int64_t i, float v) {
+  if (dt == DT_BF16) reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
+  else if (dt == DT_I32) reinterpret_cast<int*>(p)[i] = static_cast<int>(v);
+  else reinterpret_cast<float*>(p)[i] = v;
+}
+
+// ---- box: fused reconstruct -------------------------------------------------
+
+constexpr int kBoxThreads = 256;
+constexpr int kSmemTerms = 32;
+
+template <typename T, int V>
+__global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, const DevCell* __restrict__ cells,
+                                                           const DevTerm* __restrict__ terms,
+                                                           const DevChunk* __restrict__ chunks) {
+  using A = typename Acc<T>::type;
+  __shared__ DevCell sc;
+  __shared__ DevTerm st[kSmemTerms];
+  const DevChunk ch = chunks[blockIdx.x];
+  if (threadIdx.x == 0) sc = cells[ch.cell];
+  __syncthreads();
+  const int nt = sc.nterms;
+  for (int i = threadIdx.x; i < nt && i < kSmemTerms; i += blockDim.x) st[i] = terms[sc.term0 + i];
+  __syncthreads();
+  const int rank = sc.rank;
+  const std::int64_t inner_vecs = sc.ext[rank - 1] / V;
+  for (std::int64_t u = threadIdx.x; u < ch.count; u += blockDim.x) {
+    std::int64_t lin = ch.begin + u;
+    std::int64_t coord[kBoxRank];
+    coord[rank - 1] = (lin % inner_vecs) * V;
+    lin /= inner_vecs;
+#pragma unroll
+    for (int d = kBoxRank - 2; d >= 0; --d) {
+      if (d < rank - 1) {
+        coord[d] = lin % sc.ext[d];
+        lin /= sc.ext[d];
+      }
+    }
+    std::int64_t doff = sc.dst_off;
+#pragma unroll
+    for (int d = 0; d < kBoxRank; ++d)
+      if (d < rank) doff += coord[d] * sc.dst_str[d];
+    A acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = A(0);
+    for (int t = 0; t < nt; ++t) {
+      const DevTerm& tm = t < kSmemTerms ? st[t] : terms[sc.term0 + t];
+      std::int64_t soff = tm.offset;
+#pragma unroll
+      for (int d = 0; d < kBoxRank; ++d)
+        if (d < rank) soff += coord[d] * tm.str[d];
+      A v[V];
+      load_vec<T, V>(reinterpret_cast<const T*>(tm.src) + soff, v);
+      if (tm.add) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] += v[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = v[i];
+      }
+    }
+    store_vec<T, V>(dst + doff, acc);
+  }
+}
+
+template <typename T>
+void box_dispatch(void* dst, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks, int vec,
+                  cudaStream_t s) {
+  constexpr int VV = 16 / sizeof(T);
+  if (vec > 1) {
+    box_kernel<T, VV><<<nchunks, kBoxThreads, 0, s>>>(static_cast<T*>(dst), cells, terms, chunks);
+  } else {
+    box_kernel<T, 1><<<nchunks, kBoxThreads, 0, s>>>(static_cast<T*>(dst), cells, terms, chunks);
+  }
+}
+
+// ---- elementwise -----------------------------------------------------------
+
+constexpr int kMaxEwIn = 8;
+struct EwPtrs {
+  const void* p[kMaxEwIn];
+};
+
+template <int OP>
+__device__ __forceinline__ float ew_apply(float a, float b) {
+  if constexpr (OP == 0) return a + b;
+  if constexpr (OP == 1) return a * b;
+  return fmaxf(a, b);
+}
+
+template <typename T, int OP>
+__global__ void __launch_bounds__(256) ew_kernel(EwPtrs in, int nin, T* __restrict__ out, std::int64_t nvec) {
+  constexpr int V = 16 / sizeof(T);
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < nvec;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    float acc[V], v[V];
+    load_vec<T, V>(static_cast<const T*>(in.p[0]) + i * V, acc);
+    for (int k = 1; k < nin; ++k) {
+      load_vec<T, V>(static_cast<const T*>(in.p[k]) + i * V, v);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] = ew_apply<OP>(acc[j], v[j]);
+    }
+    store_vec<T, V>(out + i * V, acc);
+  }
+}
+
+template <typename T, int OP>
+__global__ void ew_tail_kernel(EwPtrs in, int nin, T* __restrict__ out, std::int64_t begin, std::int64_t count) {
+  std::int64_t i = begin + blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= begin + count) return;
+  float acc = to_acc<T>(static_cast<const T*>(in.p[0])[i]);
+  for (int k = 1; k < nin; ++k) acc = ew_apply<OP>(acc, to_acc<T>(static_cast<const T*>(in.p[k])[i]));
+  out[i] = from_acc<T>(acc);
+}
+
+template <typename T, int OP>
+void ew_typed(const void* const* ins, int nin, void* out, std::int64_t count, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  EwPtrs p{};
+  bool aligned = (reinterpret_cast<std::uintptr_t>(out) % 16) == 0;
+  for (int i = 0; i < nin; ++i) {
+    p.p[i] = ins[i];
+    aligned = aligned && (reinterpret_cast<std::uintptr_t>(ins[i]) % 16) == 0;
+  }
+  std::int64_t nvec = aligned ? count / V : 0;
+  if (nvec > 0) {
+    ew_kernel<T, OP><<<grid_for(nvec, 256), 256, 0, s>>>(p, nin, static_cast<T*>(out), nvec);
+  }
+  std::int64_t rest = count - nvec * V;
+  if (rest > 0) {
+    ew_tail_kernel<T, OP><<<static_cast<int>((rest + 255) / 256), 256, 0, s>>>(p, nin, static_cast<T*>(out),
+                                                                               nvec * V, rest);
+  }
+}
+
+// ---- reduce-sum --------------------------------------------------------------
+
+// inner == 1: one warp per output row, lanes stride the reduced axis.
+template <typename T>
+__global__ void reduce_rows_kernel(const T* __restrict__ in, T* __restrict__ out, std::int64_t outer,
+                                   std::int64_t axis_len) {
+  std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / 32;
+  int lane = threadIdx.x & 31;
+  std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * blockDim.x / 32;
+  for (std::int64_t r = warp; r < outer; r += nwarps) {
+    float acc = 0.f;
+    for (std::int64_t a = lane; a < axis_len; a += 32) acc += to_acc<T>(in[r * axis_len + a]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[r] = from_acc<T>(acc);
+  }
+}
+
+// inner > 1: one thread per (outer, inner) column, coalesced along inner.
+template <typename T>
+__global__ void reduce_cols_kernel(const T* __restrict__ in, T* __restrict__ out, std::int64_t outer,
+                                   std::int64_t axis_len, std::int64_t inner) {
+  std::int64_t total = outer * inner;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    std::int64_t o = i / inner, c = i % inner;
+    const T* p = in + o * axis_len * inner + c;
+    float acc = 0.f;
+    for (std::int64_t a = 0; a < axis_len; ++a) acc += to_acc<T>(p[a * inner]);
+    out[i] = from_acc<T>(acc);
+  }
+}
+
+// ---- embedding ---------------------------------------------------------------
+
+template <typename T>
+__global__ void emb_lookup_kernel(const int* __restrict__ idx, const T* __restrict__ table, T* __restrict__ out,
+                                  std::int64_t n, std::int64_t rows, std::int64_t h, std::int64_t lo) {
+  std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / 32;
+  int lane = threadIdx.x & 31;
+  std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * blockDim.x / 32;
+  for (std::int64_t j = warp; j < n; j += nwarps) {
+    std::int64_t id = idx[j];
+    bool in_shard = id >= lo && id < lo + rows;
+    for (std::int64_t c = lane; c < h; c += 32) {
+      out[j * h + c] = in_shard ? table[(id - lo) * h + c] : from_acc<T>(0.f);
+    }
+  }
+}
+
+template <typename T>
+__global__ void emb_grad_kernel(const int* __restrict__ idx, const T* __restrict__ gout, float* __restrict__ acc,
+                                std::int64_t n, std::int64_t rows, std::int64_t h, std::int64_t lo) {
+  std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / 32;
+  int lane = threadIdx.x & 31;
+  std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * blockDim.x / 32;
+  for (std::int64_t j = warp; j < n; j += nwarps) {
+    std::int64_t id = idx[j];
+    if (id < lo || id >= lo + rows) continue;
+    for (std::int64_t c = lane; c < h; c += 32) atomicAdd(acc + (id - lo) * h + c, to_acc<T>(gout[j * h + c]));
+  }
+}
+
+__global__ void convert_kernel(int dt, void* out, const float* __restrict__ in, std::int64_t count) {
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    store_any(out, dt, i, in[i]);
+}
+
+__global__ void zero_kernel(float* p, std::int64_t count) {
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    p[i] = 0.f;
+}
+
+// ---- SIMT GEMM (small / unaligned shapes, fp32 plans) ------------------------
+// C[m,n] = op(A)[m,k] · op(B)[k,n], fp32 FFMA accumulation in k order.
+
+constexpr int kTM = 64, kTN = 64, kTK = 16;
+
+__global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs a) {
+  __shared__ float As[kTK][kTM + 4];
+  __shared__ float Bs[kTK][kTN + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const std::int64_t m0 = static_cast<std::int64_t>(blockIdx.y) * kTM;
+  const std::int64_t n0 = static_cast<std::int64_t>(blockIdx.x) * kTN;
+  float acc[4][4] = {};
+  // A element (i, kk): ta ? A[kk, i] (A stored [k, m]) : A[i, kk] (stored [m, k])
+  for (std::int64_t k0 = 0; k0 < a.k; k0 += kTK) {
+    for (int e = threadIdx.x; e < kTK * kTM; e += 256) {
+      int kk, ii;
+      if (a.ta) {
+        ii = e % kTM;
+        kk = e / kTM;
+      } else {
+        kk = e % kTK;
+        ii = e / kTK;
+      }
+      std::int64_t gi = m0 + ii, gk = k0 + kk;
+      float v = 0.f;
+      if (gi < a.m && gk < a.k) v = load_any(a.A, a.da, a.ta ? gk * a.m + gi : gi * a.k + gk);
+      As[kk][ii] = v;
+    }
+    // B element (kk, j): tb ? B[j, kk] (stored [n, k]) : B[kk, j] (stored [k, n])
+    for (int e = threadIdx.x; e < kTK * kTN; e += 256) {
+      int kk, jj;
+      if (a.tb) {
+        kk = e % kTK;
+        jj = e / kTK;
+      } else {
+        jj = e % kTN;
+        kk = e / kTN;
+      }
+      std::int64_t gj = n0 + jj, gk = k0 + kk;
+      float v = 0.f;
+      if (gj < a.n && gk < a.k) v = load_any(a.B, a.db, a.tb ? gj * a.k + gk : gk * a.n + gj);
+      Bs[kk][jj] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kTK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    std::int64_t gi = m0 + ty * 4 + i;
+    if (gi >= a.m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      std::int64_t gj = n0 + tx * 4 + j;
+      if (gj < a.n) store_any(a.C, a.dc, gi * a.n + gj, acc[i][j]);
+    }
+  }
+}
+
+}  // namespace
+
+void launch_box(void* dst, int dtype, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks,
+                int vec, cudaStream_t s) {
+  if (nchunks == 0) return;
+  switch (dtype) {
+    case DT_F32: box_dispatch<float>(dst, cells, terms, chunks, nchunks, vec, s); break;
+    case DT_BF16: box_dispatch<__nv_bfloat16>(dst, cells, terms, chunks, nchunks, vec, s); break;
+    case DT_I32: box_dispatch<int>(dst, cells, terms, chunks, nchunks, vec, s); break;
+    default: throw std::runtime_error("box: bad dtype");
+  }
+  check_launch("box_kernel");
+}
+
+void launch_ew(int op, int dtype, const void* const* ins, int nin, void* out, std::int64_t count, cudaStream_t s) {
+  if (nin > kMaxEwIn) throw std::runtime_error("ew: too many inputs per launch");
+  if (count == 0) return;
+#define PLANC_EW(T)                                                       \
+  switch (op) {                                                           \
+    case 0: ew_typed<T, 0>(ins, nin, out, count, s); break;               \
+    case 1: ew_typed<T, 1>(ins, nin, out, count, s); break;               \
+    default: ew_typed<T, 2>(ins, nin, out, count, s); break;              \
+  }
+  if (dtype == DT_F32) {
+    PLANC_EW(float)
+  } else if (dtype == DT_BF16) {
+    PLANC_EW(__nv_bfloat16)
+  } else {
+    throw std::runtime_error("ew: unsupported dtype");
+  }
+#undef PLANC_EW
+  check_launch("ew_kernel");
+}
+
+void launch_reduce(int dtype, const void* in, void* out, std::int64_t outer, std::int64_t axis_len,
+                   std::int64_t inner, cudaStream_t s) {
+  if (dtype == DT_F32) {
+    if (inner == 1)
+      reduce_rows_kernel<float><<<grid_for(outer * 32, 256), 256, 0, s>>>(static_cast<const float*>(in),
+                                                                           static_cast<float*>(out), outer, axis_len);
+    else
+      reduce_cols_kernel<float><<<grid_for(outer * inner, 256), 256, 0, s>>>(
+          static_cast<const float*>(in), static_cast<float*>(out), outer, axis_len, inner);
+  } else if (dtype == DT_BF16) {
+    using B = __nv_bfloat16;
+    if (inner == 1)
+      reduce_rows_kernel<B><<<grid_for(outer * 32, 256), 256, 0, s>>>(static_cast<const B*>(in),
+                                                                       static_cast<B*>(out), outer, axis_len);
+    else
+      reduce_cols_kernel<B><<<grid_for(outer * inner, 256), 256, 0, s>>>(static_cast<const B*>(in),
+                                                                         static_cast<B*>(out), outer, axis_len, inner);
+  } else {
+    throw std::runtime_error("reduce: unsupported dtype");
+  }
+  check_launch("reduce_kernel");
+}
+
+void launch_emb_lookup(int dtype, const int* idx, const void* table, void* out, std::int64_t n, std::int64_t rows,
+                       std::int64_t h, std::int64_t lo, cudaStream_t s) {
+  int g = grid_for(n * 32, 256);
+  if (dtype == DT_F32)
+    emb_lookup_kernel<float><<<g, 256, 0, s>>>(idx, static_cast<const float*>(table), static_cast<float*>(out), n,
+                                                rows, h, lo);
+  else if (dtype == DT_BF16)
+    emb_lookup_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(idx, static_cast<const __nv_bfloat16*>(table),
+                                                        static_cast<__nv_bfloat16*>(out), n, rows, h, lo);
+  else
+    throw std::runtime_error("embedding: unsupported dtype");
+  check_launch("emb_lookup_kernel");
+}
+
+void launch_emb_grad(int dtype, const int* idx, const void* gout, void* out, float* scratch, std::int64_t n,
+                     std::int64_t rows, std::int64_t h, std::int64_t lo, cudaStream_t s) {
+  float* acc = dtype == DT_F32 ? static_cast<float*>(out) : scratch;
+  zero_kernel<<<grid_for(rows * h, 256), 256, 0, s>>>(acc, rows * h);
+  int g = grid_for(n * 32, 256);
+  if (dtype == DT_F32)
+    emb_grad_kernel<float><<<g, 256, 0, s>>>(idx, static_cast<const float*>(gout), acc, n, rows, h, lo);
+  else if (dtype == DT_BF16)
+    emb_grad_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(idx, static_cast<const __nv_bfloat16*>(gout), acc, n, rows,
+                                                      h, lo);
+  else
+    throw std::runtime_error("embedding-grad: unsupported dtype");
+  if (dtype != DT_F32) convert_kernel<<<grid_for(rows * h, 256), 256, 0, s>>>(dtype, out, acc, rows * h);
+  check_launch("emb_grad_kernel");
+}
+
+void launch_gemm_simt(const GemmArgs& a, cudaStream_t s) {
+  if (a.m == 0 || a.n == 0) return;
+  if (a.k == 0) {
+    // Empty contraction: C = 0.
+    std::int64_t cnt = a.m * a.n;
+    if (a.dc == DT_F32) {
+      zero_kernel<<<grid_for(cnt, 256), 256, 0, s>>>(static_cast<float*>(a.C), cnt);
+    } else {
+      cudaMemsetAsync(a.C, 0, cnt * 2, s);
+    }
+    check_launch("gemm_zero");
+    return;
+  }
+  dim3 grid(static_cast<unsigned>((a.n + kTN - 1) / kTN), static_cast<unsigned>((a.m + kTM - 1) / kTM));
+  gemm_simt_kernel<<<grid, 256, 0, s>>>(a);
+  check_launch("gemm_simt_kernel");
+}
+
+void launch_convert(int dtype_out, void* out, const float* in, std::int64_t count, cudaStream_t s) {
+  convert_kernel<<<grid_for(count, 256), 256, 0, s>>>(dtype_out, out, in, count);
+  check_launch("convert_kernel");
+}
+
+void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s) {
+  zero_kernel<<<grid_for(count, 256), 256, 0, s>>>(p, count);
+  check_launch("zero_kernel");
+}
+
+}  // namespace planc_b200

@@ -1,0 +1,90 @@
+// Device kernels of the B200 plan executor (sm_100a).
+//
+// Sub-operators (reference eval_compute, proj/src/refexec.cpp:142-257):
+//   gemm   matmul with transpose_a / transpose_b       (refexec.cpp:142-168)
+//   ew     N-ary add / mul / max, same shape           (refexec.cpp:178-193)
+//   reduce reduce-sum over one axis                    (refexec.cpp:194-215)
+//   emb    embedding lookup / grad with vocab offset   (refexec.cpp:216-250)
+// Adapters (reference reconstruct, refexec.cpp:102-140): one "box" kernel
+// executes a static cell program — every destination cell is written once as
+// 0 ∘ term_0 ∘ term_1 … (∘ = copy | add, in piece order). Sources may be
+// local buffers, other lanes' buffers on the same GPU, or NVLink peer
+// pointers, so split / concat / reduce-assemble / recv / every collective
+// member output is one fused gather(-reduce) launch with no pack/unpack pass.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace planc_b200 {
+
+enum DT : int { DT_F32 = 0, DT_BF16 = 1, DT_I32 = 2 };
+
+constexpr int kBoxRank = 6;
+
+struct DevTerm {
+  const void* src;
+  std::int64_t offset;
+  std::int64_t str[kBoxRank];
+  int add;
+  int pad;
+};
+
+struct DevCell {
+  std::int64_t ext[kBoxRank];
+  std::int64_t dst_str[kBoxRank];
+  std::int64_t dst_off;
+  std::int64_t elems;
+  int rank;
+  int nterms;
+  int term0;
+  int vec;  // elements per vector access (1, 4 or 8), innermost contiguous
+};
+
+struct DevChunk {
+  int cell;
+  int pad;
+  std::int64_t begin;  // in vector units
+  std::int64_t count;  // in vector units
+};
+
+struct GemmArgs {
+  const void* A;
+  const void* B;
+  void* C;
+  std::int64_t m, n, k;
+  bool ta, tb;
+  int da, db, dc;
+};
+
+// Launchers (all asynchronous on `s`).
+// `vec` != 0: every chunk's cell is innermost-contiguous with 16-byte
+// aligned offsets (the executor splits a box program into vector / scalar
+// launches).
+void launch_box(void* dst, int dtype, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks,
+                int nchunks, int vec, cudaStream_t s);
+void launch_ew(int op, int dtype, const void* const* ins, int nin, void* out, std::int64_t count, cudaStream_t s);
+void launch_reduce(int dtype, const void* in, void* out, std::int64_t outer, std::int64_t axis_len,
+                   std::int64_t inner, cudaStream_t s);
+void launch_emb_lookup(int dtype, const int* idx, const void* table, void* out, std::int64_t n, std::int64_t rows,
+                       std::int64_t h, std::int64_t lo, cudaStream_t s);
+void launch_emb_grad(int dtype, const int* idx, const void* gout, void* out, float* scratch, std::int64_t n,
+                     std::int64_t rows, std::int64_t h, std::int64_t lo, cudaStream_t s);
+void launch_gemm_simt(const GemmArgs& a, cudaStream_t s);
+void launch_convert(int dtype_out, void* out, const float* in, std::int64_t count, cudaStream_t s);
+void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s);
+
+// tcgen05 / TMEM / TMA GEMM (gemm_sm100.cu).
+bool gemm_sm100_eligible(const GemmArgs& a);
+void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s);
+
+// Dispatch: tcgen05 path when eligible, SIMT tile kernel otherwise.
+inline void launch_gemm(const GemmArgs& a, cudaStream_t s, bool allow_tc, bool* used_tc) {
+  bool tc = allow_tc && gemm_sm100_eligible(a);
+  if (used_tc) *used_tc = tc;
+  if (tc) launch_gemm_sm100(a, s);
+  else launch_gemm_simt(a, s);
+}
+
+}  // namespace planc_b200

@@ -1,0 +1,786 @@
+#include "program.hpp"
+
+#include <algorithm>
+#include <map>
+#include <set>
+#include <sstream>
+#include <tuple>
+#include <unordered_map>
+#include <unordered_set>
+
+namespace planc_b200 {
+
+const char* dtype_name(DType d) {
+  switch (d) {
+    case DType::f32: return "f32";
+    case DType::bf16: return "bf16";
+    case DType::i32: return "i32";
+  }
+  return "?";
+}
+
+const char* instr_kind_name(InstrKind k) {
+  switch (k) {
+    case InstrKind::gemm: return "gemm";
+    case InstrKind::ew: return "ew";
+    case InstrKind::reduce: return "reduce";
+    case InstrKind::emb_lookup: return "emb_lookup";
+    case InstrKind::emb_grad: return "emb_grad";
+    case InstrKind::box: return "box";
+    case InstrKind::nop: return "nop";
+  }
+  return "?";
+}
+
+namespace {
+
+std::vector<std::int64_t> row_major_strides(const std::vector<std::int64_t>& shape) {
+  std::vector<std::int64_t> s(shape.size(), 1);
+  for (int i = static_cast<int>(shape.size()) - 2; i >= 0; --i) s[i] = s[i + 1] * shape[i + 1];
+  return s;
+}
+
+std::vector<std::int64_t> region_shape(const Region& r) {
+  std::vector<std::int64_t> s;
+  for (const auto& iv : r) s.push_back(iv.length());
+  return s;
+}
+
+// Drops unit dims and merges dims that are contiguous in the destination and
+// in every source term, so most cells become 1-D or 2-D strided copies.
+void collapse(Cell& c) {
+  int w = 0;
+  for (int d = 0; d < c.rank; ++d) {
+    if (c.extents[d] == 1) continue;
+    c.extents[w] = c.extents[d];
+    c.dst_strides[w] = c.dst_strides[d];
+    for (auto& t : c.terms) t.strides[w] = t.strides[d];
+    ++w;
+  }
+  c.rank = w;
+  if (c.rank == 0) {
+    c.rank = 1;
+    c.extents[0] = 1;
+    c.dst_strides[0] = 1;
+    for (auto& t : c.terms) t.strides[0] = 1;
+    return;
+  }
+  w = 0;
+  for (int d = 1; d < c.rank; ++d) {
+    bool ok = c.dst_strides[w] == c.dst_strides[d] * c.extents[d];
+    for (const auto& t : c.terms) ok = ok && t.strides[w] == t.strides[d] * c.extents[d];
+    if (ok) {
+      c.extents[w] *= c.extents[d];
+      c.dst_strides[w] = c.dst_strides[d];
+      for (auto& t : c.terms) t.strides[w] = t.strides[d];
+    } else {
+      ++w;
+      c.extents[w] = c.extents[d];
+      c.dst_strides[w] = c.dst_strides[d];
+      for (auto& t : c.terms) t.strides[w] = t.strides[d];
+    }
+  }
+  c.rank = w + 1;
+}
+
+}  // namespace
+
+std::vector<Cell> reconstruct_cells(const Mask& target, const std::vector<std::int64_t>& target_shape,
+                                    const std::vector<std::pair<const Mask*, int>>& pieces,
+                                    const std::vector<BufferDesc>& buffers, bool vv_extension,
+                                    const std::string& ctx) {
+  const Region& treg = target.region;
+  const int rank = static_cast<int>(treg.size());
+  if (rank > kMaxCellRank) throw UsageError("tensor rank above " + std::to_string(kMaxCellRank));
+  struct Used {
+    const Mask* mask;
+    int buffer;
+    bool add;
+    Region ov;
+  };
+  std::vector<Used> used;
+  std::int64_t touched = 0;
+  for (const auto& [m, buf] : pieces) {
+    bool add;
+    if (m->value_count == target.value_count && m->value_index == target.value_index) {
+      add = false;  // refexec.cpp:110-112 copy
+    } else if (target.value_count == 1 && m->value_count > 1) {
+      add = true;  // refexec.cpp:113-114 summand
+    } else if (vv_extension && m->value_count > target.value_count &&
+               m->value_count % target.value_count == 0 &&
+               m->value_index / (m->value_count / target.value_count) == target.value_index) {
+      add = true;  // V(m*v) -> V(v): sub-parts of the target's value part
+    } else {
+      continue;  // refexec.cpp:115-117
+    }
+    Region ov;
+    if (!region_intersect(m->region, treg, &ov)) continue;
+    touched += region_volume(ov);
+    used.push_back({m, buf, add, ov});
+  }
+  if (touched < region_volume(treg)) {
+    throw InternalError("reconstruct: region " + region_to_string(treg) + " not fully covered (" + ctx + ")");
+  }
+  // Grid of all overlap boundaries: inside each grid cell the ordered set of
+  // contributing pieces is constant.
+  std::vector<std::vector<std::int64_t>> bounds(rank);
+  for (int d = 0; d < rank; ++d) {
+    std::set<std::int64_t> b = {treg[d].lo, treg[d].hi};
+    for (const auto& u : used) {
+      b.insert(u.ov[d].lo);
+      b.insert(u.ov[d].hi);
+    }
+    bounds[d].assign(b.begin(), b.end());
+  }
+  auto tstr = row_major_strides(target_shape);
+  std::vector<Cell> cells;
+  std::vector<std::size_t> idx(rank, 0);
+  if (rank == 0) return cells;
+  while (true) {
+    Region box(rank);
+    for (int d = 0; d < rank; ++d) box[d] = {bounds[d][idx[d]], bounds[d][idx[d] + 1]};
+    Cell c;
+    c.rank = rank;
+    for (int d = 0; d < rank; ++d) {
+      c.extents[d] = box[d].length();
+      c.dst_strides[d] = tstr[d];
+      c.dst_offset += (box[d].lo - treg[d].lo) * tstr[d];
+    }
+    for (const auto& u : used) {
+      bool inside = true;
+      for (int d = 0; d < rank; ++d) inside = inside && u.ov[d].lo <= box[d].lo && box[d].hi <= u.ov[d].hi;
+      if (!inside) continue;
+      const BufferDesc& src = buffers[u.buffer];
+      auto sstr = row_major_strides(src.shape);
+      Term t;
+      t.buffer = u.buffer;
+      t.add = u.add;
+      for (int d = 0; d < rank; ++d) {
+        t.strides[d] = sstr[d];
+        t.offset += (box[d].lo - u.mask->region[d].lo) * sstr[d];
+      }
+      // A copy overwrites everything accumulated so far (refexec.cpp:126-130).
+      if (!t.add) c.terms.clear();
+      c.terms.push_back(t);
+    }
+    collapse(c);
+    cells.push_back(std::move(c));
+    int d = rank - 1;
+    while (d >= 0) {
+      if (++idx[d] + 1 < bounds[d].size()) break;
+      idx[d] = 0;
+      --d;
+    }
+    if (d < 0) break;
+  }
+  return cells;
+}
+
+namespace {
+
+struct Builder {
+  const ExecutionPlan& plan;
+  const ProgramOptions& opt;
+  Program P;
+  std::map<int, int> lane_of_device;
+  std::map<int, DType> pt_dtype;
+  std::unordered_map<int, int> vt_buf;          // vt -> buffer
+  std::map<std::tuple<int, int, std::vector<std::int64_t>>, int> placement;  // (lane, pt, region) -> buf
+  std::unordered_set<int> issued_vts;
+  std::unordered_map<int, int> channel_src;      // channel -> send input vt
+  std::vector<int> op_last_instr;                // op idx -> last instruction (-1)
+  std::vector<int> op_first_instr;
+  std::unordered_map<int, std::vector<int>> sync_before;  // after op -> before ops
+  std::vector<bool> op_issued;
+
+  Builder(const ExecutionPlan& p, const ProgramOptions& o) : plan(p), opt(o) {}
+
+  int lane_of_op(const OpNode& op) {
+    auto it = plan.assignment.find(op.id);
+    if (it == plan.assignment.end()) throw InternalError("op " + op.id + " has no device assignment");
+    auto l = lane_of_device.find(it->second);
+    if (l == lane_of_device.end()) {
+      throw InternalError("op " + op.id + " assigned to device " + std::to_string(it->second) + " without a lane");
+    }
+    return l->second;
+  }
+
+  int new_buffer(int lane, int pt, const Mask& mask, int vt) {
+    BufferDesc b;
+    b.id = static_cast<int>(P.buffers.size());
+    b.lane = lane;
+    b.ptensor = pt;
+    b.mask = mask;
+    b.dtype = pt_dtype.at(pt);
+    b.shape = region_shape(mask.region);
+    b.elems = region_volume(mask.region);
+    b.bytes = b.elems * dtype_size(b.dtype);
+    b.vt = vt;
+    std::int64_t& arena = P.lane_arena_bytes[lane];
+    b.offset = arena;
+    arena += (b.bytes + 255) / 256 * 256;
+    P.buffers.push_back(b);
+    return b.id;
+  }
+
+  int out_buffer(int vt_id, int lane) {
+    const VTensor& v = plan.vt(vt_id);
+    int b = new_buffer(lane, v.ptensor, v.mask, vt_id);
+    vt_buf[vt_id] = b;
+    if (static_cast<int>(P.vt_buffer.size()) <= vt_id) P.vt_buffer.resize(vt_id + 1, -1);
+    P.vt_buffer[vt_id] = b;
+    return b;
+  }
+
+  // refexec.cpp:378-394 (feed_ready / feed_value) + 366-376 (input_value)
+  bool feed_ready(int cvt) {
+    const VTensor& v = plan.vt(cvt);
+    if (plan.is_graph_input(v.ptensor)) return true;
+    auto f = plan.feeds.find(cvt);
+    if (f == plan.feeds.end()) {
+      throw InternalError("run_plan: consumer view " + std::to_string(cvt) + " of op " + v.owner_op +
+                          " has no feed");
+    }
+    return issued_vts.count(f->second) > 0;
+  }
+
+  int input_buffer(int cvt, int lane) {
+    auto f = plan.feeds.find(cvt);
+    const VTensor& v = plan.vt(cvt);
+    if (f != plan.feeds.end()) {
+      int b = vt_buf.at(f->second);
+      const BufferDesc& bd = P.buffers[b];
+      if (!(bd.mask.region == v.mask.region)) {
+        throw InternalError("feed of view " + std::to_string(cvt) + " covers " + region_to_string(bd.mask.region) +
+                            ", consumer wants " + region_to_string(v.mask.region));
+      }
+      if (bd.lane != lane) {
+        throw InternalError("feed of view " + std::to_string(cvt) + " crosses lanes without an adapter");
+      }
+      return b;
+    }
+    if (v.mask.value_count != 1) throw UsageError("run_plan: graph input consumed as partial value");
+    std::vector<std::int64_t> key;
+    for (const auto& iv : v.mask.region) {
+      key.push_back(iv.lo);
+      key.push_back(iv.hi);
+    }
+    auto k = std::make_tuple(lane, v.ptensor, key);
+    auto it = placement.find(k);
+    if (it != placement.end()) return it->second;
+    Mask m;
+    m.region = v.mask.region;
+    int b = new_buffer(lane, v.ptensor, m, cvt);
+    P.buffers[b].graph_input = true;
+    TensorKind kind = plan.pt(v.ptensor).kind;
+    P.buffers[b].weight = kind == TensorKind::weight || kind == TensorKind::optimizer_state;
+    placement[k] = b;
+    return b;
+  }
+
+  Instr& emit(InstrKind kind, int lane, int stream, int op_idx, const std::string& label) {
+    Instr in;
+    in.id = static_cast<int>(P.instrs.size());
+    in.kind = kind;
+    in.lane = lane;
+    in.stream = stream;
+    in.op = op_idx;
+    in.label = label;
+    P.instrs.push_back(std::move(in));
+    P.issue_order.push_back(P.instrs.back().id);
+    if (op_idx >= 0) {
+      if (op_first_instr[op_idx] < 0) op_first_instr[op_idx] = P.instrs.back().id;
+      op_last_instr[op_idx] = P.instrs.back().id;
+    }
+    return P.instrs.back();
+  }
+
+  void finish_deps(Instr& in) {
+    std::set<int> d;
+    for (int b : in.in_bufs) {
+      if (P.buffers[b].producer >= 0) d.insert(P.buffers[b].producer);
+    }
+    for (const auto& c : in.cells) {
+      for (const auto& t : c.terms) {
+        if (P.buffers[t.buffer].producer >= 0) d.insert(P.buffers[t.buffer].producer);
+      }
+    }
+    in.deps.assign(d.begin(), d.end());
+    for (int b : in.out_bufs) P.buffers[b].producer = in.id;
+  }
+
+  double box_bytes(const Instr& in) {
+    double by = 0;
+    std::int64_t es = dtype_size(P.buffers[in.out_bufs[0]].dtype);
+    for (const auto& c : in.cells) by += static_cast<double>(c.elems()) * es * (1 + c.terms.size());
+    return by;
+  }
+
+  void emit_box(int op_idx, const OpNode& op, int lane, int stream, int out_vt,
+                const std::vector<std::pair<const Mask*, int>>& pieces, const std::string& ctx) {
+    int ob = out_buffer(out_vt, lane);
+    const VTensor& ov = plan.vt(out_vt);
+    Instr& in = emit(InstrKind::box, lane, stream, op_idx, op.id);
+    in.out_bufs = {ob};
+    in.cells = reconstruct_cells(ov.mask, P.buffers[ob].shape, pieces, P.buffers, opt.value_split_extension, ctx);
+    std::set<int> ins;
+    for (const auto& c : in.cells)
+      for (const auto& t : c.terms) ins.insert(t.buffer);
+    in.in_bufs.assign(ins.begin(), ins.end());
+    in.bytes = box_bytes(in);
+    finish_deps(in);
+  }
+
+  void exec_compute(int op_idx) {
+    const OpNode& op = plan.ops[op_idx];
+    int lane = lane_of_op(op);
+    std::vector<int> ib;
+    for (int v : op.inputs) ib.push_back(input_buffer(v, lane));
+    auto shape_of = [&](int b) { return P.buffers[b].shape; };
+    switch (op.kind) {
+      case OpKind::matmul: {
+        if (ib.size() != 2 || op.outputs.size() != 1) throw InternalError("matmul arity in " + op.id);
+        auto a = shape_of(ib[0]), bsh = shape_of(ib[1]);
+        if (a.size() != 2 || bsh.size() != 2) throw InternalError("matmul operands must be rank 2 in " + op.id);
+        std::int64_t m = op.transpose_a ? a[1] : a[0], k = op.transpose_a ? a[0] : a[1];
+        std::int64_t k2 = op.transpose_b ? bsh[1] : bsh[0], n = op.transpose_b ? bsh[0] : bsh[1];
+        if (k != k2) throw InternalError("matmul operand inner extents differ in " + op.id);  // refexec.cpp:154
+        int ob = out_buffer(op.outputs[0], lane);
+        auto c = shape_of(ob);
+        if (c.size() != 2 || c[0] != m || c[1] != n) throw InternalError("matmul output shape mismatch in " + op.id);
+        Instr& in = emit(InstrKind::gemm, lane, 0, op_idx, op.id);
+        in.in_bufs = ib;
+        in.out_bufs = {ob};
+        in.m = m;
+        in.n = n;
+        in.k = k;
+        in.ta = op.transpose_a;
+        in.tb = op.transpose_b;
+        in.flops = 2.0 * m * n * k;
+        in.bytes = static_cast<double>(P.buffers[ib[0]].bytes + P.buffers[ib[1]].bytes + P.buffers[ob].bytes);
+        finish_deps(in);
+        break;
+      }
+      case OpKind::ew_add:
+      case OpKind::ew_mul:
+      case OpKind::ew_max: {
+        if (ib.empty() || op.outputs.size() != 1) throw InternalError("elementwise arity in " + op.id);
+        for (std::size_t i = 1; i < ib.size(); ++i) {
+          if (shape_of(ib[i]) != shape_of(ib[0])) throw InternalError("elementwise shape mismatch in " + op.id);
+        }
+        int ob = out_buffer(op.outputs[0], lane);
+        if (P.buffers[ob].elems != P.buffers[ib[0]].elems) throw InternalError("elementwise output shape in " + op.id);
+        Instr& in = emit(InstrKind::ew, lane, 0, op_idx, op.id);
+        in.in_bufs = ib;
+        in.out_bufs = {ob};
+        in.ew = op.kind == OpKind::ew_add ? EwOp::add : op.kind == OpKind::ew_mul ? EwOp::mul : EwOp::max;
+        in.count = P.buffers[ob].elems;
+        in.flops = static_cast<double>(in.count) * (ib.size() - 1);
+        in.bytes = static_cast<double>(in.count) * dtype_size(P.buffers[ob].dtype) * (ib.size() + 1);
+        finish_deps(in);
+        break;
+      }
+      case OpKind::reduce_sum: {
+        if (ib.size() != 1 || op.outputs.size() != 1) throw InternalError("reduce arity in " + op.id);
+        auto s = shape_of(ib[0]);
+        int axis = op.axis < 0 ? 0 : op.axis;
+        if (axis >= static_cast<int>(s.size())) throw InternalError("reduce axis out of range in " + op.id);
+        int ob = out_buffer(op.outputs[0], lane);
+        Instr& in = emit(InstrKind::reduce, lane, 0, op_idx, op.id);
+        in.in_bufs = ib;
+        in.out_bufs = {ob};
+        in.outer = 1;
+        in.inner = 1;
+        for (int i = 0; i < axis; ++i) in.outer *= s[i];
+        in.axis_len = s[axis];
+        for (std::size_t i = axis + 1; i < s.size(); ++i) in.inner *= s[i];
+        if (P.buffers[ob].elems != in.outer * in.inner) throw InternalError("reduce output shape in " + op.id);
+        in.flops = static_cast<double>(P.buffers[ib[0]].elems);
+        in.bytes = static_cast<double>(P.buffers[ib[0]].bytes + P.buffers[ob].bytes);
+        finish_deps(in);
+        break;
+      }
+      case OpKind::embedding_lookup: {
+        if (ib.size() != 2 || op.outputs.size() != 1) throw InternalError("embedding arity in " + op.id);
+        auto idx = shape_of(ib[0]), table = shape_of(ib[1]);
+        if (idx.size() != 1 || table.size() != 2) throw InternalError("embedding operand ranks in " + op.id);
+        int ob = out_buffer(op.outputs[0], lane);
+        Instr& in = emit(InstrKind::emb_lookup, lane, 0, op_idx, op.id);
+        in.in_bufs = ib;
+        in.out_bufs = {ob};
+        in.n_idx = idx[0];
+        in.rows = table[0];
+        in.h = table[1];
+        in.lo = plan.vt(op.inputs[1]).mask.region[0].lo;  // refexec.cpp:219
+        if (P.buffers[ob].elems != in.n_idx * in.h) throw InternalError("embedding output shape in " + op.id);
+        std::int64_t es = dtype_size(P.buffers[ob].dtype);
+        in.bytes = static_cast<double>(in.n_idx * 4 + 2 * in.n_idx * in.h * es);
+        finish_deps(in);
+        break;
+      }
+      case OpKind::embedding_grad: {
+        if (ib.size() != 2 || op.outputs.size() != 1) throw InternalError("embedding-grad arity in " + op.id);
+        auto idx = shape_of(ib[0]), g = shape_of(ib[1]);
+        if (idx.size() != 1 || g.size() != 2) throw InternalError("embedding-grad operand ranks in " + op.id);
+        int ob = out_buffer(op.outputs[0], lane);
+        const Region& oreg = plan.vt(op.outputs[0]).mask.region;  // refexec.cpp:236-238
+        Instr& in = emit(InstrKind::emb_grad, lane, 0, op_idx, op.id);
+        in.in_bufs = ib;
+        in.out_bufs = {ob};
+        in.n_idx = idx[0];
+        in.h = g[1];
+        in.lo = oreg[0].lo;
+        in.rows = oreg[0].length();
+        if (P.buffers[ob].elems != in.rows * in.h) throw InternalError("embedding-grad output shape in " + op.id);
+        std::int64_t es = dtype_size(P.buffers[ob].dtype);
+        in.flops = static_cast<double>(in.n_idx * in.h);
+        in.bytes = static_cast<double>(in.n_idx * 4 + in.n_idx * in.h * es + in.rows * in.h * es);
+        finish_deps(in);
+        break;
+      }
+      case OpKind::identity: {
+        if (ib.size() != 1 || op.outputs.size() != 1) throw InternalError("identity arity in " + op.id);
+        std::vector<std::pair<const Mask*, int>> pieces;
+        Mask m = P.buffers[ib[0]].mask;
+        const VTensor& ov = plan.vt(op.outputs[0]);
+        // identity copies its operand whole (refexec.cpp:251): same extents,
+        // placed at the output view's coordinates.
+        if (region_shape(m.region) != region_shape(ov.mask.region)) {
+          throw InternalError("identity shape mismatch in " + op.id);
+        }
+        Mask src = ov.mask;
+        pieces.push_back({&src, ib[0]});
+        emit_box(op_idx, op, lane, 0, op.outputs[0], pieces, "op " + op.id);
+        P.instrs.back().label = op.id;
+        break;
+      }
+      default:
+        throw UsageError(std::string("refexec: unsupported op kind ") + op_kind_name(op.kind) + " (" + op.id + ")");
+    }
+  }
+
+  void exec_op(int op_idx) {
+    const OpNode& op = plan.ops[op_idx];
+    int lane = lane_of_op(op);
+    switch (op.kind) {
+      case OpKind::free_buffer:
+        break;  // refexec.cpp:416-417: bookkeeping only
+      case OpKind::send:
+        if (op.inputs.size() != 1) throw InternalError("send arity in " + op.id);
+        input_buffer(op.inputs[0], lane);
+        channel_src[op.channel] = op.inputs[0];
+        break;
+      case OpKind::recv: {  // refexec.cpp:422-425
+        if (op.outputs.size() != 1) throw InternalError("recv arity in " + op.id);
+        int svt = channel_src.at(op.channel);
+        const VTensor& sv = plan.vt(svt);
+        int src_lane = lane_of_op(plan.op(sv.owner_op));
+        int sb = input_buffer(svt, src_lane);
+        const VTensor& ov = plan.vt(op.outputs[0]);
+        if (region_shape(sv.mask.region) != region_shape(ov.mask.region)) {
+          throw InternalError("channel " + std::to_string(op.channel) + " piece shape mismatch at " + op.id);
+        }
+        Mask src = ov.mask;  // the channel carries the value as-is
+        std::vector<std::pair<const Mask*, int>> pieces = {{&src, sb}};
+        emit_box(op_idx, op, lane, 1, op.outputs[0], pieces, "op " + op.id);
+        Instr& in = P.instrs.back();
+        in.wire_bytes = static_cast<double>(P.buffers[sb].bytes);
+        break;
+      }
+      case OpKind::split:
+      case OpKind::concat:
+      case OpKind::reduce_assemble: {  // refexec.cpp:426-441
+        std::vector<std::pair<const Mask*, int>> pieces;
+        for (int v : op.inputs) pieces.push_back({&plan.vt(v).mask, input_buffer(v, lane)});
+        for (int out : op.outputs) emit_box(op_idx, op, lane, 0, out, pieces, "op " + op.id);
+        break;
+      }
+      default:
+        exec_compute(op_idx);
+    }
+    for (int v : op.outputs) issued_vts.insert(v);
+  }
+
+  // refexec.cpp:459-481: every member's output reconstructed from all
+  // members' input pieces.
+  void exec_collective(const CollectiveGroup& grp) {
+    std::vector<std::pair<const Mask*, int>> pieces;
+    for (const auto& oid : grp.ops) {
+      const OpNode& m = plan.op(oid);
+      int lane = lane_of_op(m);
+      for (int v : m.inputs) pieces.push_back({&plan.vt(v).mask, input_buffer(v, lane)});
+    }
+    double n = static_cast<double>(grp.message_bytes), k = grp.k;
+    double wire = 0;  // NCCL bus-bandwidth conventions
+    if (grp.primitive == "all-reduce") wire = 2.0 * (k - 1) / k * n;
+    else if (grp.primitive == "all-gather" || grp.primitive == "reduce-scatter" || grp.primitive == "all-to-all")
+      wire = (k - 1) / k * n;
+    else wire = n;
+    for (const auto& oid : grp.ops) {
+      int oi = plan.op_idx(oid);
+      const OpNode& m = plan.ops[oi];
+      int lane = lane_of_op(m);
+      for (int out : m.outputs) {
+        emit_box(oi, m, lane, 1, out, pieces, "collective " + oid);
+        P.instrs.back().wire_bytes = wire;
+        P.instrs.back().label = grp.primitive + ":" + oid;
+      }
+      for (int v : m.outputs) issued_vts.insert(v);
+      op_issued[oi] = true;
+    }
+  }
+
+  bool sync_ready(int op_idx) {
+    if (!opt.honor_sync_edges) return true;
+    auto it = sync_before.find(op_idx);
+    if (it == sync_before.end()) return true;
+    for (int b : it->second) {
+      if (!op_issued[b]) return false;
+    }
+    return true;
+  }
+
+  void add_sync_deps(int op_idx) {
+    if (!opt.honor_sync_edges) return;
+    auto it = sync_before.find(op_idx);
+    if (it == sync_before.end() || op_first_instr[op_idx] < 0) return;
+    Instr& first = P.instrs[op_first_instr[op_idx]];
+    for (int b : it->second) {
+      int li = op_last_instr[b];
+      if (li >= 0 && P.instrs[li].lane != first.lane) {
+        first.deps.push_back(li);
+      }
+    }
+    std::sort(first.deps.begin(), first.deps.end());
+    first.deps.erase(std::unique(first.deps.begin(), first.deps.end()), first.deps.end());
+  }
+
+  void run() {
+    P.num_lanes = static_cast<int>(plan.lanes.size());
+    P.lane_arena_bytes.assign(P.num_lanes, 0);
+    for (int l = 0; l < P.num_lanes; ++l) {
+      lane_of_device[plan.lanes[l].device] = l;
+      P.lane_device.push_back(plan.lanes[l].device);
+    }
+    // Element types: elem_size 4 -> f32, 2 -> bf16; embedding index operands
+    // hold integer row ids and are stored as i32 (refexec.cpp:221).
+    std::set<int> index_pts;
+    for (const auto& op : plan.ops) {
+      if ((op.kind == OpKind::embedding_lookup || op.kind == OpKind::embedding_grad) && !op.inputs.empty()) {
+        index_pts.insert(plan.vt(op.inputs[0]).ptensor);
+      }
+    }
+    for (const auto& [id, pt] : plan.ptensors) {
+      if (index_pts.count(id)) pt_dtype[id] = DType::i32;
+      else if (pt.elem_size == 4) pt_dtype[id] = DType::f32;
+      else if (pt.elem_size == 2) pt_dtype[id] = DType::bf16;
+      else throw UsageError("unsupported elem_size " + std::to_string(pt.elem_size) + " on ptensor " +
+                            std::to_string(id));
+    }
+    for (const auto& op : plan.ops) {
+      if (op.kind == OpKind::embedding_lookup || op.kind == OpKind::embedding_grad || op.kind == OpKind::send ||
+          op.kind == OpKind::recv || op.kind == OpKind::split || op.kind == OpKind::concat ||
+          op.kind == OpKind::collective || op.kind == OpKind::free_buffer || op.kind == OpKind::identity) {
+        continue;
+      }
+      for (int v : op.inputs) {
+        if (index_pts.count(plan.vt(v).ptensor)) {
+          throw UsageError("index tensor " + std::to_string(plan.vt(v).ptensor) + " consumed by " + op.id);
+        }
+      }
+    }
+    op_last_instr.assign(plan.ops.size(), -1);
+    op_first_instr.assign(plan.ops.size(), -1);
+    op_issued.assign(plan.ops.size(), false);
+    for (const auto& [a, b] : plan.sync_edges) {
+      sync_before[plan.op_idx(b)].push_back(plan.op_idx(a));
+    }
+
+    // Issue simulation: refexec.cpp:396-530 with "issued" as readiness.
+    std::map<int, std::vector<int>> members;  // group -> op idx
+    for (const auto& [gid, grp] : plan.coll_groups) {
+      for (const auto& oid : grp.ops) members[gid].push_back(plan.op_idx(oid));
+    }
+    std::vector<std::size_t> cursor(P.num_lanes, 0);
+    std::unordered_map<int, std::pair<int, std::size_t>> op_pos;
+    std::vector<std::vector<int>> lane_ops(P.num_lanes);
+    for (int l = 0; l < P.num_lanes; ++l) {
+      for (std::size_t t = 0; t < plan.lanes[l].tasks.size(); ++t) {
+        int oi = plan.op_idx(plan.lanes[l].tasks[t].op);
+        op_pos[oi] = {l, t};
+        lane_ops[l].push_back(oi);
+      }
+    }
+    auto arrived = [&](int oi) {
+      auto it = op_pos.find(oi);
+      if (it == op_pos.end()) throw InternalError("collective member " + plan.ops[oi].id + " is in no lane");
+      return cursor[it->second.first] == it->second.second;
+    };
+    std::set<int> channels_sent;
+    bool progress = true;
+    while (progress) {
+      progress = false;
+      for (int l = 0; l < P.num_lanes; ++l) {
+        while (cursor[l] < lane_ops[l].size()) {
+          int oi = lane_ops[l][cursor[l]];
+          const OpNode& op = plan.ops[oi];
+          bool ready = true;
+          if (op.kind == OpKind::recv) {
+            ready = channels_sent.count(op.channel) > 0;
+          } else if (op.kind == OpKind::collective) {
+            auto mit = members.find(op.coll_group);
+            if (mit == members.end()) throw InternalError("unknown collective group for " + op.id);
+            for (int m : mit->second) ready = ready && arrived(m);
+            if (ready) {
+              for (int m : mit->second)
+                for (int v : plan.ops[m].inputs) ready = ready && feed_ready(v);
+            }
+            if (ready) {
+              for (int m : mit->second) ready = ready && sync_ready(m);
+            }
+          } else {
+            for (int v : op.inputs) ready = ready && feed_ready(v);
+            ready = ready && sync_ready(oi);
+          }
+          if (!ready) break;
+          if (op.kind == OpKind::collective) {
+            exec_collective(plan.coll_groups.at(op.coll_group));
+            for (int m : members.at(op.coll_group)) {
+              add_sync_deps(m);
+              auto [ml, mt] = op_pos.at(m);
+              cursor[ml] = mt + 1;
+            }
+          } else {
+            exec_op(oi);
+            if (op.kind == OpKind::send) channels_sent.insert(op.channel);
+            op_issued[oi] = true;
+            add_sync_deps(oi);
+            cursor[l]++;
+          }
+          progress = true;
+        }
+      }
+    }
+    for (int l = 0; l < P.num_lanes; ++l) {
+      if (cursor[l] < lane_ops[l].size()) {
+        throw InternalError("run_plan: pairing deadlock at task " + plan.ops[lane_ops[l][cursor[l]]].id +
+                            " on device " + std::to_string(plan.lanes[l].device));
+      }
+    }
+
+    // Output reassembly table (refexec.cpp:532-556).
+    std::map<int, std::vector<int>> piece_vts;
+    for (const auto& op : plan.ops) {
+      if (op.inserted) continue;
+      for (int v : op.outputs) piece_vts[plan.vt(v).ptensor].push_back(v);
+    }
+    for (const auto& [pt, vts] : piece_vts) {
+      std::set<std::tuple<std::vector<std::int64_t>, int, int>> seen;
+      std::vector<int> bufs;
+      for (int v : vts) {
+        const Mask& m = plan.vt(v).mask;
+        std::vector<std::int64_t> key;
+        for (const auto& iv : m.region) {
+          key.push_back(iv.lo);
+          key.push_back(iv.hi);
+        }
+        if (!seen.insert({key, m.value_index, m.value_count}).second) continue;
+        auto it = vt_buf.find(v);
+        if (it == vt_buf.end()) throw InternalError("output view " + std::to_string(v) + " was never produced");
+        bufs.push_back(it->second);
+      }
+      P.outputs.push_back({pt, bufs});
+    }
+    std::set<int> gi;
+    for (const auto& b : P.buffers) {
+      if (b.graph_input) gi.insert(b.ptensor);
+    }
+    P.graph_inputs.assign(gi.begin(), gi.end());
+    P.lane_flops.assign(P.num_lanes, 0);
+    P.lane_bytes.assign(P.num_lanes, 0);
+    P.lane_wire_bytes.assign(P.num_lanes, 0);
+    for (const auto& in : P.instrs) {
+      P.lane_flops[in.lane] += in.flops;
+      P.lane_bytes[in.lane] += in.kind == InstrKind::gemm ? 0 : in.bytes;
+      P.lane_wire_bytes[in.lane] += in.wire_bytes;
+      P.total_flops += in.flops;
+      P.total_bytes += in.kind == InstrKind::gemm ? 0 : in.bytes;
+      P.total_wire_bytes += in.wire_bytes;
+    }
+  }
+};
+
+}  // namespace
+
+Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt) {
+  Builder b(plan, opt);
+  b.run();
+  return std::move(b.P);
+}
+
+std::string Program::describe_json() const {
+  std::ostringstream os;
+  os << "{\"num_lanes\":" << num_lanes << ",\"lane_device\":[";
+  for (std::size_t i = 0; i < lane_device.size(); ++i) os << (i ? "," : "") << lane_device[i];
+  os << "],\"buffers\":[";
+  for (std::size_t i = 0; i < buffers.size(); ++i) {
+    const auto& b = buffers[i];
+    os << (i ? "," : "") << "{\"id\":" << b.id << ",\"lane\":" << b.lane << ",\"pt\":" << b.ptensor
+       << ",\"dtype\":\"" << dtype_name(b.dtype) << "\",\"region\":[";
+    for (std::size_t d = 0; d < b.mask.region.size(); ++d) {
+      os << (d ? "," : "") << "[" << b.mask.region[d].lo << "," << b.mask.region[d].hi << "]";
+    }
+    os << "],\"value\":[" << b.mask.value_index << "," << b.mask.value_count << "],\"bytes\":" << b.bytes
+       << ",\"offset\":" << b.offset << ",\"graph_input\":" << (b.graph_input ? "true" : "false")
+       << ",\"weight\":" << (b.weight ? "true" : "false") << ",\"producer\":" << b.producer << "}";
+  }
+  os << "],\"instrs\":[";
+  for (std::size_t i = 0; i < instrs.size(); ++i) {
+    const auto& in = instrs[i];
+    os << (i ? "," : "") << "{\"id\":" << in.id << ",\"kind\":\"" << instr_kind_name(in.kind)
+       << "\",\"lane\":" << in.lane << ",\"stream\":" << in.stream << ",\"op\":" << in.op << ",\"label\":\""
+       << in.label << "\",\"in\":[";
+    for (std::size_t j = 0; j < in.in_bufs.size(); ++j) os << (j ? "," : "") << in.in_bufs[j];
+    os << "],\"out\":[";
+    for (std::size_t j = 0; j < in.out_bufs.size(); ++j) os << (j ? "," : "") << in.out_bufs[j];
+    os << "],\"deps\":[";
+    for (std::size_t j = 0; j < in.deps.size(); ++j) os << (j ? "," : "") << in.deps[j];
+    os << "],\"m\":" << in.m << ",\"n\":" << in.n << ",\"k\":" << in.k << ",\"ta\":" << in.ta << ",\"tb\":" << in.tb
+       << ",\"ew\":" << static_cast<int>(in.ew) << ",\"count\":" << in.count << ",\"outer\":" << in.outer
+       << ",\"axis_len\":" << in.axis_len << ",\"inner\":" << in.inner << ",\"n_idx\":" << in.n_idx
+       << ",\"rows\":" << in.rows << ",\"h\":" << in.h << ",\"lo\":" << in.lo << ",\"flops\":" << in.flops
+       << ",\"bytes\":" << in.bytes << ",\"wire_bytes\":" << in.wire_bytes << ",\"cells\":[";
+    for (std::size_t c = 0; c < in.cells.size(); ++c) {
+      const auto& cl = in.cells[c];
+      os << (c ? "," : "") << "{\"rank\":" << cl.rank << ",\"ext\":[";
+      for (int d = 0; d < cl.rank; ++d) os << (d ? "," : "") << cl.extents[d];
+      os << "],\"dst_off\":" << cl.dst_offset << ",\"dst_str\":[";
+      for (int d = 0; d < cl.rank; ++d) os << (d ? "," : "") << cl.dst_strides[d];
+      os << "],\"terms\":[";
+      for (std::size_t t = 0; t < cl.terms.size(); ++t) {
+        const auto& tm = cl.terms[t];
+        os << (t ? "," : "") << "{\"buf\":" << tm.buffer << ",\"off\":" << tm.offset << ",\"add\":" << tm.add
+           << ",\"str\":[";
+        for (int d = 0; d < cl.rank; ++d) os << (d ? "," : "") << tm.strides[d];
+        os << "]}";
+      }
+      os << "]}";
+    }
+    os << "]}";
+  }
+  os << "],\"issue_order\":[";
+  for (std::size_t i = 0; i < issue_order.size(); ++i) os << (i ? "," : "") << issue_order[i];
+  os << "],\"outputs\":[";
+  for (std::size_t i = 0; i < outputs.size(); ++i) {
+    os << (i ? "," : "") << "[" << outputs[i].first << ",[";
+    for (std::size_t j = 0; j < outputs[i].second.size(); ++j) os << (j ? "," : "") << outputs[i].second[j];
+    os << "]]";
+  }
+  os << "],\"lane_arena_bytes\":[";
+  for (std::size_t i = 0; i < lane_arena_bytes.size(); ++i) os << (i ? "," : "") << lane_arena_bytes[i];
+  os << "],\"total_flops\":" << total_flops << ",\"total_bytes\":" << total_bytes
+     << ",\"total_wire_bytes\":" << total_wire_bytes << "}";
+  return os.str();
+}
+
+}  // namespace planc_b200

@@ -1,0 +1,144 @@
+// Host-side plan compiler: ExecutionPlan -> per-lane device programs.
+//
+// Replaces the interpretation loop of the reference's run_plan
+// (proj/src/refexec.cpp:361-557) with a one-time lowering:
+//   * every producer-output vTensor gets its own device buffer on its lane;
+//     consumer views alias their feed (plan.feeds, exact mask match) and
+//     graph-input views get a placement buffer (refexec.cpp:366-376);
+//   * every task becomes zero or more device instructions: sub-operator
+//     kernels for compute ops (eval_compute, refexec.cpp:142-257) and
+//     box-copy/accumulate "cell" programs for every adapter — split, concat,
+//     reduce-assemble, recv and each collective member's output — restating
+//     reconstruct (refexec.cpp:102-140) as a static schedule of
+//     (destination box, ordered source terms, copy|add) cells;
+//   * the host issue order is the reference's round-robin lane-cursor loop
+//     (refexec.cpp:483-522) with "issued" as readiness, so pairing deadlocks
+//     are reported exactly where run_plan reports them (refexec.cpp:523-530);
+//   * cross-lane dependencies (send->recv, collective rendezvous, sync_edges)
+//     become explicit producer->consumer instruction edges, realised on the
+//     GPU as CUDA events between per-lane streams.
+// Nothing in this file touches CUDA; the lowering is unit-tested on CPU.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace planc_b200 {
+
+enum class DType : std::uint8_t { f32 = 0, bf16 = 1, i32 = 2 };
+inline std::int64_t dtype_size(DType d) { return d == DType::bf16 ? 2 : 4; }
+const char* dtype_name(DType d);
+
+constexpr int kMaxCellRank = 6;
+
+struct BufferDesc {
+  int id = 0;
+  int lane = 0;
+  int ptensor = 0;
+  Mask mask;
+  DType dtype = DType::f32;
+  std::vector<std::int64_t> shape;  // region extents, row-major dense
+  std::int64_t elems = 0;
+  std::int64_t bytes = 0;
+  std::int64_t offset = 0;     // byte offset inside the lane arena
+  bool graph_input = false;    // filled by placement from host inputs
+  bool weight = false;         // graph input of kind weight / optimizer state
+  int producer = -1;           // instruction writing it (-1: placement)
+  int vt = -1;                 // producing vTensor (or first placed view)
+};
+
+// One source of a cell: a box of another buffer, copied or accumulated.
+struct Term {
+  int buffer = 0;
+  std::int64_t offset = 0;  // element offset of the cell origin in the source
+  std::int64_t strides[kMaxCellRank] = {0};
+  bool add = false;
+};
+
+// Destination box of an adapter output with its ordered source terms.
+// value = 0; for term in terms: value = term (copy) | value += term (add).
+struct Cell {
+  int rank = 0;
+  std::int64_t extents[kMaxCellRank] = {0};
+  std::int64_t dst_offset = 0;
+  std::int64_t dst_strides[kMaxCellRank] = {0};
+  std::vector<Term> terms;
+  std::int64_t elems() const {
+    std::int64_t v = 1;
+    for (int i = 0; i < rank; ++i) v *= extents[i];
+    return v;
+  }
+};
+
+enum class InstrKind { gemm, ew, reduce, emb_lookup, emb_grad, box, nop };
+const char* instr_kind_name(InstrKind k);
+
+enum class EwOp { add = 0, mul = 1, max = 2 };
+
+struct Instr {
+  int id = 0;
+  InstrKind kind = InstrKind::nop;
+  int lane = 0;
+  int stream = 0;  // 0 = lane compute stream, 1 = lane adapter stream
+  int op = -1;     // index into plan.ops
+  std::vector<int> in_bufs;
+  std::vector<int> out_bufs;
+  std::vector<int> deps;  // producer instructions (all, incl. same stream)
+  // gemm: C[m,n] = op(A)·op(B)
+  std::int64_t m = 0, n = 0, k = 0;
+  bool ta = false, tb = false;
+  // ew
+  EwOp ew = EwOp::add;
+  std::int64_t count = 0;
+  // reduce: in [outer, axis_len, inner] -> out [outer, inner]
+  std::int64_t outer = 0, axis_len = 0, inner = 0;
+  // embedding: idx[n_idx], table/grad rows, width h, vocab offset lo
+  std::int64_t n_idx = 0, rows = 0, h = 0, lo = 0;
+  // box
+  std::vector<Cell> cells;
+  // accounting (algorithmic, from masks)
+  double flops = 0;
+  double bytes = 0;       // HBM bytes read + written
+  double wire_bytes = 0;  // NCCL bus-bandwidth convention bytes (adapters)
+  std::string label;
+};
+
+struct ProgramOptions {
+  bool value_split_extension = true;  // V(m*v) -> V(v) sums
+  bool honor_sync_edges = true;
+};
+
+struct Program {
+  int num_lanes = 0;
+  std::vector<int> lane_device;          // plan device id per lane
+  std::vector<BufferDesc> buffers;
+  std::vector<Instr> instrs;
+  std::vector<int> issue_order;          // instruction ids, global host order
+  std::vector<std::int64_t> lane_arena_bytes;
+  std::vector<int> vt_buffer;            // vt id -> buffer (-1 if none)
+  // Output reassembly (refexec.cpp:532-556): per produced pTensor, the
+  // deduplicated (region, value part) producer buffers, in op order.
+  struct OutputPiece {
+    int buffer;
+  };
+  std::vector<std::pair<int, std::vector<int>>> outputs;  // pt -> buffers
+  std::vector<int> graph_inputs;         // pTensor ids needing host data
+  double total_flops = 0, total_bytes = 0, total_wire_bytes = 0;
+  std::vector<double> lane_flops, lane_bytes, lane_wire_bytes;
+
+  std::string describe_json() const;
+};
+
+Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt = {});
+
+// Reconstruct-as-cells (refexec.cpp:102-140): target buffer box from ordered
+// pieces. Exposed for tests.
+std::vector<Cell> reconstruct_cells(const Mask& target, const std::vector<std::int64_t>& target_shape,
+                                    const std::vector<std::pair<const Mask*, int>>& pieces,
+                                    const std::vector<BufferDesc>& buffers, bool vv_extension,
+                                    const std::string& ctx);
+
+}  // namespace planc_b200

@@ -1,0 +1,675 @@
+#include "runtime.hpp"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+#include <set>
+#include <stdexcept>
+
+namespace planc_b200 {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+int dt_of(DType d) { return d == DType::bf16 ? DT_BF16 : d == DType::i32 ? DT_I32 : DT_F32; }
+
+std::uint16_t f32_to_bf16_rne(float f) {
+  std::uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return static_cast<std::uint16_t>((u >> 16) | 0x40);  // NaN
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<std::uint16_t>(u >> 16);
+}
+
+float bf16_to_f32(std::uint16_t h) {
+  std::uint32_t u = static_cast<std::uint32_t>(h) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+// Host-side value of element i of a device-typed buffer.
+double host_elem(const std::vector<char>& raw, DType d, std::int64_t i) {
+  switch (d) {
+    case DType::f32: {
+      float f;
+      std::memcpy(&f, raw.data() + 4 * i, 4);
+      return f;
+    }
+    case DType::bf16: {
+      std::uint16_t h;
+      std::memcpy(&h, raw.data() + 2 * i, 2);
+      return bf16_to_f32(h);
+    }
+    case DType::i32: {
+      std::int32_t v;
+      std::memcpy(&v, raw.data() + 4 * i, 4);
+      return v;
+    }
+  }
+  return 0;
+}
+
+void put_elem(char* dst, DType d, std::int64_t i, double v) {
+  switch (d) {
+    case DType::f32: {
+      float f = static_cast<float>(v);
+      std::memcpy(dst + 4 * i, &f, 4);
+      break;
+    }
+    case DType::bf16: {
+      std::uint16_t h = f32_to_bf16_rne(static_cast<float>(v));
+      std::memcpy(dst + 2 * i, &h, 2);
+      break;
+    }
+    case DType::i32: {
+      std::int32_t x = static_cast<std::int32_t>(v);
+      std::memcpy(dst + 4 * i, &x, 4);
+      break;
+    }
+  }
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+}  // namespace
+
+Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gpu, const ExecOptions& opt)
+    : opt_(opt) {
+  plan_ = load_plan(plan_json);
+  ProgramOptions po;
+  po.value_split_extension = opt.value_split_extension;
+  prog_ = build_program(plan_, po);
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  lanes_.resize(prog_.num_lanes);
+  std::set<int> gset;
+  for (int l = 0; l < prog_.num_lanes; ++l) {
+    int g = lane_gpu.empty() ? 0 : lane_gpu[l % lane_gpu.size()];
+    if (g < 0 || g >= ndev) throw UsageError("lane " + std::to_string(l) + " mapped to missing GPU " + std::to_string(g));
+    lanes_[l].gpu = g;
+    gset.insert(g);
+  }
+  gpus_.assign(gset.begin(), gset.end());
+  // Lanes on different GPUs read each other's buffers through NVLink peer
+  // mappings inside the box kernels.
+  for (int a : gpus_) {
+    DeviceGuard dg(a);
+    for (int b : gpus_) {
+      if (a == b) continue;
+      int can = 0;
+      ck(cudaDeviceCanAccessPeer(&can, a, b), "cudaDeviceCanAccessPeer");
+      if (!can) throw UsageError("GPU " + std::to_string(a) + " cannot map GPU " + std::to_string(b));
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else ck(e, "cudaDeviceEnablePeerAccess");
+    }
+  }
+  for (int l = 0; l < prog_.num_lanes; ++l) {
+    DeviceGuard dg(lanes_[l].gpu);
+    std::int64_t bytes = std::max<std::int64_t>(prog_.lane_arena_bytes[l], 256);
+    ck(cudaMalloc(&lanes_[l].arena, bytes), "cudaMalloc(arena)");
+    for (auto& s : lanes_[l].stream) ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  }
+  {
+    DeviceGuard dg(lanes_.empty() ? 0 : lanes_[0].gpu);
+    ck(cudaStreamCreateWithFlags(&origin_, cudaStreamNonBlocking), "origin stream");
+    ck(cudaEventCreateWithFlags(&ev_begin_, cudaEventDisableTiming), "event");
+    ck(cudaEventCreate(&ev_end_), "event");
+  }
+  for (int l = 0; l < prog_.num_lanes; ++l) {
+    DeviceGuard dg(lanes_[l].gpu);
+    for (int s = 0; s < 2; ++s) {
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      lane_join_.push_back(e);
+    }
+  }
+  // Element types must agree across an elementwise op's operands.
+  for (const auto& in : prog_.instrs) {
+    if (in.kind == InstrKind::ew) {
+      DType d = prog_.buffers[in.out_bufs[0]].dtype;
+      for (int b : in.in_bufs) {
+        if (prog_.buffers[b].dtype != d) {
+          throw UsageError("elementwise op " + plan_.ops[in.op].id + " mixes element sizes");
+        }
+      }
+    }
+  }
+  // Events for producer -> consumer edges that cross streams.
+  irt_.resize(prog_.instrs.size());
+  for (const auto& in : prog_.instrs) {
+    for (int d : in.deps) {
+      const Instr& p = prog_.instrs[d];
+      if ((p.lane != in.lane || p.stream != in.stream) && !irt_[d].done) {
+        DeviceGuard dg(lanes_[p.lane].gpu);
+        ck(cudaEventCreateWithFlags(&irt_[d].done, cudaEventDisableTiming), "event");
+      }
+    }
+    if (in.kind == InstrKind::emb_grad && prog_.buffers[in.out_bufs[0]].dtype != DType::f32) {
+      DeviceGuard dg(lanes_[in.lane].gpu);
+      ck(cudaMalloc(&irt_[in.id].scratch, sizeof(float) * in.rows * in.h), "cudaMalloc(scratch)");
+    }
+  }
+  build_box_tables();
+  kernels_per_step_ = 0;
+  for (const auto& in : prog_.instrs) {
+    switch (in.kind) {
+      case InstrKind::nop: break;
+      case InstrKind::box: kernels_per_step_ += static_cast<int>(irt_[in.id].box.size()); break;
+      case InstrKind::emb_grad: kernels_per_step_ += prog_.buffers[in.out_bufs[0]].dtype == DType::f32 ? 2 : 3; break;
+      case InstrKind::ew: kernels_per_step_ += 1 + (in.count % 8 != 0 ? 1 : 0); break;
+      default: kernels_per_step_ += 1;
+    }
+    if (in.kind == InstrKind::gemm) {
+      GemmArgs a{};
+      a.m = in.m;
+      a.n = in.n;
+      a.k = in.k;
+      a.ta = in.ta;
+      a.tb = in.tb;
+      a.da = dt_of(prog_.buffers[in.in_bufs[0]].dtype);
+      a.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
+      a.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
+      if (opt_.allow_tensor_cores && gemm_sm100_eligible(a)) ++gemm_tc_per_step_;
+    }
+  }
+}
+
+Executor::~Executor() {
+  for (auto& l : lanes_) {
+    cudaSetDevice(l.gpu);
+    for (auto& s : l.stream)
+      if (s) cudaStreamDestroy(s);
+    if (l.arena) cudaFree(l.arena);
+  }
+  for (auto& r : irt_) {
+    if (r.done) cudaEventDestroy(r.done);
+    if (r.scratch) cudaFree(r.scratch);
+  }
+  for (void* p : table_allocs_) cudaFree(p);
+  for (auto e : lane_join_) cudaEventDestroy(e);
+  for (void* p : pinned_in_) cudaFreeHost(p);
+  for (void* p : pinned_out_) cudaFreeHost(p);
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  if (ev_begin_) cudaEventDestroy(ev_begin_);
+  if (ev_end_) cudaEventDestroy(ev_end_);
+  if (origin_) cudaStreamDestroy(origin_);
+}
+
+void* Executor::buf_ptr(int b) const {
+  const BufferDesc& d = prog_.buffers[b];
+  return lanes_[d.lane].arena + d.offset;
+}
+
+cudaStream_t Executor::stream_of(const Instr& in) const { return lanes_[in.lane].stream[in.stream]; }
+
+void Executor::build_box_tables() {
+  constexpr std::int64_t kChunkUnits = 4096;
+  for (const auto& in : prog_.instrs) {
+    if (in.kind != InstrKind::box) continue;
+    const BufferDesc& ob = prog_.buffers[in.out_bufs[0]];
+    const std::int64_t V = 16 / dtype_size(ob.dtype);
+    std::vector<const Cell*> groups[2];
+    for (const auto& c : in.cells) {
+      bool vec = c.dst_strides[c.rank - 1] == 1 && c.extents[c.rank - 1] % V == 0 && c.dst_offset % V == 0;
+      for (int d = 0; d + 1 < c.rank; ++d) vec = vec && c.dst_strides[d] % V == 0;
+      for (const auto& t : c.terms) {
+        vec = vec && t.strides[c.rank - 1] == 1 && t.offset % V == 0;
+        for (int d = 0; d + 1 < c.rank; ++d) vec = vec && t.strides[d] % V == 0;
+      }
+      groups[vec ? 1 : 0].push_back(&c);
+    }
+    for (int g = 0; g < 2; ++g) {
+      if (groups[g].empty()) continue;
+      std::int64_t width = g ? V : 1;
+      std::vector<DevCell> cells;
+      std::vector<DevTerm> terms;
+      std::vector<DevChunk> chunks;
+      for (const Cell* c : groups[g]) {
+        DevCell dc{};
+        dc.rank = c->rank;
+        for (int d = 0; d < c->rank; ++d) {
+          dc.ext[d] = c->extents[d];
+          dc.dst_str[d] = c->dst_strides[d];
+        }
+        dc.dst_off = c->dst_offset;
+        dc.elems = c->elems();
+        dc.nterms = static_cast<int>(c->terms.size());
+        dc.term0 = static_cast<int>(terms.size());
+        dc.vec = static_cast<int>(width);
+        for (const auto& t : c->terms) {
+          DevTerm dt{};
+          dt.src = buf_ptr(t.buffer);
+          dt.offset = t.offset;
+          for (int d = 0; d < c->rank; ++d) dt.str[d] = t.strides[d];
+          dt.add = t.add ? 1 : 0;
+          terms.push_back(dt);
+        }
+        int ci = static_cast<int>(cells.size());
+        cells.push_back(dc);
+        std::int64_t units = dc.elems / width;
+        for (std::int64_t b = 0; b < units; b += kChunkUnits) {
+          DevChunk ch{};
+          ch.cell = ci;
+          ch.begin = b;
+          ch.count = std::min(kChunkUnits, units - b);
+          chunks.push_back(ch);
+        }
+      }
+      if (chunks.empty()) continue;
+      DeviceGuard dg(lanes_[in.lane].gpu);
+      std::size_t cb = cells.size() * sizeof(DevCell), tb = terms.size() * sizeof(DevTerm),
+                  hb = chunks.size() * sizeof(DevChunk);
+      char* mem = nullptr;
+      ck(cudaMalloc(&mem, cb + tb + hb + 64), "cudaMalloc(box table)");
+      table_allocs_.push_back(mem);
+      ck(cudaMemcpy(mem, cells.data(), cb, cudaMemcpyHostToDevice), "box table");
+      if (tb) ck(cudaMemcpy(mem + cb, terms.data(), tb, cudaMemcpyHostToDevice), "box table");
+      ck(cudaMemcpy(mem + cb + tb, chunks.data(), hb, cudaMemcpyHostToDevice), "box table");
+      BoxLaunch bl;
+      bl.cells = reinterpret_cast<DevCell*>(mem);
+      bl.terms = reinterpret_cast<DevTerm*>(mem + cb);
+      bl.chunks = reinterpret_cast<DevChunk*>(mem + cb + tb);
+      bl.nchunks = static_cast<int>(chunks.size());
+      bl.vec = g;
+      irt_[in.id].box.push_back(bl);
+    }
+  }
+}
+
+void Executor::set_input(int ptensor, const double* data, const std::vector<std::int64_t>& shape) {
+  HostTensor t;
+  t.shape = shape;
+  std::int64_t vol = 1;
+  for (auto e : shape) vol *= e;
+  t.data.assign(data, data + vol);
+  inputs_[ptensor] = std::move(t);
+  inputs_dirty_ = true;
+}
+
+// Graph-input placement (refexec.cpp:366-376): each view's region of the
+// host pTensor, converted to the device element type.
+void Executor::place_inputs() {
+  if (!inputs_dirty_) return;
+  for (const auto& b : prog_.buffers) {
+    if (!b.graph_input) continue;
+    auto it = inputs_.find(b.ptensor);
+    if (it == inputs_.end()) throw UsageError("run_plan: missing input tensor " + std::to_string(b.ptensor));
+    const PTensor& pt = plan_.pt(b.ptensor);
+    if (it->second.shape != pt.shape) {
+      throw UsageError("input tensor " + std::to_string(b.ptensor) + " has the wrong shape");
+    }
+    std::vector<char> host(b.bytes);
+    const int rank = static_cast<int>(b.shape.size());
+    std::vector<std::int64_t> gstr(rank, 1);
+    for (int d = rank - 2; d >= 0; --d) gstr[d] = gstr[d + 1] * pt.shape[d + 1];
+    std::vector<std::int64_t> idx(rank, 0);
+    for (std::int64_t e = 0; e < b.elems; ++e) {
+      std::int64_t g = 0;
+      for (int d = 0; d < rank; ++d) g += (b.mask.region[d].lo + idx[d]) * gstr[d];
+      put_elem(host.data(), b.dtype, e, it->second.data[g]);
+      for (int d = rank - 1; d >= 0; --d) {
+        if (++idx[d] < b.shape[d]) break;
+        idx[d] = 0;
+      }
+    }
+    DeviceGuard dg(lanes_[b.lane].gpu);
+    ck(cudaMemcpy(buf_ptr(b.id), host.data(), b.bytes, cudaMemcpyHostToDevice), "input placement");
+  }
+  inputs_dirty_ = false;
+}
+
+void Executor::launch_instr(const Instr& in, cudaStream_t s) {
+  switch (in.kind) {
+    case InstrKind::nop:
+      return;
+    case InstrKind::gemm: {
+      GemmArgs a{};
+      a.A = buf_ptr(in.in_bufs[0]);
+      a.B = buf_ptr(in.in_bufs[1]);
+      a.C = buf_ptr(in.out_bufs[0]);
+      a.m = in.m;
+      a.n = in.n;
+      a.k = in.k;
+      a.ta = in.ta;
+      a.tb = in.tb;
+      a.da = dt_of(prog_.buffers[in.in_bufs[0]].dtype);
+      a.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
+      a.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
+      launch_gemm(a, s, opt_.allow_tensor_cores, nullptr);
+      return;
+    }
+    case InstrKind::ew: {
+      int dt = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
+      std::vector<const void*> ptrs;
+      for (int b : in.in_bufs) ptrs.push_back(buf_ptr(b));
+      void* out = buf_ptr(in.out_bufs[0]);
+      // Left fold in chunks of 8 operands: ((x0∘x1)∘…)∘x7, then (out∘x8)∘…
+      std::size_t pos = 0;
+      while (pos < ptrs.size()) {
+        std::vector<const void*> grp;
+        if (pos > 0) grp.push_back(out);
+        while (grp.size() < 8 && pos < ptrs.size()) grp.push_back(ptrs[pos++]);
+        launch_ew(static_cast<int>(in.ew), dt, grp.data(), static_cast<int>(grp.size()), out, in.count, s);
+      }
+      return;
+    }
+    case InstrKind::reduce:
+      launch_reduce(dt_of(prog_.buffers[in.out_bufs[0]].dtype), buf_ptr(in.in_bufs[0]), buf_ptr(in.out_bufs[0]),
+                    in.outer, in.axis_len, in.inner, s);
+      return;
+    case InstrKind::emb_lookup:
+      launch_emb_lookup(dt_of(prog_.buffers[in.out_bufs[0]].dtype), static_cast<const int*>(buf_ptr(in.in_bufs[0])),
+                        buf_ptr(in.in_bufs[1]), buf_ptr(in.out_bufs[0]), in.n_idx, in.rows, in.h, in.lo, s);
+      return;
+    case InstrKind::emb_grad:
+      launch_emb_grad(dt_of(prog_.buffers[in.out_bufs[0]].dtype), static_cast<const int*>(buf_ptr(in.in_bufs[0])),
+                      buf_ptr(in.in_bufs[1]), buf_ptr(in.out_bufs[0]), irt_[in.id].scratch, in.n_idx, in.rows, in.h,
+                      in.lo, s);
+      return;
+    case InstrKind::box: {
+      int dt = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
+      for (const auto& bl : irt_[in.id].box) {
+        launch_box(buf_ptr(in.out_bufs[0]), dt, bl.cells, bl.terms, bl.chunks, bl.nchunks, bl.vec, s);
+      }
+      return;
+    }
+  }
+}
+
+void Executor::issue_step(bool, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>*) {
+  int cur = -1;
+  auto set_dev = [&](int g) {
+    if (g != cur && gpus_.size() > 1) {
+      ck(cudaSetDevice(g), "cudaSetDevice");
+    }
+    cur = g;
+  };
+  set_dev(lanes_[0].gpu);
+  ck(cudaEventRecord(ev_begin_, origin_), "record begin");
+  for (auto& l : lanes_)
+    for (auto s : l.stream) ck(cudaStreamWaitEvent(s, ev_begin_, 0), "wait begin");
+  for (int id : prog_.issue_order) {
+    const Instr& in = prog_.instrs[id];
+    cudaStream_t s = stream_of(in);
+    set_dev(lanes_[in.lane].gpu);
+    for (int d : in.deps) {
+      const Instr& p = prog_.instrs[d];
+      if (p.lane != in.lane || p.stream != in.stream) ck(cudaStreamWaitEvent(s, irt_[d].done, 0), "wait dep");
+    }
+    launch_instr(in, s);
+    if (irt_[id].done) ck(cudaEventRecord(irt_[id].done, s), "record done");
+  }
+  int j = 0;
+  for (auto& l : lanes_) {
+    set_dev(l.gpu);
+    for (auto s : l.stream) {
+      ck(cudaEventRecord(lane_join_[j], s), "record join");
+      ++j;
+    }
+  }
+  set_dev(lanes_[0].gpu);
+  for (auto e : lane_join_) ck(cudaStreamWaitEvent(origin_, e, 0), "wait join");
+}
+
+void Executor::ensure_graph() {
+  if (!opt_.use_graph || graph_exec_) return;
+  DeviceGuard dg(lanes_[0].gpu);
+  ck(cudaStreamBeginCapture(origin_, cudaStreamCaptureModeThreadLocal), "begin capture");
+  bool ok = true;
+  try {
+    issue_step(false, nullptr);
+  } catch (const std::exception&) {
+    ok = false;
+  }
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(origin_, &g);
+  if (!ok || e != cudaSuccess || !g) {
+    cudaGetLastError();
+    if (g) cudaGraphDestroy(g);
+    opt_.use_graph = false;  // eager issue from here on
+    return;
+  }
+  e = cudaGraphInstantiate(&graph_exec_, g, 0);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    graph_exec_ = nullptr;
+    opt_.use_graph = false;
+    return;
+  }
+  graph_ = g;
+}
+
+double Executor::run(int iters) {
+  place_inputs();
+  ensure_graph();
+  DeviceGuard dg(lanes_[0].gpu);
+  auto step = [&]() {
+    if (graph_exec_) ck(cudaGraphLaunch(graph_exec_, origin_), "graph launch");
+    else issue_step(false, nullptr);
+  };
+  if (iters <= 0) {
+    step();
+    ck(cudaStreamSynchronize(origin_), "step");
+    return 0;
+  }
+  cudaEvent_t t0, t1;
+  ck(cudaEventCreate(&t0), "event");
+  ck(cudaEventCreate(&t1), "event");
+  ck(cudaEventRecord(t0, origin_), "record");
+  for (int i = 0; i < iters; ++i) step();
+  ck(cudaEventRecord(t1, origin_), "record");
+  ck(cudaEventSynchronize(t1), "sync");
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, t0, t1), "elapsed");
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  return ms / iters;
+}
+
+double Executor::run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_bytes) {
+  place_inputs();
+  ensure_graph();
+  DeviceGuard dg(lanes_[0].gpu);
+  if (pinned_in_.empty() && pinned_out_.empty()) {
+    // Step inputs: non-weight graph-input placements, staged from pinned host
+    // memory in device element type (weights stay resident, like a trainer).
+    for (const auto& b : prog_.buffers) {
+      if (!b.graph_input || b.weight) continue;
+      void* h = nullptr;
+      ck(cudaMallocHost(&h, std::max<std::int64_t>(b.bytes, 1)), "cudaMallocHost");
+      ck(cudaMemcpy(h, buf_ptr(b.id), b.bytes, cudaMemcpyDeviceToHost), "stage input");
+      pinned_in_.push_back(h);
+      e2e_in_bufs_.push_back(b.id);
+    }
+    // Step results: every piece of a terminal (never consumed), non-weight
+    // produced pTensor.
+    std::set<int> consumed;
+    for (const auto& op : plan_.ops)
+      for (int v : op.inputs) consumed.insert(plan_.vt(v).ptensor);
+    for (const auto& [pt, bufs] : prog_.outputs) {
+      TensorKind k = plan_.pt(pt).kind;
+      if (consumed.count(pt) || k == TensorKind::weight || k == TensorKind::optimizer_state) continue;
+      for (int b : bufs) {
+        void* h = nullptr;
+        ck(cudaMallocHost(&h, std::max<std::int64_t>(prog_.buffers[b].bytes, 1)), "cudaMallocHost");
+        pinned_out_.push_back(h);
+        e2e_out_bufs_.push_back(b);
+      }
+    }
+  }
+  std::int64_t hb = 0, db = 0;
+  for (int b : e2e_in_bufs_) hb += prog_.buffers[b].bytes;
+  for (int b : e2e_out_bufs_) db += prog_.buffers[b].bytes;
+  if (h2d_bytes) *h2d_bytes = hb;
+  if (d2h_bytes) *d2h_bytes = db;
+  auto step = [&]() {
+    for (std::size_t i = 0; i < e2e_in_bufs_.size(); ++i) {
+      const auto& b = prog_.buffers[e2e_in_bufs_[i]];
+      ck(cudaMemcpyAsync(buf_ptr(b.id), pinned_in_[i], b.bytes, cudaMemcpyHostToDevice, origin_), "h2d");
+    }
+    if (graph_exec_) ck(cudaGraphLaunch(graph_exec_, origin_), "graph launch");
+    else issue_step(false, nullptr);
+    for (std::size_t i = 0; i < e2e_out_bufs_.size(); ++i) {
+      const auto& b = prog_.buffers[e2e_out_bufs_[i]];
+      ck(cudaMemcpyAsync(pinned_out_[i], buf_ptr(b.id), b.bytes, cudaMemcpyDeviceToHost, origin_), "d2h");
+    }
+  };
+  step();
+  ck(cudaStreamSynchronize(origin_), "warmup");
+  cudaEvent_t t0, t1;
+  ck(cudaEventCreate(&t0), "event");
+  ck(cudaEventCreate(&t1), "event");
+  ck(cudaEventRecord(t0, origin_), "record");
+  for (int i = 0; i < iters; ++i) step();
+  ck(cudaEventRecord(t1, origin_), "record");
+  ck(cudaEventSynchronize(t1), "sync");
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, t0, t1), "elapsed");
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  return ms / std::max(iters, 1);
+}
+
+std::vector<KernelStat> Executor::profile() {
+  place_inputs();
+  std::map<std::string, KernelStat> acc;
+  std::vector<std::string> order;
+  for (int id : prog_.issue_order) {
+    const Instr& in = prog_.instrs[id];
+    if (in.kind == InstrKind::nop) continue;
+    DeviceGuard dg(lanes_[in.lane].gpu);
+    cudaStream_t s = lanes_[in.lane].stream[0];
+    for (auto& l : lanes_) {
+      cudaSetDevice(l.gpu);
+      ck(cudaDeviceSynchronize(), "profile sync");
+    }
+    cudaSetDevice(lanes_[in.lane].gpu);
+    cudaEvent_t a, b;
+    ck(cudaEventCreate(&a), "event");
+    ck(cudaEventCreate(&b), "event");
+    ck(cudaEventRecord(a, s), "record");
+    launch_instr(in, s);
+    ck(cudaEventRecord(b, s), "record");
+    ck(cudaEventSynchronize(b), "sync");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    std::string kind;
+    switch (in.kind) {
+      case InstrKind::gemm: {
+        GemmArgs g{};
+        g.m = in.m;
+        g.n = in.n;
+        g.k = in.k;
+        g.ta = in.ta;
+        g.tb = in.tb;
+        g.da = dt_of(prog_.buffers[in.in_bufs[0]].dtype);
+        g.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
+        g.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
+        kind = opt_.allow_tensor_cores && gemm_sm100_eligible(g) ? "gemm_tc" : "gemm_simt";
+        break;
+      }
+      case InstrKind::ew: kind = "ew"; break;
+      case InstrKind::reduce: kind = "reduce"; break;
+      case InstrKind::emb_lookup:
+      case InstrKind::emb_grad: kind = "embedding"; break;
+      case InstrKind::box:
+        // Collective member outputs are labelled "<primitive>:<op>".
+        kind = in.label.find(':') != std::string::npos ? "box_collective"
+               : in.wire_bytes > 0                     ? "box_p2p"
+                                                       : "box_local";
+        break;
+      default: kind = "other";
+    }
+    auto& st = acc[kind];
+    if (st.kind.empty()) {
+      st.kind = kind;
+      order.push_back(kind);
+    }
+    st.launches += 1;
+    st.ms += ms;
+    st.flops += in.flops;
+    st.bytes += in.bytes;
+    st.wire_bytes += in.wire_bytes;
+  }
+  std::vector<KernelStat> out;
+  for (const auto& k : order) out.push_back(acc[k]);
+  return out;
+}
+
+std::vector<int> Executor::output_ids() const {
+  std::vector<int> ids;
+  for (const auto& o : prog_.outputs) ids.push_back(o.first);
+  return ids;
+}
+
+// Reassembly of a produced pTensor (refexec.cpp:532-556): the deduplicated
+// producer pieces are read back and reconstructed into the full tensor on
+// the host in double, like the reference returns them.
+HostTensor Executor::get_output(int ptensor) {
+  const std::vector<int>* bufs = nullptr;
+  for (const auto& o : prog_.outputs)
+    if (o.first == ptensor) bufs = &o.second;
+  if (!bufs) throw UsageError("ptensor " + std::to_string(ptensor) + " is not a plan output");
+  for (auto& l : lanes_) {
+    DeviceGuard dg(l.gpu);
+    ck(cudaDeviceSynchronize(), "sync before readback");
+  }
+  const PTensor& pt = plan_.pt(ptensor);
+  HostTensor out;
+  out.shape = pt.shape;
+  out.data.assign(pt.volume(), 0.0);
+  Mask full;
+  for (auto e : pt.shape) full.region.push_back({0, e});
+  std::vector<std::pair<const Mask*, int>> pieces;
+  std::map<int, std::vector<char>> raw;
+  for (int b : *bufs) {
+    const BufferDesc& bd = prog_.buffers[b];
+    pieces.push_back({&bd.mask, b});
+    std::vector<char> r(bd.bytes);
+    DeviceGuard dg(lanes_[bd.lane].gpu);
+    ck(cudaMemcpy(r.data(), buf_ptr(b), bd.bytes, cudaMemcpyDeviceToHost), "readback");
+    raw[b] = std::move(r);
+  }
+  auto cells = reconstruct_cells(full, pt.shape, pieces, prog_.buffers, opt_.value_split_extension,
+                                 "output " + std::to_string(ptensor));
+  for (const auto& c : cells) {
+    std::int64_t n = c.elems();
+    std::vector<std::int64_t> idx(c.rank, 0);
+    for (std::int64_t e = 0; e < n; ++e) {
+      std::int64_t doff = c.dst_offset;
+      for (int d = 0; d < c.rank; ++d) doff += idx[d] * c.dst_strides[d];
+      double v = 0;
+      for (const auto& t : c.terms) {
+        std::int64_t so = t.offset;
+        for (int d = 0; d < c.rank; ++d) so += idx[d] * t.strides[d];
+        double x = host_elem(raw[t.buffer], prog_.buffers[t.buffer].dtype, so);
+        v = t.add ? v + x : x;
+      }
+      out.data[doff] = v;
+      for (int d = c.rank - 1; d >= 0; --d) {
+        if (++idx[d] < c.extents[d]) break;
+        idx[d] = 0;
+      }
+    }
+  }
+  return out;
+}
+
+}  // namespace planc_b200

@@ -1,0 +1,121 @@
+// B200 plan executor runtime: device memory, per-lane streams, cross-lane
+// events, CUDA-graph capture of one plan step, inputs/outputs.
+//
+// The drop-in replacement for the reference's
+//   TensorMap planc::run_plan(const ExecutionPlan&, const TensorMap&)
+// (reference include/planc/refexec.hpp:43, proj/src/refexec.cpp:361-557).
+// One Executor owns one plan; every plan lane ("device" of the plan) is
+// mapped to a CUDA device ordinal (several lanes may share one B200, each
+// with its own streams, which is how multi-device plans are parity-tested on
+// one GPU). Lanes on different GPUs of one process read each other's buffers
+// through NVLink peer mappings inside the same fused box kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "plan.hpp"
+#include "program.hpp"
+
+namespace planc_b200 {
+
+struct HostTensor {
+  std::vector<std::int64_t> shape;
+  std::vector<double> data;
+};
+
+struct KernelStat {
+  std::string kind;  // gemm_tc, gemm_simt, ew, reduce, emb, box_local, box_coll, box_recv
+  int launches = 0;
+  double ms = 0;
+  double flops = 0;
+  double bytes = 0;
+  double wire_bytes = 0;
+};
+
+struct ExecOptions {
+  bool use_graph = true;       // capture one step into a CUDA graph
+  bool allow_tensor_cores = true;
+  bool value_split_extension = true;
+};
+
+class Executor {
+ public:
+  Executor(const std::string& plan_json, const std::vector<int>& lane_gpu, const ExecOptions& opt);
+  ~Executor();
+  Executor(const Executor&) = delete;
+  Executor& operator=(const Executor&) = delete;
+
+  const ExecutionPlan& plan() const { return plan_; }
+  const Program& program() const { return prog_; }
+
+  void set_input(int ptensor, const double* data, const std::vector<std::int64_t>& shape);
+  // Runs `iters` plan steps; returns mean device milliseconds per step
+  // (CUDA events on the origin stream, after one untimed warm-up when
+  // iters > 0 and the graph is not yet built).
+  double run(int iters);
+  // End-to-end: per step, H2D of every non-weight graph-input placement from
+  // pinned host memory, the step, D2H of every terminal output piece.
+  double run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_bytes);
+  // Per-kernel-family device time of one eagerly issued, serialised step.
+  std::vector<KernelStat> profile();
+  HostTensor get_output(int ptensor);
+  std::vector<int> output_ids() const;
+  int kernels_per_step() const { return kernels_per_step_; }
+  int gemm_tc_launches() const { return gemm_tc_per_step_; }
+  bool graph_captured() const { return graph_exec_ != nullptr; }
+
+ private:
+  struct LaneRt {
+    int gpu = 0;
+    char* arena = nullptr;
+    cudaStream_t stream[2] = {nullptr, nullptr};
+  };
+  struct BoxLaunch {
+    DevCell* cells = nullptr;
+    DevTerm* terms = nullptr;
+    DevChunk* chunks = nullptr;
+    int nchunks = 0;
+    int vec = 0;
+  };
+  struct InstrRt {
+    std::vector<BoxLaunch> box;
+    cudaEvent_t done = nullptr;  // recorded when a later instruction on another stream depends on it
+    float* scratch = nullptr;
+  };
+
+  void* buf_ptr(int b) const;
+  cudaStream_t stream_of(const Instr& in) const;
+  void build_box_tables();
+  void place_inputs();
+  void issue_step(bool timing_events, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* ev);
+  void launch_instr(const Instr& in, cudaStream_t s);
+  void ensure_graph();
+
+  ExecutionPlan plan_;
+  Program prog_;
+  ExecOptions opt_;
+  std::vector<LaneRt> lanes_;
+  std::vector<InstrRt> irt_;
+  std::vector<int> gpus_;  // distinct devices
+  std::vector<void*> table_allocs_;
+  std::map<int, HostTensor> inputs_;
+  bool inputs_dirty_ = true;
+  cudaStream_t origin_ = nullptr;
+  cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr;
+  std::vector<cudaEvent_t> lane_join_;
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  int kernels_per_step_ = 0;
+  int gemm_tc_per_step_ = 0;
+  // e2e staging
+  std::vector<void*> pinned_in_, pinned_out_;
+  std::vector<int> e2e_in_bufs_, e2e_out_bufs_;
+};
+
+}  // namespace planc_b200

@@ -1,0 +1,190 @@
+"""Regenerates the golden parity fixtures in tests/golden/ (test infrastructure).
+
+Every case is produced by the UNMODIFIED reference (oracle/_ref, built from
+/root/reference by oracle/Makefile) in this container:
+
+  graph.json  the graph document (reference fixtures or oracle/docs.py)
+  plan.json   reference compile() -> save_plan() (proj/src/compile.cpp:7,
+              simulate.cpp:492) — the executor's input
+  io.npz      in_<pt>: random_integer_inputs(graph, seed) (refexec.cpp:559)
+              exp_<pt>: run_reference(graph, inputs)     (refexec.cpp:264)
+              ref_<pt>: run_plan(plan, inputs)            (refexec.cpp:361),
+                        absent when the reference executor throws
+  meta.json   seed, tolerance, provenance (reference test file:line)
+
+The GPU box has no /root/reference, so the tests read these committed files.
+Run:  python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from oracle import docs, refpy  # noqa: E402
+
+TP_TEST_DOC = json.dumps({
+    "ptensors": [
+        {"id": 0, "shape": [4, 4], "elem_size": 4, "kind": "activation"},
+        {"id": 1, "shape": [4, 4], "elem_size": 4, "kind": "weight"},
+        {"id": 2, "shape": [4, 4], "elem_size": 4, "kind": "activation"},
+        {"id": 3, "shape": [4, 4], "elem_size": 4, "kind": "weight"},
+        {"id": 4, "shape": [4, 4], "elem_size": 4, "kind": "activation"}],
+    "ops": [
+        {"id": "mm1", "kind": "matmul", "inputs": [0, 1], "outputs": [2], "direction": "forward", "flops": 128},
+        {"id": "mm2", "kind": "matmul", "inputs": [2, 3], "outputs": [4], "direction": "forward", "flops": 128}]})
+
+REDUCE_DOC = json.dumps({
+    "ptensors": [{"id": 0, "shape": [2, 3], "elem_size": 4, "kind": "activation"},
+                 {"id": 1, "shape": [2], "elem_size": 4, "kind": "activation"}],
+    "ops": [{"id": "r", "kind": "reduce-sum", "inputs": [0], "outputs": [1], "direction": "forward",
+             "flops": 6, "attrs": {"axis": 1}}]})
+
+EMB_DOC = json.dumps({
+    "ptensors": [
+        {"id": 0, "shape": [3], "elem_size": 4, "kind": "activation"},
+        {"id": 1, "shape": [4, 2], "elem_size": 4, "kind": "weight"},
+        {"id": 2, "shape": [3, 2], "elem_size": 4, "kind": "activation"},
+        {"id": 3, "shape": [3, 2], "elem_size": 4, "kind": "gradient", "grad_of": 2},
+        {"id": 4, "shape": [4, 2], "elem_size": 4, "kind": "gradient", "grad_of": 1}],
+    "ops": [
+        {"id": "e", "kind": "embedding-lookup", "inputs": [0, 1], "outputs": [2], "direction": "forward", "flops": 6},
+        {"id": "ge", "kind": "embedding-grad", "inputs": [0, 3], "outputs": [4], "direction": "backward",
+         "flops": 6, "backward_of": "e"}]})
+
+
+def chain2(rows, cols, mid, elem=4):
+    """Two chained matmuls A[rows,mid]·W1[mid,cols] -> T, T·W2[cols,cols] -> C."""
+    return json.dumps({
+        "ptensors": [
+            {"id": 0, "shape": [rows, mid], "elem_size": elem, "kind": "activation"},
+            {"id": 1, "shape": [mid, cols], "elem_size": elem, "kind": "weight"},
+            {"id": 2, "shape": [rows, cols], "elem_size": elem, "kind": "activation"},
+            {"id": 3, "shape": [cols, cols], "elem_size": elem, "kind": "weight"},
+            {"id": 4, "shape": [rows, cols], "elem_size": elem, "kind": "activation"}],
+        "ops": [
+            {"id": "mm1", "kind": "matmul", "inputs": [0, 1], "outputs": [2], "direction": "forward",
+             "flops": 2.0 * rows * cols * mid},
+            {"id": "mm2", "kind": "matmul", "inputs": [2, 3], "outputs": [4], "direction": "forward",
+             "flops": 2.0 * rows * cols * cols}]})
+
+
+def cases():
+    tu = dict(testutil_cluster=1)
+    mlp = refpy.mlp_doc()
+    out = [
+        # name, doc, compile spec, seed, rel_tol, provenance
+        ("mlp_dp2", mlp, dict(strategy="data_parallel", devices=2, **tu), 5, 0.0,
+         "test_refexec.cpp:89-98 (DP plan seed 5)"),
+        ("mlp_dp2_naive", mlp, dict(strategy="data_parallel", devices=2, pattern_match=0, **tu), 21, 0.0,
+         "test_materialize.cpp:341-351 / test_refexec.cpp:142-150 (send/recv + reduce-assemble)"),
+        ("mlp_dp4", refpy.mlp_doc(batch=8, hidden=8), dict(strategy="data_parallel", devices=4, **tu), 77, 0.0,
+         "test_commplan.cpp:332-366 (DP all-reduce seed 77)"),
+        ("mlp_bias_dp2", refpy.mlp_doc(bias=True), dict(strategy="data_parallel", devices=2, **tu), 13, 0.0,
+         "mlp_doc bias variant (identity backward)"),
+        ("tp_value_split", TP_TEST_DOC, dict(strategy="manual", devices=2, target_ops="mm1@v,mm2@s0", **tu), 9,
+         0.0, "test_refexec.cpp:100-140 (value split + collective seed 9)"),
+        ("reduce_sum", REDUCE_DOC, dict(strategy="none", devices=1), 1, 0.0, "test_refexec.cpp:43-57"),
+        ("embedding", EMB_DOC, dict(strategy="none", devices=1), 2, 0.0, "test_refexec.cpp:59-87"),
+        ("embed_interlaced", refpy.embed_doc(), dict(strategy="interlaced", devices=2, micro_batches=2, **tu),
+         952, 0.0, "acceptance.cpp:405-452 (criterion 9 interlaced, seed 950+K)"),
+        ("embed_shard2", refpy.embed_doc(batch=8, vocab=8, hidden=4),
+         dict(strategy="manual", devices=2, target_ops="emb@e,fw0@s0,fw1@s0", **tu), 31, 0.0,
+         "vocabulary-sharded embedding (shard_embed_algo, transform.cpp:~330)"),
+        ("coshard4_recompute", refpy.coshard_doc(),
+         dict(strategy="coshard", devices=1, shards=4, target_ops="op1,op2", **tu), 7007, 0.0,
+         "acceptance.cpp:324-350 (criterion 7, co-shard + recompute)"),
+        ("three_pass_3f1b", refpy.three_pass_doc(), dict(strategy="3f1b", devices=2, stages=2, micro_batches=2, **tu),
+         902, 0.0, "acceptance.cpp:405-452 (criterion 9 3F1B, seed 900+K)"),
+        ("mlp_1f1b_dp2", refpy.mlp_doc(layers=2, batch=8, hidden=4),
+         dict(strategy="1f1b", devices=4, stages=2, micro_batches=2, inner_dp=2, **tu), 41, 0.0,
+         "test_strategies.cpp (1F1B + inner DP; naive gradient sync)"),
+        ("mlp_gpipe", refpy.mlp_doc(layers=4, batch=8, hidden=4),
+         dict(strategy="gpipe", devices=2, stages=2, micro_batches=4, **tu), 19, 0.0,
+         "test_strategies.cpp (GPipe)"),
+        # Adapter coverage on 4 devices (SURVEY §8c probe-verified primitives).
+        ("adapt_v_to_r4", chain2(8, 8, 8), dict(strategy="manual", devices=4, target_ops="mm1@v,mm2@r"), 101, 0.0,
+         "V->R all-reduce"),
+        ("adapt_v_to_d4", chain2(8, 8, 8), dict(strategy="manual", devices=4, target_ops="mm1@v,mm2@s0"), 102, 0.0,
+         "V->D reduce-scatter"),
+        ("adapt_d_to_r4", chain2(8, 8, 8), dict(strategy="manual", devices=4, target_ops="mm1@s0,mm2@r"), 103, 0.0,
+         "D->R all-gather"),
+        ("adapt_d1_to_d0_4", chain2(8, 8, 8), dict(strategy="manual", devices=4, target_ops="mm1@s1,mm2@s0"), 104,
+         0.0, "D(1,k)->D(k,1) all-to-all"),
+        ("adapt_r_to_d4", chain2(8, 8, 8), dict(strategy="manual", devices=4, target_ops="mm1@r,mm2@s0"), 105, 0.0,
+         "R->D local split"),
+        ("adapt_v_to_d8", chain2(16, 16, 16), dict(strategy="manual", devices=8, target_ops="mm1@v,mm2@s0"), 106,
+         0.0, "V->D on 8 devices"),
+        ("adapt_vv_gap", chain2(256, 256, 8), dict(strategy="manual", devices=4, target_ops="mm1@v,mm2@s1"), 107,
+         0.0, "large V(4)->D plan: Dijkstra may pick multi-step V->V (SURVEY fact 6)"),
+        ("cross_group_copy", chain2(8, 8, 8),
+         dict(strategy="manual", devices=4, target_ops="mm1@s0@0@2,mm2@s0@2@2", testutil_cluster=1,
+              group_size=2), 108, 0.0, "disjoint device groups: group-copy (rvd.cpp:328-382)"),
+        ("cross_group_scatter", chain2(8, 8, 8),
+         dict(strategy="manual", devices=4, target_ops="mm1@r@0@1,mm2@s0@2@2", testutil_cluster=1,
+              group_size=2), 109, 0.0, "disjoint device groups: rd-scatter (rvd.cpp:418-463)"),
+        ("cross_group_rs", chain2(8, 8, 8),
+         dict(strategy="manual", devices=4, target_ops="mm1@v@0@2,mm2@s0@2@2", testutil_cluster=1,
+              group_size=2), 110, 0.0, "disjoint device groups: value -> dim across groups"),
+        # bf16 (elem_size 2) variants: rounding to bf16 -> stated tolerance.
+        ("mlp_dp2_bf16", refpy.with_elem_size(mlp, 2), dict(strategy="data_parallel", devices=2, **tu), 5, 2e-2,
+         "bf16 DP"),
+        ("tp_value_split_bf16", refpy.with_elem_size(TP_TEST_DOC, 2),
+         dict(strategy="manual", devices=2, target_ops="mm1@v,mm2@s0", **tu), 9, 2e-2, "bf16 TP"),
+    ]
+    for k in (1, 2, 4):
+        out.append((f"gpt_block_tp{k}", docs.dumps(docs.gpt_block_doc(16, 16, elem_size=4, train=True)),
+                    dict(strategy="megatron_tp", devices=k), 60 + k, 0.0, "C2 Megatron TP block (train), fp32"))
+    out.append(("gpt_block_tp2_bf16", docs.dumps(docs.gpt_block_doc(16, 16, elem_size=2, train=True)),
+                dict(strategy="megatron_tp", devices=2), 70, 2e-2, "C2 Megatron TP block (train), bf16"))
+    out.append(("gpt_block_fwd_tp2_mma", docs.dumps(docs.gpt_block_doc(256, 128, elem_size=2, train=False)),
+                dict(strategy="megatron_tp", devices=2), 71, 2e-2,
+                "C2 forward at tensor-core-eligible shapes (bf16)"))
+    return out
+
+
+def main():
+    index = []
+    for name, doc, spec, seed, tol, prov in cases():
+        d = os.path.join(HERE, name)
+        os.makedirs(d, exist_ok=True)
+        plan = refpy.compile_plan(doc, **spec)
+        inputs = refpy.random_integer_inputs(doc, seed)
+        expected = refpy.run_reference(doc, inputs)
+        arrays = {f"in_{k}": v for k, v in inputs.items()}
+        arrays.update({f"exp_{k}": v for k, v in expected.items()})
+        ref_status = "ok"
+        try:
+            ref_out, _ = refpy.run_plan(plan, inputs)
+            ok, msg = refpy.compare_outputs(expected, ref_out, tol)
+            ref_status = "ok" if ok else "mismatch: " + msg
+            arrays.update({f"ref_{k}": v for k, v in ref_out.items()})
+        except refpy.RefError as e:
+            ref_status = "throws: " + str(e)
+        with open(os.path.join(d, "graph.json"), "w") as f:
+            f.write(doc)
+        with open(os.path.join(d, "plan.json"), "w") as f:
+            f.write(plan)
+        np.savez_compressed(os.path.join(d, "io.npz"), **arrays)
+        pj = json.loads(plan)
+        meta = dict(name=name, seed=seed, rel_tol=tol, provenance=prov, spec=spec,
+                    reference_run_plan=ref_status, lanes=len(pj["lanes"]),
+                    tasks=sum(len(l["tasks"]) for l in pj["lanes"]),
+                    collectives=sorted({g["primitive"] for g in pj["coll_groups"]}),
+                    op_kinds=sorted({o["kind"] for o in pj["ops"]}))
+        with open(os.path.join(d, "meta.json"), "w") as f:
+            json.dump(meta, f, indent=1)
+        index.append(name)
+        print(f"{name:24s} lanes={meta['lanes']} tasks={meta['tasks']:4d} ref={ref_status[:60]} "
+              f"coll={meta['collectives']} kinds={meta['op_kinds']}")
+    with open(os.path.join(HERE, "index.json"), "w") as f:
+        json.dump(index, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

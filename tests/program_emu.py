@@ -1,0 +1,95 @@
+"""TEST INFRASTRUCTURE — numpy interpreter of the executor's lowered program.
+
+Runs the JSON from ``planc_b200.describe(plan)`` (buffers, instructions, box
+cells, issue order) on the CPU in float64 so the host-side lowering — feeds,
+placement, cell decomposition of every adapter, issue order, output
+reassembly table — is checked against the reference oracle without a GPU.
+It is a checker for tests only; the product never executes on the CPU.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def _strided_view(flat, offset, strides, extents):
+    idx = np.full(tuple(extents), offset, dtype=np.int64)
+    for d, (s, e) in enumerate(zip(strides, extents)):
+        shape = [1] * len(extents)
+        shape[d] = e
+        idx = idx + (np.arange(e, dtype=np.int64) * s).reshape(shape)
+    return idx
+
+
+def run_program(desc: dict, plan: dict, inputs: dict) -> dict:
+    bufs = {b["id"]: b for b in desc["buffers"]}
+    data = {}
+    for b in desc["buffers"]:
+        n = 1
+        for lo, hi in b["region"]:
+            n *= hi - lo
+        data[b["id"]] = np.zeros(n)
+        if b["graph_input"]:
+            x = np.asarray(inputs[b["pt"]], dtype=np.float64)
+            sl = tuple(slice(lo, hi) for lo, hi in b["region"])
+            data[b["id"]] = x[sl].reshape(-1).copy()
+    shape = {b["id"]: [hi - lo for lo, hi in b["region"]] for b in desc["buffers"]}
+    for iid in desc["issue_order"]:
+        ins = desc["instrs"][iid]
+        k = ins["kind"]
+        if k == "gemm":
+            a = data[ins["in"][0]].reshape(shape[ins["in"][0]])
+            b = data[ins["in"][1]].reshape(shape[ins["in"][1]])
+            a = a.T if ins["ta"] else a
+            b = b.T if ins["tb"] else b
+            data[ins["out"][0]] = (a @ b).reshape(-1)
+        elif k == "ew":
+            out = data[ins["in"][0]].copy()
+            for x in ins["in"][1:]:
+                out = (out + data[x], out * data[x], np.maximum(out, data[x]))[ins["ew"]]
+            data[ins["out"][0]] = out
+        elif k == "reduce":
+            x = data[ins["in"][0]].reshape(ins["outer"], ins["axis_len"], ins["inner"])
+            data[ins["out"][0]] = x.sum(axis=1).reshape(-1)
+        elif k == "emb_lookup":
+            idx = data[ins["in"][0]].astype(np.int64)
+            tab = data[ins["in"][1]].reshape(ins["rows"], ins["h"])
+            out = np.zeros((ins["n_idx"], ins["h"]))
+            ok = (idx >= ins["lo"]) & (idx < ins["lo"] + ins["rows"])
+            out[ok] = tab[idx[ok] - ins["lo"]]
+            data[ins["out"][0]] = out.reshape(-1)
+        elif k == "emb_grad":
+            idx = data[ins["in"][0]].astype(np.int64)
+            g = data[ins["in"][1]].reshape(ins["n_idx"], ins["h"])
+            out = np.zeros((ins["rows"], ins["h"]))
+            for j in range(ins["n_idx"]):
+                if ins["lo"] <= idx[j] < ins["lo"] + ins["rows"]:
+                    out[idx[j] - ins["lo"]] += g[j]
+            data[ins["out"][0]] = out.reshape(-1)
+        elif k == "box":
+            ob = ins["out"][0]
+            out = np.zeros_like(data[ob])
+            for c in ins["cells"]:
+                di = _strided_view(out, c["dst_off"], c["dst_str"], c["ext"])
+                v = np.zeros(di.shape)
+                for t in c["terms"]:
+                    si = _strided_view(data[t["buf"]], t["off"], t["str"], c["ext"])
+                    v = v + data[t["buf"]][si] if t["add"] else data[t["buf"]][si].copy()
+                out[di] = v
+            data[ob] = out
+    outputs = {}
+    for pt, blist in desc["outputs"]:
+        full_shape = next(p["shape"] for p in plan["ptensors"] if p["id"] == pt)
+        res = np.zeros(full_shape)
+        # Pieces: same copy/add rule as reconstruct, in order.
+        acc_set = np.zeros(full_shape, dtype=bool)
+        for b in blist:
+            bd = bufs[b]
+            sl = tuple(slice(lo, hi) for lo, hi in bd["region"])
+            piece = data[b].reshape(shape[b])
+            if bd["value"][1] == 1:
+                res[sl] = piece
+            else:
+                res[sl] = res[sl] + piece
+            acc_set[sl] = True
+        outputs[pt] = res
+    return outputs

@@ -1,0 +1,187 @@
+"""Host-side lowering and the C-ABI library, on CPU (no compute calls).
+
+The executor compiles a plan into buffers + instructions + box cell
+programs + issue order without touching CUDA (planc_b200_describe). A numpy
+interpreter of that program (tests/program_emu.py, test-only) must reproduce
+the reference outputs for every golden plan; error behaviour must match the
+reference's exception classes.
+"""
+import ctypes
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import golden_cases
+import paper_2301_08984_b200 as pb
+from oracle import planc_oracle as po
+from program_emu import run_program
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "planc_b200.h")).read()
+    declared = set(re.findall(r"\b(planc_b200_[a-z0-9_]+)\s*\(", header))
+    assert len(declared) >= 15
+    lib = ctypes.CDLL(pb.library_path())
+    for sym in sorted(declared):
+        assert hasattr(lib, sym), sym
+    assert "sm_100a" in pb.version()
+
+
+@pytest.mark.parametrize("name", golden_cases.names())
+def test_lowered_program_reproduces_reference(name):
+    g = golden_cases.load(name)
+    desc = pb.describe(g["plan"])
+    out = run_program(desc, json.loads(g["plan"]), g["inputs"])
+    ok, msg = po.compare_outputs(g["expected"], out, 0.0)
+    assert ok, msg
+
+
+@pytest.mark.parametrize("name", golden_cases.names())
+def test_lowering_invariants(name):
+    g = golden_cases.load(name)
+    desc = pb.describe(g["plan"])
+    writers = {}
+    for ins in desc["instrs"]:
+        for b in ins["out"]:
+            assert b not in writers, "every buffer is written exactly once per step"
+            writers[b] = ins["id"]
+        for d in ins["deps"]:
+            assert d < ins["id"], "dependencies point backwards in issue order"
+    assert desc["issue_order"] == sorted(desc["issue_order"])
+    for b in desc["buffers"]:
+        assert b["offset"] % 256 == 0
+        if not b["graph_input"]:
+            assert b["id"] in writers
+    # Every box cell is in bounds of its source and destination buffers.
+    size = {b["id"]: b["bytes"] // (2 if b["dtype"] == "bf16" else 4) for b in desc["buffers"]}
+    for ins in desc["instrs"]:
+        for c in ins["cells"]:
+            hi = c["dst_off"] + sum((e - 1) * s for e, s in zip(c["ext"], c["dst_str"]))
+            assert 0 <= c["dst_off"] and hi < size[ins["out"][0]]
+            for t in c["terms"]:
+                thi = t["off"] + sum((e - 1) * s for e, s in zip(c["ext"], t["str"]))
+                assert 0 <= t["off"] and thi < size[t["buf"]]
+
+
+def test_collectives_become_single_fused_box_per_member():
+    g = golden_cases.load("adapt_v_to_d4")
+    desc = pb.describe(g["plan"])
+    coll = [i for i in desc["instrs"] if ":" in i["label"]]
+    assert len(coll) == 4
+    for i in coll:
+        assert i["kind"] == "box" and i["stream"] == 1
+        # reduce-scatter: each member's slice sums the 4 partial pieces
+        assert all(len(c["terms"]) == 4 and all(t["add"] for t in c["terms"]) for c in i["cells"])
+        assert len({b for b in i["in"]}) == 4
+
+
+def test_allgather_cells_copy_each_slice():
+    g = golden_cases.load("adapt_d_to_r4")
+    desc = pb.describe(g["plan"])
+    coll = [i for i in desc["instrs"] if i["label"].startswith("all-gather")]
+    assert coll
+    for i in coll:
+        assert len(i["cells"]) == 4
+        assert all(len(c["terms"]) == 1 and not c["terms"][0]["add"] for c in i["cells"])
+
+
+def test_strict_value_mode_matches_reference_rule():
+    # With the reference rule the V(4)->V(2) extension is off; golden plans
+    # never need it, so both modes lower identically.
+    g = golden_cases.load("mlp_dp2")
+    a = pb.describe(g["plan"])
+    b = pb.describe(g["plan"], strict_value=True)
+    assert a["instrs"] == b["instrs"]
+
+
+def test_malformed_plan_is_schema_error():
+    with pytest.raises(pb.SchemaError):
+        pb.describe("{not json")
+    with pytest.raises(pb.SchemaError):
+        pb.describe(json.dumps({"ptensors": []}))
+    plan = json.loads(golden_cases.load("mlp_dp2")["plan"])
+    plan["ops"][0]["kind"] = "softmax"
+    with pytest.raises(pb.SchemaError):
+        pb.describe(json.dumps(plan))
+
+
+def test_missing_feed_is_internal_error():
+    plan = json.loads(golden_cases.load("mlp_dp2")["plan"])
+    plan["feeds"] = plan["feeds"][1:]
+    with pytest.raises(pb.InternalError, match="no feed"):
+        pb.describe(json.dumps(plan))
+
+
+def test_crossed_recvs_deadlock_like_run_plan():
+    # test_simulate.cpp:188-221 style negative control: swap the order of a
+    # lane's recvs against its peer's sends -> pairing deadlock.
+    g = golden_cases.load("mlp_dp2_naive")
+    plan = json.loads(g["plan"])
+    # make lane 0 wait for a channel that lane 1 only sends after waiting on lane 0
+    recvs = {}
+    for lane in plan["lanes"]:
+        for t in lane["tasks"]:
+            if t["kind"] == "recv":
+                recvs.setdefault(lane["device"], []).append(t)
+    lane0 = plan["lanes"][0]["tasks"]
+    lane1 = plan["lanes"][1]["tasks"]
+    first_recv0 = next(i for i, t in enumerate(lane0) if t["kind"] == "recv")
+    first_recv1 = next(i for i, t in enumerate(lane1) if t["kind"] == "recv")
+    lane0.insert(0, lane0.pop(first_recv0))
+    lane1.insert(0, lane1.pop(first_recv1))
+    with pytest.raises(pb.InternalError, match="deadlock"):
+        pb.describe(json.dumps(plan))
+    with pytest.raises(po.InternalError, match="deadlock"):
+        po.run_plan(json.dumps(plan), g["inputs"])
+
+
+def test_corrupted_channels_are_detected():
+    # test_refexec.cpp:142-181: swap two same-shaped value-part sends.
+    g = golden_cases.load("mlp_dp2_naive")
+    plan = json.loads(g["plan"])
+    vts = {v["id"]: v for v in plan["vtensors"]}
+    sends = [o for o in plan["ops"] if o["kind"] == "send" and vts[o["inputs"][0]]["value"][1] > 1]
+    assert len(sends) >= 2
+    s0, s1 = sends[0], sends[1]
+    s0["channel"], s1["channel"] = s1["channel"], s0["channel"]
+    for lane in plan["lanes"]:
+        for t in lane["tasks"]:
+            if t["op"] == s0["id"]:
+                t["channel"] = s0["channel"]
+            if t["op"] == s1["id"]:
+                t["channel"] = s1["channel"]
+    text = json.dumps(plan)
+    try:
+        out = run_program(pb.describe(text), plan, g["inputs"])
+        assert not po.compare_outputs(g["expected"], out)[0]
+    except pb.PlancError:
+        pass
+
+
+def test_unsupported_elem_size_is_usage_error():
+    plan = json.loads(golden_cases.load("mlp_dp2")["plan"])
+    plan["ptensors"][0]["elem_size"] = 8
+    with pytest.raises(pb.UsageError):
+        pb.describe(json.dumps(plan))
+
+
+def test_partial_value_graph_input_is_usage_error():
+    plan = json.loads(golden_cases.load("reduce_sum")["plan"])
+    for v in plan["vtensors"]:
+        if v["ptensor"] == 0:
+            v["value"] = [0, 2]
+    with pytest.raises(pb.UsageError, match="partial value"):
+        pb.describe(json.dumps(plan))
+
+
+def test_accounting_matches_masks():
+    g = golden_cases.load("gpt_block_tp2")
+    desc = pb.describe(g["plan"])
+    flops = sum(i["flops"] for i in desc["instrs"] if i["kind"] == "gemm")
+    T, H = 16, 16
+    assert flops == pytest.approx(3 * 22 * T * H * H)  # fwd + 2x bwd GEMMs of the block
