@@ -1,0 +1,296 @@
+#!/usr/bin/env python3
+"""Plan-step benchmark of the B200 SuperScaler plan executor.
+
+Metric (BASELINE.json): plan-step samples/sec at 1/2/4/8 B200 (% roofline),
+adapter bus GB/s vs NVLink. A step is one execution of every lane's tasks of
+a plan emitted by the reference front end (plans/*.plan.json); samples are
+rows of the graph's batch dimension (tokens for C2).
+
+Default workload (configs[1]): GPT-3-style transformer block,
+Megatron tensor-parallel plan, train step (forward + backward + optimizer),
+T=8192 tokens, H=2048, FFN=4H, bf16; TP degree = number of GPUs.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1l]
+  python bench.py --impl reference ...   # the reference's CPU run_plan
+
+Multi-GPU: under torchrun every rank joins the barriers and the timing
+reduction; rank 0 drives all N GPUs of the box (plan lanes -> devices
+0..N-1, fused box kernels over NVLink peer memory). Prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PLANS = os.path.join(ROOT, "plans")
+
+
+def plan_name(config: str, n: int) -> str:
+    return {"c2": f"c2_tp{n}", "c1l": f"c1l_dp{n}"}[config]
+
+
+def load_plan(name):
+    with open(os.path.join(PLANS, name + ".plan.json")) as f:
+        plan = f.read()
+    with open(os.path.join(PLANS, name + ".meta.json")) as f:
+        meta = json.load(f)
+    return plan, meta
+
+
+def synthetic_inputs(plan_json: str, seed: int = 0) -> dict:
+    """Integer-valued inputs in {-1, 0, 1} for every graph-input pTensor."""
+    p = json.loads(plan_json)
+    produced = set()
+    vts = {v["id"]: v for v in p["vtensors"]}
+    for o in p["ops"]:
+        for v in o["outputs"]:
+            produced.add(vts[v]["ptensor"])
+    rng = np.random.default_rng(seed)
+    return {pt["id"]: rng.integers(-1, 2, size=pt["shape"]).astype(np.float64)
+            for pt in p["ptensors"] if pt["id"] not in produced}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                      "-i", ",".join(map(str, self.gpus))], capture_output=True, text=True,
+                                     timeout=5).stdout
+                for line in out.strip().splitlines():
+                    f = [x.strip() for x in line.split(",")]
+                    if len(f) >= 9:
+                        self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return dict(hbm=j["hbm_gbs"], bf16=j["bf16_tflops"], bf16_sus=j["bf16_tflops_sustained"], src="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+NVLINK_GBS = 900.0  # nominal per direction per GPU (measured peer copy 770)
+
+
+def cpu_baseline(config: str, budget_s: float = 20.0):
+    """The reference's own CPU executor (oracle/_ref run_plan, 1 thread) on the
+    reduced-shape plan of the same graph, bounded in time."""
+    from oracle import refpy  # checker / baseline only
+
+    name = plan_name(config, 1) + "_cpu"
+    plan, meta = load_plan(name)
+    inputs = synthetic_inputs(plan, 1)
+    _, secs = refpy.run_plan(plan, inputs, iters=1)
+    iters = max(1, min(50, int(budget_s / max(secs, 1e-6))))
+    _, secs = refpy.run_plan(plan, inputs, iters=iters)
+    sps = meta["samples_per_step"] / secs
+    shape = f"T={meta.get('tokens', meta.get('batch'))},H={meta['hidden']}"
+    return dict(value=sps, unit="samples/s", cores=1, kind="reference",
+                sample=f"{iters} x run_plan of {name} ({shape}, same graph at reduced shape; "
+                       f"{secs:.3f} s/step, single-threaded reference executor)"), secs
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    val, secs = cpu_baseline(args.config, budget_s=max(5.0, 60.0 / max(args.steps + args.warmup, 1)))
+    name = plan_name(args.config, 1)
+    _, meta = load_plan(name)
+    line = {"metric": "plan step samples/sec", "value": val["value"], "unit": "samples/s", "impl": "reference",
+            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": name + "_cpu", "config": args.config},
+            "cpu_baseline": val, "e2e": {"value": val["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
+                                         "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=["c2", "c1l"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    n = args.gpus
+    name = plan_name(args.config, n)
+    plan, meta = load_plan(name)
+    result = None
+    if rank == 0:
+        import paper_2301_08984_b200 as pb
+
+        peaks = measured_peaks()
+        inputs = synthetic_inputs(plan)
+        ex = pb.Executor(plan, lane_gpus=list(range(n)))
+        ex.set_inputs(inputs)
+        ex.run(args.warmup)  # warm-up (graph capture + W steps)
+        st = ex.stats()
+    if dist:
+        dist.barrier()
+    if rank == 0:
+        with ClockSampler(list(range(n))) as clk:
+            ms = ex.run(args.steps)
+        clocks = clk.summary()
+        e2e_ms, h2d, d2h = ex.run_e2e(args.steps)
+        prof = [ex.profile() for _ in range(3)]
+        ex.close()
+        sps = meta["samples_per_step"] / (ms / 1e3)
+        # Dominant kernel (largest share of the serialised step) and its roofline.
+        fam = {}
+        for pr in prof:
+            for p in pr:
+                f = fam.setdefault(p["kind"], dict(ms=0.0, launches=0, flops=0.0, bytes=0.0, wire=0.0))
+                f["ms"] += p["ms"] / len(prof)
+                f["launches"] += p["launches"] / len(prof)
+                f["flops"] += p["flops"] / len(prof)
+                f["bytes"] += p["bytes"] / len(prof)
+                f["wire"] += p["wire_bytes"] / len(prof)
+        total_prof = sum(f["ms"] for f in fam.values())
+        top = max(fam, key=lambda k: fam[k]["ms"])
+        t = fam[top]
+        if top.startswith("gemm"):
+            achieved = t["flops"] / (t["ms"] / 1e3) / 1e12
+            roof = {"kernel": top, "bound": "tensor", "achieved": achieved, "peak": peaks["bf16"],
+                    "unit": "TFLOP/s", "frac": achieved / peaks["bf16"], "traffic": None,
+                    "peak_source": peaks["src"] + " burst (kernels timed individually)",
+                    "share_of_step": t["ms"] / total_prof,
+                    "per_launch": {"flops": t["flops"] / max(t["launches"], 1),
+                                   "ms": t["ms"] / max(t["launches"], 1)}}
+        else:
+            achieved = t["bytes"] / (t["ms"] / 1e3) / 1e9
+            roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
+                    "frac": achieved / peaks["hbm"], "traffic": None, "peak_source": peaks["src"],
+                    "share_of_step": t["ms"] / total_prof}
+        # Plan-level roofline: max over lanes of
+        # F/P + M/HBM vs W/NVLink, against the measured sustained peaks.
+        t_roof = max(st["max_lane_gemm_flops"] / (peaks["bf16_sus"] * 1e12)
+                     + st["max_lane_hbm_bytes"] / (peaks["hbm"] * 1e9),
+                     st["max_lane_wire_bytes"] / (NVLINK_GBS * 1e9))
+        families = {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
+                        "tflops" if k.startswith("gemm") else "gbs":
+                            round((v["flops"] / 1e12 if k.startswith("gemm") else v["bytes"] / 1e9)
+                                  / max(v["ms"] / 1e3, 1e-12), 2)} for k, v in fam.items()}
+        coll = fam.get("box_collective")
+        result = {
+            "metric": "plan step samples/sec", "value": sps, "unit": "samples/s", "n_gpus": n,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (integer-valued inputs in {-1,0,1})",
+            "config": {"workload": name, "config": args.config, "plan": f"plans/{name}.plan.json",
+                       "shape": {k: meta[k] for k in ("tokens", "batch", "hidden") if k in meta},
+                       "parallelism": (f"tp{n}" if args.config == "c2" else f"dp{n}"),
+                       "sample": meta["sample"], "l2": "step working set " +
+                       f"{st['device_bytes'] / 2**30:.1f} GiB > 126 MB L2 (no flush needed)",
+                       "lanes": st["num_lanes"], "tasks": st["num_tasks"], "launch": (
+                           "CUDA graph" if st["graph_captured"] else "eager")},
+            "roofline": roof,
+            "plan_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
+                              "gemm_tflop_per_step": st["flops"] / 1e12, "hbm_gb_per_step": st["hbm_bytes"] / 1e9,
+                              "wire_gb_per_step": st["wire_bytes"] / 1e9,
+                              "peaks": {"bf16_tflops": peaks["bf16_sus"], "hbm_gbs": peaks["hbm"],
+                                        "nvlink_gbs": NVLINK_GBS, "source": peaks["src"] + " (sustained bf16)"}},
+            "adapter_bus_gbs": (None if not coll or coll["wire"] == 0 else
+                                {"value": coll["wire"] / (coll["ms"] / 1e3) / 1e9, "vs_nvlink_gbs": NVLINK_GBS}),
+            "kernel_families": families,
+            "e2e": {"value": meta["samples_per_step"] / (e2e_ms / 1e3), "unit": "samples/s",
+                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "via": "planc_b200_run_e2e (C ABI): pinned H2D of step inputs, graph step, D2H of results"},
+            "gpu_launches": st["kernels_per_step"] * args.steps,
+            "gemm_tc_launches_per_step": st["gemm_tc_per_step"],
+            "clocks": clocks,
+        }
+        if not args.no_cpu_baseline and n == 1:
+            try:
+                cb, _ = cpu_baseline(args.config)
+                small, smeta = load_plan(plan_name(args.config, 1) + "_cpu")
+                with pb.Executor(small, lane_gpus=[0]) as sx:
+                    sx.set_inputs(synthetic_inputs(small, 1))
+                    sx.run(3)
+                    sms = sx.run(20)
+                cb["gpu_value_same_shape"] = smeta["samples_per_step"] / (sms / 1e3)
+                result["cpu_baseline"] = cb
+            except Exception as e:  # reference library not shipped
+                result["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
+    if dist:
+        import torch
+
+        t = torch.tensor([result["ms_per_step"] if result else 0.0], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if result:
+            result["ms_per_step"] = float(t.item())
+        dist.barrier()
+        dist.destroy_process_group()
+    if result:
+        print(json.dumps(result))
+
+
+if __name__ == "__main__":
+    main()

@@ -84,6 +84,10 @@ int planc_b200_ptensor_shape(planc_b200_exec* h, int ptensor, int64_t* shape, in
 /* Reassembled value of a produced pTensor as doubles (volume elements). */
 int planc_b200_get_output(planc_b200_exec* h, int ptensor, double* out, int64_t capacity);
 
+/* Debug / verification: the value of one device buffer (a vTensor piece,
+ * ids as in planc_b200_describe) as doubles. Returns its element count. */
+int64_t planc_b200_read_buffer(planc_b200_exec* h, int buffer, double* out, int64_t capacity);
+
 /* Graph-input pTensors the plan places (ascending id). */
 int planc_b200_num_inputs(planc_b200_exec* h);
 int planc_b200_input_ids(planc_b200_exec* h, int* ids, int cap);

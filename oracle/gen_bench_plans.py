@@ -1,0 +1,66 @@
+"""Generates the benchmark plans in plans/ with the UNMODIFIED reference
+front end (oracle/_ref: load_graph -> sProgram -> compile -> save_plan).
+
+Plans are the executor's INPUT (what the reference compiler emits); they are
+generated once here, where /root/reference exists, and committed — the GPU
+box has no reference. Shapes follow SURVEY.md §8d:
+
+  c2   GPT-3-style block (oracle/docs.py gpt_block_doc), train step,
+       T=8192 tokens (4 seq x 2048), H=2048, FFN=4H, bf16,
+       Megatron TP = 1/2/4/8 (megatron_tp sProgram)
+  c1l  2-layer MLP (reference mlp_doc) B=16384, H=4096, bf16, DP = 1/2/4/8
+  *_cpu  the same graphs at the reduced shape the CPU executor can run
+       (T=H=128; SURVEY §8d "CPU baseline")
+
+Run:  python oracle/gen_bench_plans.py
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, ROOT)
+
+from oracle import docs, refpy  # noqa: E402
+
+OUT = os.path.join(ROOT, "plans")
+
+
+def write(name, graph, plan, meta):
+    with open(os.path.join(OUT, name + ".plan.json"), "w") as f:
+        f.write(plan)
+    with open(os.path.join(OUT, name + ".graph.json"), "w") as f:
+        f.write(graph)
+    pj = json.loads(plan)
+    meta = dict(meta, lanes=len(pj["lanes"]), tasks=sum(len(l["tasks"]) for l in pj["lanes"]),
+                collectives=sorted({g["primitive"] for g in pj["coll_groups"]}))
+    with open(os.path.join(OUT, name + ".meta.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+    print(name, meta["lanes"], meta["tasks"], meta["collectives"])
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    for T, H, tag in ((8192, 2048, ""), (128, 128, "_cpu")):
+        g = docs.dumps(docs.gpt_block_doc(T, H, elem_size=2, train=True))
+        for k in (1, 2, 4, 8):
+            if tag and k > 1:
+                continue
+            plan = refpy.compile_plan(g, strategy="megatron_tp", devices=k)
+            write(f"c2_tp{k}{tag}", g, plan, dict(config="c2", tokens=T, hidden=H, tp=k, dtype="bf16",
+                                                  samples_per_step=T, sample="token (row of X)"))
+    for B, H, tag in ((16384, 4096, ""), (128, 128, "_cpu")):
+        g = refpy.with_elem_size(refpy.mlp_doc(layers=2, batch=B, hidden=H), 2)
+        for k in (1, 2, 4, 8):
+            if tag and k > 1:
+                continue
+            plan = refpy.compile_plan(g, strategy="data_parallel", devices=k)
+            write(f"c1l_dp{k}{tag}", g, plan, dict(config="c1l", batch=B, hidden=H, dp=k, dtype="bf16",
+                                                   samples_per_step=B, sample="row of the batch"))
+
+
+if __name__ == "__main__":
+    main()

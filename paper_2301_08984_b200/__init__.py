@@ -99,6 +99,8 @@ def _load():
     L.planc_b200_ptensor_shape.argtypes = [vp, c_int, P(c_i64), c_int, P(c_int)]
     L.planc_b200_get_output.argtypes = [vp, c_int, P(c_dbl), c_i64]
     L.planc_b200_get_stats.argtypes = [vp, P(_Stats)]
+    L.planc_b200_read_buffer.argtypes = [vp, c_int, P(c_dbl), c_i64]
+    L.planc_b200_read_buffer.restype = c_i64
     L.planc_b200_profile.argtypes = [vp, P(ctypes.c_char_p)]
     L.planc_b200_describe.argtypes = [ctypes.c_char_p, ctypes.c_uint32, P(vp)]
     L.planc_b200_free.argtypes = [vp]
@@ -198,6 +200,15 @@ class Executor:
                                              out.size))
         return out
 
+    def read_buffer(self, buffer: int) -> np.ndarray:
+        L = _load()
+        n = L.planc_b200_read_buffer(self._h, buffer, None, 0)
+        if n < 0:
+            _check(1)
+        out = np.empty(n, dtype=np.float64)
+        L.planc_b200_read_buffer(self._h, buffer, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n)
+        return out
+
     def outputs(self) -> dict:
         return {pid: self.get_output(pid) for pid in self.output_ids()}
 
@@ -233,14 +244,26 @@ def run_plan(plan_json: str, inputs: dict, lane_gpus=None, flags: int = 0) -> di
         return ex.outputs()
 
 
-def compare_outputs(expected: dict, actual: dict, rel_tol: float = 0.0):
-    """``planc::compare_outputs`` (refexec.cpp:604-631): |e-a| <= tol*max(1,|e|)."""
+def compare_outputs(expected: dict, actual: dict, rel_tol: float = 0.0, normwise: bool = False):
+    """``planc::compare_outputs`` (refexec.cpp:604-631): |e-a| <= tol*max(1,|e|).
+
+    ``normwise=True`` scales the tolerance by the tensor's magnitude instead,
+    |e-a| <= tol*max(1, max|e|) — the stated bf16 criterion: after a bf16
+    rounding of partial sums, elementwise relative error is unbounded where
+    the exact result cancels to near zero.
+    """
     for pid in sorted(expected):
         e = np.asarray(expected[pid], dtype=np.float64)
         if pid not in actual or tuple(np.shape(actual[pid])) != e.shape:
             return False, f"mismatch on tensor {pid} (missing or shape)"
         a = np.asarray(actual[pid], dtype=np.float64)
-        bad = (e != a) if rel_tol == 0.0 else (np.abs(e - a) > rel_tol * np.maximum(1.0, np.abs(e)))
+        if rel_tol == 0.0:
+            bad = e != a
+        elif normwise:
+            scale = max(1.0, float(np.abs(e).max())) if e.size else 1.0
+            bad = np.abs(e - a) > rel_tol * scale
+        else:
+            bad = np.abs(e - a) > rel_tol * np.maximum(1.0, np.abs(e))
         if bad.any():
             idx = np.unravel_index(int(np.argmax(bad)), e.shape)
             return False, (f"mismatch on tensor {pid} at {list(map(int, idx))}: "

@@ -1,5 +1,6 @@
 // extern "C" boundary (include/planc_b200.h): exceptions become return
 // codes, mirroring the reference's error classes (util.hpp:17-29).
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
@@ -148,6 +149,17 @@ int planc_b200_get_output(planc_b200_exec* h, int ptensor, double* out, int64_t 
     if (static_cast<std::int64_t>(t.data.size()) > capacity) throw UsageError("output buffer too small");
     std::memcpy(out, t.data.data(), t.data.size() * sizeof(double));
   });
+}
+
+int64_t planc_b200_read_buffer(planc_b200_exec* h, int buffer, double* out, int64_t capacity) {
+  std::int64_t n = -1;
+  int rc = guarded([&] {
+    if (!h) throw UsageError("null handle");
+    auto v = h->ex->read_buffer(buffer);
+    n = static_cast<std::int64_t>(v.size());
+    if (out) std::memcpy(out, v.data(), sizeof(double) * std::min<std::int64_t>(n, capacity));
+  });
+  return rc == PLANC_B200_OK ? n : -1;
 }
 
 int planc_b200_get_stats(planc_b200_exec* h, planc_b200_stats* s) {

@@ -1,7 +1,362 @@
-// tcgen05 GEMM — placeholder until the tensor-core path lands.
+// tcgen05 / TMEM / TMA GEMM for the plan's matmul sub-operators (sm_100a).
+//
+// C[m,n] = op(A)[m,k] · op(B)[k,n] with bf16 operands, fp32 accumulation in
+// tensor memory, bf16 or fp32 output — the reference's matmul_eval
+// (proj/src/refexec.cpp:142-168) including transpose_a / transpose_b, which
+// are not materialised: a transposed operand is simply loaded MN-major and the
+// UMMA instruction descriptor's major bits say so.
+//
+// Structure (one 128x256 output tile per CTA, 6 warps):
+//   warp 0      TMA producer: 4-stage smem ring (A 16 KB + B 32 KB per stage,
+//               128B-swizzled), mbarrier full/empty pipeline
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (kind::f16, M=128, N=256, K=16 per instruction), commits
+//               free smem stages and finally the accumulator
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 TMEM -> registers, convert,
+//               16-byte global stores
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
 #include "kernels.cuh"
 
 namespace planc_b200 {
-bool gemm_sm100_eligible(const GemmArgs&) { return false; }
-void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) { launch_gemm_simt(a, s); }
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;  // 128 bytes of bf16: one 128B swizzle row
+constexpr int STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
+constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int NUM_THREADS = 192;
+constexpr int TMEM_COLS = 256;
+
+// ---- PTX wrappers ------------------------------------------------------------
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
+  std::uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra.uni DONE;\n"
+      "bra.uni LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, std::uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(std::uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_mma(std::uint32_t tmem_d, std::uint64_t adesc, std::uint64_t bdesc,
+                                       std::uint32_t idesc, std::uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// Shared-memory matrix descriptor (tcgen05 "version 1"), SWIZZLE_128B.
+__device__ __forceinline__ std::uint64_t smem_desc(std::uint32_t addr, std::uint32_t lbo, std::uint32_t sbo) {
+  std::uint64_t d = 0;
+  d |= static_cast<std::uint64_t>((addr >> 4) & 0x3FFFu);
+  d |= static_cast<std::uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<std::uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;  // version
+  d |= 2ull << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::f16, A/B bf16, D f32, M=128, N=256.
+__host__ __device__ constexpr std::uint32_t make_idesc(bool a_mn, bool b_mn) {
+  return (1u << 4)                              // D format f32
+         | (1u << 7)                            // A bf16
+         | (1u << 10)                           // B bf16
+         | ((a_mn ? 1u : 0u) << 15)             // A major
+         | ((b_mn ? 1u : 0u) << 16)             // B major
+         | (static_cast<std::uint32_t>(BN >> 3) << 17)  // N
+         | (static_cast<std::uint32_t>(BM >> 4) << 24); // M
+}
+
+__device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---- kernel --------------------------------------------------------------------
+
+template <bool A_MN, bool B_MN, bool C_BF16>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* __restrict__ C,
+                   int m, int n, int k) {
+  extern __shared__ std::uint8_t smem_raw[];
+  std::uint8_t* smem =
+      reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  std::uint8_t* sA = smem;
+  std::uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sB + STAGES * B_STAGE_BYTES);
+  std::uint64_t* empty = full + STAGES;
+  std::uint64_t* tmem_full = empty + STAGES;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int m0 = blockIdx.y * BM;
+  const int n0 = blockIdx.x * BN;
+  const int num_k = (k + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < num_k; ++kb) {
+        const int s = kb % STAGES;
+        const std::uint32_t phase = (kb / STAGES) & 1;
+        mbar_wait(&empty[s], phase ^ 1);
+        mbar_expect_tx(&full[s], A_STAGE_BYTES + B_STAGE_BYTES);
+        std::uint8_t* a = sA + s * A_STAGE_BYTES;
+        std::uint8_t* b = sB + s * B_STAGE_BYTES;
+        if (A_MN) {
+#pragma unroll
+          for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * (64 * BK * 2), &tmA, m0 + 64 * j, kb * BK, &full[s]);
+        } else {
+          tma_load_2d(a, &tmA, kb * BK, m0, &full[s]);
+        }
+        if (B_MN) {
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * (64 * BK * 2), &tmB, n0 + 64 * j, kb * BK, &full[s]);
+        } else {
+          tma_load_2d(b, &tmB, kb * BK, n0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr std::uint32_t idesc = make_idesc(A_MN, B_MN);
+      for (int kb = 0; kb < num_k; ++kb) {
+        const int s = kb % STAGES;
+        const std::uint32_t phase = (kb / STAGES) & 1;
+        mbar_wait(&full[s], phase);
+        tc_fence_after();
+        const std::uint32_t a_base = smem_u32(sA + s * A_STAGE_BYTES);
+        const std::uint32_t b_base = smem_u32(sB + s * B_STAGE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          // K-major: 16 elements = 32 bytes along the swizzled row; rows of
+          // 128 B, 8-row groups 1024 B apart (SBO). MN-major: 16 K-rows =
+          // 2048 B; 64-element MN blocks 8 KB apart (LBO), 8-row K groups
+          // 1024 B apart (SBO).
+          std::uint64_t ad = A_MN ? smem_desc(a_base + kk * 2048, 64 * BK * 2, 1024)
+                                  : smem_desc(a_base + kk * 32, 16, 1024);
+          std::uint64_t bd = B_MN ? smem_desc(b_base + kk * 2048, 64 * BK * 2, 1024)
+                                  : smem_desc(b_base + kk * 32, 16, 1024);
+          tc_mma(tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+        }
+        tc_commit(&empty[s]);
+      }
+      tc_commit(tmem_full);
+    }
+  } else {
+    // Epilogue warps 2..5: warp w may only touch TMEM lanes 32*(w%4)..+31.
+    const int q = warp % 4;
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int row = m0 + q * 32 + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      std::uint32_t r[32];
+      tmem_ld32(tmem + (static_cast<std::uint32_t>(q * 32) << 16) + c * 32, r);
+      const int col0 = n0 + c * 32;
+      if (row >= m || col0 >= n) continue;
+      if (C_BF16) {
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(C) + static_cast<std::int64_t>(row) * n + col0;
+        if (col0 + 32 <= n) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 pk;
+            std::uint32_t* w = reinterpret_cast<std::uint32_t*>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]),
+                                                       __uint_as_float(r[v * 8 + 2 * e + 1]));
+              w[e] = *reinterpret_cast<std::uint32_t*>(&h);
+            }
+            *reinterpret_cast<uint4*>(out + v * 8) = pk;
+          }
+        } else {
+          for (int e = 0; e < 32 && col0 + e < n; ++e) out[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+        }
+      } else {
+        float* out = static_cast<float*>(C) + static_cast<std::int64_t>(row) * n + col0;
+        if (col0 + 32 <= n) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            float4 f = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+            *reinterpret_cast<float4*>(out + 4 * v) = f;
+          }
+        } else {
+          for (int e = 0; e < 32 && col0 + e < n; ++e) out[e] = __uint_as_float(r[e]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+  }
+}
+
+// ---- host ---------------------------------------------------------------------
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+  });
+  if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// bf16 row-major [rows][cols] matrix, box {64 cols, box_rows}, 128B swizzle.
+CUtensorMap make_map(const void* base, std::int64_t rows, std::int64_t cols, int box_rows) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+template <bool A_MN, bool B_MN, bool C_BF16>
+void launch_typed(const GemmArgs& a, cudaStream_t s) {
+  static unsigned attr_set_mask = 0;  // per device ordinal
+  auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_set_mask & (1u << dev))) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc smem attribute: ") + cudaGetErrorString(e));
+    attr_set_mask |= 1u << dev;
+  }
+  // A: [m][k] (K-major) or, transposed, [k][m] (MN-major); B: [k][n]
+  // (MN-major) or, transposed, [n][k] (K-major).
+  CUtensorMap ma = A_MN ? make_map(a.A, a.k, a.m, BK) : make_map(a.A, a.m, a.k, BM);
+  CUtensorMap mb = B_MN ? make_map(a.B, a.k, a.n, BK) : make_map(a.B, a.n, a.k, BN);
+  dim3 grid(static_cast<unsigned>((a.n + BN - 1) / BN), static_cast<unsigned>((a.m + BM - 1) / BM));
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, a.C, static_cast<int>(a.m), static_cast<int>(a.n),
+                                              static_cast<int>(a.k));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc_kernel: ") + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+bool gemm_sm100_eligible(const GemmArgs& a) {
+  if (a.da != DT_BF16 || a.db != DT_BF16 || (a.dc != DT_BF16 && a.dc != DT_F32)) return false;
+  if (a.m <= 0 || a.n <= 0 || a.k <= 0) return false;
+  if (a.m > (1 << 30) || a.n > (1 << 30) || a.k > (1 << 30)) return false;
+  // TMA: 16-byte global row pitch for both operands; 16-byte C vectors.
+  if ((a.ta ? a.m : a.k) % 8 != 0) return false;
+  if ((a.tb ? a.k : a.n) % 8 != 0) return false;
+  if (a.n % 8 != 0) return false;
+  // Tiny GEMMs stay on the SIMT path (a 128x256 tile would be mostly idle).
+  if (a.m * a.n * a.k < (std::int64_t(1) << 20)) return false;
+  return true;
+}
+
+void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
+  const bool a_mn = a.ta, b_mn = !a.tb, cb = a.dc == DT_BF16;
+#define PLANC_TC(AM, BMN, CB) \
+  if (a_mn == AM && b_mn == BMN && cb == CB) return launch_typed<AM, BMN, CB>(a, s);
+  PLANC_TC(false, false, false)
+  PLANC_TC(false, false, true)
+  PLANC_TC(false, true, false)
+  PLANC_TC(false, true, true)
+  PLANC_TC(true, false, false)
+  PLANC_TC(true, false, true)
+  PLANC_TC(true, true, false)
+  PLANC_TC(true, true, true)
+#undef PLANC_TC
+}
+
 }  // namespace planc_b200

@@ -153,7 +153,7 @@ template <typename T>
 void box_dispatch(void* dst, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks, int vec,
                   cudaStream_t s) {
   constexpr int VV = 16 / sizeof(T);
-  if (vec > 1) {
+  if (vec) {
     box_kernel<T, VV><<<nchunks, kBoxThreads, 0, s>>>(static_cast<T*>(dst), cells, terms, chunks);
   } else {
     box_kernel<T, 1><<<nchunks, kBoxThreads, 0, s>>>(static_cast<T*>(dst), cells, terms, chunks);

@@ -613,6 +613,22 @@ std::vector<KernelStat> Executor::profile() {
   return out;
 }
 
+std::vector<double> Executor::read_buffer(int buffer) {
+  if (buffer < 0 || buffer >= static_cast<int>(prog_.buffers.size())) throw UsageError("no such buffer");
+  const BufferDesc& bd = prog_.buffers[buffer];
+  DeviceGuard dg(lanes_[bd.lane].gpu);
+  for (auto& l : lanes_) {
+    cudaSetDevice(l.gpu);
+    ck(cudaDeviceSynchronize(), "sync before readback");
+  }
+  cudaSetDevice(lanes_[bd.lane].gpu);
+  std::vector<char> r(bd.bytes);
+  ck(cudaMemcpy(r.data(), buf_ptr(buffer), bd.bytes, cudaMemcpyDeviceToHost), "readback");
+  std::vector<double> out(bd.elems);
+  for (std::int64_t i = 0; i < bd.elems; ++i) out[i] = host_elem(r, bd.dtype, i);
+  return out;
+}
+
 std::vector<int> Executor::output_ids() const {
   std::vector<int> ids;
   for (const auto& o : prog_.outputs) ids.push_back(o.first);

@@ -65,6 +65,8 @@ class Executor {
   // Per-kernel-family device time of one eagerly issued, serialised step.
   std::vector<KernelStat> profile();
   HostTensor get_output(int ptensor);
+  // Raw value of one device buffer (a vTensor piece) as doubles.
+  std::vector<double> read_buffer(int buffer);
   std::vector<int> output_ids() const;
   int kernels_per_step() const { return kernels_per_step_; }
   int gemm_tc_launches() const { return gemm_tc_per_step_; }

@@ -29,7 +29,7 @@ def _run(plan, inputs, flags=0, lanes=None):
 def test_golden_plan_parity(name):
     g = golden_cases.load(name)
     out, st = _run(g["plan"], g["inputs"])
-    ok, msg = pb.compare_outputs(g["expected"], out, g["meta"]["rel_tol"])
+    ok, msg = pb.compare_outputs(g["expected"], out, g["meta"]["rel_tol"], normwise=True)
     assert ok, msg
     assert st["kernels_per_step"] > 0
 
@@ -40,7 +40,7 @@ def test_golden_plan_parity(name):
 def test_parity_across_launch_modes(name, flags):
     g = golden_cases.load(name)
     out, _ = _run(g["plan"], g["inputs"], flags=flags)
-    ok, msg = pb.compare_outputs(g["expected"], out, g["meta"]["rel_tol"])
+    ok, msg = pb.compare_outputs(g["expected"], out, g["meta"]["rel_tol"], normwise=True)
     assert ok, msg
 
 
@@ -89,7 +89,7 @@ def test_e2e_counts_bytes():
         ms, h2d, d2h = ex.run_e2e(3)
         assert ms > 0 and h2d > 0 and d2h > 0
         out = ex.outputs()
-    ok, msg = pb.compare_outputs(g["expected"], out, 2e-2)
+    ok, msg = pb.compare_outputs(g["expected"], out, 2e-2, normwise=True)
     assert ok, msg
 
 
