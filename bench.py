@@ -75,27 +75,39 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                      "-i", ",".join(map(str, self.gpus))], capture_output=True, text=True,
-                                     timeout=5).stdout
-                for line in out.strip().splitlines():
-                    f = [x.strip() for x in line.split(",")]
-                    if len(f) >= 9:
-                        self.samples.append(f)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        # One continuously sampling nvidia-smi (every 50 ms) for the timed region.
+        cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
+               "-i", ",".join(map(str, self.gpus))]
+        try:
+            self._proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            return
+        for line in self._proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                self.samples.append(f)
+            if self._stop.is_set():
+                break
 
     def __enter__(self):
+        self._proc = None
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        deadline = time.time() + 3.0
+        while not self.samples and time.time() < deadline:  # sampler is live before timing starts
+            time.sleep(0.01)
         return self
 
     def __exit__(self, *a):
+        time.sleep(0.06)  # at least one sample after the timed region ends
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+        self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
