@@ -6,18 +6,23 @@
 // are not materialised: a transposed operand is simply loaded MN-major and the
 // UMMA instruction descriptor's major bits say so.
 //
-// Structure (one 128x256 output tile per CTA, 6 warps):
+// Structure: persistent, one CTA per SM, 128x256 output tiles in grouped
+// raster order (8 M-blocks per group for L2 reuse of B), 6 warps:
 //   warp 0      TMA producer: 4-stage smem ring (A 16 KB + B 32 KB per stage,
-//               128B-swizzled), mbarrier full/empty pipeline
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//               (kind::f16, M=128, N=256, K=16 per instruction), commits
-//               free smem stages and finally the accumulator
+//               128B-swizzled), mbarrier full/empty pipeline running across
+//               tiles
+//   warp 1      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//               + single-thread tcgen05.mma issuer (kind::f16, M=128, N=256,
+//               K=16 per instruction); commits free smem stages and, per
+//               tile, the accumulator it just finished
 //   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 TMEM -> registers, convert,
-//               16-byte global stores
+//               16-byte global stores; releases the accumulator so the MMA
+//               warp fills it with the tile after next while this one drains
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -37,7 +42,8 @@ constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
 constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int NUM_THREADS = 192;
-constexpr int TMEM_COLS = 256;
+constexpr int TMEM_COLS = 512;  // 2 accumulators x BN fp32 columns
+constexpr int GROUP_M = 8;
 
 // ---- PTX wrappers ------------------------------------------------------------
 
@@ -47,6 +53,10 @@ __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
 
 __device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
@@ -132,6 +142,56 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&r
 
 // ---- kernel --------------------------------------------------------------------
 
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
+  const int per_group = GROUP_M * tiles_n;
+  const int group = t / per_group;
+  const int first_m = group * GROUP_M;
+  const int gm = min(tiles_m - first_m, GROUP_M);
+  const int r = t % per_group;
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
+
+template <bool C_BF16>
+__device__ __forceinline__ void store_row_chunk(void* C, int row, int col0, int m, int n, const std::uint32_t (&r)[32]) {
+  if (row >= m || col0 >= n) return;
+  if (C_BF16) {
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(C) + static_cast<std::int64_t>(row) * n + col0;
+    if (col0 + 32 <= n) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 pk;
+        std::uint32_t* w = reinterpret_cast<std::uint32_t*>(&pk);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 h =
+              __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]), __uint_as_float(r[v * 8 + 2 * e + 1]));
+          w[e] = *reinterpret_cast<std::uint32_t*>(&h);
+        }
+        *reinterpret_cast<uint4*>(out + v * 8) = pk;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (col0 + e < n) out[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+    }
+  } else {
+    float* out = static_cast<float*>(C) + static_cast<std::int64_t>(row) * n + col0;
+    if (col0 + 32 <= n) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        *reinterpret_cast<float4*>(out + 4 * v) = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                                              __uint_as_float(r[4 * v + 2]),
+                                                              __uint_as_float(r[4 * v + 3]));
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (col0 + e < n) out[e] = __uint_as_float(r[e]);
+    }
+  }
+}
+
 template <bool A_MN, bool B_MN, bool C_BF16>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* __restrict__ C,
@@ -143,13 +203,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   std::uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sB + STAGES * B_STAGE_BYTES);
   std::uint64_t* empty = full + STAGES;
-  std::uint64_t* tmem_full = empty + STAGES;
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tmem_full + 1);
+  std::uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
+  std::uint64_t* tempty = tfull + 2;      // [2] accumulator drained
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int m0 = blockIdx.y * BM;
-  const int n0 = blockIdx.x * BN;
+  const int tiles_m = (m + BM - 1) / BM;
+  const int tiles_n = (n + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
   const int num_k = (k + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -159,7 +221,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -175,95 +240,90 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < num_k; ++kb) {
-        const int s = kb % STAGES;
-        const std::uint32_t phase = (kb / STAGES) & 1;
-        mbar_wait(&empty[s], phase ^ 1);
-        mbar_expect_tx(&full[s], A_STAGE_BYTES + B_STAGE_BYTES);
-        std::uint8_t* a = sA + s * A_STAGE_BYTES;
-        std::uint8_t* b = sB + s * B_STAGE_BYTES;
-        if (A_MN) {
+      int it = 0;  // global k-block counter across tiles (ring position)
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, tiles_m, tiles_n, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < num_k; ++kb, ++it) {
+          const int s = it % STAGES;
+          const std::uint32_t phase = (it / STAGES) & 1;
+          mbar_wait(&empty[s], phase ^ 1);
+          mbar_expect_tx(&full[s], A_STAGE_BYTES + B_STAGE_BYTES);
+          std::uint8_t* a = sA + s * A_STAGE_BYTES;
+          std::uint8_t* b = sB + s * B_STAGE_BYTES;
+          if (A_MN) {
 #pragma unroll
-          for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * (64 * BK * 2), &tmA, m0 + 64 * j, kb * BK, &full[s]);
-        } else {
-          tma_load_2d(a, &tmA, kb * BK, m0, &full[s]);
-        }
-        if (B_MN) {
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * (64 * BK * 2), &tmA, m0 + 64 * j, kb * BK, &full[s]);
+          } else {
+            tma_load_2d(a, &tmA, kb * BK, m0, &full[s]);
+          }
+          if (B_MN) {
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * (64 * BK * 2), &tmB, n0 + 64 * j, kb * BK, &full[s]);
-        } else {
-          tma_load_2d(b, &tmB, kb * BK, n0, &full[s]);
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * (64 * BK * 2), &tmB, n0 + 64 * j, kb * BK, &full[s]);
+          } else {
+            tma_load_2d(b, &tmB, kb * BK, n0, &full[s]);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr std::uint32_t idesc = make_idesc(A_MN, B_MN);
-      for (int kb = 0; kb < num_k; ++kb) {
-        const int s = kb % STAGES;
-        const std::uint32_t phase = (kb / STAGES) & 1;
-        mbar_wait(&full[s], phase);
+      int it = 0, local = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const std::uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
-        const std::uint32_t a_base = smem_u32(sA + s * A_STAGE_BYTES);
-        const std::uint32_t b_base = smem_u32(sB + s * B_STAGE_BYTES);
+        const std::uint32_t d = tmem + static_cast<std::uint32_t>(acc * BN);
+        for (int kb = 0; kb < num_k; ++kb, ++it) {
+          const int s = it % STAGES;
+          const std::uint32_t phase = (it / STAGES) & 1;
+          mbar_wait(&full[s], phase);
+          tc_fence_after();
+          const std::uint32_t a_base = smem_u32(sA + s * A_STAGE_BYTES);
+          const std::uint32_t b_base = smem_u32(sB + s * B_STAGE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          // K-major: 16 elements = 32 bytes along the swizzled row; rows of
-          // 128 B, 8-row groups 1024 B apart (SBO). MN-major: 16 K-rows =
-          // 2048 B; 64-element MN blocks 8 KB apart (LBO), 8-row K groups
-          // 1024 B apart (SBO).
-          std::uint64_t ad = A_MN ? smem_desc(a_base + kk * 2048, 64 * BK * 2, 1024)
-                                  : smem_desc(a_base + kk * 32, 16, 1024);
-          std::uint64_t bd = B_MN ? smem_desc(b_base + kk * 2048, 64 * BK * 2, 1024)
-                                  : smem_desc(b_base + kk * 32, 16, 1024);
-          tc_mma(tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            // K-major: 16 elements = 32 bytes along the swizzled row; rows of
+            // 128 B, 8-row groups 1024 B apart (SBO). MN-major: 16 K-rows =
+            // 2048 B; 64-element MN blocks 8 KB apart (LBO), 8-row K groups
+            // 1024 B apart (SBO).
+            std::uint64_t ad = A_MN ? smem_desc(a_base + kk * 2048, 64 * BK * 2, 1024)
+                                    : smem_desc(a_base + kk * 32, 16, 1024);
+            std::uint64_t bd = B_MN ? smem_desc(b_base + kk * 2048, 64 * BK * 2, 1024)
+                                    : smem_desc(b_base + kk * 32, 16, 1024);
+            tc_mma(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty[s]);  // smem stage free once these MMAs retire
         }
-        tc_commit(&empty[s]);
+        tc_commit(&tfull[acc]);  // accumulator complete
       }
-      tc_commit(tmem_full);
     }
   } else {
     // Epilogue warps 2..5: warp w may only touch TMEM lanes 32*(w%4)..+31.
     const int q = warp % 4;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const int row = m0 + q * 32 + lane;
+    int local = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      int mb, nb;
+      tile_coords(t, tiles_m, tiles_n, mb, nb);
+      const int acc = local & 1;
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      const int row = mb * BM + q * 32 + lane;
+      const std::uint32_t base = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      std::uint32_t r[32];
-      tmem_ld32(tmem + (static_cast<std::uint32_t>(q * 32) << 16) + c * 32, r);
-      const int col0 = n0 + c * 32;
-      if (row >= m || col0 >= n) continue;
-      if (C_BF16) {
-        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(C) + static_cast<std::int64_t>(row) * n + col0;
-        if (col0 + 32 <= n) {
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint4 pk;
-            std::uint32_t* w = reinterpret_cast<std::uint32_t*>(&pk);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]),
-                                                       __uint_as_float(r[v * 8 + 2 * e + 1]));
-              w[e] = *reinterpret_cast<std::uint32_t*>(&h);
-            }
-            *reinterpret_cast<uint4*>(out + v * 8) = pk;
-          }
-        } else {
-          for (int e = 0; e < 32 && col0 + e < n; ++e) out[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+      for (int c = 0; c < BN / 32; ++c) {
+        std::uint32_t r[32];
+        tmem_ld32(base + c * 32, r);
+        if (c == BN / 32 - 1) {
+          // All TMEM reads of this accumulator are complete: hand it back.
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-      } else {
-        float* out = static_cast<float*>(C) + static_cast<std::int64_t>(row) * n + col0;
-        if (col0 + 32 <= n) {
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            float4 f = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-            *reinterpret_cast<float4*>(out + 4 * v) = f;
-          }
-        } else {
-          for (int e = 0; e < 32 && col0 + e < n; ++e) out[e] = __uint_as_float(r[e]);
-        }
+        store_row_chunk<C_BF16>(C, row, nb * BN + c * 32, m, n, r);
       }
     }
   }
@@ -310,19 +370,22 @@ CUtensorMap make_map(const void* base, std::int64_t rows, std::int64_t cols, int
 template <bool A_MN, bool B_MN, bool C_BF16>
 void launch_typed(const GemmArgs& a, cudaStream_t s) {
   static unsigned attr_set_mask = 0;  // per device ordinal
+  static int num_sms[32] = {0};
   auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16>;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set_mask & (1u << dev))) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc smem attribute: ") + cudaGetErrorString(e));
+    cudaDeviceGetAttribute(&num_sms[dev & 31], cudaDevAttrMultiProcessorCount, dev);
     attr_set_mask |= 1u << dev;
   }
   // A: [m][k] (K-major) or, transposed, [k][m] (MN-major); B: [k][n]
   // (MN-major) or, transposed, [n][k] (K-major).
   CUtensorMap ma = A_MN ? make_map(a.A, a.k, a.m, BK) : make_map(a.A, a.m, a.k, BM);
   CUtensorMap mb = B_MN ? make_map(a.B, a.k, a.n, BK) : make_map(a.B, a.n, a.k, BN);
-  dim3 grid(static_cast<unsigned>((a.n + BN - 1) / BN), static_cast<unsigned>((a.m + BM - 1) / BM));
+  const std::int64_t tiles = ((a.m + BM - 1) / BM) * ((a.n + BN - 1) / BN);
+  const int grid = static_cast<int>(std::min<std::int64_t>(tiles, num_sms[dev & 31] > 0 ? num_sms[dev & 31] : 148));
   kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, a.C, static_cast<int>(a.m), static_cast<int>(a.n),
                                               static_cast<int>(a.k));
   cudaError_t e = cudaGetLastError();

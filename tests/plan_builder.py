@@ -1,0 +1,44 @@
+"""TEST INFRASTRUCTURE — minimal plan.json documents for single sub-operators.
+
+Builds ExecutionPlan wire documents (reference simulate.cpp:492-602 schema)
+for one op on one lane, so kernel-level tests can run on the GPU box where
+the reference front end is absent. Used only by tests.
+"""
+import json
+
+
+def single_op_plan(kind, in_shapes, out_shape, in_elem=2, out_elem=2, attrs=None):
+    attrs = attrs or {}
+    pts, vts, feeds = [], [], []
+    ins = []
+    for i, shp in enumerate(in_shapes):
+        pts.append({"id": i, "shape": list(shp), "elem_size": in_elem if not isinstance(in_elem, list) else in_elem[i],
+                    "kind": "activation"})
+        vts.append({"id": 100 + i, "ptensor": i, "region": [[0, e] for e in shp], "value": [0, 1],
+                    "replica": [0, 1], "side": "in", "owner": "op"})
+        ins.append(100 + i)
+    out_pt = len(in_shapes)
+    pts.append({"id": out_pt, "shape": list(out_shape), "elem_size": out_elem, "kind": "activation"})
+    vts.append({"id": 200, "ptensor": out_pt, "region": [[0, e] for e in out_shape], "value": [0, 1],
+                "replica": [0, 1], "side": "out", "owner": "op"})
+    op = {"id": "op", "kind": kind, "inputs": ins, "outputs": [200], "direction": "forward", "flops": 0.0,
+          "doc_order": 0, "inserted": False}
+    op.update(attrs)
+    doc = {"ptensors": pts, "vtensors": vts, "ops": [op], "assignment": {"op": 0}, "feeds": feeds,
+           "coll_groups": [], "sync_edges": [],
+           "lanes": [{"device": 0, "tasks": [{"kind": "compute", "op": "op", "duration": 0.0, "bytes": 0}]}],
+           "cluster": {"devices": [{"id": 0, "group": 0, "memory": 1 << 34}],
+                       "intra_link": {"bandwidth": 1e11, "latency": 1e-6},
+                       "inter_link": {"bandwidth": 1e10, "latency": 1e-5}, "device_throughput": 1e12}}
+    return json.dumps(doc), out_pt
+
+
+def matmul_plan(m, n, k, ta=False, tb=False, in_elem=2, out_elem=2):
+    a = (k, m) if ta else (m, k)
+    b = (n, k) if tb else (k, n)
+    attrs = {}
+    if ta:
+        attrs["transpose_a"] = True
+    if tb:
+        attrs["transpose_b"] = True
+    return single_op_plan("matmul", [a, b], (m, n), in_elem, out_elem, attrs)

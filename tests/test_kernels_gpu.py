@@ -1,0 +1,103 @@
+"""Kernel-level GPU tests through single-op plans (C ABI).
+
+GEMM: the tcgen05 path (bf16 operands, fp32 TMEM accumulation) against a
+float64 matmul of the same bf16-rounded operands, over all transpose
+combinations, tile tails, persistent multi-tile grids and fp32 output;
+normwise tolerance 2^-8 (one bf16 rounding of the output). The SIMT path is
+checked the same way with NO_TENSOR_CORES. Memory-bound kernels: exact on
+integer data.
+"""
+import numpy as np
+import pytest
+
+import paper_2301_08984_b200 as pb
+from plan_builder import matmul_plan, single_op_plan
+
+pytestmark = pytest.mark.gpu
+
+
+def bf16_round(x):
+    a = np.ascontiguousarray(x, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16 << 16
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def run_single(plan, inputs, out_pt, flags=0):
+    with pb.Executor(plan, lane_gpus=[0], flags=flags) as ex:
+        ex.set_inputs(inputs)
+        ex.run(0)
+        st = ex.stats()
+        return ex.get_output(out_pt), st
+
+
+GEMM_SHAPES = [
+    (128, 256, 64), (256, 512, 128), (300, 520, 200), (1000, 1000, 1000),
+    (2048, 2048, 8192), (8192, 2048, 2048), (1024, 8192, 512), (136, 264, 24),
+]
+
+
+@pytest.mark.parametrize("m,n,k", GEMM_SHAPES)
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+def test_gemm_tcgen05_vs_fp64(m, n, k, ta, tb):
+    if m * n * k > 2 ** 33 and (ta, tb) != (False, False):
+        pytest.skip("one transpose variant at the largest shapes")
+    rng = np.random.default_rng(m * 7 + n * 3 + k)
+    plan, out_pt = matmul_plan(m, n, k, ta, tb)
+    a = bf16_round(rng.standard_normal((k, m) if ta else (m, k)))
+    b = bf16_round(rng.standard_normal((n, k) if tb else (k, n)))
+    out, st = run_single(plan, {0: a, 1: b}, out_pt)
+    assert st["gemm_tc_per_step"] == 1
+    ref = (a.T if ta else a) @ (b.T if tb else b)
+    err = np.abs(out - ref).max() / max(1.0, np.abs(ref).max())
+    assert err < 2.0 ** -8, err
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, True)])
+def test_gemm_tcgen05_fp32_output(ta, tb):
+    m, n, k = 384, 512, 320
+    rng = np.random.default_rng(5)
+    plan, out_pt = matmul_plan(m, n, k, ta, tb, in_elem=2, out_elem=4)
+    a = rng.integers(-4, 5, size=(k, m) if ta else (m, k)).astype(np.float64)
+    b = rng.integers(-4, 5, size=(n, k) if tb else (k, n)).astype(np.float64)
+    out, st = run_single(plan, {0: a, 1: b}, out_pt)
+    assert st["gemm_tc_per_step"] == 1
+    ref = (a.T if ta else a) @ (b.T if tb else b)
+    assert np.array_equal(out, ref)  # integer products, fp32 accumulate: exact
+
+
+@pytest.mark.parametrize("m,n,k", [(37, 53, 29), (128, 256, 64), (300, 200, 100)])
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, True), (True, False)])
+@pytest.mark.parametrize("elem", [2, 4])
+def test_gemm_simt(m, n, k, ta, tb, elem):
+    rng = np.random.default_rng(m + n + k)
+    plan, out_pt = matmul_plan(m, n, k, ta, tb, in_elem=elem, out_elem=4)
+    a = rng.integers(-4, 5, size=(k, m) if ta else (m, k)).astype(np.float64)
+    b = rng.integers(-4, 5, size=(n, k) if tb else (k, n)).astype(np.float64)
+    out, st = run_single(plan, {0: a, 1: b}, out_pt, flags=pb.NO_TENSOR_CORES)
+    assert st["gemm_tc_per_step"] == 0
+    assert np.array_equal(out, (a.T if ta else a) @ (b.T if tb else b))
+
+
+@pytest.mark.parametrize("kind,fn", [("add", np.add), ("mul", np.multiply), ("max", np.maximum)])
+@pytest.mark.parametrize("n_in,shape,elem", [(2, (1031,), 4), (3, (64, 72), 2), (9, (8, 16), 4),
+                                             (2, (4096, 2048), 2)])
+def test_elementwise(kind, fn, n_in, shape, elem):
+    rng = np.random.default_rng(n_in)
+    plan, out_pt = single_op_plan(kind, [shape] * n_in, shape, elem, elem)
+    ins = {i: rng.integers(-3, 4, size=shape).astype(np.float64) for i in range(n_in)}
+    out, _ = run_single(plan, ins, out_pt)
+    ref = ins[0]
+    for i in range(1, n_in):
+        ref = fn(ref, ins[i])
+    assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("shape,axis", [((5, 7), 0), ((5, 7), 1), ((3, 4, 5), 1), ((9,), 0), ((2048, 1024), 1)])
+def test_reduce_sum(shape, axis):
+    rng = np.random.default_rng(3)
+    out_shape = tuple(e for i, e in enumerate(shape) if i != axis) or (1,)
+    plan, out_pt = single_op_plan("reduce-sum", [shape], out_shape, 4, 4, {"axis": axis})
+    x = rng.integers(-4, 5, size=shape).astype(np.float64)
+    out, _ = run_single(plan, {0: x}, out_pt)
+    assert np.array_equal(out.reshape(-1), x.sum(axis=axis).reshape(-1))
