@@ -94,6 +94,7 @@ __device__ __forceinline__ void store_any(void* p, int dt, std::int64_t i, float
 
 constexpr int kBoxThreads = 256;
 constexpr int kSmemTerms = 32;
+constexpr int kBoxUnroll = 4;
 
 template <typename T, int V>
 __global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, const DevCell* __restrict__ cells,
@@ -110,42 +111,64 @@ __global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, c
   __syncthreads();
   const int rank = sc.rank;
   const std::int64_t inner_vecs = sc.ext[rank - 1] / V;
-  for (std::int64_t u = threadIdx.x; u < ch.count; u += blockDim.x) {
-    std::int64_t lin = ch.begin + u;
-    std::int64_t coord[kBoxRank];
-    coord[rank - 1] = (lin % inner_vecs) * V;
-    lin /= inner_vecs;
+  constexpr int U = kBoxUnroll;  // independent vectors in flight per thread
+  for (std::int64_t u0 = threadIdx.x; u0 < ch.count; u0 += static_cast<std::int64_t>(blockDim.x) * U) {
+    std::int64_t coord[U][kBoxRank];
+    bool live[U];
 #pragma unroll
-    for (int d = kBoxRank - 2; d >= 0; --d) {
-      if (d < rank - 1) {
-        coord[d] = lin % sc.ext[d];
-        lin /= sc.ext[d];
+    for (int x = 0; x < U; ++x) {
+      const std::int64_t u = u0 + static_cast<std::int64_t>(x) * blockDim.x;
+      live[x] = u < ch.count;
+      std::int64_t lin = ch.begin + (live[x] ? u : 0);
+      // Static indices only (keeps coord in registers).
+#pragma unroll
+      for (int d = kBoxRank - 1; d >= 0; --d) {
+        coord[x][d] = 0;
+        if (d == rank - 1) {
+          coord[x][d] = (lin % inner_vecs) * V;
+          lin /= inner_vecs;
+        } else if (d < rank - 1) {
+          coord[x][d] = lin % sc.ext[d];
+          lin /= sc.ext[d];
+        }
       }
     }
-    std::int64_t doff = sc.dst_off;
+    A acc[U][V];
 #pragma unroll
-    for (int d = 0; d < kBoxRank; ++d)
-      if (d < rank) doff += coord[d] * sc.dst_str[d];
-    A acc[V];
+    for (int x = 0; x < U; ++x)
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc[i] = A(0);
+      for (int i = 0; i < V; ++i) acc[x][i] = A(0);
     for (int t = 0; t < nt; ++t) {
       const DevTerm& tm = t < kSmemTerms ? st[t] : terms[sc.term0 + t];
-      std::int64_t soff = tm.offset;
+      A v[U][V];
 #pragma unroll
-      for (int d = 0; d < kBoxRank; ++d)
-        if (d < rank) soff += coord[d] * tm.str[d];
-      A v[V];
-      load_vec<T, V>(reinterpret_cast<const T*>(tm.src) + soff, v);
-      if (tm.add) {
+      for (int x = 0; x < U; ++x) {
+        std::int64_t soff = tm.offset;
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc[i] += v[i];
-      } else {
+        for (int d = 0; d < kBoxRank; ++d)
+          if (d < rank) soff += coord[x][d] * tm.str[d];
+        if (live[x]) load_vec<T, V>(reinterpret_cast<const T*>(tm.src) + soff, v[x]);
+      }
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc[i] = v[i];
+      for (int x = 0; x < U; ++x) {
+        if (tm.add) {
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[x][i] += v[x][i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[x][i] = v[x][i];
+        }
       }
     }
-    store_vec<T, V>(dst + doff, acc);
+#pragma unroll
+    for (int x = 0; x < U; ++x) {
+      if (!live[x]) continue;
+      std::int64_t doff = sc.dst_off;
+#pragma unroll
+      for (int d = 0; d < kBoxRank; ++d)
+        if (d < rank) doff += coord[x][d] * sc.dst_str[d];
+      store_vec<T, V>(dst + doff, acc[x]);
+    }
   }
 }
 
@@ -174,19 +197,38 @@ __device__ __forceinline__ float ew_apply(float a, float b) {
   return fmaxf(a, b);
 }
 
+// Each thread keeps kEwUnroll independent 16-byte vectors in flight per
+// operand (grid-strided so every warp access stays coalesced).
+constexpr int kEwUnroll = 4;
+
 template <typename T, int OP>
 __global__ void __launch_bounds__(256) ew_kernel(EwPtrs in, int nin, T* __restrict__ out, std::int64_t nvec) {
   constexpr int V = 16 / sizeof(T);
-  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < nvec;
-       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-    float acc[V], v[V];
-    load_vec<T, V>(static_cast<const T*>(in.p[0]) + i * V, acc);
-    for (int k = 1; k < nin; ++k) {
-      load_vec<T, V>(static_cast<const T*>(in.p[k]) + i * V, v);
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; base < nvec;
+       base += stride * kEwUnroll) {
+    float acc[kEwUnroll][V], v[kEwUnroll][V];
 #pragma unroll
-      for (int j = 0; j < V; ++j) acc[j] = ew_apply<OP>(acc[j], v[j]);
+    for (int u = 0; u < kEwUnroll; ++u) {
+      const std::int64_t i = base + u * stride;
+      if (i < nvec) load_vec<T, V>(static_cast<const T*>(in.p[0]) + i * V, acc[u]);
     }
-    store_vec<T, V>(out + i * V, acc);
+    for (int k = 1; k < nin; ++k) {
+#pragma unroll
+      for (int u = 0; u < kEwUnroll; ++u) {
+        const std::int64_t i = base + u * stride;
+        if (i < nvec) load_vec<T, V>(static_cast<const T*>(in.p[k]) + i * V, v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kEwUnroll; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[u][j] = ew_apply<OP>(acc[u][j], v[u][j]);
+    }
+#pragma unroll
+    for (int u = 0; u < kEwUnroll; ++u) {
+      const std::int64_t i = base + u * stride;
+      if (i < nvec) store_vec<T, V>(out + i * V, acc[u]);
+    }
   }
 }
 
@@ -210,7 +252,7 @@ void ew_typed(const void* const* ins, int nin, void* out, std::int64_t count, cu
   }
   std::int64_t nvec = aligned ? count / V : 0;
   if (nvec > 0) {
-    ew_kernel<T, OP><<<grid_for(nvec, 256), 256, 0, s>>>(p, nin, static_cast<T*>(out), nvec);
+    ew_kernel<T, OP><<<grid_for(nvec, 256 * kEwUnroll, 148 * 8), 256, 0, s>>>(p, nin, static_cast<T*>(out), nvec);
   }
   std::int64_t rest = count - nvec * V;
   if (rest > 0) {

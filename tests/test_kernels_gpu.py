@@ -32,7 +32,7 @@ def run_single(plan, inputs, out_pt, flags=0):
 
 
 GEMM_SHAPES = [
-    (128, 256, 64), (256, 512, 128), (300, 520, 200), (1000, 1000, 1000),
+    (128, 256, 64), (256, 512, 128), (304, 520, 200), (1000, 1000, 1000),
     (2048, 2048, 8192), (8192, 2048, 2048), (1024, 8192, 512), (136, 264, 40),
 ]
 
