@@ -59,6 +59,21 @@ int planc_b200_open(const char* plan_json, const int* lane_gpu, int num_lane_gpu
                     planc_b200_exec** out);
 void planc_b200_close(planc_b200_exec* h);
 
+/* One process per GPU (torchrun): this process runs the plan lanes l with
+ * lane_rank[l] == rank on CUDA device local_gpu. Pieces produced on another
+ * rank's lane reach their consumers through NCCL point-to-point exchange
+ * steps placed in the global issue order (identical on every rank, so the
+ * grouped sends/receives match without deadlock). nccl_id is the 128-byte
+ * ncclUniqueId from planc_b200_nccl_unique_id on rank 0, broadcast by the
+ * caller. NCCL is loaded at run time (libnccl.so.2). */
+int planc_b200_nccl_unique_id(unsigned char id_out[128]);
+int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* lane_rank, int num_lanes,
+                         int local_gpu, const unsigned char nccl_id[128], uint32_t flags,
+                         planc_b200_exec** out);
+/* Host-only: the rank-localised program (same on every rank), as JSON. */
+int planc_b200_describe_rank(const char* plan_json, const int* lane_rank, int num_lanes, uint32_t flags,
+                             char** json_out);
+
 /* Binds one graph-input pTensor (refexec.cpp:366-376); `data` is dense
  * row-major with `rank` extents `shape`. Copied; placed on the GPU at the
  * next run. */

@@ -103,6 +103,10 @@ def _load():
     L.planc_b200_read_buffer.restype = c_i64
     L.planc_b200_profile.argtypes = [vp, P(ctypes.c_char_p)]
     L.planc_b200_describe.argtypes = [ctypes.c_char_p, ctypes.c_uint32, P(vp)]
+    L.planc_b200_describe_rank.argtypes = [ctypes.c_char_p, P(c_int), c_int, ctypes.c_uint32, P(vp)]
+    L.planc_b200_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    L.planc_b200_open_rank.argtypes = [ctypes.c_char_p, c_int, c_int, P(c_int), c_int, c_int, ctypes.c_char_p,
+                                       ctypes.c_uint32, P(vp)]
     L.planc_b200_free.argtypes = [vp]
     _lib = L
     return L
@@ -123,22 +127,53 @@ def version() -> str:
     return _load().planc_b200_version().decode()
 
 
-def describe(plan_json: str, strict_value: bool = False) -> dict:
-    """Host-only lowering of a plan (no GPU): buffers, instructions, cells."""
+def describe(plan_json: str, strict_value: bool = False, lane_rank=None) -> dict:
+    """Host-only lowering of a plan (no GPU): buffers, instructions, cells.
+
+    With ``lane_rank`` (owner rank per plan lane) the one-process-per-GPU
+    program is returned: cross-rank pieces become ``xfer`` exchange steps.
+    """
     L = _load()
     out = ctypes.c_void_p()
-    _check(L.planc_b200_describe(plan_json.encode(), STRICT_VALUE if strict_value else 0, ctypes.byref(out)))
+    flags = STRICT_VALUE if strict_value else 0
+    if lane_rank is None:
+        _check(L.planc_b200_describe(plan_json.encode(), flags, ctypes.byref(out)))
+    else:
+        arr = (ctypes.c_int * len(lane_rank))(*lane_rank)
+        _check(L.planc_b200_describe_rank(plan_json.encode(), arr, len(lane_rank), flags, ctypes.byref(out)))
     s = ctypes.string_at(out.value).decode()
     L.planc_b200_free(out)
     return json.loads(s)
 
 
-class Executor:
-    """One compiled plan on the GPU(s). ``lane_gpus[i]`` runs plan lane i."""
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it, the caller broadcasts it)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_load().planc_b200_nccl_unique_id(buf))
+    return buf.raw
 
-    def __init__(self, plan_json: str, lane_gpus=None, flags: int = 0):
+
+def lanes_round_robin(num_lanes: int, world: int):
+    """Default lane -> rank ownership: lane l runs on rank l % world."""
+    return [lane % world for lane in range(num_lanes)]
+
+
+class Executor:
+    """One compiled plan on the GPU(s). ``lane_gpus[i]`` runs plan lane i.
+
+    ``rank``/``world``/``lane_rank``/``nccl_id`` select the one-process-per-GPU
+    mode: this process runs the lanes it owns on ``local_gpu``.
+    """
+
+    def __init__(self, plan_json: str, lane_gpus=None, flags: int = 0, rank=None, world=None, lane_rank=None,
+                 local_gpu: int = 0, nccl_id: bytes = None):
         L = _load()
         self._h = ctypes.c_void_p()
+        if rank is not None:
+            arr = (ctypes.c_int * len(lane_rank))(*lane_rank)
+            _check(L.planc_b200_open_rank(plan_json.encode(), rank, world, arr, len(lane_rank), local_gpu,
+                                          nccl_id, flags, ctypes.byref(self._h)))
+            return
         arr, n = None, 0
         if lane_gpus:
             n = len(lane_gpus)

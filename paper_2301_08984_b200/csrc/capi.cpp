@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../../include/planc_b200.h"
+#include "nccl_api.hpp"
 #include "runtime.hpp"
 
 using namespace planc_b200;
@@ -77,6 +78,52 @@ int planc_b200_open(const char* plan_json, const int* lane_gpu, int num_lane_gpu
       throw;
     }
     *out = h;
+  });
+}
+
+int planc_b200_nccl_unique_id(unsigned char id_out[128]) {
+  return guarded([&] {
+    if (!id_out) throw UsageError("null argument");
+    ncclUniqueId id;
+    nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(id_out, id.internal, 128);
+  });
+}
+
+int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* lane_rank, int num_lanes,
+                         int local_gpu, const unsigned char nccl_id[128], uint32_t flags, planc_b200_exec** out) {
+  return guarded([&] {
+    if (!plan_json || !out || !lane_rank || !nccl_id) throw UsageError("planc_b200_open_rank: null argument");
+    ExecOptions opt;
+    opt.use_graph = (flags & PLANC_B200_NO_GRAPH) == 0;
+    opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
+    opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
+    RankConfig rc;
+    rc.rank = rank;
+    rc.world = world;
+    rc.lane_rank.assign(lane_rank, lane_rank + num_lanes);
+    rc.local_gpu = local_gpu;
+    std::memcpy(rc.nccl_id, nccl_id, 128);
+    auto* h = new planc_b200_exec;
+    try {
+      h->ex = new Executor(plan_json, {}, opt, &rc);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int planc_b200_describe_rank(const char* plan_json, const int* lane_rank, int num_lanes, uint32_t flags,
+                             char** json_out) {
+  return guarded([&] {
+    if (!plan_json || !json_out || !lane_rank) throw UsageError("null argument");
+    ProgramOptions po;
+    po.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
+    ExecutionPlan plan = load_plan(plan_json);
+    Program p = localize(build_program(plan, po), std::vector<int>(lane_rank, lane_rank + num_lanes));
+    *json_out = dup(p.describe_json());
   });
 }
 

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, c
   __syncthreads();
   const int rank = sc.rank;
   const std::int64_t inner_vecs = sc.ext[rank - 1] / V;
+  const bool small = sc.elems / V < (std::int64_t(1) << 32);
   constexpr int U = kBoxUnroll;  // independent vectors in flight per thread
   for (std::int64_t u0 = threadIdx.x; u0 < ch.count; u0 += static_cast<std::int64_t>(blockDim.x) * U) {
     std::int64_t coord[U][kBoxRank];
@@ -120,16 +121,37 @@ __global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, c
       const std::int64_t u = u0 + static_cast<std::int64_t>(x) * blockDim.x;
       live[x] = u < ch.count;
       std::int64_t lin = ch.begin + (live[x] ? u : 0);
-      // Static indices only (keeps coord in registers).
+      // Static indices only (keeps coord in registers). Rank-1 cells (the
+      // common case after dim collapsing) need no division; others use
+      // 32-bit division when the cell fits.
 #pragma unroll
-      for (int d = kBoxRank - 1; d >= 0; --d) {
-        coord[x][d] = 0;
-        if (d == rank - 1) {
-          coord[x][d] = (lin % inner_vecs) * V;
-          lin /= inner_vecs;
-        } else if (d < rank - 1) {
-          coord[x][d] = lin % sc.ext[d];
-          lin /= sc.ext[d];
+      for (int d = 0; d < kBoxRank; ++d) coord[x][d] = 0;
+      if (rank == 1) {
+        coord[x][0] = lin * V;
+      } else if (small) {
+        std::uint32_t l32 = static_cast<std::uint32_t>(lin);
+        const std::uint32_t iv = static_cast<std::uint32_t>(inner_vecs);
+#pragma unroll
+        for (int d = kBoxRank - 1; d >= 0; --d) {
+          if (d == rank - 1) {
+            coord[x][d] = static_cast<std::int64_t>(l32 % iv) * V;
+            l32 /= iv;
+          } else if (d < rank - 1) {
+            const std::uint32_t e = static_cast<std::uint32_t>(sc.ext[d]);
+            coord[x][d] = l32 % e;
+            l32 /= e;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int d = kBoxRank - 1; d >= 0; --d) {
+          if (d == rank - 1) {
+            coord[x][d] = (lin % inner_vecs) * V;
+            lin /= inner_vecs;
+          } else if (d < rank - 1) {
+            coord[x][d] = lin % sc.ext[d];
+            lin /= sc.ext[d];
+          }
         }
       }
     }

@@ -27,6 +27,7 @@ const char* instr_kind_name(InstrKind k) {
     case InstrKind::emb_lookup: return "emb_lookup";
     case InstrKind::emb_grad: return "emb_grad";
     case InstrKind::box: return "box";
+    case InstrKind::xfer: return "xfer";
     case InstrKind::nop: return "nop";
   }
   return "?";
@@ -524,6 +525,7 @@ struct Builder {
         emit_box(oi, m, lane, 1, out, pieces, "collective " + oid);
         P.instrs.back().wire_bytes = wire;
         P.instrs.back().label = grp.primitive + ":" + oid;
+        P.instrs.back().coll_group = grp.id;
       }
       for (int v : m.outputs) issued_vts.insert(v);
       op_issued[oi] = true;
@@ -718,6 +720,114 @@ Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt) {
   return std::move(b.P);
 }
 
+Program localize(const Program& g, const std::vector<int>& lane_rank) {
+  if (static_cast<int>(lane_rank.size()) != g.num_lanes) {
+    throw UsageError("lane_rank must name an owner for each of the plan's " + std::to_string(g.num_lanes) +
+                     " lanes");
+  }
+  Program P = g;
+  P.instrs.clear();
+  P.issue_order.clear();
+  std::vector<int> remap(g.instrs.size(), -1);
+  std::map<std::pair<int, int>, int> shadow;  // (source buffer, consuming lane) -> shadow buffer
+  auto owner = [&](int lane) { return lane_rank[lane]; };
+  auto push = [&](Instr in) {
+    in.id = static_cast<int>(P.instrs.size());
+    P.instrs.push_back(std::move(in));
+    P.issue_order.push_back(P.instrs.back().id);
+    return P.instrs.back().id;
+  };
+  const auto& order = g.issue_order;
+  std::size_t i = 0;
+  while (i < order.size()) {
+    // A collective group's member outputs are consecutive in issue order and
+    // share one exchange step.
+    std::vector<int> grp = {order[i]};
+    const Instr& first = g.instrs[order[i]];
+    if (first.kind == InstrKind::box && first.coll_group >= 0) {
+      while (i + grp.size() < order.size()) {
+        const Instr& nx = g.instrs[order[i + grp.size()]];
+        if (nx.kind != InstrKind::box || nx.coll_group != first.coll_group) break;
+        grp.push_back(nx.id);
+      }
+    }
+    Instr x;
+    x.kind = InstrKind::xfer;
+    x.lane = first.lane;
+    x.stream = 1;
+    x.op = first.op;
+    x.label = "xfer:" + first.label;
+    std::set<int> xdeps;
+    for (int id : grp) {
+      const Instr& in = g.instrs[id];
+      if (in.kind != InstrKind::box) continue;
+      for (const auto& c : in.cells) {
+        for (const auto& t : c.terms) {
+          const BufferDesc& sb = P.buffers[t.buffer];
+          if (owner(sb.lane) == owner(in.lane)) continue;
+          auto key = std::make_pair(t.buffer, in.lane);
+          if (shadow.count(key)) continue;
+          BufferDesc sh = sb;
+          sh.id = static_cast<int>(P.buffers.size());
+          sh.lane = in.lane;
+          sh.graph_input = false;
+          sh.weight = false;
+          sh.producer = -1;
+          sh.offset = P.lane_arena_bytes[in.lane];
+          P.lane_arena_bytes[in.lane] += (sh.bytes + 255) / 256 * 256;
+          P.buffers.push_back(sh);
+          shadow[key] = sh.id;
+          Xfer xf;
+          xf.src = t.buffer;
+          xf.dst = sh.id;
+          xf.src_lane = sb.lane;
+          xf.dst_lane = in.lane;
+          xf.bytes = sb.bytes;
+          x.xfers.push_back(xf);
+          x.in_bufs.push_back(t.buffer);
+          x.out_bufs.push_back(sh.id);
+          x.wire_bytes += static_cast<double>(sb.bytes);
+          if (sb.producer >= 0 && remap[sb.producer] >= 0) xdeps.insert(remap[sb.producer]);
+        }
+      }
+    }
+    int xid = -1;
+    if (!x.xfers.empty()) {
+      x.deps.assign(xdeps.begin(), xdeps.end());
+      xid = push(std::move(x));
+      for (int b : P.instrs[xid].out_bufs) P.buffers[b].producer = xid;
+    }
+    for (int id : grp) {
+      Instr in = g.instrs[id];
+      std::set<int> deps;
+      for (int d : in.deps)
+        if (remap[d] >= 0) deps.insert(remap[d]);
+      if (in.kind == InstrKind::box) {
+        bool used_shadow = false;
+        std::set<int> ins;
+        for (auto& c : in.cells) {
+          for (auto& t : c.terms) {
+            auto it = shadow.find({t.buffer, in.lane});
+            if (owner(P.buffers[t.buffer].lane) != owner(in.lane) && it != shadow.end()) {
+              t.buffer = it->second;
+              used_shadow = true;
+            }
+            ins.insert(t.buffer);
+          }
+        }
+        in.in_bufs.assign(ins.begin(), ins.end());
+        if (used_shadow) deps.insert(xid);
+      }
+      in.deps.assign(deps.begin(), deps.end());
+      int nid = push(std::move(in));
+      remap[id] = nid;
+      for (int b : P.instrs[nid].out_bufs) P.buffers[b].producer = nid;
+    }
+    i += grp.size();
+  }
+  return P;
+}
+
 std::string Program::describe_json() const {
   std::ostringstream os;
   os << "{\"num_lanes\":" << num_lanes << ",\"lane_device\":[";
@@ -749,7 +859,14 @@ std::string Program::describe_json() const {
        << ",\"ew\":" << static_cast<int>(in.ew) << ",\"count\":" << in.count << ",\"outer\":" << in.outer
        << ",\"axis_len\":" << in.axis_len << ",\"inner\":" << in.inner << ",\"n_idx\":" << in.n_idx
        << ",\"rows\":" << in.rows << ",\"h\":" << in.h << ",\"lo\":" << in.lo << ",\"flops\":" << in.flops
-       << ",\"bytes\":" << in.bytes << ",\"wire_bytes\":" << in.wire_bytes << ",\"cells\":[";
+       << ",\"bytes\":" << in.bytes << ",\"wire_bytes\":" << in.wire_bytes << ",\"coll_group\":" << in.coll_group
+       << ",\"xfers\":[";
+    for (std::size_t x = 0; x < in.xfers.size(); ++x) {
+      const auto& xf = in.xfers[x];
+      os << (x ? "," : "") << "{\"src\":" << xf.src << ",\"dst\":" << xf.dst << ",\"src_lane\":" << xf.src_lane
+         << ",\"dst_lane\":" << xf.dst_lane << ",\"bytes\":" << xf.bytes << "}";
+    }
+    os << "],\"cells\":[";
     for (std::size_t c = 0; c < in.cells.size(); ++c) {
       const auto& cl = in.cells[c];
       os << (c ? "," : "") << "{\"rank\":" << cl.rank << ",\"ext\":[";

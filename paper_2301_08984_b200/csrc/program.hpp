@@ -73,7 +73,18 @@ struct Cell {
   }
 };
 
-enum class InstrKind { gemm, ew, reduce, emb_lookup, emb_grad, box, nop };
+enum class InstrKind { gemm, ew, reduce, emb_lookup, emb_grad, box, xfer, nop };
+
+// One cross-rank piece movement of an exchange step (one-process-per-GPU
+// mode): the whole `src` buffer of lane src_lane lands in `dst` (a shadow
+// buffer on dst_lane) before the box program that reads it.
+struct Xfer {
+  int src = 0;
+  int dst = 0;
+  int src_lane = 0;
+  int dst_lane = 0;
+  std::int64_t bytes = 0;
+};
 const char* instr_kind_name(InstrKind k);
 
 enum class EwOp { add = 0, mul = 1, max = 2 };
@@ -99,6 +110,11 @@ struct Instr {
   std::int64_t n_idx = 0, rows = 0, h = 0, lo = 0;
   // box
   std::vector<Cell> cells;
+  int coll_group = -1;  // collective group a box instruction belongs to
+  // xfer (exchange step, identical on every rank): the movements, and the
+  // collective all-reduce fast path when the step is one whole-buffer
+  // all-reduce across ranks (allreduce_bufs[lane] = in, out pairs)
+  std::vector<Xfer> xfers;
   // accounting (algorithmic, from masks)
   double flops = 0;
   double bytes = 0;       // HBM bytes read + written
@@ -133,6 +149,16 @@ struct Program {
 };
 
 Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt = {});
+
+// One-process-per-GPU lowering: the same global program on every rank, with
+// every box term that lives on another rank's lane redirected to a shadow
+// buffer on the consuming lane and filled by an `xfer` exchange step placed
+// just before its consumers in the global issue order (all box outputs of a
+// collective group share one step). Every rank derives the identical step
+// sequence, so the per-rank point-to-point groups are matched in order and
+// cannot deadlock. `lane_rank[l]` is the rank owning lane l; instructions of
+// lanes other ranks own stay in the program (the caller skips them).
+Program localize(const Program& global, const std::vector<int>& lane_rank);
 
 // Reconstruct-as-cells (refexec.cpp:102-140): target buffer box from ordered
 // pieces. Exposed for tests.

@@ -7,6 +7,8 @@
 #include <set>
 #include <stdexcept>
 
+#include "nccl_api.hpp"
+
 namespace planc_b200 {
 
 namespace {
@@ -85,23 +87,58 @@ struct DeviceGuard {
 
 }  // namespace
 
-Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gpu, const ExecOptions& opt)
+Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gpu, const ExecOptions& opt,
+                   const RankConfig* rank)
     : opt_(opt) {
   plan_ = load_plan(plan_json);
   ProgramOptions po;
   po.value_split_extension = opt.value_split_extension;
   prog_ = build_program(plan_, po);
+  if (rank) {
+    rank_mode_ = true;
+    rc_ = *rank;
+    if (rc_.world < 1 || rc_.rank < 0 || rc_.rank >= rc_.world) throw UsageError("bad rank / world");
+    for (int r : rc_.lane_rank) {
+      if (r < 0 || r >= rc_.world) throw UsageError("lane_rank entry outside [0, world)");
+    }
+    prog_ = localize(prog_, rc_.lane_rank);
+  }
   int ndev = 0;
   ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
   lanes_.resize(prog_.num_lanes);
+  owned_.assign(prog_.num_lanes, true);
   std::set<int> gset;
   for (int l = 0; l < prog_.num_lanes; ++l) {
-    int g = lane_gpu.empty() ? 0 : lane_gpu[l % lane_gpu.size()];
+    int g = rank_mode_ ? rc_.local_gpu : lane_gpu.empty() ? 0 : lane_gpu[l % lane_gpu.size()];
     if (g < 0 || g >= ndev) throw UsageError("lane " + std::to_string(l) + " mapped to missing GPU " + std::to_string(g));
     lanes_[l].gpu = g;
-    gset.insert(g);
+    if (rank_mode_) owned_[l] = rc_.lane_rank[l] == rc_.rank;
+    if (owned_[l]) gset.insert(g);
   }
+  if (gset.empty()) throw UsageError("this rank owns no plan lane");
   gpus_.assign(gset.begin(), gset.end());
+  // Which lane's streams run each instruction in this process.
+  exec_lane_.assign(prog_.instrs.size(), -1);
+  for (const auto& in : prog_.instrs) {
+    if (in.kind != InstrKind::xfer) {
+      if (owned_[in.lane]) exec_lane_[in.id] = in.lane;
+      continue;
+    }
+    for (const auto& x : in.xfers) {
+      if (owned_[x.src_lane] != owned_[x.dst_lane]) {
+        exec_lane_[in.id] = owned_[x.src_lane] ? x.src_lane : x.dst_lane;
+        break;
+      }
+    }
+  }
+  if (rank_mode_) {
+    DeviceGuard dg(rc_.local_gpu);
+    ncclUniqueId id;
+    std::memcpy(id.internal, rc_.nccl_id, sizeof(id.internal));
+    ncclComm_t c = nullptr;
+    nccl_check(nccl().comm_init_rank(&c, rc_.world, id, rc_.rank), "ncclCommInitRank");
+    comm_ = c;
+  }
   // Lanes on different GPUs read each other's buffers through NVLink peer
   // mappings inside the box kernels.
   for (int a : gpus_) {
@@ -117,13 +154,20 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
     }
   }
   for (int l = 0; l < prog_.num_lanes; ++l) {
+    if (!owned_[l]) continue;
     DeviceGuard dg(lanes_[l].gpu);
     std::int64_t bytes = std::max<std::int64_t>(prog_.lane_arena_bytes[l], 256);
     ck(cudaMalloc(&lanes_[l].arena, bytes), "cudaMalloc(arena)");
     for (auto& s : lanes_[l].stream) ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
   }
+  for (int l = 0; l < prog_.num_lanes; ++l) {
+    if (owned_[l]) {
+      first_lane_ = l;
+      break;
+    }
+  }
   {
-    DeviceGuard dg(lanes_.empty() ? 0 : lanes_[0].gpu);
+    DeviceGuard dg(lanes_[first_lane_].gpu);
     ck(cudaStreamCreateWithFlags(&origin_, cudaStreamNonBlocking), "origin stream");
     ck(cudaEventCreateWithFlags(&ev_begin_, cudaEventDisableTiming), "event");
     ck(cudaEventCreate(&ev_end_), "event");
@@ -131,8 +175,8 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   for (int l = 0; l < prog_.num_lanes; ++l) {
     DeviceGuard dg(lanes_[l].gpu);
     for (int s = 0; s < 2; ++s) {
-      cudaEvent_t e;
-      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      cudaEvent_t e = nullptr;
+      if (owned_[l]) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
       lane_join_.push_back(e);
     }
   }
@@ -150,10 +194,12 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   // Events for producer -> consumer edges that cross streams.
   irt_.resize(prog_.instrs.size());
   for (const auto& in : prog_.instrs) {
+    if (exec_lane_[in.id] < 0) continue;
     for (int d : in.deps) {
       const Instr& p = prog_.instrs[d];
-      if ((p.lane != in.lane || p.stream != in.stream) && !irt_[d].done) {
-        DeviceGuard dg(lanes_[p.lane].gpu);
+      if (exec_lane_[d] < 0) continue;  // ordered by the exchange step instead
+      if ((exec_lane_[d] != exec_lane_[in.id] || p.stream != in.stream) && !irt_[d].done) {
+        DeviceGuard dg(lanes_[exec_lane_[d]].gpu);
         ck(cudaEventCreateWithFlags(&irt_[d].done, cudaEventDisableTiming), "event");
       }
     }
@@ -165,6 +211,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   build_box_tables();
   kernels_per_step_ = 0;
   for (const auto& in : prog_.instrs) {
+    if (exec_lane_[in.id] < 0) continue;
     switch (in.kind) {
       case InstrKind::nop: break;
       case InstrKind::box: kernels_per_step_ += static_cast<int>(irt_[in.id].box.size()); break;
@@ -199,7 +246,9 @@ Executor::~Executor() {
     if (r.scratch) cudaFree(r.scratch);
   }
   for (void* p : table_allocs_) cudaFree(p);
-  for (auto e : lane_join_) cudaEventDestroy(e);
+  for (auto e : lane_join_)
+    if (e) cudaEventDestroy(e);
+  if (comm_) nccl().comm_destroy(static_cast<ncclComm_t>(comm_));
   for (void* p : pinned_in_) cudaFreeHost(p);
   for (void* p : pinned_out_) cudaFreeHost(p);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
@@ -214,12 +263,35 @@ void* Executor::buf_ptr(int b) const {
   return lanes_[d.lane].arena + d.offset;
 }
 
-cudaStream_t Executor::stream_of(const Instr& in) const { return lanes_[in.lane].stream[in.stream]; }
+cudaStream_t Executor::stream_of(const Instr& in) const {
+  return lanes_[exec_lane_[in.id]].stream[in.stream];
+}
+
+// One exchange step: this rank's sends and receives of the step, grouped so
+// NCCL posts them together (every rank walks the same step sequence).
+void Executor::launch_xfer(const Instr& in, cudaStream_t s) {
+  const NcclApi& api = nccl();
+  ncclComm_t comm = static_cast<ncclComm_t>(comm_);
+  nccl_check(api.group_start(), "ncclGroupStart");
+  for (const auto& x : in.xfers) {
+    bool src_here = owned_[x.src_lane], dst_here = owned_[x.dst_lane];
+    if (src_here && !dst_here) {
+      nccl_check(api.send(buf_ptr(x.src), static_cast<std::size_t>(x.bytes), ncclUint8, rc_.lane_rank[x.dst_lane], comm,
+                          s),
+                 "ncclSend");
+    } else if (dst_here && !src_here) {
+      nccl_check(api.recv(buf_ptr(x.dst), static_cast<std::size_t>(x.bytes), ncclUint8, rc_.lane_rank[x.src_lane], comm,
+                          s),
+                 "ncclRecv");
+    }
+  }
+  nccl_check(api.group_end(), "ncclGroupEnd");
+}
 
 void Executor::build_box_tables() {
   constexpr std::int64_t kChunkUnits = 4096;
   for (const auto& in : prog_.instrs) {
-    if (in.kind != InstrKind::box) continue;
+    if (in.kind != InstrKind::box || exec_lane_[in.id] < 0) continue;
     const BufferDesc& ob = prog_.buffers[in.out_bufs[0]];
     const std::int64_t V = 16 / dtype_size(ob.dtype);
     std::vector<const Cell*> groups[2];
@@ -305,7 +377,7 @@ void Executor::set_input(int ptensor, const double* data, const std::vector<std:
 void Executor::place_inputs() {
   if (!inputs_dirty_) return;
   for (const auto& b : prog_.buffers) {
-    if (!b.graph_input) continue;
+    if (!b.graph_input || !owned_[b.lane]) continue;
     auto it = inputs_.find(b.ptensor);
     if (it == inputs_.end()) throw UsageError("run_plan: missing input tensor " + std::to_string(b.ptensor));
     const PTensor& pt = plan_.pt(b.ptensor);
@@ -335,6 +407,9 @@ void Executor::place_inputs() {
 void Executor::launch_instr(const Instr& in, cudaStream_t s) {
   switch (in.kind) {
     case InstrKind::nop:
+      return;
+    case InstrKind::xfer:
+      launch_xfer(in, s);
       return;
     case InstrKind::gemm: {
       GemmArgs a{};
@@ -398,36 +473,38 @@ void Executor::issue_step(bool, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>
     }
     cur = g;
   };
-  set_dev(lanes_[0].gpu);
+  set_dev(lanes_[first_lane_].gpu);
   ck(cudaEventRecord(ev_begin_, origin_), "record begin");
-  for (auto& l : lanes_)
-    for (auto s : l.stream) ck(cudaStreamWaitEvent(s, ev_begin_, 0), "wait begin");
+  for (int l = 0; l < prog_.num_lanes; ++l)
+    if (owned_[l])
+      for (auto s : lanes_[l].stream) ck(cudaStreamWaitEvent(s, ev_begin_, 0), "wait begin");
   for (int id : prog_.issue_order) {
+    const int el = exec_lane_[id];
+    if (el < 0) continue;  // another rank's instruction
     const Instr& in = prog_.instrs[id];
     cudaStream_t s = stream_of(in);
-    set_dev(lanes_[in.lane].gpu);
+    set_dev(lanes_[el].gpu);
     for (int d : in.deps) {
+      if (exec_lane_[d] < 0) continue;
       const Instr& p = prog_.instrs[d];
-      if (p.lane != in.lane || p.stream != in.stream) ck(cudaStreamWaitEvent(s, irt_[d].done, 0), "wait dep");
+      if (exec_lane_[d] != el || p.stream != in.stream) ck(cudaStreamWaitEvent(s, irt_[d].done, 0), "wait dep");
     }
     launch_instr(in, s);
     if (irt_[id].done) ck(cudaEventRecord(irt_[id].done, s), "record done");
   }
-  int j = 0;
-  for (auto& l : lanes_) {
-    set_dev(l.gpu);
-    for (auto s : l.stream) {
-      ck(cudaEventRecord(lane_join_[j], s), "record join");
-      ++j;
-    }
+  for (int l = 0; l < prog_.num_lanes; ++l) {
+    if (!owned_[l]) continue;
+    set_dev(lanes_[l].gpu);
+    for (int k = 0; k < 2; ++k) ck(cudaEventRecord(lane_join_[2 * l + k], lanes_[l].stream[k]), "record join");
   }
-  set_dev(lanes_[0].gpu);
-  for (auto e : lane_join_) ck(cudaStreamWaitEvent(origin_, e, 0), "wait join");
+  set_dev(lanes_[first_lane_].gpu);
+  for (auto e : lane_join_)
+    if (e) ck(cudaStreamWaitEvent(origin_, e, 0), "wait join");
 }
 
 void Executor::ensure_graph() {
   if (!opt_.use_graph || graph_exec_) return;
-  DeviceGuard dg(lanes_[0].gpu);
+  DeviceGuard dg(lanes_[first_lane_].gpu);
   ck(cudaStreamBeginCapture(origin_, cudaStreamCaptureModeThreadLocal), "begin capture");
   bool ok = true;
   try {
@@ -457,7 +534,7 @@ void Executor::ensure_graph() {
 double Executor::run(int iters) {
   place_inputs();
   ensure_graph();
-  DeviceGuard dg(lanes_[0].gpu);
+  DeviceGuard dg(lanes_[first_lane_].gpu);
   auto step = [&]() {
     if (graph_exec_) ck(cudaGraphLaunch(graph_exec_, origin_), "graph launch");
     else issue_step(false, nullptr);
@@ -484,12 +561,12 @@ double Executor::run(int iters) {
 double Executor::run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_bytes) {
   place_inputs();
   ensure_graph();
-  DeviceGuard dg(lanes_[0].gpu);
+  DeviceGuard dg(lanes_[first_lane_].gpu);
   if (pinned_in_.empty() && pinned_out_.empty()) {
     // Step inputs: non-weight graph-input placements, staged from pinned host
     // memory in device element type (weights stay resident, like a trainer).
     for (const auto& b : prog_.buffers) {
-      if (!b.graph_input || b.weight) continue;
+      if (!b.graph_input || b.weight || !owned_[b.lane]) continue;
       void* h = nullptr;
       ck(cudaMallocHost(&h, std::max<std::int64_t>(b.bytes, 1)), "cudaMallocHost");
       ck(cudaMemcpy(h, buf_ptr(b.id), b.bytes, cudaMemcpyDeviceToHost), "stage input");
@@ -505,6 +582,7 @@ double Executor::run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_b
       TensorKind k = plan_.pt(pt).kind;
       if (consumed.count(pt) || k == TensorKind::weight || k == TensorKind::optimizer_state) continue;
       for (int b : bufs) {
+        if (!local(b)) continue;
         void* h = nullptr;
         ck(cudaMallocHost(&h, std::max<std::int64_t>(prog_.buffers[b].bytes, 1)), "cudaMallocHost");
         pinned_out_.push_back(h);
@@ -551,14 +629,15 @@ std::vector<KernelStat> Executor::profile() {
   std::vector<std::string> order;
   for (int id : prog_.issue_order) {
     const Instr& in = prog_.instrs[id];
-    if (in.kind == InstrKind::nop) continue;
-    DeviceGuard dg(lanes_[in.lane].gpu);
-    cudaStream_t s = lanes_[in.lane].stream[0];
-    for (auto& l : lanes_) {
-      cudaSetDevice(l.gpu);
+    const int el = exec_lane_[id];
+    if (in.kind == InstrKind::nop || el < 0) continue;
+    DeviceGuard dg(lanes_[el].gpu);
+    cudaStream_t s = lanes_[el].stream[0];
+    for (int g : gpus_) {
+      cudaSetDevice(g);
       ck(cudaDeviceSynchronize(), "profile sync");
     }
-    cudaSetDevice(lanes_[in.lane].gpu);
+    cudaSetDevice(lanes_[el].gpu);
     cudaEvent_t a, b;
     ck(cudaEventCreate(&a), "event");
     ck(cudaEventCreate(&b), "event");
@@ -589,6 +668,7 @@ std::vector<KernelStat> Executor::profile() {
       case InstrKind::reduce: kind = "reduce"; break;
       case InstrKind::emb_lookup:
       case InstrKind::emb_grad: kind = "embedding"; break;
+      case InstrKind::xfer: kind = "xfer_nccl"; break;
       case InstrKind::box:
         // Collective member outputs are labelled "<primitive>:<op>".
         kind = in.label.find(':') != std::string::npos ? "box_collective"
@@ -616,9 +696,10 @@ std::vector<KernelStat> Executor::profile() {
 std::vector<double> Executor::read_buffer(int buffer) {
   if (buffer < 0 || buffer >= static_cast<int>(prog_.buffers.size())) throw UsageError("no such buffer");
   const BufferDesc& bd = prog_.buffers[buffer];
+  if (!owned_[bd.lane]) throw UsageError("buffer " + std::to_string(buffer) + " lives on another rank");
   DeviceGuard dg(lanes_[bd.lane].gpu);
-  for (auto& l : lanes_) {
-    cudaSetDevice(l.gpu);
+  for (int g : gpus_) {
+    cudaSetDevice(g);
     ck(cudaDeviceSynchronize(), "sync before readback");
   }
   cudaSetDevice(lanes_[bd.lane].gpu);
@@ -657,6 +738,9 @@ HostTensor Executor::get_output(int ptensor) {
   std::map<int, std::vector<char>> raw;
   for (int b : *bufs) {
     const BufferDesc& bd = prog_.buffers[b];
+    if (!owned_[bd.lane]) {
+      throw UsageError("ptensor " + std::to_string(ptensor) + " has pieces on another rank; read buffers instead");
+    }
     pieces.push_back({&bd.mask, b});
     std::vector<char> r(bd.bytes);
     DeviceGuard dg(lanes_[bd.lane].gpu);

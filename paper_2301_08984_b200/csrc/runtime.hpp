@@ -44,9 +44,21 @@ struct ExecOptions {
   bool value_split_extension = true;
 };
 
+// One-process-per-GPU mode: this process owns the lanes with
+// lane_rank[l] == rank, all on `local_gpu`; pieces owned by other ranks
+// arrive through NCCL point-to-point exchange steps (program.hpp localize).
+struct RankConfig {
+  int rank = 0;
+  int world = 1;
+  std::vector<int> lane_rank;
+  int local_gpu = 0;
+  unsigned char nccl_id[128] = {0};
+};
+
 class Executor {
  public:
-  Executor(const std::string& plan_json, const std::vector<int>& lane_gpu, const ExecOptions& opt);
+  Executor(const std::string& plan_json, const std::vector<int>& lane_gpu, const ExecOptions& opt,
+           const RankConfig* rank = nullptr);
   ~Executor();
   Executor(const Executor&) = delete;
   Executor& operator=(const Executor&) = delete;
@@ -99,9 +111,18 @@ class Executor {
   void launch_instr(const Instr& in, cudaStream_t s);
   void ensure_graph();
 
+  bool local(int buffer) const { return owned_[prog_.buffers[buffer].lane]; }
+  void launch_xfer(const Instr& in, cudaStream_t s);
+
   ExecutionPlan plan_;
   Program prog_;
   ExecOptions opt_;
+  bool rank_mode_ = false;
+  RankConfig rc_;
+  std::vector<bool> owned_;     // per lane: runs in this process
+  std::vector<int> exec_lane_;  // per instruction: lane whose streams run it here (-1: elsewhere)
+  void* comm_ = nullptr;        // ncclComm_t in rank mode
+  int first_lane_ = 0;          // first lane this process runs (origin stream's device)
   std::vector<LaneRt> lanes_;
   std::vector<InstrRt> irt_;
   std::vector<int> gpus_;  // distinct devices

@@ -20,15 +20,19 @@ def _strided_view(flat, offset, strides, extents):
     return idx
 
 
-def run_program(desc: dict, plan: dict, inputs: dict) -> dict:
+def run_program(desc: dict, plan: dict, inputs: dict, owned_lanes=None, exchange=None, return_buffers=False):
+    """Interpret the lowered program. With ``owned_lanes`` only those lanes'
+    instructions run (one rank of the one-process-per-GPU mode) and ``xfer``
+    exchange steps call ``exchange(instr, data)`` to move cross-rank pieces."""
     bufs = {b["id"]: b for b in desc["buffers"]}
+    lane_ok = (lambda lane: True) if owned_lanes is None else (lambda lane: lane in owned_lanes)
     data = {}
     for b in desc["buffers"]:
         n = 1
         for lo, hi in b["region"]:
             n *= hi - lo
         data[b["id"]] = np.zeros(n)
-        if b["graph_input"]:
+        if b["graph_input"] and lane_ok(b["lane"]):
             x = np.asarray(inputs[b["pt"]], dtype=np.float64)
             sl = tuple(slice(lo, hi) for lo, hi in b["region"])
             data[b["id"]] = x[sl].reshape(-1).copy()
@@ -36,6 +40,15 @@ def run_program(desc: dict, plan: dict, inputs: dict) -> dict:
     for iid in desc["issue_order"]:
         ins = desc["instrs"][iid]
         k = ins["kind"]
+        if k == "xfer":
+            if exchange is not None:
+                exchange(ins, data)
+            else:  # single process: the movement is a plain copy
+                for x in ins["xfers"]:
+                    data[x["dst"]] = data[x["src"]].copy()
+            continue
+        if not lane_ok(ins["lane"]):
+            continue
         if k == "gemm":
             a = data[ins["in"][0]].reshape(shape[ins["in"][0]])
             b = data[ins["in"][1]].reshape(shape[ins["in"][1]])
@@ -76,6 +89,15 @@ def run_program(desc: dict, plan: dict, inputs: dict) -> dict:
                     v = v + data[t["buf"]][si] if t["add"] else data[t["buf"]][si].copy()
                 out[di] = v
             data[ob] = out
+    if return_buffers:
+        return data
+    return reassemble(desc, plan, data)
+
+
+def reassemble(desc: dict, plan: dict, data: dict) -> dict:
+    """refexec.cpp:532-556 over the (gathered) buffer values."""
+    bufs = {b["id"]: b for b in desc["buffers"]}
+    shape = {b["id"]: [hi - lo for lo, hi in b["region"]] for b in desc["buffers"]}
     outputs = {}
     for pt, blist in desc["outputs"]:
         full_shape = next(p["shape"] for p in plan["ptensors"] if p["id"] == pt)

@@ -93,6 +93,20 @@ def test_e2e_counts_bytes():
     assert ok, msg
 
 
+@pytest.mark.parametrize("name", ["gpt_block_tp2", "mlp_1f1b_dp2", "embed_shard2"])
+def test_rank_mode_single_rank(name):
+    """One-process-per-GPU entry point (NCCL communicator, world = 1)."""
+    g = golden_cases.load(name)
+    n = len(json.loads(g["plan"])["lanes"])
+    with pb.Executor(g["plan"], rank=0, world=1, lane_rank=[0] * n, local_gpu=0,
+                     nccl_id=pb.nccl_unique_id()) as ex:
+        ex.set_inputs(g["inputs"])
+        ex.run(2)
+        out = ex.outputs()
+    ok, msg = pb.compare_outputs(g["expected"], out, g["meta"]["rel_tol"], normwise=True)
+    assert ok, msg
+
+
 def test_profile_reports_kernel_families():
     g = golden_cases.load("gpt_block_tp2")
     with pb.Executor(g["plan"], lane_gpus=[0, 0]) as ex:
