@@ -91,118 +91,124 @@ __device__ __forceinline__ void store_any(void* p, int dt, std::int64_t i, float
 }
 
 // ---- box: fused reconstruct -------------------------------------------------
+// One block per chunk of kBoxThreads*kBoxUnroll vector units of one cell;
+// every thread owns kBoxUnroll independent 16-byte vectors (all terms' loads
+// in flight before any store). R = highest cell rank of the launch, so the
+// common rank-1/2 cells carry no unused coordinates. Cell and term records
+// are read through the read-only path (warp-uniform broadcasts); no smem,
+// no barriers.
 
 constexpr int kBoxThreads = 256;
-constexpr int kSmemTerms = 32;
 constexpr int kBoxUnroll = 4;
 
-template <typename T, int V>
+template <typename T, int V, int R>
 __global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, const DevCell* __restrict__ cells,
                                                            const DevTerm* __restrict__ terms,
                                                            const DevChunk* __restrict__ chunks) {
   using A = typename Acc<T>::type;
-  __shared__ DevCell sc;
-  __shared__ DevTerm st[kSmemTerms];
+  constexpr int U = kBoxUnroll;
   const DevChunk ch = chunks[blockIdx.x];
-  if (threadIdx.x == 0) sc = cells[ch.cell];
-  __syncthreads();
-  const int nt = sc.nterms;
-  for (int i = threadIdx.x; i < nt && i < kSmemTerms; i += blockDim.x) st[i] = terms[sc.term0 + i];
-  __syncthreads();
-  const int rank = sc.rank;
-  const std::int64_t inner_vecs = sc.ext[rank - 1] / V;
-  const bool small = sc.elems / V < (std::int64_t(1) << 32);
-  constexpr int U = kBoxUnroll;  // independent vectors in flight per thread
-  for (std::int64_t u0 = threadIdx.x; u0 < ch.count; u0 += static_cast<std::int64_t>(blockDim.x) * U) {
-    std::int64_t coord[U][kBoxRank];
-    bool live[U];
+  const DevCell* c = cells + ch.cell;
+  const int rank = __ldg(&c->rank);
+  const int nt = __ldg(&c->nterms);
+  const int term0 = __ldg(&c->term0);
+  std::int64_t ext[R], dstr[R];
 #pragma unroll
-    for (int x = 0; x < U; ++x) {
-      const std::int64_t u = u0 + static_cast<std::int64_t>(x) * blockDim.x;
-      live[x] = u < ch.count;
-      std::int64_t lin = ch.begin + (live[x] ? u : 0);
-      // Static indices only (keeps coord in registers). Rank-1 cells (the
-      // common case after dim collapsing) need no division; others use
-      // 32-bit division when the cell fits.
+  for (int d = 0; d < R; ++d) {
+    ext[d] = d < rank ? __ldg(&c->ext[d]) : 1;
+    dstr[d] = d < rank ? __ldg(&c->dst_str[d]) : 0;
+  }
+  const std::int64_t dst_off = __ldg(&c->dst_off);
+  std::int64_t inner_ext = ext[0];
 #pragma unroll
-      for (int d = 0; d < kBoxRank; ++d) coord[x][d] = 0;
-      if (rank == 1) {
-        coord[x][0] = lin * V;
-      } else if (small) {
-        std::uint32_t l32 = static_cast<std::uint32_t>(lin);
-        const std::uint32_t iv = static_cast<std::uint32_t>(inner_vecs);
+  for (int d = 1; d < R; ++d)
+    if (d == rank - 1) inner_ext = ext[d];  // static indices keep ext[] in registers
+  const std::int64_t inner_vecs = inner_ext / V;
+  std::int64_t coord[U][R];
+  bool live[U];
 #pragma unroll
-        for (int d = kBoxRank - 1; d >= 0; --d) {
-          if (d == rank - 1) {
-            coord[x][d] = static_cast<std::int64_t>(l32 % iv) * V;
-            l32 /= iv;
-          } else if (d < rank - 1) {
-            const std::uint32_t e = static_cast<std::uint32_t>(sc.ext[d]);
-            coord[x][d] = l32 % e;
-            l32 /= e;
-          }
-        }
-      } else {
+  for (int x = 0; x < U; ++x) {
+    const std::int64_t u = threadIdx.x + static_cast<std::int64_t>(x) * kBoxThreads;
+    live[x] = u < ch.count;
+    std::int64_t lin = ch.begin + (live[x] ? u : 0);
 #pragma unroll
-        for (int d = kBoxRank - 1; d >= 0; --d) {
-          if (d == rank - 1) {
-            coord[x][d] = (lin % inner_vecs) * V;
-            lin /= inner_vecs;
-          } else if (d < rank - 1) {
-            coord[x][d] = lin % sc.ext[d];
-            lin /= sc.ext[d];
-          }
+    for (int d = 0; d < R; ++d) coord[x][d] = 0;
+    if (R == 1 || rank == 1) {
+      coord[x][0] = lin * V;
+    } else {
+      // 32-bit division: chunk tables are built only for cells < 2^32 units.
+      std::uint32_t l32 = static_cast<std::uint32_t>(lin);
+      const std::uint32_t iv = static_cast<std::uint32_t>(inner_vecs);
+#pragma unroll
+      for (int d = R - 1; d >= 0; --d) {
+        if (d == rank - 1) {
+          coord[x][d] = static_cast<std::int64_t>(l32 % iv) * V;
+          l32 /= iv;
+        } else if (d < rank - 1) {
+          const std::uint32_t e = static_cast<std::uint32_t>(ext[d]);
+          coord[x][d] = l32 % e;
+          l32 /= e;
         }
       }
-    }
-    A acc[U][V];
-#pragma unroll
-    for (int x = 0; x < U; ++x)
-#pragma unroll
-      for (int i = 0; i < V; ++i) acc[x][i] = A(0);
-    for (int t = 0; t < nt; ++t) {
-      const DevTerm& tm = t < kSmemTerms ? st[t] : terms[sc.term0 + t];
-      A v[U][V];
-#pragma unroll
-      for (int x = 0; x < U; ++x) {
-        std::int64_t soff = tm.offset;
-#pragma unroll
-        for (int d = 0; d < kBoxRank; ++d)
-          if (d < rank) soff += coord[x][d] * tm.str[d];
-        if (live[x]) load_vec<T, V>(reinterpret_cast<const T*>(tm.src) + soff, v[x]);
-      }
-#pragma unroll
-      for (int x = 0; x < U; ++x) {
-        if (tm.add) {
-#pragma unroll
-          for (int i = 0; i < V; ++i) acc[x][i] += v[x][i];
-        } else {
-#pragma unroll
-          for (int i = 0; i < V; ++i) acc[x][i] = v[x][i];
-        }
-      }
-    }
-#pragma unroll
-    for (int x = 0; x < U; ++x) {
-      if (!live[x]) continue;
-      std::int64_t doff = sc.dst_off;
-#pragma unroll
-      for (int d = 0; d < kBoxRank; ++d)
-        if (d < rank) doff += coord[x][d] * sc.dst_str[d];
-      store_vec<T, V>(dst + doff, acc[x]);
     }
   }
+  A acc[U][V];
+#pragma unroll
+  for (int x = 0; x < U; ++x)
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[x][i] = A(0);
+  for (int t = 0; t < nt; ++t) {
+    const DevTerm* tm = terms + term0 + t;
+    const T* src = reinterpret_cast<const T*>(__ldg(reinterpret_cast<const unsigned long long*>(&tm->src)));
+    const std::int64_t toff = __ldg(&tm->offset);
+    const int add = __ldg(&tm->add);
+    std::int64_t tstr[R];
+#pragma unroll
+    for (int d = 0; d < R; ++d) tstr[d] = d < rank ? __ldg(&tm->str[d]) : 0;
+    A v[U][V];
+#pragma unroll
+    for (int x = 0; x < U; ++x) {
+      std::int64_t soff = toff;
+#pragma unroll
+      for (int d = 0; d < R; ++d) soff += coord[x][d] * tstr[d];
+      if (live[x]) load_vec<T, V>(src + soff, v[x]);
+    }
+#pragma unroll
+    for (int x = 0; x < U; ++x) {
+      if (add) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[x][i] += v[x][i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[x][i] = v[x][i];
+      }
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < U; ++x) {
+    if (!live[x]) continue;
+    std::int64_t doff = dst_off;
+#pragma unroll
+    for (int d = 0; d < R; ++d) doff += coord[x][d] * dstr[d];
+    store_vec<T, V>(dst + doff, acc[x]);
+  }
+}
+
+template <typename T, int V>
+void box_rank_dispatch(void* dst, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks,
+                       int max_rank, cudaStream_t s) {
+  T* d = static_cast<T*>(dst);
+  if (max_rank <= 1) box_kernel<T, V, 1><<<nchunks, kBoxThreads, 0, s>>>(d, cells, terms, chunks);
+  else if (max_rank == 2) box_kernel<T, V, 2><<<nchunks, kBoxThreads, 0, s>>>(d, cells, terms, chunks);
+  else box_kernel<T, V, kBoxRank><<<nchunks, kBoxThreads, 0, s>>>(d, cells, terms, chunks);
 }
 
 template <typename T>
 void box_dispatch(void* dst, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks, int vec,
-                  cudaStream_t s) {
+                  int max_rank, cudaStream_t s) {
   constexpr int VV = 16 / sizeof(T);
-  if (vec) {
-    box_kernel<T, VV><<<nchunks, kBoxThreads, 0, s>>>(static_cast<T*>(dst), cells, terms, chunks);
-  } else {
-    box_kernel<T, 1><<<nchunks, kBoxThreads, 0, s>>>(static_cast<T*>(dst), cells, terms, chunks);
-  }
+  if (vec) box_rank_dispatch<T, VV>(dst, cells, terms, chunks, nchunks, max_rank, s);
+  else box_rank_dispatch<T, 1>(dst, cells, terms, chunks, nchunks, max_rank, s);
 }
 
 // ---- elementwise -----------------------------------------------------------
@@ -274,7 +280,8 @@ void ew_typed(const void* const* ins, int nin, void* out, std::int64_t count, cu
   }
   std::int64_t nvec = aligned ? count / V : 0;
   if (nvec > 0) {
-    ew_kernel<T, OP><<<grid_for(nvec, 256 * kEwUnroll, 148 * 8), 256, 0, s>>>(p, nin, static_cast<T*>(out), nvec);
+    // One pass: every thread owns kEwUnroll vectors (no grid-stride tail).
+    ew_kernel<T, OP><<<grid_for(nvec, 256 * kEwUnroll, 1 << 30), 256, 0, s>>>(p, nin, static_cast<T*>(out), nvec);
   }
   std::int64_t rest = count - nvec * V;
   if (rest > 0) {
@@ -431,12 +438,12 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs a) {
 }  // namespace
 
 void launch_box(void* dst, int dtype, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks,
-                int vec, cudaStream_t s) {
+                int vec, int max_rank, cudaStream_t s) {
   if (nchunks == 0) return;
   switch (dtype) {
-    case DT_F32: box_dispatch<float>(dst, cells, terms, chunks, nchunks, vec, s); break;
-    case DT_BF16: box_dispatch<__nv_bfloat16>(dst, cells, terms, chunks, nchunks, vec, s); break;
-    case DT_I32: box_dispatch<int>(dst, cells, terms, chunks, nchunks, vec, s); break;
+    case DT_F32: box_dispatch<float>(dst, cells, terms, chunks, nchunks, vec, max_rank, s); break;
+    case DT_BF16: box_dispatch<__nv_bfloat16>(dst, cells, terms, chunks, nchunks, vec, max_rank, s); break;
+    case DT_I32: box_dispatch<int>(dst, cells, terms, chunks, nchunks, vec, max_rank, s); break;
     default: throw std::runtime_error("box: bad dtype");
   }
   check_launch("box_kernel");

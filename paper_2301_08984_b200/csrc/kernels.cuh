@@ -62,8 +62,11 @@ struct GemmArgs {
 // `vec` != 0: every chunk's cell is innermost-contiguous with 16-byte
 // aligned offsets (the executor splits a box program into vector / scalar
 // launches).
+// `max_rank` is the highest cell rank in the launch; every chunk covers at
+// most kBoxChunkUnits vector units of one cell.
+constexpr int kBoxChunkUnits = 1024;
 void launch_box(void* dst, int dtype, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks,
-                int nchunks, int vec, cudaStream_t s);
+                int nchunks, int vec, int max_rank, cudaStream_t s);
 void launch_ew(int op, int dtype, const void* const* ins, int nin, void* out, std::int64_t count, cudaStream_t s);
 void launch_reduce(int dtype, const void* in, void* out, std::int64_t outer, std::int64_t axis_len,
                    std::int64_t inner, cudaStream_t s);

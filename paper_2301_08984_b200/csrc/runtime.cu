@@ -289,7 +289,7 @@ void Executor::launch_xfer(const Instr& in, cudaStream_t s) {
 }
 
 void Executor::build_box_tables() {
-  constexpr std::int64_t kChunkUnits = 4096;
+  constexpr std::int64_t kChunkUnits = kBoxChunkUnits;
   for (const auto& in : prog_.instrs) {
     if (in.kind != InstrKind::box || exec_lane_[in.id] < 0) continue;
     const BufferDesc& ob = prog_.buffers[in.out_bufs[0]];
@@ -310,6 +310,7 @@ void Executor::build_box_tables() {
       std::vector<DevCell> cells;
       std::vector<DevTerm> terms;
       std::vector<DevChunk> chunks;
+      int max_rank = 1;
       for (const Cell* c : groups[g]) {
         DevCell dc{};
         dc.rank = c->rank;
@@ -332,7 +333,9 @@ void Executor::build_box_tables() {
         }
         int ci = static_cast<int>(cells.size());
         cells.push_back(dc);
+        max_rank = std::max(max_rank, c->rank);
         std::int64_t units = dc.elems / width;
+        if (units >= (std::int64_t(1) << 32)) throw UsageError("adapter cell above 2^32 vector units");
         for (std::int64_t b = 0; b < units; b += kChunkUnits) {
           DevChunk ch{};
           ch.cell = ci;
@@ -357,6 +360,7 @@ void Executor::build_box_tables() {
       bl.chunks = reinterpret_cast<DevChunk*>(mem + cb + tb);
       bl.nchunks = static_cast<int>(chunks.size());
       bl.vec = g;
+      bl.max_rank = max_rank;
       irt_[in.id].box.push_back(bl);
     }
   }
@@ -458,7 +462,7 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
     case InstrKind::box: {
       int dt = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
       for (const auto& bl : irt_[in.id].box) {
-        launch_box(buf_ptr(in.out_bufs[0]), dt, bl.cells, bl.terms, bl.chunks, bl.nchunks, bl.vec, s);
+        launch_box(buf_ptr(in.out_bufs[0]), dt, bl.cells, bl.terms, bl.chunks, bl.nchunks, bl.vec, bl.max_rank, s);
       }
       return;
     }

@@ -96,6 +96,7 @@ class Executor {
     DevChunk* chunks = nullptr;
     int nchunks = 0;
     int vec = 0;
+    int max_rank = 1;
   };
   struct InstrRt {
     std::vector<BoxLaunch> box;
