@@ -53,15 +53,39 @@ __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(float v) {
 }
 
 // V consecutive elements (V*sizeof(T) = 16 bytes when V > 1).
+// Unpacking is done with shifts / bit casts on the loaded words (no
+// address-taken locals, so nothing is demoted to local memory).
+__device__ __forceinline__ void unpack_word(std::uint32_t w, float& lo, float& hi) {
+  lo = __uint_as_float(w << 16);
+  hi = __uint_as_float(w & 0xffff0000u);
+}
+__device__ __forceinline__ std::uint32_t pack_word(float lo, float hi) {
+  return static_cast<std::uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(lo))) |
+         (static_cast<std::uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(hi))) << 16);
+}
+
 template <typename T, int V>
 __device__ __forceinline__ void load_vec(const T* p, typename Acc<T>::type (&o)[V]) {
   if constexpr (V == 1) {
     o[0] = to_acc<T>(*p);
+  } else if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    uint4 r = __ldg(reinterpret_cast<const uint4*>(p));
+    unpack_word(r.x, o[0], o[1]);
+    unpack_word(r.y, o[2], o[3]);
+    unpack_word(r.z, o[4], o[5]);
+    unpack_word(r.w, o[6], o[7]);
+  } else if constexpr (std::is_same<T, float>::value) {
+    float4 r = __ldg(reinterpret_cast<const float4*>(p));
+    o[0] = r.x;
+    o[1] = r.y;
+    o[2] = r.z;
+    o[3] = r.w;
   } else {
-    uint4 raw = __ldg(reinterpret_cast<const uint4*>(p));
-    const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-    for (int i = 0; i < V; ++i) o[i] = to_acc<T>(e[i]);
+    int4 r = __ldg(reinterpret_cast<const int4*>(p));
+    o[0] = r.x;
+    o[1] = r.y;
+    o[2] = r.z;
+    o[3] = r.w;
   }
 }
 
@@ -69,12 +93,13 @@ template <typename T, int V>
 __device__ __forceinline__ void store_vec(T* p, const typename Acc<T>::type (&v)[V]) {
   if constexpr (V == 1) {
     *p = from_acc<T>(v[0]);
+  } else if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    *reinterpret_cast<uint4*>(p) =
+        make_uint4(pack_word(v[0], v[1]), pack_word(v[2], v[3]), pack_word(v[4], v[5]), pack_word(v[6], v[7]));
+  } else if constexpr (std::is_same<T, float>::value) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
   } else {
-    uint4 raw;
-    T* e = reinterpret_cast<T*>(&raw);
-#pragma unroll
-    for (int i = 0; i < V; ++i) e[i] = from_acc<T>(v[i]);
-    *reinterpret_cast<uint4*>(p) = raw;
+    *reinterpret_cast<int4*>(p) = make_int4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -226,22 +251,24 @@ __device__ __forceinline__ float ew_apply(float a, float b) {
 }
 
 // Each thread keeps kEwUnroll independent 16-byte vectors in flight per
-// operand (grid-strided so every warp access stays coalesced).
+// operand; a block covers one contiguous 16 KB span per operand (DRAM page
+// locality) with every warp access coalesced.
 constexpr int kEwUnroll = 4;
 
-template <typename T, int OP>
-__global__ void __launch_bounds__(256) ew_kernel(EwPtrs in, int nin, T* __restrict__ out, std::int64_t nvec) {
+template <typename T, int OP, int NIN>
+__global__ void __launch_bounds__(256) ew_kernel(EwPtrs in, T* __restrict__ out, std::int64_t nvec) {
   constexpr int V = 16 / sizeof(T);
-  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-  for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; base < nvec;
-       base += stride * kEwUnroll) {
+  const std::int64_t stride = blockDim.x;
+  for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x) * kEwUnroll + threadIdx.x; base < nvec;
+       base += static_cast<std::int64_t>(gridDim.x) * blockDim.x * kEwUnroll) {
     float acc[kEwUnroll][V], v[kEwUnroll][V];
 #pragma unroll
     for (int u = 0; u < kEwUnroll; ++u) {
       const std::int64_t i = base + u * stride;
       if (i < nvec) load_vec<T, V>(static_cast<const T*>(in.p[0]) + i * V, acc[u]);
     }
-    for (int k = 1; k < nin; ++k) {
+#pragma unroll
+    for (int k = 1; k < NIN; ++k) {  // NIN is static: operand pointers stay in the param bank
 #pragma unroll
       for (int u = 0; u < kEwUnroll; ++u) {
         const std::int64_t i = base + u * stride;
@@ -260,13 +287,28 @@ __global__ void __launch_bounds__(256) ew_kernel(EwPtrs in, int nin, T* __restri
   }
 }
 
-template <typename T, int OP>
-__global__ void ew_tail_kernel(EwPtrs in, int nin, T* __restrict__ out, std::int64_t begin, std::int64_t count) {
+template <typename T, int OP, int NIN>
+__global__ void ew_tail_kernel(EwPtrs in, T* __restrict__ out, std::int64_t begin, std::int64_t count) {
   std::int64_t i = begin + blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
   if (i >= begin + count) return;
   float acc = to_acc<T>(static_cast<const T*>(in.p[0])[i]);
-  for (int k = 1; k < nin; ++k) acc = ew_apply<OP>(acc, to_acc<T>(static_cast<const T*>(in.p[k])[i]));
+#pragma unroll
+  for (int k = 1; k < NIN; ++k) acc = ew_apply<OP>(acc, to_acc<T>(static_cast<const T*>(in.p[k])[i]));
   out[i] = from_acc<T>(acc);
+}
+
+template <typename T, int OP, int NIN>
+void ew_launch(const EwPtrs& p, void* out, std::int64_t nvec, std::int64_t count, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  if (nvec > 0) {
+    // One pass: every thread owns kEwUnroll vectors (no grid-stride tail).
+    ew_kernel<T, OP, NIN><<<grid_for(nvec, 256 * kEwUnroll, 1 << 30), 256, 0, s>>>(p, static_cast<T*>(out), nvec);
+  }
+  std::int64_t rest = count - nvec * V;
+  if (rest > 0) {
+    ew_tail_kernel<T, OP, NIN><<<static_cast<int>((rest + 255) / 256), 256, 0, s>>>(p, static_cast<T*>(out),
+                                                                                    nvec * V, rest);
+  }
 }
 
 template <typename T, int OP>
@@ -279,14 +321,15 @@ void ew_typed(const void* const* ins, int nin, void* out, std::int64_t count, cu
     aligned = aligned && (reinterpret_cast<std::uintptr_t>(ins[i]) % 16) == 0;
   }
   std::int64_t nvec = aligned ? count / V : 0;
-  if (nvec > 0) {
-    // One pass: every thread owns kEwUnroll vectors (no grid-stride tail).
-    ew_kernel<T, OP><<<grid_for(nvec, 256 * kEwUnroll, 1 << 30), 256, 0, s>>>(p, nin, static_cast<T*>(out), nvec);
-  }
-  std::int64_t rest = count - nvec * V;
-  if (rest > 0) {
-    ew_tail_kernel<T, OP><<<static_cast<int>((rest + 255) / 256), 256, 0, s>>>(p, nin, static_cast<T*>(out),
-                                                                               nvec * V, rest);
+  switch (nin) {
+    case 1: ew_launch<T, OP, 1>(p, out, nvec, count, s); break;
+    case 2: ew_launch<T, OP, 2>(p, out, nvec, count, s); break;
+    case 3: ew_launch<T, OP, 3>(p, out, nvec, count, s); break;
+    case 4: ew_launch<T, OP, 4>(p, out, nvec, count, s); break;
+    case 5: ew_launch<T, OP, 5>(p, out, nvec, count, s); break;
+    case 6: ew_launch<T, OP, 6>(p, out, nvec, count, s); break;
+    case 7: ew_launch<T, OP, 7>(p, out, nvec, count, s); break;
+    default: ew_launch<T, OP, 8>(p, out, nvec, count, s); break;
   }
 }
 
