@@ -130,50 +130,42 @@ template <typename T, int V, int R>
 __global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, const DevCell* __restrict__ cells,
                                                            const DevTerm* __restrict__ terms,
                                                            const DevChunk* __restrict__ chunks) {
+  // Every cell of the launch has exactly rank R (the host pads lower-rank
+  // cells with leading unit dims), so all coordinate indexing is static and
+  // stays in registers.
   using A = typename Acc<T>::type;
   constexpr int U = kBoxUnroll;
   const DevChunk ch = chunks[blockIdx.x];
   const DevCell* c = cells + ch.cell;
-  const int rank = __ldg(&c->rank);
   const int nt = __ldg(&c->nterms);
   const int term0 = __ldg(&c->term0);
-  std::int64_t ext[R], dstr[R];
+  std::int64_t dstr[R];
+  std::uint32_t ext[R];
 #pragma unroll
   for (int d = 0; d < R; ++d) {
-    ext[d] = d < rank ? __ldg(&c->ext[d]) : 1;
-    dstr[d] = d < rank ? __ldg(&c->dst_str[d]) : 0;
+    ext[d] = static_cast<std::uint32_t>(__ldg(&c->ext[d]));
+    dstr[d] = __ldg(&c->dst_str[d]);
   }
   const std::int64_t dst_off = __ldg(&c->dst_off);
-  std::int64_t inner_ext = ext[0];
-#pragma unroll
-  for (int d = 1; d < R; ++d)
-    if (d == rank - 1) inner_ext = ext[d];  // static indices keep ext[] in registers
-  const std::int64_t inner_vecs = inner_ext / V;
+  const std::uint32_t inner_vecs = ext[R - 1] / V;
   std::int64_t coord[U][R];
   bool live[U];
 #pragma unroll
   for (int x = 0; x < U; ++x) {
     const std::int64_t u = threadIdx.x + static_cast<std::int64_t>(x) * kBoxThreads;
     live[x] = u < ch.count;
-    std::int64_t lin = ch.begin + (live[x] ? u : 0);
-#pragma unroll
-    for (int d = 0; d < R; ++d) coord[x][d] = 0;
-    if (R == 1 || rank == 1) {
+    const std::int64_t lin = ch.begin + (live[x] ? u : 0);
+    if constexpr (R == 1) {
       coord[x][0] = lin * V;
     } else {
       // 32-bit division: chunk tables are built only for cells < 2^32 units.
       std::uint32_t l32 = static_cast<std::uint32_t>(lin);
-      const std::uint32_t iv = static_cast<std::uint32_t>(inner_vecs);
+      coord[x][R - 1] = static_cast<std::int64_t>(l32 % inner_vecs) * V;
+      l32 /= inner_vecs;
 #pragma unroll
-      for (int d = R - 1; d >= 0; --d) {
-        if (d == rank - 1) {
-          coord[x][d] = static_cast<std::int64_t>(l32 % iv) * V;
-          l32 /= iv;
-        } else if (d < rank - 1) {
-          const std::uint32_t e = static_cast<std::uint32_t>(ext[d]);
-          coord[x][d] = l32 % e;
-          l32 /= e;
-        }
+      for (int d = R - 2; d >= 0; --d) {
+        coord[x][d] = l32 % ext[d];
+        l32 /= ext[d];
       }
     }
   }
@@ -189,7 +181,7 @@ __global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, c
     const int add = __ldg(&tm->add);
     std::int64_t tstr[R];
 #pragma unroll
-    for (int d = 0; d < R; ++d) tstr[d] = d < rank ? __ldg(&tm->str[d]) : 0;
+    for (int d = 0; d < R; ++d) tstr[d] = __ldg(&tm->str[d]);
     A v[U][V];
 #pragma unroll
     for (int x = 0; x < U; ++x) {

@@ -310,13 +310,19 @@ void Executor::build_box_tables() {
       std::vector<DevCell> cells;
       std::vector<DevTerm> terms;
       std::vector<DevChunk> chunks;
+      // Launch rank: 1, 2 or kBoxRank; lower-rank cells get leading unit
+      // dims so the kernel indexes coordinates statically.
       int max_rank = 1;
+      for (const Cell* c : groups[g]) max_rank = std::max(max_rank, c->rank);
+      const int R = max_rank <= 1 ? 1 : max_rank <= 2 ? 2 : kBoxRank;
+      max_rank = R;
       for (const Cell* c : groups[g]) {
+        const int pad = R - c->rank;
         DevCell dc{};
-        dc.rank = c->rank;
-        for (int d = 0; d < c->rank; ++d) {
-          dc.ext[d] = c->extents[d];
-          dc.dst_str[d] = c->dst_strides[d];
+        dc.rank = R;
+        for (int d = 0; d < R; ++d) {
+          dc.ext[d] = d < pad ? 1 : c->extents[d - pad];
+          dc.dst_str[d] = d < pad ? 0 : c->dst_strides[d - pad];
         }
         dc.dst_off = c->dst_offset;
         dc.elems = c->elems();
@@ -327,13 +333,12 @@ void Executor::build_box_tables() {
           DevTerm dt{};
           dt.src = buf_ptr(t.buffer);
           dt.offset = t.offset;
-          for (int d = 0; d < c->rank; ++d) dt.str[d] = t.strides[d];
+          for (int d = 0; d < R; ++d) dt.str[d] = d < pad ? 0 : t.strides[d - pad];
           dt.add = t.add ? 1 : 0;
           terms.push_back(dt);
         }
         int ci = static_cast<int>(cells.size());
         cells.push_back(dc);
-        max_rank = std::max(max_rank, c->rank);
         std::int64_t units = dc.elems / width;
         if (units >= (std::int64_t(1) << 32)) throw UsageError("adapter cell above 2^32 vector units");
         for (std::int64_t b = 0; b < units; b += kChunkUnits) {
