@@ -44,6 +44,9 @@ extern "C" {
 #define PLANC_B200_NO_TENSOR_CORES 0x2u /* force the SIMT GEMM (debug / A-B checks) */
 #define PLANC_B200_STRICT_VALUE 0x4u    /* reference value-part rule only: V(m*v)->V(v) pieces are
                                            skipped like refexec.cpp:110-117 instead of summed */
+#define PLANC_B200_SERIAL_LANES 0x8u    /* one stream per lane: a lane's tasks run strictly in plan
+                                           order (default: only data dependencies and sync edges order
+                                           a lane's work, spread over several streams) */
 
 typedef struct planc_b200_exec planc_b200_exec;
 

@@ -35,6 +35,7 @@ _LIB_PATH = os.path.join(_HERE, "_lib", "libplanc_b200.so")
 NO_GRAPH = 0x1
 NO_TENSOR_CORES = 0x2
 STRICT_VALUE = 0x4
+SERIAL_LANES = 0x8
 
 
 class PlancError(RuntimeError):

@@ -68,6 +68,7 @@ int planc_b200_open(const char* plan_json, const int* lane_gpu, int num_lane_gpu
     opt.use_graph = (flags & PLANC_B200_NO_GRAPH) == 0;
     opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
     opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
+    if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
     std::vector<int> lanes;
     for (int i = 0; lane_gpu && i < num_lane_gpu; ++i) lanes.push_back(lane_gpu[i]);
     auto* h = new planc_b200_exec;
@@ -98,6 +99,7 @@ int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* 
     opt.use_graph = (flags & PLANC_B200_NO_GRAPH) == 0;
     opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
     opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
+    if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
     RankConfig rc;
     rc.rank = rank;
     rc.world = world;

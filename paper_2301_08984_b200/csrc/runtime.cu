@@ -131,6 +131,35 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       }
     }
   }
+  // Stream of each instruction within its lane: continue the stream of the
+  // most recent dependency that ended a stream's chain, else take the least
+  // recently used stream. Only data dependencies (and sync edges) then order
+  // a lane's work, via events between streams.
+  {
+    const int ns = std::max(1, std::min(opt_.streams_per_lane, kLaneStreams));
+    exec_stream_.assign(prog_.instrs.size(), 0);
+    std::vector<std::vector<int>> last(prog_.num_lanes, std::vector<int>(ns, -1));
+    for (int id : prog_.issue_order) {
+      const int el = exec_lane_[id];
+      if (el < 0) continue;
+      const Instr& in = prog_.instrs[id];
+      int pick = -1, best_dep = -1;
+      for (int s = 0; s < ns; ++s) {
+        const int l = last[el][s];
+        if (l >= 0 && l > best_dep && std::find(in.deps.begin(), in.deps.end(), l) != in.deps.end()) {
+          best_dep = l;
+          pick = s;
+        }
+      }
+      if (pick < 0) {
+        pick = 0;
+        for (int s = 1; s < ns; ++s)
+          if (last[el][s] < last[el][pick]) pick = s;
+      }
+      exec_stream_[id] = pick;
+      last[el][pick] = id;
+    }
+  }
   if (rank_mode_) {
     DeviceGuard dg(rc_.local_gpu);
     ncclUniqueId id;
@@ -174,7 +203,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   }
   for (int l = 0; l < prog_.num_lanes; ++l) {
     DeviceGuard dg(lanes_[l].gpu);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kLaneStreams; ++s) {
       cudaEvent_t e = nullptr;
       if (owned_[l]) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
       lane_join_.push_back(e);
@@ -198,7 +227,8 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
     for (int d : in.deps) {
       const Instr& p = prog_.instrs[d];
       if (exec_lane_[d] < 0) continue;  // ordered by the exchange step instead
-      if ((exec_lane_[d] != exec_lane_[in.id] || p.stream != in.stream) && !irt_[d].done) {
+      (void)p;
+      if ((exec_lane_[d] != exec_lane_[in.id] || exec_stream_[d] != exec_stream_[in.id]) && !irt_[d].done) {
         DeviceGuard dg(lanes_[exec_lane_[d]].gpu);
         ck(cudaEventCreateWithFlags(&irt_[d].done, cudaEventDisableTiming), "event");
       }
@@ -264,7 +294,7 @@ void* Executor::buf_ptr(int b) const {
 }
 
 cudaStream_t Executor::stream_of(const Instr& in) const {
-  return lanes_[exec_lane_[in.id]].stream[in.stream];
+  return lanes_[exec_lane_[in.id]].stream[exec_stream_[in.id]];
 }
 
 // One exchange step: this rank's sends and receives of the step, grouped so
@@ -496,7 +526,9 @@ void Executor::issue_step(bool, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>
     for (int d : in.deps) {
       if (exec_lane_[d] < 0) continue;
       const Instr& p = prog_.instrs[d];
-      if (exec_lane_[d] != el || p.stream != in.stream) ck(cudaStreamWaitEvent(s, irt_[d].done, 0), "wait dep");
+      (void)p;
+      if (exec_lane_[d] != el || exec_stream_[d] != exec_stream_[id])
+        ck(cudaStreamWaitEvent(s, irt_[d].done, 0), "wait dep");
     }
     launch_instr(in, s);
     if (irt_[id].done) ck(cudaEventRecord(irt_[id].done, s), "record done");
@@ -504,7 +536,8 @@ void Executor::issue_step(bool, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>
   for (int l = 0; l < prog_.num_lanes; ++l) {
     if (!owned_[l]) continue;
     set_dev(lanes_[l].gpu);
-    for (int k = 0; k < 2; ++k) ck(cudaEventRecord(lane_join_[2 * l + k], lanes_[l].stream[k]), "record join");
+    for (int k = 0; k < kLaneStreams; ++k)
+      ck(cudaEventRecord(lane_join_[kLaneStreams * l + k], lanes_[l].stream[k]), "record join");
   }
   set_dev(lanes_[first_lane_].gpu);
   for (auto e : lane_join_)

@@ -38,10 +38,16 @@ struct KernelStat {
   double wire_bytes = 0;
 };
 
+// Streams per lane. Instructions of a lane are spread over them so that only
+// true data dependencies (and sync edges) order work: independent GEMMs,
+// elementwise ops and adapters of one lane overlap on the GPU.
+constexpr int kLaneStreams = 4;
+
 struct ExecOptions {
   bool use_graph = true;       // capture one step into a CUDA graph
   bool allow_tensor_cores = true;
   bool value_split_extension = true;
+  int streams_per_lane = kLaneStreams;  // 1 = issue a lane strictly in plan order
 };
 
 // One-process-per-GPU mode: this process owns the lanes with
@@ -88,7 +94,7 @@ class Executor {
   struct LaneRt {
     int gpu = 0;
     char* arena = nullptr;
-    cudaStream_t stream[2] = {nullptr, nullptr};
+    cudaStream_t stream[kLaneStreams] = {};
   };
   struct BoxLaunch {
     DevCell* cells = nullptr;
@@ -122,6 +128,7 @@ class Executor {
   RankConfig rc_;
   std::vector<bool> owned_;     // per lane: runs in this process
   std::vector<int> exec_lane_;  // per instruction: lane whose streams run it here (-1: elsewhere)
+  std::vector<int> exec_stream_;  // per instruction: stream index within its lane
   void* comm_ = nullptr;        // ncclComm_t in rank mode
   int first_lane_ = 0;          // first lane this process runs (origin stream's device)
   std::vector<LaneRt> lanes_;
