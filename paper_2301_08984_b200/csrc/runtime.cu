@@ -281,6 +281,14 @@ Executor::~Executor() {
   if (comm_) nccl().comm_destroy(static_cast<ncclComm_t>(comm_));
   for (void* p : pinned_in_) cudaFreeHost(p);
   for (void* p : pinned_out_) cudaFreeHost(p);
+  for (int k = 0; k < 2; ++k) {
+    for (void* p : e2e_stage_in_[k]) cudaFree(p);
+    for (void* p : e2e_stage_out_[k]) cudaFree(p);
+    for (cudaEvent_t e : {ev_h2d_[k], ev_in_free_[k], ev_out_ready_[k], ev_out_free_[k]})
+      if (e) cudaEventDestroy(e);
+  }
+  if (h2d_stream_) cudaStreamDestroy(h2d_stream_);
+  if (d2h_stream_) cudaStreamDestroy(d2h_stream_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
   if (ev_begin_) cudaEventDestroy(ev_begin_);
@@ -637,25 +645,90 @@ double Executor::run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_b
   for (int b : e2e_out_bufs_) db += prog_.buffers[b].bytes;
   if (h2d_bytes) *h2d_bytes = hb;
   if (d2h_bytes) *d2h_bytes = db;
-  auto step = [&]() {
+  // Pipelined steps: step i+1's inputs cross PCIe (copy stream) while step i
+  // computes, and step i's results cross back while step i+1 computes.
+  // Every step still moves all of its own bytes: H2D into one of two device
+  // staging sets, a device copy into the placement buffers at step start,
+  // the step, a device copy of the results into one of two result sets, D2H.
+  if (e2e_stage_in_[0].empty()) {
+    for (int k = 0; k < 2; ++k) {
+      for (int b : e2e_in_bufs_) {
+        void* d = nullptr;
+        ck(cudaMalloc(&d, std::max<std::int64_t>(prog_.buffers[b].bytes, 1)), "cudaMalloc(stage)");
+        e2e_stage_in_[k].push_back(d);
+      }
+      for (int b : e2e_out_bufs_) {
+        void* d = nullptr;
+        ck(cudaMalloc(&d, std::max<std::int64_t>(prog_.buffers[b].bytes, 1)), "cudaMalloc(stage)");
+        e2e_stage_out_[k].push_back(d);
+      }
+    }
+    ck(cudaStreamCreateWithFlags(&h2d_stream_, cudaStreamNonBlocking), "h2d stream");
+    ck(cudaStreamCreateWithFlags(&d2h_stream_, cudaStreamNonBlocking), "d2h stream");
+    for (int k = 0; k < 2; ++k) {
+      for (cudaEvent_t* e : {&ev_h2d_[k], &ev_in_free_[k], &ev_out_ready_[k], &ev_out_free_[k]}) {
+        ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+      }
+    }
+  }
+  auto issue_h2d = [&](int slot) {  // inputs of the step using staging set `slot`
+    ck(cudaStreamWaitEvent(h2d_stream_, ev_in_free_[slot], 0), "wait stage free");
+    for (std::size_t i = 0; i < e2e_in_bufs_.size(); ++i) {
+      ck(cudaMemcpyAsync(e2e_stage_in_[slot][i], pinned_in_[i], prog_.buffers[e2e_in_bufs_[i]].bytes,
+                         cudaMemcpyHostToDevice, h2d_stream_),
+         "h2d");
+    }
+    ck(cudaEventRecord(ev_h2d_[slot], h2d_stream_), "record h2d");
+  };
+  auto compute = [&](int slot) {
+    ck(cudaStreamWaitEvent(origin_, ev_h2d_[slot], 0), "wait h2d");
     for (std::size_t i = 0; i < e2e_in_bufs_.size(); ++i) {
       const auto& b = prog_.buffers[e2e_in_bufs_[i]];
-      ck(cudaMemcpyAsync(buf_ptr(b.id), pinned_in_[i], b.bytes, cudaMemcpyHostToDevice, origin_), "h2d");
+      ck(cudaMemcpyAsync(buf_ptr(b.id), e2e_stage_in_[slot][i], b.bytes, cudaMemcpyDeviceToDevice, origin_), "in");
     }
+    ck(cudaEventRecord(ev_in_free_[slot], origin_), "record stage free");
     if (graph_exec_) ck(cudaGraphLaunch(graph_exec_, origin_), "graph launch");
     else issue_step(false, nullptr);
+    ck(cudaStreamWaitEvent(origin_, ev_out_free_[slot], 0), "wait out free");
     for (std::size_t i = 0; i < e2e_out_bufs_.size(); ++i) {
       const auto& b = prog_.buffers[e2e_out_bufs_[i]];
-      ck(cudaMemcpyAsync(pinned_out_[i], buf_ptr(b.id), b.bytes, cudaMemcpyDeviceToHost, origin_), "d2h");
+      ck(cudaMemcpyAsync(e2e_stage_out_[slot][i], buf_ptr(b.id), b.bytes, cudaMemcpyDeviceToDevice, origin_), "out");
     }
+    ck(cudaEventRecord(ev_out_ready_[slot], origin_), "record out ready");
   };
-  step();
+  auto issue_d2h = [&](int slot) {
+    ck(cudaStreamWaitEvent(d2h_stream_, ev_out_ready_[slot], 0), "wait out ready");
+    for (std::size_t i = 0; i < e2e_out_bufs_.size(); ++i) {
+      ck(cudaMemcpyAsync(pinned_out_[i], e2e_stage_out_[slot][i], prog_.buffers[e2e_out_bufs_[i]].bytes,
+                         cudaMemcpyDeviceToHost, d2h_stream_),
+         "d2h");
+    }
+    ck(cudaEventRecord(ev_out_free_[slot], d2h_stream_), "record out free");
+  };
+  auto run_steps = [&](int n, cudaEvent_t start) {
+    if (start) {
+      ck(cudaStreamWaitEvent(h2d_stream_, start, 0), "wait start");
+      ck(cudaStreamWaitEvent(d2h_stream_, start, 0), "wait start");
+    }
+    issue_h2d(0);
+    for (int i = 0; i < n; ++i) {
+      if (i + 1 < n) issue_h2d((i + 1) & 1);
+      compute(i & 1);
+      issue_d2h(i & 1);
+    }
+    cudaEvent_t done;
+    ck(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(done, d2h_stream_), "record done");
+    ck(cudaStreamWaitEvent(origin_, done, 0), "join d2h");
+    cudaEventDestroy(done);
+  };
+  run_steps(2, nullptr);
   ck(cudaStreamSynchronize(origin_), "warmup");
   cudaEvent_t t0, t1;
   ck(cudaEventCreate(&t0), "event");
   ck(cudaEventCreate(&t1), "event");
   ck(cudaEventRecord(t0, origin_), "record");
-  for (int i = 0; i < iters; ++i) step();
+  run_steps(std::max(iters, 1), t0);
   ck(cudaEventRecord(t1, origin_), "record");
   ck(cudaEventSynchronize(t1), "sync");
   float ms = 0;

@@ -147,6 +147,9 @@ class Executor {
   // e2e staging
   std::vector<void*> pinned_in_, pinned_out_;
   std::vector<int> e2e_in_bufs_, e2e_out_bufs_;
+  std::vector<void*> e2e_stage_in_[2], e2e_stage_out_[2];  // device staging, double-buffered
+  cudaStream_t h2d_stream_ = nullptr, d2h_stream_ = nullptr;
+  cudaEvent_t ev_h2d_[2] = {}, ev_in_free_[2] = {}, ev_out_ready_[2] = {}, ev_out_free_[2] = {};
 };
 
 }  // namespace planc_b200
