@@ -13,9 +13,12 @@ T=8192 tokens, H=2048, FFN=4H, bf16; TP degree = number of GPUs.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1l]
   python bench.py --impl reference ...   # the reference's CPU run_plan
 
-Multi-GPU: under torchrun every rank joins the barriers and the timing
-reduction; rank 0 drives all N GPUs of the box (plan lanes -> devices
-0..N-1, fused box kernels over NVLink peer memory). Prints ONE JSON line.
+Multi-GPU: under torchrun one process per GPU — rank r runs plan lane r on
+LOCAL_RANK's GPU; pieces of other ranks' lanes move in NCCL exchange steps
+(all-reduce groups as ncclAllReduce). Times are the max over ranks (CUDA
+events per rank). Without torchrun, --gpus N drives N GPUs from one process
+(lanes read each other's buffers over NVLink peer mappings). Prints ONE
+JSON line (rank 0).
 """
 from __future__ import annotations
 
@@ -91,6 +94,9 @@ class ClockSampler:
 
     def __enter__(self):
         self._proc = None
+        self._t = None
+        if not self.gpus:  # only rank 0 samples
+            return self
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         deadline = time.time() + 3.0
@@ -99,6 +105,8 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
+        if self._t is None:
+            return
         time.sleep(0.06)  # at least one sample after the timed region ends
         self._stop.set()
         if self._proc is not None:
@@ -196,24 +204,48 @@ def main():
     name = plan_name(args.config, n)
     plan, meta = load_plan(name)
     result = None
-    if rank == 0:
-        import paper_2301_08984_b200 as pb
+    import paper_2301_08984_b200 as pb
 
-        peaks = measured_peaks()
-        inputs = synthetic_inputs(plan)
+    peaks = measured_peaks()
+    inputs = synthetic_inputs(plan)
+    nlanes = len(json.loads(plan)["lanes"])
+    if dist:
+        # One process per GPU: this rank runs lanes l with l % world == rank
+        # on its local GPU; cross-rank pieces move over NCCL.
+        import torch
+
+        local = int(os.environ.get("LOCAL_RANK", rank))
+        torch.cuda.set_device(local)
+        box = [pb.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        ex = pb.Executor(plan, rank=rank, world=world, lane_rank=pb.lanes_round_robin(nlanes, world),
+                         local_gpu=local, nccl_id=box[0])
+    else:
         ex = pb.Executor(plan, lane_gpus=list(range(n)))
-        ex.set_inputs(inputs)
-        ex.run(args.warmup)  # warm-up (graph capture + W steps)
-        st = ex.stats()
+    ex.set_inputs(inputs)
+    ex.run(args.warmup)  # warm-up (graph capture + W steps)
+    st = ex.stats()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     if dist:
         dist.barrier()
+    with ClockSampler(list(range(n)) if rank == 0 else []) as clk:
+        ms = ex.run(args.steps)
+    ms = max_over_ranks(ms)
+    clocks = clk.summary()
+    e2e_ms, h2d, d2h = ex.run_e2e(args.steps)
+    e2e_ms = max_over_ranks(e2e_ms)
+    prof = [ex.profile() for _ in range(3)]  # every rank: exchange steps pair up
+    ex.close()
     if rank == 0:
-        with ClockSampler(list(range(n))) as clk:
-            ms = ex.run(args.steps)
-        clocks = clk.summary()
-        e2e_ms, h2d, d2h = ex.run_e2e(args.steps)
-        prof = [ex.profile() for _ in range(3)]
-        ex.close()
         sps = meta["samples_per_step"] / (ms / 1e3)
         # Dominant kernel (largest share of the serialised step) and its roofline.
         fam = {}
@@ -292,12 +324,6 @@ def main():
             except Exception as e:  # reference library not shipped
                 result["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
     if dist:
-        import torch
-
-        t = torch.tensor([result["ms_per_step"] if result else 0.0], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        if result:
-            result["ms_per_step"] = float(t.item())
         dist.barrier()
         dist.destroy_process_group()
     if result:

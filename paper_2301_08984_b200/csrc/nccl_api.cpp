@@ -28,6 +28,7 @@ const NcclApi& nccl() {
     api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(sym("ncclCommDestroy"));
     api.send = reinterpret_cast<decltype(api.send)>(sym("ncclSend"));
     api.recv = reinterpret_cast<decltype(api.recv)>(sym("ncclRecv"));
+    api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(sym("ncclAllReduce"));
     api.group_start = reinterpret_cast<decltype(api.group_start)>(sym("ncclGroupStart"));
     api.group_end = reinterpret_cast<decltype(api.group_end)>(sym("ncclGroupEnd"));
     api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));

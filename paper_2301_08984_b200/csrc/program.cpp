@@ -751,6 +751,76 @@ Program localize(const Program& g, const std::vector<int>& lane_rank) {
         grp.push_back(nx.id);
       }
     }
+    if (grp.size() > 1 && first.kind == InstrKind::box && first.coll_group >= 0) {
+      // All-reduce fast path: every member output is the plain elementwise
+      // sum of the same k whole input buffers, one per member lane, and the
+      // member lanes sit on k distinct ranks covering every rank.
+      bool ar = true;
+      std::map<int, int> in_of_lane;  // member lane -> its partial input buffer
+      std::set<int> inputs, ranks;
+      int world = 0;
+      for (int r : lane_rank) world = std::max(world, r + 1);
+      for (int id : grp) {
+        const Instr& in = g.instrs[id];
+        const BufferDesc& ob = P.buffers[in.out_bufs[0]];
+        if (in.cells.size() != 1 || !ranks.insert(owner(in.lane)).second) {
+          ar = false;
+          break;
+        }
+        const Cell& c = in.cells[0];
+        ar = ar && c.dst_offset == 0 && c.elems() == ob.elems && c.terms.size() == grp.size() && c.rank == 1 &&
+             c.dst_strides[0] == 1;
+        std::set<int> ts;
+        for (const auto& t : c.terms) {
+          const BufferDesc& sb = P.buffers[t.buffer];
+          ar = ar && t.add && t.offset == 0 && t.strides[0] == 1 && sb.elems == ob.elems && sb.dtype == ob.dtype;
+          ts.insert(t.buffer);
+          if (in_of_lane.count(sb.lane) && in_of_lane[sb.lane] != t.buffer) ar = false;
+          in_of_lane[sb.lane] = t.buffer;
+        }
+        if (inputs.empty()) inputs = ts;
+        ar = ar && ts == inputs && ts.size() == grp.size();
+        if (!ar) break;
+      }
+      if (ar && static_cast<int>(ranks.size()) == world && in_of_lane.size() == grp.size()) {
+        Instr x;
+        x.kind = InstrKind::xfer;
+        x.allreduce = true;
+        x.lane = first.lane;
+        x.stream = 1;
+        x.op = first.op;
+        x.label = "allreduce:" + first.label;
+        x.coll_group = first.coll_group;
+        std::set<int> xdeps;
+        for (int id : grp) {
+          const Instr& in = g.instrs[id];
+          auto it = in_of_lane.find(in.lane);
+          if (it == in_of_lane.end()) {
+            ar = false;
+            break;
+          }
+          Xfer xf;
+          xf.src = it->second;
+          xf.dst = in.out_bufs[0];
+          xf.src_lane = xf.dst_lane = in.lane;
+          xf.bytes = P.buffers[xf.dst].bytes;
+          x.xfers.push_back(xf);
+          x.in_bufs.push_back(xf.src);
+          x.out_bufs.push_back(xf.dst);
+          x.wire_bytes = in.wire_bytes;
+          for (int d : in.deps)
+            if (remap[d] >= 0) xdeps.insert(remap[d]);
+        }
+        if (ar) {
+          x.deps.assign(xdeps.begin(), xdeps.end());
+          int xid = push(std::move(x));
+          for (int b : P.instrs[xid].out_bufs) P.buffers[b].producer = xid;
+          for (int id : grp) remap[id] = xid;
+          i += grp.size();
+          continue;
+        }
+      }
+    }
     Instr x;
     x.kind = InstrKind::xfer;
     x.lane = first.lane;
@@ -860,6 +930,7 @@ std::string Program::describe_json() const {
        << ",\"axis_len\":" << in.axis_len << ",\"inner\":" << in.inner << ",\"n_idx\":" << in.n_idx
        << ",\"rows\":" << in.rows << ",\"h\":" << in.h << ",\"lo\":" << in.lo << ",\"flops\":" << in.flops
        << ",\"bytes\":" << in.bytes << ",\"wire_bytes\":" << in.wire_bytes << ",\"coll_group\":" << in.coll_group
+       << ",\"allreduce\":" << (in.allreduce ? "true" : "false")
        << ",\"xfers\":[";
     for (std::size_t x = 0; x < in.xfers.size(); ++x) {
       const auto& xf = in.xfers[x];

@@ -111,10 +111,12 @@ struct Instr {
   // box
   std::vector<Cell> cells;
   int coll_group = -1;  // collective group a box instruction belongs to
-  // xfer (exchange step, identical on every rank): the movements, and the
-  // collective all-reduce fast path when the step is one whole-buffer
-  // all-reduce across ranks (allreduce_bufs[lane] = in, out pairs)
+  // xfer (exchange step, identical on every rank): the piece movements; or,
+  // when `allreduce`, one whole-buffer sum across all ranks where each
+  // entry is a member lane's (src = its partial input, dst = its output)
+  // and every dst receives the sum of all srcs (ncclAllReduce).
   std::vector<Xfer> xfers;
+  bool allreduce = false;
   // accounting (algorithmic, from masks)
   double flops = 0;
   double bytes = 0;       // HBM bytes read + written

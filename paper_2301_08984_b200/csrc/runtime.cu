@@ -125,7 +125,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       continue;
     }
     for (const auto& x : in.xfers) {
-      if (owned_[x.src_lane] != owned_[x.dst_lane]) {
+      if (in.allreduce ? owned_[x.src_lane] : owned_[x.src_lane] != owned_[x.dst_lane]) {
         exec_lane_[in.id] = owned_[x.src_lane] ? x.src_lane : x.dst_lane;
         break;
       }
@@ -310,6 +310,17 @@ cudaStream_t Executor::stream_of(const Instr& in) const {
 void Executor::launch_xfer(const Instr& in, cudaStream_t s) {
   const NcclApi& api = nccl();
   ncclComm_t comm = static_cast<ncclComm_t>(comm_);
+  if (in.allreduce) {
+    // One member per rank; this rank's member sums every rank's partial.
+    for (const auto& x : in.xfers) {
+      if (!owned_[x.src_lane]) continue;
+      const BufferDesc& b = prog_.buffers[x.dst];
+      ncclDataType_t dt = b.dtype == DType::bf16 ? ncclBfloat16 : b.dtype == DType::i32 ? ncclInt32 : ncclFloat32;
+      nccl_check(api.all_reduce(buf_ptr(x.src), buf_ptr(x.dst), static_cast<std::size_t>(b.elems), dt, ncclSum, comm, s),
+                 "ncclAllReduce");
+    }
+    return;
+  }
   nccl_check(api.group_start(), "ncclGroupStart");
   for (const auto& x : in.xfers) {
     bool src_here = owned_[x.src_lane], dst_here = owned_[x.dst_lane];

@@ -43,6 +43,10 @@ def run_program(desc: dict, plan: dict, inputs: dict, owned_lanes=None, exchange
         if k == "xfer":
             if exchange is not None:
                 exchange(ins, data)
+            elif ins.get("allreduce"):  # single process: every member gets the sum
+                total = sum(data[x["src"]] for x in ins["xfers"])
+                for x in ins["xfers"]:
+                    data[x["dst"]] = total.copy()
             else:  # single process: the movement is a plain copy
                 for x in ins["xfers"]:
                     data[x["dst"]] = data[x["src"]].copy()

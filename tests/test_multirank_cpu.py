@@ -53,6 +53,14 @@ def _worker(rank, world, port, names, result_q):
             n_steps = [0]
 
             def exchange(ins, data):
+                if ins["allreduce"]:  # ncclAllReduce over the world: one member per rank
+                    mine = [x for x in ins["xfers"] if lane_rank[x["src_lane"]] == rank]
+                    assert len(mine) == 1
+                    t = torch.from_numpy(data[mine[0]["src"]].copy())
+                    dist.all_reduce(t)
+                    data[mine[0]["dst"]] = t.numpy().copy()
+                    n_steps[0] += 1
+                    return
                 ops, recvs = [], []
                 for x in ins["xfers"]:
                     src_r, dst_r = lane_rank[x["src_lane"]], lane_rank[x["dst_lane"]]
@@ -121,8 +129,13 @@ def test_localised_program_invariants():
                         assert lane_rank[desc["buffers"][t["buf"]]["lane"]] == lane_rank[ins["lane"]]
             if ins["kind"] == "xfer":
                 for x in ins["xfers"]:
-                    assert lane_rank[x["src_lane"]] != lane_rank[x["dst_lane"]]
+                    if ins["allreduce"]:
+                        assert x["src_lane"] == x["dst_lane"]  # one member per rank
+                    else:
+                        assert lane_rank[x["src_lane"]] != lane_rank[x["dst_lane"]]
                     assert desc["buffers"][x["dst"]]["bytes"] == x["bytes"]
+                if ins["allreduce"]:
+                    assert sorted(lane_rank[x["src_lane"]] for x in ins["xfers"]) == [0, 1]
         # single-rank ownership needs no exchange at all
         solo = pb.describe(g["plan"], lane_rank=[0] * len(plan["lanes"]))
         assert not any(i["kind"] == "xfer" for i in solo["instrs"])
