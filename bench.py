@@ -40,12 +40,23 @@ PLANS = os.path.join(ROOT, "plans")
 
 
 def plan_name(config: str, n: int) -> str:
-    return {"c2": f"c2_tp{n}", "c1l": f"c1l_dp{n}"}[config]
+    """c2 / c1l plans are compiled per GPU count (TP / DP degree n); the
+    pipeline (c3: 8 lanes), co-shard (c4: 1 lane) and 3F1B (c5: 2 lanes)
+    plans have a fixed lane count — with fewer GPUs, lanes share GPUs."""
+    return {"c2": f"c2_tp{n}", "c1l": f"c1l_dp{n}", "c3": "c3_pp4dp2", "c4": "c4_coshard4",
+            "c5": "c5_3f1b"}[config]
 
 
 def load_plan(name):
-    with open(os.path.join(PLANS, name + ".plan.json")) as f:
-        plan = f.read()
+    path = os.path.join(PLANS, name + ".plan.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            plan = f.read()
+    else:  # large plans are stored gzipped
+        import gzip
+
+        with gzip.open(path + ".gz", "rt") as f:
+            plan = f.read()
     with open(os.path.join(PLANS, name + ".meta.json")) as f:
         meta = json.load(f)
     return plan, meta
@@ -178,7 +189,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c2", "c1l"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c1l", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -289,8 +300,10 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (integer-valued inputs in {-1,0,1})",
             "config": {"workload": name, "config": args.config, "plan": f"plans/{name}.plan.json",
-                       "shape": {k: meta[k] for k in ("tokens", "batch", "hidden") if k in meta},
-                       "parallelism": (f"tp{n}" if args.config == "c2" else f"dp{n}"),
+                       "shape": {k: meta[k] for k in ("tokens", "batch", "hidden", "middle", "layers") if k in meta},
+                       "parallelism": {"c2": f"tp{n}", "c1l": f"dp{n}", "c3": "pp4 x dp2 (1F1B, K=8)",
+                                       "c4": "co-shard x4", "c5": "3F1B pp2 (K=4)"}[args.config],
+                       "lanes_per_gpu": nlanes / max(n, 1),
                        "sample": meta["sample"], "l2": "step working set " +
                        f"{st['device_bytes'] / 2**30:.1f} GiB > 126 MB L2 (no flush needed)",
                        "lanes": st["num_lanes"], "tasks": st["num_tasks"], "launch": (

@@ -35,8 +35,29 @@ def _op(i, kind, ins, outs, direction, flops, attrs=None, backward_of=None):
     return o
 
 
+def gpt_stack_doc(layers: int, tokens: int, hidden: int, elem_size: int = 2) -> dict:
+    """`layers` chained GPT blocks (train step) — SURVEY §8d config C3.
+
+    Layer l's input is layer l-1's OUT; the gradient arriving at layer l's
+    OUT is layer l+1's input gradient, so one backward chain runs through the
+    stack. Every op carries its `layer`, which the pipeline sPrograms group
+    into stages (reference strategies.cpp:168-276).
+    """
+    stride = 200
+    pts, ops = [], []
+    for l in range(layers):
+        base = l * stride
+        x_in = None if l == 0 else (l - 1) * stride + 19  # previous OUT
+        g_out = None if l == layers - 1 else (l + 1) * stride + 100 + 12  # next layer's dX
+        d = gpt_block_doc(tokens, hidden, elem_size, True, layer=l, prefix=f"L{l}.", base=base, x_in=x_in,
+                          g_out=g_out)
+        pts += d["ptensors"]
+        ops += d["ops"]
+    return {"ptensors": pts, "ops": ops}
+
+
 def gpt_block_doc(tokens: int, hidden: int, elem_size: int = 2, train: bool = True,
-                  layer: int = 0, prefix: str = "", base: int = 0, x_in=None) -> dict:
+                  layer: int = 0, prefix: str = "", base: int = 0, x_in=None, g_out=None) -> dict:
     """GPT-3-style transformer block proxy.
 
     Forward: Q = X·Wq, K = X·Wk (column-parallel), S = Q*K (attention proxy),
@@ -76,14 +97,19 @@ def gpt_block_doc(tokens: int, hidden: int, elem_size: int = 2, train: bool = Tr
     if train:
         g = {k: b + 100 + v for k, v in dict(OUT=0, Y=1, Fa=2, F1=3, X2a=4, X2=5, O=6, S=7, Q=8,
                                                K=9, Xq=10, Xk=11, X=12).items()}
+        if g_out is not None:
+            g["OUT"] = g_out  # produced by the next layer's backward (declared there)
         gw = {k: b + 120 + v for k, v in dict(Wq=0, Wk=1, Wo=2, W1=3, W2=4).items()}
         nw = {k: b + 130 + v for k, v in dict(Wq=0, Wk=1, Wo=2, W1=3, W2=4).items()}
-        for name, shp, of in (("OUT", (T, H), ids["OUT"]), ("Y", (T, H), ids["Y"]),
-                              ("Fa", (T, F), ids["Fa"]), ("F1", (T, F), ids["F1"]),
-                              ("X2a", (T, H), ids["X2"]), ("X2", (T, H), ids["X2"]),
-                              ("O", (T, H), ids["O"]), ("S", (T, H), ids["S"]),
-                              ("Q", (T, H), ids["Q"]), ("K", (T, H), ids["K"]),
-                              ("Xq", (T, H), X), ("Xk", (T, H), X), ("X", (T, H), X)):
+        for item in ((() if g_out is not None else ("OUT", (T, H), ids["OUT"])), ("Y", (T, H), ids["Y"]),
+                     ("Fa", (T, F), ids["Fa"]), ("F1", (T, F), ids["F1"]),
+                     ("X2a", (T, H), ids["X2"]), ("X2", (T, H), ids["X2"]),
+                     ("O", (T, H), ids["O"]), ("S", (T, H), ids["S"]),
+                     ("Q", (T, H), ids["Q"]), ("K", (T, H), ids["K"]),
+                     ("Xq", (T, H), X), ("Xk", (T, H), X), ("X", (T, H), X)):
+            if not item:
+                continue
+            name, shp, of = item
             pts.append(_pt(g[name], shp, "gradient", e, of))
         for w, shp in (("Wq", (H, H)), ("Wk", (H, H)), ("Wo", (H, H)), ("W1", (H, F)), ("W2", (F, H))):
             pts.append(_pt(gw[w], shp, "gradient", e, ids[w]))

@@ -30,8 +30,14 @@ OUT = os.path.join(ROOT, "plans")
 
 
 def write(name, graph, plan, meta):
-    with open(os.path.join(OUT, name + ".plan.json"), "w") as f:
-        f.write(plan)
+    if len(plan) > (2 << 20):  # large plans (C3) are stored gzipped
+        import gzip
+
+        with gzip.open(os.path.join(OUT, name + ".plan.json.gz"), "wt", compresslevel=9) as f:
+            f.write(plan)
+    else:
+        with open(os.path.join(OUT, name + ".plan.json"), "w") as f:
+            f.write(plan)
     with open(os.path.join(OUT, name + ".graph.json"), "w") as f:
         f.write(graph)
     pj = json.loads(plan)
@@ -52,6 +58,26 @@ def main():
             plan = refpy.compile_plan(g, strategy="megatron_tp", devices=k)
             write(f"c2_tp{k}{tag}", g, plan, dict(config="c2", tokens=T, hidden=H, tp=k, dtype="bf16",
                                                   samples_per_step=T, sample="token (row of X)"))
+    # C3: GPT stack, 1F1B pipeline S=4 x inner DP 2 (8 lanes), K=8 micro-batches.
+    # (8 layers = 2 per stage keeps the plan ~10^4 tasks; SURVEY §7 "plan scale".)
+    for L, T, H, tag in ((8, 32768, 2048, ""), (4, 256, 64, "_cpu")):
+        g = docs.dumps(docs.gpt_stack_doc(L, T, H, elem_size=2))
+        plan = refpy.compile_plan(g, strategy="1f1b", devices=8, stages=4, micro_batches=8, inner_dp=2)
+        write(f"c3_pp4dp2{tag}", g, plan, dict(config="c3", layers=L, tokens=T, hidden=H, stages=4, inner_dp=2,
+                                                micro_batches=8, dtype="bf16", samples_per_step=T,
+                                                sample="token (row of X)"))
+    # C4: co-shard x4 of the FFN-like pair (op1, op2) on one device (Swin stage proxy).
+    for B, H, M, tag in ((16384, 512, 2048, ""), (128, 64, 256, "_cpu")):
+        g = refpy.with_elem_size(refpy.coshard_doc(batch=B, hidden=H, middle=M), 2)
+        plan = refpy.compile_plan(g, strategy="coshard", devices=1, shards=4, target_ops="op1,op2")
+        write(f"c4_coshard4{tag}", g, plan, dict(config="c4", batch=B, hidden=H, middle=M, shards=4, dtype="bf16",
+                                                  samples_per_step=B, sample="row of the batch"))
+    # C5: three chained forward passes + one backward (Evoformer proxy), 3F1B S=2.
+    for B, H, tag in ((32768, 256, ""), (128, 32, "_cpu")):
+        g = refpy.with_elem_size(refpy.three_pass_doc(layers=4, batch=B, hidden=H), 2)
+        plan = refpy.compile_plan(g, strategy="3f1b", devices=2, stages=2, micro_batches=4)
+        write(f"c5_3f1b{tag}", g, plan, dict(config="c5", batch=B, hidden=H, stages=2, micro_batches=4,
+                                              dtype="bf16", samples_per_step=B, sample="row of the MSA batch"))
     for B, H, tag in ((16384, 4096, ""), (128, 128, "_cpu")):
         g = refpy.with_elem_size(refpy.mlp_doc(layers=2, batch=B, hidden=H), 2)
         for k in (1, 2, 4, 8):

@@ -142,6 +142,9 @@ def cases():
                     dict(strategy="megatron_tp", devices=k), 60 + k, 0.0, "C2 Megatron TP block (train), fp32"))
     out.append(("gpt_block_tp2_bf16", docs.dumps(docs.gpt_block_doc(16, 16, elem_size=2, train=True)),
                 dict(strategy="megatron_tp", devices=2), 70, 2e-2, "C2 Megatron TP block (train), bf16"))
+    out.append(("gpt_stack2_1f1b_bf16", docs.dumps(docs.gpt_stack_doc(2, 32, 16, elem_size=2)),
+                dict(strategy="1f1b", devices=4, stages=2, micro_batches=2, inner_dp=2), 72, 2e-2,
+                "C3 shape: stacked GPT blocks, 1F1B pipeline x inner DP (P2P + naive gradient sync), bf16"))
     out.append(("gpt_block_fwd_tp2_mma", docs.dumps(docs.gpt_block_doc(256, 128, elem_size=2, train=False)),
                 dict(strategy="megatron_tp", devices=2), 71, 2e-2,
                 "C2 forward at tensor-core-eligible shapes (bf16)"))
