@@ -284,11 +284,23 @@ def main():
             roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
                     "frac": achieved / peaks["hbm"], "traffic": None, "peak_source": peaks["src"],
                     "share_of_step": t["ms"] / total_prof}
-        # Plan-level roofline: max over lanes of
-        # F/P + M/HBM vs W/NVLink, against the measured sustained peaks.
-        t_roof = max(st["max_lane_gemm_flops"] / (peaks["bf16_sus"] * 1e12)
-                     + st["max_lane_hbm_bytes"] / (peaks["hbm"] * 1e9),
-                     st["max_lane_wire_bytes"] / (NVLINK_GBS * 1e9))
+        # Plan-level roofline: max over GPUs of
+        # F/P + M/HBM vs W/NVLink, against the measured sustained peaks, from
+        # the host lowering's per-instruction algorithmic work. Lanes sharing
+        # a GPU add up; their adapter bytes then stay in HBM (no NVLink).
+        desc = pb.describe(plan)
+        gpu_of = [lane % n for lane in range(nlanes)]
+        F, M, W = [0.0] * n, [0.0] * n, [0.0] * n
+        for ins in desc["instrs"]:
+            gidx = gpu_of[ins["lane"]]
+            if ins["kind"] == "gemm":
+                F[gidx] += ins["flops"]
+            else:
+                M[gidx] += ins["bytes"]
+            if n > 1:
+                W[gidx] += ins["wire_bytes"]
+        t_roof = max(max(F[i] / (peaks["bf16_sus"] * 1e12) + M[i] / (peaks["hbm"] * 1e9),
+                         W[i] / (NVLINK_GBS * 1e9)) for i in range(n))
         families = {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
                         "tflops" if k.startswith("gemm") else "gbs":
                             round((v["flops"] / 1e12 if k.startswith("gemm") else v["bytes"] / 1e9)
