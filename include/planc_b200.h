@@ -133,6 +133,13 @@ int planc_b200_get_stats(planc_b200_exec* h, planc_b200_stats* out);
  * (caller frees with planc_b200_free). */
 int planc_b200_profile(planc_b200_exec* h, char** json_out);
 
+/* Measured timeline of one step (per-task CUDA events, streams and overlap as
+ * in a timed step) in the shape of the reference simulator's
+ * SimReport::timeline_json (simulate.cpp:373-383): a JSON array of
+ * {"device","op","kind","start","end"} (seconds) plus "instr" / "stream".
+ * Caller frees with planc_b200_free. */
+int planc_b200_timeline(planc_b200_exec* h, char** json_out);
+
 /* Host-only lowering (no GPU needed): the executor's device program for a
  * plan as JSON — buffers, instructions, box cells, issue order. */
 int planc_b200_describe(const char* plan_json, uint32_t flags, char** json_out);

@@ -349,6 +349,18 @@ char* ref_run_plan(const char* plan_json, const char* inputs, int iters,
   }
 }
 
+// The reference's discrete-event simulator (simulate.cpp:102-318): returns
+// {"report": to_json(), "timeline": timeline_json()} for a plan document.
+char* ref_simulate(const char* plan_json) {
+  try {
+    auto rep = simulate(load_plan(plan_json));
+    return dup_string("{\"report\":" + rep.to_json() + ",\"timeline\":" + rep.timeline_json() + "}");
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
 // Re-serializes a plan through the reference's own load_plan/save_plan.
 char* ref_roundtrip_plan(const char* plan_json) {
   try {

@@ -47,6 +47,7 @@ def lib():
             ("ref_chain_doc", []),
             ("ref_compile", [cp, cp]),
             ("ref_roundtrip_plan", [cp]),
+            ("ref_simulate", [cp]),
         ]:
             f = getattr(L, name)
             f.argtypes = args
@@ -146,6 +147,11 @@ def compile_plan(graph_doc: str, **spec) -> str:
 
 def roundtrip_plan(plan_json: str) -> str:
     return _take_str(lib().ref_roundtrip_plan(plan_json.encode()))
+
+
+def simulate(plan_json: str) -> dict:
+    """Reference simulator (simulate.cpp:102): {"report": ..., "timeline": [...]}."""
+    return json.loads(_take_str(lib().ref_simulate(plan_json.encode())))
 
 
 def random_integer_inputs(graph_doc: str, seed: int, magnitude: int = 4) -> dict:

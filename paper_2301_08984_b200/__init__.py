@@ -103,6 +103,7 @@ def _load():
     L.planc_b200_read_buffer.argtypes = [vp, c_int, P(c_dbl), c_i64]
     L.planc_b200_read_buffer.restype = c_i64
     L.planc_b200_profile.argtypes = [vp, P(ctypes.c_char_p)]
+    L.planc_b200_timeline.argtypes = [vp, P(vp)]
     L.planc_b200_describe.argtypes = [ctypes.c_char_p, ctypes.c_uint32, P(vp)]
     L.planc_b200_describe_rank.argtypes = [ctypes.c_char_p, P(c_int), c_int, ctypes.c_uint32, P(vp)]
     L.planc_b200_nccl_unique_id.argtypes = [ctypes.c_char_p]
@@ -264,6 +265,15 @@ class Executor:
         s = _Stats()
         _check(_load().planc_b200_get_stats(self._h, ctypes.byref(s)))
         return {k: getattr(s, k) for k, _ in _Stats._fields_}
+
+    def timeline(self):
+        """Measured per-task timeline of one step (simulator timeline shape)."""
+        L = _load()
+        out = ctypes.c_void_p()
+        _check(L.planc_b200_timeline(self._h, ctypes.byref(out)))
+        s = ctypes.string_at(out.value).decode()
+        L.planc_b200_free(out)
+        return json.loads(s)
 
     def profile(self):
         out = ctypes.c_char_p()

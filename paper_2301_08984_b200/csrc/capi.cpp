@@ -255,6 +255,13 @@ int planc_b200_profile(planc_b200_exec* h, char** json_out) {
   });
 }
 
+int planc_b200_timeline(planc_b200_exec* h, char** json_out) {
+  return guarded([&] {
+    if (!h || !json_out) throw UsageError("null argument");
+    *json_out = dup(h->ex->timeline_json());
+  });
+}
+
 int planc_b200_describe(const char* plan_json, uint32_t flags, char** json_out) {
   return guarded([&] {
     if (!plan_json || !json_out) throw UsageError("null argument");

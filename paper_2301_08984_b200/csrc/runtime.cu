@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstring>
 #include <set>
+#include <sstream>
 #include <stdexcept>
 
 #include "nccl_api.hpp"
@@ -747,6 +748,77 @@ double Executor::run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_b
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);
   return ms / std::max(iters, 1);
+}
+
+std::string Executor::timeline_json() {
+  place_inputs();
+  DeviceGuard dg(lanes_[first_lane_].gpu);
+  for (int g : gpus_) {
+    cudaSetDevice(g);
+    ck(cudaDeviceSynchronize(), "timeline sync");
+  }
+  cudaSetDevice(lanes_[first_lane_].gpu);
+  const std::size_t n = prog_.instrs.size();
+  std::vector<cudaEvent_t> ev0(n, nullptr), ev1(n, nullptr);
+  cudaEvent_t base;
+  ck(cudaEventCreate(&base), "event");
+  ck(cudaEventRecord(base, origin_), "record base");
+  for (int l = 0; l < prog_.num_lanes; ++l)
+    if (owned_[l])
+      for (auto s : lanes_[l].stream) ck(cudaStreamWaitEvent(s, base, 0), "wait base");
+  for (int id : prog_.issue_order) {
+    const int el = exec_lane_[id];
+    if (el < 0) continue;
+    const Instr& in = prog_.instrs[id];
+    cudaSetDevice(lanes_[el].gpu);
+    cudaStream_t s = stream_of(in);
+    for (int d : in.deps) {
+      if (exec_lane_[d] < 0) continue;
+      if (exec_lane_[d] != el || exec_stream_[d] != exec_stream_[id])
+        ck(cudaStreamWaitEvent(s, irt_[d].done ? irt_[d].done : ev1[d], 0), "wait dep");
+    }
+    ck(cudaEventCreate(&ev0[id]), "event");
+    ck(cudaEventCreate(&ev1[id]), "event");
+    ck(cudaEventRecord(ev0[id], s), "record");
+    launch_instr(in, s);
+    ck(cudaEventRecord(ev1[id], s), "record");
+    if (irt_[id].done) ck(cudaEventRecord(irt_[id].done, s), "record done");
+  }
+  for (int g : gpus_) {
+    cudaSetDevice(g);
+    ck(cudaDeviceSynchronize(), "timeline sync");
+  }
+  auto task_kind = [&](const Instr& in) -> const char* {
+    if (in.kind == InstrKind::xfer) return "collective";
+    const OpNode& op = plan_.ops[in.op];
+    switch (op.kind) {
+      case OpKind::recv: return "recv";
+      case OpKind::send: return "send";
+      case OpKind::collective: return "collective";
+      default: return "compute";
+    }
+  };
+  std::ostringstream os;
+  os.precision(9);
+  os << "[";
+  bool first = true;
+  for (int id : prog_.issue_order) {
+    if (!ev0[id]) continue;
+    const Instr& in = prog_.instrs[id];
+    float a = 0, b = 0;
+    ck(cudaEventElapsedTime(&a, base, ev0[id]), "elapsed");
+    ck(cudaEventElapsedTime(&b, base, ev1[id]), "elapsed");
+    os << (first ? "" : ",") << "{\"device\":" << prog_.lane_device[exec_lane_[id]] << ",\"op\":\""
+       << (in.op >= 0 ? plan_.ops[in.op].id : in.label) << "\",\"kind\":\"" << task_kind(in) << "\",\"instr\":\""
+       << instr_kind_name(in.kind) << "\",\"stream\":" << exec_stream_[id] << ",\"start\":" << a * 1e-3
+       << ",\"end\":" << b * 1e-3 << "}";
+    first = false;
+    cudaEventDestroy(ev0[id]);
+    cudaEventDestroy(ev1[id]);
+  }
+  os << "]";
+  cudaEventDestroy(base);
+  return os.str();
 }
 
 std::vector<KernelStat> Executor::profile() {

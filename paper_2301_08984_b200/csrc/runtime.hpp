@@ -82,6 +82,10 @@ class Executor {
   double run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_bytes);
   // Per-kernel-family device time of one eagerly issued, serialised step.
   std::vector<KernelStat> profile();
+  // Measured timeline of one eagerly issued step (streams and overlap as in
+  // a timed step), in the reference simulator's timeline_json shape
+  // (simulate.cpp:373-383): [{device, op, kind, start, end}] in seconds.
+  std::string timeline_json();
   HostTensor get_output(int ptensor);
   // Raw value of one device buffer (a vTensor piece) as doubles.
   std::vector<double> read_buffer(int buffer);
