@@ -33,8 +33,9 @@ def write(name, graph, plan, meta):
     if len(plan) > (2 << 20):  # large plans (C3) are stored gzipped
         import gzip
 
-        with gzip.open(os.path.join(OUT, name + ".plan.json.gz"), "wt", compresslevel=9) as f:
-            f.write(plan)
+        with open(os.path.join(OUT, name + ".plan.json.gz"), "wb") as raw:
+            with gzip.GzipFile(fileobj=raw, mode="wb", compresslevel=9, mtime=0) as f:  # deterministic bytes
+                f.write(plan.encode())
     else:
         with open(os.path.join(OUT, name + ".plan.json"), "w") as f:
             f.write(plan)
@@ -78,6 +79,14 @@ def main():
         plan = refpy.compile_plan(g, strategy="3f1b", devices=2, stages=2, micro_batches=4)
         write(f"c5_3f1b{tag}", g, plan, dict(config="c5", batch=B, hidden=H, stages=2, micro_batches=4,
                                               dtype="bf16", samples_per_step=B, sample="row of the MSA batch"))
+    # Unpartitioned single-lane plans of the C3/C4/C5 graphs at full size: the
+    # partition-invariance property tests compare the partitioned plans
+    # against them (tests/test_fullsize_gpu.py).
+    for name, g in (("c3_ref1", docs.dumps(docs.gpt_stack_doc(8, 32768, 2048, elem_size=2))),
+                    ("c4_ref1", refpy.with_elem_size(refpy.coshard_doc(batch=16384, hidden=512, middle=2048), 2)),
+                    ("c5_ref1", refpy.with_elem_size(refpy.three_pass_doc(layers=4, batch=32768, hidden=256), 2))):
+        plan = refpy.compile_plan(g, strategy="none", devices=1)
+        write(name, g, plan, dict(config=name[:2], strategy="none", dtype="bf16"))
     for B, H, tag in ((16384, 4096, ""), (128, 128, "_cpu")):
         g = refpy.with_elem_size(refpy.mlp_doc(layers=2, batch=B, hidden=H), 2)
         for k in (1, 2, 4, 8):

@@ -1,0 +1,78 @@
+"""Full-size parity through a size-independent property: partition invariance.
+
+At the benchmark shapes the CPU oracle cannot run, so every partitioned plan
+the reference front end emitted (Megatron TP, DP, 1F1B x DP, co-shard,
+3F1B) is checked against the unpartitioned plan of the same graph on the
+same inputs: the terminal outputs (forward output, input gradient, updated
+weights) must agree within the bf16 tolerance, normwise 2e-2 — the
+adapters (all-reduce, P2P, reduce-assemble, concat, split) must neither
+lose nor double-count any partial sum. Inputs follow a standard init
+(weights N(0, 1/fan_in), activations N(0, 1)) so values stay finite in bf16
+through the stacked blocks. All lanes of a plan share cuda:0.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+import paper_2301_08984_b200 as pb  # noqa: E402
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def init_inputs(plan_json, seed=0):
+    p = json.loads(plan_json)
+    vts = {v["id"]: v for v in p["vtensors"]}
+    produced = {vts[v]["ptensor"] for o in p["ops"] for v in o["outputs"]}
+    rng = np.random.default_rng(seed)
+    out = {}
+    for pt in p["ptensors"]:
+        if pt["id"] in produced:
+            continue
+        shp = pt["shape"]
+        x = rng.standard_normal(shp)
+        if pt["kind"] == "weight":
+            x /= np.sqrt(shp[0])
+        out[pt["id"]] = x
+    return out
+
+
+def terminal_outputs(plan_json):
+    p = json.loads(plan_json)
+    vts = {v["id"]: v for v in p["vtensors"]}
+    consumed = {vts[v]["ptensor"] for o in p["ops"] for v in o["inputs"]}
+    produced = {vts[v]["ptensor"] for o in p["ops"] if not o["inserted"] for v in o["outputs"]}
+    return sorted(produced - consumed)
+
+
+def run(plan_json, inputs, ids):
+    nl = len(json.loads(plan_json)["lanes"])
+    with pb.Executor(plan_json, lane_gpus=[0] * nl) as ex:
+        ex.set_inputs(inputs)
+        ex.run(0)
+        return {i: ex.get_output(i) for i in ids}
+
+
+@pytest.mark.parametrize("base,parts", [("c2_tp1", ["c2_tp2", "c2_tp4"]), ("c1l_dp1", ["c1l_dp2"]),
+                                        ("c4_ref1", ["c4_coshard4"]), ("c5_ref1", ["c5_3f1b"]),
+                                        ("c3_ref1", ["c3_pp4dp2"])])
+def test_partition_invariance_at_full_size(base, parts):
+    plan0, _ = bench.load_plan(base)
+    inputs = init_inputs(plan0)
+    ids = terminal_outputs(plan0)
+    assert ids
+    ref = run(plan0, inputs, ids)
+    for name in parts:
+        plan, _ = bench.load_plan(name)
+        assert terminal_outputs(plan) == ids
+        got = run(plan, inputs, ids)
+        for i in ids:
+            assert np.isfinite(got[i]).all(), (name, i)
+        ok, msg = pb.compare_outputs(ref, got, 2e-2, normwise=True)
+        assert ok, f"{name} vs {base}: {msg}"
