@@ -303,13 +303,19 @@ def compare_outputs(expected: dict, actual: dict, rel_tol: float = 0.0, normwise
         if pid not in actual or tuple(np.shape(actual[pid])) != e.shape:
             return False, f"mismatch on tensor {pid} (missing or shape)"
         a = np.asarray(actual[pid], dtype=np.float64)
+        nan_e, nan_a = np.isnan(e), np.isnan(a)
         if rel_tol == 0.0:
-            bad = e != a
-        elif normwise:
-            scale = max(1.0, float(np.abs(e).max())) if e.size else 1.0
-            bad = np.abs(e - a) > rel_tol * scale
+            bad = (e != a) & ~(nan_e & nan_a)
         else:
-            bad = np.abs(e - a) > rel_tol * np.maximum(1.0, np.abs(e))
+            with np.errstate(invalid="ignore"):
+                if normwise:
+                    fin = np.abs(e[np.isfinite(e)])
+                    scale = max(1.0, float(fin.max())) if fin.size else 1.0
+                    bad = ~(np.abs(e - a) <= rel_tol * scale)
+                else:
+                    bad = ~(np.abs(e - a) <= rel_tol * np.maximum(1.0, np.abs(e)))
+            bad &= ~((nan_e & nan_a) | (np.isinf(e) & (e == a)))
+        bad |= nan_e != nan_a  # a NaN on one side only is always a mismatch
         if bad.any():
             idx = np.unravel_index(int(np.argmax(bad)), e.shape)
             return False, (f"mismatch on tensor {pid} at {list(map(int, idx))}: "

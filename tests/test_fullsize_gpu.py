@@ -37,8 +37,9 @@ def init_inputs(plan_json, seed=0):
             continue
         shp = pt["shape"]
         x = rng.standard_normal(shp)
-        if pt["kind"] == "weight":
-            x /= np.sqrt(shp[0])
+        # weights N(0, 1/fan_in); activations / incoming gradients N(0, 0.1^2)
+        # (the block's S = Q*K squares magnitudes, so the stack stays finite)
+        x = x / np.sqrt(shp[0]) if pt["kind"] == "weight" else 0.1 * x
         out[pt["id"]] = x
     return out
 
