@@ -23,6 +23,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -35,15 +36,22 @@ namespace planc_b200 {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BN = 256;
 constexpr int BK = 64;  // 128 bytes of bf16: one 128B swizzle row
-constexpr int STAGES = 4;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
-constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int NUM_THREADS = 192;
-constexpr int TMEM_COLS = 512;  // 2 accumulators x BN fp32 columns
 constexpr int GROUP_M = 8;
+
+// Tile width BN in {256, 128, 64}: smem ring depth fills ~200 KB, TMEM holds
+// two BN-column fp32 accumulators (power of two >= 32 columns).
+template <int BN_>
+struct Cfg {
+  static constexpr int BN = BN_;
+  static constexpr int B_STAGE_BYTES = BN * BK * 2;
+  static constexpr int STAGES_RAW = (200 * 1024) / (A_STAGE_BYTES + B_STAGE_BYTES);
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+};
 
 // ---- PTX wrappers ------------------------------------------------------------
 
@@ -116,7 +124,8 @@ __device__ __forceinline__ std::uint64_t smem_desc(std::uint32_t addr, std::uint
   return d;
 }
 
-// Instruction descriptor: kind::f16, A/B bf16, D f32, M=128, N=256.
+// Instruction descriptor: kind::f16, A/B bf16, D f32, M=128, N=BN.
+template <int BN>
 __host__ __device__ constexpr std::uint32_t make_idesc(bool a_mn, bool b_mn) {
   return (1u << 4)                              // D format f32
          | (1u << 7)                            // A bf16
@@ -192,11 +201,14 @@ __device__ __forceinline__ void store_row_chunk(void* C, int row, int col0, int 
   }
 }
 
-template <bool A_MN, bool B_MN, bool C_BF16>
+template <bool A_MN, bool B_MN, bool C_BF16, int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* __restrict__ C,
                    int m, int n, int k) {
   extern __shared__ std::uint8_t smem_raw[];
+  constexpr int STAGES = Cfg<BN>::STAGES;
+  constexpr int B_STAGE_BYTES = Cfg<BN>::B_STAGE_BYTES;
+  constexpr int TMEM_COLS = Cfg<BN>::TMEM_COLS;
   std::uint8_t* smem =
       reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
   std::uint8_t* sA = smem;
@@ -269,7 +281,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr std::uint32_t idesc = make_idesc(A_MN, B_MN);
+      constexpr std::uint32_t idesc = make_idesc<BN>(A_MN, B_MN);
       int it = 0, local = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
         const int acc = local & 1;
@@ -367,11 +379,12 @@ CUtensorMap make_map(const void* base, std::int64_t rows, std::int64_t cols, int
   return m;
 }
 
-template <bool A_MN, bool B_MN, bool C_BF16>
+template <bool A_MN, bool B_MN, bool C_BF16, int BN>
 void launch_typed(const GemmArgs& a, cudaStream_t s) {
   static unsigned attr_set_mask = 0;  // per device ordinal
   static int num_sms[32] = {0};
-  auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16>;
+  constexpr int SMEM_BYTES = Cfg<BN>::SMEM_BYTES;
+  auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16, BN>;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set_mask & (1u << dev))) {
@@ -394,6 +407,28 @@ void launch_typed(const GemmArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+// Tile width: the candidate minimising (waves over the SMs) x (per-tile MMA
+// time ~ BN, plus a fixed per-tile cost), so narrow / small GEMMs get more,
+// narrower tiles. PLANC_B200_GEMM_BN=256|128|64 forces one (experiments).
+int gemm_sm100_tile_n(const GemmArgs& a) {
+  const char* env = std::getenv("PLANC_B200_GEMM_BN");
+  const int forced = env ? std::atoi(env) : 0;
+  if (forced == 256 || forced == 128 || forced == 64) return forced;
+  const std::int64_t sms = 148;
+  int best = 256;
+  double best_cost = 1e300;
+  for (int bn : {256, 128, 64}) {
+    const std::int64_t tiles = ((a.m + BM - 1) / BM) * ((a.n + bn - 1) / bn);
+    const std::int64_t waves = (tiles + sms - 1) / sms;
+    const double cost = static_cast<double>(waves) * (bn + 64.0);
+    if (cost < best_cost * 0.97) {  // prefer wider tiles unless clearly better
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
+}
+
 bool gemm_sm100_eligible(const GemmArgs& a) {
   if (a.da != DT_BF16 || a.db != DT_BF16 || (a.dc != DT_BF16 && a.dc != DT_F32)) return false;
   if (a.m <= 0 || a.n <= 0 || a.k <= 0) return false;
@@ -409,8 +444,13 @@ bool gemm_sm100_eligible(const GemmArgs& a) {
 
 void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
   const bool a_mn = a.ta, b_mn = !a.tb, cb = a.dc == DT_BF16;
-#define PLANC_TC(AM, BMN, CB) \
-  if (a_mn == AM && b_mn == BMN && cb == CB) return launch_typed<AM, BMN, CB>(a, s);
+  const int bn = gemm_sm100_tile_n(a);
+#define PLANC_TC(AM, BMN, CB)                                                   \
+  if (a_mn == AM && b_mn == BMN && cb == CB) {                                 \
+    if (bn == 256) return launch_typed<AM, BMN, CB, 256>(a, s);                \
+    if (bn == 128) return launch_typed<AM, BMN, CB, 128>(a, s);                \
+    return launch_typed<AM, BMN, CB, 64>(a, s);                                \
+  }
   PLANC_TC(false, false, false)
   PLANC_TC(false, false, true)
   PLANC_TC(false, true, false)

@@ -80,6 +80,7 @@ void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s);
 
 // tcgen05 / TMEM / TMA GEMM (gemm_sm100.cu).
 bool gemm_sm100_eligible(const GemmArgs& a);
+int gemm_sm100_tile_n(const GemmArgs& a);  // 256, 128 or 64
 void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s);
 
 // Dispatch: tcgen05 path when eligible, SIMT tile kernel otherwise.

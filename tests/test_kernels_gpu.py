@@ -53,6 +53,22 @@ def test_gemm_tcgen05_vs_fp64(m, n, k, ta, tb):
     assert err < 2.0 ** -8, err
 
 
+@pytest.mark.parametrize("bn", ["256", "128", "64"])
+@pytest.mark.parametrize("m,n,k,ta,tb", [(304, 520, 200, False, False), (1000, 1000, 1000, True, False),
+                                         (2048, 512, 4096, False, True), (512, 128, 384, True, True)])
+def test_gemm_tcgen05_every_tile_width(bn, m, n, k, ta, tb, monkeypatch):
+    monkeypatch.setenv("PLANC_B200_GEMM_BN", bn)
+    rng = np.random.default_rng(m + n + k)
+    plan, out_pt = matmul_plan(m, n, k, ta, tb)
+    a = bf16_round(rng.standard_normal((k, m) if ta else (m, k)))
+    b = bf16_round(rng.standard_normal((n, k) if tb else (k, n)))
+    out, st = run_single(plan, {0: a, 1: b}, out_pt, flags=pb.NO_GRAPH)
+    assert st["gemm_tc_per_step"] == 1
+    ref = (a.T if ta else a) @ (b.T if tb else b)
+    err = np.abs(out - ref).max() / max(1.0, np.abs(ref).max())
+    assert err < 2.0 ** -8, err
+
+
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, True)])
 def test_gemm_tcgen05_fp32_output(ta, tb):
     m, n, k = 384, 512, 320

@@ -23,6 +23,10 @@ SHAPES = [  # (name, m, n, k, ta, tb)
     ("bwd Fa^T.dY", F, H, T, True, False),
     ("bwd X2^T.dF1", H, F, T, True, False),
     ("bwd X^T.dQ", H, H, T, True, False),
+    ("c4 shard X.W1", 16384, 512, 512, False, False),
+    ("c4 shard dT^T", 512, 512, 16384, True, False),
+    ("c5 mb X.W", 8192, 256, 256, False, False),
+    ("c5 mb dX", 8192, 256, 256, False, True),
 ]
 
 
@@ -54,12 +58,21 @@ def cublas(m, n, k, ta, tb, iters=30):
     return e0.elapsed_time(e1) / iters
 
 
+import os  # noqa: E402
+
 rows = []
 for name, m, n, k, ta, tb in SHAPES:
     fl = 2.0 * m * n * k
-    o = ours(m, n, k, ta, tb)
+    row = {"gemm": name, "m": m, "n": n, "k": k, "ta": ta, "tb": tb}
+    for bn in ("auto", "256", "128", "64"):
+        if bn == "auto":
+            os.environ.pop("PLANC_B200_GEMM_BN", None)
+        else:
+            os.environ["PLANC_B200_GEMM_BN"] = bn
+        o = ours(m, n, k, ta, tb)
+        row[f"ours_{bn}_tflops"] = round(fl / o / 1e9, 1)
+    os.environ.pop("PLANC_B200_GEMM_BN", None)
     c = cublas(m, n, k, ta, tb)
-    rows.append({"gemm": name, "m": m, "n": n, "k": k, "ta": ta, "tb": tb, "ours_ms": round(o, 4),
-                 "ours_tflops": round(fl / o / 1e9, 1), "cublas_ms": round(c, 4),
-                 "cublas_tflops": round(fl / c / 1e9, 1)})
+    row["cublas_tflops"] = round(fl / c / 1e9, 1)
+    rows.append(row)
 print(json.dumps(rows, indent=1))
