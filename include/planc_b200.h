@@ -140,6 +140,11 @@ int planc_b200_profile(planc_b200_exec* h, char** json_out);
  * Caller frees with planc_b200_free. */
 int planc_b200_timeline(planc_b200_exec* h, char** json_out);
 
+/* Host-only: which GEMM path a matmul of this shape takes — tcgen05 tensor
+ * cores (1) or the SIMT kernel (0) — and the tensor-core tile width. */
+int planc_b200_gemm_config(int64_t m, int64_t n, int64_t k, int ta, int tb, int a_bf16, int b_bf16, int c_bf16,
+                           int* tensor_cores, int* tile_n);
+
 /* Host-only lowering (no GPU needed): the executor's device program for a
  * plan as JSON — buffers, instructions, box cells, issue order. */
 int planc_b200_describe(const char* plan_json, uint32_t flags, char** json_out);

@@ -255,6 +255,23 @@ int planc_b200_profile(planc_b200_exec* h, char** json_out) {
   });
 }
 
+int planc_b200_gemm_config(int64_t m, int64_t n, int64_t k, int ta, int tb, int a_bf16, int b_bf16, int c_bf16,
+                           int* tensor_cores, int* tile_n) {
+  GemmArgs a{};
+  a.m = m;
+  a.n = n;
+  a.k = k;
+  a.ta = ta != 0;
+  a.tb = tb != 0;
+  a.da = a_bf16 ? DT_BF16 : DT_F32;
+  a.db = b_bf16 ? DT_BF16 : DT_F32;
+  a.dc = c_bf16 ? DT_BF16 : DT_F32;
+  const bool tc = gemm_sm100_eligible(a);
+  if (tensor_cores) *tensor_cores = tc ? 1 : 0;
+  if (tile_n) *tile_n = tc ? gemm_sm100_tile_n(a) : 0;
+  return PLANC_B200_OK;
+}
+
 int planc_b200_timeline(planc_b200_exec* h, char** json_out) {
   return guarded([&] {
     if (!h || !json_out) throw UsageError("null argument");
