@@ -36,6 +36,7 @@ NO_GRAPH = 0x1
 NO_TENSOR_CORES = 0x2
 STRICT_VALUE = 0x4
 SERIAL_LANES = 0x8
+NO_FUSION = 0x10
 
 
 class PlancError(RuntimeError):
@@ -129,7 +130,7 @@ def version() -> str:
     return _load().planc_b200_version().decode()
 
 
-def describe(plan_json: str, strict_value: bool = False, lane_rank=None) -> dict:
+def describe(plan_json: str, strict_value: bool = False, lane_rank=None, flags: int = 0) -> dict:
     """Host-only lowering of a plan (no GPU): buffers, instructions, cells.
 
     With ``lane_rank`` (owner rank per plan lane) the one-process-per-GPU
@@ -137,7 +138,7 @@ def describe(plan_json: str, strict_value: bool = False, lane_rank=None) -> dict
     """
     L = _load()
     out = ctypes.c_void_p()
-    flags = STRICT_VALUE if strict_value else 0
+    flags = flags | (STRICT_VALUE if strict_value else 0)
     if lane_rank is None:
         _check(L.planc_b200_describe(plan_json.encode(), flags, ctypes.byref(out)))
     else:

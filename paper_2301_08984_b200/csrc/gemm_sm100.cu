@@ -161,6 +161,87 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nb = r / gm;
 }
 
+__device__ __forceinline__ float epi_apply(int op, float a, float b) {
+  return op == 0 ? a + b : op == 1 ? a * b : fmaxf(a, b);
+}
+
+__device__ __forceinline__ std::uint32_t bf16_pair(float lo, float hi) {
+  return static_cast<std::uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(lo))) |
+         (static_cast<std::uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(hi))) << 16);
+}
+
+__device__ __forceinline__ void bf16_unpair(std::uint32_t w, float& lo, float& hi) {
+  lo = __uint_as_float(w << 16);
+  hi = __uint_as_float(w & 0xffff0000u);
+}
+
+// bf16 output chunk of 32 columns plus the fused elementwise consumers of
+// the same 32 elements (all operands [m, n] row-major bf16). Every operand
+// index is static so nothing leaves registers.
+__device__ __forceinline__ void store_row_chunk_fused(void* C, int row, int col0, int m, int n,
+                                                      const std::uint32_t (&r)[32], const EpiParams& epi) {
+  if (row >= m || col0 >= n) return;
+  const std::int64_t off = static_cast<std::int64_t>(row) * n + col0;
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(C) + off;
+  if (col0 + 32 <= n) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      std::uint32_t w[4];
+      float c[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        w[e] = bf16_pair(__uint_as_float(r[v * 8 + 2 * e]), __uint_as_float(r[v * 8 + 2 * e + 1]));
+        bf16_unpair(w[e], c[2 * e], c[2 * e + 1]);  // the stored (rounded) value feeds the consumers
+      }
+      *reinterpret_cast<uint4*>(out + v * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+      for (int o = 0; o < kMaxEpiOps; ++o) {
+        if (o >= epi.n_ops) break;
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < kMaxEpiIn; ++i) {
+          if (i >= epi.ops[o].n_in) break;
+          float x[8];
+          if (i == epi.ops[o].gemm_pos) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = c[j];
+          } else {
+            const uint4 q =
+                __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(epi.ops[o].in[i]) + off + v * 8));
+            bf16_unpair(q.x, x[0], x[1]);
+            bf16_unpair(q.y, x[2], x[3]);
+            bf16_unpair(q.z, x[4], x[5]);
+            bf16_unpair(q.w, x[6], x[7]);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = i == 0 ? x[j] : epi_apply(epi.ops[o].op, acc[j], x[j]);
+        }
+        *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.ops[o].out) + off + v * 8) =
+            make_uint4(bf16_pair(acc[0], acc[1]), bf16_pair(acc[2], acc[3]), bf16_pair(acc[4], acc[5]),
+                       bf16_pair(acc[6], acc[7]));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      if (col0 + e >= n) continue;  // static e keeps r[] in registers
+      const __nv_bfloat16 h = __float2bfloat16_rn(__uint_as_float(r[e]));
+      out[e] = h;
+      const float cv = __bfloat162float(h);
+      for (int o = 0; o < epi.n_ops; ++o) {
+        float acc = 0.f;
+        for (int i = 0; i < epi.ops[o].n_in; ++i) {
+          const float x = i == epi.ops[o].gemm_pos
+                              ? cv
+                              : __bfloat162float(static_cast<const __nv_bfloat16*>(epi.ops[o].in[i])[off + e]);
+          acc = i == 0 ? x : epi_apply(epi.ops[o].op, acc, x);
+        }
+        static_cast<__nv_bfloat16*>(epi.ops[o].out)[off + e] = __float2bfloat16_rn(acc);
+      }
+    }
+  }
+}
+
 template <bool C_BF16>
 __device__ __forceinline__ void store_row_chunk(void* C, int row, int col0, int m, int n, const std::uint32_t (&r)[32]) {
   if (row >= m || col0 >= n) return;
@@ -201,10 +282,10 @@ __device__ __forceinline__ void store_row_chunk(void* C, int row, int col0, int 
   }
 }
 
-template <bool A_MN, bool B_MN, bool C_BF16, int BN>
+template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* __restrict__ C,
-                   int m, int n, int k) {
+                   int m, int n, int k, const __grid_constant__ EpiParams epi) {
   extern __shared__ std::uint8_t smem_raw[];
   constexpr int STAGES = Cfg<BN>::STAGES;
   constexpr int B_STAGE_BYTES = Cfg<BN>::B_STAGE_BYTES;
@@ -335,7 +416,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        store_row_chunk<C_BF16>(C, row, nb * BN + c * 32, m, n, r);
+        if constexpr (FUSE) {
+          store_row_chunk_fused(C, row, nb * BN + c * 32, m, n, r, epi);
+        } else {
+          store_row_chunk<C_BF16>(C, row, nb * BN + c * 32, m, n, r);
+        }
       }
     }
   }
@@ -379,12 +464,12 @@ CUtensorMap make_map(const void* base, std::int64_t rows, std::int64_t cols, int
   return m;
 }
 
-template <bool A_MN, bool B_MN, bool C_BF16, int BN>
+template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 void launch_typed(const GemmArgs& a, cudaStream_t s) {
   static unsigned attr_set_mask = 0;  // per device ordinal
   static int num_sms[32] = {0};
   constexpr int SMEM_BYTES = Cfg<BN>::SMEM_BYTES;
-  auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16, BN>;
+  auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16, BN, FUSE>;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set_mask & (1u << dev))) {
@@ -400,7 +485,7 @@ void launch_typed(const GemmArgs& a, cudaStream_t s) {
   const std::int64_t tiles = ((a.m + BM - 1) / BM) * ((a.n + BN - 1) / BN);
   const int grid = static_cast<int>(std::min<std::int64_t>(tiles, num_sms[dev & 31] > 0 ? num_sms[dev & 31] : 148));
   kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, a.C, static_cast<int>(a.m), static_cast<int>(a.n),
-                                              static_cast<int>(a.k));
+                                              static_cast<int>(a.k), a.epi);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc_kernel: ") + cudaGetErrorString(e));
 }
@@ -445,11 +530,25 @@ bool gemm_sm100_eligible(const GemmArgs& a) {
 void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
   const bool a_mn = a.ta, b_mn = !a.tb, cb = a.dc == DT_BF16;
   const int bn = gemm_sm100_tile_n(a);
+  if (a.epi.n_ops > 0) {
+    if (!cb) throw std::runtime_error("fused GEMM epilogue needs a bf16 output");
+#define PLANC_TCF(AM, BMN)                                                      \
+  if (a_mn == AM && b_mn == BMN) {                                             \
+    if (bn == 256) return launch_typed<AM, BMN, true, 256, true>(a, s);        \
+    if (bn == 128) return launch_typed<AM, BMN, true, 128, true>(a, s);        \
+    return launch_typed<AM, BMN, true, 64, true>(a, s);                        \
+  }
+    PLANC_TCF(false, false)
+    PLANC_TCF(false, true)
+    PLANC_TCF(true, false)
+    PLANC_TCF(true, true)
+#undef PLANC_TCF
+  }
 #define PLANC_TC(AM, BMN, CB)                                                   \
   if (a_mn == AM && b_mn == BMN && cb == CB) {                                 \
-    if (bn == 256) return launch_typed<AM, BMN, CB, 256>(a, s);                \
-    if (bn == 128) return launch_typed<AM, BMN, CB, 128>(a, s);                \
-    return launch_typed<AM, BMN, CB, 64>(a, s);                                \
+    if (bn == 256) return launch_typed<AM, BMN, CB, 256, false>(a, s);         \
+    if (bn == 128) return launch_typed<AM, BMN, CB, 128, false>(a, s);         \
+    return launch_typed<AM, BMN, CB, 64, false>(a, s);                         \
   }
   PLANC_TC(false, false, false)
   PLANC_TC(false, false, true)

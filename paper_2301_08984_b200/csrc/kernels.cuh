@@ -49,6 +49,24 @@ struct DevChunk {
   std::int64_t count;  // in vector units
 };
 
+// Elementwise ops fused into a GEMM's epilogue (bf16): out = fold(op, in[0..n_in))
+// where in[gemm_pos] is the GEMM's own bf16-rounded output value and the
+// other operands are [m, n] row-major bf16 tensors read in place — the same
+// bits the separate elementwise kernel would produce.
+constexpr int kMaxEpiOps = 2;
+constexpr int kMaxEpiIn = 4;
+struct EpiOp {
+  int op = 0;  // 0 add, 1 mul, 2 max
+  int n_in = 0;
+  int gemm_pos = 0;
+  const void* in[kMaxEpiIn] = {};
+  void* out = nullptr;
+};
+struct EpiParams {
+  int n_ops = 0;
+  EpiOp ops[kMaxEpiOps];
+};
+
 struct GemmArgs {
   const void* A;
   const void* B;
@@ -56,6 +74,7 @@ struct GemmArgs {
   std::int64_t m, n, k;
   bool ta, tb;
   int da, db, dc;
+  EpiParams epi;
 };
 
 // Launchers (all asynchronous on `s`).

@@ -717,7 +717,82 @@ struct Builder {
 Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt) {
   Builder b(plan, opt);
   b.run();
+  if (opt.fuse_epilogues) fuse_gemm_epilogues(b.P, opt);
   return std::move(b.P);
+}
+
+void fuse_gemm_epilogues(Program& P, const ProgramOptions& opt) {
+  std::vector<int> redirect(P.instrs.size(), -1);  // fused ew -> its GEMM
+  for (auto& e : P.instrs) {
+    if (e.kind != InstrKind::ew || e.in_bufs.size() > 4 || e.out_bufs.size() != 1) continue;
+    if (P.buffers[e.out_bufs[0]].dtype != DType::bf16) continue;
+    // The latest-issued GEMM among the operands' producers, same lane, bf16.
+    int g = -1, pos = -1;
+    for (std::size_t i = 0; i < e.in_bufs.size(); ++i) {
+      const BufferDesc& b = P.buffers[e.in_bufs[i]];
+      if (b.dtype != DType::bf16 || b.producer < 0) continue;
+      const Instr& cand = P.instrs[b.producer];
+      if (cand.kind != InstrKind::gemm || cand.lane != e.lane || cand.out_bufs[0] != e.in_bufs[i]) continue;
+      if (cand.m * cand.n != e.count || cand.fused.size() >= 2) continue;
+      if (std::count(e.in_bufs.begin(), e.in_bufs.end(), e.in_bufs[i]) != 1) continue;
+      if (cand.id > g) {
+        g = cand.id;
+        pos = static_cast<int>(i);
+      }
+    }
+    if (g < 0) continue;
+    Instr& G = P.instrs[g];
+    const DType da = P.buffers[G.in_bufs[0]].dtype, db = P.buffers[G.in_bufs[1]].dtype;
+    if (!opt.gemm_fusable || !opt.gemm_fusable(G, da, db, DType::bf16)) continue;
+    // Other operands must be produced before the GEMM issues.
+    bool ready = true;
+    std::set<int> extra;
+    for (std::size_t i = 0; i < e.in_bufs.size(); ++i) {
+      if (static_cast<int>(i) == pos) continue;
+      const int pr = P.buffers[e.in_bufs[i]].producer;
+      if (pr < 0) continue;
+      const int pr_eff = redirect[pr] >= 0 ? redirect[pr] : pr;
+      if (pr_eff >= g) ready = false;
+      extra.insert(pr_eff);
+    }
+    if (!ready) continue;
+    Instr::FusedEw f;
+    f.ew_instr = e.id;
+    f.op = e.ew;
+    f.in_bufs = e.in_bufs;
+    f.gemm_pos = pos;
+    f.out_buf = e.out_bufs[0];
+    G.fused.push_back(f);
+    for (int d : extra)
+      if (d != g && std::find(G.deps.begin(), G.deps.end(), d) == G.deps.end()) G.deps.push_back(d);
+    std::sort(G.deps.begin(), G.deps.end());
+    G.out_bufs.push_back(f.out_buf);
+    G.bytes += e.bytes - static_cast<double>(P.buffers[e.in_bufs[pos]].bytes);  // C is not re-read
+    G.label += "+" + e.label;
+    P.buffers[f.out_buf].producer = g;
+    redirect[e.id] = g;
+    e.kind = InstrKind::nop;
+    e.deps.clear();
+    e.in_bufs.clear();
+    e.out_bufs.clear();
+    e.bytes = 0;
+    e.flops = 0;
+  }
+  // Consumers of a fused op now wait for its GEMM.
+  for (auto& in : P.instrs) {
+    bool changed = false;
+    for (int& d : in.deps) {
+      if (redirect[d] >= 0) {
+        d = redirect[d];
+        changed = true;
+      }
+    }
+    if (changed) {
+      std::sort(in.deps.begin(), in.deps.end());
+      in.deps.erase(std::unique(in.deps.begin(), in.deps.end()), in.deps.end());
+      in.deps.erase(std::remove(in.deps.begin(), in.deps.end(), in.id), in.deps.end());
+    }
+  }
 }
 
 Program localize(const Program& g, const std::vector<int>& lane_rank) {
@@ -930,7 +1005,15 @@ std::string Program::describe_json() const {
        << ",\"axis_len\":" << in.axis_len << ",\"inner\":" << in.inner << ",\"n_idx\":" << in.n_idx
        << ",\"rows\":" << in.rows << ",\"h\":" << in.h << ",\"lo\":" << in.lo << ",\"flops\":" << in.flops
        << ",\"bytes\":" << in.bytes << ",\"wire_bytes\":" << in.wire_bytes << ",\"coll_group\":" << in.coll_group
-       << ",\"allreduce\":" << (in.allreduce ? "true" : "false")
+       << ",\"allreduce\":" << (in.allreduce ? "true" : "false") << ",\"fused\":[";
+    for (std::size_t f = 0; f < in.fused.size(); ++f) {
+      const auto& fe = in.fused[f];
+      os << (f ? "," : "") << "{\"ew_instr\":" << fe.ew_instr << ",\"ew\":" << static_cast<int>(fe.op)
+         << ",\"pos\":" << fe.gemm_pos << ",\"out\":" << fe.out_buf << ",\"in\":[";
+      for (std::size_t j = 0; j < fe.in_bufs.size(); ++j) os << (j ? "," : "") << fe.in_bufs[j];
+      os << "]}";
+    }
+    os << "]"
        << ",\"xfers\":[";
     for (std::size_t x = 0; x < in.xfers.size(); ++x) {
       const auto& xf = in.xfers[x];

@@ -117,6 +117,17 @@ struct Instr {
   // and every dst receives the sum of all srcs (ncclAllReduce).
   std::vector<Xfer> xfers;
   bool allreduce = false;
+  // gemm: elementwise consumers computed in this GEMM's epilogue (the fused
+  // ew instruction becomes a nop). Operand `gemm_pos` of each is the GEMM's
+  // own (output-rounded) value; the others are read in place.
+  struct FusedEw {
+    int ew_instr = -1;
+    EwOp op = EwOp::add;
+    std::vector<int> in_bufs;  // in fold order; in_bufs[gemm_pos] == this GEMM's output
+    int gemm_pos = 0;
+    int out_buf = -1;
+  };
+  std::vector<FusedEw> fused;
   // accounting (algorithmic, from masks)
   double flops = 0;
   double bytes = 0;       // HBM bytes read + written
@@ -127,6 +138,11 @@ struct Instr {
 struct ProgramOptions {
   bool value_split_extension = true;  // V(m*v) -> V(v) sums
   bool honor_sync_edges = true;
+  // Fuse elementwise ops that consume a fresh GEMM output on the same lane
+  // into that GEMM's epilogue (local form), for GEMMs the
+  // predicate accepts (the tensor-core path implements the fused epilogue).
+  bool fuse_epilogues = false;
+  bool (*gemm_fusable)(const Instr& gemm, DType a, DType b, DType c) = nullptr;
 };
 
 struct Program {
@@ -151,6 +167,12 @@ struct Program {
 };
 
 Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt = {});
+
+// Epilogue fusion pass (run by build_program when opt.fuse_epilogues): an
+// elementwise op whose operand is a bf16 GEMM output on the same lane, whose
+// other operands are ready before that GEMM, is computed in the GEMM's
+// epilogue; the op's instruction becomes a nop.
+void fuse_gemm_epilogues(Program& p, const ProgramOptions& opt);
 
 // One-process-per-GPU lowering: the same global program on every rank, with
 // every box term that lives on another rank's lane redirected to a shadow

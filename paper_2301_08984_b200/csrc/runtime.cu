@@ -88,12 +88,34 @@ struct DeviceGuard {
 
 }  // namespace
 
+namespace {
+bool tc_fusable(const Instr& g, DType a, DType b, DType c) {
+  GemmArgs x{};
+  x.m = g.m;
+  x.n = g.n;
+  x.k = g.k;
+  x.ta = g.ta;
+  x.tb = g.tb;
+  x.da = dt_of(a);
+  x.db = dt_of(b);
+  x.dc = dt_of(c);
+  return c == DType::bf16 && gemm_sm100_eligible(x);
+}
+}  // namespace
+
+ProgramOptions program_options(bool value_split_extension, bool fuse_epilogues) {
+  ProgramOptions po;
+  po.value_split_extension = value_split_extension;
+  po.fuse_epilogues = fuse_epilogues;
+  po.gemm_fusable = &tc_fusable;
+  return po;
+}
+
 Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gpu, const ExecOptions& opt,
                    const RankConfig* rank)
     : opt_(opt) {
   plan_ = load_plan(plan_json);
-  ProgramOptions po;
-  po.value_split_extension = opt.value_split_extension;
+  ProgramOptions po = program_options(opt.value_split_extension, opt.fuse_epilogues && opt.allow_tensor_cores);
   prog_ = build_program(plan_, po);
   if (rank) {
     rank_mode_ = true;
@@ -483,6 +505,19 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
       a.da = dt_of(prog_.buffers[in.in_bufs[0]].dtype);
       a.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
       a.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
+      a.epi.n_ops = static_cast<int>(in.fused.size());
+      for (std::size_t f = 0; f < in.fused.size(); ++f) {
+        const auto& fe = in.fused[f];
+        EpiOp& o = a.epi.ops[f];
+        o.op = static_cast<int>(fe.op);
+        o.n_in = static_cast<int>(fe.in_bufs.size());
+        o.gemm_pos = fe.gemm_pos;
+        for (std::size_t j = 0; j < fe.in_bufs.size(); ++j) o.in[j] = buf_ptr(fe.in_bufs[j]);
+        o.out = buf_ptr(fe.out_buf);
+      }
+      if (a.epi.n_ops > 0 && !(opt_.allow_tensor_cores && gemm_sm100_eligible(a))) {
+        throw InternalError("fused epilogue on a GEMM the tensor-core path does not take");
+      }
       launch_gemm(a, s, opt_.allow_tensor_cores, nullptr);
       return;
     }

@@ -48,7 +48,12 @@ struct ExecOptions {
   bool allow_tensor_cores = true;
   bool value_split_extension = true;
   int streams_per_lane = kLaneStreams;  // 1 = issue a lane strictly in plan order
+  bool fuse_epilogues = true;           // elementwise consumers computed in GEMM epilogues
 };
+
+// ProgramOptions as the executor uses them: epilogue fusion only for GEMMs
+// the tcgen05 path takes (it implements the fused epilogue).
+ProgramOptions program_options(bool value_split_extension, bool fuse_epilogues);
 
 // One-process-per-GPU mode: this process owns the lanes with
 // lane_rank[l] == rank, all on `local_gpu`; pieces owned by other ranks

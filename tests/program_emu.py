@@ -59,6 +59,11 @@ def run_program(desc: dict, plan: dict, inputs: dict, owned_lanes=None, exchange
             a = a.T if ins["ta"] else a
             b = b.T if ins["tb"] else b
             data[ins["out"][0]] = (a @ b).reshape(-1)
+            for f in ins.get("fused", []):  # elementwise consumers run in the GEMM epilogue
+                out = data[f["in"][0]].copy()
+                for x in f["in"][1:]:
+                    out = (out + data[x], out * data[x], np.maximum(out, data[x]))[f["ew"]]
+                data[f["out"]] = out
         elif k == "ew":
             out = data[ins["in"][0]].copy()
             for x in ins["in"][1:]:
