@@ -44,9 +44,9 @@ extern "C" {
 #define PLANC_B200_NO_TENSOR_CORES 0x2u /* force the SIMT GEMM (debug / A-B checks) */
 #define PLANC_B200_STRICT_VALUE 0x4u    /* reference value-part rule only: V(m*v)->V(v) pieces are
                                            skipped like refexec.cpp:110-117 instead of summed */
-#define PLANC_B200_NO_FUSION 0x10u      /* keep every elementwise op its own kernel (default: an
-                                           op consuming a fresh bf16 GEMM output on the same lane
-                                           runs in that GEMM's epilogue; same bits either way) */
+#define PLANC_B200_FUSE_EPILOGUES 0x10u /* an elementwise op consuming a fresh bf16 GEMM output on
+                                           the same lane runs in that GEMM's epilogue (same bits as
+                                           the separate kernel; default: every op its own kernel) */
 #define PLANC_B200_SERIAL_LANES 0x8u    /* one stream per lane: a lane's tasks run strictly in plan
                                            order (default: only data dependencies and sync edges order
                                            a lane's work, spread over several streams) */

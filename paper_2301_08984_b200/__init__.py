@@ -36,7 +36,7 @@ NO_GRAPH = 0x1
 NO_TENSOR_CORES = 0x2
 STRICT_VALUE = 0x4
 SERIAL_LANES = 0x8
-NO_FUSION = 0x10
+FUSE_EPILOGUES = 0x10
 
 
 class PlancError(RuntimeError):

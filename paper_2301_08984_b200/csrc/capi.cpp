@@ -69,7 +69,7 @@ int planc_b200_open(const char* plan_json, const int* lane_gpu, int num_lane_gpu
     opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
     opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
     if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
-    if (flags & PLANC_B200_NO_FUSION) opt.fuse_epilogues = false;
+    opt.fuse_epilogues = (flags & PLANC_B200_FUSE_EPILOGUES) != 0;
     std::vector<int> lanes;
     for (int i = 0; lane_gpu && i < num_lane_gpu; ++i) lanes.push_back(lane_gpu[i]);
     auto* h = new planc_b200_exec;
@@ -101,7 +101,7 @@ int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* 
     opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
     opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
     if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
-    if (flags & PLANC_B200_NO_FUSION) opt.fuse_epilogues = false;
+    opt.fuse_epilogues = (flags & PLANC_B200_FUSE_EPILOGUES) != 0;
     RankConfig rc;
     rc.rank = rank;
     rc.world = world;
@@ -124,7 +124,8 @@ int planc_b200_describe_rank(const char* plan_json, const int* lane_rank, int nu
   return guarded([&] {
     if (!plan_json || !json_out || !lane_rank) throw UsageError("null argument");
     ProgramOptions po = program_options((flags & PLANC_B200_STRICT_VALUE) == 0,
-                                        (flags & (PLANC_B200_NO_FUSION | PLANC_B200_NO_TENSOR_CORES)) == 0);
+                                        (flags & PLANC_B200_FUSE_EPILOGUES) != 0 &&
+                                            (flags & PLANC_B200_NO_TENSOR_CORES) == 0);
     ExecutionPlan plan = load_plan(plan_json);
     Program p = localize(build_program(plan, po), std::vector<int>(lane_rank, lane_rank + num_lanes));
     *json_out = dup(p.describe_json());
@@ -285,7 +286,8 @@ int planc_b200_describe(const char* plan_json, uint32_t flags, char** json_out) 
   return guarded([&] {
     if (!plan_json || !json_out) throw UsageError("null argument");
     ProgramOptions po = program_options((flags & PLANC_B200_STRICT_VALUE) == 0,
-                                        (flags & (PLANC_B200_NO_FUSION | PLANC_B200_NO_TENSOR_CORES)) == 0);
+                                        (flags & PLANC_B200_FUSE_EPILOGUES) != 0 &&
+                                            (flags & PLANC_B200_NO_TENSOR_CORES) == 0);
     ExecutionPlan plan = load_plan(plan_json);
     Program p = build_program(plan, po);
     *json_out = dup(p.describe_json());
