@@ -32,10 +32,11 @@ def test_library_exports_every_declared_symbol():
     assert "sm_100a" in pb.version()
 
 
+@pytest.mark.parametrize("flags", [0, pb.FUSE_EPILOGUES])
 @pytest.mark.parametrize("name", golden_cases.names())
-def test_lowered_program_reproduces_reference(name):
+def test_lowered_program_reproduces_reference(name, flags):
     g = golden_cases.load(name)
-    desc = pb.describe(g["plan"])
+    desc = pb.describe(g["plan"], flags=flags)
     out = run_program(desc, json.loads(g["plan"]), g["inputs"])
     # float64 interpretation: exact unless values outgrow 2^53 (summation order)
     tol = 0.0 if g["meta"].get("max_abs", 0) < 2.0 ** 53 else 1e-12
