@@ -49,7 +49,10 @@ struct Cfg {
   static constexpr int B_STAGE_BYTES = BN * BK * 2;
   static constexpr int STAGES_RAW = (200 * 1024) / (A_STAGE_BYTES + B_STAGE_BYTES);
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+  // + epilogue staging: 4 warps x 2 buffers x (32 rows x 32 cols, <= 4 B)
+  static constexpr int STAGING_BYTES = 4 * 2 * 4096;
+  static constexpr int SMEM_BYTES =
+      STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + STAGING_BYTES + 1024 /*align*/ + 1024 /*barriers + align*/;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
 };
 
@@ -92,6 +95,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
           smem_u32(dst)),
       "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Bulk tensor store smem -> global (clips rows / cols outside the tensor).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<std::uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -284,8 +296,9 @@ __device__ __forceinline__ void store_row_chunk(void* C, int row, int col0, int 
 
 template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* __restrict__ C,
-                   int m, int n, int k, const __grid_constant__ EpiParams epi) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, void* __restrict__ C, int m, int n, int k,
+                   const __grid_constant__ EpiParams epi) {
   extern __shared__ std::uint8_t smem_raw[];
   constexpr int STAGES = Cfg<BN>::STAGES;
   constexpr int B_STAGE_BYTES = Cfg<BN>::B_STAGE_BYTES;
@@ -294,7 +307,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
   std::uint8_t* sA = smem;
   std::uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sB + STAGES * B_STAGE_BYTES);
+  // Epilogue staging (1024-aligned: the 64B / 128B swizzle atoms of the C map).
+  std::uint8_t* staging = sB + STAGES * B_STAGE_BYTES;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(staging + Cfg<BN>::STAGING_BYTES);
   std::uint64_t* empty = full + STAGES;
   std::uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
   std::uint64_t* tempty = tfull + 2;      // [2] accumulator drained
@@ -396,7 +411,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // Epilogue warps 2..5: warp w may only touch TMEM lanes 32*(w%4)..+31.
+    // Each 32x32 output chunk goes TMEM -> registers -> swizzled smem
+    // staging (conflict-free 16-byte stores) -> one TMA bulk tensor store
+    // (coalesced, clipped at the tensor edge); two staging buffers per warp
+    // keep a store in flight while the next chunk is converted.
     const int q = warp % 4;
+    std::uint8_t* stg = staging + (warp - 2) * 2 * 4096;
+    int sb = 0;
     int local = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
       int mb, nb;
@@ -419,10 +440,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if constexpr (FUSE) {
           store_row_chunk_fused(C, row, nb * BN + c * 32, m, n, r, epi);
         } else {
-          store_row_chunk<C_BF16>(C, row, nb * BN + c * 32, m, n, r);
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer sb is free
+          __syncwarp();
+          std::uint8_t* buf = stg + sb * 4096;
+          if constexpr (C_BF16) {
+            // 64 B rows, SWIZZLE_64B: 16-byte chunk v lands at v ^ ((row >> 1) & 3).
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const uint4 w = make_uint4(bf16_pair(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1])),
+                                         bf16_pair(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
+                                         bf16_pair(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
+                                         bf16_pair(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
+              *reinterpret_cast<uint4*>(buf + lane * 64 + ((v ^ ((lane >> 1) & 3)) << 4)) = w;
+            }
+          } else {
+            // 128 B rows, SWIZZLE_128B: 16-byte chunk v lands at v ^ (row & 7).
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              *reinterpret_cast<uint4*>(buf + lane * 128 + ((v ^ (lane & 7)) << 4)) =
+                  make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
+          __syncwarp();
+          if (lane == 0) tma_store_2d(&tmC, buf, nb * BN + c * 32, mb * BM + q * 32);
+          sb ^= 1;
         }
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
   }
   tc_fence_before();
   __syncthreads();
@@ -464,6 +510,24 @@ CUtensorMap make_map(const void* base, std::int64_t rows, std::int64_t cols, int
   return m;
 }
 
+// Output map for the staged epilogue: [m][n] row-major, 32x32 boxes,
+// 64B swizzle for bf16 rows (64 B), 128B swizzle for fp32 rows (128 B).
+CUtensorMap make_store_map(void* base, std::int64_t m, std::int64_t n, bool bf16) {
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  const std::int64_t es = bf16 ? 2 : 4;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(m)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(n * es)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base,
+                           dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (C) failed: " + std::to_string(r));
+  return map;
+}
+
 template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 void launch_typed(const GemmArgs& a, cudaStream_t s) {
   static unsigned attr_set_mask = 0;  // per device ordinal
@@ -482,9 +546,10 @@ void launch_typed(const GemmArgs& a, cudaStream_t s) {
   // (MN-major) or, transposed, [n][k] (K-major).
   CUtensorMap ma = A_MN ? make_map(a.A, a.k, a.m, BK) : make_map(a.A, a.m, a.k, BM);
   CUtensorMap mb = B_MN ? make_map(a.B, a.k, a.n, BK) : make_map(a.B, a.n, a.k, BN);
+  CUtensorMap mc = make_store_map(a.C, a.m, a.n, C_BF16);
   const std::int64_t tiles = ((a.m + BM - 1) / BM) * ((a.n + BN - 1) / BN);
   const int grid = static_cast<int>(std::min<std::int64_t>(tiles, num_sms[dev & 31] > 0 ? num_sms[dev & 31] : 148));
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, a.C, static_cast<int>(a.m), static_cast<int>(a.n),
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, mc, a.C, static_cast<int>(a.m), static_cast<int>(a.n),
                                               static_cast<int>(a.k), a.epi);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc_kernel: ") + cudaGetErrorString(e));
