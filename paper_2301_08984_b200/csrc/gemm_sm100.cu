@@ -187,113 +187,6 @@ __device__ __forceinline__ void bf16_unpair(std::uint32_t w, float& lo, float& h
   hi = __uint_as_float(w & 0xffff0000u);
 }
 
-// bf16 output chunk of 32 columns plus the fused elementwise consumers of
-// the same 32 elements (all operands [m, n] row-major bf16). Every operand
-// index is static so nothing leaves registers.
-__device__ __forceinline__ void store_row_chunk_fused(void* C, int row, int col0, int m, int n,
-                                                      const std::uint32_t (&r)[32], const EpiParams& epi) {
-  if (row >= m || col0 >= n) return;
-  const std::int64_t off = static_cast<std::int64_t>(row) * n + col0;
-  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(C) + off;
-  if (col0 + 32 <= n) {
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      std::uint32_t w[4];
-      float c[8];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        w[e] = bf16_pair(__uint_as_float(r[v * 8 + 2 * e]), __uint_as_float(r[v * 8 + 2 * e + 1]));
-        bf16_unpair(w[e], c[2 * e], c[2 * e + 1]);  // the stored (rounded) value feeds the consumers
-      }
-      *reinterpret_cast<uint4*>(out + v * 8) = make_uint4(w[0], w[1], w[2], w[3]);
-#pragma unroll
-      for (int o = 0; o < kMaxEpiOps; ++o) {
-        if (o >= epi.n_ops) break;
-        float acc[8];
-#pragma unroll
-        for (int i = 0; i < kMaxEpiIn; ++i) {
-          if (i >= epi.ops[o].n_in) break;
-          float x[8];
-          if (i == epi.ops[o].gemm_pos) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = c[j];
-          } else {
-            const uint4 q =
-                __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(epi.ops[o].in[i]) + off + v * 8));
-            bf16_unpair(q.x, x[0], x[1]);
-            bf16_unpair(q.y, x[2], x[3]);
-            bf16_unpair(q.z, x[4], x[5]);
-            bf16_unpair(q.w, x[6], x[7]);
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] = i == 0 ? x[j] : epi_apply(epi.ops[o].op, acc[j], x[j]);
-        }
-        *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.ops[o].out) + off + v * 8) =
-            make_uint4(bf16_pair(acc[0], acc[1]), bf16_pair(acc[2], acc[3]), bf16_pair(acc[4], acc[5]),
-                       bf16_pair(acc[6], acc[7]));
-      }
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < 32; ++e) {
-      if (col0 + e >= n) continue;  // static e keeps r[] in registers
-      const __nv_bfloat16 h = __float2bfloat16_rn(__uint_as_float(r[e]));
-      out[e] = h;
-      const float cv = __bfloat162float(h);
-      for (int o = 0; o < epi.n_ops; ++o) {
-        float acc = 0.f;
-        for (int i = 0; i < epi.ops[o].n_in; ++i) {
-          const float x = i == epi.ops[o].gemm_pos
-                              ? cv
-                              : __bfloat162float(static_cast<const __nv_bfloat16*>(epi.ops[o].in[i])[off + e]);
-          acc = i == 0 ? x : epi_apply(epi.ops[o].op, acc, x);
-        }
-        static_cast<__nv_bfloat16*>(epi.ops[o].out)[off + e] = __float2bfloat16_rn(acc);
-      }
-    }
-  }
-}
-
-template <bool C_BF16>
-__device__ __forceinline__ void store_row_chunk(void* C, int row, int col0, int m, int n, const std::uint32_t (&r)[32]) {
-  if (row >= m || col0 >= n) return;
-  if (C_BF16) {
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(C) + static_cast<std::int64_t>(row) * n + col0;
-    if (col0 + 32 <= n) {
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 pk;
-        std::uint32_t* w = reinterpret_cast<std::uint32_t*>(&pk);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          __nv_bfloat162 h =
-              __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]), __uint_as_float(r[v * 8 + 2 * e + 1]));
-          w[e] = *reinterpret_cast<std::uint32_t*>(&h);
-        }
-        *reinterpret_cast<uint4*>(out + v * 8) = pk;
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (col0 + e < n) out[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
-    }
-  } else {
-    float* out = static_cast<float*>(C) + static_cast<std::int64_t>(row) * n + col0;
-    if (col0 + 32 <= n) {
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        *reinterpret_cast<float4*>(out + 4 * v) = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                                              __uint_as_float(r[4 * v + 2]),
-                                                              __uint_as_float(r[4 * v + 3]));
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (col0 + e < n) out[e] = __uint_as_float(r[e]);
-    }
-  }
-}
-
 template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -437,9 +330,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        if constexpr (FUSE) {
-          store_row_chunk_fused(C, row, nb * BN + c * 32, m, n, r, epi);
-        } else {
+        {
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer sb is free
           __syncwarp();
           std::uint8_t* buf = stg + sb * 4096;
@@ -464,6 +355,65 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
           __syncwarp();
           if (lane == 0) tma_store_2d(&tmC, buf, nb * BN + c * 32, mb * BM + q * 32);
+          if constexpr (FUSE) {
+            // Fused elementwise consumers, in the row-contiguous domain: the
+            // staged (bf16-rounded) chunk is re-read so that 4 lanes cover
+            // one 64-byte row segment — operand loads and result stores are
+            // coalesced. Bits equal the separate elementwise kernel's.
+#pragma unroll
+            for (int o = 0; o < kMaxEpiOps; ++o) {
+              if (o >= epi.n_ops) break;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int rr = (lane >> 2) + 8 * j;
+                const int v = lane & 3;
+                const int grow = mb * BM + q * 32 + rr;
+                const int gcol = nb * BN + c * 32 + 8 * v;
+                if (grow >= m || gcol >= n) continue;
+                const uint4 cw = *reinterpret_cast<const uint4*>(buf + rr * 64 + ((v ^ ((rr >> 1) & 3)) << 4));
+                float cv[8];
+                bf16_unpair(cw.x, cv[0], cv[1]);
+                bf16_unpair(cw.y, cv[2], cv[3]);
+                bf16_unpair(cw.z, cv[4], cv[5]);
+                bf16_unpair(cw.w, cv[6], cv[7]);
+                const std::int64_t off = static_cast<std::int64_t>(grow) * n + gcol;
+                const bool whole = gcol + 8 <= n;
+                float acc[8];
+#pragma unroll
+                for (int i = 0; i < kMaxEpiIn; ++i) {
+                  if (i >= epi.ops[o].n_in) break;
+                  float x[8];
+                  if (i == epi.ops[o].gemm_pos) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) x[e] = cv[e];
+                  } else {
+                    const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(epi.ops[o].in[i]) + off;
+                    if (whole) {
+                      const uint4 qv = __ldg(reinterpret_cast<const uint4*>(src));
+                      bf16_unpair(qv.x, x[0], x[1]);
+                      bf16_unpair(qv.y, x[2], x[3]);
+                      bf16_unpair(qv.z, x[4], x[5]);
+                      bf16_unpair(qv.w, x[6], x[7]);
+                    } else {
+#pragma unroll
+                      for (int e = 0; e < 8; ++e) x[e] = gcol + e < n ? __bfloat162float(src[e]) : 0.f;
+                    }
+                  }
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) acc[e] = i == 0 ? x[e] : epi_apply(epi.ops[o].op, acc[e], x[e]);
+                }
+                __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(epi.ops[o].out) + off;
+                if (whole) {
+                  *reinterpret_cast<uint4*>(dst) = make_uint4(bf16_pair(acc[0], acc[1]), bf16_pair(acc[2], acc[3]),
+                                                              bf16_pair(acc[4], acc[5]), bf16_pair(acc[6], acc[7]));
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e)
+                    if (gcol + e < n) dst[e] = __float2bfloat16_rn(acc[e]);
+                }
+              }
+            }
+          }
           sb ^= 1;
         }
       }
