@@ -271,10 +271,21 @@ def main():
         total_prof = sum(f["ms"] for f in fam.values())
         top = max(fam, key=lambda k: fam[k]["ms"])
         t = fam[top]
+        # DRAM traffic per launch of the dominant kernel from the committed
+        # ncu --set full capture of this workload (profiles/latest_traffic.json).
+        traffic, traffic_src = None, None
+        try:
+            with open(os.path.join(ROOT, "profiles", "latest_traffic.json")) as f:
+                tj = json.load(f)
+            if args.config == "c2" and n == 1 and top in tj:
+                traffic, traffic_src = tj[top]["mean"], tj["source"]
+        except Exception:
+            pass
         if top.startswith("gemm"):
             achieved = t["flops"] / (t["ms"] / 1e3) / 1e12
             roof = {"kernel": top, "bound": "tensor", "achieved": achieved, "peak": peaks["bf16"],
-                    "unit": "TFLOP/s", "frac": achieved / peaks["bf16"], "traffic": None,
+                    "unit": "TFLOP/s", "frac": achieved / peaks["bf16"], "traffic": traffic,
+                    "traffic_source": traffic_src,
                     "peak_source": peaks["src"] + " burst (kernels timed individually)",
                     "share_of_step": t["ms"] / total_prof,
                     "per_launch": {"flops": t["flops"] / max(t["launches"], 1),

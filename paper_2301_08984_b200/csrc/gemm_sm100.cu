@@ -6,18 +6,22 @@
 // are not materialised: a transposed operand is simply loaded MN-major and the
 // UMMA instruction descriptor's major bits say so.
 //
-// Structure: persistent, one CTA per SM, 128x256 output tiles in grouped
-// raster order (8 M-blocks per group for L2 reuse of B), 6 warps:
-//   warp 0      TMA producer: 4-stage smem ring (A 16 KB + B 32 KB per stage,
-//               128B-swizzled), mbarrier full/empty pipeline running across
-//               tiles
-//   warp 1      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
-//               + single-thread tcgen05.mma issuer (kind::f16, M=128, N=256,
-//               K=16 per instruction); commits free smem stages and, per
-//               tile, the accumulator it just finished
+// Structure: persistent, one CTA per SM, 128xBN output tiles (BN 256 / 128 /
+// 64 chosen per shape) in grouped raster order (8 M-blocks per group for L2
+// reuse of B), 6 warps:
+//   warp 0      TMA producer: smem ring filling ~192 KB (A 16 KB + B BN*128 B
+//               per stage, 128B-swizzled), mbarrier full/empty pipeline
+//               running across tiles
+//   warp 1      TMEM allocator (two BN-column fp32 accumulators) + single-
+//               thread tcgen05.mma issuer (kind::f16, M=128, N=BN, K=16 per
+//               instruction); commits free smem stages and, per tile, the
+//               accumulator it just finished
 //   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 TMEM -> registers, convert,
-//               16-byte global stores; releases the accumulator so the MMA
-//               warp fills it with the tile after next while this one drains
+//               64B/128B-swizzled smem staging, TMA bulk tensor store
+//               (double-buffered per warp); releases the accumulator so the
+//               MMA warp fills it with the tile after next while this one
+//               drains. Optional fused elementwise consumers (FUSE) re-read
+//               the staged chunk row-contiguously.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
