@@ -316,16 +316,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     std::uint8_t* stg = staging + (warp - 2) * 2 * 4096;
     int sb = 0;
     int local = 0;
+    // Fused-operand prefetch (FUSE): the 4 row segments this lane handles in
+    // a 32x32 chunk, per operand slot; chunk c+1 is in flight while chunk c
+    // is processed, and a tile's first chunk while its accumulator is built.
+    uint4 pf_cur[kMaxEpiSlots][4], pf_nxt[kMaxEpiSlots][4];
+    auto prefetch = [&](int mb_, int nb_, int c_, uint4(&dst)[kMaxEpiSlots][4]) {
+#pragma unroll
+      for (int s = 0; s < kMaxEpiSlots; ++s) {
+        const int o = epi.slot_op[s], i = epi.slot_in[s];
+        const __nv_bfloat16* srcb = static_cast<const __nv_bfloat16*>(epi.ops[o].in[i]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint4 val = make_uint4(0u, 0u, 0u, 0u);
+          const int rr = (lane >> 2) + 8 * j;
+          const int grow = mb_ * BM + q * 32 + rr;
+          const int gcol = nb_ * BN + c_ * 32 + 8 * (lane & 3);
+          if (s < epi.n_slots && grow < m && gcol < n) {
+            const __nv_bfloat16* p = srcb + static_cast<std::int64_t>(grow) * n + gcol;
+            if (gcol + 8 <= n) {
+              val = __ldg(reinterpret_cast<const uint4*>(p));
+            } else {
+              std::uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                if (gcol + e < n)
+                  w[e >> 1] |= static_cast<std::uint32_t>(__bfloat16_as_ushort(p[e])) << (16 * (e & 1));
+              val = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+          dst[s][j] = val;
+        }
+      }
+    };
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
       int mb, nb;
       tile_coords(t, tiles_m, tiles_n, mb, nb);
       const int acc = local & 1;
+      if constexpr (FUSE) prefetch(mb, nb, 0, pf_cur);
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
       const int row = mb * BM + q * 32 + lane;
+      (void)row;
       const std::uint32_t base = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
+        if constexpr (FUSE) {
+          if (c + 1 < BN / 32) prefetch(mb, nb, c + 1, pf_nxt);
+        }
         std::uint32_t r[32];
         tmem_ld32(base + c * 32, r);
         if (c == BN / 32 - 1) {
@@ -391,17 +428,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                     for (int e = 0; e < 8; ++e) x[e] = cv[e];
                   } else {
-                    const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(epi.ops[o].in[i]) + off;
-                    if (whole) {
-                      const uint4 qv = __ldg(reinterpret_cast<const uint4*>(src));
-                      bf16_unpair(qv.x, x[0], x[1]);
-                      bf16_unpair(qv.y, x[2], x[3]);
-                      bf16_unpair(qv.z, x[4], x[5]);
-                      bf16_unpair(qv.w, x[6], x[7]);
-                    } else {
-#pragma unroll
-                      for (int e = 0; e < 8; ++e) x[e] = gcol + e < n ? __bfloat162float(src[e]) : 0.f;
-                    }
+                    // prefetched one chunk ahead (static slot selection)
+                    const bool s1 = epi.n_slots > 1 && epi.slot_op[1] == o && epi.slot_in[1] == i;
+                    const uint4 qv = s1 ? pf_cur[1][j] : pf_cur[0][j];
+                    bf16_unpair(qv.x, x[0], x[1]);
+                    bf16_unpair(qv.y, x[2], x[3]);
+                    bf16_unpair(qv.z, x[4], x[5]);
+                    bf16_unpair(qv.w, x[6], x[7]);
                   }
 #pragma unroll
                   for (int e = 0; e < 8; ++e) acc[e] = i == 0 ? x[e] : epi_apply(epi.ops[o].op, acc[e], x[e]);
@@ -417,6 +450,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
               }
             }
+#pragma unroll
+            for (int s = 0; s < kMaxEpiSlots; ++s)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) pf_cur[s][j] = pf_nxt[s][j];
           }
           sb ^= 1;
         }

@@ -65,7 +65,13 @@ struct EpiOp {
 struct EpiParams {
   int n_ops = 0;
   EpiOp ops[kMaxEpiOps];
+  // Non-GEMM operands, one prefetch slot each (at most kMaxEpiSlots): slot
+  // s holds operand slot_in[s] of op slot_op[s].
+  int n_slots = 0;
+  int slot_op[2] = {0, 0};
+  int slot_in[2] = {0, 0};
 };
+constexpr int kMaxEpiSlots = 2;
 
 struct GemmArgs {
   const void* A;

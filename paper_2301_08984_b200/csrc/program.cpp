@@ -742,6 +742,10 @@ void fuse_gemm_epilogues(Program& P, const ProgramOptions& opt) {
     }
     if (g < 0) continue;
     Instr& G = P.instrs[g];
+    // The epilogue prefetches at most two non-GEMM operands per chunk.
+    std::size_t slots = e.in_bufs.size() - 1;
+    for (const auto& f : G.fused) slots += f.in_bufs.size() - 1;
+    if (slots > 2) continue;
     const DType da = P.buffers[G.in_bufs[0]].dtype, db = P.buffers[G.in_bufs[1]].dtype;
     if (!opt.gemm_fusable || !opt.gemm_fusable(G, da, db, DType::bf16)) continue;
     // Other operands must be produced before the GEMM issues.

@@ -512,7 +512,15 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
         o.op = static_cast<int>(fe.op);
         o.n_in = static_cast<int>(fe.in_bufs.size());
         o.gemm_pos = fe.gemm_pos;
-        for (std::size_t j = 0; j < fe.in_bufs.size(); ++j) o.in[j] = buf_ptr(fe.in_bufs[j]);
+        for (std::size_t j = 0; j < fe.in_bufs.size(); ++j) {
+          o.in[j] = buf_ptr(fe.in_bufs[j]);
+          if (static_cast<int>(j) != fe.gemm_pos) {
+            if (a.epi.n_slots >= kMaxEpiSlots) throw InternalError("fused epilogue needs more than 2 operands");
+            a.epi.slot_op[a.epi.n_slots] = static_cast<int>(f);
+            a.epi.slot_in[a.epi.n_slots] = static_cast<int>(j);
+            ++a.epi.n_slots;
+          }
+        }
         o.out = buf_ptr(fe.out_buf);
       }
       if (a.epi.n_ops > 0 && !(opt_.allow_tensor_cores && gemm_sm100_eligible(a))) {
