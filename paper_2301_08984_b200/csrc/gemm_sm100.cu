@@ -20,8 +20,8 @@
 //               64B/128B-swizzled smem staging, TMA bulk tensor store
 //               (double-buffered per warp); releases the accumulator so the
 //               MMA warp fills it with the tile after next while this one
-//               drains. Optional fused elementwise consumers (FUSE) re-read
-//               the staged chunk row-contiguously.
+//               drains. An optional fused elementwise consumer (FUSE)
+//               reads its operands one chunk ahead and leaves by TMA store.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -47,17 +47,24 @@ constexpr int GROUP_M = 8;
 
 // Tile width BN in {256, 128, 64}: smem ring depth fills ~200 KB, TMEM holds
 // two BN-column fp32 accumulators (power of two >= 32 columns).
-template <int BN_>
+template <int BN_, bool FUSE = false>
 struct Cfg {
   static constexpr int BN = BN_;
   static constexpr int B_STAGE_BYTES = BN * BK * 2;
   static constexpr int STAGES_RAW = (200 * 1024) / (A_STAGE_BYTES + B_STAGE_BYTES);
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  // + epilogue staging: 4 warps x 2 buffers x (32 rows x 32 cols, <= 4 B)
+  // + epilogue staging: 4 warps x 2 buffers x (32 rows x 32 cols, <= 4 B);
+  // FUSE (bf16): 4 warps x 2 x {C, fused result} 2 KB chunks — same size.
   static constexpr int STAGING_BYTES = 4 * 2 * 4096;
   static constexpr int SMEM_BYTES =
       STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + STAGING_BYTES + 1024 /*align*/ + 1024 /*barriers + align*/;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+};
+
+// Tensor map of a fused epilogue's result: [m][n] bf16 in the C layout
+// (32x32 boxes, 64B swizzle).
+struct EpiMaps {
+  CUtensorMap out[1];
 };
 
 // ---- PTX wrappers ------------------------------------------------------------
@@ -108,6 +115,14 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                "r"(c0), "r"(c1), "r"(smem_u32(src))
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// Same, without closing the bulk group (several stores per group).
+__device__ __forceinline__ void tma_store_2d_nc(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<std::uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -195,18 +210,19 @@ template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, void* __restrict__ C, int m, int n, int k,
-                   const __grid_constant__ EpiParams epi) {
+                   const __grid_constant__ EpiParams epi, const __grid_constant__ EpiMaps maps) {
   extern __shared__ std::uint8_t smem_raw[];
-  constexpr int STAGES = Cfg<BN>::STAGES;
-  constexpr int B_STAGE_BYTES = Cfg<BN>::B_STAGE_BYTES;
-  constexpr int TMEM_COLS = Cfg<BN>::TMEM_COLS;
+  using CF = Cfg<BN, FUSE>;
+  constexpr int STAGES = CF::STAGES;
+  constexpr int B_STAGE_BYTES = CF::B_STAGE_BYTES;
+  constexpr int TMEM_COLS = CF::TMEM_COLS;
   std::uint8_t* smem =
       reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
   std::uint8_t* sA = smem;
   std::uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
   // Epilogue staging (1024-aligned: the 64B / 128B swizzle atoms of the C map).
   std::uint8_t* staging = sB + STAGES * B_STAGE_BYTES;
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(staging + Cfg<BN>::STAGING_BYTES);
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(staging + CF::STAGING_BYTES);
   std::uint64_t* empty = full + STAGES;
   std::uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
   std::uint64_t* tempty = tfull + 2;      // [2] accumulator drained
@@ -306,7 +322,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_commit(&tfull[acc]);  // accumulator complete
       }
     }
-  } else {
+  } else if constexpr (!FUSE) {
     // Epilogue warps 2..5: warp w may only touch TMEM lanes 32*(w%4)..+31.
     // Each 32x32 output chunk goes TMEM -> registers -> swizzled smem
     // staging (conflict-free 16-byte stores) -> one TMA bulk tensor store
@@ -316,53 +332,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     std::uint8_t* stg = staging + (warp - 2) * 2 * 4096;
     int sb = 0;
     int local = 0;
-    // Fused-operand prefetch (FUSE): the 4 row segments this lane handles in
-    // a 32x32 chunk, per operand slot; chunk c+1 is in flight while chunk c
-    // is processed, and a tile's first chunk while its accumulator is built.
-    uint4 pf_cur[kMaxEpiSlots][4], pf_nxt[kMaxEpiSlots][4];
-    auto prefetch = [&](int mb_, int nb_, int c_, uint4(&dst)[kMaxEpiSlots][4]) {
-#pragma unroll
-      for (int s = 0; s < kMaxEpiSlots; ++s) {
-        const int o = epi.slot_op[s], i = epi.slot_in[s];
-        const __nv_bfloat16* srcb = static_cast<const __nv_bfloat16*>(epi.ops[o].in[i]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint4 val = make_uint4(0u, 0u, 0u, 0u);
-          const int rr = (lane >> 2) + 8 * j;
-          const int grow = mb_ * BM + q * 32 + rr;
-          const int gcol = nb_ * BN + c_ * 32 + 8 * (lane & 3);
-          if (s < epi.n_slots && grow < m && gcol < n) {
-            const __nv_bfloat16* p = srcb + static_cast<std::int64_t>(grow) * n + gcol;
-            if (gcol + 8 <= n) {
-              val = __ldg(reinterpret_cast<const uint4*>(p));
-            } else {
-              std::uint32_t w[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                if (gcol + e < n)
-                  w[e >> 1] |= static_cast<std::uint32_t>(__bfloat16_as_ushort(p[e])) << (16 * (e & 1));
-              val = make_uint4(w[0], w[1], w[2], w[3]);
-            }
-          }
-          dst[s][j] = val;
-        }
-      }
-    };
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
       int mb, nb;
       tile_coords(t, tiles_m, tiles_n, mb, nb);
       const int acc = local & 1;
-      if constexpr (FUSE) prefetch(mb, nb, 0, pf_cur);
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
-      const int row = mb * BM + q * 32 + lane;
-      (void)row;
       const std::uint32_t base = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
-        if constexpr (FUSE) {
-          if (c + 1 < BN / 32) prefetch(mb, nb, c + 1, pf_nxt);
-        }
         std::uint32_t r[32];
         tmem_ld32(base + c * 32, r);
         if (c == BN / 32 - 1) {
@@ -371,92 +349,129 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        {
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer sb is free
-          __syncwarp();
-          std::uint8_t* buf = stg + sb * 4096;
-          if constexpr (C_BF16) {
-            // 64 B rows, SWIZZLE_64B: 16-byte chunk v lands at v ^ ((row >> 1) & 3).
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer sb is free
+        __syncwarp();
+        std::uint8_t* buf = stg + sb * 4096;
+        if constexpr (C_BF16) {
+          // 64 B rows, SWIZZLE_64B: 16-byte chunk v lands at v ^ ((row >> 1) & 3).
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const uint4 w = make_uint4(bf16_pair(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1])),
-                                         bf16_pair(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
-                                         bf16_pair(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
-                                         bf16_pair(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
-              *reinterpret_cast<uint4*>(buf + lane * 64 + ((v ^ ((lane >> 1) & 3)) << 4)) = w;
-            }
-          } else {
-            // 128 B rows, SWIZZLE_128B: 16-byte chunk v lands at v ^ (row & 7).
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              *reinterpret_cast<uint4*>(buf + lane * 128 + ((v ^ (lane & 7)) << 4)) =
-                  make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-            }
+          for (int v = 0; v < 4; ++v) {
+            const uint4 w = make_uint4(bf16_pair(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1])),
+                                       bf16_pair(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
+                                       bf16_pair(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
+                                       bf16_pair(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
+            *reinterpret_cast<uint4*>(buf + lane * 64 + ((v ^ ((lane >> 1) & 3)) << 4)) = w;
           }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
-          __syncwarp();
-          if (lane == 0) tma_store_2d(&tmC, buf, nb * BN + c * 32, mb * BM + q * 32);
-          if constexpr (FUSE) {
-            // Fused elementwise consumers, in the row-contiguous domain: the
-            // staged (bf16-rounded) chunk is re-read so that 4 lanes cover
-            // one 64-byte row segment — operand loads and result stores are
-            // coalesced. Bits equal the separate elementwise kernel's.
+        } else {
+          // 128 B rows, SWIZZLE_128B: 16-byte chunk v lands at v ^ (row & 7).
 #pragma unroll
-            for (int o = 0; o < kMaxEpiOps; ++o) {
-              if (o >= epi.n_ops) break;
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int rr = (lane >> 2) + 8 * j;
-                const int v = lane & 3;
-                const int grow = mb * BM + q * 32 + rr;
-                const int gcol = nb * BN + c * 32 + 8 * v;
-                if (grow >= m || gcol >= n) continue;
-                const uint4 cw = *reinterpret_cast<const uint4*>(buf + rr * 64 + ((v ^ ((rr >> 1) & 3)) << 4));
-                float cv[8];
-                bf16_unpair(cw.x, cv[0], cv[1]);
-                bf16_unpair(cw.y, cv[2], cv[3]);
-                bf16_unpair(cw.z, cv[4], cv[5]);
-                bf16_unpair(cw.w, cv[6], cv[7]);
-                const std::int64_t off = static_cast<std::int64_t>(grow) * n + gcol;
-                const bool whole = gcol + 8 <= n;
-                float acc[8];
-#pragma unroll
-                for (int i = 0; i < kMaxEpiIn; ++i) {
-                  if (i >= epi.ops[o].n_in) break;
-                  float x[8];
-                  if (i == epi.ops[o].gemm_pos) {
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) x[e] = cv[e];
-                  } else {
-                    // prefetched one chunk ahead (static slot selection)
-                    const bool s1 = epi.n_slots > 1 && epi.slot_op[1] == o && epi.slot_in[1] == i;
-                    const uint4 qv = s1 ? pf_cur[1][j] : pf_cur[0][j];
-                    bf16_unpair(qv.x, x[0], x[1]);
-                    bf16_unpair(qv.y, x[2], x[3]);
-                    bf16_unpair(qv.z, x[4], x[5]);
-                    bf16_unpair(qv.w, x[6], x[7]);
-                  }
-#pragma unroll
-                  for (int e = 0; e < 8; ++e) acc[e] = i == 0 ? x[e] : epi_apply(epi.ops[o].op, acc[e], x[e]);
-                }
-                __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(epi.ops[o].out) + off;
-                if (whole) {
-                  *reinterpret_cast<uint4*>(dst) = make_uint4(bf16_pair(acc[0], acc[1]), bf16_pair(acc[2], acc[3]),
-                                                              bf16_pair(acc[4], acc[5]), bf16_pair(acc[6], acc[7]));
-                } else {
-#pragma unroll
-                  for (int e = 0; e < 8; ++e)
-                    if (gcol + e < n) dst[e] = __float2bfloat16_rn(acc[e]);
-                }
-              }
-            }
-#pragma unroll
-            for (int s = 0; s < kMaxEpiSlots; ++s)
-#pragma unroll
-              for (int j = 0; j < 4; ++j) pf_cur[s][j] = pf_nxt[s][j];
+          for (int v = 0; v < 8; ++v) {
+            *reinterpret_cast<uint4*>(buf + lane * 128 + ((v ^ (lane & 7)) << 4)) =
+                make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
           }
-          sb ^= 1;
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
+        __syncwarp();
+        if (lane == 0) tma_store_2d(&tmC, buf, nb * BN + c * 32, mb * BM + q * 32);
+        sb ^= 1;
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
+  } else {
+    // Fused epilogue (bf16, one elementwise consumer): lane = output row of
+    // the 32x32 chunk. The op's other operands (<= 2) are read straight into
+    // registers one chunk ahead — the first chunk of a tile while its
+    // accumulator is still being built — alternating between two register
+    // sets so no load is waited on before its chunk. C and the op result
+    // are staged swizzled side by side and leave as two TMA stores in one
+    // bulk group. Bits equal the separate kernels': the op folds its inputs
+    // in order, reading the GEMM's bf16-rounded C.
+    const int q = warp % 4;
+    std::uint8_t* stg = staging + (warp - 2) * 2 * 4096;  // [2][C 2 KB | result 2 KB]
+    const int swz = (lane >> 1) & 3;
+    const int nst = epi.n_slots;
+    const __nv_bfloat16* src0 =
+        static_cast<const __nv_bfloat16*>(epi.ops[0].in[epi.slot_in[0]]);
+    const __nv_bfloat16* src1 =
+        static_cast<const __nv_bfloat16*>(epi.ops[0].in[epi.slot_in[1]]);
+    auto load = [&](int t_, int c_, uint4(&d)[kMaxEpiSlots][4]) {
+      int mb_, nb_;
+      tile_coords(t_, tiles_m, tiles_n, mb_, nb_);
+      const int grow = mb_ * BM + q * 32 + lane;
+      const int gcol = nb_ * BN + c_ * 32;
+      const std::int64_t off = static_cast<std::int64_t>(grow) * n + gcol;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const bool ok = grow < m && gcol + 8 * v < n;  // n % 8 == 0: whole vectors
+        d[0][v] = ok && nst > 0 ? __ldg(reinterpret_cast<const uint4*>(src0 + off) + v) : make_uint4(0, 0, 0, 0);
+        d[1][v] = ok && nst > 1 ? __ldg(reinterpret_cast<const uint4*>(src1 + off) + v) : make_uint4(0, 0, 0, 0);
+      }
+    };
+    int g = 0;  // chunk counter of this warp (staging ring position)
+    auto chunk = [&](int t, int mb, int nb, int c, std::uint32_t base, int acc, uint4(&cur)[kMaxEpiSlots][4],
+                     uint4(&nxt)[kMaxEpiSlots][4]) {
+      if (c + 1 < BN / 32) load(t, c + 1, nxt);
+      else if (t + static_cast<int>(gridDim.x) < num_tiles) load(t + gridDim.x, 0, nxt);
+      std::uint32_t r[32];
+      tmem_ld32(base + c * 32, r);
+      if (c == BN / 32 - 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
+      std::uint32_t cw[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) cw[i] = bf16_pair(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // ring entry g&1 is free
+      __syncwarp();
+      std::uint8_t* buf = stg + (g & 1) * 4096;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        *reinterpret_cast<uint4*>(buf + lane * 64 + ((v ^ swz) << 4)) =
+            make_uint4(cw[4 * v], cw[4 * v + 1], cw[4 * v + 2], cw[4 * v + 3]);
+        float accv[8];
+#pragma unroll
+        for (int i = 0; i < kMaxEpiIn; ++i) {
+          if (i >= epi.ops[0].n_in) break;
+          const uint4 w = i == epi.ops[0].gemm_pos ? make_uint4(cw[4 * v], cw[4 * v + 1], cw[4 * v + 2], cw[4 * v + 3])
+                          : (nst > 1 && epi.slot_in[1] == i) ? cur[1][v]
+                                                             : cur[0][v];
+          float x[8];
+          bf16_unpair(w.x, x[0], x[1]);
+          bf16_unpair(w.y, x[2], x[3]);
+          bf16_unpair(w.z, x[4], x[5]);
+          bf16_unpair(w.w, x[6], x[7]);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) accv[e] = i == 0 ? x[e] : epi_apply(epi.ops[0].op, accv[e], x[e]);
+        }
+        *reinterpret_cast<uint4*>(buf + 2048 + lane * 64 + ((v ^ swz) << 4)) =
+            make_uint4(bf16_pair(accv[0], accv[1]), bf16_pair(accv[2], accv[3]), bf16_pair(accv[4], accv[5]),
+                       bf16_pair(accv[6], accv[7]));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        const int c0 = nb * BN + c * 32, c1 = mb * BM + q * 32;
+        tma_store_2d_nc(&tmC, buf, c0, c1);
+        tma_store_2d_nc(&maps.out[0], buf + 2048, c0, c1);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      ++g;
+    };
+    uint4 pa[kMaxEpiSlots][4], pb[kMaxEpiSlots][4];
+    if (blockIdx.x < num_tiles) load(blockIdx.x, 0, pa);
+    int local = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      int mb, nb;
+      tile_coords(t, tiles_m, tiles_n, mb, nb);
+      const int acc = local & 1;
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      const std::uint32_t base = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; c += 2) {
+        chunk(t, mb, nb, c, base, acc, pa, pb);
+        chunk(t, mb, nb, c + 1, base, acc, pb, pa);
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
@@ -523,7 +538,7 @@ template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 void launch_typed(const GemmArgs& a, cudaStream_t s) {
   static unsigned attr_set_mask = 0;  // per device ordinal
   static int num_sms[32] = {0};
-  constexpr int SMEM_BYTES = Cfg<BN>::SMEM_BYTES;
+  constexpr int SMEM_BYTES = Cfg<BN, FUSE>::SMEM_BYTES;
   auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16, BN, FUSE>;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -538,10 +553,13 @@ void launch_typed(const GemmArgs& a, cudaStream_t s) {
   CUtensorMap ma = A_MN ? make_map(a.A, a.k, a.m, BK) : make_map(a.A, a.m, a.k, BM);
   CUtensorMap mb = B_MN ? make_map(a.B, a.k, a.n, BK) : make_map(a.B, a.n, a.k, BN);
   CUtensorMap mc = make_store_map(a.C, a.m, a.n, C_BF16);
+  EpiMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  if constexpr (FUSE) maps.out[0] = make_store_map(a.epi.ops[0].out, a.m, a.n, true);
   const std::int64_t tiles = ((a.m + BM - 1) / BM) * ((a.n + BN - 1) / BN);
   const int grid = static_cast<int>(std::min<std::int64_t>(tiles, num_sms[dev & 31] > 0 ? num_sms[dev & 31] : 148));
   kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, mc, a.C, static_cast<int>(a.m), static_cast<int>(a.n),
-                                              static_cast<int>(a.k), a.epi);
+                                              static_cast<int>(a.k), a.epi, maps);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc_kernel: ") + cudaGetErrorString(e));
 }
@@ -588,6 +606,8 @@ void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
   const int bn = gemm_sm100_tile_n(a);
   if (a.epi.n_ops > 0) {
     if (!cb) throw std::runtime_error("fused GEMM epilogue needs a bf16 output");
+    if (a.epi.n_ops != 1 || a.epi.n_slots > kMaxEpiSlots || a.epi.ops[0].n_in > kMaxEpiIn)
+      throw std::runtime_error("fused GEMM epilogue: one elementwise op with <= 2 other operands");
 #define PLANC_TCF(AM, BMN)                                                      \
   if (a_mn == AM && b_mn == BMN) {                                             \
     if (bn == 256) return launch_typed<AM, BMN, true, 256, true>(a, s);        \

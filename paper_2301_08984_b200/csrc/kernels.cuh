@@ -53,7 +53,7 @@ struct DevChunk {
 // where in[gemm_pos] is the GEMM's own bf16-rounded output value and the
 // other operands are [m, n] row-major bf16 tensors read in place — the same
 // bits the separate elementwise kernel would produce.
-constexpr int kMaxEpiOps = 2;
+constexpr int kMaxEpiOps = 1;
 constexpr int kMaxEpiIn = 4;
 struct EpiOp {
   int op = 0;  // 0 add, 1 mul, 2 max

@@ -733,7 +733,7 @@ void fuse_gemm_epilogues(Program& P, const ProgramOptions& opt) {
       if (b.dtype != DType::bf16 || b.producer < 0) continue;
       const Instr& cand = P.instrs[b.producer];
       if (cand.kind != InstrKind::gemm || cand.lane != e.lane || cand.out_bufs[0] != e.in_bufs[i]) continue;
-      if (cand.m * cand.n != e.count || cand.fused.size() >= 2) continue;
+      if (cand.m * cand.n != e.count || !cand.fused.empty()) continue;  // one consumer per epilogue
       if (std::count(e.in_bufs.begin(), e.in_bufs.end(), e.in_bufs[i]) != 1) continue;
       if (cand.id > g) {
         g = cand.id;
@@ -748,7 +748,22 @@ void fuse_gemm_epilogues(Program& P, const ProgramOptions& opt) {
     if (slots > 2) continue;
     const DType da = P.buffers[G.in_bufs[0]].dtype, db = P.buffers[G.in_bufs[1]].dtype;
     if (!opt.gemm_fusable || !opt.gemm_fusable(G, da, db, DType::bf16)) continue;
-    // Other operands must be produced before the GEMM issues.
+    // Other operands must be produced before the GEMM issues — and already
+    // be (transitive) dependencies of it, so that fusion adds no edge to the
+    // dependency graph and cannot delay the GEMM behind work it used to
+    // overlap with on another stream.
+    std::set<int> anc;
+    {
+      std::vector<int> stack{g};
+      while (!stack.empty()) {
+        const int x = stack.back();
+        stack.pop_back();
+        for (int d : P.instrs[x].deps) {
+          const int dd = redirect[d] >= 0 ? redirect[d] : d;
+          if (anc.insert(dd).second) stack.push_back(dd);
+        }
+      }
+    }
     bool ready = true;
     std::set<int> extra;
     for (std::size_t i = 0; i < e.in_bufs.size(); ++i) {
@@ -756,7 +771,7 @@ void fuse_gemm_epilogues(Program& P, const ProgramOptions& opt) {
       const int pr = P.buffers[e.in_bufs[i]].producer;
       if (pr < 0) continue;
       const int pr_eff = redirect[pr] >= 0 ? redirect[pr] : pr;
-      if (pr_eff >= g) ready = false;
+      if (pr_eff >= g || !anc.count(pr_eff)) ready = false;
       extra.insert(pr_eff);
     }
     if (!ready) continue;

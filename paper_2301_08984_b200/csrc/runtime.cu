@@ -903,6 +903,7 @@ std::vector<KernelStat> Executor::profile() {
         g.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
         g.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
         kind = opt_.allow_tensor_cores && gemm_sm100_eligible(g) ? "gemm_tc" : "gemm_simt";
+        if (!in.fused.empty()) kind += "_fused" + std::to_string(in.fused.size());
         break;
       }
       case InstrKind::ew: kind = "ew"; break;

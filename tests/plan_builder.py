@@ -42,3 +42,21 @@ def matmul_plan(m, n, k, ta=False, tb=False, in_elem=2, out_elem=2):
     if tb:
         attrs["transpose_b"] = True
     return single_op_plan("matmul", [a, b], (m, n), in_elem, out_elem, attrs)
+
+
+def matmul_add_plan(m, n, k, ta=False, tb=False):
+    """C = op(A)·op(B); E = C + D (bf16): a GEMM with one fusable consumer."""
+    doc = json.loads(matmul_plan(m, n, k, ta, tb)[0])
+    doc["ptensors"] += [{"id": 3, "shape": [m, n], "elem_size": 2, "kind": "activation"},
+                        {"id": 4, "shape": [m, n], "elem_size": 2, "kind": "activation"}]
+    full = [[0, m], [0, n]]
+    doc["vtensors"] += [
+        {"id": 201, "ptensor": 2, "region": full, "value": [0, 1], "replica": [0, 1], "side": "in", "owner": "add"},
+        {"id": 202, "ptensor": 3, "region": full, "value": [0, 1], "replica": [0, 1], "side": "in", "owner": "add"},
+        {"id": 203, "ptensor": 4, "region": full, "value": [0, 1], "replica": [0, 1], "side": "out", "owner": "add"}]
+    doc["ops"].append({"id": "add", "kind": "add", "inputs": [201, 202], "outputs": [203], "direction": "forward",
+                       "flops": 0.0, "doc_order": 1, "inserted": False})
+    doc["assignment"]["add"] = 0
+    doc["feeds"].append([201, 200])
+    doc["lanes"][0]["tasks"].append({"kind": "compute", "op": "add", "duration": 0.0, "bytes": 0})
+    return json.dumps(doc), 4
