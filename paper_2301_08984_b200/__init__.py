@@ -110,6 +110,8 @@ def _load():
     L.planc_b200_nccl_unique_id.argtypes = [ctypes.c_char_p]
     L.planc_b200_open_rank.argtypes = [ctypes.c_char_p, c_int, c_int, P(c_int), c_int, c_int, ctypes.c_char_p,
                                        ctypes.c_uint32, P(vp)]
+    L.planc_b200_gemm_schedule.argtypes = [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, P(c_int), P(c_int),
+                                           P(c_int), P(c_int), P(c_i64)]
     L.planc_b200_free.argtypes = [vp]
     _lib = L
     return L
@@ -147,6 +149,19 @@ def describe(plan_json: str, strict_value: bool = False, lane_rank=None, flags: 
     s = ctypes.string_at(out.value).decode()
     L.planc_b200_free(out)
     return json.loads(s)
+
+
+def gemm_schedule(m: int, n: int, k: int, ta: bool = False, tb: bool = False, c_bf16: bool = True,
+                  sms: int = 148) -> dict:
+    """Host-only: the tcgen05 GEMM's launch schedule (tile width, grid, whole
+    tiles, stream-K CTAs, workspace bytes) for a bf16 matmul of this shape."""
+    L = _load()
+    bn, grid, dp, sk = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    ws = ctypes.c_int64()
+    _check(L.planc_b200_gemm_schedule(m, n, k, int(ta), int(tb), int(c_bf16), sms, ctypes.byref(bn),
+                                      ctypes.byref(grid), ctypes.byref(dp), ctypes.byref(sk), ctypes.byref(ws)))
+    return {"tile_n": bn.value, "grid": grid.value, "dp_tiles": dp.value, "sk_ctas": sk.value,
+            "ws_bytes": ws.value}
 
 
 def nccl_unique_id() -> bytes:

@@ -275,6 +275,29 @@ int planc_b200_gemm_config(int64_t m, int64_t n, int64_t k, int ta, int tb, int 
   return PLANC_B200_OK;
 }
 
+int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, int c_bf16, int sms, int* tile_n,
+                             int* grid, int* dp_tiles, int* sk_ctas, int64_t* ws_bytes) {
+  return guarded([&] {
+    if (sms <= 0) throw UsageError("sms must be positive");
+    GemmArgs a{};
+    a.m = m;
+    a.n = n;
+    a.k = k;
+    a.ta = ta != 0;
+    a.tb = tb != 0;
+    a.da = DT_BF16;
+    a.db = DT_BF16;
+    a.dc = c_bf16 ? DT_BF16 : DT_F32;
+    if (!gemm_sm100_eligible(a)) throw UsageError("shape does not take the tensor-core path");
+    GemmSchedule sc = gemm_sm100_schedule(a, sms);
+    if (tile_n) *tile_n = sc.bn;
+    if (grid) *grid = sc.grid;
+    if (dp_tiles) *dp_tiles = sc.dp_tiles;
+    if (sk_ctas) *sk_ctas = sc.sk_ctas;
+    if (ws_bytes) *ws_bytes = sc.ws_bytes;
+  });
+}
+
 int planc_b200_timeline(planc_b200_exec* h, char** json_out) {
   return guarded([&] {
     if (!h || !json_out) throw UsageError("null argument");

@@ -44,6 +44,7 @@ constexpr int BK = 64;  // 128 bytes of bf16: one 128B swizzle row
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int NUM_THREADS = 192;
 constexpr int GROUP_M = 8;
+constexpr int kSkDepth = 2;  // stream-K partials loaded per round trip
 
 // Tile width BN in {256, 128, 64}: smem ring depth fills ~200 KB, TMEM holds
 // two BN-column fp32 accumulators (power of two >= 32 columns).
@@ -66,6 +67,48 @@ struct Cfg {
 struct EpiMaps {
   CUtensorMap out[1];
 };
+
+// Stream-K tail (data-parallel waves, then the remaining tiles' k-iterations
+// split evenly over the CTAs): tiles [0, dp_tiles) go whole to CTA
+// t % gridDim.x; CTA b < sk_ctas then takes k-iterations [lo(b), lo(b+1)) of
+// the linearised (tile, k-block) space of tiles [dp_tiles, tiles). A tile
+// covered by several CTAs is reduced by whichever of them arrives last (per
+// 32-row quarter: a counter per quarter, no CTA ever waits on another), in
+// fixed CTA (= k) order from fp32 partials — the same bits whatever the
+// arrival order.
+struct SkParams {
+  int dp_tiles = 0;
+  int sk_ctas = 0;
+  long long sk_iters = 0;
+  float* partials = nullptr;  // [sk_ctas][2 slots][4 quarters][BN/32 chunks][8][32] float4
+  int* counters = nullptr;    // [(tiles - dp_tiles) * 4], zero between launches
+};
+
+__device__ __forceinline__ long long sk_lo(const SkParams& sk, int b) {
+  return static_cast<long long>(b) * sk.sk_iters / sk.sk_ctas;
+}
+
+// CTA whose stream-K range holds iteration x: max b with lo(b) <= x.
+__device__ __forceinline__ int sk_owner(const SkParams& sk, long long x) {
+  return static_cast<int>(((x + 1) * sk.sk_ctas - 1) / sk.sk_iters);
+}
+
+// Calls f(tile, kb0, kb1) for this CTA's work items in order.
+template <typename F>
+__device__ __forceinline__ void for_each_work(int num_k, const SkParams& sk, F&& f) {
+  for (int t = blockIdx.x; t < sk.dp_tiles; t += gridDim.x) f(t, 0, num_k);
+  if (static_cast<int>(blockIdx.x) < sk.sk_ctas) {
+    long long it = sk_lo(sk, blockIdx.x);
+    const long long hi = sk_lo(sk, blockIdx.x + 1);
+    while (it < hi) {
+      const int j = static_cast<int>(it / num_k);
+      const int kb0 = static_cast<int>(it - static_cast<long long>(j) * num_k);
+      const int kb1 = static_cast<int>(min(static_cast<long long>(num_k), kb0 + (hi - it)));
+      f(sk.dp_tiles + j, kb0, kb1);
+      it += kb1 - kb0;
+    }
+  }
+}
 
 // ---- PTX wrappers ------------------------------------------------------------
 
@@ -210,7 +253,8 @@ template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, void* __restrict__ C, int m, int n, int k,
-                   const __grid_constant__ EpiParams epi, const __grid_constant__ EpiMaps maps) {
+                   const __grid_constant__ EpiParams epi, const __grid_constant__ EpiMaps maps,
+                   const __grid_constant__ SkParams sk) {
   extern __shared__ std::uint8_t smem_raw[];
   using CF = Cfg<BN, FUSE>;
   constexpr int STAGES = CF::STAGES;
@@ -261,12 +305,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int it = 0;  // global k-block counter across tiles (ring position)
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int it = 0;  // global k-block counter across work items (ring position)
+      for_each_work(num_k, sk, [&](int t, int kb0, int kb1) {
         int mb, nb;
         tile_coords(t, tiles_m, tiles_n, mb, nb);
         const int m0 = mb * BM, n0 = nb * BN;
-        for (int kb = 0; kb < num_k; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const std::uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&empty[s], phase ^ 1);
@@ -286,19 +330,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tma_load_2d(b, &tmB, kb * BK, n0, &full[s]);
           }
         }
-      }
+      });
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr std::uint32_t idesc = make_idesc<BN>(A_MN, B_MN);
       int it = 0, local = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      for_each_work(num_k, sk, [&](int, int kb0, int kb1) {
         const int acc = local & 1;
         const std::uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
         const std::uint32_t d = tmem + static_cast<std::uint32_t>(acc * BN);
-        for (int kb = 0; kb < num_k; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const std::uint32_t phase = (it / STAGES) & 1;
           mbar_wait(&full[s], phase);
@@ -315,12 +359,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                     : smem_desc(a_base + kk * 32, 16, 1024);
             std::uint64_t bd = B_MN ? smem_desc(b_base + kk * 2048, 64 * BK * 2, 1024)
                                     : smem_desc(b_base + kk * 32, 16, 1024);
-            tc_mma(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            tc_mma(d, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
           }
           tc_commit(&empty[s]);  // smem stage free once these MMAs retire
         }
         tc_commit(&tfull[acc]);  // accumulator complete
-      }
+        ++local;
+      });
     }
   } else if constexpr (!FUSE) {
     // Epilogue warps 2..5: warp w may only touch TMEM lanes 32*(w%4)..+31.
@@ -332,50 +377,134 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     std::uint8_t* stg = staging + (warp - 2) * 2 * 4096;
     int sb = 0;
     int local = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+    auto store_chunk = [&](const std::uint32_t(&r)[32], int mb, int nb, int c) {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer sb is free
+      __syncwarp();
+      std::uint8_t* buf = stg + sb * 4096;
+      if constexpr (C_BF16) {
+        // 64 B rows, SWIZZLE_64B: 16-byte chunk v lands at v ^ ((row >> 1) & 3).
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const uint4 w = make_uint4(bf16_pair(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1])),
+                                     bf16_pair(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
+                                     bf16_pair(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
+                                     bf16_pair(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
+          *reinterpret_cast<uint4*>(buf + lane * 64 + ((v ^ ((lane >> 1) & 3)) << 4)) = w;
+        }
+      } else {
+        // 128 B rows, SWIZZLE_128B: 16-byte chunk v lands at v ^ (row & 7).
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          *reinterpret_cast<uint4*>(buf + lane * 128 + ((v ^ (lane & 7)) << 4)) =
+              make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
+      __syncwarp();
+      if (lane == 0) tma_store_2d(&tmC, buf, nb * BN + c * 32, mb * BM + q * 32);
+      sb ^= 1;
+    };
+    // fp32 partial of (CTA b, slot, this quarter, chunk c): 8 float4 per
+    // lane, lane-interleaved so every access is one coalesced 512 B row.
+    auto partial_ptr = [&](int b, int slot, int c) {
+      return reinterpret_cast<float4*>(sk.partials) +
+             ((static_cast<std::int64_t>((b * 2 + slot) * 4 + q) * (BN / 32) + c) * 8) * 32 + lane;
+    };
+    for_each_work(num_k, sk, [&](int t, int kb0, int kb1) {
       int mb, nb;
       tile_coords(t, tiles_m, tiles_n, mb, nb);
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ++local;
       tc_fence_after();
       const std::uint32_t base = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
+      if (kb0 == 0 && kb1 == num_k) {  // whole tile
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          std::uint32_t r[32];
+          tmem_ld32(base + c * 32, r);
+          if (c == BN / 32 - 1) {
+            // All TMEM reads of this accumulator are complete: hand it back.
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          store_chunk(r, mb, nb, c);
+        }
+        return;
+      }
+      // Stream-K segment: publish the fp32 partial, count the arrival.
+      const int j = t - sk.dp_tiles;
+      const long long x0 = static_cast<long long>(j) * num_k;
+      const int me = blockIdx.x;
+      const int myslot = sk_lo(sk, me) >= x0 ? 0 : 1;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         std::uint32_t r[32];
         tmem_ld32(base + c * 32, r);
-        if (c == BN / 32 - 1) {
-          // All TMEM reads of this accumulator are complete: hand it back.
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer sb is free
-        __syncwarp();
-        std::uint8_t* buf = stg + sb * 4096;
-        if constexpr (C_BF16) {
-          // 64 B rows, SWIZZLE_64B: 16-byte chunk v lands at v ^ ((row >> 1) & 3).
+        float4* dst = partial_ptr(me, myslot, c);
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const uint4 w = make_uint4(bf16_pair(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1])),
-                                       bf16_pair(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
-                                       bf16_pair(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
-                                       bf16_pair(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
-            *reinterpret_cast<uint4*>(buf + lane * 64 + ((v ^ ((lane >> 1) & 3)) << 4)) = w;
-          }
-        } else {
-          // 128 B rows, SWIZZLE_128B: 16-byte chunk v lands at v ^ (row & 7).
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            *reinterpret_cast<uint4*>(buf + lane * 128 + ((v ^ (lane & 7)) << 4)) =
-                make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-          }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
-        __syncwarp();
-        if (lane == 0) tma_store_2d(&tmC, buf, nb * BN + c * 32, mb * BM + q * 32);
-        sb ^= 1;
+        for (int v = 0; v < 8; ++v)
+          __stcg(dst + v * 32, make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                           __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])));
       }
-    }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      __threadfence();
+      __syncwarp();
+      int old = 0;
+      if (lane == 0) old = atomicAdd(&sk.counters[j * 4 + q], 1);
+      old = __shfl_sync(0xffffffffu, old, 0);
+      const int b_first = sk_owner(sk, x0), b_last = sk_owner(sk, x0 + num_k - 1);
+      if (old != b_last - b_first) return;  // another CTA finishes this quarter
+      // Last arrival: sum every segment's partial in k order, store.
+      __threadfence();
+      if (lane == 0) sk.counters[j * 4 + q] = 0;  // ready for the next launch
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        // Loads of kSkDepth partials in flight, folded in CTA order.
+        float4 sum[8];
+#pragma unroll 1
+        for (int b0 = b_first; b0 <= b_last; b0 += kSkDepth) {
+          float4 p[kSkDepth][8];
+#pragma unroll
+          for (int d = 0; d < kSkDepth; ++d) {
+            const int b = b0 + d;
+            if (b <= b_last) {
+              const float4* src = partial_ptr(b, sk_lo(sk, b) >= x0 ? 0 : 1, c);
+#pragma unroll
+              for (int v = 0; v < 8; ++v) p[d][v] = __ldcg(src + v * 32);
+            }
+          }
+#pragma unroll
+          for (int d = 0; d < kSkDepth; ++d) {
+            const int b = b0 + d;
+            if (b > b_last) break;
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              if (b == b_first) {
+                sum[v] = p[d][v];
+              } else {
+                sum[v].x += p[d][v].x;
+                sum[v].y += p[d][v].y;
+                sum[v].z += p[d][v].z;
+                sum[v].w += p[d][v].w;
+              }
+            }
+          }
+        }
+        std::uint32_t r[32];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          r[4 * v] = __float_as_uint(sum[v].x);
+          r[4 * v + 1] = __float_as_uint(sum[v].y);
+          r[4 * v + 2] = __float_as_uint(sum[v].z);
+          r[4 * v + 3] = __float_as_uint(sum[v].w);
+        }
+        store_chunk(r, mb, nb, c);
+      }
+    });
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
   } else {
     // Fused epilogue (bf16, one elementwise consumer): lane = output row of
@@ -534,10 +663,21 @@ CUtensorMap make_store_map(void* base, std::int64_t m, std::int64_t n, bool bf16
   return map;
 }
 
-template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
-void launch_typed(const GemmArgs& a, cudaStream_t s) {
-  static unsigned attr_set_mask = 0;  // per device ordinal
+int device_sms() {
   static int num_sms[32] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (num_sms[dev & 31] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    num_sms[dev & 31] = v > 0 ? v : 148;
+  }
+  return num_sms[dev & 31];
+}
+
+template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
+void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
+  static unsigned attr_set_mask = 0;  // per device ordinal
   constexpr int SMEM_BYTES = Cfg<BN, FUSE>::SMEM_BYTES;
   auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16, BN, FUSE>;
   int dev = 0;
@@ -545,7 +685,6 @@ void launch_typed(const GemmArgs& a, cudaStream_t s) {
   if (!(attr_set_mask & (1u << dev))) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc smem attribute: ") + cudaGetErrorString(e));
-    cudaDeviceGetAttribute(&num_sms[dev & 31], cudaDevAttrMultiProcessorCount, dev);
     attr_set_mask |= 1u << dev;
   }
   // A: [m][k] (K-major) or, transposed, [k][m] (MN-major); B: [k][n]
@@ -556,36 +695,105 @@ void launch_typed(const GemmArgs& a, cudaStream_t s) {
   EpiMaps maps;
   std::memset(&maps, 0, sizeof(maps));
   if constexpr (FUSE) maps.out[0] = make_store_map(a.epi.ops[0].out, a.m, a.n, true);
-  const std::int64_t tiles = ((a.m + BM - 1) / BM) * ((a.n + BN - 1) / BN);
-  const int grid = static_cast<int>(std::min<std::int64_t>(tiles, num_sms[dev & 31] > 0 ? num_sms[dev & 31] : 148));
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, mc, a.C, static_cast<int>(a.m), static_cast<int>(a.n),
-                                              static_cast<int>(a.k), a.epi, maps);
+  SkParams sk;
+  sk.dp_tiles = sc.dp_tiles;
+  sk.sk_ctas = sc.sk_ctas;
+  sk.sk_iters = sc.sk_iters;
+  if (sc.sk_ctas > 0) {
+    char* ws = static_cast<char*>(a.ws);
+    sk.counters = reinterpret_cast<int*>(ws);
+    sk.partials = reinterpret_cast<float*>(ws + sc.counter_bytes);
+  }
+  kern<<<sc.grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, mc, a.C, static_cast<int>(a.m), static_cast<int>(a.n),
+                                                static_cast<int>(a.k), a.epi, maps, sk);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc_kernel: ") + cudaGetErrorString(e));
 }
 
+// Modelled time (us) of one launch, calibrated on B200 single-GEMM graphs
+// (profiles/r01/gemm_streamk*.jsonl): per k-block MMA time by tile width
+// (128x256 blocks ~0.35 us with every SM busy; 128x128 / 128x64 blocks are
+// shared-memory-bandwidth bound at ~0.28 us), a per-tile epilogue cost, and
+// for stream-K the fp32 partial writes plus the last arrival's reduction,
+// which is L2-latency bound: one ~1 us round trip per kSkDepth partials per
+// 32-column chunk.
+double kb_us(int bn) { return bn == 256 ? 0.35 : 0.28; }
+constexpr double kTileUs = 0.3;
+constexpr double kSkRoundTripUs = 1.0;
+constexpr double kSkWriteChunkUs = 0.15;
+constexpr int kMinSkIters = 4;  // k-blocks per stream-K range, at least
+
+GemmSchedule schedule_for(std::int64_t m, std::int64_t n, std::int64_t k, int bn, bool allow_sk, int sms,
+                          bool force_sk = false) {
+  GemmSchedule sc;
+  sc.bn = bn;
+  sc.tiles = ((m + BM - 1) / BM) * ((n + bn - 1) / bn);
+  sc.num_k = (k + BK - 1) / BK;
+  const std::int64_t waves = (sc.tiles + sms - 1) / sms;
+  sc.grid = static_cast<int>(std::min<std::int64_t>(sc.tiles, sms));
+  sc.dp_tiles = sc.tiles;
+  sc.model_us = static_cast<double>(waves) * (sc.num_k * kb_us(bn) + kTileUs);
+  if (!allow_sk || sc.tiles % sms == 0) return sc;
+  // Whole waves minus one stay data-parallel; the rest (< 2 waves of tiles)
+  // is shared by `ctas` CTAs — every count from ~one segment per tile up to
+  // the whole GPU is tried (fewer CTAs = shallower reductions).
+  const std::int64_t dp_waves = sc.tiles >= sms ? sc.tiles / sms - 1 : 0;
+  const std::int64_t sk_tiles = sc.tiles - dp_waves * sms;
+  const long long iters = sk_tiles * sc.num_k;
+  const int max_ctas = static_cast<int>(std::min<long long>(sms, iters / kMinSkIters));
+  GemmSchedule best = sc;
+  if (force_sk) best.model_us = 1e300;
+  for (int ctas = static_cast<int>(std::min<std::int64_t>(sk_tiles, sms)); ctas <= max_ctas; ++ctas) {
+    const long long per = (iters + ctas - 1) / ctas;
+    if (ctas <= sk_tiles && per >= sc.num_k) continue;  // no tile would be shared
+    const long long covers = std::min<long long>((sc.num_k + per - 1) / per + 1, ctas);
+    const double chunks = bn / 32.0;
+    const double fix = chunks * (2 * kSkWriteChunkUs + kSkRoundTripUs * ((covers + kSkDepth - 1) / kSkDepth));
+    const double t = static_cast<double>(dp_waves) * (sc.num_k * kb_us(bn) + kTileUs) + per * kb_us(bn) + kTileUs + fix;
+    if (t >= best.model_us) continue;
+    best.dp_tiles = static_cast<int>(dp_waves * sms);
+    best.sk_ctas = ctas;
+    best.sk_iters = iters;
+    best.grid = dp_waves > 0 ? sms : ctas;
+    best.counter_bytes = (sk_tiles * 4 * 4 + 255) / 256 * 256;
+    best.ws_bytes = best.counter_bytes + static_cast<std::int64_t>(ctas) * 2 * BM * bn * 4;
+    best.model_us = t;
+  }
+  return best;
+}
+
 }  // namespace
 
-// Tile width: the candidate minimising (waves over the SMs) x (per-tile MMA
-// time ~ BN, plus a fixed per-tile cost), so narrow / small GEMMs get more,
-// narrower tiles. PLANC_B200_GEMM_BN=256|128|64 forces one (experiments).
-int gemm_sm100_tile_n(const GemmArgs& a) {
+// Tile width and stream-K split: the candidate with the least modelled time
+// (data-parallel preferred unless stream-K is clearly faster, wider tiles
+// unless narrower ones are). PLANC_B200_GEMM_BN=256|128|64 forces a width,
+// PLANC_B200_STREAMK=0 disables stream-K, =2 takes it whenever it applies.
+GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   const char* env = std::getenv("PLANC_B200_GEMM_BN");
   const int forced = env ? std::atoi(env) : 0;
-  if (forced == 256 || forced == 128 || forced == 64) return forced;
-  const std::int64_t sms = 148;
-  int best = 256;
-  double best_cost = 1e300;
+  const char* skenv = std::getenv("PLANC_B200_STREAMK");
+  const int skmode = skenv ? std::atoi(skenv) : 1;
+  const bool allow_sk = skmode != 0 && a.epi.n_ops == 0 && (a.allow_streamk || skmode == 2);
+  GemmSchedule best;
+  bool have = false;
   for (int bn : {256, 128, 64}) {
-    const std::int64_t tiles = ((a.m + BM - 1) / BM) * ((a.n + bn - 1) / bn);
-    const std::int64_t waves = (tiles + sms - 1) / sms;
-    const double cost = static_cast<double>(waves) * (bn + 64.0);
-    if (cost < best_cost * 0.97) {  // prefer wider tiles unless clearly better
-      best_cost = cost;
-      best = bn;
+    if (forced && bn != forced) continue;
+    GemmSchedule dp = schedule_for(a.m, a.n, a.k, bn, false, sms);
+    GemmSchedule sk = schedule_for(a.m, a.n, a.k, bn, allow_sk, sms, skmode == 2);
+    GemmSchedule c = (sk.sk_ctas > 0 && (skmode == 2 || sk.model_us < 0.9 * dp.model_us)) ? sk : dp;
+    if (!have || c.model_us < best.model_us * 0.97) {
+      best = c;
+      have = true;
     }
   }
   return best;
+}
+
+int gemm_sm100_tile_n(const GemmArgs& a) { return gemm_sm100_schedule(a, 148).bn; }
+
+std::int64_t gemm_sm100_workspace_bytes(const GemmArgs& a) {
+  if (!gemm_sm100_eligible(a)) return 0;
+  return gemm_sm100_schedule(a, device_sms()).ws_bytes;
 }
 
 bool gemm_sm100_eligible(const GemmArgs& a) {
@@ -603,16 +811,20 @@ bool gemm_sm100_eligible(const GemmArgs& a) {
 
 void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
   const bool a_mn = a.ta, b_mn = !a.tb, cb = a.dc == DT_BF16;
-  const int bn = gemm_sm100_tile_n(a);
+  GemmSchedule sc = gemm_sm100_schedule(a, device_sms());
+  if (sc.sk_ctas > 0 && (a.ws == nullptr || a.ws_bytes < sc.ws_bytes)) {
+    sc = schedule_for(a.m, a.n, a.k, sc.bn, false, device_sms());  // no workspace: data-parallel
+  }
+  const int bn = sc.bn;
   if (a.epi.n_ops > 0) {
     if (!cb) throw std::runtime_error("fused GEMM epilogue needs a bf16 output");
     if (a.epi.n_ops != 1 || a.epi.n_slots > kMaxEpiSlots || a.epi.ops[0].n_in > kMaxEpiIn)
       throw std::runtime_error("fused GEMM epilogue: one elementwise op with <= 2 other operands");
 #define PLANC_TCF(AM, BMN)                                                      \
   if (a_mn == AM && b_mn == BMN) {                                             \
-    if (bn == 256) return launch_typed<AM, BMN, true, 256, true>(a, s);        \
-    if (bn == 128) return launch_typed<AM, BMN, true, 128, true>(a, s);        \
-    return launch_typed<AM, BMN, true, 64, true>(a, s);                        \
+    if (bn == 256) return launch_typed<AM, BMN, true, 256, true>(a, sc, s);    \
+    if (bn == 128) return launch_typed<AM, BMN, true, 128, true>(a, sc, s);    \
+    return launch_typed<AM, BMN, true, 64, true>(a, sc, s);                    \
   }
     PLANC_TCF(false, false)
     PLANC_TCF(false, true)
@@ -622,9 +834,9 @@ void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
   }
 #define PLANC_TC(AM, BMN, CB)                                                   \
   if (a_mn == AM && b_mn == BMN && cb == CB) {                                 \
-    if (bn == 256) return launch_typed<AM, BMN, CB, 256, false>(a, s);         \
-    if (bn == 128) return launch_typed<AM, BMN, CB, 128, false>(a, s);         \
-    return launch_typed<AM, BMN, CB, 64, false>(a, s);                         \
+    if (bn == 256) return launch_typed<AM, BMN, CB, 256, false>(a, sc, s);     \
+    if (bn == 128) return launch_typed<AM, BMN, CB, 128, false>(a, sc, s);     \
+    return launch_typed<AM, BMN, CB, 64, false>(a, sc, s);                     \
   }
   PLANC_TC(false, false, false)
   PLANC_TC(false, false, true)

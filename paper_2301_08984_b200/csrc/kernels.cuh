@@ -81,6 +81,30 @@ struct GemmArgs {
   bool ta, tb;
   int da, db, dc;
   EpiParams epi;
+  // Stream-K workspace (counters + fp32 partials), owned by the caller and
+  // used by one launch at a time; null / too small -> data-parallel only.
+  void* ws = nullptr;
+  std::int64_t ws_bytes = 0;
+  // Stream-K spends more SM-time than whole tiles for a shorter critical
+  // path: worth it when the GPU has nothing else to run (one lane per GPU),
+  // not when co-resident lanes fill the idle SMs with their own work.
+  bool allow_streamk = true;
+};
+
+// Launch schedule of the tcgen05 GEMM: tile width, persistent grid, and the
+// stream-K tail (tiles [dp_tiles, tiles) shared by sk_ctas CTAs in equal
+// k-iteration ranges).
+struct GemmSchedule {
+  int bn = 256;
+  int grid = 0;
+  std::int64_t tiles = 0;
+  std::int64_t num_k = 0;
+  int dp_tiles = 0;
+  int sk_ctas = 0;
+  long long sk_iters = 0;
+  std::int64_t counter_bytes = 0;
+  std::int64_t ws_bytes = 0;  // 0 without stream-K
+  double model_us = 0;
 };
 
 // Launchers (all asynchronous on `s`).
@@ -106,6 +130,8 @@ void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s);
 // tcgen05 / TMEM / TMA GEMM (gemm_sm100.cu).
 bool gemm_sm100_eligible(const GemmArgs& a);
 int gemm_sm100_tile_n(const GemmArgs& a);  // 256, 128 or 64
+GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms);
+std::int64_t gemm_sm100_workspace_bytes(const GemmArgs& a);  // on the current device
 void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s);
 
 // Dispatch: tcgen05 path when eligible, SIMT tile kernel otherwise.

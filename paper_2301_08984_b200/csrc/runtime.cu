@@ -282,7 +282,22 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       a.da = dt_of(prog_.buffers[in.in_bufs[0]].dtype);
       a.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
       a.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
-      if (opt_.allow_tensor_cores && gemm_sm100_eligible(a)) ++gemm_tc_per_step_;
+      a.allow_streamk = gemm_streamk_ok(exec_lane_[in.id]);
+      if (opt_.allow_tensor_cores && gemm_sm100_eligible(a)) {
+        ++gemm_tc_per_step_;
+        LaneRt& lr = lanes_[exec_lane_[in.id]];
+        DeviceGuard dg(lr.gpu);
+        std::int64_t& need = lr.gemm_ws_bytes[exec_stream_[in.id]];
+        need = std::max(need, gemm_sm100_workspace_bytes(a));
+      }
+    }
+  }
+  for (auto& lr : lanes_) {
+    for (int k = 0; k < kLaneStreams; ++k) {
+      if (lr.gemm_ws_bytes[k] == 0) continue;
+      DeviceGuard dg(lr.gpu);
+      ck(cudaMalloc(&lr.gemm_ws[k], lr.gemm_ws_bytes[k]), "cudaMalloc(gemm workspace)");
+      ck(cudaMemset(lr.gemm_ws[k], 0, lr.gemm_ws_bytes[k]), "memset(gemm workspace)");  // stream-K counters
     }
   }
 }
@@ -292,6 +307,8 @@ Executor::~Executor() {
     cudaSetDevice(l.gpu);
     for (auto& s : l.stream)
       if (s) cudaStreamDestroy(s);
+    for (void* w : l.gemm_ws)
+      if (w) cudaFree(w);
     if (l.arena) cudaFree(l.arena);
   }
   for (auto& r : irt_) {
@@ -317,6 +334,13 @@ Executor::~Executor() {
   if (ev_begin_) cudaEventDestroy(ev_begin_);
   if (ev_end_) cudaEventDestroy(ev_end_);
   if (origin_) cudaStreamDestroy(origin_);
+}
+
+bool Executor::gemm_streamk_ok(int lane) const {
+  int sharing = 0;
+  for (int l = 0; l < prog_.num_lanes; ++l)
+    if (owned_[l] && lanes_[l].gpu == lanes_[lane].gpu) ++sharing;
+  return sharing == 1;
 }
 
 void* Executor::buf_ptr(int b) const {
@@ -522,6 +546,12 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
           }
         }
         o.out = buf_ptr(fe.out_buf);
+      }
+      {
+        const LaneRt& lr = lanes_[exec_lane_[in.id]];
+        a.ws = lr.gemm_ws[exec_stream_[in.id]];
+        a.ws_bytes = lr.gemm_ws_bytes[exec_stream_[in.id]];
+        a.allow_streamk = gemm_streamk_ok(exec_lane_[in.id]);
       }
       if (a.epi.n_ops > 0 && !(opt_.allow_tensor_cores && gemm_sm100_eligible(a))) {
         throw InternalError("fused epilogue on a GEMM the tensor-core path does not take");

@@ -104,6 +104,9 @@ class Executor {
     int gpu = 0;
     char* arena = nullptr;
     cudaStream_t stream[kLaneStreams] = {};
+    // Stream-K GEMM workspace per stream (GEMMs on one stream never overlap).
+    void* gemm_ws[kLaneStreams] = {};
+    std::int64_t gemm_ws_bytes[kLaneStreams] = {};
   };
   struct BoxLaunch {
     DevCell* cells = nullptr;
@@ -120,6 +123,7 @@ class Executor {
   };
 
   void* buf_ptr(int b) const;
+  bool gemm_streamk_ok(int lane) const;  // the lane has its GPU to itself
   cudaStream_t stream_of(const Instr& in) const;
   void build_box_tables();
   void place_inputs();

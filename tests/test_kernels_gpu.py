@@ -82,6 +82,50 @@ def test_gemm_tcgen05_fp32_output(ta, tb):
     assert np.array_equal(out, ref)  # integer products, fp32 accumulate: exact
 
 
+# Stream-K tail (PLANC_B200_STREAMK=2 forces it wherever it applies): shapes
+# whose tiles do not fill whole waves, k not a multiple of a stream-K range,
+# tails in m / n / k, several CTAs per tile and several tiles per CTA.
+SK_SHAPES = [(512, 512, 16384, True, False), (256, 256, 8192, True, False), (8192, 2048, 2048, False, False),
+             (2048, 2048, 8192, True, False), (1000, 1000, 3000, False, True), (304, 520, 4200, True, True),
+             (136, 264, 1000, False, False)]
+
+
+@pytest.mark.parametrize("bn", ["256", "128", "64"])
+@pytest.mark.parametrize("m,n,k,ta,tb", SK_SHAPES)
+def test_gemm_streamk_vs_fp64(bn, m, n, k, ta, tb, monkeypatch):
+    monkeypatch.setenv("PLANC_B200_GEMM_BN", bn)
+    monkeypatch.setenv("PLANC_B200_STREAMK", "2")
+    sched = pb.gemm_schedule(m, n, k, ta, tb)
+    rng = np.random.default_rng(m + 3 * n + k)
+    plan, out_pt = matmul_plan(m, n, k, ta, tb)
+    a = bf16_round(rng.standard_normal((k, m) if ta else (m, k)))
+    b = bf16_round(rng.standard_normal((n, k) if tb else (k, n)))
+    with pb.Executor(plan, lane_gpus=[0]) as ex:
+        ex.set_inputs({0: a, 1: b})
+        ex.run(3)  # graph replays: the tile counters must be re-armed each launch
+        out = ex.get_output(out_pt)
+        ex.run(2)
+        again = ex.get_output(out_pt)
+    ref = (a.T if ta else a) @ (b.T if tb else b)
+    err = np.abs(out - ref).max() / max(1.0, np.abs(ref).max())
+    assert err < 2.0 ** -8, (err, sched)
+    assert np.array_equal(out, again)  # fixed reduction order: same bits every step
+
+
+@pytest.mark.parametrize("m,n,k,ta,tb", [(512, 512, 16384, True, False), (304, 520, 4200, True, True)])
+def test_gemm_streamk_fp32_exact(m, n, k, ta, tb, monkeypatch):
+    """Integer operands: every partial and the k-ordered sum are exact."""
+    monkeypatch.setenv("PLANC_B200_STREAMK", "2")
+    assert pb.gemm_schedule(m, n, k, ta, tb, c_bf16=False)["sk_ctas"] > 0
+    rng = np.random.default_rng(11)
+    plan, out_pt = matmul_plan(m, n, k, ta, tb, in_elem=2, out_elem=4)
+    a = rng.integers(-4, 5, size=(k, m) if ta else (m, k)).astype(np.float64)
+    b = rng.integers(-4, 5, size=(n, k) if tb else (k, n)).astype(np.float64)
+    out, st = run_single(plan, {0: a, 1: b}, out_pt)
+    assert st["gemm_tc_per_step"] == 1
+    assert np.array_equal(out, (a.T if ta else a) @ (b.T if tb else b))
+
+
 @pytest.mark.parametrize("m,n,k", [(37, 53, 29), (128, 256, 64), (300, 200, 100)])
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, True), (True, False)])
 @pytest.mark.parametrize("elem", [2, 4])

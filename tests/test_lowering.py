@@ -188,3 +188,41 @@ def test_accounting_matches_masks():
     flops = sum(i["flops"] for i in desc["instrs"] if i["kind"] == "gemm")
     T, H = 16, 8
     assert flops == pytest.approx(3 * 22 * T * H * H)  # fwd + 2x bwd GEMMs of the block
+
+
+@pytest.mark.parametrize("m,n,k,ta", [(8192, 2048, 2048, False), (512, 512, 16384, True), (256, 256, 8192, True),
+                                      (2048, 2048, 8192, True), (1000, 1000, 3000, False), (136, 264, 1000, False)])
+@pytest.mark.parametrize("sk_mode", ["1", "2"])
+def test_gemm_schedule_covers_every_k_block_once(m, n, k, ta, sk_mode, monkeypatch):
+    """The tcgen05 GEMM's work split (host-only): data-parallel tiles plus
+    stream-K ranges cover every (tile, k-block) exactly once, and every
+    shared tile's segments come from consecutive CTAs (the fixed reduction
+    order)."""
+    monkeypatch.setenv("PLANC_B200_STREAMK", sk_mode)
+    sms = 148
+    sc = pb.gemm_schedule(m, n, k, ta, False, sms=sms)
+    bn = sc["tile_n"]
+    tiles = -(-m // 128) * -(-n // bn)
+    num_k = -(-k // 64)
+    assert 0 < sc["grid"] <= sms
+    seen = {}
+    for b in range(sc["grid"]):
+        for t in range(b, sc["dp_tiles"], sc["grid"]):
+            for kb in range(num_k):
+                seen.setdefault((t, kb), []).append(b)
+    if sc["sk_ctas"]:
+        assert sc["ws_bytes"] > 0 and sc["dp_tiles"] % sms == 0
+        iters = (tiles - sc["dp_tiles"]) * num_k
+        lo = [b * iters // sc["sk_ctas"] for b in range(sc["sk_ctas"] + 1)]
+        for b in range(sc["sk_ctas"]):
+            for x in range(lo[b], lo[b + 1]):
+                seen.setdefault((sc["dp_tiles"] + x // num_k, x % num_k), []).append(b)
+    else:
+        assert sc["ws_bytes"] == 0 and sc["dp_tiles"] == tiles
+    assert sorted(seen) == [(t, kb) for t in range(tiles) for kb in range(num_k)]
+    assert all(len(v) == 1 for v in seen.values())
+    for t in range(sc["dp_tiles"], tiles):
+        owners = sorted({seen[(t, kb)][0] for kb in range(num_k)})
+        assert owners == list(range(owners[0], owners[-1] + 1))
+    if sk_mode == "2" and tiles % sms:
+        assert sc["sk_ctas"] > 0 or (tiles - sc["dp_tiles"]) * num_k < 8
