@@ -14,11 +14,14 @@ T=8192 tokens, H=2048, FFN=4H, bf16; TP degree = number of GPUs.
   python bench.py --impl reference ...   # the reference's CPU run_plan
 
 Multi-GPU: under torchrun one process per GPU — rank r runs plan lane r on
-LOCAL_RANK's GPU; pieces of other ranks' lanes move in NCCL exchange steps
-(all-reduce groups as ncclAllReduce). Times are the max over ranks (CUDA
-events per rank). Without torchrun, --gpus N drives N GPUs from one process
-(lanes read each other's buffers over NVLink peer mappings). Prints ONE
-JSON line (rank 0).
+LOCAL_RANK's GPU. Transport (--transport): `peer` (default) maps every
+other rank's lane arenas through CUDA IPC, so adapter box kernels read the
+peer GPU's pieces in place over NVLink (all-reduces as a reduce-scatter
+phase + an all-gather phase) and cross-rank order is kept by device flags;
+`nccl` moves whole pieces in NCCL exchange steps (all-reduce groups as
+ncclAllReduce). Times are the max over ranks (CUDA events per rank).
+Without torchrun, --gpus N drives N GPUs from one process (lanes read each
+other's buffers over NVLink peer mappings). Prints ONE JSON line (rank 0).
 """
 from __future__ import annotations
 
@@ -192,6 +195,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c2", "c1l", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="one-process-per-GPU data path (torchrun): CUDA-IPC peer memory or NCCL exchange steps")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -220,17 +225,41 @@ def main():
     peaks = measured_peaks()
     inputs = synthetic_inputs(plan)
     nlanes = len(json.loads(plan)["lanes"])
+    transport = None
     if dist:
         # One process per GPU: this rank runs lanes l with l % world == rank
-        # on its local GPU; cross-rank pieces move over NCCL.
+        # on its local GPU; cross-rank pieces move over NVLink (peer memory or
+        # NCCL).
         import torch
 
         local = int(os.environ.get("LOCAL_RANK", rank))
+        if os.environ.get("PLANC_B200_BENCH_SAME_GPU"):  # test hook: every rank on GPU 0
+            local = 0
         torch.cuda.set_device(local)
-        box = [pb.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(box, src=0)
-        ex = pb.Executor(plan, rank=rank, world=world, lane_rank=pb.lanes_round_robin(nlanes, world),
-                         local_gpu=local, nccl_id=box[0])
+        lane_rank = pb.lanes_round_robin(nlanes, world)
+        transport = args.transport
+        ex = None
+        if transport == "peer":
+            def exchange(blob):
+                out = [None] * world
+                dist.all_gather_object(out, blob)
+                return out
+
+            try:
+                ex = pb.Executor(plan, rank=rank, world=world, lane_rank=lane_rank, local_gpu=local,
+                                 peer_exchange=exchange)
+            except pb.PlancError as e:  # e.g. no CUDA IPC between these GPUs
+                transport = "nccl (peer memory unavailable: %s)" % str(e)[:120]
+            ok = torch.tensor([1 if ex is not None else 0])
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() == 0 and ex is not None:
+                ex.close()
+                ex = None
+                transport = "nccl (peer memory unavailable on another rank)"
+        if ex is None:
+            box = [pb.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0)
+            ex = pb.Executor(plan, rank=rank, world=world, lane_rank=lane_rank, local_gpu=local, nccl_id=box[0])
     else:
         ex = pb.Executor(plan, lane_gpus=list(range(n)))
     ex.set_inputs(inputs)
@@ -255,6 +284,8 @@ def main():
     e2e_ms, h2d, d2h = ex.run_e2e(args.steps)
     e2e_ms = max_over_ranks(e2e_ms)
     prof = [ex.profile() for _ in range(3)]  # every rank: exchange steps pair up
+    if dist:
+        dist.barrier()  # peer memory: no rank unmaps / frees while another still reads
     ex.close()
     if rank == 0:
         sps = meta["samples_per_step"] / (ms / 1e3)
@@ -316,7 +347,12 @@ def main():
                         "tflops" if k.startswith("gemm") else "gbs":
                             round((v["flops"] / 1e12 if k.startswith("gemm") else v["bytes"] / 1e9)
                                   / max(v["ms"] / 1e3, 1e-12), 2)} for k, v in fam.items()}
-        coll = fam.get("box_collective")
+        # Adapter bus bandwidth: wire bytes (NCCL bus-bandwidth convention) of
+        # the cross-GPU adapter launches over their device time.
+        adapters = [fam[k] for k in ("box_collective", "box_p2p", "xfer_nccl") if k in fam]
+        coll = None
+        if adapters:
+            coll = {"wire": sum(a["wire"] for a in adapters), "ms": sum(a["ms"] for a in adapters)}
         result = {
             "metric": "plan step samples/sec", "value": sps, "unit": "samples/s", "n_gpus": n,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -329,6 +365,8 @@ def main():
                        "lanes_per_gpu": nlanes / max(n, 1),
                        "sample": meta["sample"], "l2": "step working set " +
                        f"{st['device_bytes'] / 2**30:.1f} GiB > 126 MB L2 (no flush needed)",
+                       "transport": (("peer memory (CUDA IPC over NVLink, device flags)" if transport == "peer"
+                                      else transport) if dist else "single process"),
                        "lanes": st["num_lanes"], "tasks": st["num_tasks"], "launch": (
                            "CUDA graph" if st["graph_captured"] else "eager")},
             "roofline": roof,

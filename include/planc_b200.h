@@ -47,6 +47,8 @@ extern "C" {
 #define PLANC_B200_FUSE_EPILOGUES 0x10u /* an elementwise op consuming a fresh bf16 GEMM output on
                                            the same lane runs in that GEMM's epilogue (same bits as
                                            the separate kernel; default: every op its own kernel) */
+#define PLANC_B200_PEER_MEMORY 0x20u     /* planc_b200_open_rank / describe_rank: peer-memory transport
+                                           (CUDA IPC over NVLink, device flags) instead of NCCL */
 #define PLANC_B200_SERIAL_LANES 0x8u    /* one stream per lane: a lane's tasks run strictly in plan
                                            order (default: only data dependencies and sync edges order
                                            a lane's work, spread over several streams) */
@@ -76,9 +78,25 @@ int planc_b200_nccl_unique_id(unsigned char id_out[128]);
 int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* lane_rank, int num_lanes,
                          int local_gpu, const unsigned char nccl_id[128], uint32_t flags,
                          planc_b200_exec** out);
-/* Host-only: the rank-localised program (same on every rank), as JSON. */
+/* Host-only: the rank-localised program (same on every rank), as JSON.
+ * With PLANC_B200_PEER_MEMORY: the global program and its cross-rank flag
+ * schedule ("peer_sync": per-instruction wait slots and (rank, slot) signals). */
 int planc_b200_describe_rank(const char* plan_json, const int* lane_rank, int num_lanes, uint32_t flags,
                              char** json_out);
+
+/* Peer-memory transport (open_rank with PLANC_B200_PEER_MEMORY; nccl_id may
+ * be NULL). No NCCL: each rank maps every other rank's lane arenas through
+ * CUDA IPC (NVLink peer memory); adapter box kernels — split / concat /
+ * reduce-assemble / recv / every collective member output, all-reduces as a
+ * reduce-scatter phase plus an all-gather phase — read the pieces in place on
+ * the peer GPU, and cross-rank dependencies are device flags (release /
+ * acquire at system scope, a step-end barrier across ranks). Before the first
+ * step every rank exports a blob of planc_b200_peer_blob_bytes bytes, the
+ * caller all-gathers them (rank order, concatenated) and every rank imports
+ * the lot. After import, get_output / read_buffer read any rank's pieces. */
+int64_t planc_b200_peer_blob_bytes(planc_b200_exec* h);
+int planc_b200_peer_export(planc_b200_exec* h, unsigned char* blob, int64_t capacity);
+int planc_b200_peer_import(planc_b200_exec* h, const unsigned char* blobs, int64_t blob_bytes);
 
 /* Binds one graph-input pTensor (refexec.cpp:366-376); `data` is dense
  * row-major with `rank` extents `shape`. Copied; placed on the GPU at the

@@ -37,6 +37,7 @@ NO_TENSOR_CORES = 0x2
 STRICT_VALUE = 0x4
 SERIAL_LANES = 0x8
 FUSE_EPILOGUES = 0x10
+PEER_MEMORY = 0x20
 
 
 class PlancError(RuntimeError):
@@ -110,6 +111,10 @@ def _load():
     L.planc_b200_nccl_unique_id.argtypes = [ctypes.c_char_p]
     L.planc_b200_open_rank.argtypes = [ctypes.c_char_p, c_int, c_int, P(c_int), c_int, c_int, ctypes.c_char_p,
                                        ctypes.c_uint32, P(vp)]
+    L.planc_b200_peer_blob_bytes.argtypes = [vp]
+    L.planc_b200_peer_blob_bytes.restype = c_i64
+    L.planc_b200_peer_export.argtypes = [vp, ctypes.c_char_p, c_i64]
+    L.planc_b200_peer_import.argtypes = [vp, ctypes.c_char_p, c_i64]
     L.planc_b200_gemm_schedule.argtypes = [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, P(c_int), P(c_int),
                                            P(c_int), P(c_int), P(c_i64)]
     L.planc_b200_free.argtypes = [vp]
@@ -136,7 +141,9 @@ def describe(plan_json: str, strict_value: bool = False, lane_rank=None, flags: 
     """Host-only lowering of a plan (no GPU): buffers, instructions, cells.
 
     With ``lane_rank`` (owner rank per plan lane) the one-process-per-GPU
-    program is returned: cross-rank pieces become ``xfer`` exchange steps.
+    program is returned: cross-rank pieces become ``xfer`` exchange steps
+    (NCCL transport), or — with ``flags`` including PEER_MEMORY — the global
+    program plus its cross-rank flag schedule (``peer_sync``).
     """
     L = _load()
     out = ctypes.c_void_p()
@@ -179,18 +186,31 @@ def lanes_round_robin(num_lanes: int, world: int):
 class Executor:
     """One compiled plan on the GPU(s). ``lane_gpus[i]`` runs plan lane i.
 
-    ``rank``/``world``/``lane_rank``/``nccl_id`` select the one-process-per-GPU
-    mode: this process runs the lanes it owns on ``local_gpu``.
+    ``rank``/``world``/``lane_rank`` select the one-process-per-GPU mode: this
+    process runs the lanes it owns on ``local_gpu``. Transport: NCCL exchange
+    steps (``nccl_id`` from rank 0), or peer memory (``peer_exchange``: a
+    callable all-gathering one ``bytes`` blob per rank, e.g. over
+    torch.distributed — every rank maps the others' arenas via CUDA IPC).
     """
 
     def __init__(self, plan_json: str, lane_gpus=None, flags: int = 0, rank=None, world=None, lane_rank=None,
-                 local_gpu: int = 0, nccl_id: bytes = None):
+                 local_gpu: int = 0, nccl_id: bytes = None, peer_exchange=None):
         L = _load()
         self._h = ctypes.c_void_p()
         if rank is not None:
             arr = (ctypes.c_int * len(lane_rank))(*lane_rank)
+            if peer_exchange is not None:
+                flags |= PEER_MEMORY
             _check(L.planc_b200_open_rank(plan_json.encode(), rank, world, arr, len(lane_rank), local_gpu,
                                           nccl_id, flags, ctypes.byref(self._h)))
+            if peer_exchange is not None:
+                n = L.planc_b200_peer_blob_bytes(self._h)
+                blob = ctypes.create_string_buffer(n)
+                _check(L.planc_b200_peer_export(self._h, blob, n))
+                blobs = list(peer_exchange(blob.raw))
+                if len(blobs) != world or any(len(b) != n for b in blobs):
+                    raise UsageError("peer_exchange must return one blob per rank")
+                _check(L.planc_b200_peer_import(self._h, b"".join(blobs), n))
             return
         arr, n = None, 0
         if lane_gpus:

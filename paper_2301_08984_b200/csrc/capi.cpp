@@ -95,7 +95,9 @@ int planc_b200_nccl_unique_id(unsigned char id_out[128]) {
 int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* lane_rank, int num_lanes,
                          int local_gpu, const unsigned char nccl_id[128], uint32_t flags, planc_b200_exec** out) {
   return guarded([&] {
-    if (!plan_json || !out || !lane_rank || !nccl_id) throw UsageError("planc_b200_open_rank: null argument");
+    const bool peer = (flags & PLANC_B200_PEER_MEMORY) != 0;
+    if (!plan_json || !out || !lane_rank || (!nccl_id && !peer)) throw UsageError("planc_b200_open_rank: null argument");
+    if (num_lanes < 1) throw UsageError("planc_b200_open_rank: the plan's lanes need owners");
     ExecOptions opt;
     opt.use_graph = (flags & PLANC_B200_NO_GRAPH) == 0;
     opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
@@ -107,7 +109,8 @@ int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* 
     rc.world = world;
     rc.lane_rank.assign(lane_rank, lane_rank + num_lanes);
     rc.local_gpu = local_gpu;
-    std::memcpy(rc.nccl_id, nccl_id, 128);
+    if (nccl_id) std::memcpy(rc.nccl_id, nccl_id, 128);
+    rc.peer_memory = peer;
     auto* h = new planc_b200_exec;
     try {
       h->ex = new Executor(plan_json, {}, opt, &rc);
@@ -127,8 +130,56 @@ int planc_b200_describe_rank(const char* plan_json, const int* lane_rank, int nu
                                         (flags & PLANC_B200_FUSE_EPILOGUES) != 0 &&
                                             (flags & PLANC_B200_NO_TENSOR_CORES) == 0);
     ExecutionPlan plan = load_plan(plan_json);
-    Program p = localize(build_program(plan, po), std::vector<int>(lane_rank, lane_rank + num_lanes));
-    *json_out = dup(p.describe_json());
+    const std::vector<int> lr(lane_rank, lane_rank + num_lanes);
+    if ((flags & PLANC_B200_PEER_MEMORY) == 0) {
+      po.two_phase_allreduce = false;  // NCCL exchange steps: whole-buffer ncclAllReduce
+      *json_out = dup(localize(build_program(plan, po), lr).describe_json());
+      return;
+    }
+    // Peer-memory mode: the global program plus its cross-rank flag schedule.
+    Program p = build_program(plan, po);
+    PeerSync ps = peer_sync_schedule(p, lr);
+    std::string js = p.describe_json();
+    std::ostringstream os;
+    os << ",\"peer_sync\":{\"slots\":[";
+    for (std::size_t r = 0; r < ps.slots.size(); ++r) os << (r ? "," : "") << ps.slots[r];
+    os << "],\"waits\":[";
+    for (std::size_t i = 0; i < ps.waits.size(); ++i) {
+      os << (i ? "," : "") << "[";
+      for (std::size_t j = 0; j < ps.waits[i].size(); ++j) os << (j ? "," : "") << ps.waits[i][j];
+      os << "]";
+    }
+    os << "],\"signals\":[";
+    for (std::size_t i = 0; i < ps.signals.size(); ++i) {
+      os << (i ? "," : "") << "[";
+      for (std::size_t j = 0; j < ps.signals[i].size(); ++j)
+        os << (j ? "," : "") << "[" << ps.signals[i][j].first << "," << ps.signals[i][j].second << "]";
+      os << "]";
+    }
+    os << "]}}";
+    js.pop_back();  // closing brace of the program object
+    *json_out = dup(js + os.str());
+  });
+}
+
+int64_t planc_b200_peer_blob_bytes(planc_b200_exec* h) {
+  if (!h) return -1;
+  return peer_blob_bytes(h->ex->program().num_lanes);
+}
+
+int planc_b200_peer_export(planc_b200_exec* h, unsigned char* blob, int64_t capacity) {
+  return guarded([&] {
+    if (!h || !blob) throw UsageError("planc_b200_peer_export: null argument");
+    std::vector<unsigned char> b = h->ex->peer_export();
+    if (capacity < static_cast<int64_t>(b.size())) throw UsageError("planc_b200_peer_export: blob capacity too small");
+    std::memcpy(blob, b.data(), b.size());
+  });
+}
+
+int planc_b200_peer_import(planc_b200_exec* h, const unsigned char* blobs, int64_t blob_bytes) {
+  return guarded([&] {
+    if (!h || !blobs) throw UsageError("planc_b200_peer_import: null argument");
+    h->ex->peer_import(blobs, blob_bytes);
   });
 }
 

@@ -585,4 +585,46 @@ void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s) {
   check_launch("zero_kernel");
 }
 
+// ---- peer-memory flags ------------------------------------------------------
+
+__global__ void peer_epoch_kernel(unsigned* epoch) { *epoch += 1u; }
+
+__global__ void peer_flags_kernel(const unsigned* epoch, PeerFlags f, unsigned long long timeout_ns, unsigned* err) {
+  const unsigned e = *reinterpret_cast<const volatile unsigned*>(epoch);
+  const int t = threadIdx.x;
+  if (t < f.n_sig) {
+    // Everything this stream wrote before this kernel is visible at system
+    // scope to whoever acquires the flag.
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.sig[t]), "r"(e) : "memory");
+  }
+  if (t < f.n_wait) {
+    unsigned long long t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f.wait[t]) : "memory");
+      if (static_cast<int>(v - e) >= 0) break;  // wrap-safe v >= e
+      __nanosleep(256);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > timeout_ns) {
+        if (err) *reinterpret_cast<volatile unsigned*>(err) = f.code;
+        __threadfence_system();
+        __trap();
+      }
+    }
+  }
+}
+
+void launch_peer_epoch(unsigned* epoch, cudaStream_t s) {
+  peer_epoch_kernel<<<1, 1, 0, s>>>(epoch);
+  check_launch("peer_epoch_kernel");
+}
+
+void launch_peer_flags(const unsigned* epoch, const PeerFlags& f, unsigned long long timeout_ns, unsigned* err,
+                       cudaStream_t s) {
+  peer_flags_kernel<<<1, 32, 0, s>>>(epoch, f, timeout_ns, err);
+  check_launch("peer_flags_kernel");
+}
+
 }  // namespace planc_b200

@@ -127,6 +127,25 @@ void launch_gemm_simt(const GemmArgs& a, cudaStream_t s);
 void launch_convert(int dtype_out, void* out, const float* in, std::int64_t count, cudaStream_t s);
 void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s);
 
+// Cross-rank ordering in peer-memory mode (program.hpp PeerSync). One
+// launch first publishes the step epoch (*epoch) to every `sig` flag
+// (release at system scope: the stream's earlier writes are visible to a
+// peer that acquires the flag), then waits until every `wait` flag has
+// reached the epoch (acquire, system scope). A wait that does not complete
+// within timeout_ns records `code` in *err (host-mapped) and traps, so a
+// broken schedule fails the context instead of hanging the GPU.
+constexpr int kMaxPeerFlags = 16;
+struct PeerFlags {
+  int n_sig = 0;
+  int n_wait = 0;
+  unsigned* sig[kMaxPeerFlags] = {};
+  const unsigned* wait[kMaxPeerFlags] = {};
+  unsigned code = 0;  // reported on timeout (instruction id + 1, or ~0u for the step barrier)
+};
+void launch_peer_epoch(unsigned* epoch, cudaStream_t s);
+void launch_peer_flags(const unsigned* epoch, const PeerFlags& f, unsigned long long timeout_ns, unsigned* err,
+                       cudaStream_t s);
+
 // tcgen05 / TMEM / TMA GEMM (gemm_sm100.cu).
 bool gemm_sm100_eligible(const GemmArgs& a);
 int gemm_sm100_tile_n(const GemmArgs& a);  // 256, 128 or 64

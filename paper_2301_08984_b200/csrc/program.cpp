@@ -717,6 +717,7 @@ struct Builder {
 Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt) {
   Builder b(plan, opt);
   b.run();
+  if (opt.two_phase_allreduce) two_phase_allreduce(b.P);
   if (opt.fuse_epilogues) fuse_gemm_epilogues(b.P, opt);
   return std::move(b.P);
 }
@@ -812,6 +813,204 @@ void fuse_gemm_epilogues(Program& P, const ProgramOptions& opt) {
       in.deps.erase(std::remove(in.deps.begin(), in.deps.end(), in.id), in.deps.end());
     }
   }
+}
+
+namespace {
+
+// Per-lane and total accounting from the instruction list.
+void recount(Program& P) {
+  P.lane_flops.assign(P.num_lanes, 0);
+  P.lane_bytes.assign(P.num_lanes, 0);
+  P.lane_wire_bytes.assign(P.num_lanes, 0);
+  P.total_flops = P.total_bytes = P.total_wire_bytes = 0;
+  for (const auto& in : P.instrs) {
+    const double by = in.kind == InstrKind::gemm ? 0 : in.bytes;
+    P.lane_flops[in.lane] += in.flops;
+    P.lane_bytes[in.lane] += by;
+    P.lane_wire_bytes[in.lane] += in.wire_bytes;
+    P.total_flops += in.flops;
+    P.total_bytes += by;
+    P.total_wire_bytes += in.wire_bytes;
+  }
+}
+
+// The members of an all-reduce group in issue order: every member output is
+// one rank-1 cell covering the whole buffer whose terms add the same k whole
+// input buffers (one per member lane, same order for every member). Returns
+// the inputs in term order, or an empty vector when the group is anything
+// else (reduce-scatter, all-gather, partial targets, ...).
+std::vector<int> allreduce_inputs(const Program& P, const std::vector<int>& grp) {
+  std::vector<int> inputs;
+  std::set<int> lanes, in_lanes;
+  for (int id : grp) {
+    const Instr& in = P.instrs[id];
+    if (in.kind != InstrKind::box || in.out_bufs.size() != 1 || in.cells.size() != 1) return {};
+    const BufferDesc& ob = P.buffers[in.out_bufs[0]];
+    if (!lanes.insert(in.lane).second) return {};
+    const Cell& c = in.cells[0];
+    if (c.rank != 1 || c.dst_offset != 0 || c.dst_strides[0] != 1 || c.elems() != ob.elems ||
+        c.terms.size() != grp.size())
+      return {};
+    std::vector<int> ts;
+    for (const auto& t : c.terms) {
+      const BufferDesc& sb = P.buffers[t.buffer];
+      if (!t.add || t.offset != 0 || t.strides[0] != 1 || sb.elems != ob.elems || sb.dtype != ob.dtype) return {};
+      ts.push_back(t.buffer);
+    }
+    if (inputs.empty()) inputs = ts;
+    if (ts != inputs) return {};
+  }
+  for (int b : inputs)
+    if (!in_lanes.insert(P.buffers[b].lane).second) return {};
+  if (in_lanes != lanes) return {};
+  return inputs;
+}
+
+}  // namespace
+
+void two_phase_allreduce(Program& g) {
+  Program P = g;
+  P.instrs.clear();
+  P.issue_order.clear();
+  std::vector<int> remap(g.instrs.size(), -1);
+  auto push = [&](Instr in) {
+    in.id = static_cast<int>(P.instrs.size());
+    P.instrs.push_back(std::move(in));
+    P.issue_order.push_back(P.instrs.back().id);
+    return P.instrs.back().id;
+  };
+  auto remapped = [&](const std::vector<int>& deps) {
+    std::set<int> d;
+    for (int x : deps) {
+      if (remap[x] < 0) throw InternalError("two-phase all-reduce: dependency issued after its consumer");
+      d.insert(remap[x]);
+    }
+    return std::vector<int>(d.begin(), d.end());
+  };
+  const auto& order = g.issue_order;
+  std::size_t i = 0;
+  while (i < order.size()) {
+    std::vector<int> grp = {order[i]};
+    const Instr& first = g.instrs[order[i]];
+    if (first.kind == InstrKind::box && first.coll_group >= 0) {
+      while (i + grp.size() < order.size()) {
+        const Instr& nx = g.instrs[order[i + grp.size()]];
+        if (nx.kind != InstrKind::box || nx.coll_group != first.coll_group) break;
+        grp.push_back(nx.id);
+      }
+    }
+    const std::int64_t k = static_cast<std::int64_t>(grp.size());
+    std::vector<int> inputs = k > 1 ? allreduce_inputs(g, grp) : std::vector<int>{};
+    const std::int64_t E = inputs.empty() ? 0 : g.buffers[first.out_bufs[0]].elems;
+    constexpr std::int64_t kAlign = 8;  // 16-byte bf16 / 32-byte fp32 slice boundaries
+    if (inputs.empty() || E < kAlign * k) {
+      for (int id : grp) {
+        Instr in = g.instrs[id];
+        in.deps = remapped(in.deps);
+        remap[id] = push(std::move(in));
+      }
+      i += grp.size();
+      continue;
+    }
+    std::vector<std::int64_t> bound(k + 1);
+    for (std::int64_t j = 0; j <= k; ++j) bound[j] = j == k ? E : (E * j / k) / kAlign * kAlign;
+    const std::int64_t es = dtype_size(g.buffers[first.out_bufs[0]].dtype);
+    auto slice_cell = [&](std::int64_t j) {
+      Cell c;
+      c.rank = 1;
+      c.extents[0] = bound[j + 1] - bound[j];
+      c.dst_offset = bound[j];
+      c.dst_strides[0] = 1;
+      return c;
+    };
+    // Phase 1 (reduce-scatter): member j reduces slice j of every input.
+    std::vector<int> rs(k);
+    for (std::int64_t j = 0; j < k; ++j) {
+      Instr in = g.instrs[grp[j]];
+      Cell c = slice_cell(j);
+      for (const auto& t0 : in.cells[0].terms) {
+        Term t = t0;
+        t.offset = bound[j];
+        c.terms.push_back(t);
+      }
+      in.cells = {c};
+      in.in_bufs = inputs;
+      std::sort(in.in_bufs.begin(), in.in_bufs.end());
+      in.deps = remapped(in.deps);
+      in.bytes = static_cast<double>(c.elems()) * es * (1 + k);
+      in.wire_bytes = g.instrs[grp[j]].wire_bytes / 2;
+      in.label += "#rs";
+      rs[j] = push(std::move(in));
+    }
+    // Phase 2 (all-gather): member j copies every other member's slice.
+    for (std::int64_t j = 0; j < k; ++j) {
+      Instr in = g.instrs[grp[j]];
+      in.cells.clear();
+      in.in_bufs.clear();
+      std::int64_t moved = 0;
+      for (std::int64_t o = 0; o < k; ++o) {
+        if (o == j) continue;
+        Cell c = slice_cell(o);
+        Term t;
+        t.buffer = g.instrs[grp[o]].out_bufs[0];
+        t.offset = bound[o];
+        t.strides[0] = 1;
+        t.add = false;
+        c.terms.push_back(t);
+        moved += c.elems();
+        in.cells.push_back(c);
+        in.in_bufs.push_back(t.buffer);
+      }
+      std::sort(in.in_bufs.begin(), in.in_bufs.end());
+      std::vector<int> deps = remapped(in.deps);
+      deps.insert(deps.end(), rs.begin(), rs.end());
+      std::sort(deps.begin(), deps.end());
+      deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+      in.deps = deps;
+      in.bytes = static_cast<double>(moved) * es * 2;
+      in.wire_bytes = g.instrs[grp[j]].wire_bytes / 2;
+      in.label += "#ag";
+      remap[grp[j]] = push(std::move(in));
+    }
+    i += grp.size();
+  }
+  for (auto& b : P.buffers)
+    if (b.producer >= 0) b.producer = remap[b.producer];
+  for (auto& in : P.instrs)
+    for (auto& f : in.fused)
+      if (f.ew_instr >= 0) f.ew_instr = remap[f.ew_instr];
+  recount(P);
+  g = std::move(P);
+}
+
+PeerSync peer_sync_schedule(const Program& p, const std::vector<int>& lane_rank) {
+  if (static_cast<int>(lane_rank.size()) != p.num_lanes) {
+    throw UsageError("lane_rank must name an owner for each of the plan's " + std::to_string(p.num_lanes) +
+                     " lanes");
+  }
+  int world = 0;
+  for (int r : lane_rank) world = std::max(world, r + 1);
+  PeerSync s;
+  s.waits.resize(p.instrs.size());
+  s.signals.resize(p.instrs.size());
+  s.slots.assign(world, 0);
+  std::map<std::pair<int, int>, int> slot;  // (producer instr, consumer rank) -> slot
+  for (const auto& in : p.instrs) {
+    if (in.kind == InstrKind::nop) continue;
+    const int rc = lane_rank[in.lane];
+    for (int d : in.deps) {
+      const Instr& pr = p.instrs[d];
+      if (pr.kind == InstrKind::nop || lane_rank[pr.lane] == rc) continue;
+      auto key = std::make_pair(d, rc);
+      auto it = slot.find(key);
+      if (it == slot.end()) {
+        it = slot.emplace(key, s.slots[rc]++).first;
+        s.signals[d].push_back({rc, it->second});
+      }
+      s.waits[in.id].push_back(it->second);
+    }
+  }
+  return s;
 }
 
 Program localize(const Program& g, const std::vector<int>& lane_rank) {

@@ -142,6 +142,13 @@ struct ProgramOptions {
   // into that GEMM's epilogue (local form), for GEMMs the
   // predicate accepts (the tensor-core path implements the fused epilogue).
   bool fuse_epilogues = false;
+  // All-reduce groups (every member output = the sum of the same k whole
+  // member inputs) as two box phases: member j sums slice j of all inputs
+  // (reduce-scatter), then copies the other members' reduced slices
+  // (all-gather). Same terms in the same order, so the same bits; each
+  // member reads ~2n instead of k*n (over NVLink when members sit on other
+  // GPUs or ranks).
+  bool two_phase_allreduce = true;
   bool (*gemm_fusable)(const Instr& gemm, DType a, DType b, DType c) = nullptr;
 };
 
@@ -173,6 +180,27 @@ Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt = {})
 // other operands are ready before that GEMM, is computed in the GEMM's
 // epilogue; the op's instruction becomes a nop.
 void fuse_gemm_epilogues(Program& p, const ProgramOptions& opt);
+
+// The two-phase all-reduce pass (ProgramOptions::two_phase_allreduce), run
+// by build_program before epilogue fusion. Rebuilds the program in issue
+// order (instruction ids stay dense and ascending along the issue order).
+void two_phase_allreduce(Program& p);
+
+// Peer-memory one-process-per-GPU mode: every rank runs the global program's
+// instructions of its own lanes and reads other ranks' buffers in place
+// (CUDA IPC mappings of their arenas over NVLink). A dependency edge between
+// instructions of different ranks becomes a device flag: after the producer,
+// its rank writes the step epoch into a ready slot owned by the consumer's
+// rank; before the consumer, its rank waits until that slot reaches the
+// epoch. Slots are numbered per consumer rank in instruction order, so every
+// rank derives the same numbering. (Cross-step reuse of a buffer is ordered by
+// a step-end barrier across ranks.)
+struct PeerSync {
+  std::vector<std::vector<int>> waits;                    // per instr: ready slots on its own rank
+  std::vector<std::vector<std::pair<int, int>>> signals;  // per instr: (consumer rank, slot)
+  std::vector<int> slots;                                 // per rank: number of ready slots
+};
+PeerSync peer_sync_schedule(const Program& p, const std::vector<int>& lane_rank);
 
 // One-process-per-GPU lowering: the same global program on every rank, with
 // every box term that lives on another rank's lane redirected to a shadow

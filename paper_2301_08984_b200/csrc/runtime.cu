@@ -116,6 +116,9 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
     : opt_(opt) {
   plan_ = load_plan(plan_json);
   ProgramOptions po = program_options(opt.value_split_extension, opt.fuse_epilogues && opt.allow_tensor_cores);
+  // NCCL exchange steps lower whole-buffer all-reduce groups to
+  // ncclAllReduce; every other mode runs them as two box phases.
+  po.two_phase_allreduce = !(rank && !rank->peer_memory);
   prog_ = build_program(plan_, po);
   if (rank) {
     rank_mode_ = true;
@@ -124,7 +127,13 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
     for (int r : rc_.lane_rank) {
       if (r < 0 || r >= rc_.world) throw UsageError("lane_rank entry outside [0, world)");
     }
-    prog_ = localize(prog_, rc_.lane_rank);
+    if (rc_.peer_memory) {
+      if (rc_.world > kPeerMaxRanks) throw UsageError("peer-memory mode supports at most 64 ranks");
+      peer_ = true;
+      psync_ = peer_sync_schedule(prog_, rc_.lane_rank);
+    } else {
+      prog_ = localize(prog_, rc_.lane_rank);
+    }
   }
   int ndev = 0;
   ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
@@ -183,7 +192,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       last[el][pick] = id;
     }
   }
-  if (rank_mode_) {
+  if (rank_mode_ && !peer_) {
     DeviceGuard dg(rc_.local_gpu);
     ncclUniqueId id;
     std::memcpy(id.internal, rc_.nccl_id, sizeof(id.internal));
@@ -261,13 +270,32 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       ck(cudaMalloc(&irt_[in.id].scratch, sizeof(float) * in.rows * in.h), "cudaMalloc(scratch)");
     }
   }
-  build_box_tables();
+  if (peer_) {
+    // This rank's flag block: epoch, step barrier slots, ready slots.
+    DeviceGuard dg(rc_.local_gpu);
+    const std::size_t words = kFlagReady + static_cast<std::size_t>(psync_.slots[rc_.rank]) + 1;
+    ck(cudaMalloc(&flags_, words * sizeof(unsigned)), "cudaMalloc(peer flags)");
+    ck(cudaMemset(flags_, 0, words * sizeof(unsigned)), "memset(peer flags)");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&peer_err_), sizeof(unsigned), cudaHostAllocMapped), "cudaHostAlloc");
+    *peer_err_ = 0;
+    double secs = 60.0;
+    if (const char* t = std::getenv("PLANC_B200_PEER_TIMEOUT_S")) secs = std::max(0.1, std::atof(t));
+    peer_timeout_ns_ = static_cast<unsigned long long>(secs * 1e9);
+    lane_mapped_.assign(prog_.num_lanes, false);
+    // Box tables need every rank's arena: built by peer_import.
+  } else {
+    build_box_tables();
+  }
   kernels_per_step_ = 0;
   for (const auto& in : prog_.instrs) {
     if (exec_lane_[in.id] < 0) continue;
+    if (peer_) {
+      kernels_per_step_ += static_cast<int>((psync_.waits[in.id].size() + kMaxPeerFlags - 1) / kMaxPeerFlags);
+      kernels_per_step_ += static_cast<int>((psync_.signals[in.id].size() + kMaxPeerFlags - 1) / kMaxPeerFlags);
+    }
     switch (in.kind) {
       case InstrKind::nop: break;
-      case InstrKind::box: kernels_per_step_ += static_cast<int>(irt_[in.id].box.size()); break;
+      case InstrKind::box: kernels_per_step_ += static_cast<int>(irt_[in.id].box.size()); break;  // peer: at import
       case InstrKind::emb_grad: kernels_per_step_ += prog_.buffers[in.out_bufs[0]].dtype == DType::f32 ? 2 : 3; break;
       case InstrKind::ew: kernels_per_step_ += 1 + (in.count % 8 != 0 ? 1 : 0); break;
       default: kernels_per_step_ += 1;
@@ -303,14 +331,18 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
 }
 
 Executor::~Executor() {
-  for (auto& l : lanes_) {
+  for (std::size_t i = 0; i < lanes_.size(); ++i) {
+    auto& l = lanes_[i];
     cudaSetDevice(l.gpu);
     for (auto& s : l.stream)
       if (s) cudaStreamDestroy(s);
     for (void* w : l.gemm_ws)
       if (w) cudaFree(w);
-    if (l.arena) cudaFree(l.arena);
+    if (l.arena && !(i < lane_mapped_.size() && lane_mapped_[i])) cudaFree(l.arena);
   }
+  for (void* p : ipc_mapped_) cudaIpcCloseMemHandle(p);
+  if (flags_) cudaFree(flags_);
+  if (peer_err_) cudaFreeHost(peer_err_);
   for (auto& r : irt_) {
     if (r.done) cudaEventDestroy(r.done);
     if (r.scratch) cudaFree(r.scratch);
@@ -382,6 +414,141 @@ void Executor::launch_xfer(const Instr& in, cudaStream_t s) {
     }
   }
   nccl_check(api.group_end(), "ncclGroupEnd");
+}
+
+// ---- peer-memory rank mode -----------------------------------------------
+
+std::vector<unsigned char> Executor::peer_export() const {
+  if (!peer_) throw UsageError("peer_export: executor was not opened in peer-memory rank mode");
+  std::vector<unsigned char> blob(static_cast<std::size_t>(peer_blob_bytes(prog_.num_lanes)), 0);
+  const std::uint32_t hdr[5] = {0x50423250u /* "PB2P" */, 1u, static_cast<std::uint32_t>(rc_.rank),
+                                static_cast<std::uint32_t>(rc_.world), static_cast<std::uint32_t>(prog_.num_lanes)};
+  std::memcpy(blob.data(), hdr, sizeof(hdr));
+  const std::size_t hs = sizeof(cudaIpcMemHandle_t);
+  DeviceGuard dg(rc_.local_gpu);
+  for (int l = 0; l < prog_.num_lanes; ++l) {
+    if (!owned_[l]) continue;
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, lanes_[l].arena), "cudaIpcGetMemHandle(arena)");
+    std::memcpy(blob.data() + kPeerBlobHeader + hs * l, &h, hs);
+  }
+  cudaIpcMemHandle_t h;
+  ck(cudaIpcGetMemHandle(&h, flags_), "cudaIpcGetMemHandle(flags)");
+  std::memcpy(blob.data() + kPeerBlobHeader + hs * prog_.num_lanes, &h, hs);
+  return blob;
+}
+
+void Executor::peer_import(const unsigned char* blobs, std::int64_t blob_bytes) {
+  if (!peer_) throw UsageError("peer_import: executor was not opened in peer-memory rank mode");
+  if (peer_ready_) throw UsageError("peer_import: peers already mapped");
+  if (blob_bytes != peer_blob_bytes(prog_.num_lanes)) throw UsageError("peer_import: blob size mismatch");
+  const std::size_t hs = sizeof(cudaIpcMemHandle_t);
+  DeviceGuard dg(rc_.local_gpu);
+  peer_flags_.assign(rc_.world, nullptr);
+  peer_flags_[rc_.rank] = flags_;
+  for (int r = 0; r < rc_.world; ++r) {
+    const unsigned char* b = blobs + blob_bytes * r;
+    std::uint32_t hdr[5];
+    std::memcpy(hdr, b, sizeof(hdr));
+    if (hdr[0] != 0x50423250u || hdr[1] != 1u || hdr[2] != static_cast<std::uint32_t>(r) ||
+        hdr[3] != static_cast<std::uint32_t>(rc_.world) || hdr[4] != static_cast<std::uint32_t>(prog_.num_lanes)) {
+      throw UsageError("peer_import: blob " + std::to_string(r) + " is not rank " + std::to_string(r) +
+                       "'s export of this plan");
+    }
+    if (r == rc_.rank) continue;
+    for (int l = 0; l < prog_.num_lanes; ++l) {
+      if (rc_.lane_rank[l] != r) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, b + kPeerBlobHeader + hs * l, hs);
+      void* p = nullptr;
+      ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(arena)");
+      ipc_mapped_.push_back(p);
+      lanes_[l].arena = static_cast<char*>(p);
+      lane_mapped_[l] = true;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, b + kPeerBlobHeader + hs * prog_.num_lanes, hs);
+    void* p = nullptr;
+    ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(flags)");
+    ipc_mapped_.push_back(p);
+    peer_flags_[r] = static_cast<unsigned*>(p);
+  }
+  peer_ready_ = true;
+  build_box_tables();
+  for (const auto& in : prog_.instrs)
+    if (in.kind == InstrKind::box && exec_lane_[in.id] >= 0) kernels_per_step_ += static_cast<int>(irt_[in.id].box.size());
+  kernels_per_step_ += 1 + (rc_.world > 1 ? 1 : 0);  // epoch + step barrier
+}
+
+void Executor::peer_check_ready() const {
+  if (peer_ && !peer_ready_) {
+    throw UsageError("peer-memory rank mode: exchange the ranks' peer_export blobs with peer_import first");
+  }
+}
+
+void Executor::peer_flags(const std::vector<unsigned*>& sig, const std::vector<const unsigned*>& wait, unsigned code,
+                          cudaStream_t s) {
+  std::size_t is = 0, iw = 0;
+  while (is < sig.size() || iw < wait.size()) {
+    PeerFlags f;
+    f.code = code;
+    while (is < sig.size() && f.n_sig < kMaxPeerFlags) f.sig[f.n_sig++] = sig[is++];
+    while (iw < wait.size() && f.n_wait < kMaxPeerFlags) f.wait[f.n_wait++] = wait[iw++];
+    launch_peer_flags(flags_, f, peer_timeout_ns_, peer_err_, s);
+  }
+}
+
+void Executor::peer_wait(int id, cudaStream_t s) {
+  if (!peer_ || psync_.waits[id].empty()) return;
+  std::vector<const unsigned*> w;
+  for (int slot : psync_.waits[id]) w.push_back(flags_ + kFlagReady + slot);
+  peer_flags({}, w, static_cast<unsigned>(id) + 1u, s);
+}
+
+void Executor::peer_signal(int id, cudaStream_t s) {
+  if (!peer_ || psync_.signals[id].empty()) return;
+  std::vector<unsigned*> sg;
+  for (const auto& [r, slot] : psync_.signals[id]) sg.push_back(peer_flags_[r] + kFlagReady + slot);
+  peer_flags(sg, {}, static_cast<unsigned>(id) + 1u, s);
+}
+
+void Executor::peer_step_begin(cudaStream_t s) {
+  if (peer_) launch_peer_epoch(flags_, s);
+}
+
+// Step-end barrier: no rank starts the next step (and rewrites a buffer)
+// before every rank has finished reading this step's pieces.
+void Executor::peer_step_end(cudaStream_t s) {
+  if (!peer_ || rc_.world == 1) return;
+  std::vector<unsigned*> sg;
+  std::vector<const unsigned*> w;
+  for (int r = 0; r < rc_.world; ++r) {
+    if (r == rc_.rank) continue;
+    sg.push_back(peer_flags_[r] + kFlagBarrier + rc_.rank);
+    w.push_back(flags_ + kFlagBarrier + r);
+  }
+  peer_flags(sg, w, ~0u, s);
+}
+
+// Synchronises every device this process drives; a peer wait that timed out
+// is reported as such instead of as a bare launch failure.
+void Executor::sync_all(const char* what) {
+  for (int g : gpus_) {
+    DeviceGuard dg(g);
+    check_sync(cudaDeviceSynchronize(), what);
+  }
+}
+
+void Executor::check_sync(cudaError_t e, const char* what) const {
+  if (e == cudaSuccess) return;
+  if (peer_err_ && *peer_err_) {
+    const unsigned c = *peer_err_;
+    throw InternalError(std::string("peer-memory rank mode: rank ") + std::to_string(rc_.rank) +
+                        (c == ~0u ? " timed out in the step barrier"
+                                  : " timed out waiting for the producers of instruction " + std::to_string(c - 1)) +
+                        " (" + cudaGetErrorString(e) + ")");
+  }
+  ck(e, what);
 }
 
 void Executor::build_box_tables() {
@@ -606,6 +773,7 @@ void Executor::issue_step(bool, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>
     cur = g;
   };
   set_dev(lanes_[first_lane_].gpu);
+  peer_step_begin(origin_);
   ck(cudaEventRecord(ev_begin_, origin_), "record begin");
   for (int l = 0; l < prog_.num_lanes; ++l)
     if (owned_[l])
@@ -623,16 +791,24 @@ void Executor::issue_step(bool, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>
       if (exec_lane_[d] != el || exec_stream_[d] != exec_stream_[id])
         ck(cudaStreamWaitEvent(s, irt_[d].done, 0), "wait dep");
     }
+    peer_wait(id, s);
     launch_instr(in, s);
+    peer_signal(id, s);
     if (irt_[id].done) ck(cudaEventRecord(irt_[id].done, s), "record done");
   }
+  join_lanes();
+  peer_step_end(origin_);
+}
+
+// The origin stream waits for every lane stream (ends on the origin's device).
+void Executor::join_lanes() {
   for (int l = 0; l < prog_.num_lanes; ++l) {
     if (!owned_[l]) continue;
-    set_dev(lanes_[l].gpu);
+    if (gpus_.size() > 1) ck(cudaSetDevice(lanes_[l].gpu), "cudaSetDevice");
     for (int k = 0; k < kLaneStreams; ++k)
       ck(cudaEventRecord(lane_join_[kLaneStreams * l + k], lanes_[l].stream[k]), "record join");
   }
-  set_dev(lanes_[first_lane_].gpu);
+  ck(cudaSetDevice(lanes_[first_lane_].gpu), "cudaSetDevice");
   for (auto e : lane_join_)
     if (e) ck(cudaStreamWaitEvent(origin_, e, 0), "wait join");
 }
@@ -667,6 +843,7 @@ void Executor::ensure_graph() {
 }
 
 double Executor::run(int iters) {
+  peer_check_ready();
   place_inputs();
   ensure_graph();
   DeviceGuard dg(lanes_[first_lane_].gpu);
@@ -676,7 +853,7 @@ double Executor::run(int iters) {
   };
   if (iters <= 0) {
     step();
-    ck(cudaStreamSynchronize(origin_), "step");
+    check_sync(cudaStreamSynchronize(origin_), "step");
     return 0;
   }
   cudaEvent_t t0, t1;
@@ -685,7 +862,7 @@ double Executor::run(int iters) {
   ck(cudaEventRecord(t0, origin_), "record");
   for (int i = 0; i < iters; ++i) step();
   ck(cudaEventRecord(t1, origin_), "record");
-  ck(cudaEventSynchronize(t1), "sync");
+  check_sync(cudaEventSynchronize(t1), "sync");
   float ms = 0;
   ck(cudaEventElapsedTime(&ms, t0, t1), "elapsed");
   cudaEventDestroy(t0);
@@ -694,6 +871,7 @@ double Executor::run(int iters) {
 }
 
 double Executor::run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_bytes) {
+  peer_check_ready();
   place_inputs();
   ensure_graph();
   DeviceGuard dg(lanes_[first_lane_].gpu);
@@ -808,14 +986,14 @@ double Executor::run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_b
     cudaEventDestroy(done);
   };
   run_steps(2, nullptr);
-  ck(cudaStreamSynchronize(origin_), "warmup");
+  check_sync(cudaStreamSynchronize(origin_), "warmup");
   cudaEvent_t t0, t1;
   ck(cudaEventCreate(&t0), "event");
   ck(cudaEventCreate(&t1), "event");
   ck(cudaEventRecord(t0, origin_), "record");
   run_steps(std::max(iters, 1), t0);
   ck(cudaEventRecord(t1, origin_), "record");
-  ck(cudaEventSynchronize(t1), "sync");
+  check_sync(cudaEventSynchronize(t1), "sync");
   float ms = 0;
   ck(cudaEventElapsedTime(&ms, t0, t1), "elapsed");
   cudaEventDestroy(t0);
@@ -824,17 +1002,16 @@ double Executor::run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_b
 }
 
 std::string Executor::timeline_json() {
+  peer_check_ready();
   place_inputs();
   DeviceGuard dg(lanes_[first_lane_].gpu);
-  for (int g : gpus_) {
-    cudaSetDevice(g);
-    ck(cudaDeviceSynchronize(), "timeline sync");
-  }
+  sync_all("timeline sync");
   cudaSetDevice(lanes_[first_lane_].gpu);
   const std::size_t n = prog_.instrs.size();
   std::vector<cudaEvent_t> ev0(n, nullptr), ev1(n, nullptr);
   cudaEvent_t base;
   ck(cudaEventCreate(&base), "event");
+  peer_step_begin(origin_);
   ck(cudaEventRecord(base, origin_), "record base");
   for (int l = 0; l < prog_.num_lanes; ++l)
     if (owned_[l])
@@ -852,15 +1029,18 @@ std::string Executor::timeline_json() {
     }
     ck(cudaEventCreate(&ev0[id]), "event");
     ck(cudaEventCreate(&ev1[id]), "event");
+    peer_wait(id, s);
     ck(cudaEventRecord(ev0[id], s), "record");
     launch_instr(in, s);
     ck(cudaEventRecord(ev1[id], s), "record");
+    peer_signal(id, s);
     if (irt_[id].done) ck(cudaEventRecord(irt_[id].done, s), "record done");
   }
-  for (int g : gpus_) {
-    cudaSetDevice(g);
-    ck(cudaDeviceSynchronize(), "timeline sync");
+  if (peer_) {
+    join_lanes();
+    peer_step_end(origin_);
   }
+  sync_all("timeline sync");
   auto task_kind = [&](const Instr& in) -> const char* {
     if (in.kind == InstrKind::xfer) return "collective";
     const OpNode& op = plan_.ops[in.op];
@@ -895,7 +1075,13 @@ std::string Executor::timeline_json() {
 }
 
 std::vector<KernelStat> Executor::profile() {
+  peer_check_ready();
   place_inputs();
+  {
+    DeviceGuard dg(lanes_[first_lane_].gpu);
+    peer_step_begin(origin_);
+    sync_all("profile sync");
+  }
   std::map<std::string, KernelStat> acc;
   std::vector<std::string> order;
   for (int id : prog_.issue_order) {
@@ -904,18 +1090,17 @@ std::vector<KernelStat> Executor::profile() {
     if (in.kind == InstrKind::nop || el < 0) continue;
     DeviceGuard dg(lanes_[el].gpu);
     cudaStream_t s = lanes_[el].stream[0];
-    for (int g : gpus_) {
-      cudaSetDevice(g);
-      ck(cudaDeviceSynchronize(), "profile sync");
-    }
+    sync_all("profile sync");
     cudaSetDevice(lanes_[el].gpu);
     cudaEvent_t a, b;
     ck(cudaEventCreate(&a), "event");
     ck(cudaEventCreate(&b), "event");
+    peer_wait(id, s);
     ck(cudaEventRecord(a, s), "record");
     launch_instr(in, s);
     ck(cudaEventRecord(b, s), "record");
-    ck(cudaEventSynchronize(b), "sync");
+    peer_signal(id, s);
+    check_sync(cudaEventSynchronize(b), "sync");
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
     cudaEventDestroy(a);
@@ -960,6 +1145,11 @@ std::vector<KernelStat> Executor::profile() {
     st.bytes += in.bytes;
     st.wire_bytes += in.wire_bytes;
   }
+  {
+    DeviceGuard dg(lanes_[first_lane_].gpu);
+    peer_step_end(origin_);
+    sync_all("profile sync");
+  }
   std::vector<KernelStat> out;
   for (const auto& k : order) out.push_back(acc[k]);
   return out;
@@ -968,7 +1158,8 @@ std::vector<KernelStat> Executor::profile() {
 std::vector<double> Executor::read_buffer(int buffer) {
   if (buffer < 0 || buffer >= static_cast<int>(prog_.buffers.size())) throw UsageError("no such buffer");
   const BufferDesc& bd = prog_.buffers[buffer];
-  if (!owned_[bd.lane]) throw UsageError("buffer " + std::to_string(buffer) + " lives on another rank");
+  peer_check_ready();
+  if (!readable(bd.lane)) throw UsageError("buffer " + std::to_string(buffer) + " lives on another rank");
   DeviceGuard dg(lanes_[bd.lane].gpu);
   for (int g : gpus_) {
     cudaSetDevice(g);
@@ -1010,7 +1201,7 @@ HostTensor Executor::get_output(int ptensor) {
   std::map<int, std::vector<char>> raw;
   for (int b : *bufs) {
     const BufferDesc& bd = prog_.buffers[b];
-    if (!owned_[bd.lane]) {
+    if (!readable(bd.lane)) {
       throw UsageError("ptensor " + std::to_string(ptensor) + " has pieces on another rank; read buffers instead");
     }
     pieces.push_back({&bd.mask, b});

@@ -58,13 +58,34 @@ ProgramOptions program_options(bool value_split_extension, bool fuse_epilogues);
 // One-process-per-GPU mode: this process owns the lanes with
 // lane_rank[l] == rank, all on `local_gpu`; pieces owned by other ranks
 // arrive through NCCL point-to-point exchange steps (program.hpp localize).
+//
+// With `peer_memory` there is no NCCL: every rank maps the other ranks' lane
+// arenas (CUDA IPC, NVLink) and runs the global program's instructions of its
+// own lanes; box terms read other ranks' pieces in place and cross-rank
+// dependencies are device flags (program.hpp PeerSync). The arenas are
+// exchanged by the caller between construction and the first step
+// (peer_export on every rank, all-gather, peer_import).
 struct RankConfig {
   int rank = 0;
   int world = 1;
   std::vector<int> lane_rank;
   int local_gpu = 0;
   unsigned char nccl_id[128] = {0};
+  bool peer_memory = false;
 };
+
+// Flag block layout (32-bit words): [0] step epoch, [kFlagBarrier + r] step
+// barrier slot written by rank r, [kFlagReady + i] ready slot i.
+constexpr int kPeerMaxRanks = 64;
+constexpr std::size_t kFlagBarrier = 64;
+constexpr std::size_t kFlagReady = kFlagBarrier + kPeerMaxRanks;
+
+// Peer-memory export blob: header + one cudaIpcMemHandle per plan lane (zero
+// for lanes another rank owns) + the rank's flag block handle.
+constexpr std::int64_t kPeerBlobHeader = 32;
+inline std::int64_t peer_blob_bytes(int num_lanes) {
+  return kPeerBlobHeader + static_cast<std::int64_t>(sizeof(cudaIpcMemHandle_t)) * (num_lanes + 1);
+}
 
 class Executor {
  public:
@@ -98,6 +119,10 @@ class Executor {
   int kernels_per_step() const { return kernels_per_step_; }
   int gemm_tc_launches() const { return gemm_tc_per_step_; }
   bool graph_captured() const { return graph_exec_ != nullptr; }
+  // Peer-memory mode: this rank's blob, and every rank's blobs (rank order,
+  // `world` x peer_blob_bytes) to map the other ranks' arenas and flags.
+  std::vector<unsigned char> peer_export() const;
+  void peer_import(const unsigned char* blobs, std::int64_t blob_bytes);
 
  private:
   struct LaneRt {
@@ -132,7 +157,20 @@ class Executor {
   void ensure_graph();
 
   bool local(int buffer) const { return owned_[prog_.buffers[buffer].lane]; }
+  // Readable here: owned, or mapped from its rank in peer-memory mode.
+  bool readable(int lane) const { return owned_[lane] || (peer_ && peer_ready_); }
   void launch_xfer(const Instr& in, cudaStream_t s);
+  // Peer-memory mode: flag launches around one instruction / a step.
+  void peer_check_ready() const;
+  void peer_wait(int id, cudaStream_t s);
+  void peer_signal(int id, cudaStream_t s);
+  void peer_step_begin(cudaStream_t s);
+  void peer_step_end(cudaStream_t s);
+  void peer_flags(const std::vector<unsigned*>& sig, const std::vector<const unsigned*>& wait, unsigned code,
+                  cudaStream_t s);
+  void sync_all(const char* what);
+  void join_lanes();
+  void check_sync(cudaError_t e, const char* what) const;
 
   ExecutionPlan plan_;
   Program prog_;
@@ -142,7 +180,17 @@ class Executor {
   std::vector<bool> owned_;     // per lane: runs in this process
   std::vector<int> exec_lane_;  // per instruction: lane whose streams run it here (-1: elsewhere)
   std::vector<int> exec_stream_;  // per instruction: stream index within its lane
-  void* comm_ = nullptr;        // ncclComm_t in rank mode
+  void* comm_ = nullptr;        // ncclComm_t in rank mode (NCCL exchange steps)
+  // Peer-memory rank mode.
+  bool peer_ = false;
+  bool peer_ready_ = false;               // other ranks' arenas / flags mapped
+  PeerSync psync_;
+  unsigned* flags_ = nullptr;             // this rank's flag block (epoch, barrier, ready slots)
+  std::vector<unsigned*> peer_flags_;     // per rank: its flag block as mapped here
+  std::vector<void*> ipc_mapped_;         // cudaIpcOpenMemHandle results (closed, not freed)
+  std::vector<bool> lane_mapped_;         // lane arena is an IPC mapping
+  unsigned* peer_err_ = nullptr;          // host-mapped timeout report
+  unsigned long long peer_timeout_ns_ = 0;
   int first_lane_ = 0;          // first lane this process runs (origin stream's device)
   std::vector<LaneRt> lanes_;
   std::vector<InstrRt> irt_;

@@ -89,7 +89,7 @@ def run_program(desc: dict, plan: dict, inputs: dict, owned_lanes=None, exchange
             data[ins["out"][0]] = out.reshape(-1)
         elif k == "box":
             ob = ins["out"][0]
-            out = np.zeros_like(data[ob])
+            out = data[ob].copy()  # a box writes only its cells (two-phase all-reduce: two boxes per output)
             for c in ins["cells"]:
                 di = _strided_view(out, c["dst_off"], c["dst_str"], c["ext"])
                 v = np.zeros(di.shape)

@@ -51,11 +51,27 @@ def test_lowering_invariants(name):
     writers = {}
     for ins in desc["instrs"]:
         for b in ins["out"]:
-            assert b not in writers, "every buffer is written exactly once per step"
-            writers[b] = ins["id"]
+            writers.setdefault(b, []).append(ins["id"])
         for d in ins["deps"]:
             assert d < ins["id"], "dependencies point backwards in issue order"
     assert desc["issue_order"] == sorted(desc["issue_order"])
+    # Every buffer element is written exactly once per step: a buffer with
+    # several writers (two-phase all-reduce) is covered by disjoint box cells,
+    # and its last writer depends on the others.
+    nel = {b["id"]: b["bytes"] // (2 if b["dtype"] == "bf16" else 4) for b in desc["buffers"]}
+    for b, ws in writers.items():
+        if len(ws) == 1:
+            continue
+        hit = np.zeros(nel[b], dtype=np.int64)
+        for w in ws:
+            ins = desc["instrs"][w]
+            assert ins["kind"] == "box" and ins["out"] == [b]
+            for c in ins["cells"]:
+                idx = c["dst_off"] + sum(np.arange(e).reshape([-1 if i == d else 1 for i in range(len(c["ext"]))]) * st
+                                         for d, (e, st) in enumerate(zip(c["ext"], c["dst_str"])))
+                np.add.at(hit, np.asarray(idx).reshape(-1), 1)
+        assert (hit == 1).all(), f"buffer {b}: box writers overlap or leave gaps"
+        assert set(ws[:-1]) <= set(desc["instrs"][ws[-1]]["deps"])
     for b in desc["buffers"]:
         assert b["offset"] % 256 == 0
         if not b["graph_input"]:
@@ -69,6 +85,59 @@ def test_lowering_invariants(name):
             for t in c["terms"]:
                 thi = t["off"] + sum((e - 1) * s for e, s in zip(c["ext"], t["str"]))
                 assert 0 <= t["off"] and thi < size[t["buf"]]
+
+
+def test_allreduce_runs_as_reduce_scatter_then_all_gather():
+    g = golden_cases.load("adapt_v_to_r4")
+    desc = pb.describe(g["plan"])
+    rs = [i for i in desc["instrs"] if i["label"].endswith("#rs")]
+    ag = [i for i in desc["instrs"] if i["label"].endswith("#ag")]
+    assert len(rs) == 4 and len(ag) == 4
+    for j, (r, a) in enumerate(zip(rs, ag)):
+        assert r["lane"] == a["lane"] and r["out"] == a["out"]
+        # phase 1: one slice, all four partials added in the same order
+        assert len(r["cells"]) == 1 and len(r["cells"][0]["terms"]) == 4
+        assert all(t["add"] for t in r["cells"][0]["terms"])
+        # phase 2: the three other members' reduced slices, copied
+        assert len(a["cells"]) == 3 and all(len(c["terms"]) == 1 and not c["terms"][0]["add"] for c in a["cells"])
+        assert {t["buf"] for c in a["cells"] for t in c["terms"]} == {x["out"][0] for x in rs if x is not r}
+        assert {x["id"] for x in rs} <= set(a["deps"])
+        assert r["wire_bytes"] + a["wire_bytes"] > 0
+    # the NCCL exchange lowering keeps one whole-buffer ncclAllReduce instead
+    nccl = pb.describe(g["plan"], lane_rank=[0, 1, 2, 3])
+    assert any(i["kind"] == "xfer" and i["allreduce"] for i in nccl["instrs"])
+
+
+@pytest.mark.parametrize("name", ["adapt_v_to_r4", "mlp_dp2", "gpt_block_tp2", "mlp_1f1b_dp2", "three_pass_3f1b"])
+def test_peer_sync_schedule(name):
+    # Peer-memory rank mode: every cross-rank dependency edge is one flag
+    # slot on the consumer's rank, signalled once by the producer.
+    g = golden_cases.load(name)
+    plan = json.loads(g["plan"])
+    nl = len(plan["lanes"])
+    for world in (2, nl):
+        lane_rank = pb.lanes_round_robin(nl, world)
+        desc = pb.describe(g["plan"], lane_rank=lane_rank, flags=pb.PEER_MEMORY)
+        ps = desc["peer_sync"]
+        assert not any(i["kind"] == "xfer" for i in desc["instrs"])
+        rank_of = lambda i: lane_rank[desc["instrs"][i]["lane"]]  # noqa: E731
+        expect_waits = 0
+        seen = {}
+        for ins in desc["instrs"]:
+            cross = [d for d in ins["deps"] if desc["instrs"][d]["kind"] != "nop" and rank_of(d) != rank_of(ins["id"])]
+            if ins["kind"] == "nop":
+                cross = []
+            assert len(ps["waits"][ins["id"]]) == len(cross)
+            expect_waits += len(cross)
+            for d, slot in zip(cross, ps["waits"][ins["id"]]):
+                key = (d, rank_of(ins["id"]))
+                assert seen.setdefault(key, slot) == slot
+                assert [rank_of(ins["id"]), slot] in ps["signals"][d]
+        for r in range(world):
+            used = sorted({s for (d, rr), s in seen.items() if rr == r})
+            assert used == list(range(ps["slots"][r]))
+        if nl > 1 and world > 1:
+            assert expect_waits > 0
 
 
 def test_collectives_become_single_fused_box_per_member():
