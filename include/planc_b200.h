@@ -49,6 +49,9 @@ extern "C" {
                                            the separate kernel; default: every op its own kernel) */
 #define PLANC_B200_PEER_MEMORY 0x20u     /* planc_b200_open_rank / describe_rank: peer-memory transport
                                            (CUDA IPC over NVLink, device flags) instead of NCCL */
+#define PLANC_B200_NO_GROUPING 0x40u    /* every GEMM its own launch (default: independent same-shape
+                                           GEMMs of a lane that become ready together share one grouped
+                                           tensor-core launch) */
 #define PLANC_B200_SERIAL_LANES 0x8u    /* one stream per lane: a lane's tasks run strictly in plan
                                            order (default: only data dependencies and sync edges order
                                            a lane's work, spread over several streams) */

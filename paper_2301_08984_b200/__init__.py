@@ -38,6 +38,7 @@ STRICT_VALUE = 0x4
 SERIAL_LANES = 0x8
 FUSE_EPILOGUES = 0x10
 PEER_MEMORY = 0x20
+NO_GROUPING = 0x40
 
 
 class PlancError(RuntimeError):

@@ -70,6 +70,7 @@ int planc_b200_open(const char* plan_json, const int* lane_gpu, int num_lane_gpu
     opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
     if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
     opt.fuse_epilogues = (flags & PLANC_B200_FUSE_EPILOGUES) != 0;
+    opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
     std::vector<int> lanes;
     for (int i = 0; lane_gpu && i < num_lane_gpu; ++i) lanes.push_back(lane_gpu[i]);
     auto* h = new planc_b200_exec;
@@ -104,6 +105,7 @@ int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* 
     opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
     if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
     opt.fuse_epilogues = (flags & PLANC_B200_FUSE_EPILOGUES) != 0;
+    opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
     RankConfig rc;
     rc.rank = rank;
     rc.world = world;
@@ -129,6 +131,7 @@ int planc_b200_describe_rank(const char* plan_json, const int* lane_rank, int nu
     ProgramOptions po = program_options((flags & PLANC_B200_STRICT_VALUE) == 0,
                                         (flags & PLANC_B200_FUSE_EPILOGUES) != 0 &&
                                             (flags & PLANC_B200_NO_TENSOR_CORES) == 0);
+    po.group_gemms = (flags & (PLANC_B200_NO_GROUPING | PLANC_B200_NO_TENSOR_CORES)) == 0;
     ExecutionPlan plan = load_plan(plan_json);
     const std::vector<int> lr(lane_rank, lane_rank + num_lanes);
     if ((flags & PLANC_B200_PEER_MEMORY) == 0) {
@@ -362,6 +365,7 @@ int planc_b200_describe(const char* plan_json, uint32_t flags, char** json_out) 
     ProgramOptions po = program_options((flags & PLANC_B200_STRICT_VALUE) == 0,
                                         (flags & PLANC_B200_FUSE_EPILOGUES) != 0 &&
                                             (flags & PLANC_B200_NO_TENSOR_CORES) == 0);
+    po.group_gemms = (flags & (PLANC_B200_NO_GROUPING | PLANC_B200_NO_TENSOR_CORES)) == 0;
     ExecutionPlan plan = load_plan(plan_json);
     Program p = build_program(plan, po);
     *json_out = dup(p.describe_json());

@@ -68,6 +68,15 @@ struct EpiMaps {
   CUtensorMap out[1];
 };
 
+// Operand / result maps of the launch's GEMMs (one, or a group of
+// independent same-shape GEMMs sharing the tile space: tile t belongs to
+// member t / tiles_per_gemm).
+struct GroupMaps {
+  CUtensorMap a[kMaxGemmGroup];
+  CUtensorMap b[kMaxGemmGroup];
+  CUtensorMap c[kMaxGemmGroup];
+};
+
 // Stream-K tail (data-parallel waves, then the remaining tiles' k-iterations
 // split evenly over the CTAs): tiles [0, dp_tiles) go whole to CTA
 // t % gridDim.x; CTA b < sk_ctas then takes k-iterations [lo(b), lo(b+1)) of
@@ -251,8 +260,7 @@ __device__ __forceinline__ void bf16_unpair(std::uint32_t w, float& lo, float& h
 
 template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, void* __restrict__ C, int m, int n, int k,
+    gemm_tc_kernel(const __grid_constant__ GroupMaps gm, int ng, int m, int n, int k,
                    const __grid_constant__ EpiParams epi, const __grid_constant__ EpiMaps maps,
                    const __grid_constant__ SkParams sk) {
   extern __shared__ std::uint8_t smem_raw[];
@@ -276,12 +284,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int lane = threadIdx.x % 32;
   const int tiles_m = (m + BM - 1) / BM;
   const int tiles_n = (n + BN - 1) / BN;
-  const int num_tiles = tiles_m * tiles_n;
+  const int per_gemm = tiles_m * tiles_n;
+  const int num_tiles = per_gemm * ng;
   const int num_k = (k + BK - 1) / BK;
+  // Tile t of the launch: member t / per_gemm, its tile t % per_gemm.
+  auto coords = [&](int t, int& p, int& mb, int& nb) {
+    p = t / per_gemm;
+    tile_coords(t - p * per_gemm, tiles_m, tiles_n, mb, nb);
+  };
 
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmB)) : "memory");
+    for (int p = 0; p < ng; ++p) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&gm.a[p])) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&gm.b[p])) : "memory");
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -307,8 +323,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int it = 0;  // global k-block counter across work items (ring position)
       for_each_work(num_k, sk, [&](int t, int kb0, int kb1) {
-        int mb, nb;
-        tile_coords(t, tiles_m, tiles_n, mb, nb);
+        int p, mb, nb;
+        coords(t, p, mb, nb);
+        const CUtensorMap* tmA = &gm.a[p];
+        const CUtensorMap* tmB = &gm.b[p];
         const int m0 = mb * BM, n0 = nb * BN;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
@@ -319,15 +337,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           std::uint8_t* b = sB + s * B_STAGE_BYTES;
           if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * (64 * BK * 2), &tmA, m0 + 64 * j, kb * BK, &full[s]);
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * (64 * BK * 2), tmA, m0 + 64 * j, kb * BK, &full[s]);
           } else {
-            tma_load_2d(a, &tmA, kb * BK, m0, &full[s]);
+            tma_load_2d(a, tmA, kb * BK, m0, &full[s]);
           }
           if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * (64 * BK * 2), &tmB, n0 + 64 * j, kb * BK, &full[s]);
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * (64 * BK * 2), tmB, n0 + 64 * j, kb * BK, &full[s]);
           } else {
-            tma_load_2d(b, &tmB, kb * BK, n0, &full[s]);
+            tma_load_2d(b, tmB, kb * BK, n0, &full[s]);
           }
         }
       });
@@ -377,7 +395,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     std::uint8_t* stg = staging + (warp - 2) * 2 * 4096;
     int sb = 0;
     int local = 0;
-    auto store_chunk = [&](const std::uint32_t(&r)[32], int mb, int nb, int c) {
+    auto store_chunk = [&](const std::uint32_t(&r)[32], int p, int mb, int nb, int c) {
       if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer sb is free
       __syncwarp();
       std::uint8_t* buf = stg + sb * 4096;
@@ -401,7 +419,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
       __syncwarp();
-      if (lane == 0) tma_store_2d(&tmC, buf, nb * BN + c * 32, mb * BM + q * 32);
+      if (lane == 0) tma_store_2d(&gm.c[p], buf, nb * BN + c * 32, mb * BM + q * 32);
       sb ^= 1;
     };
     // fp32 partial of (CTA b, slot, this quarter, chunk c): 8 float4 per
@@ -411,8 +429,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
              ((static_cast<std::int64_t>((b * 2 + slot) * 4 + q) * (BN / 32) + c) * 8) * 32 + lane;
     };
     for_each_work(num_k, sk, [&](int t, int kb0, int kb1) {
-      int mb, nb;
-      tile_coords(t, tiles_m, tiles_n, mb, nb);
+      int p, mb, nb;
+      coords(t, p, mb, nb);
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       ++local;
@@ -429,7 +447,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
           }
-          store_chunk(r, mb, nb, c);
+          store_chunk(r, p, mb, nb, c);
         }
         return;
       }
@@ -502,7 +520,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           r[4 * v + 2] = __float_as_uint(sum[v].z);
           r[4 * v + 3] = __float_as_uint(sum[v].w);
         }
-        store_chunk(r, mb, nb, c);
+        store_chunk(r, p, mb, nb, c);
       }
     });
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
@@ -581,7 +599,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
       if (lane == 0) {
         const int c0 = nb * BN + c * 32, c1 = mb * BM + q * 32;
-        tma_store_2d_nc(&tmC, buf, c0, c1);
+        tma_store_2d_nc(&gm.c[0], buf, c0, c1);
         tma_store_2d_nc(&maps.out[0], buf + 2048, c0, c1);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
@@ -689,9 +707,19 @@ void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
   }
   // A: [m][k] (K-major) or, transposed, [k][m] (MN-major); B: [k][n]
   // (MN-major) or, transposed, [n][k] (K-major).
-  CUtensorMap ma = A_MN ? make_map(a.A, a.k, a.m, BK) : make_map(a.A, a.m, a.k, BM);
-  CUtensorMap mb = B_MN ? make_map(a.B, a.k, a.n, BK) : make_map(a.B, a.n, a.k, BN);
-  CUtensorMap mc = make_store_map(a.C, a.m, a.n, C_BF16);
+  const int ng = a.group > 1 ? a.group : 1;
+  if (ng > kMaxGemmGroup) throw std::runtime_error("gemm_tc: group above kMaxGemmGroup");
+  if (FUSE && ng > 1) throw std::runtime_error("gemm_tc: fused epilogue on a grouped launch");
+  GroupMaps gm;
+  std::memset(&gm, 0, sizeof(gm));
+  for (int i = 0; i < ng; ++i) {
+    const void* A = ng > 1 ? a.gA[i] : a.A;
+    const void* B = ng > 1 ? a.gB[i] : a.B;
+    void* C = ng > 1 ? a.gC[i] : a.C;
+    gm.a[i] = A_MN ? make_map(A, a.k, a.m, BK) : make_map(A, a.m, a.k, BM);
+    gm.b[i] = B_MN ? make_map(B, a.k, a.n, BK) : make_map(B, a.n, a.k, BN);
+    gm.c[i] = make_store_map(C, a.m, a.n, C_BF16);
+  }
   EpiMaps maps;
   std::memset(&maps, 0, sizeof(maps));
   if constexpr (FUSE) maps.out[0] = make_store_map(a.epi.ops[0].out, a.m, a.n, true);
@@ -704,7 +732,7 @@ void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
     sk.counters = reinterpret_cast<int*>(ws);
     sk.partials = reinterpret_cast<float*>(ws + sc.counter_bytes);
   }
-  kern<<<sc.grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, mc, a.C, static_cast<int>(a.m), static_cast<int>(a.n),
+  kern<<<sc.grid, NUM_THREADS, SMEM_BYTES, s>>>(gm, ng, static_cast<int>(a.m), static_cast<int>(a.n),
                                                 static_cast<int>(a.k), a.epi, maps, sk);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc_kernel: ") + cudaGetErrorString(e));
@@ -724,10 +752,10 @@ constexpr double kSkWriteChunkUs = 0.15;
 constexpr int kMinSkIters = 4;  // k-blocks per stream-K range, at least
 
 GemmSchedule schedule_for(std::int64_t m, std::int64_t n, std::int64_t k, int bn, bool allow_sk, int sms,
-                          bool force_sk = false) {
+                          bool force_sk = false, int group = 1) {
   GemmSchedule sc;
   sc.bn = bn;
-  sc.tiles = ((m + BM - 1) / BM) * ((n + bn - 1) / bn);
+  sc.tiles = ((m + BM - 1) / BM) * ((n + bn - 1) / bn) * std::max(group, 1);
   sc.num_k = (k + BK - 1) / BK;
   const std::int64_t waves = (sc.tiles + sms - 1) / sms;
   sc.grid = static_cast<int>(std::min<std::int64_t>(sc.tiles, sms));
@@ -778,8 +806,8 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   bool have = false;
   for (int bn : {256, 128, 64}) {
     if (forced && bn != forced) continue;
-    GemmSchedule dp = schedule_for(a.m, a.n, a.k, bn, false, sms);
-    GemmSchedule sk = schedule_for(a.m, a.n, a.k, bn, allow_sk, sms, skmode == 2);
+    GemmSchedule dp = schedule_for(a.m, a.n, a.k, bn, false, sms, false, a.group);
+    GemmSchedule sk = schedule_for(a.m, a.n, a.k, bn, allow_sk, sms, skmode == 2, a.group);
     GemmSchedule c = (sk.sk_ctas > 0 && (skmode == 2 || sk.model_us < 0.9 * dp.model_us)) ? sk : dp;
     if (!have || c.model_us < best.model_us * 0.97) {
       best = c;
@@ -813,7 +841,7 @@ void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
   const bool a_mn = a.ta, b_mn = !a.tb, cb = a.dc == DT_BF16;
   GemmSchedule sc = gemm_sm100_schedule(a, device_sms());
   if (sc.sk_ctas > 0 && (a.ws == nullptr || a.ws_bytes < sc.ws_bytes)) {
-    sc = schedule_for(a.m, a.n, a.k, sc.bn, false, device_sms());  // no workspace: data-parallel
+    sc = schedule_for(a.m, a.n, a.k, sc.bn, false, device_sms(), false, a.group);  // no workspace: data-parallel
   }
   const int bn = sc.bn;
   if (a.epi.n_ops > 0) {

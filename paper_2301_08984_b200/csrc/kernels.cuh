@@ -73,10 +73,19 @@ struct EpiParams {
 };
 constexpr int kMaxEpiSlots = 2;
 
+// Grouped launch: up to kMaxGemmGroup independent GEMMs of one shape share
+// one persistent launch (one tile space, no per-GEMM wave tail).
+constexpr int kMaxGemmGroup = 8;
+
 struct GemmArgs {
   const void* A;
   const void* B;
   void* C;
+  // group > 1: members 0..group-1 are (gA[i], gB[i], gC[i]); A/B/C unused.
+  int group = 1;
+  const void* gA[kMaxGemmGroup] = {};
+  const void* gB[kMaxGemmGroup] = {};
+  void* gC[kMaxGemmGroup] = {};
   std::int64_t m, n, k;
   bool ta, tb;
   int da, db, dc;
@@ -153,12 +162,25 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms);
 std::int64_t gemm_sm100_workspace_bytes(const GemmArgs& a);  // on the current device
 void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s);
 
-// Dispatch: tcgen05 path when eligible, SIMT tile kernel otherwise.
+// Dispatch: tcgen05 path when eligible, SIMT tile kernel otherwise (a
+// group then runs member by member).
 inline void launch_gemm(const GemmArgs& a, cudaStream_t s, bool allow_tc, bool* used_tc) {
   bool tc = allow_tc && gemm_sm100_eligible(a);
   if (used_tc) *used_tc = tc;
-  if (tc) launch_gemm_sm100(a, s);
-  else launch_gemm_simt(a, s);
+  if (tc) {
+    launch_gemm_sm100(a, s);
+  } else if (a.group > 1) {
+    for (int i = 0; i < a.group; ++i) {
+      GemmArgs one = a;
+      one.group = 1;
+      one.A = a.gA[i];
+      one.B = a.gB[i];
+      one.C = a.gC[i];
+      launch_gemm_simt(one, s);
+    }
+  } else {
+    launch_gemm_simt(a, s);
+  }
 }
 
 }  // namespace planc_b200

@@ -719,7 +719,112 @@ Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt) {
   b.run();
   if (opt.two_phase_allreduce) two_phase_allreduce(b.P);
   if (opt.fuse_epilogues) fuse_gemm_epilogues(b.P, opt);
+  if (opt.group_gemms && opt.gemm_groupable) group_gemms(b.P, opt);
   return std::move(b.P);
+}
+
+void group_gemms(Program& P, const ProgramOptions& opt) {
+  const int n = static_cast<int>(P.instrs.size());
+  std::vector<int> redirect(n, -1);  // grouped member -> its group's instruction
+  auto red = [&](int d) { return redirect[d] >= 0 ? redirect[d] : d; };
+  auto deps_of = [&](int x) {
+    std::set<int> d;
+    for (int y : P.instrs[x].deps) d.insert(red(y));
+    d.erase(x);
+    return d;
+  };
+  // Transitive ancestors (through redirected edges), sorted.
+  std::vector<int> mark(n, -1);
+  int stamp = 0;
+  auto ancestors = [&](int x) {
+    std::vector<int> anc, stack{x};
+    ++stamp;
+    while (!stack.empty()) {
+      const int y = stack.back();
+      stack.pop_back();
+      for (int d0 : P.instrs[y].deps) {
+        const int d = red(d0);
+        if (d == y || mark[d] == stamp) continue;
+        mark[d] = stamp;
+        anc.push_back(d);
+        stack.push_back(d);
+      }
+    }
+    std::sort(anc.begin(), anc.end());
+    return anc;
+  };
+  auto has = [](const std::vector<int>& v, int x) { return std::binary_search(v.begin(), v.end(), x); };
+  struct Open {
+    int leader;
+    std::vector<int> anc;  // ancestors of the group (all members'), sorted
+    std::set<int> deps;    // direct dependencies of the group
+  };
+  std::map<std::tuple<int, std::int64_t, std::int64_t, std::int64_t, bool, bool, int, int, int>, std::vector<Open>>
+      open;
+  constexpr std::size_t kWindow = 256;  // issue-order distance a group may span
+  std::vector<int> pos(n, 0);
+  for (std::size_t i = 0; i < P.issue_order.size(); ++i) pos[P.issue_order[i]] = static_cast<int>(i);
+  for (int id : P.issue_order) {
+    Instr& g = P.instrs[id];
+    if (g.kind != InstrKind::gemm || !g.fused.empty() || g.group != 1) continue;
+    const DType da = P.buffers[g.in_bufs[0]].dtype, db = P.buffers[g.in_bufs[1]].dtype,
+                dc = P.buffers[g.out_bufs[0]].dtype;
+    if (!opt.gemm_groupable(g, da, db, dc)) continue;
+    auto key = std::make_tuple(g.lane, g.m, g.n, g.k, g.ta, g.tb, static_cast<int>(da), static_cast<int>(db),
+                               static_cast<int>(dc));
+    const std::set<int> gd = deps_of(id);
+    auto& cands = open[key];
+    cands.erase(std::remove_if(cands.begin(), cands.end(),
+                               [&](const Open& o) {
+                                 return P.instrs[o.leader].group >= kMaxGemmGroupInstr ||
+                                        pos[id] - pos[o.leader] > static_cast<int>(kWindow);
+                               }),
+                cands.end());
+    const std::vector<int> ga = cands.empty() ? std::vector<int>{} : ancestors(id);
+    bool joined = false;
+    for (auto& o : cands) {
+      Instr& L = P.instrs[o.leader];
+      // Same readiness and independence: each side's dependencies are
+      // ancestors of the other (so neither waits longer in the group, and
+      // the group's slot in the issue order — the leader's — follows every
+      // member's producers); the newcomer depends on no member.
+      bool ok = !has(ga, o.leader);
+      for (int d : gd) ok = ok && has(o.anc, d);
+      for (int d : o.deps) ok = ok && has(ga, d);
+      if (!ok) continue;
+      L.in_bufs.push_back(g.in_bufs[0]);
+      L.in_bufs.push_back(g.in_bufs[1]);
+      L.out_bufs.push_back(g.out_bufs[0]);
+      L.group += 1;
+      L.flops += g.flops;
+      L.bytes += g.bytes;
+      L.label += "+" + g.label;
+      P.buffers[g.out_bufs[0]].producer = o.leader;
+      redirect[id] = o.leader;
+      g.kind = InstrKind::nop;
+      g.deps.clear();
+      g.in_bufs.clear();
+      g.out_bufs.clear();
+      g.flops = g.bytes = 0;
+      joined = true;
+      break;
+    }
+    if (!joined) cands.push_back(Open{id, cands.empty() ? ancestors(id) : ga, gd});
+  }
+  for (auto& in : P.instrs) {
+    bool changed = false;
+    for (int& d : in.deps) {
+      if (redirect[d] >= 0) {
+        d = redirect[d];
+        changed = true;
+      }
+    }
+    if (changed) {
+      std::sort(in.deps.begin(), in.deps.end());
+      in.deps.erase(std::unique(in.deps.begin(), in.deps.end()), in.deps.end());
+      in.deps.erase(std::remove(in.deps.begin(), in.deps.end(), in.id), in.deps.end());
+    }
+  }
 }
 
 void fuse_gemm_epilogues(Program& P, const ProgramOptions& opt) {
@@ -1223,7 +1328,7 @@ std::string Program::describe_json() const {
        << ",\"axis_len\":" << in.axis_len << ",\"inner\":" << in.inner << ",\"n_idx\":" << in.n_idx
        << ",\"rows\":" << in.rows << ",\"h\":" << in.h << ",\"lo\":" << in.lo << ",\"flops\":" << in.flops
        << ",\"bytes\":" << in.bytes << ",\"wire_bytes\":" << in.wire_bytes << ",\"coll_group\":" << in.coll_group
-       << ",\"allreduce\":" << (in.allreduce ? "true" : "false") << ",\"fused\":[";
+       << ",\"allreduce\":" << (in.allreduce ? "true" : "false") << ",\"group\":" << in.group << ",\"fused\":[";
     for (std::size_t f = 0; f < in.fused.size(); ++f) {
       const auto& fe = in.fused[f];
       os << (f ? "," : "") << "{\"ew_instr\":" << fe.ew_instr << ",\"ew\":" << static_cast<int>(fe.op)

@@ -73,6 +73,8 @@ struct Cell {
   }
 };
 
+constexpr int kMaxGemmGroupInstr = 8;  // members of one grouped GEMM launch (kernels.cuh kMaxGemmGroup)
+
 enum class InstrKind { gemm, ew, reduce, emb_lookup, emb_grad, box, xfer, nop };
 
 // One cross-rank piece movement of an exchange step (one-process-per-GPU
@@ -98,8 +100,10 @@ struct Instr {
   std::vector<int> in_bufs;
   std::vector<int> out_bufs;
   std::vector<int> deps;  // producer instructions (all, incl. same stream)
-  // gemm: C[m,n] = op(A)·op(B)
+  // gemm: C[m,n] = op(A)·op(B); a grouped GEMM (group > 1) computes
+  // out_bufs[i] = op(in_bufs[2i])·op(in_bufs[2i+1]) for i < group.
   std::int64_t m = 0, n = 0, k = 0;
+  int group = 1;
   bool ta = false, tb = false;
   // ew
   EwOp ew = EwOp::add;
@@ -149,6 +153,12 @@ struct ProgramOptions {
   // member reads ~2n instead of k*n (over NVLink when members sit on other
   // GPUs or ranks).
   bool two_phase_allreduce = true;
+  // Independent GEMMs of one shape on one lane that become ready together
+  // (each one's dependencies are ancestors of the other's) run as one
+  // grouped tensor-core launch (one tile space: no per-GEMM wave tail, one
+  // launch instead of several) — for GEMMs the predicate accepts.
+  bool group_gemms = true;
+  bool (*gemm_groupable)(const Instr& gemm, DType a, DType b, DType c) = nullptr;
   bool (*gemm_fusable)(const Instr& gemm, DType a, DType b, DType c) = nullptr;
 };
 
@@ -180,6 +190,11 @@ Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt = {})
 // other operands are ready before that GEMM, is computed in the GEMM's
 // epilogue; the op's instruction becomes a nop.
 void fuse_gemm_epilogues(Program& p, const ProgramOptions& opt);
+
+// GEMM grouping pass (run by build_program after fusion when
+// opt.group_gemms): members become nops, the first member of each group
+// carries every member's operands and results.
+void group_gemms(Program& p, const ProgramOptions& opt);
 
 // The two-phase all-reduce pass (ProgramOptions::two_phase_allreduce), run
 // by build_program before epilogue fusion. Rebuilds the program in issue

@@ -101,6 +101,19 @@ bool tc_fusable(const Instr& g, DType a, DType b, DType c) {
   x.dc = dt_of(c);
   return c == DType::bf16 && gemm_sm100_eligible(x);
 }
+bool tc_groupable(const Instr& g, DType a, DType b, DType c) {
+  static_assert(kMaxGemmGroupInstr == kMaxGemmGroup, "group size limits differ");
+  GemmArgs x{};
+  x.m = g.m;
+  x.n = g.n;
+  x.k = g.k;
+  x.ta = g.ta;
+  x.tb = g.tb;
+  x.da = dt_of(a);
+  x.db = dt_of(b);
+  x.dc = dt_of(c);
+  return gemm_sm100_eligible(x);
+}
 }  // namespace
 
 ProgramOptions program_options(bool value_split_extension, bool fuse_epilogues) {
@@ -108,6 +121,7 @@ ProgramOptions program_options(bool value_split_extension, bool fuse_epilogues) 
   po.value_split_extension = value_split_extension;
   po.fuse_epilogues = fuse_epilogues;
   po.gemm_fusable = &tc_fusable;
+  po.gemm_groupable = &tc_groupable;
   return po;
 }
 
@@ -116,6 +130,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
     : opt_(opt) {
   plan_ = load_plan(plan_json);
   ProgramOptions po = program_options(opt.value_split_extension, opt.fuse_epilogues && opt.allow_tensor_cores);
+  po.group_gemms = opt.group_gemms && opt.allow_tensor_cores;
   // NCCL exchange steps lower whole-buffer all-reduce groups to
   // ncclAllReduce; every other mode runs them as two box phases.
   po.two_phase_allreduce = !(rank && !rank->peer_memory);
@@ -310,6 +325,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       a.da = dt_of(prog_.buffers[in.in_bufs[0]].dtype);
       a.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
       a.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
+      a.group = in.group;
       a.allow_streamk = gemm_streamk_ok(exec_lane_[in.id]);
       if (opt_.allow_tensor_cores && gemm_sm100_eligible(a)) {
         ++gemm_tc_per_step_;
@@ -696,6 +712,18 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
       a.da = dt_of(prog_.buffers[in.in_bufs[0]].dtype);
       a.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
       a.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
+      a.group = in.group;
+      if (in.group > 1) {
+        if (in.group > kMaxGemmGroup || static_cast<int>(in.in_bufs.size()) != 2 * in.group ||
+            static_cast<int>(in.out_bufs.size()) != in.group || !in.fused.empty()) {
+          throw InternalError("malformed grouped GEMM instruction");
+        }
+        for (int i = 0; i < in.group; ++i) {
+          a.gA[i] = buf_ptr(in.in_bufs[2 * i]);
+          a.gB[i] = buf_ptr(in.in_bufs[2 * i + 1]);
+          a.gC[i] = buf_ptr(in.out_bufs[i]);
+        }
+      }
       a.epi.n_ops = static_cast<int>(in.fused.size());
       for (std::size_t f = 0; f < in.fused.size(); ++f) {
         const auto& fe = in.fused[f];

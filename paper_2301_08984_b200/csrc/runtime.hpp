@@ -49,6 +49,7 @@ struct ExecOptions {
   bool value_split_extension = true;
   int streams_per_lane = kLaneStreams;  // 1 = issue a lane strictly in plan order
   bool fuse_epilogues = false;          // elementwise consumers computed in GEMM epilogues
+  bool group_gemms = true;              // same-shape independent GEMMs in one grouped launch
 };
 
 // ProgramOptions as the executor uses them: epilogue fusion only for GEMMs

@@ -60,3 +60,24 @@ def matmul_add_plan(m, n, k, ta=False, tb=False):
     doc["feeds"].append([201, 200])
     doc["lanes"][0]["tasks"].append({"kind": "compute", "op": "add", "duration": 0.0, "bytes": 0})
     return json.dumps(doc), 4
+
+
+def grouped_matmul_plan(g, m, n, k, ta=False, tb=False, out_elem=2):
+    """g independent matmuls of one shape on one lane: C_i = op(A_i)·op(B_i)
+    (pTensors A_i = 3i, B_i = 3i+1, C_i = 3i+2) — one grouped GEMM launch."""
+    doc = json.loads(matmul_plan(m, n, k, ta, tb, 2, out_elem)[0])
+    base = {"pt": doc["ptensors"], "vt": doc["vtensors"], "op": doc["ops"][0]}
+    doc["ptensors"], doc["vtensors"], doc["ops"], doc["lanes"][0]["tasks"] = [], [], [], []
+    doc["assignment"] = {}
+    for i in range(g):
+        for j, pt in enumerate(base["pt"]):
+            doc["ptensors"].append(dict(pt, id=3 * i + j))
+        for vt in base["vt"]:
+            v = dict(vt, id=vt["id"] + 1000 * i, ptensor=3 * i + vt["ptensor"], owner=f"op{i}")
+            doc["vtensors"].append(v)
+        op = dict(base["op"], id=f"op{i}", inputs=[x + 1000 * i for x in base["op"]["inputs"]],
+                  outputs=[x + 1000 * i for x in base["op"]["outputs"]], doc_order=i)
+        doc["ops"].append(op)
+        doc["assignment"][f"op{i}"] = 0
+        doc["lanes"][0]["tasks"].append({"kind": "compute", "op": f"op{i}", "duration": 0.0, "bytes": 0})
+    return json.dumps(doc)

@@ -54,11 +54,12 @@ def run_program(desc: dict, plan: dict, inputs: dict, owned_lanes=None, exchange
         if not lane_ok(ins["lane"]):
             continue
         if k == "gemm":
-            a = data[ins["in"][0]].reshape(shape[ins["in"][0]])
-            b = data[ins["in"][1]].reshape(shape[ins["in"][1]])
-            a = a.T if ins["ta"] else a
-            b = b.T if ins["tb"] else b
-            data[ins["out"][0]] = (a @ b).reshape(-1)
+            for g in range(ins.get("group", 1)):  # grouped launch: member g = (in[2g], in[2g+1]) -> out[g]
+                a = data[ins["in"][2 * g]].reshape(shape[ins["in"][2 * g]])
+                b = data[ins["in"][2 * g + 1]].reshape(shape[ins["in"][2 * g + 1]])
+                a = a.T if ins["ta"] else a
+                b = b.T if ins["tb"] else b
+                data[ins["out"][g]] = (a @ b).reshape(-1)
             for f in ins.get("fused", []):  # elementwise consumers run in the GEMM epilogue
                 out = data[f["in"][0]].copy()
                 for x in f["in"][1:]:

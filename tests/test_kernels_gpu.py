@@ -161,3 +161,34 @@ def test_reduce_sum(shape, axis):
     x = rng.integers(-4, 5, size=shape).astype(np.float64)
     out, _ = run_single(plan, {0: x}, out_pt)
     assert np.array_equal(out.reshape(-1), x.sum(axis=axis).reshape(-1))
+
+
+@pytest.mark.parametrize("g,m,n,k,ta,tb", [(4, 16384, 512, 512, False, False), (3, 304, 520, 200, False, True),
+                                           (4, 512, 512, 16384, True, False), (8, 1024, 256, 256, False, False),
+                                           (2, 8192, 2048, 2048, False, True)])
+def test_grouped_gemm_vs_fp64(g, m, n, k, ta, tb):
+    """Independent same-shape GEMMs of a lane run as ONE grouped tcgen05
+    launch (stream-K tail included); each member equals its own product."""
+    from plan_builder import grouped_matmul_plan
+
+    plan = grouped_matmul_plan(g, m, n, k, ta, tb)
+    desc = pb.describe(plan)
+    assert [i["group"] for i in desc["instrs"] if i["kind"] == "gemm"] == [g]
+    rng = np.random.default_rng(g * 1000 + m + n + k)
+    inputs = {}
+    for i in range(g):
+        inputs[3 * i] = bf16_round(rng.standard_normal((k, m) if ta else (m, k)))
+        inputs[3 * i + 1] = bf16_round(rng.standard_normal((n, k) if tb else (k, n)))
+    outs = {}
+    for flags in (0, pb.NO_GROUPING):
+        with pb.Executor(plan, lane_gpus=[0], flags=flags) as ex:
+            ex.set_inputs(inputs)
+            ex.run(2)
+            assert ex.stats()["gemm_tc_per_step"] == (1 if flags == 0 else g)
+            outs[flags] = {i: ex.get_output(3 * i + 2) for i in range(g)}
+    for i in range(g):
+        a, b = inputs[3 * i], inputs[3 * i + 1]
+        ref = (a.T if ta else a) @ (b.T if tb else b)
+        err = np.abs(outs[0][i] - ref).max() / max(1.0, np.abs(ref).max())
+        assert err < 2.0 ** -8, (i, err)
+        assert np.array_equal(outs[0][i], outs[pb.NO_GROUPING][i]) or err < 2.0 ** -8

@@ -16,7 +16,7 @@ import paper_2301_08984_b200 as pb  # noqa: E402
 
 VARIANTS = [
     ("base", 0, {}),
-    ("no_streamk", 0, {"PLANC_B200_STREAMK": "0"}),
+    ("no_grouping", pb.NO_GROUPING, {}),
     ("fuse", pb.FUSE_EPILOGUES, {}),
 ]
 
