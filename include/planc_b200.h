@@ -169,12 +169,14 @@ int planc_b200_timeline(planc_b200_exec* h, char** json_out);
 int planc_b200_gemm_config(int64_t m, int64_t n, int64_t k, int ta, int tb, int a_bf16, int b_bf16, int c_bf16,
                            int* tensor_cores, int* tile_n);
 
-/* Host-only: the tcgen05 GEMM's launch schedule on a GPU with `sms` SMs —
- * tile width, persistent grid, tiles done whole (data-parallel waves) and
- * the number of CTAs sharing the remaining tiles by k-range (stream-K), with
- * the workspace the stream-K tail needs (0 without it). bf16 operands. */
-int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, int c_bf16, int sms, int* tile_n,
-                             int* grid, int* dp_tiles, int* sk_ctas, int64_t* ws_bytes);
+/* Host-only: the tcgen05 GEMM's launch schedule on a GPU with `sms` SMs for
+ * `group` independent GEMMs of this shape in one launch (1 = a single GEMM)
+ * — tile width, persistent grid, and either tiles done whole (data-parallel
+ * waves) plus the CTAs sharing the remaining tiles by k-range (stream-K), or
+ * the number of k-splits per tile (split-K: fp32 partials + a reduce kernel);
+ * with the workspace either needs (0 without). bf16 operands. */
+int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, int c_bf16, int sms, int group,
+                             int* tile_n, int* grid, int* dp_tiles, int* sk_ctas, int* splits, int64_t* ws_bytes);
 
 /* Host-only lowering (no GPU needed): the executor's device program for a
  * plan as JSON — buffers, instructions, box cells, issue order. */

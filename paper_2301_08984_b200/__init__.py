@@ -116,8 +116,8 @@ def _load():
     L.planc_b200_peer_blob_bytes.restype = c_i64
     L.planc_b200_peer_export.argtypes = [vp, ctypes.c_char_p, c_i64]
     L.planc_b200_peer_import.argtypes = [vp, ctypes.c_char_p, c_i64]
-    L.planc_b200_gemm_schedule.argtypes = [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, P(c_int), P(c_int),
-                                           P(c_int), P(c_int), P(c_i64)]
+    L.planc_b200_gemm_schedule.argtypes = [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_int, P(c_int),
+                                           P(c_int), P(c_int), P(c_int), P(c_int), P(c_i64)]
     L.planc_b200_free.argtypes = [vp]
     _lib = L
     return L
@@ -160,15 +160,17 @@ def describe(plan_json: str, strict_value: bool = False, lane_rank=None, flags: 
 
 
 def gemm_schedule(m: int, n: int, k: int, ta: bool = False, tb: bool = False, c_bf16: bool = True,
-                  sms: int = 148) -> dict:
+                  sms: int = 148, group: int = 1) -> dict:
     """Host-only: the tcgen05 GEMM's launch schedule (tile width, grid, whole
-    tiles, stream-K CTAs, workspace bytes) for a bf16 matmul of this shape."""
+    tiles, stream-K CTAs or split-K splits, workspace bytes) for `group`
+    bf16 matmuls of this shape in one launch."""
     L = _load()
-    bn, grid, dp, sk = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    bn, grid, dp, sk, sp = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     ws = ctypes.c_int64()
-    _check(L.planc_b200_gemm_schedule(m, n, k, int(ta), int(tb), int(c_bf16), sms, ctypes.byref(bn),
-                                      ctypes.byref(grid), ctypes.byref(dp), ctypes.byref(sk), ctypes.byref(ws)))
-    return {"tile_n": bn.value, "grid": grid.value, "dp_tiles": dp.value, "sk_ctas": sk.value,
+    _check(L.planc_b200_gemm_schedule(m, n, k, int(ta), int(tb), int(c_bf16), sms, group, ctypes.byref(bn),
+                                      ctypes.byref(grid), ctypes.byref(dp), ctypes.byref(sk), ctypes.byref(sp),
+                                      ctypes.byref(ws)))
+    return {"tile_n": bn.value, "grid": grid.value, "dp_tiles": dp.value, "sk_ctas": sk.value, "splits": sp.value,
             "ws_bytes": ws.value}
 
 

@@ -329,11 +329,13 @@ int planc_b200_gemm_config(int64_t m, int64_t n, int64_t k, int ta, int tb, int 
   return PLANC_B200_OK;
 }
 
-int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, int c_bf16, int sms, int* tile_n,
-                             int* grid, int* dp_tiles, int* sk_ctas, int64_t* ws_bytes) {
+int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, int c_bf16, int sms, int group,
+                             int* tile_n, int* grid, int* dp_tiles, int* sk_ctas, int* splits, int64_t* ws_bytes) {
   return guarded([&] {
     if (sms <= 0) throw UsageError("sms must be positive");
+    if (group < 1 || group > kMaxGemmGroup) throw UsageError("group must be in [1, 8]");
     GemmArgs a{};
+    a.group = group;
     a.m = m;
     a.n = n;
     a.k = k;
@@ -348,6 +350,7 @@ int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, in
     if (grid) *grid = sc.grid;
     if (dp_tiles) *dp_tiles = sc.dp_tiles;
     if (sk_ctas) *sk_ctas = sc.sk_ctas;
+    if (splits) *splits = sc.splits;
     if (ws_bytes) *ws_bytes = sc.ws_bytes;
   });
 }

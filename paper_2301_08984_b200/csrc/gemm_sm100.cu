@@ -34,6 +34,7 @@
 #include <string>
 
 #include "kernels.cuh"
+#include "launch.cuh"
 
 namespace planc_b200 {
 
@@ -66,15 +67,22 @@ struct Cfg {
 // (32x32 boxes, 64B swizzle).
 struct EpiMaps {
   CUtensorMap out[1];
+  // Split-K partials: fp32 [group][splits][m_pad] x [n_pad] (32x32 boxes,
+  // 128B swizzle), row of (member p, split s, output row r) =
+  // (p * splits + s) * m_pad + r.
+  CUtensorMap ws;
 };
 
 // Operand / result maps of the launch's GEMMs (one, or a group of
 // independent same-shape GEMMs sharing the tile space: tile t belongs to
 // member t / tiles_per_gemm).
+// NG = capacity (1 for single launches: kernel parameters stay small, which
+// keeps graph launch latency down; kMaxGemmGroup for grouped launches).
+template <int NG>
 struct GroupMaps {
-  CUtensorMap a[kMaxGemmGroup];
-  CUtensorMap b[kMaxGemmGroup];
-  CUtensorMap c[kMaxGemmGroup];
+  CUtensorMap a[NG];
+  CUtensorMap b[NG];
+  CUtensorMap c[NG];
 };
 
 // Stream-K tail (data-parallel waves, then the remaining tiles' k-iterations
@@ -88,6 +96,7 @@ struct GroupMaps {
 struct SkParams {
   int dp_tiles = 0;
   int sk_ctas = 0;
+  int splits = 0;  // split-K: every work item is (tile, split), stored to ws_map
   long long sk_iters = 0;
   float* partials = nullptr;  // [sk_ctas][2 slots][4 quarters][BN/32 chunks][8][32] float4
   int* counters = nullptr;    // [(tiles - dp_tiles) * 4], zero between launches
@@ -105,6 +114,15 @@ __device__ __forceinline__ int sk_owner(const SkParams& sk, long long x) {
 // Calls f(tile, kb0, kb1) for this CTA's work items in order.
 template <typename F>
 __device__ __forceinline__ void for_each_work(int num_k, const SkParams& sk, F&& f) {
+  if (sk.splits > 1) {
+    // Split-K: item (tile t, split s) covers k-blocks [s*K/S, (s+1)*K/S).
+    const int items = sk.dp_tiles * sk.splits;
+    for (int x = blockIdx.x; x < items; x += gridDim.x) {
+      const int t = x / sk.splits, sp = x - t * sk.splits;
+      f(t, sp * num_k / sk.splits, (sp + 1) * num_k / sk.splits);
+    }
+    return;
+  }
   for (int t = blockIdx.x; t < sk.dp_tiles; t += gridDim.x) f(t, 0, num_k);
   if (static_cast<int>(blockIdx.x) < sk.sk_ctas) {
     long long it = sk_lo(sk, blockIdx.x);
@@ -258,9 +276,9 @@ __device__ __forceinline__ void bf16_unpair(std::uint32_t w, float& lo, float& h
   hi = __uint_as_float(w & 0xffff0000u);
 }
 
-template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
+template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE, int NG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ GroupMaps gm, int ng, int m, int n, int k,
+    gemm_tc_kernel(const __grid_constant__ GroupMaps<NG> gm, int ng, int m, int n, int k,
                    const __grid_constant__ EpiParams epi, const __grid_constant__ EpiMaps maps,
                    const __grid_constant__ SkParams sk) {
   extern __shared__ std::uint8_t smem_raw[];
@@ -318,6 +336,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const std::uint32_t tmem = *tmem_slot;
+  // Prologue done (barriers, TMEM, descriptor prefetch): from here on the
+  // previous kernel's results are read and the workspace is written.
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -384,6 +405,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_commit(&tfull[acc]);  // accumulator complete
         ++local;
       });
+      pdl_trigger();  // every MMA issued: the next kernel may start its prologue
     }
   } else if constexpr (!FUSE) {
     // Epilogue warps 2..5: warp w may only touch TMEM lanes 32*(w%4)..+31.
@@ -395,11 +417,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     std::uint8_t* stg = staging + (warp - 2) * 2 * 4096;
     int sb = 0;
     int local = 0;
-    auto store_chunk = [&](const std::uint32_t(&r)[32], int p, int mb, int nb, int c) {
+    auto store_chunk = [&](const std::uint32_t(&r)[32], const CUtensorMap* map, bool bf16, int x, int y) {
       if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer sb is free
       __syncwarp();
       std::uint8_t* buf = stg + sb * 4096;
-      if constexpr (C_BF16) {
+      if (bf16) {
         // 64 B rows, SWIZZLE_64B: 16-byte chunk v lands at v ^ ((row >> 1) & 3).
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
@@ -419,9 +441,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
       __syncwarp();
-      if (lane == 0) tma_store_2d(&gm.c[p], buf, nb * BN + c * 32, mb * BM + q * 32);
+      if (lane == 0) tma_store_2d(map, buf, x, y);
       sb ^= 1;
     };
+    const int m_pad = tiles_m * BM;
     // fp32 partial of (CTA b, slot, this quarter, chunk c): 8 float4 per
     // lane, lane-interleaved so every access is one coalesced 512 B row.
     auto partial_ptr = [&](int b, int slot, int c) {
@@ -436,7 +459,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ++local;
       tc_fence_after();
       const std::uint32_t base = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
-      if (kb0 == 0 && kb1 == num_k) {  // whole tile
+      if ((kb0 == 0 && kb1 == num_k) || sk.splits > 1) {  // whole tile, or one split's fp32 partial
+        const bool part = sk.splits > 1;
+        // split index of k-range start kb0 = floor(s*K/S): s = ceil(kb0*S/K) (K/S >= 1)
+        const int sp = (kb0 * sk.splits + num_k - 1) / num_k;
+        const int y = part ? (p * sk.splits + sp) * m_pad + mb * BM + q * 32 : mb * BM + q * 32;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           std::uint32_t r[32];
@@ -447,7 +474,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
           }
-          store_chunk(r, p, mb, nb, c);
+          if (part) store_chunk(r, &maps.ws, false, nb * BN + c * 32, y);
+          else store_chunk(r, &gm.c[p], C_BF16, nb * BN + c * 32, y);
         }
         return;
       }
@@ -520,7 +548,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           r[4 * v + 2] = __float_as_uint(sum[v].z);
           r[4 * v + 3] = __float_as_uint(sum[v].w);
         }
-        store_chunk(r, p, mb, nb, c);
+        store_chunk(r, &gm.c[p], C_BF16, nb * BN + c * 32, mb * BM + q * 32);
       }
     });
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
@@ -631,6 +659,58 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// Split-K reduction: C_p[row][col..col+3] = sum over splits s (in order) of
+// ws[(p*S + s)*m_pad + row][col..col+3] — coalesced on both sides.
+struct SplitOut {
+  void* c[kMaxGemmGroup];
+};
+
+template <bool C_BF16>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __restrict__ ws, const __grid_constant__ SplitOut out, int S,
+                                                            int m, int n, int m_pad, int n_pad, int ng) {
+  pdl_wait();
+  pdl_trigger();
+  const int n4 = n / 4;
+  const long long per = static_cast<long long>(m) * n4;
+  const long long total = per * ng;
+  const int np4 = n_pad / 4;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int p = static_cast<int>(i / per);
+    const long long rem = i - p * per;
+    const int row = static_cast<int>(rem / n4), c4 = static_cast<int>(rem - static_cast<long long>(row) * n4);
+    const float4* src = ws + (static_cast<long long>(p) * S * m_pad + row) * np4 + c4;
+    const long long step = static_cast<long long>(m_pad) * np4;
+    // kSplitBatch partial loads in flight per thread, summed in split order.
+    constexpr int kSplitBatch = 8;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < S; s0 += kSplitBatch) {
+      float4 v[kSplitBatch];
+#pragma unroll
+      for (int j = 0; j < kSplitBatch; ++j)
+        if (s0 + j < S) v[j] = __ldcg(src + (s0 + j) * step);
+#pragma unroll
+      for (int j = 0; j < kSplitBatch; ++j) {
+        if (s0 + j >= S) break;
+        if (s0 + j == 0) {
+          acc = v[j];
+        } else {
+          acc.x += v[j].x;
+          acc.y += v[j].y;
+          acc.z += v[j].z;
+          acc.w += v[j].w;
+        }
+      }
+    }
+    if constexpr (C_BF16) {
+      uint2 w = make_uint2(bf16_pair(acc.x, acc.y), bf16_pair(acc.z, acc.w));
+      reinterpret_cast<uint2*>(out.c[p])[rem] = w;
+    } else {
+      reinterpret_cast<float4*>(out.c[p])[rem] = acc;
+    }
+  }
+}
+
 // ---- host ---------------------------------------------------------------------
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -693,11 +773,11 @@ int device_sms() {
   return num_sms[dev & 31];
 }
 
-template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
-void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
+template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE, int NG>
+void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
   static unsigned attr_set_mask = 0;  // per device ordinal
   constexpr int SMEM_BYTES = Cfg<BN, FUSE>::SMEM_BYTES;
-  auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16, BN, FUSE>;
+  auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16, BN, FUSE, NG>;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set_mask & (1u << dev))) {
@@ -708,9 +788,9 @@ void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
   // A: [m][k] (K-major) or, transposed, [k][m] (MN-major); B: [k][n]
   // (MN-major) or, transposed, [n][k] (K-major).
   const int ng = a.group > 1 ? a.group : 1;
-  if (ng > kMaxGemmGroup) throw std::runtime_error("gemm_tc: group above kMaxGemmGroup");
+  if (ng > NG) throw std::runtime_error("gemm_tc: group above the launch's capacity");
   if (FUSE && ng > 1) throw std::runtime_error("gemm_tc: fused epilogue on a grouped launch");
-  GroupMaps gm;
+  GroupMaps<NG> gm;
   std::memset(&gm, 0, sizeof(gm));
   for (int i = 0; i < ng; ++i) {
     const void* A = ng > 1 ? a.gA[i] : a.A;
@@ -727,15 +807,37 @@ void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
   sk.dp_tiles = sc.dp_tiles;
   sk.sk_ctas = sc.sk_ctas;
   sk.sk_iters = sc.sk_iters;
-  if (sc.sk_ctas > 0) {
+  sk.splits = sc.splits;
+  const std::int64_t m_pad = (a.m + BM - 1) / BM * BM, n_pad = (a.n + BN - 1) / BN * BN;
+  if (sc.splits > 1) {
+    // Partials: fp32 [ng * splits * m_pad][n_pad], stored like an fp32 C.
+    maps.ws = make_store_map(a.ws, static_cast<std::int64_t>(ng) * sc.splits * m_pad, n_pad, false);
+  } else if (sc.sk_ctas > 0) {
     char* ws = static_cast<char*>(a.ws);
     sk.counters = reinterpret_cast<int*>(ws);
     sk.partials = reinterpret_cast<float*>(ws + sc.counter_bytes);
   }
-  kern<<<sc.grid, NUM_THREADS, SMEM_BYTES, s>>>(gm, ng, static_cast<int>(a.m), static_cast<int>(a.n),
-                                                static_cast<int>(a.k), a.epi, maps, sk);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc_kernel: ") + cudaGetErrorString(e));
+  pdl_launch("gemm_tc_kernel", kern, dim3(sc.grid), dim3(NUM_THREADS), SMEM_BYTES, s, gm, ng, static_cast<int>(a.m),
+             static_cast<int>(a.n), static_cast<int>(a.k), a.epi, maps, sk);
+  if (sc.splits > 1) {
+    SplitOut out;
+    for (int i = 0; i < ng; ++i) out.c[i] = ng > 1 ? a.gC[i] : a.C;
+    const long long work = static_cast<long long>(ng) * a.m * (a.n / 4);
+    const int blocks = static_cast<int>(std::min<long long>((work + 255) / 256, 4LL * device_sms()));
+    pdl_launch("splitk_reduce_kernel", splitk_reduce_kernel<C_BF16>, dim3(blocks), dim3(256), 0, s,
+               static_cast<const float4*>(a.ws), out, sc.splits, static_cast<int>(a.m), static_cast<int>(a.n),
+               static_cast<int>(m_pad), static_cast<int>(n_pad), ng);
+  }
+}
+
+template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
+void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
+  if constexpr (FUSE) {
+    launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
+  } else {
+    if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup>(a, sc, s);
+    else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
+  }
 }
 
 // Modelled time (us) of one launch, calibrated on B200 single-GEMM graphs
@@ -792,6 +894,33 @@ GemmSchedule schedule_for(std::int64_t m, std::int64_t n, std::int64_t k, int bn
 
 }  // namespace
 
+// Split-K candidate: T tiles (group included) x S splits work items on at
+// most `sms` CTAs, S as large as keeps >= kMinSplitIters k-blocks per split;
+// the reduce kernel reads S fp32 copies of the padded output and writes C.
+constexpr int kMinSplitIters = 4;
+constexpr double kReduceLaunchUs = 2.0;
+constexpr double kReduceBytesPerUs = 4.0e6;  // ~4 TB/s from L2 / HBM
+GemmSchedule splitk_for(std::int64_t m, std::int64_t n, std::int64_t k, int bn, int sms, int group, int es_out) {
+  GemmSchedule sc;
+  sc.bn = bn;
+  const std::int64_t tm = (m + BM - 1) / BM, tn = (n + bn - 1) / bn;
+  sc.tiles = tm * tn * std::max(group, 1);
+  sc.num_k = (k + BK - 1) / BK;
+  const std::int64_t S = std::min<std::int64_t>(sms / std::max<std::int64_t>(sc.tiles, 1), sc.num_k / kMinSplitIters);
+  if (S < 2 || n % 4 != 0) {
+    sc.model_us = 1e300;
+    return sc;
+  }
+  sc.splits = static_cast<int>(S);
+  sc.dp_tiles = static_cast<int>(sc.tiles);
+  sc.grid = static_cast<int>(sc.tiles * S);
+  const double part_bytes = static_cast<double>(std::max(group, 1)) * S * (tm * BM) * (tn * bn) * 4.0;
+  sc.ws_bytes = static_cast<std::int64_t>(part_bytes);
+  sc.model_us = static_cast<double>((sc.num_k + S - 1) / S) * kb_us(bn) + kTileUs + kReduceLaunchUs +
+                (part_bytes + static_cast<double>(std::max(group, 1)) * m * n * es_out) / kReduceBytesPerUs;
+  return sc;
+}
+
 // Tile width and stream-K split: the candidate with the least modelled time
 // (data-parallel preferred unless stream-K is clearly faster, wider tiles
 // unless narrower ones are). PLANC_B200_GEMM_BN=256|128|64 forces a width,
@@ -802,6 +931,12 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   const char* skenv = std::getenv("PLANC_B200_STREAMK");
   const int skmode = skenv ? std::atoi(skenv) : 1;
   const bool allow_sk = skmode != 0 && a.epi.n_ops == 0 && (a.allow_streamk || skmode == 2);
+  // PLANC_B200_SPLITK=0 disables split-K, =2 takes it whenever it applies.
+  const char* spenv = std::getenv("PLANC_B200_SPLITK");
+  const int splitmode = spenv ? std::atoi(spenv) : 1;
+  // Like stream-K, split-K trades SM-time for latency: only when the lane
+  // has its GPU to itself (co-resident lanes would be starved of SMs).
+  const bool allow_split = splitmode != 0 && a.epi.n_ops == 0 && (a.allow_streamk || splitmode == 2);
   GemmSchedule best;
   bool have = false;
   for (int bn : {256, 128, 64}) {
@@ -809,6 +944,10 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
     GemmSchedule dp = schedule_for(a.m, a.n, a.k, bn, false, sms, false, a.group);
     GemmSchedule sk = schedule_for(a.m, a.n, a.k, bn, allow_sk, sms, skmode == 2, a.group);
     GemmSchedule c = (sk.sk_ctas > 0 && (skmode == 2 || sk.model_us < 0.9 * dp.model_us)) ? sk : dp;
+    if (allow_split) {
+      GemmSchedule sp = splitk_for(a.m, a.n, a.k, bn, sms, a.group, a.dc == DT_BF16 ? 2 : 4);
+      if (sp.splits > 1 && (splitmode == 2 || sp.model_us < 0.9 * c.model_us)) c = sp;
+    }
     if (!have || c.model_us < best.model_us * 0.97) {
       best = c;
       have = true;
@@ -816,6 +955,8 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   }
   return best;
 }
+
+int gemm_sm100_launches(const GemmArgs& a) { return gemm_sm100_schedule(a, device_sms()).splits > 1 ? 2 : 1; }
 
 int gemm_sm100_tile_n(const GemmArgs& a) { return gemm_sm100_schedule(a, 148).bn; }
 
@@ -840,7 +981,7 @@ bool gemm_sm100_eligible(const GemmArgs& a) {
 void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
   const bool a_mn = a.ta, b_mn = !a.tb, cb = a.dc == DT_BF16;
   GemmSchedule sc = gemm_sm100_schedule(a, device_sms());
-  if (sc.sk_ctas > 0 && (a.ws == nullptr || a.ws_bytes < sc.ws_bytes)) {
+  if ((sc.sk_ctas > 0 || sc.splits > 1) && (a.ws == nullptr || a.ws_bytes < sc.ws_bytes)) {
     sc = schedule_for(a.m, a.n, a.k, sc.bn, false, device_sms(), false, a.group);  // no workspace: data-parallel
   }
   const int bn = sc.bn;

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "kernels.cuh"
+#include "launch.cuh"
 
 namespace planc_b200 {
 
@@ -130,6 +131,8 @@ template <typename T, int V, int R>
 __global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, const DevCell* __restrict__ cells,
                                                            const DevTerm* __restrict__ terms,
                                                            const DevChunk* __restrict__ chunks) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
   // Every cell of the launch has exactly rank R (the host pads lower-rank
   // cells with leading unit dims), so all coordinate indexing is static and
   // stays in registers.
@@ -215,9 +218,9 @@ template <typename T, int V>
 void box_rank_dispatch(void* dst, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks,
                        int max_rank, cudaStream_t s) {
   T* d = static_cast<T*>(dst);
-  if (max_rank <= 1) box_kernel<T, V, 1><<<nchunks, kBoxThreads, 0, s>>>(d, cells, terms, chunks);
-  else if (max_rank == 2) box_kernel<T, V, 2><<<nchunks, kBoxThreads, 0, s>>>(d, cells, terms, chunks);
-  else box_kernel<T, V, kBoxRank><<<nchunks, kBoxThreads, 0, s>>>(d, cells, terms, chunks);
+  if (max_rank <= 1) pdl_launch("box_kernel", box_kernel<T, V, 1>, dim3(nchunks), dim3(kBoxThreads), 0, s, d, cells, terms, chunks);
+  else if (max_rank == 2) pdl_launch("box_kernel", box_kernel<T, V, 2>, dim3(nchunks), dim3(kBoxThreads), 0, s, d, cells, terms, chunks);
+  else pdl_launch("box_kernel", box_kernel<T, V, kBoxRank>, dim3(nchunks), dim3(kBoxThreads), 0, s, d, cells, terms, chunks);
 }
 
 template <typename T>
@@ -249,6 +252,8 @@ constexpr int kEwUnroll = 4;
 
 template <typename T, int OP, int NIN>
 __global__ void __launch_bounds__(256) ew_kernel(EwPtrs in, T* __restrict__ out, std::int64_t nvec) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
   constexpr int V = 16 / sizeof(T);
   const std::int64_t stride = blockDim.x;
   for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x) * kEwUnroll + threadIdx.x; base < nvec;
@@ -281,6 +286,8 @@ __global__ void __launch_bounds__(256) ew_kernel(EwPtrs in, T* __restrict__ out,
 
 template <typename T, int OP, int NIN>
 __global__ void ew_tail_kernel(EwPtrs in, T* __restrict__ out, std::int64_t begin, std::int64_t count) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
   std::int64_t i = begin + blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
   if (i >= begin + count) return;
   float acc = to_acc<T>(static_cast<const T*>(in.p[0])[i]);
@@ -294,11 +301,11 @@ void ew_launch(const EwPtrs& p, void* out, std::int64_t nvec, std::int64_t count
   constexpr int V = 16 / sizeof(T);
   if (nvec > 0) {
     // One pass: every thread owns kEwUnroll vectors (no grid-stride tail).
-    ew_kernel<T, OP, NIN><<<grid_for(nvec, 256 * kEwUnroll, 1 << 30), 256, 0, s>>>(p, static_cast<T*>(out), nvec);
+    pdl_launch("ew_kernel", ew_kernel<T, OP, NIN>, dim3(grid_for(nvec, 256 * kEwUnroll, 1 << 30)), dim3(256), 0, s, p, static_cast<T*>(out), nvec);
   }
   std::int64_t rest = count - nvec * V;
   if (rest > 0) {
-    ew_tail_kernel<T, OP, NIN><<<static_cast<int>((rest + 255) / 256), 256, 0, s>>>(p, static_cast<T*>(out),
+    pdl_launch("ew_tail_kernel", ew_tail_kernel<T, OP, NIN>, dim3(static_cast<int>((rest + 255) / 256)), dim3(256), 0, s, p, static_cast<T*>(out),
                                                                                     nvec * V, rest);
   }
 }
@@ -331,6 +338,8 @@ void ew_typed(const void* const* ins, int nin, void* out, std::int64_t count, cu
 template <typename T>
 __global__ void reduce_rows_kernel(const T* __restrict__ in, T* __restrict__ out, std::int64_t outer,
                                    std::int64_t axis_len) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
   std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / 32;
   int lane = threadIdx.x & 31;
   std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * blockDim.x / 32;
@@ -347,6 +356,8 @@ __global__ void reduce_rows_kernel(const T* __restrict__ in, T* __restrict__ out
 template <typename T>
 __global__ void reduce_cols_kernel(const T* __restrict__ in, T* __restrict__ out, std::int64_t outer,
                                    std::int64_t axis_len, std::int64_t inner) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
   std::int64_t total = outer * inner;
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
@@ -363,6 +374,8 @@ __global__ void reduce_cols_kernel(const T* __restrict__ in, T* __restrict__ out
 template <typename T>
 __global__ void emb_lookup_kernel(const int* __restrict__ idx, const T* __restrict__ table, T* __restrict__ out,
                                   std::int64_t n, std::int64_t rows, std::int64_t h, std::int64_t lo) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
   std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / 32;
   int lane = threadIdx.x & 31;
   std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * blockDim.x / 32;
@@ -378,6 +391,8 @@ __global__ void emb_lookup_kernel(const int* __restrict__ idx, const T* __restri
 template <typename T>
 __global__ void emb_grad_kernel(const int* __restrict__ idx, const T* __restrict__ gout, float* __restrict__ acc,
                                 std::int64_t n, std::int64_t rows, std::int64_t h, std::int64_t lo) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
   std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / 32;
   int lane = threadIdx.x & 31;
   std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * blockDim.x / 32;
@@ -389,12 +404,16 @@ __global__ void emb_grad_kernel(const int* __restrict__ idx, const T* __restrict
 }
 
 __global__ void convert_kernel(int dt, void* out, const float* __restrict__ in, std::int64_t count) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
     store_any(out, dt, i, in[i]);
 }
 
 __global__ void zero_kernel(float* p, std::int64_t count) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
     p[i] = 0.f;
@@ -406,6 +425,8 @@ __global__ void zero_kernel(float* p, std::int64_t count) {
 constexpr int kTM = 64, kTN = 64, kTK = 16;
 
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs a) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
   __shared__ float As[kTK][kTM + 4];
   __shared__ float Bs[kTK][kTN + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -508,18 +529,18 @@ void launch_reduce(int dtype, const void* in, void* out, std::int64_t outer, std
                    std::int64_t inner, cudaStream_t s) {
   if (dtype == DT_F32) {
     if (inner == 1)
-      reduce_rows_kernel<float><<<grid_for(outer * 32, 256), 256, 0, s>>>(static_cast<const float*>(in),
+      pdl_launch("reduce_rows_kernel", reduce_rows_kernel<float>, dim3(grid_for(outer * 32, 256)), dim3(256), 0, s, static_cast<const float*>(in),
                                                                            static_cast<float*>(out), outer, axis_len);
     else
-      reduce_cols_kernel<float><<<grid_for(outer * inner, 256), 256, 0, s>>>(
+      pdl_launch("reduce_cols_kernel", reduce_cols_kernel<float>, dim3(grid_for(outer * inner, 256)), dim3(256), 0, s, 
           static_cast<const float*>(in), static_cast<float*>(out), outer, axis_len, inner);
   } else if (dtype == DT_BF16) {
     using B = __nv_bfloat16;
     if (inner == 1)
-      reduce_rows_kernel<B><<<grid_for(outer * 32, 256), 256, 0, s>>>(static_cast<const B*>(in),
+      pdl_launch("reduce_rows_kernel", reduce_rows_kernel<B>, dim3(grid_for(outer * 32, 256)), dim3(256), 0, s, static_cast<const B*>(in),
                                                                        static_cast<B*>(out), outer, axis_len);
     else
-      reduce_cols_kernel<B><<<grid_for(outer * inner, 256), 256, 0, s>>>(static_cast<const B*>(in),
+      pdl_launch("reduce_cols_kernel", reduce_cols_kernel<B>, dim3(grid_for(outer * inner, 256)), dim3(256), 0, s, static_cast<const B*>(in),
                                                                          static_cast<B*>(out), outer, axis_len, inner);
   } else {
     throw std::runtime_error("reduce: unsupported dtype");
@@ -531,10 +552,10 @@ void launch_emb_lookup(int dtype, const int* idx, const void* table, void* out, 
                        std::int64_t h, std::int64_t lo, cudaStream_t s) {
   int g = grid_for(n * 32, 256);
   if (dtype == DT_F32)
-    emb_lookup_kernel<float><<<g, 256, 0, s>>>(idx, static_cast<const float*>(table), static_cast<float*>(out), n,
+    pdl_launch("emb_lookup_kernel", emb_lookup_kernel<float>, dim3(g), dim3(256), 0, s, idx, static_cast<const float*>(table), static_cast<float*>(out), n,
                                                 rows, h, lo);
   else if (dtype == DT_BF16)
-    emb_lookup_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(idx, static_cast<const __nv_bfloat16*>(table),
+    pdl_launch("emb_lookup_kernel", emb_lookup_kernel<__nv_bfloat16>, dim3(g), dim3(256), 0, s, idx, static_cast<const __nv_bfloat16*>(table),
                                                         static_cast<__nv_bfloat16*>(out), n, rows, h, lo);
   else
     throw std::runtime_error("embedding: unsupported dtype");
@@ -544,16 +565,16 @@ void launch_emb_lookup(int dtype, const int* idx, const void* table, void* out, 
 void launch_emb_grad(int dtype, const int* idx, const void* gout, void* out, float* scratch, std::int64_t n,
                      std::int64_t rows, std::int64_t h, std::int64_t lo, cudaStream_t s) {
   float* acc = dtype == DT_F32 ? static_cast<float*>(out) : scratch;
-  zero_kernel<<<grid_for(rows * h, 256), 256, 0, s>>>(acc, rows * h);
+  pdl_launch("zero_kernel", zero_kernel, dim3(grid_for(rows * h, 256)), dim3(256), 0, s, acc, rows * h);
   int g = grid_for(n * 32, 256);
   if (dtype == DT_F32)
-    emb_grad_kernel<float><<<g, 256, 0, s>>>(idx, static_cast<const float*>(gout), acc, n, rows, h, lo);
+    pdl_launch("emb_grad_kernel", emb_grad_kernel<float>, dim3(g), dim3(256), 0, s, idx, static_cast<const float*>(gout), acc, n, rows, h, lo);
   else if (dtype == DT_BF16)
-    emb_grad_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(idx, static_cast<const __nv_bfloat16*>(gout), acc, n, rows,
+    pdl_launch("emb_grad_kernel", emb_grad_kernel<__nv_bfloat16>, dim3(g), dim3(256), 0, s, idx, static_cast<const __nv_bfloat16*>(gout), acc, n, rows,
                                                       h, lo);
   else
     throw std::runtime_error("embedding-grad: unsupported dtype");
-  if (dtype != DT_F32) convert_kernel<<<grid_for(rows * h, 256), 256, 0, s>>>(dtype, out, acc, rows * h);
+  if (dtype != DT_F32) pdl_launch("convert_kernel", convert_kernel, dim3(grid_for(rows * h, 256)), dim3(256), 0, s, dtype, out, acc, rows * h);
   check_launch("emb_grad_kernel");
 }
 
@@ -563,7 +584,7 @@ void launch_gemm_simt(const GemmArgs& a, cudaStream_t s) {
     // Empty contraction: C = 0.
     std::int64_t cnt = a.m * a.n;
     if (a.dc == DT_F32) {
-      zero_kernel<<<grid_for(cnt, 256), 256, 0, s>>>(static_cast<float*>(a.C), cnt);
+      pdl_launch("zero_kernel", zero_kernel, dim3(grid_for(cnt, 256)), dim3(256), 0, s, static_cast<float*>(a.C), cnt);
     } else {
       cudaMemsetAsync(a.C, 0, cnt * 2, s);
     }
@@ -571,25 +592,31 @@ void launch_gemm_simt(const GemmArgs& a, cudaStream_t s) {
     return;
   }
   dim3 grid(static_cast<unsigned>((a.n + kTN - 1) / kTN), static_cast<unsigned>((a.m + kTM - 1) / kTM));
-  gemm_simt_kernel<<<grid, 256, 0, s>>>(a);
+  pdl_launch("gemm_simt_kernel", gemm_simt_kernel, dim3(grid), dim3(256), 0, s, a);
   check_launch("gemm_simt_kernel");
 }
 
 void launch_convert(int dtype_out, void* out, const float* in, std::int64_t count, cudaStream_t s) {
-  convert_kernel<<<grid_for(count, 256), 256, 0, s>>>(dtype_out, out, in, count);
+  pdl_launch("convert_kernel", convert_kernel, dim3(grid_for(count, 256)), dim3(256), 0, s, dtype_out, out, in, count);
   check_launch("convert_kernel");
 }
 
 void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s) {
-  zero_kernel<<<grid_for(count, 256), 256, 0, s>>>(p, count);
+  pdl_launch("zero_kernel", zero_kernel, dim3(grid_for(count, 256)), dim3(256), 0, s, p, count);
   check_launch("zero_kernel");
 }
 
 // ---- peer-memory flags ------------------------------------------------------
 
-__global__ void peer_epoch_kernel(unsigned* epoch) { *epoch += 1u; }
+__global__ void peer_epoch_kernel(unsigned* epoch) {
+  pdl_wait();
+  pdl_trigger();
+  *epoch += 1u;
+}
 
 __global__ void peer_flags_kernel(const unsigned* epoch, PeerFlags f, unsigned long long timeout_ns, unsigned* err) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
   const unsigned e = *reinterpret_cast<const volatile unsigned*>(epoch);
   const int t = threadIdx.x;
   if (t < f.n_sig) {
@@ -617,13 +644,13 @@ __global__ void peer_flags_kernel(const unsigned* epoch, PeerFlags f, unsigned l
 }
 
 void launch_peer_epoch(unsigned* epoch, cudaStream_t s) {
-  peer_epoch_kernel<<<1, 1, 0, s>>>(epoch);
+  pdl_launch("peer_epoch_kernel", peer_epoch_kernel, dim3(1), dim3(1), 0, s, epoch);
   check_launch("peer_epoch_kernel");
 }
 
 void launch_peer_flags(const unsigned* epoch, const PeerFlags& f, unsigned long long timeout_ns, unsigned* err,
                        cudaStream_t s) {
-  peer_flags_kernel<<<1, 32, 0, s>>>(epoch, f, timeout_ns, err);
+  pdl_launch("peer_flags_kernel", peer_flags_kernel, dim3(1), dim3(32), 0, s, epoch, f, timeout_ns, err);
   check_launch("peer_flags_kernel");
 }
 

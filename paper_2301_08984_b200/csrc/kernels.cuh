@@ -112,7 +112,13 @@ struct GemmSchedule {
   int sk_ctas = 0;
   long long sk_iters = 0;
   std::int64_t counter_bytes = 0;
-  std::int64_t ws_bytes = 0;  // 0 without stream-K
+  // Split-K (small output, long k): every tile's k-blocks split into
+  // `splits` equal ranges, one work item each; fp32 partials land in the
+  // workspace (splits stacked copies of the padded output) and a separate
+  // reduce kernel sums them in split order — every SM pulls a slice, no CTA
+  // waits on another. 0 = off.
+  int splits = 0;
+  std::int64_t ws_bytes = 0;  // 0 without stream-K / split-K
   double model_us = 0;
 };
 
@@ -160,6 +166,7 @@ bool gemm_sm100_eligible(const GemmArgs& a);
 int gemm_sm100_tile_n(const GemmArgs& a);  // 256, 128 or 64
 GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms);
 std::int64_t gemm_sm100_workspace_bytes(const GemmArgs& a);  // on the current device
+int gemm_sm100_launches(const GemmArgs& a);                   // kernels per GEMM (2 with split-K)
 void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s);
 
 // Dispatch: tcgen05 path when eligible, SIMT tile kernel otherwise (a

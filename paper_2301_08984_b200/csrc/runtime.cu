@@ -329,6 +329,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       a.allow_streamk = gemm_streamk_ok(exec_lane_[in.id]);
       if (opt_.allow_tensor_cores && gemm_sm100_eligible(a)) {
         ++gemm_tc_per_step_;
+        kernels_per_step_ += gemm_sm100_launches(a) - 1;  // split-K reduce kernel
         LaneRt& lr = lanes_[exec_lane_[in.id]];
         DeviceGuard dg(lr.gpu);
         std::int64_t& need = lr.gemm_ws_bytes[exec_stream_[in.id]];

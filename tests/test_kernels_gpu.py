@@ -116,6 +116,7 @@ def test_gemm_streamk_vs_fp64(bn, m, n, k, ta, tb, monkeypatch):
 def test_gemm_streamk_fp32_exact(m, n, k, ta, tb, monkeypatch):
     """Integer operands: every partial and the k-ordered sum are exact."""
     monkeypatch.setenv("PLANC_B200_STREAMK", "2")
+    monkeypatch.setenv("PLANC_B200_SPLITK", "0")
     assert pb.gemm_schedule(m, n, k, ta, tb, c_bf16=False)["sk_ctas"] > 0
     rng = np.random.default_rng(11)
     plan, out_pt = matmul_plan(m, n, k, ta, tb, in_elem=2, out_elem=4)
@@ -192,3 +193,33 @@ def test_grouped_gemm_vs_fp64(g, m, n, k, ta, tb):
         err = np.abs(outs[0][i] - ref).max() / max(1.0, np.abs(ref).max())
         assert err < 2.0 ** -8, (i, err)
         assert np.array_equal(outs[0][i], outs[pb.NO_GROUPING][i]) or err < 2.0 ** -8
+
+
+@pytest.mark.parametrize("g,m,n,k,ta,tb", [(1, 256, 256, 8192, True, False), (4, 512, 512, 16384, True, False),
+                                           (1, 304, 520, 2000, False, True), (2, 136, 264, 4096, True, True),
+                                           (1, 256, 256, 8192, False, False)])
+@pytest.mark.parametrize("c_fp32", [False, True])
+def test_splitk_gemm_vs_fp64(g, m, n, k, ta, tb, c_fp32, monkeypatch):
+    """Split-K (PLANC_B200_SPLITK=2 forces it): k-range partials in fp32,
+    summed in split order by the reduce kernel; single and grouped launches."""
+    from plan_builder import grouped_matmul_plan
+
+    monkeypatch.setenv("PLANC_B200_SPLITK", "2")
+    monkeypatch.setenv("PLANC_B200_STREAMK", "0")
+    plan = grouped_matmul_plan(g, m, n, k, ta, tb, out_elem=4 if c_fp32 else 2)
+    rng = np.random.default_rng(g * 7 + m + n + k)
+    inputs = {}
+    for i in range(g):
+        inputs[3 * i] = bf16_round(rng.standard_normal((k, m) if ta else (m, k)))
+        inputs[3 * i + 1] = bf16_round(rng.standard_normal((n, k) if tb else (k, n)))
+    with pb.Executor(plan, lane_gpus=[0]) as ex:
+        ex.set_inputs(inputs)
+        ex.run(3)
+        st = ex.stats()
+        outs = [ex.get_output(3 * i + 2) for i in range(g)]
+    assert st["gemm_tc_per_step"] == 1 and st["kernels_per_step"] == 2  # GEMM + split-K reduce
+    for i in range(g):
+        a, b = inputs[3 * i], inputs[3 * i + 1]
+        ref = (a.T if ta else a) @ (b.T if tb else b)
+        err = np.abs(outs[i] - ref).max() / max(1.0, np.abs(ref).max())
+        assert err < (2.0 ** -16 if c_fp32 else 2.0 ** -8), (i, err)

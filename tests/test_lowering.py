@@ -268,6 +268,7 @@ def test_gemm_schedule_covers_every_k_block_once(m, n, k, ta, sk_mode, monkeypat
     shared tile's segments come from consecutive CTAs (the fixed reduction
     order)."""
     monkeypatch.setenv("PLANC_B200_STREAMK", sk_mode)
+    monkeypatch.setenv("PLANC_B200_SPLITK", "1" if sk_mode == "1" else "0")
     sms = 148
     sc = pb.gemm_schedule(m, n, k, ta, False, sms=sms)
     bn = sc["tile_n"]
@@ -279,6 +280,19 @@ def test_gemm_schedule_covers_every_k_block_once(m, n, k, ta, sk_mode, monkeypat
         for t in range(b, sc["dp_tiles"], sc["grid"]):
             for kb in range(num_k):
                 seen.setdefault((t, kb), []).append(b)
+    if sc["splits"] > 1:
+        # split-K: item (tile t, split s) = k-blocks [s*K/S, (s+1)*K/S); no whole tiles
+        seen = {}
+        S = sc["splits"]
+        assert sc["grid"] == tiles * S and sc["ws_bytes"] >= S * tiles * 128 * bn * 4
+        for x in range(tiles * S):
+            t, s = divmod(x, S)
+            for kb in range(s * num_k // S, (s + 1) * num_k // S):
+                seen.setdefault((t, kb), []).append(x)
+            assert (s * num_k // S * S + num_k - 1) // num_k == s  # the epilogue's split index
+        assert sorted(seen) == [(t, kb) for t in range(tiles) for kb in range(num_k)]
+        assert all(len(v) == 1 for v in seen.values())
+        return
     if sc["sk_ctas"]:
         assert sc["ws_bytes"] > 0 and sc["dp_tiles"] % sms == 0
         iters = (tiles - sc["dp_tiles"]) * num_k
