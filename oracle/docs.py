@@ -145,3 +145,129 @@ def gpt_block_doc(tokens: int, hidden: int, elem_size: int = 2, train: bool = Tr
 
 def dumps(doc: dict) -> str:
     return json.dumps(doc)
+
+
+# ---- schema extension --------------------------------------
+# Kinds the reference front end rejects (document.cpp:43-53) are compiled
+# through stand-ins with the same data flow and partitioning — unary ops as
+# `identity`, binary gradient ops as `mul` — and written back into the
+# compiled plan by rewrite_plan (op ids are preserved by op-trans as
+# "<id>/<i>" and "<id>~rc").
+EXT_STANDIN = {"softmax": "identity", "layernorm": "identity", "gelu": "identity",
+               "softmax-grad": "mul", "layernorm-grad": "mul", "gelu-grad": "mul"}
+
+
+def gpt_block_ext_doc(tokens: int, hidden: int, head: int, elem_size: int = 2, train: bool = True) -> dict:
+    """Transformer block with the extended sub-operators (config C2x):
+    N1 = LN(X); Q = N1·Wq, K = N1·Wk (column-parallel); P = softmax over
+    each `head`-wide segment of Q (per attention head, split with the heads);
+    S = P*K; O = S·Wo (row-parallel); X2 = O + X; N2 = LN(X2);
+    F1 = N2·W1 (column-parallel); Fa = GELU(F1); Y = Fa·W2 (row-parallel);
+    OUT = Y + X2. LayerNorms are replicated (full rows), as in Megatron.
+    ``train`` adds the backward (softmax-grad / layernorm-grad / gelu-grad and
+    the transposed GEMMs) and one optimizer add per weight."""
+    T, H, Fd = tokens, hidden, 4 * hidden
+    e = elem_size
+    ids = dict(X=0, Wq=1, Wk=2, Wo=3, W1=4, W2=5, N1=10, Q=11, K=12, P=13, S=14, O=15, X2=16, N2=17, F1=18,
+               Fa=19, Y=20, OUT=21)
+    pts = [_pt(ids["X"], (T, H), "activation", e)]
+    for w, shp in (("Wq", (H, H)), ("Wk", (H, H)), ("Wo", (H, H)), ("W1", (H, Fd)), ("W2", (Fd, H))):
+        pts.append(_pt(ids[w], shp, "weight", e))
+    for a, shp in (("N1", (T, H)), ("Q", (T, H)), ("K", (T, H)), ("P", (T, H)), ("S", (T, H)), ("O", (T, H)),
+                   ("X2", (T, H)), ("N2", (T, H)), ("F1", (T, Fd)), ("Fa", (T, Fd)), ("Y", (T, H)),
+                   ("OUT", (T, H))):
+        pts.append(_pt(ids[a], shp, "activation", e))
+    A = {"layer": 0, "batch_dim": 0}
+    SEG = dict(A, segment=head)
+    mm = lambda m, n, k: 2.0 * m * n * k  # noqa: E731
+    ops = [
+        _op("ln1", "layernorm", [ids["X"]], [ids["N1"]], "forward", 8 * T * H, A),
+        _op("colq", "matmul", [ids["N1"], ids["Wq"]], [ids["Q"]], "forward", mm(T, H, H), A),
+        _op("colk", "matmul", [ids["N1"], ids["Wk"]], [ids["K"]], "forward", mm(T, H, H), A),
+        _op("tpsm", "softmax", [ids["Q"]], [ids["P"]], "forward", 8 * T * H, SEG),
+        _op("tpmul", "mul", [ids["P"], ids["K"]], [ids["S"]], "forward", T * H, A),
+        _op("rowo", "matmul", [ids["S"], ids["Wo"]], [ids["O"]], "forward", mm(T, H, H), A),
+        _op("res1", "add", [ids["O"], ids["X"]], [ids["X2"]], "forward", T * H, A),
+        _op("ln2", "layernorm", [ids["X2"]], [ids["N2"]], "forward", 8 * T * H, A),
+        _op("colf1", "matmul", [ids["N2"], ids["W1"]], [ids["F1"]], "forward", mm(T, Fd, H), A),
+        _op("tpgelu", "gelu", [ids["F1"]], [ids["Fa"]], "forward", 8 * T * Fd, A),
+        _op("roww2", "matmul", [ids["Fa"], ids["W2"]], [ids["Y"]], "forward", mm(T, H, Fd), A),
+        _op("res2", "add", [ids["Y"], ids["X2"]], [ids["OUT"]], "forward", T * H, A),
+    ]
+    if train:
+        g = {k: 100 + v for k, v in dict(OUT=0, Y=1, Fa=2, F1=3, N2=4, X2a=5, X2=6, O=7, S=8, P=9, K=10, Q=11,
+                                         N1q=12, N1k=13, N1=14, X1=15, X=16).items()}
+        of = dict(OUT="OUT", Y="Y", Fa="Fa", F1="F1", N2="N2", X2a="X2", X2="X2", O="O", S="S", P="P", K="K",
+                  Q="Q", N1q="N1", N1k="N1", N1="N1", X1="X", X="X")
+        for name, src in of.items():
+            shp = next(q["shape"] for q in pts if q["id"] == ids[src])
+            pts.append(_pt(g[name], shp, "gradient", e, ids[src]))
+        gw = {k: 130 + v for k, v in dict(Wq=0, Wk=1, Wo=2, W1=3, W2=4).items()}
+        nw = {k: 140 + v for k, v in dict(Wq=0, Wk=1, Wo=2, W1=3, W2=4).items()}
+        for w, shp in (("Wq", (H, H)), ("Wk", (H, H)), ("Wo", (H, H)), ("W1", (H, Fd)), ("W2", (Fd, H))):
+            pts.append(_pt(gw[w], shp, "gradient", e, ids[w]))
+            pts.append(_pt(nw[w], shp, "weight", e))
+        B = {"layer": 0}
+        TA = dict(B, transpose_a=True)
+        TB = dict(B, transpose_b=True)
+        ops += [
+            _op("gres2", "identity", [g["OUT"]], [g["Y"]], "backward", 0, B, "res2"),
+            _op("gw2a", "matmul", [g["Y"], ids["W2"]], [g["Fa"]], "backward", mm(T, Fd, H), TB, "roww2"),
+            _op("gw2w", "matmul", [ids["Fa"], g["Y"]], [gw["W2"]], "backward", mm(Fd, H, T), TA, "roww2"),
+            _op("ggelu", "gelu-grad", [ids["F1"], g["Fa"]], [g["F1"]], "backward", 8 * T * Fd, B, "tpgelu"),
+            _op("gf1a", "matmul", [g["F1"], ids["W1"]], [g["N2"]], "backward", mm(T, H, Fd), TB, "colf1"),
+            _op("gf1w", "matmul", [ids["N2"], g["F1"]], [gw["W1"]], "backward", mm(H, Fd, T), TA, "colf1"),
+            _op("gln2", "layernorm-grad", [ids["X2"], g["N2"]], [g["X2a"]], "backward", 8 * T * H, B, "ln2"),
+            _op("gres2x", "add", [g["X2a"], g["OUT"]], [g["X2"]], "backward", T * H, B, "res2"),
+            _op("gres1", "identity", [g["X2"]], [g["O"]], "backward", 0, B, "res1"),
+            _op("gwoa", "matmul", [g["O"], ids["Wo"]], [g["S"]], "backward", mm(T, H, H), TB, "rowo"),
+            _op("gwow", "matmul", [ids["S"], g["O"]], [gw["Wo"]], "backward", mm(H, H, T), TA, "rowo"),
+            _op("gmulp", "mul", [g["S"], ids["K"]], [g["P"]], "backward", T * H, B, "tpmul"),
+            _op("gmulk", "mul", [g["S"], ids["P"]], [g["K"]], "backward", T * H, B, "tpmul"),
+            _op("gsm", "softmax-grad", [ids["P"], g["P"]], [g["Q"]], "backward", 8 * T * H, dict(B, segment=head),
+                "tpsm"),
+            _op("gqa", "matmul", [g["Q"], ids["Wq"]], [g["N1q"]], "backward", mm(T, H, H), TB, "colq"),
+            _op("gqw", "matmul", [ids["N1"], g["Q"]], [gw["Wq"]], "backward", mm(H, H, T), TA, "colq"),
+            _op("gka", "matmul", [g["K"], ids["Wk"]], [g["N1k"]], "backward", mm(T, H, H), TB, "colk"),
+            _op("gkw", "matmul", [ids["N1"], g["K"]], [gw["Wk"]], "backward", mm(H, H, T), TA, "colk"),
+            _op("gln1s", "add", [g["N1q"], g["N1k"]], [g["N1"]], "backward", T * H, B, "ln1"),
+            _op("gln1", "layernorm-grad", [ids["X"], g["N1"]], [g["X1"]], "backward", 8 * T * H, B, "ln1"),
+            _op("gres1x", "add", [g["X1"], g["X2"]], [g["X"]], "backward", T * H, B, "res1"),
+        ]
+        for w, kind in (("Wq", "optc"), ("Wk", "optc"), ("W1", "optc"), ("Wo", "optr"), ("W2", "optr")):
+            shp = next(q["shape"] for q in pts if q["id"] == ids[w])
+            ops.append(_op(kind + w.lower(), "add", [ids[w], gw[w]], [nw[w]], "optimizer", shp[0] * shp[1], B))
+    return {"ptensors": pts, "ops": ops}
+
+
+def standin_doc(doc: dict) -> dict:
+    """The document the reference front end accepts: extended kinds replaced
+    by their stand-ins (same operands, same partitioning behaviour)."""
+    out = json.loads(json.dumps(doc))
+    for op in out["ops"]:
+        if op["kind"] in EXT_STANDIN:
+            op["kind"] = EXT_STANDIN[op["kind"]]
+            op.get("attrs", {}).pop("segment", None)
+    return out
+
+
+def rewrite_plan(plan_json: str, doc: dict) -> str:
+    """Writes the extended kinds (and their segment / eps) back into a plan
+    compiled from standin_doc(doc)."""
+    ext = {op["id"]: op for op in doc["ops"] if op["kind"] in EXT_STANDIN}
+    p = json.loads(plan_json)
+    n = 0
+    for op in p["ops"]:
+        base = op["id"].split("/")[0].split("~")[0]
+        if base in ext:
+            src = ext[base]
+            op["kind"] = src["kind"]
+            attrs = src.get("attrs", {})
+            if attrs.get("segment"):
+                op["segment"] = attrs["segment"]
+            if "eps" in attrs:
+                op["eps"] = attrs["eps"]
+            n += 1
+    if n == 0:
+        raise ValueError("rewrite_plan: no extended op found in the plan")
+    return json.dumps(p)

@@ -24,6 +24,18 @@ off by default so the restatement is bit-compatible with the reference:
 
 Parity pinning: tests/test_oracle.py checks this module against the compiled
 reference (oracle/_ref) and the golden fixtures in tests/golden/.
+
+Schema extension (NOT part of the reference, whose
+document.cpp:43-53 rejects these kinds): row-wise sub-operators of a
+transformer block over the last axis, in segments of ``segment`` elements
+(default: the whole last axis) — ``softmax`` / ``softmax-grad`` (per
+attention head when segment = head width), ``layernorm`` / ``layernorm-grad``
+(no affine, ``eps`` default 1e-5, population variance) and elementwise
+``gelu`` / ``gelu-grad`` (erf form). ``eval_ext`` restates them in float64;
+``run_graph`` evaluates a graph document op by op (the run_reference shape,
+refexec.cpp:264-350) for the extended vocabulary. Parity of these kinds is
+pinned against torch's float64 implementations (tests/test_ext_oracle.py),
+not against the reference, which has none.
 """
 from __future__ import annotations
 
@@ -140,7 +152,96 @@ def eval_compute(op, ins, in_masks, out_masks):
         return [out]
     if kind == "identity":
         return [ins[0].copy()]
+    if kind in EXT_KINDS:
+        return [eval_ext(kind, ins, op.get("segment", 0), op.get("eps", 1e-5), in_masks)]
     raise UsageError(f"refexec: unsupported op kind {kind} ({op['id']})")
+
+
+EXT_KINDS = ("softmax", "softmax-grad", "layernorm", "layernorm-grad", "gelu", "gelu-grad")
+
+
+def _erf(x):
+    try:
+        from scipy.special import erf
+
+        return erf(x)
+    except ImportError:  # pragma: no cover
+        import math
+
+        return np.vectorize(math.erf)(x)
+
+
+def eval_ext(kind, ins, segment=0, eps=1e-5, in_masks=None):
+    """Extended kinds in float64. Row-wise kinds work on segments of
+    ``segment`` elements of the last axis (0 = the whole last axis); a piece
+    must hold whole segments (its last-axis region aligned to the segment)."""
+    x = np.asarray(ins[0], dtype=np.float64)
+    if kind == "gelu":
+        return 0.5 * x * (1.0 + _erf(x / np.sqrt(2.0)))
+    if kind == "gelu-grad":  # ins = (x, dy)
+        dy = np.asarray(ins[1], dtype=np.float64)
+        cdf = 0.5 * (1.0 + _erf(x / np.sqrt(2.0)))
+        pdf = np.exp(-0.5 * x * x) / np.sqrt(2.0 * np.pi)
+        return dy * (cdf + x * pdf)
+    n = x.shape[-1]
+    seg = segment or n
+    if n % seg != 0:
+        raise UsageError(f"{kind}: last-axis extent {n} is not a multiple of the segment {seg}")
+    if in_masks is not None and segment and in_masks[0]["region"][-1][0] % seg != 0:
+        raise UsageError(f"{kind}: piece does not start on a segment boundary")
+    shp = x.shape
+    xs = x.reshape(-1, seg)
+    if kind == "softmax":
+        e = np.exp(xs - xs.max(axis=1, keepdims=True))
+        return (e / e.sum(axis=1, keepdims=True)).reshape(shp)
+    if kind == "softmax-grad":  # ins = (y, dy)
+        dy = np.asarray(ins[1], dtype=np.float64).reshape(-1, seg)
+        return (xs * (dy - (dy * xs).sum(axis=1, keepdims=True))).reshape(shp)
+    mean = xs.mean(axis=1, keepdims=True)
+    var = ((xs - mean) ** 2).mean(axis=1, keepdims=True)
+    rstd = 1.0 / np.sqrt(var + eps)
+    xhat = (xs - mean) * rstd
+    if kind == "layernorm":
+        return xhat.reshape(shp)
+    if kind == "layernorm-grad":  # ins = (x, dy)
+        dy = np.asarray(ins[1], dtype=np.float64).reshape(-1, seg)
+        return (rstd * (dy - dy.mean(axis=1, keepdims=True) - xhat * (dy * xhat).mean(axis=1, keepdims=True))
+                ).reshape(shp)
+    raise UsageError(f"unsupported extended kind {kind}")
+
+
+def bf16_round(x):
+    """Round-to-nearest-even to bfloat16, returned as float64."""
+    a = np.ascontiguousarray(x, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16 << 16
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def run_graph(doc, inputs, round_bf16=False):
+    """Graph-level evaluation (the shape of run_reference, refexec.cpp:264-350)
+    for documents using the extended kinds: every op in document order on
+    whole pTensors; returns every produced pTensor. ``round_bf16``: outputs of
+    2-byte pTensors are rounded to bfloat16 (the executor's storage points),
+    each op computing in float64 from rounded operands."""
+    g = json.loads(doc) if isinstance(doc, str) else doc
+    vals = {int(k): np.asarray(v, dtype=np.float64) for k, v in inputs.items()}
+    shapes = {p["id"]: tuple(p["shape"]) for p in g["ptensors"]}
+    half = {p["id"] for p in g["ptensors"] if p["elem_size"] == 2}
+    out = {}
+    for op in g["ops"]:
+        attrs = dict(op.get("attrs", {}))
+        o = dict(op, **attrs)
+        ins = [vals[i] for i in op["inputs"]]
+        masks = [{"region": [[0, e] for e in shapes[i]], "value": [0, 1]} for i in op["inputs"]]
+        omasks = [{"region": [[0, e] for e in shapes[i]], "value": [0, 1]} for i in op["outputs"]]
+        res = eval_compute(o, ins, masks, omasks)
+        for pid, v in zip(op["outputs"], res):
+            vals[pid] = v.reshape(shapes[pid])
+            if round_bf16 and pid in half:
+                vals[pid] = bf16_round(vals[pid])
+            out[pid] = vals[pid]
+    return out
 
 
 class Plan:

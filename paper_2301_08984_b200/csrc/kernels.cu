@@ -606,6 +606,207 @@ void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s) {
   check_launch("zero_kernel");
 }
 
+namespace {
+
+// ---- schema extension: row-wise sub-operators and GELU ----------------------
+// One warp per segment; every lane walks the segment in 16-byte vectors
+// (V elements) with fp32 statistics merged by warp shuffles, then a second
+// (and, for layernorm-grad, third) pass re-reads the segment — from L1/L2,
+// the segment being a few KB — and writes. HBM traffic: inputs once, output
+// once.
+
+constexpr int kRowWarps = 8;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T, int OP, int V>
+__global__ void __launch_bounds__(kRowWarps * 32) row_kernel(const T* __restrict__ a, const T* __restrict__ b,
+                                                             T* __restrict__ out, long long nseg, int seg, float eps) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
+  const int lane = threadIdx.x % 32;
+  const long long sidx = blockIdx.x * static_cast<long long>(kRowWarps) + threadIdx.x / 32;
+  if (sidx >= nseg) return;
+  const long long base = sidx * seg;
+  const T* x = a + base;
+  const T* dy = b ? b + base : nullptr;
+  T* o = out + base;
+  const int nv = seg / V;  // vectors per segment
+  float xv[V], gv[V], ov[V];
+  if constexpr (OP == 0) {  // softmax: online max / sum, then write
+    float m = -INFINITY, sm = 0.f;
+    for (int i = lane; i < nv; i += 32) {
+      load_vec<T, V>(x + i * V, xv);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        if (xv[e] > m) {
+          sm = sm * expf(m - xv[e]) + 1.f;
+          m = xv[e];
+        } else {
+          sm += expf(xv[e] - m);
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, off), s2 = __shfl_xor_sync(0xffffffffu, sm, off);
+      const float mm = fmaxf(m, m2);
+      sm = (sm > 0.f ? sm * expf(m - mm) : 0.f) + (s2 > 0.f ? s2 * expf(m2 - mm) : 0.f);
+      m = mm;
+    }
+    const float inv = 1.f / sm;
+    for (int i = lane; i < nv; i += 32) {
+      load_vec<T, V>(x + i * V, xv);
+#pragma unroll
+      for (int e = 0; e < V; ++e) ov[e] = expf(xv[e] - m) * inv;
+      store_vec<T, V>(o + i * V, ov);
+    }
+  } else if constexpr (OP == 1) {  // softmax-grad: dx = y * (dy - sum(dy * y))
+    float dot = 0.f;
+    for (int i = lane; i < nv; i += 32) {
+      load_vec<T, V>(x + i * V, xv);
+      load_vec<T, V>(dy + i * V, gv);
+#pragma unroll
+      for (int e = 0; e < V; ++e) dot += xv[e] * gv[e];
+    }
+    dot = warp_sum(dot);
+    for (int i = lane; i < nv; i += 32) {
+      load_vec<T, V>(x + i * V, xv);
+      load_vec<T, V>(dy + i * V, gv);
+#pragma unroll
+      for (int e = 0; e < V; ++e) ov[e] = xv[e] * (gv[e] - dot);
+      store_vec<T, V>(o + i * V, ov);
+    }
+  } else {  // layernorm / layernorm-grad: Welford statistics (Chan merge across lanes)
+    float cnt = 0.f, mean = 0.f, m2 = 0.f;
+    for (int i = lane; i < nv; i += 32) {
+      load_vec<T, V>(x + i * V, xv);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        cnt += 1.f;
+        const float d = xv[e] - mean;
+        mean += d / cnt;
+        m2 += d * (xv[e] - mean);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float c2 = __shfl_xor_sync(0xffffffffu, cnt, off), mn2 = __shfl_xor_sync(0xffffffffu, mean, off),
+                  q2 = __shfl_xor_sync(0xffffffffu, m2, off);
+      const float c = cnt + c2;
+      if (c > 0.f) {
+        const float d = mn2 - mean;
+        mean += d * (c2 / c);
+        m2 += q2 + d * d * (cnt * c2 / c);
+      }
+      cnt = c;
+    }
+    const float rstd = rsqrtf(m2 / static_cast<float>(seg) + eps);
+    if constexpr (OP == 2) {
+      for (int i = lane; i < nv; i += 32) {
+        load_vec<T, V>(x + i * V, xv);
+#pragma unroll
+        for (int e = 0; e < V; ++e) ov[e] = (xv[e] - mean) * rstd;
+        store_vec<T, V>(o + i * V, ov);
+      }
+    } else {  // dx = rstd * (dy - mean(dy) - xhat * mean(dy * xhat))
+      float sdy = 0.f, sdx = 0.f;
+      for (int i = lane; i < nv; i += 32) {
+        load_vec<T, V>(x + i * V, xv);
+        load_vec<T, V>(dy + i * V, gv);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          sdy += gv[e];
+          sdx += gv[e] * (xv[e] - mean) * rstd;
+        }
+      }
+      const float inv_n = 1.f / static_cast<float>(seg);
+      const float mdy = warp_sum(sdy) * inv_n, mdx = warp_sum(sdx) * inv_n;
+      for (int i = lane; i < nv; i += 32) {
+        load_vec<T, V>(x + i * V, xv);
+        load_vec<T, V>(dy + i * V, gv);
+#pragma unroll
+        for (int e = 0; e < V; ++e) ov[e] = rstd * (gv[e] - mdy - (xv[e] - mean) * rstd * mdx);
+        store_vec<T, V>(o + i * V, ov);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_grad_f(float x, float g) {
+  const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
+  const float pdf = expf(-0.5f * x * x) * 0.39894228040143268f;
+  return g * (cdf + x * pdf);
+}
+
+template <typename T, int OP, int V>
+__global__ void __launch_bounds__(256) act_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out,
+                                                  long long count) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
+  const long long nvec = count / V;
+  float xv[V], gv[V], ov[V];
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    load_vec<T, V>(a + i * V, xv);
+    if constexpr (OP == 5) load_vec<T, V>(b + i * V, gv);
+#pragma unroll
+    for (int e = 0; e < V; ++e) ov[e] = OP == 4 ? gelu_f(xv[e]) : gelu_grad_f(xv[e], OP == 5 ? gv[e] : 0.f);
+    store_vec<T, V>(out + i * V, ov);
+  }
+  // scalar tail (count % V elements)
+  const long long t = nvec * V + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x < count - nvec * V) {
+    const float x0 = to_acc<T>(a[t]);
+    out[t] = from_acc<T>(OP == 4 ? gelu_f(x0) : gelu_grad_f(x0, OP == 5 ? to_acc<T>(b[t]) : 0.f));
+  }
+}
+
+template <typename T>
+void rowwise_typed(int op, const void* a, const void* b, void* out, std::int64_t count, std::int64_t seg, float eps,
+                   cudaStream_t s) {
+  constexpr int VV = 16 / sizeof(T);
+  const T* A = static_cast<const T*>(a);
+  const T* B = static_cast<const T*>(b);
+  T* O = static_cast<T*>(out);
+  if (op == 4 || op == 5) {
+    const long long nvec = count / VV;
+    const dim3 g(grid_for(std::max<long long>(nvec, 1), 256 * 4));
+    if (op == 4) pdl_launch("act_kernel", act_kernel<T, 4, VV>, g, dim3(256), 0, s, A, B, O, (long long)count);
+    else pdl_launch("act_kernel", act_kernel<T, 5, VV>, g, dim3(256), 0, s, A, B, O, (long long)count);
+    return;
+  }
+  if (seg <= 0 || count % seg != 0 || seg > (1 << 30)) throw std::runtime_error("rowwise: bad segment");
+  const long long nseg = count / seg;
+  const dim3 g(static_cast<unsigned>((nseg + kRowWarps - 1) / kRowWarps));
+  const dim3 blk(kRowWarps * 32);
+  const int sg = static_cast<int>(seg);
+#define PLANC_ROW(OPV, V) pdl_launch("row_kernel", row_kernel<T, OPV, V>, g, blk, 0, s, A, B, O, nseg, sg, eps)
+  const bool vec = seg % VV == 0;
+  switch (op) {
+    case 0: if (vec) PLANC_ROW(0, VV); else PLANC_ROW(0, 1); break;
+    case 1: if (vec) PLANC_ROW(1, VV); else PLANC_ROW(1, 1); break;
+    case 2: if (vec) PLANC_ROW(2, VV); else PLANC_ROW(2, 1); break;
+    default: if (vec) PLANC_ROW(3, VV); else PLANC_ROW(3, 1); break;
+  }
+#undef PLANC_ROW
+}
+
+}  // namespace
+
+void launch_rowwise(int op, int dtype, const void* a, const void* b, void* out, std::int64_t count, std::int64_t seg,
+                    float eps, cudaStream_t s) {
+  if (count == 0) return;
+  if (dtype == DT_BF16) rowwise_typed<__nv_bfloat16>(op, a, b, out, count, seg, eps, s);
+  else if (dtype == DT_F32) rowwise_typed<float>(op, a, b, out, count, seg, eps, s);
+  else throw std::runtime_error("rowwise: element type must be fp32 or bf16");
+}
+
 // ---- peer-memory flags ------------------------------------------------------
 
 __global__ void peer_epoch_kernel(unsigned* epoch) {

@@ -139,6 +139,12 @@ void launch_emb_lookup(int dtype, const int* idx, const void* table, void* out, 
 void launch_emb_grad(int dtype, const int* idx, const void* gout, void* out, float* scratch, std::int64_t n,
                      std::int64_t rows, std::int64_t h, std::int64_t lo, cudaStream_t s);
 void launch_gemm_simt(const GemmArgs& a, cudaStream_t s);
+// Schema extension (program.hpp RowOp): softmax / softmax_grad / layernorm /
+// layernorm_grad over `count / seg` contiguous segments of `seg` elements
+// (one warp per segment, fp32 statistics, 16-byte vectors), gelu / gelu_grad
+// elementwise. `b` is the second operand (dy) of the *_grad ops.
+void launch_rowwise(int op, int dtype, const void* a, const void* b, void* out, std::int64_t count, std::int64_t seg,
+                    float eps, cudaStream_t s);
 void launch_convert(int dtype_out, void* out, const float* in, std::int64_t count, cudaStream_t s);
 void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s);
 

@@ -51,6 +51,12 @@ const char* op_kind_name(OpKind k) {
     case OpKind::recv: return "recv";
     case OpKind::collective: return "collective";
     case OpKind::free_buffer: return "free";
+    case OpKind::softmax: return "softmax";
+    case OpKind::softmax_grad: return "softmax-grad";
+    case OpKind::layernorm: return "layernorm";
+    case OpKind::layernorm_grad: return "layernorm-grad";
+    case OpKind::gelu: return "gelu";
+    case OpKind::gelu_grad: return "gelu-grad";
   }
   return "?";
 }
@@ -65,7 +71,10 @@ OpKind op_kind_from_doc(const std::string& s) {
       {"embedding-lookup", OpKind::embedding_lookup}, {"embedding-grad", OpKind::embedding_grad},
       {"identity", OpKind::identity}, {"split", OpKind::split}, {"concat", OpKind::concat},
       {"reduce-assemble", OpKind::reduce_assemble}, {"send", OpKind::send}, {"recv", OpKind::recv},
-      {"collective", OpKind::collective}, {"free", OpKind::free_buffer}};
+      {"collective", OpKind::collective}, {"free", OpKind::free_buffer},
+      // schema extension (oracle/planc_oracle.py eval_ext)
+      {"softmax", OpKind::softmax}, {"softmax-grad", OpKind::softmax_grad}, {"layernorm", OpKind::layernorm},
+      {"layernorm-grad", OpKind::layernorm_grad}, {"gelu", OpKind::gelu}, {"gelu-grad", OpKind::gelu_grad}};
   auto it = m.find(s);
   if (it == m.end()) throw SchemaError("plan document: unknown op kind " + s);
   return it->second;
@@ -188,6 +197,9 @@ ExecutionPlan load_plan(const std::string& document) {
       if (o.contains("coll_group")) op.coll_group = static_cast<int>(o.at("coll_group").as_int());
       if (o.contains("free_vtensor")) op.free_vtensor = static_cast<int>(o.at("free_vtensor").as_int());
       if (o.contains("primitive")) op.primitive = o.at("primitive").as_string();
+      if (o.contains("segment")) op.segment = o.at("segment").as_int();
+      if (o.contains("eps")) op.eps = o.at("eps").as_double();
+      if (op.segment < 0 || !(op.eps >= 0)) throw SchemaError("plan document: bad segment / eps on op " + op.id);
       plan.ops.push_back(std::move(op));
     }
     for (const auto& kv : j.at("assignment").obj) {

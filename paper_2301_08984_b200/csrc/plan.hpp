@@ -78,6 +78,10 @@ struct VTensor {
 enum class OpKind {
   matmul, ew_add, ew_mul, ew_max, reduce_sum, embedding_lookup, embedding_grad, identity,
   split, concat, reduce_assemble, send, recv, collective, free_buffer,
+  // Schema extension (not in the reference: document.cpp:43-53 rejects
+  // them): row-wise transformer sub-operators over the last axis in
+  // segments of `segment` elements (0 = the whole axis), and GELU.
+  softmax, softmax_grad, layernorm, layernorm_grad, gelu, gelu_grad,
 };
 const char* op_kind_name(OpKind k);
 
@@ -98,6 +102,8 @@ struct OpNode {
   int coll_group = -1;
   int free_vtensor = -1;
   std::string primitive;
+  std::int64_t segment = 0;  // extension: row-wise segment width (0 = whole last axis)
+  double eps = 1e-5;         // extension: layernorm epsilon
 
   bool is_elementwise() const {
     return kind == OpKind::ew_add || kind == OpKind::ew_mul || kind == OpKind::ew_max;

@@ -29,6 +29,7 @@ const char* instr_kind_name(InstrKind k) {
     case InstrKind::box: return "box";
     case InstrKind::xfer: return "xfer";
     case InstrKind::nop: return "nop";
+    case InstrKind::rowwise: return "rowwise";
   }
   return "?";
 }
@@ -453,6 +454,57 @@ struct Builder {
         pieces.push_back({&src, ib[0]});
         emit_box(op_idx, op, lane, 0, op.outputs[0], pieces, "op " + op.id);
         P.instrs.back().label = op.id;
+        break;
+      }
+      case OpKind::softmax:
+      case OpKind::softmax_grad:
+      case OpKind::layernorm:
+      case OpKind::layernorm_grad:
+      case OpKind::gelu:
+      case OpKind::gelu_grad: {
+        // Schema extension (oracle/planc_oracle.py eval_ext).
+        const bool binary = op.kind == OpKind::softmax_grad || op.kind == OpKind::layernorm_grad ||
+                            op.kind == OpKind::gelu_grad;
+        if (ib.size() != (binary ? 2u : 1u) || op.outputs.size() != 1) throw InternalError("arity in " + op.id);
+        int ob = out_buffer(op.outputs[0], lane);
+        for (int b : ib)
+          if (shape_of(b) != shape_of(ob)) throw InternalError("operand shape mismatch in " + op.id);
+        Instr& in = emit(InstrKind::rowwise, lane, 0, op_idx, op.id);
+        in.in_bufs = ib;
+        in.out_bufs = {ob};
+        in.count = P.buffers[ob].elems;
+        in.row_op = op.kind == OpKind::softmax          ? RowOp::softmax
+                    : op.kind == OpKind::softmax_grad   ? RowOp::softmax_grad
+                    : op.kind == OpKind::layernorm      ? RowOp::layernorm
+                    : op.kind == OpKind::layernorm_grad ? RowOp::layernorm_grad
+                    : op.kind == OpKind::gelu           ? RowOp::gelu
+                                                        : RowOp::gelu_grad;
+        in.eps = op.eps;
+        const auto sh = shape_of(ob);
+        const std::int64_t n = sh.empty() ? 1 : sh.back();
+        if (in.row_op != RowOp::gelu && in.row_op != RowOp::gelu_grad) {
+          // Segments of the pTensor's last axis; a piece holds whole segments.
+          const PTensor& pt = plan.pt(plan.vt(op.outputs[0]).ptensor);
+          const std::int64_t full = pt.shape.empty() ? 1 : pt.shape.back();
+          in.seg = op.segment > 0 ? op.segment : full;
+          const Region& r = plan.vt(op.outputs[0]).mask.region;
+          const std::int64_t lo = r.empty() ? 0 : r.back().lo;
+          if (n % in.seg != 0 || lo % in.seg != 0 || full % in.seg != 0) {
+            throw UsageError(std::string(op_kind_name(op.kind)) + " " + op.id +
+                             ": the piece's last-axis region does not hold whole segments of " +
+                             std::to_string(in.seg));
+          }
+          for (int v : op.inputs) {
+            const Region& ri = plan.vt(v).mask.region;
+            if (!ri.empty() && ri.back().lo % in.seg != 0) {
+              throw UsageError(std::string(op_kind_name(op.kind)) + " " + op.id + ": input piece not segment-aligned");
+            }
+          }
+        }
+        const std::int64_t es = dtype_size(P.buffers[ob].dtype);
+        in.bytes = static_cast<double>(in.count) * es * (ib.size() + 1);
+        in.flops = static_cast<double>(in.count) * 8;
+        finish_deps(in);
         break;
       }
       default:
@@ -1326,7 +1378,8 @@ std::string Program::describe_json() const {
     os << "],\"m\":" << in.m << ",\"n\":" << in.n << ",\"k\":" << in.k << ",\"ta\":" << in.ta << ",\"tb\":" << in.tb
        << ",\"ew\":" << static_cast<int>(in.ew) << ",\"count\":" << in.count << ",\"outer\":" << in.outer
        << ",\"axis_len\":" << in.axis_len << ",\"inner\":" << in.inner << ",\"n_idx\":" << in.n_idx
-       << ",\"rows\":" << in.rows << ",\"h\":" << in.h << ",\"lo\":" << in.lo << ",\"flops\":" << in.flops
+       << ",\"rows\":" << in.rows << ",\"h\":" << in.h << ",\"lo\":" << in.lo << ",\"row_op\":"
+       << static_cast<int>(in.row_op) << ",\"seg\":" << in.seg << ",\"eps\":" << in.eps << ",\"flops\":" << in.flops
        << ",\"bytes\":" << in.bytes << ",\"wire_bytes\":" << in.wire_bytes << ",\"coll_group\":" << in.coll_group
        << ",\"allreduce\":" << (in.allreduce ? "true" : "false") << ",\"group\":" << in.group << ",\"fused\":[";
     for (std::size_t f = 0; f < in.fused.size(); ++f) {

@@ -75,7 +75,10 @@ struct Cell {
 
 constexpr int kMaxGemmGroupInstr = 8;  // members of one grouped GEMM launch (kernels.cuh kMaxGemmGroup)
 
-enum class InstrKind { gemm, ew, reduce, emb_lookup, emb_grad, box, xfer, nop };
+enum class InstrKind { gemm, ew, reduce, emb_lookup, emb_grad, box, xfer, nop, rowwise };
+
+// Row-wise / activation sub-operators of the schema extension.
+enum class RowOp { softmax = 0, softmax_grad = 1, layernorm = 2, layernorm_grad = 3, gelu = 4, gelu_grad = 5 };
 
 // One cross-rank piece movement of an exchange step (one-process-per-GPU
 // mode): the whole `src` buffer of lane src_lane lands in `dst` (a shadow
@@ -112,6 +115,11 @@ struct Instr {
   std::int64_t outer = 0, axis_len = 0, inner = 0;
   // embedding: idx[n_idx], table/grad rows, width h, vocab offset lo
   std::int64_t n_idx = 0, rows = 0, h = 0, lo = 0;
+  // rowwise: `count` elements = count / seg segments of `seg` contiguous
+  // elements (gelu / gelu_grad: seg unused); in_bufs = x (or y) [, dy]
+  RowOp row_op = RowOp::softmax;
+  std::int64_t seg = 0;
+  double eps = 0;
   // box
   std::vector<Cell> cells;
   int coll_group = -1;  // collective group a box instruction belongs to

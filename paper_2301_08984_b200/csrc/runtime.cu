@@ -258,8 +258,11 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   }
   // Element types must agree across an elementwise op's operands.
   for (const auto& in : prog_.instrs) {
-    if (in.kind == InstrKind::ew) {
+    if (in.kind == InstrKind::ew || in.kind == InstrKind::rowwise) {
       DType d = prog_.buffers[in.out_bufs[0]].dtype;
+      if (in.kind == InstrKind::rowwise && d == DType::i32) {
+        throw UsageError("op " + plan_.ops[in.op].id + ": row-wise operators need fp32 or bf16 tensors");
+      }
       for (int b : in.in_bufs) {
         if (prog_.buffers[b].dtype != d) {
           throw UsageError("elementwise op " + plan_.ops[in.op].id + " mixes element sizes");
@@ -783,6 +786,11 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
                       buf_ptr(in.in_bufs[1]), buf_ptr(in.out_bufs[0]), irt_[in.id].scratch, in.n_idx, in.rows, in.h,
                       in.lo, s);
       return;
+    case InstrKind::rowwise:
+      launch_rowwise(static_cast<int>(in.row_op), dt_of(prog_.buffers[in.out_bufs[0]].dtype), buf_ptr(in.in_bufs[0]),
+                     in.in_bufs.size() > 1 ? buf_ptr(in.in_bufs[1]) : nullptr, buf_ptr(in.out_bufs[0]), in.count, in.seg,
+                     static_cast<float>(in.eps), s);
+      return;
     case InstrKind::box: {
       int dt = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
       for (const auto& bl : irt_[in.id].box) {
@@ -1151,6 +1159,7 @@ std::vector<KernelStat> Executor::profile() {
         break;
       }
       case InstrKind::ew: kind = "ew"; break;
+      case InstrKind::rowwise: kind = "rowwise"; break;
       case InstrKind::reduce: kind = "reduce"; break;
       case InstrKind::emb_lookup:
       case InstrKind::emb_grad: kind = "embedding"; break;

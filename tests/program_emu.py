@@ -88,6 +88,13 @@ def run_program(desc: dict, plan: dict, inputs: dict, owned_lanes=None, exchange
                 if ins["lo"] <= idx[j] < ins["lo"] + ins["rows"]:
                     out[idx[j] - ins["lo"]] += g[j]
             data[ins["out"][0]] = out.reshape(-1)
+        elif k == "rowwise":  # schema extension: row-wise sub-operators / GELU
+            from oracle import planc_oracle as po
+
+            names = ["softmax", "softmax-grad", "layernorm", "layernorm-grad", "gelu", "gelu-grad"]
+            seg = ins["seg"] if ins["row_op"] < 4 else 1
+            xs = [data[b].reshape(-1, seg) for b in ins["in"]]
+            data[ins["out"][0]] = po.eval_ext(names[ins["row_op"]], xs, seg, ins["eps"]).reshape(-1)
         elif k == "box":
             ob = ins["out"][0]
             out = data[ob].copy()  # a box writes only its cells (two-phase all-reduce: two boxes per output)
