@@ -46,7 +46,7 @@ def plan_name(config: str, n: int) -> str:
     """c2 / c1l plans are compiled per GPU count (TP / DP degree n); the
     pipeline (c3: 8 lanes), co-shard (c4: 1 lane) and 3F1B (c5: 2 lanes)
     plans have a fixed lane count — with fewer GPUs, lanes share GPUs."""
-    return {"c2": f"c2_tp{n}", "c1l": f"c1l_dp{n}", "c3": "c3_pp4dp2", "c4": "c4_coshard4",
+    return {"c2": f"c2_tp{n}", "c2x": f"c2x_tp{n}", "c1l": f"c1l_dp{n}", "c3": "c3_pp4dp2", "c4": "c4_coshard4",
             "c5": "c5_3f1b"}[config]
 
 
@@ -160,6 +160,12 @@ def cpu_baseline(config: str, budget_s: float = 20.0):
     from oracle import refpy  # checker / baseline only
 
     name = plan_name(config, 1) + "_cpu"
+    note = ""
+    if config == "c2x":
+        # The reference executor has no layernorm / softmax / GELU: it runs the
+        # stand-in plan (identity / mul in their place, same data flow).
+        name += "_standin"
+        note = "; stand-in plan: identity/mul where the extension has LN/softmax/GELU"
     plan, meta = load_plan(name)
     inputs = synthetic_inputs(plan, 1)
     _, secs = refpy.run_plan(plan, inputs, iters=1)
@@ -169,7 +175,7 @@ def cpu_baseline(config: str, budget_s: float = 20.0):
     shape = f"T={meta.get('tokens', meta.get('batch'))},H={meta['hidden']}"
     return dict(value=sps, unit="samples/s", cores=1, kind="reference",
                 sample=f"{iters} x run_plan of {name} ({shape}, same graph at reduced shape; "
-                       f"{secs:.3f} s/step, single-threaded reference executor)"), secs
+                       f"{secs:.3f} s/step, single-threaded reference executor{note})"), secs
 
 
 def run_reference_arm(args, rank, world):
@@ -192,7 +198,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c2", "c1l", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c2x", "c1l", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
@@ -359,8 +365,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (integer-valued inputs in {-1,0,1})",
             "config": {"workload": name, "config": args.config, "plan": f"plans/{name}.plan.json",
-                       "shape": {k: meta[k] for k in ("tokens", "batch", "hidden", "middle", "layers") if k in meta},
-                       "parallelism": {"c2": f"tp{n}", "c1l": f"dp{n}", "c3": "pp4 x dp2 (1F1B, K=8)",
+                       "shape": {k: meta[k] for k in ("tokens", "batch", "hidden", "middle", "layers", "head") if k in meta},
+                       "parallelism": {"c2": f"tp{n}", "c2x": f"tp{n}", "c1l": f"dp{n}", "c3": "pp4 x dp2 (1F1B, K=8)",
                                        "c4": "co-shard x4", "c5": "3F1B pp2 (K=4)"}[args.config],
                        "lanes_per_gpu": nlanes / max(n, 1),
                        "sample": meta["sample"], "l2": "step working set " +

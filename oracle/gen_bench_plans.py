@@ -9,10 +9,16 @@ box has no reference. Shapes follow SURVEY.md §8d:
        T=8192 tokens (4 seq x 2048), H=2048, FFN=4H, bf16,
        Megatron TP = 1/2/4/8 (megatron_tp sProgram)
   c1l  2-layer MLP (reference mlp_doc) B=16384, H=4096, bf16, DP = 1/2/4/8
+  c2x  the schema-extension transformer block (docs.gpt_block_ext_doc: LN,
+       per-head softmax, GELU and their gradients), T=8192, H=2048, 16 heads
+       of 128, bf16, Megatron TP = 1/2/4/8 — compiled by the reference front
+       end on the stand-in document and rewritten (docs.rewrite_plan); the
+       *_cpu_standin plan keeps the stand-ins so the reference CPU executor
+       (which has no LN / softmax / GELU) can be timed on the same data flow
   *_cpu  the same graphs at the reduced shape the CPU executor can run
        (T=H=128; SURVEY §8d "CPU baseline")
 
-Run:  python oracle/gen_bench_plans.py
+Run:  python oracle/gen_bench_plans.py [config ...]   (default: all)
 """
 from __future__ import annotations
 
@@ -49,8 +55,29 @@ def write(name, graph, plan, meta):
     print(name, meta["lanes"], meta["tasks"], meta["collectives"])
 
 
+def gen_c2x():
+    for T, H, hd, tag in ((8192, 2048, 128, ""), (128, 128, 32, "_cpu")):
+        doc = docs.gpt_block_ext_doc(T, H, hd, elem_size=2, train=True)
+        stand = docs.dumps(docs.standin_doc(doc))
+        meta = dict(config="c2x", tokens=T, hidden=H, head=hd, dtype="bf16", samples_per_step=T,
+                    sample="token (row of X)", extension=True)
+        for k in (1, 2, 4, 8):
+            if tag and k > 1:
+                continue
+            plan = refpy.compile_plan(stand, strategy="megatron_tp", devices=k)
+            write(f"c2x_tp{k}{tag}", docs.dumps(doc), docs.rewrite_plan(plan, doc), dict(meta, tp=k))
+            if tag:
+                write(f"c2x_tp{k}{tag}_standin", stand, plan, dict(meta, tp=k, standin=True))
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    only = set(sys.argv[1:])
+    if only:
+        if "c2x" in only:
+            gen_c2x()
+        return
+    gen_c2x()
     for T, H, tag in ((8192, 2048, ""), (128, 128, "_cpu")):
         g = docs.dumps(docs.gpt_block_doc(T, H, elem_size=2, train=True))
         for k in (1, 2, 4, 8):

@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) row_kernel(const T* __restrict
       sm = (sm > 0.f ? sm * expf(m - mm) : 0.f) + (s2 > 0.f ? s2 * expf(m2 - mm) : 0.f);
       m = mm;
     }
-    const float inv = 1.f / sm;
+    const float inv = __fdividef(1.f, sm);
     for (int i = lane; i < nv; i += 32) {
       load_vec<T, V>(x + i * V, xv);
 #pragma unroll
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) row_kernel(const T* __restrict
       for (int e = 0; e < V; ++e) {
         cnt += 1.f;
         const float d = xv[e] - mean;
-        mean += d / cnt;
+        mean += d * __fdividef(1.f, cnt);
         m2 += d * (xv[e] - mean);
       }
     }
@@ -700,12 +700,12 @@ __global__ void __launch_bounds__(kRowWarps * 32) row_kernel(const T* __restrict
       const float c = cnt + c2;
       if (c > 0.f) {
         const float d = mn2 - mean;
-        mean += d * (c2 / c);
-        m2 += q2 + d * d * (cnt * c2 / c);
+        mean += d * (c2 * __fdividef(1.f, c));
+        m2 += q2 + d * d * (cnt * c2 * __fdividef(1.f, c));
       }
       cnt = c;
     }
-    const float rstd = rsqrtf(m2 / static_cast<float>(seg) + eps);
+    const float rstd = rsqrtf(m2 * __fdividef(1.f, static_cast<float>(seg)) + eps);
     if constexpr (OP == 2) {
       for (int i = lane; i < nv; i += 32) {
         load_vec<T, V>(x + i * V, xv);
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) row_kernel(const T* __restrict
           sdx += gv[e] * (xv[e] - mean) * rstd;
         }
       }
-      const float inv_n = 1.f / static_cast<float>(seg);
+      const float inv_n = __fdividef(1.f, static_cast<float>(seg));
       const float mdy = warp_sum(sdy) * inv_n, mdx = warp_sum(sdx) * inv_n;
       for (int i = lane; i < nv; i += 32) {
         load_vec<T, V>(x + i * V, xv);
@@ -737,11 +737,137 @@ __global__ void __launch_bounds__(kRowWarps * 32) row_kernel(const T* __restrict
   }
 }
 
-__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+// Register-resident variant: a segment of seg = LPS x R x V elements or
+// fewer lives in the registers of an LPS-lane group (32 / LPS segments per
+// warp): ONE global read per operand, exact two-pass statistics from
+// registers, group-local shuffles. Taken whenever R <= 16 (softmax heads of
+// 128, LayerNorm rows of 2048 bf16).
+template <int LPS>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int o = LPS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <int LPS>
+__device__ __forceinline__ float group_max(float v) {
+#pragma unroll
+  for (int o = LPS / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <typename T, int OP, int V, int LPS, int R>
+__global__ void __launch_bounds__(kRowWarps * 32) row_reg_kernel(const T* __restrict__ a, const T* __restrict__ b,
+                                                                 T* __restrict__ out, long long nseg, int seg,
+                                                                 float eps) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
+  constexpr int G = 32 / LPS;  // segments per warp
+  const int lane = threadIdx.x % 32, j = lane % LPS;
+  const long long sidx = (blockIdx.x * static_cast<long long>(kRowWarps) + threadIdx.x / 32) * G + lane / LPS;
+  const bool live_seg = sidx < nseg;  // whole groups retire together; shuffles stay warp-wide
+  const int nv = seg / V;
+  const long long base = (live_seg ? sidx : 0) * seg;
+  float x[R][V], g[R][V];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int vi = j + r * LPS;
+    const bool ok = live_seg && vi < nv;
+#pragma unroll
+    for (int e = 0; e < V; ++e) x[r][e] = g[r][e] = 0.f;
+    if (ok) {
+      load_vec<T, V>(a + base + vi * V, x[r]);
+      if constexpr (OP == 1 || OP == 3) load_vec<T, V>(b + base + vi * V, g[r]);
+    }
+  }
+  auto valid = [&](int r) { return live_seg && j + r * LPS < nv; };
+  const float inv_n = __fdividef(1.f, static_cast<float>(seg));
+  if constexpr (OP == 0) {  // softmax
+    float m = -INFINITY;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (valid(r))
+#pragma unroll
+        for (int e = 0; e < V; ++e) m = fmaxf(m, x[r][e]);
+    m = group_max<LPS>(m);
+    float sm = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        x[r][e] = valid(r) ? exp2f((x[r][e] - m) * 1.4426950408889634f) : 0.f;
+        sm += x[r][e];
+      }
+    const float inv = __fdividef(1.f, group_sum<LPS>(sm));
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) x[r][e] *= inv;
+  } else if constexpr (OP == 1) {  // softmax-grad
+    float dot = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) dot += x[r][e] * g[r][e];
+    dot = group_sum<LPS>(dot);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) x[r][e] = x[r][e] * (g[r][e] - dot);
+  } else {  // layernorm / layernorm-grad: two-pass mean / variance from registers
+    float sx = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) sx += x[r][e];
+    const float mean = group_sum<LPS>(sx) * inv_n;
+    float sq = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (valid(r))
+#pragma unroll
+        for (int e = 0; e < V; ++e) sq += (x[r][e] - mean) * (x[r][e] - mean);
+    const float rstd = rsqrtf(group_sum<LPS>(sq) * inv_n + eps);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) x[r][e] = (x[r][e] - mean) * rstd;  // xhat
+    if constexpr (OP == 3) {
+      float sdy = 0.f, sdx = 0.f;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          sdy += g[r][e];
+          sdx += g[r][e] * x[r][e];
+        }
+      const float mdy = group_sum<LPS>(sdy) * inv_n, mdx = group_sum<LPS>(sdx) * inv_n;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int e = 0; e < V; ++e) x[r][e] = rstd * (g[r][e] - mdy - x[r][e] * mdx);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (valid(r)) store_vec<T, V>(out + base + (j + r * LPS) * V, x[r]);
+}
+
+// Phi(x) = 0.5 (1 + erf(x / sqrt 2)) with erf from Abramowitz & Stegun 7.1.26
+// (|error| <= 1.5e-7) on e = exp(-x^2 / 2) — the same exponential GELU's
+// gradient needs for the normal pdf. A third of erff's instructions: the
+// GELU kernels stay memory-bound.
+__device__ __forceinline__ float normal_cdf_e(float x, float e) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float t = __fdividef(1.f, fmaf(0.3275911f, z, 1.f));
+  const float poly =
+      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f), 0.254829592f);
+  const float erf_abs = 1.f - poly * e;
+  return 0.5f * (1.f + copysignf(erf_abs, x));
+}
+__device__ __forceinline__ float gelu_f(float x) { return x * normal_cdf_e(x, __expf(-0.5f * x * x)); }
 __device__ __forceinline__ float gelu_grad_f(float x, float g) {
-  const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
-  const float pdf = expf(-0.5f * x * x) * 0.39894228040143268f;
-  return g * (cdf + x * pdf);
+  const float e = __expf(-0.5f * x * x);
+  return g * (normal_cdf_e(x, e) + x * e * 0.39894228040143268f);
 }
 
 template <typename T, int OP, int V>
@@ -786,8 +912,48 @@ void rowwise_typed(int op, const void* a, const void* b, void* out, std::int64_t
   const dim3 g(static_cast<unsigned>((nseg + kRowWarps - 1) / kRowWarps));
   const dim3 blk(kRowWarps * 32);
   const int sg = static_cast<int>(seg);
-#define PLANC_ROW(OPV, V) pdl_launch("row_kernel", row_kernel<T, OPV, V>, g, blk, 0, s, A, B, O, nseg, sg, eps)
   const bool vec = seg % VV == 0;
+  // Register-resident path: LPS lanes (power of two) x R vectors per segment.
+  if (vec) {
+    const long long nv = seg / VV;
+    int lps = 1;
+    while (lps < 32 && lps < nv) lps <<= 1;
+    const long long r = (nv + lps - 1) / lps;
+    if (r <= 64 / VV) {  // <= 64 fp32 registers per operand per lane
+      const int R = r <= 1 ? 1 : r <= 2 ? 2 : r <= 4 ? 4 : r <= 8 ? 8 : 16;
+      const long long per_block = static_cast<long long>(kRowWarps) * (32 / lps);
+      const dim3 gr(static_cast<unsigned>((nseg + per_block - 1) / per_block));
+#define PLANC_RR(OPV, L, RR)                                                                                       \
+  return pdl_launch("row_reg_kernel", row_reg_kernel<T, OPV, VV, L, RR>, gr, blk, 0, s, A, B, O, nseg, sg, eps)
+#define PLANC_RR_R(OPV, L)       \
+  switch (R) {                   \
+    case 1: PLANC_RR(OPV, L, 1); \
+    case 2: PLANC_RR(OPV, L, 2); \
+    case 4: PLANC_RR(OPV, L, 4); \
+    case 8: PLANC_RR(OPV, L, 8); \
+    default: PLANC_RR(OPV, L, (VV == 4 ? 16 : 8)); \
+  }
+#define PLANC_RR_L(OPV)                 \
+  switch (lps) {                        \
+    case 1: PLANC_RR(OPV, 1, 1);        \
+    case 2: PLANC_RR(OPV, 2, 1);        \
+    case 4: PLANC_RR(OPV, 4, 1);        \
+    case 8: PLANC_RR(OPV, 8, 1);        \
+    case 16: PLANC_RR(OPV, 16, 1);      \
+    default: PLANC_RR_R(OPV, 32);       \
+  }
+      switch (op) {
+        case 0: PLANC_RR_L(0);
+        case 1: PLANC_RR_L(1);
+        case 2: PLANC_RR_L(2);
+        default: PLANC_RR_L(3);
+      }
+#undef PLANC_RR_L
+#undef PLANC_RR_R
+#undef PLANC_RR
+    }
+  }
+#define PLANC_ROW(OPV, V) pdl_launch("row_kernel", row_kernel<T, OPV, V>, g, blk, 0, s, A, B, O, nseg, sg, eps)
   switch (op) {
     case 0: if (vec) PLANC_ROW(0, VV); else PLANC_ROW(0, 1); break;
     case 1: if (vec) PLANC_ROW(1, VV); else PLANC_ROW(1, 1); break;
