@@ -44,9 +44,10 @@ extern "C" {
 #define PLANC_B200_NO_TENSOR_CORES 0x2u /* force the SIMT GEMM (debug / A-B checks) */
 #define PLANC_B200_STRICT_VALUE 0x4u    /* reference value-part rule only: V(m*v)->V(v) pieces are
                                            skipped like refexec.cpp:110-117 instead of summed */
-#define PLANC_B200_FUSE_EPILOGUES 0x10u /* an elementwise op consuming a fresh bf16 GEMM output on
-                                           the same lane runs in that GEMM's epilogue (same bits as
-                                           the separate kernel; default: every op its own kernel) */
+#define PLANC_B200_FUSE_EPILOGUES 0x10u /* (default, kept for compatibility) an elementwise op consuming a
+                                           fresh bf16 GEMM output on the same lane runs in that GEMM's
+                                           epilogue — same bits as the separate kernel */
+#define PLANC_B200_NO_FUSION 0x80u      /* every elementwise op its own kernel (no epilogue fusion) */
 #define PLANC_B200_PEER_MEMORY 0x20u     /* planc_b200_open_rank / describe_rank: peer-memory transport
                                            (CUDA IPC over NVLink, device flags) instead of NCCL */
 #define PLANC_B200_NO_GROUPING 0x40u    /* every GEMM its own launch (default: independent same-shape
@@ -172,11 +173,13 @@ int planc_b200_gemm_config(int64_t m, int64_t n, int64_t k, int ta, int tb, int 
 /* Host-only: the tcgen05 GEMM's launch schedule on a GPU with `sms` SMs for
  * `group` independent GEMMs of this shape in one launch (1 = a single GEMM)
  * — tile width, persistent grid, and either tiles done whole (data-parallel
- * waves) plus the CTAs sharing the remaining tiles by k-range (stream-K), or
- * the number of k-splits per tile (split-K: fp32 partials + a reduce kernel);
- * with the workspace either needs (0 without). bf16 operands. */
+ * waves) followed by half_items half-width tiles (the last partial wave,
+ * 128 x tile_n/2 each) or by the CTAs sharing the remaining tiles by k-range
+ * (stream-K), or the number of k-splits per tile (split-K: fp32 partials + a
+ * reduce kernel); with the workspace either needs (0 without). bf16 operands. */
 int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, int c_bf16, int sms, int group,
-                             int* tile_n, int* grid, int* dp_tiles, int* sk_ctas, int* splits, int64_t* ws_bytes);
+                             int* tile_n, int* grid, int* dp_tiles, int* sk_ctas, int* splits, int* half_items,
+                             int64_t* ws_bytes);
 
 /* Host-only lowering (no GPU needed): the executor's device program for a
  * plan as JSON — buffers, instructions, box cells, issue order. */

@@ -69,7 +69,7 @@ int planc_b200_open(const char* plan_json, const int* lane_gpu, int num_lane_gpu
     opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
     opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
     if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
-    opt.fuse_epilogues = (flags & PLANC_B200_FUSE_EPILOGUES) != 0;
+    opt.fuse_epilogues = (flags & PLANC_B200_NO_FUSION) == 0;
     opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
     std::vector<int> lanes;
     for (int i = 0; lane_gpu && i < num_lane_gpu; ++i) lanes.push_back(lane_gpu[i]);
@@ -104,7 +104,7 @@ int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* 
     opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
     opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
     if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
-    opt.fuse_epilogues = (flags & PLANC_B200_FUSE_EPILOGUES) != 0;
+    opt.fuse_epilogues = (flags & PLANC_B200_NO_FUSION) == 0;
     opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
     RankConfig rc;
     rc.rank = rank;
@@ -129,7 +129,7 @@ int planc_b200_describe_rank(const char* plan_json, const int* lane_rank, int nu
   return guarded([&] {
     if (!plan_json || !json_out || !lane_rank) throw UsageError("null argument");
     ProgramOptions po = program_options((flags & PLANC_B200_STRICT_VALUE) == 0,
-                                        (flags & PLANC_B200_FUSE_EPILOGUES) != 0 &&
+                                        (flags & PLANC_B200_NO_FUSION) == 0 &&
                                             (flags & PLANC_B200_NO_TENSOR_CORES) == 0);
     po.group_gemms = (flags & (PLANC_B200_NO_GROUPING | PLANC_B200_NO_TENSOR_CORES)) == 0;
     ExecutionPlan plan = load_plan(plan_json);
@@ -330,7 +330,8 @@ int planc_b200_gemm_config(int64_t m, int64_t n, int64_t k, int ta, int tb, int 
 }
 
 int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, int c_bf16, int sms, int group,
-                             int* tile_n, int* grid, int* dp_tiles, int* sk_ctas, int* splits, int64_t* ws_bytes) {
+                             int* tile_n, int* grid, int* dp_tiles, int* sk_ctas, int* splits, int* half_items,
+                             int64_t* ws_bytes) {
   return guarded([&] {
     if (sms <= 0) throw UsageError("sms must be positive");
     if (group < 1 || group > kMaxGemmGroup) throw UsageError("group must be in [1, 8]");
@@ -351,6 +352,7 @@ int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, in
     if (dp_tiles) *dp_tiles = sc.dp_tiles;
     if (sk_ctas) *sk_ctas = sc.sk_ctas;
     if (splits) *splits = sc.splits;
+    if (half_items) *half_items = sc.half_items;
     if (ws_bytes) *ws_bytes = sc.ws_bytes;
   });
 }
@@ -366,7 +368,7 @@ int planc_b200_describe(const char* plan_json, uint32_t flags, char** json_out) 
   return guarded([&] {
     if (!plan_json || !json_out) throw UsageError("null argument");
     ProgramOptions po = program_options((flags & PLANC_B200_STRICT_VALUE) == 0,
-                                        (flags & PLANC_B200_FUSE_EPILOGUES) != 0 &&
+                                        (flags & PLANC_B200_NO_FUSION) == 0 &&
                                             (flags & PLANC_B200_NO_TENSOR_CORES) == 0);
     po.group_gemms = (flags & (PLANC_B200_NO_GROUPING | PLANC_B200_NO_TENSOR_CORES)) == 0;
     ExecutionPlan plan = load_plan(plan_json);

@@ -97,6 +97,10 @@ struct SkParams {
   int dp_tiles = 0;
   int sk_ctas = 0;
   int splits = 0;  // split-K: every work item is (tile, split), stored to ws_map
+  // Half-width tail: after dp_tiles whole tiles, the remaining tiles run as
+  // half_items tiles of 128 x BN/2 (item h: half h & 1 of tile dp_tiles + h / 2),
+  // so a last wave of r < grid/2 tiles takes half a tile-time.
+  int half_items = 0;
   long long sk_iters = 0;
   float* partials = nullptr;  // [sk_ctas][2 slots][4 quarters][BN/32 chunks][8][32] float4
   int* counters = nullptr;    // [(tiles - dp_tiles) * 4], zero between launches
@@ -111,7 +115,8 @@ __device__ __forceinline__ int sk_owner(const SkParams& sk, long long x) {
   return static_cast<int>(((x + 1) * sk.sk_ctas - 1) / sk.sk_iters);
 }
 
-// Calls f(tile, kb0, kb1) for this CTA's work items in order.
+// Calls f(tile, kb0, kb1, half) for this CTA's work items in order; half is
+// -1 for a whole tile, else which 128 x BN/2 half of the tile.
 template <typename F>
 __device__ __forceinline__ void for_each_work(int num_k, const SkParams& sk, F&& f) {
   if (sk.splits > 1) {
@@ -119,11 +124,18 @@ __device__ __forceinline__ void for_each_work(int num_k, const SkParams& sk, F&&
     const int items = sk.dp_tiles * sk.splits;
     for (int x = blockIdx.x; x < items; x += gridDim.x) {
       const int t = x / sk.splits, sp = x - t * sk.splits;
-      f(t, sp * num_k / sk.splits, (sp + 1) * num_k / sk.splits);
+      f(t, sp * num_k / sk.splits, (sp + 1) * num_k / sk.splits, -1);
     }
     return;
   }
-  for (int t = blockIdx.x; t < sk.dp_tiles; t += gridDim.x) f(t, 0, num_k);
+  if (sk.half_items > 0) {
+    for (int x = blockIdx.x; x < sk.dp_tiles + sk.half_items; x += gridDim.x) {
+      if (x < sk.dp_tiles) f(x, 0, num_k, -1);
+      else f(sk.dp_tiles + (x - sk.dp_tiles) / 2, 0, num_k, (x - sk.dp_tiles) & 1);
+    }
+    return;
+  }
+  for (int t = blockIdx.x; t < sk.dp_tiles; t += gridDim.x) f(t, 0, num_k, -1);
   if (static_cast<int>(blockIdx.x) < sk.sk_ctas) {
     long long it = sk_lo(sk, blockIdx.x);
     const long long hi = sk_lo(sk, blockIdx.x + 1);
@@ -131,7 +143,7 @@ __device__ __forceinline__ void for_each_work(int num_k, const SkParams& sk, F&&
       const int j = static_cast<int>(it / num_k);
       const int kb0 = static_cast<int>(it - static_cast<long long>(j) * num_k);
       const int kb1 = static_cast<int>(min(static_cast<long long>(num_k), kb0 + (hi - it)));
-      f(sk.dp_tiles + j, kb0, kb1);
+      f(sk.dp_tiles + j, kb0, kb1, -1);
       it += kb1 - kb0;
     }
   }
@@ -343,12 +355,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;  // global k-block counter across work items (ring position)
-      for_each_work(num_k, sk, [&](int t, int kb0, int kb1) {
+      for_each_work(num_k, sk, [&](int t, int kb0, int kb1, int half) {
         int p, mb, nb;
         coords(t, p, mb, nb);
         const CUtensorMap* tmA = &gm.a[p];
         const CUtensorMap* tmB = &gm.b[p];
-        const int m0 = mb * BM, n0 = nb * BN;
+        // A half tile loads the B rows from its own first column (the box's
+        // upper half is unused, and zero-filled past the tensor edge).
+        const int m0 = mb * BM, n0 = nb * BN + (half > 0 ? BN / 2 : 0);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const std::uint32_t phase = (it / STAGES) & 1;
@@ -373,9 +387,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr std::uint32_t idesc = make_idesc<BN>(A_MN, B_MN);
+      constexpr std::uint32_t idesc_full = make_idesc<BN>(A_MN, B_MN);
+      constexpr std::uint32_t idesc_half = make_idesc<(BN >= 128 ? BN / 2 : BN)>(A_MN, B_MN);
       int it = 0, local = 0;
-      for_each_work(num_k, sk, [&](int, int kb0, int kb1) {
+      for_each_work(num_k, sk, [&](int, int kb0, int kb1, int half) {
+        const std::uint32_t idesc = half >= 0 ? idesc_half : idesc_full;
         const int acc = local & 1;
         const std::uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
@@ -451,7 +467,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       return reinterpret_cast<float4*>(sk.partials) +
              ((static_cast<std::int64_t>((b * 2 + slot) * 4 + q) * (BN / 32) + c) * 8) * 32 + lane;
     };
-    for_each_work(num_k, sk, [&](int t, int kb0, int kb1) {
+    for_each_work(num_k, sk, [&](int t, int kb0, int kb1, int half) {
       int p, mb, nb;
       coords(t, p, mb, nb);
       const int acc = local & 1;
@@ -464,18 +480,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // split index of k-range start kb0 = floor(s*K/S): s = ceil(kb0*S/K) (K/S >= 1)
         const int sp = (kb0 * sk.splits + num_k - 1) / num_k;
         const int y = part ? (p * sk.splits + sp) * m_pad + mb * BM + q * 32 : mb * BM + q * 32;
+        const int chunks = half >= 0 ? BN / 64 : BN / 32;
+        const int x0 = nb * BN + (half > 0 ? BN / 2 : 0);
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < chunks; ++c) {
           std::uint32_t r[32];
           tmem_ld32(base + c * 32, r);
-          if (c == BN / 32 - 1) {
+          if (c == chunks - 1) {
             // All TMEM reads of this accumulator are complete: hand it back.
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
           }
-          if (part) store_chunk(r, &maps.ws, false, nb * BN + c * 32, y);
-          else store_chunk(r, &gm.c[p], C_BF16, nb * BN + c * 32, y);
+          if (part) store_chunk(r, &maps.ws, false, x0 + c * 32, y);
+          else store_chunk(r, &gm.c[p], C_BF16, x0 + c * 32, y);
         }
         return;
       }
@@ -808,6 +826,7 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
   sk.sk_ctas = sc.sk_ctas;
   sk.sk_iters = sc.sk_iters;
   sk.splits = sc.splits;
+  sk.half_items = sc.half_items;
   const std::int64_t m_pad = (a.m + BM - 1) / BM * BM, n_pad = (a.n + BN - 1) / BN * BN;
   if (sc.splits > 1) {
     // Partials: fp32 [ng * splits * m_pad][n_pad], stored like an fp32 C.
@@ -854,7 +873,7 @@ constexpr double kSkWriteChunkUs = 0.15;
 constexpr int kMinSkIters = 4;  // k-blocks per stream-K range, at least
 
 GemmSchedule schedule_for(std::int64_t m, std::int64_t n, std::int64_t k, int bn, bool allow_sk, int sms,
-                          bool force_sk = false, int group = 1) {
+                          bool force_sk = false, int group = 1, bool allow_half = true) {
   GemmSchedule sc;
   sc.bn = bn;
   sc.tiles = ((m + BM - 1) / BM) * ((n + bn - 1) / bn) * std::max(group, 1);
@@ -863,6 +882,14 @@ GemmSchedule schedule_for(std::int64_t m, std::int64_t n, std::int64_t k, int bn
   sc.grid = static_cast<int>(std::min<std::int64_t>(sc.tiles, sms));
   sc.dp_tiles = sc.tiles;
   sc.model_us = static_cast<double>(waves) * (sc.num_k * kb_us(bn) + kTileUs);
+  // Half-width tail: a last wave of r <= sms/2 tiles runs as 2r half tiles.
+  const std::int64_t rem = sc.tiles % sms;
+  if (allow_half && bn >= 128 && rem > 0 && 2 * rem <= sms && sc.tiles > sms) {
+    sc.dp_tiles = static_cast<int>(sc.tiles - rem);
+    sc.half_items = static_cast<int>(2 * rem);
+    sc.model_us = static_cast<double>(waves - 1) * (sc.num_k * kb_us(bn) + kTileUs) +
+                  0.5 * sc.num_k * kb_us(bn) + kTileUs;
+  }
   if (!allow_sk || sc.tiles % sms == 0) return sc;
   // Whole waves minus one stay data-parallel; the rest (< 2 waves of tiles)
   // is shared by `ctas` CTAs — every count from ~one segment per tile up to
@@ -881,6 +908,7 @@ GemmSchedule schedule_for(std::int64_t m, std::int64_t n, std::int64_t k, int bn
     const double fix = chunks * (2 * kSkWriteChunkUs + kSkRoundTripUs * ((covers + kSkDepth - 1) / kSkDepth));
     const double t = static_cast<double>(dp_waves) * (sc.num_k * kb_us(bn) + kTileUs) + per * kb_us(bn) + kTileUs + fix;
     if (t >= best.model_us) continue;
+    best.half_items = 0;
     best.dp_tiles = static_cast<int>(dp_waves * sms);
     best.sk_ctas = ctas;
     best.sk_iters = iters;
@@ -941,8 +969,15 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   bool have = false;
   for (int bn : {256, 128, 64}) {
     if (forced && bn != forced) continue;
-    GemmSchedule dp = schedule_for(a.m, a.n, a.k, bn, false, sms, false, a.group);
-    GemmSchedule sk = schedule_for(a.m, a.n, a.k, bn, allow_sk, sms, skmode == 2, a.group);
+    // PLANC_B200_HALF_TAIL=1 enables the half-width tail (off by default:
+    // inside a plan step the idle SMs of a partial last wave already run
+    // other streams' work, and the A/B on C2 / C2x / C1-L measured the tail
+    // 2-3 % slower — profiles/r01/ab_plans_half_tail.jsonl); the fused
+    // epilogue walks whole tiles only.
+    const char* hv = std::getenv("PLANC_B200_HALF_TAIL");
+    const bool allow_half = a.epi.n_ops == 0 && hv && hv[0] == '1';
+    GemmSchedule dp = schedule_for(a.m, a.n, a.k, bn, false, sms, false, a.group, allow_half);
+    GemmSchedule sk = schedule_for(a.m, a.n, a.k, bn, allow_sk, sms, skmode == 2, a.group, allow_half);
     GemmSchedule c = (sk.sk_ctas > 0 && (skmode == 2 || sk.model_us < 0.9 * dp.model_us)) ? sk : dp;
     if (allow_split) {
       GemmSchedule sp = splitk_for(a.m, a.n, a.k, bn, sms, a.group, a.dc == DT_BF16 ? 2 : 4);
@@ -982,7 +1017,8 @@ void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
   const bool a_mn = a.ta, b_mn = !a.tb, cb = a.dc == DT_BF16;
   GemmSchedule sc = gemm_sm100_schedule(a, device_sms());
   if ((sc.sk_ctas > 0 || sc.splits > 1) && (a.ws == nullptr || a.ws_bytes < sc.ws_bytes)) {
-    sc = schedule_for(a.m, a.n, a.k, sc.bn, false, device_sms(), false, a.group);  // no workspace: data-parallel
+    sc = schedule_for(a.m, a.n, a.k, sc.bn, false, device_sms(), false, a.group,
+                      a.epi.n_ops == 0);  // no workspace: data-parallel
   }
   const int bn = sc.bn;
   if (a.epi.n_ops > 0) {

@@ -118,6 +118,9 @@ struct GemmSchedule {
   // reduce kernel sums them in split order — every SM pulls a slice, no CTA
   // waits on another. 0 = off.
   int splits = 0;
+  // Half-width tail (data-parallel only): tiles [dp_tiles, tiles) run as
+  // half_items = 2 x (tiles - dp_tiles) tiles of 128 x bn/2.
+  int half_items = 0;
   std::int64_t ws_bytes = 0;  // 0 without stream-K / split-K
   double model_us = 0;
 };

@@ -48,7 +48,7 @@ struct ExecOptions {
   bool allow_tensor_cores = true;
   bool value_split_extension = true;
   int streams_per_lane = kLaneStreams;  // 1 = issue a lane strictly in plan order
-  bool fuse_epilogues = false;          // elementwise consumers computed in GEMM epilogues
+  bool fuse_epilogues = true;           // elementwise consumers computed in GEMM epilogues
   bool group_gemms = true;              // same-shape independent GEMMs in one grouped launch
 };
 

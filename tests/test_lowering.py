@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     assert "sm_100a" in pb.version()
 
 
-@pytest.mark.parametrize("flags", [0, pb.FUSE_EPILOGUES])
+@pytest.mark.parametrize("flags", [0, pb.NO_FUSION])
 @pytest.mark.parametrize("name", golden_cases.names())
 def test_lowered_program_reproduces_reference(name, flags):
     g = golden_cases.load(name)
@@ -276,6 +276,17 @@ def test_gemm_schedule_covers_every_k_block_once(m, n, k, ta, sk_mode, monkeypat
     num_k = -(-k // 64)
     assert 0 < sc["grid"] <= sms
     seen = {}
+    if sc["half_items"]:
+        # half-width tail: whole tiles, then both halves of every remaining tile
+        assert sc["sk_ctas"] == 0 and sc["half_items"] == 2 * (tiles - sc["dp_tiles"])
+        assert sc["dp_tiles"] % sms == 0 and sc["half_items"] <= sms
+        halves = {}
+        for x in range(sc["dp_tiles"] + sc["half_items"]):
+            if x >= sc["dp_tiles"]:
+                h = x - sc["dp_tiles"]
+                halves.setdefault(sc["dp_tiles"] + h // 2, set()).add(h % 2)
+        assert all(v == {0, 1} for v in halves.values()) and len(halves) == tiles - sc["dp_tiles"]
+        return
     for b in range(sc["grid"]):
         for t in range(b, sc["dp_tiles"], sc["grid"]):
             for kb in range(num_k):

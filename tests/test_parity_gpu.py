@@ -37,7 +37,7 @@ def test_golden_plan_parity(name):
 @pytest.mark.parametrize("name", ["mlp_dp2", "gpt_block_tp2", "embed_shard2", "adapt_d1_to_d0_4",
                                   "three_pass_3f1b", "gpt_block_fwd_tp2_mma"])
 @pytest.mark.parametrize("flags", [pb.NO_GRAPH, pb.NO_TENSOR_CORES, pb.SERIAL_LANES, pb.NO_GRAPH | pb.SERIAL_LANES,
-                                   pb.FUSE_EPILOGUES, pb.FUSE_EPILOGUES | pb.NO_GRAPH])
+                                   pb.NO_FUSION, pb.NO_FUSION | pb.NO_GRAPH])
 def test_parity_across_launch_modes(name, flags):
     g = golden_cases.load(name)
     out, _ = _run(g["plan"], g["inputs"], flags=flags)

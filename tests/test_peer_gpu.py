@@ -139,6 +139,6 @@ def test_peer_memory_launch_modes():
     import paper_2301_08984_b200 as pb
 
     names = ["gpt_block_tp2", "adapt_v_to_r4", "mlp_1f1b_dp2"]
-    for flags in (pb.NO_GRAPH, pb.SERIAL_LANES, pb.FUSE_EPILOGUES):
+    for flags in (pb.NO_GRAPH, pb.SERIAL_LANES, pb.NO_FUSION):
         reps = _run_world(2, names, flags)
         _assert_ok(reps, names, 2)

@@ -17,7 +17,8 @@ import paper_2301_08984_b200 as pb  # noqa: E402
 VARIANTS = [
     ("base", 0, {}),
     ("no_grouping", pb.NO_GROUPING, {}),
-    ("fuse", pb.FUSE_EPILOGUES, {}),
+    ("half_tail", 0, {"PLANC_B200_HALF_TAIL": "1"}),
+    ("no_fusion", pb.NO_FUSION, {}),
 ]
 
 

@@ -37,7 +37,7 @@ for name, m, n, k, ta, tb in SHAPES:
             os.environ["PLANC_B200_GEMM_BN"] = bn
         row[f"gemm_only_{bn}_ms"] = round(run(matmul_plan(m, n, k, ta, tb)[0], {0: a, 1: b}, 0), 4)
         p = matmul_add_plan(m, n, k, ta, tb)[0]
-        row[f"sep_{bn}_ms"] = round(run(p, {0: a, 1: b, 3: d}, pb.SERIAL_LANES), 4)
+        row[f"sep_{bn}_ms"] = round(run(p, {0: a, 1: b, 3: d}, pb.SERIAL_LANES | pb.NO_FUSION), 4)
         row[f"fused_{bn}_ms"] = round(run(p, {0: a, 1: b, 3: d}, pb.FUSE_EPILOGUES), 4)
     os.environ.pop("PLANC_B200_GEMM_BN", None)
     rows.append(row)

@@ -17,6 +17,6 @@ if mode == "gemm":
 else:
     plan = matmul_add_plan(m, n, k)[0]
     inp[3] = rng.integers(-1, 2, size=(m, n)).astype(np.float64)
-with pb.Executor(plan, lane_gpus=[0], flags=(pb.FUSE_EPILOGUES if mode == "fused" else 0) | pb.NO_GRAPH) as ex:
+with pb.Executor(plan, lane_gpus=[0], flags=(pb.FUSE_EPILOGUES if mode == "fused" else pb.NO_FUSION) | pb.NO_GRAPH) as ex:
     ex.set_inputs(inp)
     ex.run(3)
