@@ -65,17 +65,18 @@ def load_plan(name):
     return plan, meta
 
 
-def synthetic_inputs(plan_json: str, seed: int = 0) -> dict:
-    """Integer-valued inputs in {-1, 0, 1} for every graph-input pTensor."""
+def synthetic_inputs(plan_json: str, seed: int = 0, only=None) -> dict:
+    """Integer-valued inputs in {-1, 0, 1} for every graph-input pTensor (or
+    the ids in ``only``: one rank's inputs). Each tensor draws from its own
+    seeded stream, so a rank's subset equals the same tensors of the full set."""
     p = json.loads(plan_json)
     produced = set()
     vts = {v["id"]: v for v in p["vtensors"]}
     for o in p["ops"]:
         for v in o["outputs"]:
             produced.add(vts[v]["ptensor"])
-    rng = np.random.default_rng(seed)
-    return {pt["id"]: rng.integers(-1, 2, size=pt["shape"]).astype(np.float64)
-            for pt in p["ptensors"] if pt["id"] not in produced}
+    return {pt["id"]: np.random.default_rng([seed, pt["id"]]).integers(-1, 2, size=pt["shape"]).astype(np.float64)
+            for pt in p["ptensors"] if pt["id"] not in produced and (only is None or pt["id"] in only)}
 
 
 class ClockSampler:
@@ -229,7 +230,6 @@ def main():
     import paper_2301_08984_b200 as pb
 
     peaks = measured_peaks()
-    inputs = synthetic_inputs(plan)
     nlanes = len(json.loads(plan)["lanes"])
     transport = None
     if dist:
@@ -268,7 +268,8 @@ def main():
             ex = pb.Executor(plan, rank=rank, world=world, lane_rank=lane_rank, local_gpu=local, nccl_id=box[0])
     else:
         ex = pb.Executor(plan, lane_gpus=list(range(n)))
-    ex.set_inputs(inputs)
+    # each rank generates and binds only the inputs its lanes place
+    ex.set_inputs(synthetic_inputs(plan, only=set(ex.input_ids())))
     ex.run(args.warmup)  # warm-up (graph capture + W steps)
     st = ex.stats()
 

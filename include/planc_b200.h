@@ -131,7 +131,8 @@ int planc_b200_get_output(planc_b200_exec* h, int ptensor, double* out, int64_t 
  * ids as in planc_b200_describe) as doubles. Returns its element count. */
 int64_t planc_b200_read_buffer(planc_b200_exec* h, int buffer, double* out, int64_t capacity);
 
-/* Graph-input pTensors the plan places (ascending id). */
+/* Graph-input pTensors the plan places (ascending id); in one-process-per-GPU
+ * mode, those placed on this rank's lanes (the only inputs it needs). */
 int planc_b200_num_inputs(planc_b200_exec* h);
 int planc_b200_input_ids(planc_b200_exec* h, int* ids, int cap);
 

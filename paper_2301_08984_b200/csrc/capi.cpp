@@ -229,12 +229,12 @@ int planc_b200_output_ids(planc_b200_exec* h, int* ids, int cap) {
 }
 
 int planc_b200_num_inputs(planc_b200_exec* h) {
-  return h ? static_cast<int>(h->ex->program().graph_inputs.size()) : -1;
+  return h ? static_cast<int>(h->ex->input_ids().size()) : -1;
 }
 
 int planc_b200_input_ids(planc_b200_exec* h, int* ids, int cap) {
   if (!h) return -1;
-  const auto& v = h->ex->program().graph_inputs;
+  const std::vector<int> v = h->ex->input_ids();
   for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i) ids[i] = v[i];
   return static_cast<int>(v.size());
 }

@@ -983,7 +983,10 @@ __global__ void peer_epoch_kernel(unsigned* epoch) {
 
 __global__ void peer_flags_kernel(const unsigned* epoch, PeerFlags f, unsigned long long timeout_ns, unsigned* err) {
   pdl_wait();  // launch.cuh: inputs of the previous kernel visible
-  pdl_trigger();
+  // No early pdl_trigger here: a dependent launched while this kernel spins
+  // (e.g. a persistent GEMM holding every SM's shared memory in
+  // griddepcontrol.wait) could starve the streams whose progress the awaited
+  // peers depend on. Dependents start when the wait is over (kernel exit).
   const unsigned e = *reinterpret_cast<const volatile unsigned*>(epoch);
   const int t = threadIdx.x;
   if (t < f.n_sig) {
@@ -1002,7 +1005,14 @@ __global__ void peer_flags_kernel(const unsigned* epoch, PeerFlags f, unsigned l
       __nanosleep(256);
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (now - t0 > timeout_ns) {
-        if (err) *reinterpret_cast<volatile unsigned*>(err) = f.code;
+        // err[0] code, [1] value seen, [2] epoch awaited, [3..4] flag address
+        if (err && atomicCAS(err, 0u, f.code) == 0u) {
+          const unsigned long long a = reinterpret_cast<unsigned long long>(f.wait[t]);
+          err[1] = v;
+          err[2] = e;
+          err[3] = static_cast<unsigned>(a);
+          err[4] = static_cast<unsigned>(a >> 32);
+        }
         __threadfence_system();
         __trap();
       }

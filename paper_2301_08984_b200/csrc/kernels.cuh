@@ -156,7 +156,8 @@ void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s);
 // (release at system scope: the stream's earlier writes are visible to a
 // peer that acquires the flag), then waits until every `wait` flag has
 // reached the epoch (acquire, system scope). A wait that does not complete
-// within timeout_ns records `code` in *err (host-mapped) and traps, so a
+// within timeout_ns records `code` in err[0] (host-mapped; err[1] the value
+// seen, err[2] the epoch awaited, err[3..4] the flag address) and traps, so a
 // broken schedule fails the context instead of hanging the GPU.
 constexpr int kMaxPeerFlags = 16;
 struct PeerFlags {

@@ -8,7 +8,8 @@
 // small kernels pays one launch latency instead of one per kernel. Each
 // kernel calls pdl_wait() before touching any buffer (reads or writes: the
 // split-K workspace is reused by the next GEMM on the stream) and
-// pdl_trigger() once its dependents may start their prologues. Inside CUDA
+// pdl_trigger() once its dependents may start their prologues (never before
+// a wait on other ranks: see peer_flags_kernel). Inside CUDA
 // graph capture the attribute becomes a programmatic edge; PLANC_B200_PDL=0
 // launches without it (the instructions are then no-ops).
 #pragma once

@@ -294,8 +294,8 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
     const std::size_t words = kFlagReady + static_cast<std::size_t>(psync_.slots[rc_.rank]) + 1;
     ck(cudaMalloc(&flags_, words * sizeof(unsigned)), "cudaMalloc(peer flags)");
     ck(cudaMemset(flags_, 0, words * sizeof(unsigned)), "memset(peer flags)");
-    ck(cudaHostAlloc(reinterpret_cast<void**>(&peer_err_), sizeof(unsigned), cudaHostAllocMapped), "cudaHostAlloc");
-    *peer_err_ = 0;
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&peer_err_), 8 * sizeof(unsigned), cudaHostAllocMapped), "cudaHostAlloc");
+    std::memset(peer_err_, 0, 8 * sizeof(unsigned));
     double secs = 60.0;
     if (const char* t = std::getenv("PLANC_B200_PEER_TIMEOUT_S")) secs = std::max(0.1, std::atof(t));
     peer_timeout_ns_ = static_cast<unsigned long long>(secs * 1e9);
@@ -563,10 +563,18 @@ void Executor::check_sync(cudaError_t e, const char* what) const {
   if (e == cudaSuccess) return;
   if (peer_err_ && *peer_err_) {
     const unsigned c = *peer_err_;
+    const unsigned long long addr =
+        static_cast<unsigned long long>(peer_err_[3]) | (static_cast<unsigned long long>(peer_err_[4]) << 32);
+    const long long word = static_cast<long long>(addr - reinterpret_cast<unsigned long long>(flags_)) / 4;
+    std::string where = word >= static_cast<long long>(kFlagReady) ? "ready slot " + std::to_string(word - kFlagReady)
+                        : word >= static_cast<long long>(kFlagBarrier)
+                            ? "barrier slot of rank " + std::to_string(word - kFlagBarrier)
+                            : "flag word " + std::to_string(word);
+    where += " saw " + std::to_string(peer_err_[1]) + ", awaited epoch " + std::to_string(peer_err_[2]);
     throw InternalError(std::string("peer-memory rank mode: rank ") + std::to_string(rc_.rank) +
                         (c == ~0u ? " timed out in the step barrier"
                                   : " timed out waiting for the producers of instruction " + std::to_string(c - 1)) +
-                        " (" + cudaGetErrorString(e) + ")");
+                        " (" + where + "; " + cudaGetErrorString(e) + ")");
   }
   ck(e, what);
 }
@@ -1209,6 +1217,13 @@ std::vector<double> Executor::read_buffer(int buffer) {
   std::vector<double> out(bd.elems);
   for (std::int64_t i = 0; i < bd.elems; ++i) out[i] = host_elem(r, bd.dtype, i);
   return out;
+}
+
+std::vector<int> Executor::input_ids() const {
+  std::set<int> ids;
+  for (const auto& b : prog_.buffers)
+    if (b.graph_input && owned_[b.lane]) ids.insert(b.ptensor);
+  return std::vector<int>(ids.begin(), ids.end());
 }
 
 std::vector<int> Executor::output_ids() const {

@@ -117,6 +117,8 @@ class Executor {
   // Raw value of one device buffer (a vTensor piece) as doubles.
   std::vector<double> read_buffer(int buffer);
   std::vector<int> output_ids() const;
+  // Graph-input pTensors this process places (rank mode: its own lanes').
+  std::vector<int> input_ids() const;
   int kernels_per_step() const { return kernels_per_step_; }
   int gemm_tc_launches() const { return gemm_tc_per_step_; }
   bool graph_captured() const { return graph_exec_ != nullptr; }

@@ -142,3 +142,27 @@ def test_peer_memory_launch_modes():
     for flags in (pb.NO_GRAPH, pb.SERIAL_LANES, pb.NO_FUSION):
         reps = _run_world(2, names, flags)
         _assert_ok(reps, names, 2)
+
+
+@pytest.mark.slow
+@pytest.mark.timeout(1500)
+@pytest.mark.parametrize("config,world", [("c3", 8), ("c2", 8), ("c5", 2)])
+def test_peer_memory_bench_under_torchrun(config, world):
+    """bench.py under torchrun with the peer-memory transport at full size,
+    every rank on cuda:0: persistent tcgen05 GEMMs (all SMs' shared memory)
+    interleaved with cross-rank flag waits must not starve each other (a
+    programmatic-dependent launch behind a spinning wait once deadlocked the
+    8-rank pipeline plan)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PLANC_B200_BENCH_SAME_GPU="1", PLANC_B200_PEER_TIMEOUT_S="120")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", str(world),
+           "--steps", "2", "--warmup", "3", "--config", config]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=1400)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == world and line["value"] > 0
+    assert line["config"]["transport"].startswith("peer memory")
