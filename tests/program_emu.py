@@ -20,6 +20,69 @@ def _strided_view(flat, offset, strides, extents):
     return idx
 
 
+def buffer_shapes(desc: dict) -> dict:
+    return {b["id"]: [hi - lo for lo, hi in b["region"]] for b in desc["buffers"]}
+
+
+def exec_instr(ins: dict, data: dict, shape: dict):
+    """One compute / box instruction on the flat float64 buffers in ``data``
+    (results are assigned to data[out]; a box writes only its cells)."""
+    k = ins["kind"]
+    if k == "gemm":
+        for g in range(ins.get("group", 1)):  # grouped launch: member g = (in[2g], in[2g+1]) -> out[g]
+            a = data[ins["in"][2 * g]].reshape(shape[ins["in"][2 * g]])
+            b = data[ins["in"][2 * g + 1]].reshape(shape[ins["in"][2 * g + 1]])
+            a = a.T if ins["ta"] else a
+            b = b.T if ins["tb"] else b
+            data[ins["out"][g]] = (a @ b).reshape(-1)
+        for f in ins.get("fused", []):  # elementwise consumers run in the GEMM epilogue
+            out = data[f["in"][0]].copy()
+            for x in f["in"][1:]:
+                out = (out + data[x], out * data[x], np.maximum(out, data[x]))[f["ew"]]
+            data[f["out"]] = out
+    elif k == "ew":
+        out = data[ins["in"][0]].copy()
+        for x in ins["in"][1:]:
+            out = (out + data[x], out * data[x], np.maximum(out, data[x]))[ins["ew"]]
+        data[ins["out"][0]] = out
+    elif k == "reduce":
+        x = data[ins["in"][0]].reshape(ins["outer"], ins["axis_len"], ins["inner"])
+        data[ins["out"][0]] = x.sum(axis=1).reshape(-1)
+    elif k == "emb_lookup":
+        idx = data[ins["in"][0]].astype(np.int64)
+        tab = data[ins["in"][1]].reshape(ins["rows"], ins["h"])
+        out = np.zeros((ins["n_idx"], ins["h"]))
+        ok = (idx >= ins["lo"]) & (idx < ins["lo"] + ins["rows"])
+        out[ok] = tab[idx[ok] - ins["lo"]]
+        data[ins["out"][0]] = out.reshape(-1)
+    elif k == "emb_grad":
+        idx = data[ins["in"][0]].astype(np.int64)
+        g = data[ins["in"][1]].reshape(ins["n_idx"], ins["h"])
+        out = np.zeros((ins["rows"], ins["h"]))
+        for j in range(ins["n_idx"]):
+            if ins["lo"] <= idx[j] < ins["lo"] + ins["rows"]:
+                out[idx[j] - ins["lo"]] += g[j]
+        data[ins["out"][0]] = out.reshape(-1)
+    elif k == "rowwise":  # schema extension: row-wise sub-operators / GELU
+        from oracle import planc_oracle as po
+
+        names = ["softmax", "softmax-grad", "layernorm", "layernorm-grad", "gelu", "gelu-grad"]
+        seg = ins["seg"] if ins["row_op"] < 4 else 1
+        xs = [data[b].reshape(-1, seg) for b in ins["in"]]
+        data[ins["out"][0]] = po.eval_ext(names[ins["row_op"]], xs, seg, ins["eps"]).reshape(-1)
+    elif k == "box":
+        ob = ins["out"][0]
+        out = data[ob].copy()  # a box writes only its cells (two-phase all-reduce: two boxes per output)
+        for c in ins["cells"]:
+            di = _strided_view(out, c["dst_off"], c["dst_str"], c["ext"])
+            v = np.zeros(di.shape)
+            for t in c["terms"]:
+                si = _strided_view(data[t["buf"]], t["off"], t["str"], c["ext"])
+                v = v + data[t["buf"]][si] if t["add"] else data[t["buf"]][si].copy()
+            out[di] = v
+        data[ob] = out
+
+
 def run_program(desc: dict, plan: dict, inputs: dict, owned_lanes=None, exchange=None, return_buffers=False):
     """Interpret the lowered program. With ``owned_lanes`` only those lanes'
     instructions run (one rank of the one-process-per-GPU mode) and ``xfer``
@@ -36,7 +99,7 @@ def run_program(desc: dict, plan: dict, inputs: dict, owned_lanes=None, exchange
             x = np.asarray(inputs[b["pt"]], dtype=np.float64)
             sl = tuple(slice(lo, hi) for lo, hi in b["region"])
             data[b["id"]] = x[sl].reshape(-1).copy()
-    shape = {b["id"]: [hi - lo for lo, hi in b["region"]] for b in desc["buffers"]}
+    shape = buffer_shapes(desc)
     for iid in desc["issue_order"]:
         ins = desc["instrs"][iid]
         k = ins["kind"]
@@ -53,59 +116,7 @@ def run_program(desc: dict, plan: dict, inputs: dict, owned_lanes=None, exchange
             continue
         if not lane_ok(ins["lane"]):
             continue
-        if k == "gemm":
-            for g in range(ins.get("group", 1)):  # grouped launch: member g = (in[2g], in[2g+1]) -> out[g]
-                a = data[ins["in"][2 * g]].reshape(shape[ins["in"][2 * g]])
-                b = data[ins["in"][2 * g + 1]].reshape(shape[ins["in"][2 * g + 1]])
-                a = a.T if ins["ta"] else a
-                b = b.T if ins["tb"] else b
-                data[ins["out"][g]] = (a @ b).reshape(-1)
-            for f in ins.get("fused", []):  # elementwise consumers run in the GEMM epilogue
-                out = data[f["in"][0]].copy()
-                for x in f["in"][1:]:
-                    out = (out + data[x], out * data[x], np.maximum(out, data[x]))[f["ew"]]
-                data[f["out"]] = out
-        elif k == "ew":
-            out = data[ins["in"][0]].copy()
-            for x in ins["in"][1:]:
-                out = (out + data[x], out * data[x], np.maximum(out, data[x]))[ins["ew"]]
-            data[ins["out"][0]] = out
-        elif k == "reduce":
-            x = data[ins["in"][0]].reshape(ins["outer"], ins["axis_len"], ins["inner"])
-            data[ins["out"][0]] = x.sum(axis=1).reshape(-1)
-        elif k == "emb_lookup":
-            idx = data[ins["in"][0]].astype(np.int64)
-            tab = data[ins["in"][1]].reshape(ins["rows"], ins["h"])
-            out = np.zeros((ins["n_idx"], ins["h"]))
-            ok = (idx >= ins["lo"]) & (idx < ins["lo"] + ins["rows"])
-            out[ok] = tab[idx[ok] - ins["lo"]]
-            data[ins["out"][0]] = out.reshape(-1)
-        elif k == "emb_grad":
-            idx = data[ins["in"][0]].astype(np.int64)
-            g = data[ins["in"][1]].reshape(ins["n_idx"], ins["h"])
-            out = np.zeros((ins["rows"], ins["h"]))
-            for j in range(ins["n_idx"]):
-                if ins["lo"] <= idx[j] < ins["lo"] + ins["rows"]:
-                    out[idx[j] - ins["lo"]] += g[j]
-            data[ins["out"][0]] = out.reshape(-1)
-        elif k == "rowwise":  # schema extension: row-wise sub-operators / GELU
-            from oracle import planc_oracle as po
-
-            names = ["softmax", "softmax-grad", "layernorm", "layernorm-grad", "gelu", "gelu-grad"]
-            seg = ins["seg"] if ins["row_op"] < 4 else 1
-            xs = [data[b].reshape(-1, seg) for b in ins["in"]]
-            data[ins["out"][0]] = po.eval_ext(names[ins["row_op"]], xs, seg, ins["eps"]).reshape(-1)
-        elif k == "box":
-            ob = ins["out"][0]
-            out = data[ob].copy()  # a box writes only its cells (two-phase all-reduce: two boxes per output)
-            for c in ins["cells"]:
-                di = _strided_view(out, c["dst_off"], c["dst_str"], c["ext"])
-                v = np.zeros(di.shape)
-                for t in c["terms"]:
-                    si = _strided_view(data[t["buf"]], t["off"], t["str"], c["ext"])
-                    v = v + data[t["buf"]][si] if t["add"] else data[t["buf"]][si].copy()
-                out[di] = v
-            data[ob] = out
+        exec_instr(ins, data, shape)
     if return_buffers:
         return data
     return reassemble(desc, plan, data)
