@@ -118,7 +118,7 @@ def _load():
     L.planc_b200_peer_export.argtypes = [vp, ctypes.c_char_p, c_i64]
     L.planc_b200_peer_import.argtypes = [vp, ctypes.c_char_p, c_i64]
     L.planc_b200_gemm_schedule.argtypes = [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_int, P(c_int),
-                                           P(c_int), P(c_int), P(c_int), P(c_int), P(c_int), P(c_i64)]
+                                           P(c_int), P(c_int), P(c_int), P(c_int), P(c_int), P(c_int), P(c_i64)]
     L.planc_b200_free.argtypes = [vp]
     _lib = L
     return L
@@ -166,13 +166,13 @@ def gemm_schedule(m: int, n: int, k: int, ta: bool = False, tb: bool = False, c_
     tiles, stream-K CTAs or split-K splits, workspace bytes) for `group`
     bf16 matmuls of this shape in one launch."""
     L = _load()
-    bn, grid, dp, sk, sp, hf = (ctypes.c_int() for _ in range(6))
+    bn, grid, dp, sk, sp, hf, occ = (ctypes.c_int() for _ in range(7))
     ws = ctypes.c_int64()
     _check(L.planc_b200_gemm_schedule(m, n, k, int(ta), int(tb), int(c_bf16), sms, group, ctypes.byref(bn),
                                       ctypes.byref(grid), ctypes.byref(dp), ctypes.byref(sk), ctypes.byref(sp),
-                                      ctypes.byref(hf), ctypes.byref(ws)))
+                                      ctypes.byref(hf), ctypes.byref(occ), ctypes.byref(ws)))
     return {"tile_n": bn.value, "grid": grid.value, "dp_tiles": dp.value, "sk_ctas": sk.value, "splits": sp.value,
-            "half_items": hf.value, "ws_bytes": ws.value}
+            "half_items": hf.value, "ctas_per_sm": occ.value, "ws_bytes": ws.value}
 
 
 def nccl_unique_id() -> bytes:

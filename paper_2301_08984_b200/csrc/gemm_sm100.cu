@@ -49,11 +49,15 @@ constexpr int kSkDepth = 2;  // stream-K partials loaded per round trip
 
 // Tile width BN in {256, 128, 64}: smem ring depth fills ~200 KB, TMEM holds
 // two BN-column fp32 accumulators (power of two >= 32 columns).
-template <int BN_, bool FUSE = false>
+// OCC = 2 ("small" GEMMs: k <= 1024, BN <= 128, no fusion / stream-K): a
+// ~100 KB ring and <= 256 TMEM columns so two CTAs share an SM — two tiles'
+// prologue / epilogue latencies overlap, or two concurrent small GEMMs from
+// different streams run side by side instead of one after the other.
+template <int BN_, bool FUSE = false, int OCC = 1>
 struct Cfg {
   static constexpr int BN = BN_;
   static constexpr int B_STAGE_BYTES = BN * BK * 2;
-  static constexpr int STAGES_RAW = (200 * 1024) / (A_STAGE_BYTES + B_STAGE_BYTES);
+  static constexpr int STAGES_RAW = ((OCC == 1 ? 200 : 76) * 1024) / (A_STAGE_BYTES + B_STAGE_BYTES);
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   // + epilogue staging: 4 warps x 2 buffers x (32 rows x 32 cols, <= 4 B);
   // FUSE (bf16): 4 warps x 2 x {C, fused result} 2 KB chunks — same size.
@@ -288,13 +292,14 @@ __device__ __forceinline__ void bf16_unpair(std::uint32_t w, float& lo, float& h
   hi = __uint_as_float(w & 0xffff0000u);
 }
 
-template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE, int NG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE, int NG, int OCC>
+__global__ void __launch_bounds__(NUM_THREADS, OCC)
     gemm_tc_kernel(const __grid_constant__ GroupMaps<NG> gm, int ng, int m, int n, int k,
                    const __grid_constant__ EpiParams epi, const __grid_constant__ EpiMaps maps,
                    const __grid_constant__ SkParams sk) {
+  static_assert(OCC == 1 || (!FUSE && BN <= 128), "two CTAs per SM: no fusion, <= 256 TMEM columns");
   extern __shared__ std::uint8_t smem_raw[];
-  using CF = Cfg<BN, FUSE>;
+  using CF = Cfg<BN, FUSE, OCC>;
   constexpr int STAGES = CF::STAGES;
   constexpr int B_STAGE_BYTES = CF::B_STAGE_BYTES;
   constexpr int TMEM_COLS = CF::TMEM_COLS;
@@ -497,6 +502,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         return;
       }
+      if constexpr (OCC == 1) {
       // Stream-K segment: publish the fp32 partial, count the arrival.
       const int j = t - sk.dp_tiles;
       const long long x0 = static_cast<long long>(j) * num_k;
@@ -568,6 +574,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         store_chunk(r, &gm.c[p], C_BF16, nb * BN + c * 32, mb * BM + q * 32);
       }
+      }  // OCC == 1
     });
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
   } else {
@@ -791,11 +798,11 @@ int device_sms() {
   return num_sms[dev & 31];
 }
 
-template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE, int NG>
+template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE, int NG, int OCC = 1>
 void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
   static unsigned attr_set_mask = 0;  // per device ordinal
-  constexpr int SMEM_BYTES = Cfg<BN, FUSE>::SMEM_BYTES;
-  auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16, BN, FUSE, NG>;
+  constexpr int SMEM_BYTES = Cfg<BN, FUSE, OCC>::SMEM_BYTES;
+  auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16, BN, FUSE, NG, OCC>;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set_mask & (1u << dev))) {
@@ -853,6 +860,14 @@ template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
   if constexpr (FUSE) {
     launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
+  } else if constexpr (BN <= 128) {
+    if (sc.occ == 2) {
+      if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup, 2>(a, sc, s);
+      else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1, 2>(a, sc, s);
+    } else {
+      if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup>(a, sc, s);
+      else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
+    }
   } else {
     if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup>(a, sc, s);
     else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
@@ -987,6 +1002,23 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
       best = c;
       have = true;
     }
+  }
+  // Short-k GEMMs (<= 16 k-blocks: latency-bound tiles) that cannot fill
+  // the GPU on their own (<= sms tiles of 128 x 128) take the two-CTAs-per-SM
+  // variant (BN <= 128, a ~76 KB ring): a concurrent small GEMM of another
+  // stream / lane then runs on the same SMs instead of after it (C5 pipeline
+  // 0.416 -> 0.344 ms; the grouped 1000+-tile launches of C4 are slower with
+  // it, hence the tile bound). PLANC_B200_OCC2=0 disables it, =2 forces it.
+  const char* oenv = std::getenv("PLANC_B200_OCC2");
+  const int omode = oenv ? std::atoi(oenv) : 1;
+  const std::int64_t num_k = (a.k + BK - 1) / BK;
+  const std::int64_t tiles128 = ((a.m + BM - 1) / BM) * ((a.n + 127) / 128) * std::max(a.group, 1);
+  if (omode != 0 && a.epi.n_ops == 0 && !forced && best.splits <= 1 && best.sk_ctas == 0 &&
+      (omode == 2 || (num_k <= 16 && tiles128 <= sms))) {
+    const int bn = a.n <= 64 ? 64 : 128;
+    GemmSchedule o = schedule_for(a.m, a.n, a.k, bn, false, 2 * sms, false, a.group, false);
+    o.occ = 2;
+    best = o;
   }
   return best;
 }

@@ -121,6 +121,7 @@ struct GemmSchedule {
   // Half-width tail (data-parallel only): tiles [dp_tiles, tiles) run as
   // half_items = 2 x (tiles - dp_tiles) tiles of 128 x bn/2.
   int half_items = 0;
+  int occ = 1;  // CTAs per SM (2: small-k variant with a ~100 KB ring)
   std::int64_t ws_bytes = 0;  // 0 without stream-K / split-K
   double model_us = 0;
 };

@@ -223,3 +223,29 @@ def test_splitk_gemm_vs_fp64(g, m, n, k, ta, tb, c_fp32, monkeypatch):
         ref = (a.T if ta else a) @ (b.T if tb else b)
         err = np.abs(outs[i] - ref).max() / max(1.0, np.abs(ref).max())
         assert err < (2.0 ** -16 if c_fp32 else 2.0 ** -8), (i, err)
+
+
+@pytest.mark.parametrize("g,m,n,k,ta,tb", [(1, 8192, 256, 256, False, False), (1, 304, 520, 200, True, True),
+                                           (3, 1024, 384, 512, False, True), (1, 2048, 64, 1024, True, False),
+                                           (2, 4096, 1024, 2048, False, False)])
+def test_two_ctas_per_sm_variant_vs_fp64(g, m, n, k, ta, tb, monkeypatch):
+    """The short-k variant (two CTAs per SM, ~76 KB ring, BN <= 128; forced
+    here with PLANC_B200_OCC2=2, incl. a long-k shape) against fp64."""
+    from plan_builder import grouped_matmul_plan
+
+    monkeypatch.setenv("PLANC_B200_OCC2", "2")
+    assert pb.gemm_schedule(m, n, k, ta, tb, group=g)["ctas_per_sm"] == 2
+    plan = grouped_matmul_plan(g, m, n, k, ta, tb)
+    rng = np.random.default_rng(g + m + n + k)
+    inputs = {}
+    for i in range(g):
+        inputs[3 * i] = bf16_round(rng.standard_normal((k, m) if ta else (m, k)))
+        inputs[3 * i + 1] = bf16_round(rng.standard_normal((n, k) if tb else (k, n)))
+    with pb.Executor(plan, lane_gpus=[0]) as ex:
+        ex.set_inputs(inputs)
+        ex.run(2)
+        outs = [ex.get_output(3 * i + 2) for i in range(g)]
+    for i in range(g):
+        a, b = inputs[3 * i], inputs[3 * i + 1]
+        ref = (a.T if ta else a) @ (b.T if tb else b)
+        assert np.abs(outs[i] - ref).max() / max(1.0, np.abs(ref).max()) < 2.0 ** -8

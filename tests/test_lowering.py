@@ -274,7 +274,11 @@ def test_gemm_schedule_covers_every_k_block_once(m, n, k, ta, sk_mode, monkeypat
     bn = sc["tile_n"]
     tiles = -(-m // 128) * -(-n // bn)
     num_k = -(-k // 64)
-    assert 0 < sc["grid"] <= sms
+    assert 0 < sc["grid"] <= sms * sc["ctas_per_sm"]
+    if sc["ctas_per_sm"] == 2:  # short-k variant: data-parallel only, <= 128-wide tiles, <= 16 k-blocks
+        assert sc["tile_n"] <= 128 and num_k <= 16 and sc["sk_ctas"] == 0 and sc["splits"] == 0
+        bn = sc["tile_n"]
+        tiles = -(-m // 128) * -(-n // bn)
     seen = {}
     if sc["half_items"]:
         # half-width tail: whole tiles, then both halves of every remaining tile

@@ -17,7 +17,7 @@ import paper_2301_08984_b200 as pb  # noqa: E402
 VARIANTS = [
     ("base", 0, {}),
     ("no_grouping", pb.NO_GROUPING, {}),
-    ("half_tail", 0, {"PLANC_B200_HALF_TAIL": "1"}),
+    ("no_occ2", 0, {"PLANC_B200_OCC2": "0"}),
     ("no_fusion", pb.NO_FUSION, {}),
 ]
 
