@@ -48,6 +48,8 @@ extern "C" {
                                            fresh bf16 GEMM output on the same lane runs in that GEMM's
                                            epilogue — same bits as the separate kernel */
 #define PLANC_B200_NO_FUSION 0x80u      /* every elementwise op its own kernel (no epilogue fusion) */
+#define PLANC_B200_NO_ALIAS 0x100u      /* copy even when a whole-buffer copy (recv, identity) stays on one
+                                           GPU (default: the output aliases the source, no kernel) */
 #define PLANC_B200_PEER_MEMORY 0x20u     /* planc_b200_open_rank / describe_rank: peer-memory transport
                                            (CUDA IPC over NVLink, device flags) instead of NCCL */
 #define PLANC_B200_NO_GROUPING 0x40u    /* every GEMM its own launch (default: independent same-shape

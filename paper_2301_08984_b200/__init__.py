@@ -40,6 +40,7 @@ FUSE_EPILOGUES = 0x10  # default on; NO_FUSION turns it off
 PEER_MEMORY = 0x20
 NO_GROUPING = 0x40
 NO_FUSION = 0x80
+NO_ALIAS = 0x100
 
 
 class PlancError(RuntimeError):

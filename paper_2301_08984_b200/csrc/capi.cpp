@@ -71,6 +71,7 @@ int planc_b200_open(const char* plan_json, const int* lane_gpu, int num_lane_gpu
     if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
     opt.fuse_epilogues = (flags & PLANC_B200_NO_FUSION) == 0;
     opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
+    opt.alias_copies = (flags & PLANC_B200_NO_ALIAS) == 0;
     std::vector<int> lanes;
     for (int i = 0; lane_gpu && i < num_lane_gpu; ++i) lanes.push_back(lane_gpu[i]);
     auto* h = new planc_b200_exec;
@@ -106,6 +107,7 @@ int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* 
     if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
     opt.fuse_epilogues = (flags & PLANC_B200_NO_FUSION) == 0;
     opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
+    opt.alias_copies = (flags & PLANC_B200_NO_ALIAS) == 0;
     RankConfig rc;
     rc.rank = rank;
     rc.world = world;

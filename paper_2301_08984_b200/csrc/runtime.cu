@@ -302,6 +302,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
     lane_mapped_.assign(prog_.num_lanes, false);
     // Box tables need every rank's arena: built by peer_import.
   } else {
+    plan_aliases();
     build_box_tables();
   }
   kernels_per_step_ = 0;
@@ -396,8 +397,37 @@ bool Executor::gemm_streamk_ok(int lane) const {
 }
 
 void* Executor::buf_ptr(int b) const {
+  while (!alias_.empty() && alias_[b] >= 0) b = alias_[b];
   const BufferDesc& d = prog_.buffers[b];
   return lanes_[d.lane].arena + d.offset;
+}
+
+// A box instruction that copies one whole buffer into another of the same
+// dense layout (a recv whose send lane shares the GPU, an identity op) moves
+// no data when both lanes' arenas sit in the same HBM: the output becomes an
+// alias of the source (single assignment: neither is rewritten within the
+// step) and the instruction launches nothing — its events still order its
+// consumers after its producers. Across GPUs or ranks the copy stays.
+void Executor::plan_aliases() {
+  alias_.assign(prog_.buffers.size(), -1);
+  if (rank_mode_ || !opt_.alias_copies) return;
+  std::vector<int> writers(prog_.buffers.size(), 0);
+  for (const auto& in : prog_.instrs)
+    for (int b : in.out_bufs) ++writers[b];
+  for (const auto& in : prog_.instrs) {
+    if (in.kind != InstrKind::box || exec_lane_[in.id] < 0 || in.out_bufs.size() != 1 || in.cells.size() != 1) continue;
+    const Cell& c = in.cells[0];
+    if (c.terms.size() != 1 || c.terms[0].add || c.rank != 1 || c.dst_offset != 0 || c.dst_strides[0] != 1 ||
+        c.terms[0].offset != 0 || c.terms[0].strides[0] != 1)
+      continue;
+    const BufferDesc& ob = prog_.buffers[in.out_bufs[0]];
+    const BufferDesc& sb = prog_.buffers[c.terms[0].buffer];
+    if (ob.graph_input || writers[ob.id] != 1 || ob.dtype != sb.dtype || ob.elems != sb.elems || c.elems() != ob.elems)
+      continue;
+    if (!owned_[sb.lane] || lanes_[ob.lane].gpu != lanes_[sb.lane].gpu) continue;
+    alias_[ob.id] = sb.id;
+    irt_[in.id].aliased = true;
+  }
 }
 
 cudaStream_t Executor::stream_of(const Instr& in) const {
@@ -581,8 +611,9 @@ void Executor::check_sync(cudaError_t e, const char* what) const {
 
 void Executor::build_box_tables() {
   constexpr std::int64_t kChunkUnits = kBoxChunkUnits;
+  if (alias_.empty()) alias_.assign(prog_.buffers.size(), -1);
   for (const auto& in : prog_.instrs) {
-    if (in.kind != InstrKind::box || exec_lane_[in.id] < 0) continue;
+    if (in.kind != InstrKind::box || exec_lane_[in.id] < 0 || irt_[in.id].aliased) continue;
     const BufferDesc& ob = prog_.buffers[in.out_bufs[0]];
     const std::int64_t V = 16 / dtype_size(ob.dtype);
     std::vector<const Cell*> groups[2];
@@ -1174,7 +1205,8 @@ std::vector<KernelStat> Executor::profile() {
       case InstrKind::xfer: kind = "xfer_nccl"; break;
       case InstrKind::box:
         // Collective member outputs are labelled "<primitive>:<op>".
-        kind = in.label.find(':') != std::string::npos ? "box_collective"
+        kind = irt_[in.id].aliased                      ? "alias"
+               : in.label.find(':') != std::string::npos ? "box_collective"
                : in.wire_bytes > 0                     ? "box_p2p"
                                                        : "box_local";
         break;

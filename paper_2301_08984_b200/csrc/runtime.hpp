@@ -50,6 +50,7 @@ struct ExecOptions {
   int streams_per_lane = kLaneStreams;  // 1 = issue a lane strictly in plan order
   bool fuse_epilogues = true;           // elementwise consumers computed in GEMM epilogues
   bool group_gemms = true;              // same-shape independent GEMMs in one grouped launch
+  bool alias_copies = true;             // same-GPU whole-buffer copies (recv, identity) become aliases
 };
 
 // ProgramOptions as the executor uses them: epilogue fusion only for GEMMs
@@ -146,11 +147,13 @@ class Executor {
   };
   struct InstrRt {
     std::vector<BoxLaunch> box;
+    bool aliased = false;        // whole-buffer copy on one GPU: output shares the source's memory
     cudaEvent_t done = nullptr;  // recorded when a later instruction on another stream depends on it
     float* scratch = nullptr;
   };
 
   void* buf_ptr(int b) const;
+  void plan_aliases();
   bool gemm_streamk_ok(int lane) const;  // the lane has its GPU to itself
   cudaStream_t stream_of(const Instr& in) const;
   void build_box_tables();
@@ -197,6 +200,7 @@ class Executor {
   int first_lane_ = 0;          // first lane this process runs (origin stream's device)
   std::vector<LaneRt> lanes_;
   std::vector<InstrRt> irt_;
+  std::vector<int> alias_;  // per buffer: -1, or the buffer whose memory it shares
   std::vector<int> gpus_;  // distinct devices
   std::vector<void*> table_allocs_;
   std::map<int, HostTensor> inputs_;

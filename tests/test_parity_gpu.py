@@ -37,7 +37,7 @@ def test_golden_plan_parity(name):
 @pytest.mark.parametrize("name", ["mlp_dp2", "gpt_block_tp2", "embed_shard2", "adapt_d1_to_d0_4",
                                   "three_pass_3f1b", "gpt_block_fwd_tp2_mma"])
 @pytest.mark.parametrize("flags", [pb.NO_GRAPH, pb.NO_TENSOR_CORES, pb.SERIAL_LANES, pb.NO_GRAPH | pb.SERIAL_LANES,
-                                   pb.NO_FUSION, pb.NO_FUSION | pb.NO_GRAPH])
+                                   pb.NO_FUSION, pb.NO_FUSION | pb.NO_GRAPH, pb.NO_ALIAS, pb.NO_GROUPING])
 def test_parity_across_launch_modes(name, flags):
     g = golden_cases.load(name)
     out, _ = _run(g["plan"], g["inputs"], flags=flags)
@@ -115,3 +115,24 @@ def test_profile_reports_kernel_families():
         prof = ex.profile()
     kinds = {p["kind"] for p in prof}
     assert "box_collective" in kinds and any(k.startswith("gemm") for k in kinds)
+
+
+def test_same_gpu_copies_become_aliases():
+    """A recv whose send lane shares the GPU and identity ops launch nothing
+    (the output aliases the source); results unchanged; NO_ALIAS copies."""
+    g = golden_cases.load("mlp_1f1b_dp2")
+    n = len(json.loads(g["plan"])["lanes"])
+    outs, kernels = {}, {}
+    for flags in (0, pb.NO_ALIAS):
+        with pb.Executor(g["plan"], lane_gpus=[0] * n, flags=flags) as ex:
+            ex.set_inputs(g["inputs"])
+            ex.run(2)
+            outs[flags] = ex.outputs()
+            kernels[flags] = ex.stats()["kernels_per_step"]
+            kinds = {p["kind"] for p in ex.profile()}
+        assert ("alias" in kinds) == (flags == 0)
+    assert kernels[0] < kernels[pb.NO_ALIAS]
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[pb.NO_ALIAS][k])
+    ok, msg = pb.compare_outputs(g["expected"], outs[0], 0.0)
+    assert ok, msg
