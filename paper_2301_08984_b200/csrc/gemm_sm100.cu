@@ -977,9 +977,12 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   // PLANC_B200_SPLITK=0 disables split-K, =2 takes it whenever it applies.
   const char* spenv = std::getenv("PLANC_B200_SPLITK");
   const int splitmode = spenv ? std::atoi(spenv) : 1;
-  // Like stream-K, split-K trades SM-time for latency: only when the lane
-  // has its GPU to itself (co-resident lanes would be starved of SMs).
-  const bool allow_split = splitmode != 0 && a.epi.n_ops == 0 && (a.allow_streamk || splitmode == 2);
+  // Like stream-K, split-K trades SM-time for latency: over the whole GPU
+  // when the lane has it to itself, over at most a quarter of the SMs when
+  // co-resident lanes share it (their concurrent work keeps the rest; C5's
+  // 256 x 256 x 8192 weight gradients: 4 CTAs for ~40 us -> 36 CTAs).
+  const bool allow_split = splitmode != 0 && a.epi.n_ops == 0;
+  const int split_sms = (a.allow_streamk || splitmode == 2) ? sms : std::max(1, sms / 4);
   GemmSchedule best;
   bool have = false;
   for (int bn : {256, 128, 64}) {
@@ -995,7 +998,7 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
     GemmSchedule sk = schedule_for(a.m, a.n, a.k, bn, allow_sk, sms, skmode == 2, a.group, allow_half);
     GemmSchedule c = (sk.sk_ctas > 0 && (skmode == 2 || sk.model_us < 0.9 * dp.model_us)) ? sk : dp;
     if (allow_split) {
-      GemmSchedule sp = splitk_for(a.m, a.n, a.k, bn, sms, a.group, a.dc == DT_BF16 ? 2 : 4);
+      GemmSchedule sp = splitk_for(a.m, a.n, a.k, bn, split_sms, a.group, a.dc == DT_BF16 ? 2 : 4);
       if (sp.splits > 1 && (splitmode == 2 || sp.model_us < 0.9 * c.model_us)) c = sp;
     }
     if (!have || c.model_us < best.model_us * 0.97) {
