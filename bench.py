@@ -337,7 +337,9 @@ def main():
         # F/P + M/HBM vs W/NVLink, against the measured sustained peaks, from
         # the host lowering's per-instruction algorithmic work. Lanes sharing
         # a GPU add up; their adapter bytes then stay in HBM (no NVLink).
-        desc = pb.describe(plan)
+        # algorithmic work of the PLAN (every elementwise op and copy counted,
+        # whatever the executor fuses, groups or aliases)
+        desc = pb.describe(plan, flags=pb.NO_FUSION | pb.NO_GROUPING)
         gpu_of = [lane % n for lane in range(nlanes)]
         F, M, W = [0.0] * n, [0.0] * n, [0.0] * n
         for ins in desc["instrs"]:
@@ -378,8 +380,10 @@ def main():
                            "CUDA graph" if st["graph_captured"] else "eager")},
             "roofline": roof,
             "plan_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
-                              "gemm_tflop_per_step": st["flops"] / 1e12, "hbm_gb_per_step": st["hbm_bytes"] / 1e9,
-                              "wire_gb_per_step": st["wire_bytes"] / 1e9,
+                              "gemm_tflop_per_step": sum(F) / 1e12, "hbm_gb_per_step": sum(M) / 1e9,
+                              "wire_gb_per_step": sum(W) / 1e9,
+                              "work": "the plan's algorithmic work (describe with NO_FUSION | NO_GROUPING): every "
+                                      "elementwise op and copy counted, whatever the executor fuses or aliases",
                               "peaks": {"bf16_tflops": peaks["bf16_sus"], "hbm_gbs": peaks["hbm"],
                                         "nvlink_gbs": NVLINK_GBS, "source": peaks["src"] + " (sustained bf16)"}},
             "adapter_bus_gbs": (None if not coll or coll["wire"] == 0 else

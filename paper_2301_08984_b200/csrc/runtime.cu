@@ -1193,8 +1193,9 @@ std::vector<KernelStat> Executor::profile() {
         g.da = dt_of(prog_.buffers[in.in_bufs[0]].dtype);
         g.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
         g.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
+        // One family per GEMM path: a fused elementwise epilogue is part of
+        // the GEMM kernel (its flops stay the GEMM's; the fused op's bytes ride along).
         kind = opt_.allow_tensor_cores && gemm_sm100_eligible(g) ? "gemm_tc" : "gemm_simt";
-        if (!in.fused.empty()) kind += "_fused" + std::to_string(in.fused.size());
         break;
       }
       case InstrKind::ew: kind = "ew"; break;

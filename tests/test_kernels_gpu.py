@@ -234,6 +234,7 @@ def test_two_ctas_per_sm_variant_vs_fp64(g, m, n, k, ta, tb, monkeypatch):
     from plan_builder import grouped_matmul_plan
 
     monkeypatch.setenv("PLANC_B200_OCC2", "2")
+    monkeypatch.setenv("PLANC_B200_SPLITK", "0")
     assert pb.gemm_schedule(m, n, k, ta, tb, group=g)["ctas_per_sm"] == 2
     plan = grouped_matmul_plan(g, m, n, k, ta, tb)
     rng = np.random.default_rng(g + m + n + k)
