@@ -321,8 +321,13 @@ def main():
             pass
         if top.startswith("gemm"):
             achieved = t["flops"] / (t["ms"] / 1e3) / 1e12
-            roof = {"kernel": top, "bound": "tensor", "achieved": achieved, "peak": peaks["bf16"],
-                    "unit": "TFLOP/s", "frac": achieved / peaks["bf16"], "traffic": traffic,
+            # fused elementwise epilogues add their operand / result bytes at
+            # HBM speed to the tensor-bound time (0 without fusion)
+            t_bound_s = t["flops"] / (peaks["bf16"] * 1e12) + t["bytes"] / (peaks["hbm"] * 1e9)
+            roof = {"kernel": top, "bound": "tensor (+ fused-epilogue bytes at HBM)", "achieved": achieved,
+                    "peak": peaks["bf16"], "unit": "TFLOP/s", "frac": t_bound_s / (t["ms"] / 1e3),
+                    "frac_tensor_only": achieved / peaks["bf16"],
+                    "fused_epilogue_gb_per_step": t["bytes"] / 1e9, "traffic": traffic,
                     "traffic_source": traffic_src,
                     "peak_source": peaks["src"] + " burst (kernels timed individually)",
                     "share_of_step": t["ms"] / total_prof,

@@ -1221,7 +1221,18 @@ std::vector<KernelStat> Executor::profile() {
     st.launches += 1;
     st.ms += ms;
     st.flops += in.flops;
-    st.bytes += in.bytes;
+    if (in.kind == InstrKind::gemm) {
+      // GEMM families: only the bytes of fused elementwise epilogues (the
+      // operand / result traffic of a compute-bound GEMM is not its bound).
+      double base = 0;
+      for (std::size_t i = 0; i < static_cast<std::size_t>(2 * in.group) && i < in.in_bufs.size(); ++i)
+        base += static_cast<double>(prog_.buffers[in.in_bufs[i]].bytes);
+      for (int i = 0; i < in.group && i < static_cast<int>(in.out_bufs.size()); ++i)
+        base += static_cast<double>(prog_.buffers[in.out_bufs[i]].bytes);
+      st.bytes += in.fused.empty() ? 0.0 : std::max(0.0, in.bytes - base);
+    } else {
+      st.bytes += in.bytes;
+    }
     st.wire_bytes += in.wire_bytes;
   }
   {
