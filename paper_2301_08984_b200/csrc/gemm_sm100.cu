@@ -603,8 +603,10 @@ __global__ void __launch_bounds__(NUM_THREADS, OCC)
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const bool ok = grow < m && gcol + 8 * v < n;  // n % 8 == 0: whole vectors
-        d[0][v] = ok && nst > 0 ? __ldg(reinterpret_cast<const uint4*>(src0 + off) + v) : make_uint4(0, 0, 0, 0);
-        d[1][v] = ok && nst > 1 ? __ldg(reinterpret_cast<const uint4*>(src1 + off) + v) : make_uint4(0, 0, 0, 0);
+        // Streaming loads (evict-first): the fused operand is read once and
+        // must not push the GEMM's A / B panels out of L2.
+        d[0][v] = ok && nst > 0 ? __ldcs(reinterpret_cast<const uint4*>(src0 + off) + v) : make_uint4(0, 0, 0, 0);
+        d[1][v] = ok && nst > 1 ? __ldcs(reinterpret_cast<const uint4*>(src1 + off) + v) : make_uint4(0, 0, 0, 0);
       }
     };
     int g = 0;  // chunk counter of this warp (staging ring position)
