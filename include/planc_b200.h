@@ -48,6 +48,10 @@ extern "C" {
                                            fresh bf16 GEMM output on the same lane runs in that GEMM's
                                            epilogue — same bits as the separate kernel */
 #define PLANC_B200_NO_FUSION 0x80u      /* every elementwise op its own kernel (no epilogue fusion) */
+#define PLANC_B200_NO_SCATTER 0x200u    /* all-reduce partials stored whole by their GEMM and pulled by the
+                                           reduce-scatter phase (default: a GEMM whose output only feeds an
+                                           all-reduce stores each row slice straight into the receive buffer
+                                           of the lane owning it — the transfer rides in the GEMM epilogue) */
 #define PLANC_B200_NO_ALIAS 0x100u      /* copy even when a whole-buffer copy (recv, identity) stays on one
                                            GPU (default: the output aliases the source, no kernel) */
 #define PLANC_B200_PEER_MEMORY 0x20u     /* planc_b200_open_rank / describe_rank: peer-memory transport

@@ -41,6 +41,7 @@ PEER_MEMORY = 0x20
 NO_GROUPING = 0x40
 NO_FUSION = 0x80
 NO_ALIAS = 0x100
+NO_SCATTER = 0x200
 
 
 class PlancError(RuntimeError):

@@ -72,6 +72,7 @@ int planc_b200_open(const char* plan_json, const int* lane_gpu, int num_lane_gpu
     opt.fuse_epilogues = (flags & PLANC_B200_NO_FUSION) == 0;
     opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
     opt.alias_copies = (flags & PLANC_B200_NO_ALIAS) == 0;
+    opt.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0;
     std::vector<int> lanes;
     for (int i = 0; lane_gpu && i < num_lane_gpu; ++i) lanes.push_back(lane_gpu[i]);
     auto* h = new planc_b200_exec;
@@ -108,6 +109,7 @@ int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* 
     opt.fuse_epilogues = (flags & PLANC_B200_NO_FUSION) == 0;
     opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
     opt.alias_copies = (flags & PLANC_B200_NO_ALIAS) == 0;
+    opt.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0;
     RankConfig rc;
     rc.rank = rank;
     rc.world = world;
@@ -134,6 +136,7 @@ int planc_b200_describe_rank(const char* plan_json, const int* lane_rank, int nu
                                         (flags & PLANC_B200_NO_FUSION) == 0 &&
                                             (flags & PLANC_B200_NO_TENSOR_CORES) == 0);
     po.group_gemms = (flags & (PLANC_B200_NO_GROUPING | PLANC_B200_NO_TENSOR_CORES)) == 0;
+    po.scatter_allreduce = (flags & (PLANC_B200_NO_SCATTER | PLANC_B200_NO_TENSOR_CORES)) == 0;
     ExecutionPlan plan = load_plan(plan_json);
     const std::vector<int> lr(lane_rank, lane_rank + num_lanes);
     if ((flags & PLANC_B200_PEER_MEMORY) == 0) {
@@ -374,6 +377,7 @@ int planc_b200_describe(const char* plan_json, uint32_t flags, char** json_out) 
                                         (flags & PLANC_B200_NO_FUSION) == 0 &&
                                             (flags & PLANC_B200_NO_TENSOR_CORES) == 0);
     po.group_gemms = (flags & (PLANC_B200_NO_GROUPING | PLANC_B200_NO_TENSOR_CORES)) == 0;
+    po.scatter_allreduce = (flags & (PLANC_B200_NO_SCATTER | PLANC_B200_NO_TENSOR_CORES)) == 0;
     ExecutionPlan plan = load_plan(plan_json);
     Program p = build_program(plan, po);
     *json_out = dup(p.describe_json());

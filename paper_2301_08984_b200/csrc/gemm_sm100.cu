@@ -105,6 +105,11 @@ struct SkParams {
   // half_items tiles of 128 x BN/2 (item h: half h & 1 of tile dp_tiles + h / 2),
   // so a last wave of r < grid/2 tiles takes half a tile-time.
   int half_items = 0;
+  // Reduce-scatter epilogue: row y of C goes to row y % scatter_rows of the
+  // [scatter_rows][n] buffer scatter_dst[y / scatter_rows] (0 = off) — by
+  // plain 16-byte stores from registers, valid for NVLink peer memory.
+  int scatter_rows = 0;
+  void* scatter_dst[kMaxGemmGroup] = {};
   long long sk_iters = 0;
   float* partials = nullptr;  // [sk_ctas][2 slots][4 quarters][BN/32 chunks][8][32] float4
   int* counters = nullptr;    // [(tiles - dp_tiles) * 4], zero between launches
@@ -497,8 +502,33 @@ __global__ void __launch_bounds__(NUM_THREADS, OCC)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
           }
-          if (part) store_chunk(r, &maps.ws, false, x0 + c * 32, y);
-          else store_chunk(r, &gm.c[p], C_BF16, x0 + c * 32, y);
+          if (part) {
+            store_chunk(r, &maps.ws, false, x0 + c * 32, y);
+          } else if (sk.scatter_rows > 0) {
+            // lane = row of the 32-row chunk: 32 columns straight to the
+            // owner's receive buffer (64 B bf16 / 128 B fp32 per lane).
+            const int row = y + lane, col = x0 + c * 32;
+            const int dst_i = row / sk.scatter_rows;
+            char* dst = static_cast<char*>(sk.scatter_dst[dst_i]) +
+                        (static_cast<std::int64_t>(row - dst_i * sk.scatter_rows) * n + col) * (C_BF16 ? 2 : 4);
+            if constexpr (C_BF16) {
+#pragma unroll
+              for (int v = 0; v < 4; ++v)
+                if (col + 8 * v < n)
+                  reinterpret_cast<uint4*>(dst)[v] =
+                      make_uint4(bf16_pair(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1])),
+                                 bf16_pair(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
+                                 bf16_pair(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
+                                 bf16_pair(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
+            } else {
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                if (col + 4 * v < n)
+                  reinterpret_cast<uint4*>(dst)[v] = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+            }
+          } else {
+            store_chunk(r, &gm.c[p], C_BF16, x0 + c * 32, y);
+          }
         }
         return;
       }
@@ -825,7 +855,12 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
     void* C = ng > 1 ? a.gC[i] : a.C;
     gm.a[i] = A_MN ? make_map(A, a.k, a.m, BK) : make_map(A, a.m, a.k, BM);
     gm.b[i] = B_MN ? make_map(B, a.k, a.n, BK) : make_map(B, a.n, a.k, BN);
-    gm.c[i] = make_store_map(C, a.m, a.n, C_BF16);
+    gm.c[i] = make_store_map(a.scatter > 0 ? a.gC[0] : C, a.scatter > 0 ? a.scatter_rows : a.m, a.n, C_BF16);
+  }
+  if (a.scatter > 0) {
+    if (a.scatter > kMaxGemmGroup || ng != 1 || FUSE || sc.splits > 1 || sc.sk_ctas > 0 || sc.half_items > 0 ||
+        a.scatter_rows % BM != 0 || a.scatter_rows * a.scatter != a.m)
+      throw std::runtime_error("gemm_tc: reduce-scatter epilogue needs a plain data-parallel launch");
   }
   EpiMaps maps;
   std::memset(&maps, 0, sizeof(maps));
@@ -836,6 +871,8 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
   sk.sk_iters = sc.sk_iters;
   sk.splits = sc.splits;
   sk.half_items = sc.half_items;
+  sk.scatter_rows = a.scatter > 0 ? static_cast<int>(a.scatter_rows) : 0;
+  for (int i = 0; i < a.scatter; ++i) sk.scatter_dst[i] = a.gC[i];
   const std::int64_t m_pad = (a.m + BM - 1) / BM * BM, n_pad = (a.n + BN - 1) / BN * BN;
   if (sc.splits > 1) {
     // Partials: fp32 [ng * splits * m_pad][n_pad], stored like an fp32 C.
@@ -863,11 +900,12 @@ void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
   if constexpr (FUSE) {
     launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
   } else if constexpr (BN <= 128) {
+    const bool wide = a.group > 1;  // member maps
     if (sc.occ == 2) {
-      if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup, 2>(a, sc, s);
+      if (wide) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup, 2>(a, sc, s);
       else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1, 2>(a, sc, s);
     } else {
-      if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup>(a, sc, s);
+      if (wide) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup>(a, sc, s);
       else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
     }
   } else {
@@ -975,7 +1013,7 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   const int forced = env ? std::atoi(env) : 0;
   const char* skenv = std::getenv("PLANC_B200_STREAMK");
   const int skmode = skenv ? std::atoi(skenv) : 1;
-  const bool allow_sk = skmode != 0 && a.epi.n_ops == 0 && (a.allow_streamk || skmode == 2);
+  const bool allow_sk = skmode != 0 && a.epi.n_ops == 0 && a.scatter == 0 && (a.allow_streamk || skmode == 2);
   // PLANC_B200_SPLITK=0 disables split-K, =2 takes it whenever it applies.
   const char* spenv = std::getenv("PLANC_B200_SPLITK");
   const int splitmode = spenv ? std::atoi(spenv) : 1;
@@ -983,7 +1021,7 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   // when the lane has it to itself, over at most a quarter of the SMs when
   // co-resident lanes share it (their concurrent work keeps the rest; C5's
   // 256 x 256 x 8192 weight gradients: 4 CTAs for ~40 us -> 36 CTAs).
-  const bool allow_split = splitmode != 0 && a.epi.n_ops == 0;
+  const bool allow_split = splitmode != 0 && a.epi.n_ops == 0 && a.scatter == 0;
   const int split_sms = (a.allow_streamk || splitmode == 2) ? sms : std::max(1, sms / 4);
   GemmSchedule best;
   bool have = false;
@@ -995,7 +1033,7 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
     // 2-3 % slower — profiles/r01/ab_plans_half_tail.jsonl); the fused
     // epilogue walks whole tiles only.
     const char* hv = std::getenv("PLANC_B200_HALF_TAIL");
-    const bool allow_half = a.epi.n_ops == 0 && hv && hv[0] == '1';
+    const bool allow_half = a.epi.n_ops == 0 && a.scatter == 0 && hv && hv[0] == '1';
     GemmSchedule dp = schedule_for(a.m, a.n, a.k, bn, false, sms, false, a.group, allow_half);
     GemmSchedule sk = schedule_for(a.m, a.n, a.k, bn, allow_sk, sms, skmode == 2, a.group, allow_half);
     GemmSchedule c = (sk.sk_ctas > 0 && (skmode == 2 || sk.model_us < 0.9 * dp.model_us)) ? sk : dp;

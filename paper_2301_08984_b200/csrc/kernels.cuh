@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <stdexcept>
 
 namespace planc_b200 {
 
@@ -83,6 +84,14 @@ struct GemmArgs {
   void* C;
   // group > 1: members 0..group-1 are (gA[i], gB[i], gC[i]); A/B/C unused.
   int group = 1;
+  // Reduce-scatter epilogue (scatter > 0, group == 1): output rows
+  // [i * scatter_rows, (i + 1) * scatter_rows) are stored to gC[i] — each a
+  // [scatter_rows][n] buffer, typically on the rank that owns reduce-scatter
+  // slice i (NVLink peer memory, plain 16-byte stores) — instead of C, tile
+  // by tile as the GEMM runs: the transfer of the partial sums overlaps the
+  // math. C is unused.
+  int scatter = 0;
+  std::int64_t scatter_rows = 0;
   const void* gA[kMaxGemmGroup] = {};
   const void* gB[kMaxGemmGroup] = {};
   void* gC[kMaxGemmGroup] = {};
@@ -185,6 +194,7 @@ void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s);
 inline void launch_gemm(const GemmArgs& a, cudaStream_t s, bool allow_tc, bool* used_tc) {
   bool tc = allow_tc && gemm_sm100_eligible(a);
   if (used_tc) *used_tc = tc;
+  if (a.scatter > 0 && !tc) throw std::runtime_error("reduce-scatter GEMM epilogue needs the tensor-core path");
   if (tc) {
     launch_gemm_sm100(a, s);
   } else if (a.group > 1) {

@@ -769,7 +769,7 @@ struct Builder {
 Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt) {
   Builder b(plan, opt);
   b.run();
-  if (opt.two_phase_allreduce) two_phase_allreduce(b.P);
+  if (opt.two_phase_allreduce) two_phase_allreduce(b.P, opt);
   if (opt.fuse_epilogues) fuse_gemm_epilogues(b.P, opt);
   if (opt.group_gemms && opt.gemm_groupable) group_gemms(b.P, opt);
   return std::move(b.P);
@@ -1025,7 +1025,17 @@ std::vector<int> allreduce_inputs(const Program& P, const std::vector<int>& grp)
 
 }  // namespace
 
-void two_phase_allreduce(Program& g) {
+void two_phase_allreduce(Program& g, const ProgramOptions& opt) {
+  // Which instructions read each buffer (GEMM partials may feed the
+  // all-reduce only, for the reduce-scatter epilogue).
+  std::vector<std::set<int>> readers(g.buffers.size());
+  for (const auto& in : g.instrs) {
+    for (int b : in.in_bufs) readers[b].insert(in.id);
+    for (const auto& c : in.cells)
+      for (const auto& t : c.terms) readers[t.buffer].insert(in.id);
+    for (const auto& f : in.fused)
+      for (int b : f.in_bufs) readers[b].insert(in.id);
+  }
   Program P = g;
   P.instrs.clear();
   P.issue_order.clear();
@@ -1072,6 +1082,75 @@ void two_phase_allreduce(Program& g) {
     std::vector<std::int64_t> bound(k + 1);
     for (std::int64_t j = 0; j <= k; ++j) bound[j] = j == k ? E : (E * j / k) / kAlign * kAlign;
     const std::int64_t es = dtype_size(g.buffers[first.out_bufs[0]].dtype);
+    // Reduce-scatter GEMM epilogue: every partial is the only output of an
+    // (unfused, ungrouped, tensor-core) GEMM read by this group alone, and
+    // the slices fall on 128-row boundaries.
+    const BufferDesc& ob0 = g.buffers[first.out_bufs[0]];
+    std::int64_t rows = 0, cols = 0, rows_per = 0;
+    bool scat = opt.scatter_allreduce && opt.gemm_groupable && k <= kMaxGemmGroupInstr && ob0.shape.size() == 2;
+    if (scat) {
+      rows = ob0.shape[0];
+      cols = ob0.shape[1];
+      rows_per = rows / k;
+      scat = rows % k == 0 && rows_per % 128 == 0;
+    }
+    const std::set<int> members(grp.begin(), grp.end());
+    std::vector<int> gemm_of(k, -1);
+    for (std::int64_t r = 0; scat && r < k; ++r) {
+      const BufferDesc& ib = g.buffers[inputs[r]];
+      const int pr = ib.producer;
+      scat = pr >= 0 && remap[pr] >= 0;
+      if (!scat) break;
+      const Instr& G = g.instrs[pr];
+      scat = G.kind == InstrKind::gemm && G.out_bufs.size() == 1 && G.out_bufs[0] == inputs[r] && G.fused.empty() &&
+             G.group == 1 && G.m == rows && G.n == cols && ib.shape == ob0.shape &&
+             opt.gemm_groupable(G, g.buffers[G.in_bufs[0]].dtype, g.buffers[G.in_bufs[1]].dtype, ib.dtype);
+      for (int rd : readers[inputs[r]]) scat = scat && members.count(rd);
+      gemm_of[r] = pr;
+    }
+    std::vector<std::vector<int>> recv;  // recv[j][r]: slice j of partial r, on member j's lane
+    if (scat) {
+      for (std::int64_t j = 0; j <= k; ++j) bound[j] = j * rows_per * cols;
+      recv.assign(k, std::vector<int>(k, -1));
+      for (std::int64_t j = 0; j < k; ++j) {
+        const int lane = g.instrs[grp[j]].lane;
+        for (std::int64_t r = 0; r < k; ++r) {
+          BufferDesc rb = g.buffers[inputs[r]];
+          rb.id = static_cast<int>(P.buffers.size());
+          rb.lane = lane;
+          const std::int64_t lo = rb.mask.region[0].lo;
+          rb.mask.region[0] = {lo + j * rows_per, lo + (j + 1) * rows_per};
+          rb.shape = {rows_per, cols};
+          rb.elems = rows_per * cols;
+          rb.bytes = rb.elems * es;
+          rb.offset = (P.lane_arena_bytes[lane] + 255) / 256 * 256;
+          P.lane_arena_bytes[lane] = rb.offset + rb.bytes;
+          rb.graph_input = rb.weight = false;
+          rb.producer = gemm_of[r];  // old id: remapped with every producer below
+          rb.vt = -1;
+          P.buffers.push_back(rb);
+          recv[j][r] = rb.id;
+        }
+      }
+      for (std::int64_t r = 0; r < k; ++r) {
+        Instr& G = P.instrs[remap[gemm_of[r]]];
+        G.out_bufs.clear();
+        for (std::int64_t j = 0; j < k; ++j) G.out_bufs.push_back(recv[j][r]);
+        G.scatter = static_cast<int>(k);
+        G.scatter_rows = rows_per;
+        G.wire_bytes += g.instrs[grp[r]].wire_bytes / 2;  // the reduce-scatter volume now moves here
+        P.buffers[inputs[r]].dead = true;
+        P.buffers[inputs[r]].producer = -1;
+        // output reassembly reads the slices where they landed
+        for (auto& o : P.outputs) {
+          auto it = std::find(o.second.begin(), o.second.end(), inputs[r]);
+          if (it == o.second.end()) continue;
+          const std::size_t at = static_cast<std::size_t>(it - o.second.begin());
+          o.second.erase(it);
+          for (std::int64_t j = k - 1; j >= 0; --j) o.second.insert(o.second.begin() + at, recv[j][r]);
+        }
+      }
+    }
     auto slice_cell = [&](std::int64_t j) {
       Cell c;
       c.rank = 1;
@@ -1080,7 +1159,8 @@ void two_phase_allreduce(Program& g) {
       c.dst_strides[0] = 1;
       return c;
     };
-    // Phase 1 (reduce-scatter): member j reduces slice j of every input.
+    // Phase 1 (reduce-scatter): member j reduces slice j of every input
+    // (with the scatter epilogue: the slices already landed on its lane).
     std::vector<int> rs(k);
     for (std::int64_t j = 0; j < k; ++j) {
       Instr in = g.instrs[grp[j]];
@@ -1088,14 +1168,20 @@ void two_phase_allreduce(Program& g) {
       for (const auto& t0 : in.cells[0].terms) {
         Term t = t0;
         t.offset = bound[j];
+        if (scat) {
+          const auto pos = std::find(inputs.begin(), inputs.end(), t0.buffer) - inputs.begin();
+          t.buffer = recv[j][pos];
+          t.offset = 0;
+        }
         c.terms.push_back(t);
       }
       in.cells = {c};
-      in.in_bufs = inputs;
+      in.in_bufs.clear();
+      for (const auto& t : c.terms) in.in_bufs.push_back(t.buffer);
       std::sort(in.in_bufs.begin(), in.in_bufs.end());
       in.deps = remapped(in.deps);
       in.bytes = static_cast<double>(c.elems()) * es * (1 + k);
-      in.wire_bytes = g.instrs[grp[j]].wire_bytes / 2;
+      in.wire_bytes = scat ? 0.0 : g.instrs[grp[j]].wire_bytes / 2;
       in.label += "#rs";
       rs[j] = push(std::move(in));
     }
@@ -1362,7 +1448,8 @@ std::string Program::describe_json() const {
     }
     os << "],\"value\":[" << b.mask.value_index << "," << b.mask.value_count << "],\"bytes\":" << b.bytes
        << ",\"offset\":" << b.offset << ",\"graph_input\":" << (b.graph_input ? "true" : "false")
-       << ",\"weight\":" << (b.weight ? "true" : "false") << ",\"producer\":" << b.producer << "}";
+       << ",\"weight\":" << (b.weight ? "true" : "false") << ",\"producer\":" << b.producer
+       << ",\"dead\":" << (b.dead ? "true" : "false") << "}";
   }
   os << "],\"instrs\":[";
   for (std::size_t i = 0; i < instrs.size(); ++i) {
@@ -1381,7 +1468,8 @@ std::string Program::describe_json() const {
        << ",\"rows\":" << in.rows << ",\"h\":" << in.h << ",\"lo\":" << in.lo << ",\"row_op\":"
        << static_cast<int>(in.row_op) << ",\"seg\":" << in.seg << ",\"eps\":" << in.eps << ",\"flops\":" << in.flops
        << ",\"bytes\":" << in.bytes << ",\"wire_bytes\":" << in.wire_bytes << ",\"coll_group\":" << in.coll_group
-       << ",\"allreduce\":" << (in.allreduce ? "true" : "false") << ",\"group\":" << in.group << ",\"fused\":[";
+       << ",\"allreduce\":" << (in.allreduce ? "true" : "false") << ",\"group\":" << in.group
+       << ",\"scatter\":" << in.scatter << ",\"scatter_rows\":" << in.scatter_rows << ",\"fused\":[";
     for (std::size_t f = 0; f < in.fused.size(); ++f) {
       const auto& fe = in.fused[f];
       os << (f ? "," : "") << "{\"ew_instr\":" << fe.ew_instr << ",\"ew\":" << static_cast<int>(fe.op)

@@ -48,6 +48,7 @@ struct BufferDesc {
   bool weight = false;         // graph input of kind weight / optimizer state
   int producer = -1;           // instruction writing it (-1: placement)
   int vt = -1;                 // producing vTensor (or first placed view)
+  bool dead = false;           // replaced (reduce-scatter GEMM epilogue): never written nor read
 };
 
 // One source of a cell: a box of another buffer, copied or accumulated.
@@ -107,6 +108,10 @@ struct Instr {
   // out_bufs[i] = op(in_bufs[2i])·op(in_bufs[2i+1]) for i < group.
   std::int64_t m = 0, n = 0, k = 0;
   int group = 1;
+  // gemm with a reduce-scatter epilogue: rows [i*scatter_rows, (i+1)*scatter_rows)
+  // of the product go to out_bufs[i] (receive buffers on the slice owners' lanes).
+  int scatter = 0;
+  std::int64_t scatter_rows = 0;
   bool ta = false, tb = false;
   // ew
   EwOp ew = EwOp::add;
@@ -161,6 +166,13 @@ struct ProgramOptions {
   // member reads ~2n instead of k*n (over NVLink when members sit on other
   // GPUs or ranks).
   bool two_phase_allreduce = true;
+  // ...and when every member's partial comes straight from a GEMM (a
+  // row-parallel / value-split matmul consumed only by the all-reduce), that
+  // GEMM's epilogue stores each row slice into a receive buffer on the lane
+  // owning that slice (tile by tile, over NVLink when the owner is another
+  // GPU): the reduce-scatter transfer rides in the GEMM, the phase-1 box sums
+  // local pieces in the reference's order. Needs the tensor-core predicate.
+  bool scatter_allreduce = true;
   // Independent GEMMs of one shape on one lane that become ready together
   // (each one's dependencies are ancestors of the other's) run as one
   // grouped tensor-core launch (one tile space: no per-GEMM wave tail, one
@@ -207,7 +219,7 @@ void group_gemms(Program& p, const ProgramOptions& opt);
 // The two-phase all-reduce pass (ProgramOptions::two_phase_allreduce), run
 // by build_program before epilogue fusion. Rebuilds the program in issue
 // order (instruction ids stay dense and ascending along the issue order).
-void two_phase_allreduce(Program& p);
+void two_phase_allreduce(Program& p, const ProgramOptions& opt = {});
 
 // Peer-memory one-process-per-GPU mode: every rank runs the global program's
 // instructions of its own lanes and reads other ranks' buffers in place

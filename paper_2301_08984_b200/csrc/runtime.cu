@@ -134,6 +134,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   // NCCL exchange steps lower whole-buffer all-reduce groups to
   // ncclAllReduce; every other mode runs them as two box phases.
   po.two_phase_allreduce = !(rank && !rank->peer_memory);
+  po.scatter_allreduce = opt.allow_tensor_cores && opt.scatter_allreduce;
   prog_ = build_program(plan_, po);
   if (rank) {
     rank_mode_ = true;
@@ -330,6 +331,8 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       a.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
       a.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
       a.group = in.group;
+      a.scatter = in.scatter;
+      a.scatter_rows = in.scatter_rows;
       a.allow_streamk = gemm_streamk_ok(exec_lane_[in.id]);
       if (opt_.allow_tensor_cores && gemm_sm100_eligible(a)) {
         ++gemm_tc_per_step_;
@@ -756,6 +759,14 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
       a.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
       a.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
       a.group = in.group;
+      if (in.scatter > 0) {
+        if (in.scatter > kMaxGemmGroup || static_cast<int>(in.out_bufs.size()) != in.scatter || !in.fused.empty())
+          throw InternalError("malformed reduce-scatter GEMM instruction");
+        a.scatter = in.scatter;
+        a.scatter_rows = in.scatter_rows;
+        for (int i = 0; i < in.scatter; ++i) a.gC[i] = buf_ptr(in.out_bufs[i]);
+        a.C = a.gC[0];
+      }
       if (in.group > 1) {
         if (in.group > kMaxGemmGroup || static_cast<int>(in.in_bufs.size()) != 2 * in.group ||
             static_cast<int>(in.out_bufs.size()) != in.group || !in.fused.empty()) {

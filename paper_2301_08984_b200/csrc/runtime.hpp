@@ -51,6 +51,7 @@ struct ExecOptions {
   bool fuse_epilogues = true;           // elementwise consumers computed in GEMM epilogues
   bool group_gemms = true;              // same-shape independent GEMMs in one grouped launch
   bool alias_copies = true;             // same-GPU whole-buffer copies (recv, identity) become aliases
+  bool scatter_allreduce = true;        // all-reduce partials leave the GEMM epilogue as reduce-scatter slices
 };
 
 // ProgramOptions as the executor uses them: epilogue fusion only for GEMMs

@@ -34,7 +34,13 @@ def exec_instr(ins: dict, data: dict, shape: dict):
             b = data[ins["in"][2 * g + 1]].reshape(shape[ins["in"][2 * g + 1]])
             a = a.T if ins["ta"] else a
             b = b.T if ins["tb"] else b
-            data[ins["out"][g]] = (a @ b).reshape(-1)
+            c = a @ b
+            if ins.get("scatter", 0):  # reduce-scatter epilogue: row slice i -> out[i]
+                rp = ins["scatter_rows"]
+                for i, ob in enumerate(ins["out"]):
+                    data[ob] = c[i * rp:(i + 1) * rp].reshape(-1)
+            else:
+                data[ins["out"][g]] = c.reshape(-1)
         for f in ins.get("fused", []):  # elementwise consumers run in the GEMM epilogue
             out = data[f["in"][0]].copy()
             for x in f["in"][1:]:

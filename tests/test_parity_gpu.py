@@ -37,7 +37,8 @@ def test_golden_plan_parity(name):
 @pytest.mark.parametrize("name", ["mlp_dp2", "gpt_block_tp2", "embed_shard2", "adapt_d1_to_d0_4",
                                   "three_pass_3f1b", "gpt_block_fwd_tp2_mma"])
 @pytest.mark.parametrize("flags", [pb.NO_GRAPH, pb.NO_TENSOR_CORES, pb.SERIAL_LANES, pb.NO_GRAPH | pb.SERIAL_LANES,
-                                   pb.NO_FUSION, pb.NO_FUSION | pb.NO_GRAPH, pb.NO_ALIAS, pb.NO_GROUPING])
+                                   pb.NO_FUSION, pb.NO_FUSION | pb.NO_GRAPH, pb.NO_ALIAS, pb.NO_GROUPING,
+                                   pb.NO_SCATTER])
 def test_parity_across_launch_modes(name, flags):
     g = golden_cases.load(name)
     out, _ = _run(g["plan"], g["inputs"], flags=flags)
@@ -136,3 +137,24 @@ def test_same_gpu_copies_become_aliases():
         assert np.array_equal(outs[0][k], outs[pb.NO_ALIAS][k])
     ok, msg = pb.compare_outputs(g["expected"], outs[0], 0.0)
     assert ok, msg
+
+
+@pytest.mark.parametrize("name", ["gpt_block_fwd_tp2_mma", "ext_block_fwd_tp2_mma"])
+def test_reduce_scatter_gemm_epilogue(name):
+    """Row-parallel GEMMs feeding an all-reduce store their row slices into
+    the owners' receive buffers (scatter epilogue); same results as storing
+    the partials whole (NO_SCATTER)."""
+    g = golden_cases.load(name)
+    desc = pb.describe(g["plan"])
+    assert any(i["kind"] == "gemm" and i["scatter"] for i in desc["instrs"])
+    n = len(json.loads(g["plan"])["lanes"])
+    outs = {}
+    for flags in (0, pb.NO_SCATTER):
+        with pb.Executor(g["plan"], lane_gpus=[0] * n, flags=flags) as ex:
+            ex.set_inputs(g["inputs"])
+            ex.run(2)
+            outs[flags] = ex.outputs()
+        ok, msg = pb.compare_outputs(g["expected"], outs[flags], g["meta"]["rel_tol"], normwise=True)
+        assert ok, msg
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[pb.NO_SCATTER][k]), k

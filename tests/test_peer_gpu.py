@@ -24,7 +24,8 @@ pytestmark = pytest.mark.gpu
 CASES = ["mlp_dp2", "tp_value_split", "gpt_block_tp2", "gpt_block_tp2_bf16", "adapt_v_to_r4", "adapt_v_to_d4",
          "adapt_d1_to_d0_4", "adapt_d_to_r4", "adapt_r_to_d4", "embed_shard2", "three_pass_3f1b", "mlp_1f1b_dp2",
          "mlp_dp2_naive", "cross_group_rs", "cross_group_copy", "mlp_dp4", "gpt_block_tp4", "gpt_stack2_1f1b_bf16",
-         "coshard4_recompute", "embed_interlaced", "ext_block_tp2", "ext_block_tp4", "ext_block_tp2_bf16"]
+         "coshard4_recompute", "embed_interlaced", "ext_block_tp2", "ext_block_tp4", "ext_block_tp2_bf16",
+         "gpt_block_fwd_tp2_mma", "ext_block_fwd_tp2_mma"]
 
 
 def _free_port():
