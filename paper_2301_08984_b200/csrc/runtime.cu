@@ -134,7 +134,12 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   // NCCL exchange steps lower whole-buffer all-reduce groups to
   // ncclAllReduce; every other mode runs them as two box phases.
   po.two_phase_allreduce = !(rank && !rank->peer_memory);
-  po.scatter_allreduce = opt.allow_tensor_cores && opt.scatter_allreduce;
+  // The scatter epilogue pays when the slices cross GPUs (the transfer rides
+  // in the GEMM); with every lane on one GPU it only trades TMA stores for
+  // plain ones (measured ~2 % slower, profiles/r01/ab_scatter.jsonl).
+  bool multi_gpu = rank != nullptr;
+  for (std::size_t i = 1; i < lane_gpu.size(); ++i) multi_gpu = multi_gpu || lane_gpu[i] != lane_gpu[0];
+  po.scatter_allreduce = opt.allow_tensor_cores && opt.scatter_allreduce && multi_gpu;
   prog_ = build_program(plan_, po);
   if (rank) {
     rank_mode_ = true;

@@ -149,8 +149,12 @@ def test_reduce_scatter_gemm_epilogue(name):
     assert any(i["kind"] == "gemm" and i["scatter"] for i in desc["instrs"])
     n = len(json.loads(g["plan"])["lanes"])
     outs = {}
+    # Single process, every lane on cuda:0: the executor keeps whole partials
+    # (no GPU boundary to cross) unless told the lanes sit on distinct devices;
+    # one rank per lane (world 1, every lane owned) takes the scatter path.
     for flags in (0, pb.NO_SCATTER):
-        with pb.Executor(g["plan"], lane_gpus=[0] * n, flags=flags) as ex:
+        with pb.Executor(g["plan"], flags=flags | pb.PEER_MEMORY, rank=0, world=1, lane_rank=[0] * n,
+                         local_gpu=0, peer_exchange=lambda blob: [blob]) as ex:
             ex.set_inputs(g["inputs"])
             ex.run(2)
             outs[flags] = ex.outputs()
