@@ -208,6 +208,22 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
+// Same, with an L2 eviction-priority policy (createpolicy), no group close.
+__device__ __forceinline__ void tma_store_2d_nc_hint(const CUtensorMap* map, const void* src, int c0, int c1,
+                                                     std::uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+          reinterpret_cast<std::uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ std::uint64_t l2_evict_first_policy() {
+  std::uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // Same, without closing the bulk group (several stores per group).
 __device__ __forceinline__ void tma_store_2d_nc(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
@@ -684,8 +700,11 @@ __global__ void __launch_bounds__(NUM_THREADS, OCC)
       __syncwarp();
       if (lane == 0) {
         const int c0 = nb * BN + c * 32, c1 = mb * BM + q * 32;
-        tma_store_2d_nc(&gm.c[0], buf, c0, c1);
-        tma_store_2d_nc(&maps.out[0], buf + 2048, c0, c1);
+        // The fused op streams a tensor as large as C through L2: its
+        // results leave evict-first so the GEMM's A / B panels stay resident.
+        const std::uint64_t pol = l2_evict_first_policy();
+        tma_store_2d_nc_hint(&gm.c[0], buf, c0, c1, pol);
+        tma_store_2d_nc_hint(&maps.out[0], buf + 2048, c0, c1, pol);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
       ++g;
