@@ -1,937 +1,11 @@
-// tcgen05 / TMEM / TMA GEMM for the plan's matmul sub-operators (sm_100a).
-//
-// C[m,n] = op(A)[m,k] · op(B)[k,n] with bf16 operands, fp32 accumulation in
-// tensor memory, bf16 or fp32 output — the reference's matmul_eval
-// (proj/src/refexec.cpp:142-168) including transpose_a / transpose_b, which
-// are not materialised: a transposed operand is simply loaded MN-major and the
-// UMMA instruction descriptor's major bits say so.
-//
-// Structure: persistent, one CTA per SM, 128xBN output tiles (BN 256 / 128 /
-// 64 chosen per shape) in grouped raster order (8 M-blocks per group for L2
-// reuse of B), 6 warps:
-//   warp 0      TMA producer: smem ring filling ~192 KB (A 16 KB + B BN*128 B
-//               per stage, 128B-swizzled), mbarrier full/empty pipeline
-//               running across tiles
-//   warp 1      TMEM allocator (two BN-column fp32 accumulators) + single-
-//               thread tcgen05.mma issuer (kind::f16, M=128, N=BN, K=16 per
-//               instruction); commits free smem stages and, per tile, the
-//               accumulator it just finished
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 TMEM -> registers, convert,
-//               64B/128B-swizzled smem staging, TMA bulk tensor store
-//               (double-buffered per warp); releases the accumulator so the
-//               MMA warp fills it with the tile after next while this one
-//               drains. An optional fused elementwise consumer (FUSE)
-//               reads its operands one chunk ahead and leaves by TMA store.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-#include <cuda_bf16.h>
-
-#include <algorithm>
-#include <cstdlib>
-#include <cstring>
-#include <mutex>
-#include <stdexcept>
-#include <string>
-
-#include "kernels.cuh"
-#include "launch.cuh"
+// tcgen05 GEMM: launch schedules (data-parallel / stream-K / split-K /
+// grouped / two-CTAs-per-SM / 8-epilogue-warp variants) and dispatch. Kernel
+// templates: gemm_sm100_impl.cuh; instantiations: gemm_sm100_ab*.cu.
+#include "gemm_sm100_impl.cuh"
 
 namespace planc_b200 {
 
 namespace {
-
-constexpr int BM = 128;
-constexpr int BK = 64;  // 128 bytes of bf16: one 128B swizzle row
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
-constexpr int NUM_THREADS = 192;
-constexpr int GROUP_M = 8;
-constexpr int kSkDepth = 2;  // stream-K partials loaded per round trip
-
-// Tile width BN in {256, 128, 64}: smem ring depth fills ~200 KB, TMEM holds
-// two BN-column fp32 accumulators (power of two >= 32 columns).
-// OCC = 2 ("small" GEMMs: k <= 1024, BN <= 128, no fusion / stream-K): a
-// ~100 KB ring and <= 256 TMEM columns so two CTAs share an SM — two tiles'
-// prologue / epilogue latencies overlap, or two concurrent small GEMMs from
-// different streams run side by side instead of one after the other.
-template <int BN_, bool FUSE = false, int OCC = 1>
-struct Cfg {
-  static constexpr int BN = BN_;
-  static constexpr int B_STAGE_BYTES = BN * BK * 2;
-  static constexpr int STAGES_RAW = ((OCC == 1 ? 200 : 76) * 1024) / (A_STAGE_BYTES + B_STAGE_BYTES);
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  // + epilogue staging: 4 warps x 2 buffers x (32 rows x 32 cols, <= 4 B);
-  // FUSE (bf16): 4 warps x 2 x {C, fused result} 2 KB chunks — same size.
-  static constexpr int STAGING_BYTES = 4 * 2 * 4096;
-  static constexpr int SMEM_BYTES =
-      STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + STAGING_BYTES + 1024 /*align*/ + 1024 /*barriers + align*/;
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-};
-
-// Tensor map of a fused epilogue's result: [m][n] bf16 in the C layout
-// (32x32 boxes, 64B swizzle).
-struct EpiMaps {
-  CUtensorMap out[1];
-  // Split-K partials: fp32 [group][splits][m_pad] x [n_pad] (32x32 boxes,
-  // 128B swizzle), row of (member p, split s, output row r) =
-  // (p * splits + s) * m_pad + r.
-  CUtensorMap ws;
-};
-
-// Operand / result maps of the launch's GEMMs (one, or a group of
-// independent same-shape GEMMs sharing the tile space: tile t belongs to
-// member t / tiles_per_gemm).
-// NG = capacity (1 for single launches: kernel parameters stay small, which
-// keeps graph launch latency down; kMaxGemmGroup for grouped launches).
-template <int NG>
-struct GroupMaps {
-  CUtensorMap a[NG];
-  CUtensorMap b[NG];
-  CUtensorMap c[NG];
-};
-
-// Stream-K tail (data-parallel waves, then the remaining tiles' k-iterations
-// split evenly over the CTAs): tiles [0, dp_tiles) go whole to CTA
-// t % gridDim.x; CTA b < sk_ctas then takes k-iterations [lo(b), lo(b+1)) of
-// the linearised (tile, k-block) space of tiles [dp_tiles, tiles). A tile
-// covered by several CTAs is reduced by whichever of them arrives last (per
-// 32-row quarter: a counter per quarter, no CTA ever waits on another), in
-// fixed CTA (= k) order from fp32 partials — the same bits whatever the
-// arrival order.
-struct SkParams {
-  int dp_tiles = 0;
-  int sk_ctas = 0;
-  int splits = 0;  // split-K: every work item is (tile, split), stored to ws_map
-  // Half-width tail: after dp_tiles whole tiles, the remaining tiles run as
-  // half_items tiles of 128 x BN/2 (item h: half h & 1 of tile dp_tiles + h / 2),
-  // so a last wave of r < grid/2 tiles takes half a tile-time.
-  int half_items = 0;
-  // Reduce-scatter epilogue: row y of C goes to row y % scatter_rows of the
-  // [scatter_rows][n] buffer scatter_dst[y / scatter_rows] (0 = off) — by
-  // plain 16-byte stores from registers, valid for NVLink peer memory.
-  int scatter_rows = 0;
-  void* scatter_dst[kMaxGemmGroup] = {};
-  long long sk_iters = 0;
-  float* partials = nullptr;  // [sk_ctas][2 slots][4 quarters][BN/32 chunks][8][32] float4
-  int* counters = nullptr;    // [(tiles - dp_tiles) * 4], zero between launches
-};
-
-__device__ __forceinline__ long long sk_lo(const SkParams& sk, int b) {
-  return static_cast<long long>(b) * sk.sk_iters / sk.sk_ctas;
-}
-
-// CTA whose stream-K range holds iteration x: max b with lo(b) <= x.
-__device__ __forceinline__ int sk_owner(const SkParams& sk, long long x) {
-  return static_cast<int>(((x + 1) * sk.sk_ctas - 1) / sk.sk_iters);
-}
-
-// Calls f(tile, kb0, kb1, half) for this CTA's work items in order; half is
-// -1 for a whole tile, else which 128 x BN/2 half of the tile.
-template <typename F>
-__device__ __forceinline__ void for_each_work(int num_k, const SkParams& sk, F&& f) {
-  if (sk.splits > 1) {
-    // Split-K: item (tile t, split s) covers k-blocks [s*K/S, (s+1)*K/S).
-    const int items = sk.dp_tiles * sk.splits;
-    for (int x = blockIdx.x; x < items; x += gridDim.x) {
-      const int t = x / sk.splits, sp = x - t * sk.splits;
-      f(t, sp * num_k / sk.splits, (sp + 1) * num_k / sk.splits, -1);
-    }
-    return;
-  }
-  if (sk.half_items > 0) {
-    for (int x = blockIdx.x; x < sk.dp_tiles + sk.half_items; x += gridDim.x) {
-      if (x < sk.dp_tiles) f(x, 0, num_k, -1);
-      else f(sk.dp_tiles + (x - sk.dp_tiles) / 2, 0, num_k, (x - sk.dp_tiles) & 1);
-    }
-    return;
-  }
-  for (int t = blockIdx.x; t < sk.dp_tiles; t += gridDim.x) f(t, 0, num_k, -1);
-  if (static_cast<int>(blockIdx.x) < sk.sk_ctas) {
-    long long it = sk_lo(sk, blockIdx.x);
-    const long long hi = sk_lo(sk, blockIdx.x + 1);
-    while (it < hi) {
-      const int j = static_cast<int>(it / num_k);
-      const int kb0 = static_cast<int>(it - static_cast<long long>(j) * num_k);
-      const int kb1 = static_cast<int>(min(static_cast<long long>(num_k), kb0 + (hi - it)));
-      f(sk.dp_tiles + j, kb0, kb1, -1);
-      it += kb1 - kb0;
-    }
-  }
-}
-
-// ---- PTX wrappers ------------------------------------------------------------
-
-__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
-  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
-  std::uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@p bra.uni DONE;\n"
-      "bra.uni LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(addr),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, std::uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// Bulk tensor store smem -> global (clips rows / cols outside the tensor).
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                   reinterpret_cast<std::uint64_t>(map)),
-               "r"(c0), "r"(c1), "r"(smem_u32(src))
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-
-// Same, with an L2 eviction-priority policy (createpolicy), no group close.
-__device__ __forceinline__ void tma_store_2d_nc_hint(const CUtensorMap* map, const void* src, int c0, int c1,
-                                                     std::uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
-          reinterpret_cast<std::uint64_t>(map)),
-      "r"(c0), "r"(c1), "r"(smem_u32(src)), "l"(policy)
-      : "memory");
-}
-
-__device__ __forceinline__ std::uint64_t l2_evict_first_policy() {
-  std::uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
-// Same, without closing the bulk group (several stores per group).
-__device__ __forceinline__ void tma_store_2d_nc(const CUtensorMap* map, const void* src, int c0, int c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                   reinterpret_cast<std::uint64_t>(map)),
-               "r"(c0), "r"(c1), "r"(smem_u32(src))
-               : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tc_commit(std::uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tc_mma(std::uint32_t tmem_d, std::uint64_t adesc, std::uint64_t bdesc,
-                                       std::uint32_t idesc, std::uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-
-// Shared-memory matrix descriptor (tcgen05 "version 1"), SWIZZLE_128B.
-__device__ __forceinline__ std::uint64_t smem_desc(std::uint32_t addr, std::uint32_t lbo, std::uint32_t sbo) {
-  std::uint64_t d = 0;
-  d |= static_cast<std::uint64_t>((addr >> 4) & 0x3FFFu);
-  d |= static_cast<std::uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
-  d |= static_cast<std::uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
-  d |= 1ull << 46;  // version
-  d |= 2ull << 61;  // SWIZZLE_128B
-  return d;
-}
-
-// Instruction descriptor: kind::f16, A/B bf16, D f32, M=128, N=BN.
-template <int BN>
-__host__ __device__ constexpr std::uint32_t make_idesc(bool a_mn, bool b_mn) {
-  return (1u << 4)                              // D format f32
-         | (1u << 7)                            // A bf16
-         | (1u << 10)                           // B bf16
-         | ((a_mn ? 1u : 0u) << 15)             // A major
-         | ((b_mn ? 1u : 0u) << 16)             // B major
-         | (static_cast<std::uint32_t>(BN >> 3) << 17)  // N
-         | (static_cast<std::uint32_t>(BM >> 4) << 24); // M
-}
-
-__device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// ---- kernel --------------------------------------------------------------------
-
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
-  const int per_group = GROUP_M * tiles_n;
-  const int group = t / per_group;
-  const int first_m = group * GROUP_M;
-  const int gm = min(tiles_m - first_m, GROUP_M);
-  const int r = t % per_group;
-  mb = first_m + r % gm;
-  nb = r / gm;
-}
-
-__device__ __forceinline__ float epi_apply(int op, float a, float b) {
-  return op == 0 ? a + b : op == 1 ? a * b : fmaxf(a, b);
-}
-
-__device__ __forceinline__ std::uint32_t bf16_pair(float lo, float hi) {
-  return static_cast<std::uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(lo))) |
-         (static_cast<std::uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(hi))) << 16);
-}
-
-__device__ __forceinline__ void bf16_unpair(std::uint32_t w, float& lo, float& hi) {
-  lo = __uint_as_float(w << 16);
-  hi = __uint_as_float(w & 0xffff0000u);
-}
-
-template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE, int NG, int OCC>
-__global__ void __launch_bounds__(NUM_THREADS, OCC)
-    gemm_tc_kernel(const __grid_constant__ GroupMaps<NG> gm, int ng, int m, int n, int k,
-                   const __grid_constant__ EpiParams epi, const __grid_constant__ EpiMaps maps,
-                   const __grid_constant__ SkParams sk) {
-  static_assert(OCC == 1 || (!FUSE && BN <= 128), "two CTAs per SM: no fusion, <= 256 TMEM columns");
-  extern __shared__ std::uint8_t smem_raw[];
-  using CF = Cfg<BN, FUSE, OCC>;
-  constexpr int STAGES = CF::STAGES;
-  constexpr int B_STAGE_BYTES = CF::B_STAGE_BYTES;
-  constexpr int TMEM_COLS = CF::TMEM_COLS;
-  std::uint8_t* smem =
-      reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
-  std::uint8_t* sA = smem;
-  std::uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  // Epilogue staging (1024-aligned: the 64B / 128B swizzle atoms of the C map).
-  std::uint8_t* staging = sB + STAGES * B_STAGE_BYTES;
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(staging + CF::STAGING_BYTES);
-  std::uint64_t* empty = full + STAGES;
-  std::uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
-  std::uint64_t* tempty = tfull + 2;      // [2] accumulator drained
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  const int tiles_m = (m + BM - 1) / BM;
-  const int tiles_n = (n + BN - 1) / BN;
-  const int per_gemm = tiles_m * tiles_n;
-  const int num_tiles = per_gemm * ng;
-  const int num_k = (k + BK - 1) / BK;
-  // Tile t of the launch: member t / per_gemm, its tile t % per_gemm.
-  auto coords = [&](int t, int& p, int& mb, int& nb) {
-    p = t / per_gemm;
-    tile_coords(t - p * per_gemm, tiles_m, tiles_n, mb, nb);
-  };
-
-  if (warp == 0 && lane == 0) {
-    for (int p = 0; p < ng; ++p) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&gm.a[p])) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&gm.b[p])) : "memory");
-    }
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
-  // Prologue done (barriers, TMEM, descriptor prefetch): from here on the
-  // previous kernel's results are read and the workspace is written.
-  pdl_wait();
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int it = 0;  // global k-block counter across work items (ring position)
-      for_each_work(num_k, sk, [&](int t, int kb0, int kb1, int half) {
-        int p, mb, nb;
-        coords(t, p, mb, nb);
-        const CUtensorMap* tmA = &gm.a[p];
-        const CUtensorMap* tmB = &gm.b[p];
-        // A half tile loads the B rows from its own first column (the box's
-        // upper half is unused, and zero-filled past the tensor edge).
-        const int m0 = mb * BM, n0 = nb * BN + (half > 0 ? BN / 2 : 0);
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % STAGES;
-          const std::uint32_t phase = (it / STAGES) & 1;
-          mbar_wait(&empty[s], phase ^ 1);
-          mbar_expect_tx(&full[s], A_STAGE_BYTES + B_STAGE_BYTES);
-          std::uint8_t* a = sA + s * A_STAGE_BYTES;
-          std::uint8_t* b = sB + s * B_STAGE_BYTES;
-          if (A_MN) {
-#pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * (64 * BK * 2), tmA, m0 + 64 * j, kb * BK, &full[s]);
-          } else {
-            tma_load_2d(a, tmA, kb * BK, m0, &full[s]);
-          }
-          if (B_MN) {
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * (64 * BK * 2), tmB, n0 + 64 * j, kb * BK, &full[s]);
-          } else {
-            tma_load_2d(b, tmB, kb * BK, n0, &full[s]);
-          }
-        }
-      });
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr std::uint32_t idesc_full = make_idesc<BN>(A_MN, B_MN);
-      constexpr std::uint32_t idesc_half = make_idesc<(BN >= 128 ? BN / 2 : BN)>(A_MN, B_MN);
-      int it = 0, local = 0;
-      for_each_work(num_k, sk, [&](int, int kb0, int kb1, int half) {
-        const std::uint32_t idesc = half >= 0 ? idesc_half : idesc_full;
-        const int acc = local & 1;
-        const std::uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
-        tc_fence_after();
-        const std::uint32_t d = tmem + static_cast<std::uint32_t>(acc * BN);
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % STAGES;
-          const std::uint32_t phase = (it / STAGES) & 1;
-          mbar_wait(&full[s], phase);
-          tc_fence_after();
-          const std::uint32_t a_base = smem_u32(sA + s * A_STAGE_BYTES);
-          const std::uint32_t b_base = smem_u32(sB + s * B_STAGE_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            // K-major: 16 elements = 32 bytes along the swizzled row; rows of
-            // 128 B, 8-row groups 1024 B apart (SBO). MN-major: 16 K-rows =
-            // 2048 B; 64-element MN blocks 8 KB apart (LBO), 8-row K groups
-            // 1024 B apart (SBO).
-            std::uint64_t ad = A_MN ? smem_desc(a_base + kk * 2048, 64 * BK * 2, 1024)
-                                    : smem_desc(a_base + kk * 32, 16, 1024);
-            std::uint64_t bd = B_MN ? smem_desc(b_base + kk * 2048, 64 * BK * 2, 1024)
-                                    : smem_desc(b_base + kk * 32, 16, 1024);
-            tc_mma(d, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
-          }
-          tc_commit(&empty[s]);  // smem stage free once these MMAs retire
-        }
-        tc_commit(&tfull[acc]);  // accumulator complete
-        ++local;
-      });
-      pdl_trigger();  // every MMA issued: the next kernel may start its prologue
-    }
-  } else if constexpr (!FUSE) {
-    // Epilogue warps 2..5: warp w may only touch TMEM lanes 32*(w%4)..+31.
-    // Each 32x32 output chunk goes TMEM -> registers -> swizzled smem
-    // staging (conflict-free 16-byte stores) -> one TMA bulk tensor store
-    // (coalesced, clipped at the tensor edge); two staging buffers per warp
-    // keep a store in flight while the next chunk is converted.
-    const int q = warp % 4;
-    std::uint8_t* stg = staging + (warp - 2) * 2 * 4096;
-    int sb = 0;
-    int local = 0;
-    auto store_chunk = [&](const std::uint32_t(&r)[32], const CUtensorMap* map, bool bf16, int x, int y) {
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer sb is free
-      __syncwarp();
-      std::uint8_t* buf = stg + sb * 4096;
-      if (bf16) {
-        // 64 B rows, SWIZZLE_64B: 16-byte chunk v lands at v ^ ((row >> 1) & 3).
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const uint4 w = make_uint4(bf16_pair(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1])),
-                                     bf16_pair(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
-                                     bf16_pair(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
-                                     bf16_pair(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
-          *reinterpret_cast<uint4*>(buf + lane * 64 + ((v ^ ((lane >> 1) & 3)) << 4)) = w;
-        }
-      } else {
-        // 128 B rows, SWIZZLE_128B: 16-byte chunk v lands at v ^ (row & 7).
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          *reinterpret_cast<uint4*>(buf + lane * 128 + ((v ^ (lane & 7)) << 4)) =
-              make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
-      __syncwarp();
-      if (lane == 0) tma_store_2d(map, buf, x, y);
-      sb ^= 1;
-    };
-    const int m_pad = tiles_m * BM;
-    // fp32 partial of (CTA b, slot, this quarter, chunk c): 8 float4 per
-    // lane, lane-interleaved so every access is one coalesced 512 B row.
-    auto partial_ptr = [&](int b, int slot, int c) {
-      return reinterpret_cast<float4*>(sk.partials) +
-             ((static_cast<std::int64_t>((b * 2 + slot) * 4 + q) * (BN / 32) + c) * 8) * 32 + lane;
-    };
-    for_each_work(num_k, sk, [&](int t, int kb0, int kb1, int half) {
-      int p, mb, nb;
-      coords(t, p, mb, nb);
-      const int acc = local & 1;
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
-      ++local;
-      tc_fence_after();
-      const std::uint32_t base = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
-      if ((kb0 == 0 && kb1 == num_k) || sk.splits > 1) {  // whole tile, or one split's fp32 partial
-        const bool part = sk.splits > 1;
-        // split index of k-range start kb0 = floor(s*K/S): s = ceil(kb0*S/K) (K/S >= 1)
-        const int sp = (kb0 * sk.splits + num_k - 1) / num_k;
-        const int y = part ? (p * sk.splits + sp) * m_pad + mb * BM + q * 32 : mb * BM + q * 32;
-        const int chunks = half >= 0 ? BN / 64 : BN / 32;
-        const int x0 = nb * BN + (half > 0 ? BN / 2 : 0);
-#pragma unroll 1
-        for (int c = 0; c < chunks; ++c) {
-          std::uint32_t r[32];
-          tmem_ld32(base + c * 32, r);
-          if (c == chunks - 1) {
-            // All TMEM reads of this accumulator are complete: hand it back.
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
-          if (part) {
-            store_chunk(r, &maps.ws, false, x0 + c * 32, y);
-          } else if (sk.scatter_rows > 0) {
-            // lane = row of the 32-row chunk: 32 columns straight to the
-            // owner's receive buffer (64 B bf16 / 128 B fp32 per lane).
-            const int row = y + lane, col = x0 + c * 32;
-            const int dst_i = row / sk.scatter_rows;
-            char* dst = static_cast<char*>(sk.scatter_dst[dst_i]) +
-                        (static_cast<std::int64_t>(row - dst_i * sk.scatter_rows) * n + col) * (C_BF16 ? 2 : 4);
-            if constexpr (C_BF16) {
-#pragma unroll
-              for (int v = 0; v < 4; ++v)
-                if (col + 8 * v < n)
-                  reinterpret_cast<uint4*>(dst)[v] =
-                      make_uint4(bf16_pair(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1])),
-                                 bf16_pair(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
-                                 bf16_pair(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
-                                 bf16_pair(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
-            } else {
-#pragma unroll
-              for (int v = 0; v < 8; ++v)
-                if (col + 4 * v < n)
-                  reinterpret_cast<uint4*>(dst)[v] = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-            }
-          } else {
-            store_chunk(r, &gm.c[p], C_BF16, x0 + c * 32, y);
-          }
-        }
-        return;
-      }
-      if constexpr (OCC == 1) {
-      // Stream-K segment: publish the fp32 partial, count the arrival.
-      const int j = t - sk.dp_tiles;
-      const long long x0 = static_cast<long long>(j) * num_k;
-      const int me = blockIdx.x;
-      const int myslot = sk_lo(sk, me) >= x0 ? 0 : 1;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        std::uint32_t r[32];
-        tmem_ld32(base + c * 32, r);
-        float4* dst = partial_ptr(me, myslot, c);
-#pragma unroll
-        for (int v = 0; v < 8; ++v)
-          __stcg(dst + v * 32, make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                           __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])));
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      __threadfence();
-      __syncwarp();
-      int old = 0;
-      if (lane == 0) old = atomicAdd(&sk.counters[j * 4 + q], 1);
-      old = __shfl_sync(0xffffffffu, old, 0);
-      const int b_first = sk_owner(sk, x0), b_last = sk_owner(sk, x0 + num_k - 1);
-      if (old != b_last - b_first) return;  // another CTA finishes this quarter
-      // Last arrival: sum every segment's partial in k order, store.
-      __threadfence();
-      if (lane == 0) sk.counters[j * 4 + q] = 0;  // ready for the next launch
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        // Loads of kSkDepth partials in flight, folded in CTA order.
-        float4 sum[8];
-#pragma unroll 1
-        for (int b0 = b_first; b0 <= b_last; b0 += kSkDepth) {
-          float4 p[kSkDepth][8];
-#pragma unroll
-          for (int d = 0; d < kSkDepth; ++d) {
-            const int b = b0 + d;
-            if (b <= b_last) {
-              const float4* src = partial_ptr(b, sk_lo(sk, b) >= x0 ? 0 : 1, c);
-#pragma unroll
-              for (int v = 0; v < 8; ++v) p[d][v] = __ldcg(src + v * 32);
-            }
-          }
-#pragma unroll
-          for (int d = 0; d < kSkDepth; ++d) {
-            const int b = b0 + d;
-            if (b > b_last) break;
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              if (b == b_first) {
-                sum[v] = p[d][v];
-              } else {
-                sum[v].x += p[d][v].x;
-                sum[v].y += p[d][v].y;
-                sum[v].z += p[d][v].z;
-                sum[v].w += p[d][v].w;
-              }
-            }
-          }
-        }
-        std::uint32_t r[32];
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          r[4 * v] = __float_as_uint(sum[v].x);
-          r[4 * v + 1] = __float_as_uint(sum[v].y);
-          r[4 * v + 2] = __float_as_uint(sum[v].z);
-          r[4 * v + 3] = __float_as_uint(sum[v].w);
-        }
-        store_chunk(r, &gm.c[p], C_BF16, nb * BN + c * 32, mb * BM + q * 32);
-      }
-      }  // OCC == 1
-    });
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
-  } else {
-    // Fused epilogue (bf16, one elementwise consumer): lane = output row of
-    // the 32x32 chunk. The op's other operands (<= 2) are read straight into
-    // registers one chunk ahead — the first chunk of a tile while its
-    // accumulator is still being built — alternating between two register
-    // sets so no load is waited on before its chunk. C and the op result
-    // are staged swizzled side by side and leave as two TMA stores in one
-    // bulk group. Bits equal the separate kernels': the op folds its inputs
-    // in order, reading the GEMM's bf16-rounded C.
-    const int q = warp % 4;
-    std::uint8_t* stg = staging + (warp - 2) * 2 * 4096;  // [2][C 2 KB | result 2 KB]
-    const int swz = (lane >> 1) & 3;
-    const int nst = epi.n_slots;
-    const __nv_bfloat16* src0 =
-        static_cast<const __nv_bfloat16*>(epi.ops[0].in[epi.slot_in[0]]);
-    const __nv_bfloat16* src1 =
-        static_cast<const __nv_bfloat16*>(epi.ops[0].in[epi.slot_in[1]]);
-    auto load = [&](int t_, int c_, uint4(&d)[kMaxEpiSlots][4]) {
-      int mb_, nb_;
-      tile_coords(t_, tiles_m, tiles_n, mb_, nb_);
-      const int grow = mb_ * BM + q * 32 + lane;
-      const int gcol = nb_ * BN + c_ * 32;
-      const std::int64_t off = static_cast<std::int64_t>(grow) * n + gcol;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const bool ok = grow < m && gcol + 8 * v < n;  // n % 8 == 0: whole vectors
-        // Streaming loads (evict-first): the fused operand is read once and
-        // must not push the GEMM's A / B panels out of L2.
-        d[0][v] = ok && nst > 0 ? __ldcs(reinterpret_cast<const uint4*>(src0 + off) + v) : make_uint4(0, 0, 0, 0);
-        d[1][v] = ok && nst > 1 ? __ldcs(reinterpret_cast<const uint4*>(src1 + off) + v) : make_uint4(0, 0, 0, 0);
-      }
-    };
-    int g = 0;  // chunk counter of this warp (staging ring position)
-    auto chunk = [&](int t, int mb, int nb, int c, std::uint32_t base, int acc, uint4(&cur)[kMaxEpiSlots][4],
-                     uint4(&nxt)[kMaxEpiSlots][4]) {
-      if (c + 1 < BN / 32) load(t, c + 1, nxt);
-      else if (t + static_cast<int>(gridDim.x) < num_tiles) load(t + gridDim.x, 0, nxt);
-      std::uint32_t r[32];
-      tmem_ld32(base + c * 32, r);
-      if (c == BN / 32 - 1) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-      }
-      std::uint32_t cw[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) cw[i] = bf16_pair(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // ring entry g&1 is free
-      __syncwarp();
-      std::uint8_t* buf = stg + (g & 1) * 4096;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        *reinterpret_cast<uint4*>(buf + lane * 64 + ((v ^ swz) << 4)) =
-            make_uint4(cw[4 * v], cw[4 * v + 1], cw[4 * v + 2], cw[4 * v + 3]);
-        float accv[8];
-#pragma unroll
-        for (int i = 0; i < kMaxEpiIn; ++i) {
-          if (i >= epi.ops[0].n_in) break;
-          const uint4 w = i == epi.ops[0].gemm_pos ? make_uint4(cw[4 * v], cw[4 * v + 1], cw[4 * v + 2], cw[4 * v + 3])
-                          : (nst > 1 && epi.slot_in[1] == i) ? cur[1][v]
-                                                             : cur[0][v];
-          float x[8];
-          bf16_unpair(w.x, x[0], x[1]);
-          bf16_unpair(w.y, x[2], x[3]);
-          bf16_unpair(w.z, x[4], x[5]);
-          bf16_unpair(w.w, x[6], x[7]);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) accv[e] = i == 0 ? x[e] : epi_apply(epi.ops[0].op, accv[e], x[e]);
-        }
-        *reinterpret_cast<uint4*>(buf + 2048 + lane * 64 + ((v ^ swz) << 4)) =
-            make_uint4(bf16_pair(accv[0], accv[1]), bf16_pair(accv[2], accv[3]), bf16_pair(accv[4], accv[5]),
-                       bf16_pair(accv[6], accv[7]));
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-        const int c0 = nb * BN + c * 32, c1 = mb * BM + q * 32;
-        // The fused op streams a tensor as large as C through L2: its
-        // results leave evict-first so the GEMM's A / B panels stay resident.
-        const std::uint64_t pol = l2_evict_first_policy();
-        tma_store_2d_nc_hint(&gm.c[0], buf, c0, c1, pol);
-        tma_store_2d_nc_hint(&maps.out[0], buf + 2048, c0, c1, pol);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-      ++g;
-    };
-    uint4 pa[kMaxEpiSlots][4], pb[kMaxEpiSlots][4];
-    if (blockIdx.x < num_tiles) load(blockIdx.x, 0, pa);
-    int local = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
-      int mb, nb;
-      tile_coords(t, tiles_m, tiles_n, mb, nb);
-      const int acc = local & 1;
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
-      tc_fence_after();
-      const std::uint32_t base = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; c += 2) {
-        chunk(t, mb, nb, c, base, acc, pa, pb);
-        chunk(t, mb, nb, c + 1, base, acc, pb, pa);
-      }
-    }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
-  }
-}
-
-// Split-K reduction: C_p[row][col..col+3] = sum over splits s (in order) of
-// ws[(p*S + s)*m_pad + row][col..col+3] — coalesced on both sides.
-struct SplitOut {
-  void* c[kMaxGemmGroup];
-};
-
-template <bool C_BF16>
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __restrict__ ws, const __grid_constant__ SplitOut out, int S,
-                                                            int m, int n, int m_pad, int n_pad, int ng) {
-  pdl_wait();
-  pdl_trigger();
-  const int n4 = n / 4;
-  const long long per = static_cast<long long>(m) * n4;
-  const long long total = per * ng;
-  const int np4 = n_pad / 4;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int p = static_cast<int>(i / per);
-    const long long rem = i - p * per;
-    const int row = static_cast<int>(rem / n4), c4 = static_cast<int>(rem - static_cast<long long>(row) * n4);
-    const float4* src = ws + (static_cast<long long>(p) * S * m_pad + row) * np4 + c4;
-    const long long step = static_cast<long long>(m_pad) * np4;
-    // kSplitBatch partial loads in flight per thread, summed in split order.
-    constexpr int kSplitBatch = 8;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s0 = 0; s0 < S; s0 += kSplitBatch) {
-      float4 v[kSplitBatch];
-#pragma unroll
-      for (int j = 0; j < kSplitBatch; ++j)
-        if (s0 + j < S) v[j] = __ldcg(src + (s0 + j) * step);
-#pragma unroll
-      for (int j = 0; j < kSplitBatch; ++j) {
-        if (s0 + j >= S) break;
-        if (s0 + j == 0) {
-          acc = v[j];
-        } else {
-          acc.x += v[j].x;
-          acc.y += v[j].y;
-          acc.z += v[j].z;
-          acc.w += v[j].w;
-        }
-      }
-    }
-    if constexpr (C_BF16) {
-      uint2 w = make_uint2(bf16_pair(acc.x, acc.y), bf16_pair(acc.z, acc.w));
-      reinterpret_cast<uint2*>(out.c[p])[rem] = w;
-    } else {
-      reinterpret_cast<float4*>(out.c[p])[rem] = acc;
-    }
-  }
-}
-
-// ---- host ---------------------------------------------------------------------
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess) {
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-  });
-  if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
-  return fn;
-}
-
-// bf16 row-major [rows][cols] matrix, box {64 cols, box_rows}, 128B swizzle.
-CUtensorMap make_map(const void* base, std::int64_t rows, std::int64_t cols, int box_rows) {
-  CUtensorMap m;
-  std::memset(&m, 0, sizeof(m));
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
-  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
-  return m;
-}
-
-// Output map for the staged epilogue: [m][n] row-major, 32x32 boxes,
-// 64B swizzle for bf16 rows (64 B), 128B swizzle for fp32 rows (128 B).
-CUtensorMap make_store_map(void* base, std::int64_t m, std::int64_t n, bool bf16) {
-  CUtensorMap map;
-  std::memset(&map, 0, sizeof(map));
-  const std::int64_t es = bf16 ? 2 : 4;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(m)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(n * es)};
-  cuuint32_t box[2] = {32, 32};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode_fn()(&map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base,
-                           dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (C) failed: " + std::to_string(r));
-  return map;
-}
-
-int device_sms() {
-  static int num_sms[32] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (num_sms[dev & 31] == 0) {
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    num_sms[dev & 31] = v > 0 ? v : 148;
-  }
-  return num_sms[dev & 31];
-}
-
-template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE, int NG, int OCC = 1>
-void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
-  static unsigned attr_set_mask = 0;  // per device ordinal
-  constexpr int SMEM_BYTES = Cfg<BN, FUSE, OCC>::SMEM_BYTES;
-  auto kern = gemm_tc_kernel<A_MN, B_MN, C_BF16, BN, FUSE, NG, OCC>;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!(attr_set_mask & (1u << dev))) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc smem attribute: ") + cudaGetErrorString(e));
-    attr_set_mask |= 1u << dev;
-  }
-  // A: [m][k] (K-major) or, transposed, [k][m] (MN-major); B: [k][n]
-  // (MN-major) or, transposed, [n][k] (K-major).
-  const int ng = a.group > 1 ? a.group : 1;
-  if (ng > NG) throw std::runtime_error("gemm_tc: group above the launch's capacity");
-  if (FUSE && ng > 1) throw std::runtime_error("gemm_tc: fused epilogue on a grouped launch");
-  GroupMaps<NG> gm;
-  std::memset(&gm, 0, sizeof(gm));
-  for (int i = 0; i < ng; ++i) {
-    const void* A = ng > 1 ? a.gA[i] : a.A;
-    const void* B = ng > 1 ? a.gB[i] : a.B;
-    void* C = ng > 1 ? a.gC[i] : a.C;
-    gm.a[i] = A_MN ? make_map(A, a.k, a.m, BK) : make_map(A, a.m, a.k, BM);
-    gm.b[i] = B_MN ? make_map(B, a.k, a.n, BK) : make_map(B, a.n, a.k, BN);
-    gm.c[i] = make_store_map(a.scatter > 0 ? a.gC[0] : C, a.scatter > 0 ? a.scatter_rows : a.m, a.n, C_BF16);
-  }
-  if (a.scatter > 0) {
-    if (a.scatter > kMaxGemmGroup || ng != 1 || FUSE || sc.splits > 1 || sc.sk_ctas > 0 || sc.half_items > 0 ||
-        a.scatter_rows % BM != 0 || a.scatter_rows * a.scatter != a.m)
-      throw std::runtime_error("gemm_tc: reduce-scatter epilogue needs a plain data-parallel launch");
-  }
-  EpiMaps maps;
-  std::memset(&maps, 0, sizeof(maps));
-  if constexpr (FUSE) maps.out[0] = make_store_map(a.epi.ops[0].out, a.m, a.n, true);
-  SkParams sk;
-  sk.dp_tiles = sc.dp_tiles;
-  sk.sk_ctas = sc.sk_ctas;
-  sk.sk_iters = sc.sk_iters;
-  sk.splits = sc.splits;
-  sk.half_items = sc.half_items;
-  sk.scatter_rows = a.scatter > 0 ? static_cast<int>(a.scatter_rows) : 0;
-  for (int i = 0; i < a.scatter; ++i) sk.scatter_dst[i] = a.gC[i];
-  const std::int64_t m_pad = (a.m + BM - 1) / BM * BM, n_pad = (a.n + BN - 1) / BN * BN;
-  if (sc.splits > 1) {
-    // Partials: fp32 [ng * splits * m_pad][n_pad], stored like an fp32 C.
-    maps.ws = make_store_map(a.ws, static_cast<std::int64_t>(ng) * sc.splits * m_pad, n_pad, false);
-  } else if (sc.sk_ctas > 0) {
-    char* ws = static_cast<char*>(a.ws);
-    sk.counters = reinterpret_cast<int*>(ws);
-    sk.partials = reinterpret_cast<float*>(ws + sc.counter_bytes);
-  }
-  pdl_launch("gemm_tc_kernel", kern, dim3(sc.grid), dim3(NUM_THREADS), SMEM_BYTES, s, gm, ng, static_cast<int>(a.m),
-             static_cast<int>(a.n), static_cast<int>(a.k), a.epi, maps, sk);
-  if (sc.splits > 1) {
-    SplitOut out;
-    for (int i = 0; i < ng; ++i) out.c[i] = ng > 1 ? a.gC[i] : a.C;
-    const long long work = static_cast<long long>(ng) * a.m * (a.n / 4);
-    const int blocks = static_cast<int>(std::min<long long>((work + 255) / 256, 4LL * device_sms()));
-    pdl_launch("splitk_reduce_kernel", splitk_reduce_kernel<C_BF16>, dim3(blocks), dim3(256), 0, s,
-               static_cast<const float4*>(a.ws), out, sc.splits, static_cast<int>(a.m), static_cast<int>(a.n),
-               static_cast<int>(m_pad), static_cast<int>(n_pad), ng);
-  }
-}
-
-template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
-void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
-  if constexpr (FUSE) {
-    launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
-  } else if constexpr (BN <= 128) {
-    const bool wide = a.group > 1;  // member maps
-    if (sc.occ == 2) {
-      if (wide) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup, 2>(a, sc, s);
-      else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1, 2>(a, sc, s);
-    } else {
-      if (wide) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup>(a, sc, s);
-      else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
-    }
-  } else {
-    if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup>(a, sc, s);
-    else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
-  }
-}
 
 // Modelled time (us) of one launch, calibrated on B200 single-GEMM graphs
 // (profiles/r01/gemm_streamk*.jsonl): per k-block MMA time by tile width
@@ -1082,6 +156,16 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
     o.occ = 2;
     best = o;
   }
+  // Short-k launches that fill the GPU on their own: the tile epilogue
+  // (BN/32 TMEM chunks per warp) outlasts the tile's few k-blocks of MMAs,
+  // so 8 epilogue warps split each tile's columns. PLANC_B200_EPI8=0
+  // disables it, =2 forces it on plain data-parallel launches.
+  const char* e8 = std::getenv("PLANC_B200_EPI8");
+  const int e8mode = e8 ? std::atoi(e8) : 1;
+  if (e8mode != 0 && best.occ == 1 && a.epi.n_ops == 0 && a.scatter == 0 && best.splits <= 1 && best.sk_ctas == 0 &&
+      best.half_items == 0 && (e8mode == 2 || num_k <= 16)) {
+    best.occ = 3;
+  }
   return best;
 }
 
@@ -1114,38 +198,15 @@ void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
     sc = schedule_for(a.m, a.n, a.k, sc.bn, false, device_sms(), false, a.group,
                       a.epi.n_ops == 0);  // no workspace: data-parallel
   }
-  const int bn = sc.bn;
   if (a.epi.n_ops > 0) {
     if (!cb) throw std::runtime_error("fused GEMM epilogue needs a bf16 output");
     if (a.epi.n_ops != 1 || a.epi.n_slots > kMaxEpiSlots || a.epi.ops[0].n_in > kMaxEpiIn)
       throw std::runtime_error("fused GEMM epilogue: one elementwise op with <= 2 other operands");
-#define PLANC_TCF(AM, BMN)                                                      \
-  if (a_mn == AM && b_mn == BMN) {                                             \
-    if (bn == 256) return launch_typed<AM, BMN, true, 256, true>(a, sc, s);    \
-    if (bn == 128) return launch_typed<AM, BMN, true, 128, true>(a, sc, s);    \
-    return launch_typed<AM, BMN, true, 64, true>(a, sc, s);                    \
   }
-    PLANC_TCF(false, false)
-    PLANC_TCF(false, true)
-    PLANC_TCF(true, false)
-    PLANC_TCF(true, true)
-#undef PLANC_TCF
-  }
-#define PLANC_TC(AM, BMN, CB)                                                   \
-  if (a_mn == AM && b_mn == BMN && cb == CB) {                                 \
-    if (bn == 256) return launch_typed<AM, BMN, CB, 256, false>(a, sc, s);     \
-    if (bn == 128) return launch_typed<AM, BMN, CB, 128, false>(a, sc, s);     \
-    return launch_typed<AM, BMN, CB, 64, false>(a, sc, s);                     \
-  }
-  PLANC_TC(false, false, false)
-  PLANC_TC(false, false, true)
-  PLANC_TC(false, true, false)
-  PLANC_TC(false, true, true)
-  PLANC_TC(true, false, false)
-  PLANC_TC(true, false, true)
-  PLANC_TC(true, true, false)
-  PLANC_TC(true, true, true)
-#undef PLANC_TC
+  if (!a_mn && !b_mn) return launch_gemm_tc_ab<false, false>(a, sc, s);
+  if (!a_mn && b_mn) return launch_gemm_tc_ab<false, true>(a, sc, s);
+  if (a_mn && !b_mn) return launch_gemm_tc_ab<true, false>(a, sc, s);
+  return launch_gemm_tc_ab<true, true>(a, sc, s);
 }
 
 }  // namespace planc_b200

@@ -18,7 +18,7 @@ VARIANTS = [
     ("base", 0, {}),
     ("no_grouping", pb.NO_GROUPING, {}),
     ("no_occ2", 0, {"PLANC_B200_OCC2": "0"}),
-    ("no_scatter", pb.NO_SCATTER, {}),
+    ("no_epi8", 0, {"PLANC_B200_EPI8": "0"}),
     ("no_fusion", pb.NO_FUSION, {}),
 ]
 
