@@ -166,6 +166,18 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
       best.half_items == 0 && (e8mode == 2 || num_k <= 16)) {
     best.occ = 3;
   }
+  // Cluster pairs sharing B tiles by TMA multicast (halves B's L2 -> SM
+  // traffic). PLANC_B200_CLUSTER=2 forces it on plain data-parallel
+  // launches with tiles >= 128 wide; 0 (default) leaves it off.
+  const char* cenv = std::getenv("PLANC_B200_CLUSTER");
+  const int cmode = cenv ? std::atoi(cenv) : 0;
+  if (cmode != 0 && best.occ == 1 && a.epi.n_ops == 0 && a.scatter == 0 && best.splits <= 1 && best.sk_ctas == 0 &&
+      best.half_items == 0 && best.bn >= 128 && cmode == 2) {
+    const std::int64_t pairs =
+        ((a.m + 2 * BM - 1) / (2 * BM)) * ((a.n + best.bn - 1) / best.bn) * std::max(a.group, 1);
+    best.occ = 4;
+    best.grid = static_cast<int>(2 * std::min<std::int64_t>(pairs, sms / 2));
+  }
   return best;
 }
 

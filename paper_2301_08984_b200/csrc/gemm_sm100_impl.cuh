@@ -52,6 +52,9 @@ constexpr int NUM_THREADS = 192;
 // 2 = two CTAs per SM (short-k GEMMs that cannot fill the GPU); 3 = one CTA
 // per SM with 8 epilogue warps, two per TMEM lane quarter splitting a tile's
 // columns (short-k GEMMs whose tile epilogue outlasts its MMAs).
+// 4 = one CTA per SM in clusters of two along M: the pair shares each B
+// tile — every CTA loads half of it and multicasts to both (TMA
+// .multicast::cluster), halving B's L2 -> SM traffic.
 __host__ __device__ constexpr int epi_warps(int occ) { return occ == 3 ? 8 : 4; }
 __host__ __device__ constexpr int cta_threads(int occ) { return 64 + 32 * epi_warps(occ); }
 constexpr int GROUP_M = 8;
@@ -67,7 +70,8 @@ template <int BN_, bool FUSE = false, int OCC = 1>
 struct Cfg {
   static constexpr int BN = BN_;
   static constexpr int B_STAGE_BYTES = BN * BK * 2;
-  static constexpr int STAGES_RAW = ((OCC == 1 ? 200 : OCC == 2 ? 76 : 159) * 1024) / (A_STAGE_BYTES + B_STAGE_BYTES);
+  static constexpr int STAGES_RAW =
+      ((OCC == 1 || OCC == 4 ? 200 : OCC == 2 ? 76 : 159) * 1024) / (A_STAGE_BYTES + B_STAGE_BYTES);
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   // + epilogue staging: 4 warps x 2 buffers x (32 rows x 32 cols, <= 4 B);
   // FUSE (bf16): 4 warps x 2 x {C, fused result} 2 KB chunks — same size.
@@ -235,6 +239,34 @@ __device__ __forceinline__ std::uint64_t l2_evict_first_policy() {
   return p;
 }
 
+// Multicast load: the box lands at the same smem offset in every CTA of
+// ctaMask and completes bytes on each one's mbarrier at the same offset.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, std::uint64_t* bar,
+                                               std::uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_commit_mc(std::uint64_t* bar, std::uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ std::uint32_t cluster_rank() {
+  std::uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 // Same, without closing the bulk group (several stores per group).
 __device__ __forceinline__ void tma_store_2d_nc(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
@@ -329,7 +361,9 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
     gemm_tc_kernel(const __grid_constant__ GroupMaps<NG> gm, int ng, int m, int n, int k,
                    const __grid_constant__ EpiParams epi, const __grid_constant__ EpiMaps maps,
                    const __grid_constant__ SkParams sk) {
-  static_assert(OCC == 1 || (!FUSE && (OCC == 3 || BN <= 128)), "two CTAs per SM: no fusion, <= 256 TMEM columns");
+  static_assert(OCC == 1 || (!FUSE && (OCC >= 3 || BN <= 128)), "two CTAs per SM: no fusion, <= 256 TMEM columns");
+  static_assert(OCC != 4 || BN >= 128, "cluster pairs split B tiles in 64-wide halves");
+  constexpr bool CL = OCC == 4;
   constexpr int EPI_WARPS = epi_warps(OCC);
   extern __shared__ std::uint8_t smem_raw[];
   using CF = Cfg<BN, FUSE, OCC>;
@@ -357,8 +391,29 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
   const int num_k = (k + BK - 1) / BK;
   // Tile t of the launch: member t / per_gemm, its tile t % per_gemm.
   auto coords = [&](int t, int& p, int& mb, int& nb) {
-    p = t / per_gemm;
-    tile_coords(t - p * per_gemm, tiles_m, tiles_n, mb, nb);
+    if constexpr (CL) {
+      // t = 2 * pair + rank: pairs of vertically adjacent tiles sharing nb
+      const int tiles_m2 = (tiles_m + 1) / 2;
+      const int per_pair = tiles_m2 * tiles_n;
+      const int pr = t >> 1;
+      p = pr / per_pair;
+      int mb2;
+      tile_coords(pr - p * per_pair, tiles_m2, tiles_n, mb2, nb);
+      mb = 2 * mb2 + (t & 1);  // may pass tiles_m: a zero tile whose stores are clipped
+    } else {
+      p = t / per_gemm;
+      tile_coords(t - p * per_gemm, tiles_m, tiles_n, mb, nb);
+    }
+  };
+  // Work items: for_each_work, or — cluster pairs — pair tiles in lockstep.
+  auto work = [&](auto&& f) {
+    if constexpr (CL) {
+      const int pairs = ((tiles_m + 1) / 2) * tiles_n * ng;
+      const int rank = static_cast<int>(cluster_rank());
+      for (int pr = blockIdx.x / 2; pr < pairs; pr += gridDim.x / 2) f(2 * pr + rank, 0, num_k, -1);
+    } else {
+      for_each_work(num_k, sk, f);
+    }
   };
 
   if (warp == 0 && lane == 0) {
@@ -368,7 +423,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL ? 2 : 1);  // cluster pairs: both CTAs' MMAs free a stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -384,6 +439,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL) cluster_sync();  // peer barriers initialised before any multicast / remote arrive
   tc_fence_after();
   const std::uint32_t tmem = *tmem_slot;
   // Prologue done (barriers, TMEM, descriptor prefetch): from here on the
@@ -393,7 +449,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;  // global k-block counter across work items (ring position)
-      for_each_work(num_k, sk, [&](int t, int kb0, int kb1, int half) {
+      work([&](int t, int kb0, int kb1, int half) {
         int p, mb, nb;
         coords(t, p, mb, nb);
         const CUtensorMap* tmA = &gm.a[p];
@@ -414,7 +470,17 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
           } else {
             tma_load_2d(a, tmA, kb * BK, m0, &full[s]);
           }
-          if (B_MN) {
+          if constexpr (CL) {
+            // this CTA's half of the B tile, multicast to both CTAs of the pair
+            const int r = t & 1;
+            if (B_MN) {
+#pragma unroll
+              for (int j = r * (BN / 128); j < (r + 1) * (BN / 128); ++j)
+                tma_load_2d_mc(b + j * (64 * BK * 2), tmB, n0 + 64 * j, kb * BK, &full[s], 0x3);
+            } else {
+              tma_load_2d_mc(b + r * (BN / 2) * 128, tmB, kb * BK, n0 + r * (BN / 2), &full[s], 0x3);
+            }
+          } else if (B_MN) {
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * (64 * BK * 2), tmB, n0 + 64 * j, kb * BK, &full[s]);
           } else {
@@ -428,7 +494,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       constexpr std::uint32_t idesc_full = make_idesc<BN>(A_MN, B_MN);
       constexpr std::uint32_t idesc_half = make_idesc<(BN >= 128 ? BN / 2 : BN)>(A_MN, B_MN);
       int it = 0, local = 0;
-      for_each_work(num_k, sk, [&](int, int kb0, int kb1, int half) {
+      work([&](int, int kb0, int kb1, int half) {
         const std::uint32_t idesc = half >= 0 ? idesc_half : idesc_full;
         const int acc = local & 1;
         const std::uint32_t acc_phase = (local >> 1) & 1;
@@ -454,7 +520,8 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
                                     : smem_desc(b_base + kk * 32, 16, 1024);
             tc_mma(d, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
           }
-          tc_commit(&empty[s]);  // smem stage free once these MMAs retire
+          if constexpr (CL) tc_commit_mc(&empty[s], 0x3);  // both CTAs' producers refill the stage
+          else tc_commit(&empty[s]);  // smem stage free once these MMAs retire
         }
         tc_commit(&tfull[acc]);  // accumulator complete
         ++local;
@@ -507,7 +574,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       return reinterpret_cast<float4*>(sk.partials) +
              ((static_cast<std::int64_t>((b * 2 + slot) * 4 + q) * (BN / 32) + c) * 8) * 32 + lane;
     };
-    for_each_work(num_k, sk, [&](int t, int kb0, int kb1, int half) {
+    work([&](int t, int kb0, int kb1, int half) {
       int p, mb, nb;
       coords(t, p, mb, nb);
       const int acc = local & 1;
@@ -745,6 +812,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL) cluster_sync();  // no CTA leaves while its peer may still multicast / arrive into it
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
@@ -889,7 +957,7 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
     const void* B = ng > 1 ? a.gB[i] : a.B;
     void* C = ng > 1 ? a.gC[i] : a.C;
     gm.a[i] = A_MN ? make_map(A, a.k, a.m, BK) : make_map(A, a.m, a.k, BM);
-    gm.b[i] = B_MN ? make_map(B, a.k, a.n, BK) : make_map(B, a.n, a.k, BN);
+    gm.b[i] = B_MN ? make_map(B, a.k, a.n, BK) : make_map(B, a.n, a.k, OCC == 4 ? BN / 2 : BN);
     gm.c[i] = make_store_map(a.scatter > 0 ? a.gC[0] : C, a.scatter > 0 ? a.scatter_rows : a.m, a.n, C_BF16);
   }
   if (a.scatter > 0) {
@@ -917,7 +985,8 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
     sk.counters = reinterpret_cast<int*>(ws);
     sk.partials = reinterpret_cast<float*>(ws + sc.counter_bytes);
   }
-  pdl_launch("gemm_tc_kernel", kern, dim3(sc.grid), dim3(cta_threads(OCC)), SMEM_BYTES, s, gm, ng, static_cast<int>(a.m),
+  pdl_launch_cluster("gemm_tc_kernel", kern, dim3(sc.grid), dim3(cta_threads(OCC)), SMEM_BYTES, s, OCC == 4 ? 2 : 1,
+             gm, ng, static_cast<int>(a.m),
              static_cast<int>(a.n), static_cast<int>(a.k), a.epi, maps, sk);
   if (sc.splits > 1) {
     SplitOut out;
@@ -934,6 +1003,13 @@ template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
   if constexpr (FUSE) {
     launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
+  } else if (sc.occ == 4) {
+    if constexpr (BN >= 128) {
+      if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup, 4>(a, sc, s);
+      else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1, 4>(a, sc, s);
+    } else {
+      throw std::runtime_error("gemm_tc: cluster pairs need BN >= 128");
+    }
   } else if (sc.occ == 3) {
     if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup, 3>(a, sc, s);
     else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1, 3>(a, sc, s);

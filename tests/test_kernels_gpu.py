@@ -250,3 +250,29 @@ def test_two_ctas_per_sm_variant_vs_fp64(g, m, n, k, ta, tb, monkeypatch):
         a, b = inputs[3 * i], inputs[3 * i + 1]
         ref = (a.T if ta else a) @ (b.T if tb else b)
         assert np.abs(outs[i] - ref).max() / max(1.0, np.abs(ref).max()) < 2.0 ** -8
+
+
+@pytest.mark.parametrize("g,m,n,k,ta,tb", [(1, 8192, 2048, 2048, False, False), (1, 1000, 1000, 1000, True, False),
+                                           (2, 2048, 512, 4096, False, True), (1, 384, 256, 512, True, True)])
+def test_cluster_pair_multicast_variant_vs_fp64(g, m, n, k, ta, tb, monkeypatch):
+    """Clusters of two CTAs along M sharing each B tile by TMA multicast
+    (forced with PLANC_B200_CLUSTER=2; odd M-block counts give a zero tile
+    whose stores are clipped) against fp64."""
+    from plan_builder import grouped_matmul_plan
+
+    monkeypatch.setenv("PLANC_B200_CLUSTER", "2")
+    monkeypatch.setenv("PLANC_B200_EPI8", "0")
+    plan = grouped_matmul_plan(g, m, n, k, ta, tb)
+    rng = np.random.default_rng(g + 3 * m + n + k)
+    inputs = {}
+    for i in range(g):
+        inputs[3 * i] = bf16_round(rng.standard_normal((k, m) if ta else (m, k)))
+        inputs[3 * i + 1] = bf16_round(rng.standard_normal((n, k) if tb else (k, n)))
+    with pb.Executor(plan, lane_gpus=[0]) as ex:
+        ex.set_inputs(inputs)
+        ex.run(2)
+        outs = [ex.get_output(3 * i + 2) for i in range(g)]
+    for i in range(g):
+        a, b = inputs[3 * i], inputs[3 * i + 1]
+        ref = (a.T if ta else a) @ (b.T if tb else b)
+        assert np.abs(outs[i] - ref).max() / max(1.0, np.abs(ref).max()) < 2.0 ** -8
