@@ -155,6 +155,30 @@ def measured_peaks():
 NVLINK_GBS = 900.0  # nominal per direction per GPU (measured peer copy 770)
 
 
+def pcie_bandwidth(device: int, nbytes: int = 256 << 20, reps: int = 3):
+    """Measured pinned host<->device copy bandwidth (GB/s) of this GPU's link:
+    the bound of the end-to-end arm, whose steps move their inputs / results
+    across it."""
+    import torch
+
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+    out = {}
+    for name, (dst, src) in (("h2d", (d, h)), ("d2h", (h, d))):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize(device)
+        best = 0.0
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dst.copy_(src, non_blocking=True)
+            b.record()
+            b.synchronize()
+            best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
+        out[name] = best
+    return out
+
+
 def cpu_baseline(config: str, budget_s: float = 20.0):
     """The reference's own CPU executor (oracle/_ref run_plan, 1 thread) on the
     reduced-shape plan of the same graph, bounded in time."""
@@ -294,6 +318,15 @@ def main():
     if dist:
         dist.barrier()  # peer memory: no rank unmaps / frees while another still reads
     ex.close()
+    e2e_bound = {}
+    if rank == 0:
+        try:  # the link bound of the e2e arm: max(H2D, D2H, device step) with copies overlapped
+            bw = pcie_bandwidth(int(os.environ.get("LOCAL_RANK", 0)) if dist else 0)
+            t_link = max(h2d / (bw["h2d"] * 1e9), d2h / (bw["d2h"] * 1e9)) * 1e3
+            e2e_bound = {"pcie_gbs": {k: round(v, 1) for k, v in bw.items()},
+                         "bound_ms": max(t_link, ms), "frac_of_bound": max(t_link, ms) / e2e_ms}
+        except Exception as e:  # torch / pinned memory unavailable
+            e2e_bound = {"pcie_gbs": None, "note": str(e)[:100]}
     if rank == 0:
         sps = meta["samples_per_step"] / (ms / 1e3)
         # Dominant kernel (largest share of the serialised step) and its roofline.
@@ -396,7 +429,8 @@ def main():
             "kernel_families": families,
             "e2e": {"value": meta["samples_per_step"] / (e2e_ms / 1e3), "unit": "samples/s",
                     "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "via": "planc_b200_run_e2e (C ABI): pinned H2D of step inputs, graph step, D2H of results"},
+                    "via": "planc_b200_run_e2e (C ABI): pinned H2D of step inputs, graph step, D2H of results",
+                    **e2e_bound},
             "gpu_launches": st["kernels_per_step"] * args.steps,
             "gemm_tc_launches_per_step": st["gemm_tc_per_step"],
             "clocks": clocks,
