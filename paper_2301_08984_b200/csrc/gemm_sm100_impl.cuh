@@ -317,6 +317,22 @@ __host__ __device__ constexpr std::uint32_t make_idesc(bool a_mn, bool b_mn) {
          | (static_cast<std::uint32_t>(BM >> 4) << 24); // M
 }
 
+// tcgen05.ld without the wait: the registers are valid after tmem_wait_ld()
+// (which waits for every outstanding load of the thread).
+__device__ __forceinline__ void tmem_ld32_issue(std::uint32_t taddr, std::uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -591,16 +607,9 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
         const int x0 = nb * BN + (half > 0 ? BN / 2 : 0);
         const int c_lo = EPI_WARPS == 8 ? col_half * (chunks / 2) : 0;
         const int c_hi = EPI_WARPS == 8 ? c_lo + chunks / 2 : chunks;
-#pragma unroll 1
-        for (int c = c_lo; c < c_hi; ++c) {
-          std::uint32_t r[32];
-          tmem_ld32(base + c * 32, r);
-          if (c == c_hi - 1) {
-            // All TMEM reads of this accumulator are complete: hand it back.
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
+        // The TMEM load of chunk c+1 is in flight while chunk c is emitted
+        // (ping-pong registers; tcgen05.wait::ld waits for every earlier load).
+        auto emit = [&](const std::uint32_t(&r)[32], int c) {
           if (part) {
             store_chunk(r, &maps.ws, false, x0 + c * 32, y);
           } else if (sk.scatter_rows > 0) {
@@ -627,6 +636,29 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
             }
           } else {
             store_chunk(r, &gm.c[p], C_BF16, x0 + c * 32, y);
+          }
+        };
+        auto release = [&] {  // every TMEM read of this accumulator has completed
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        };
+        std::uint32_t ra[32], rb[32];
+        tmem_ld32_issue(base + c_lo * 32, ra);
+        tmem_wait_ld();
+#pragma unroll 1
+        for (int c = c_lo; c < c_hi; c += 2) {
+          const bool has1 = c + 1 < c_hi;
+          if (has1) tmem_ld32_issue(base + (c + 1) * 32, rb);
+          else release();
+          emit(ra, c);
+          if (has1) {
+            tmem_wait_ld();
+            const bool has2 = c + 2 < c_hi;
+            if (has2) tmem_ld32_issue(base + (c + 2) * 32, ra);
+            else release();
+            emit(rb, c + 1);
+            if (has2) tmem_wait_ld();
           }
         }
         return;
