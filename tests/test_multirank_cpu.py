@@ -154,7 +154,8 @@ def test_localised_program_invariants():
 # all ranks' blocks and compares with the reference, bit-exact.
 
 PEER_CASES = ["mlp_dp2", "tp_value_split", "gpt_block_tp2", "adapt_v_to_r4", "adapt_v_to_d4", "adapt_d1_to_d0_4",
-              "embed_shard2", "three_pass_3f1b", "mlp_1f1b_dp2", "cross_group_rs", "mlp_dp2_naive", "ext_block_tp2"]
+              "embed_shard2", "three_pass_3f1b", "mlp_1f1b_dp2", "cross_group_rs", "mlp_dp2_naive", "ext_block_tp2",
+              "gpt_block_fwd_tp2_mma"]
 
 
 def _peer_worker(rank, world, port, names, result_q):
@@ -228,8 +229,7 @@ def _peer_worker(rank, world, port, names, result_q):
                             {x for f in ins.get("fused", []) for x in f["in"] + [f["out"]]}}
                     exec_instr(ins, data, shape)
                     outs = list(ins["out"]) + [f["out"] for f in ins.get("fused", [])]
-                    for b in outs:
-                        assert owner(b) == rank
+                    for b in outs:  # own pieces, or (reduce-scatter epilogue) slices stored into a peer's block
                         view(b)[:] = data[b]
                     for r, slot in ps["signals"][iid]:
                         F[r][64 + world + slot] = epoch
