@@ -973,6 +973,31 @@ void launch_rowwise(int op, int dtype, const void* a, const void* b, void* out, 
   else throw std::runtime_error("rowwise: element type must be fp32 or bf16");
 }
 
+__global__ void __launch_bounds__(256) copy_bytes_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                         long long nvec, unsigned char* __restrict__ dtail,
+                                                         const unsigned char* __restrict__ stail, int tail) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec; i += stride)
+    dst[i] = __ldcs(src + i);
+  if (blockIdx.x == 0 && static_cast<int>(threadIdx.x) < tail) dtail[threadIdx.x] = stail[threadIdx.x];
+}
+
+void launch_copy_bytes(void* dst, const void* src, std::int64_t bytes, cudaStream_t s) {
+  if (bytes <= 0) return;
+  if ((reinterpret_cast<std::uintptr_t>(dst) | reinterpret_cast<std::uintptr_t>(src)) % 16 != 0) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("copy: ") + cudaGetErrorString(e));
+    return;
+  }
+  const long long nvec = bytes / 16;
+  const int tail = static_cast<int>(bytes - nvec * 16);
+  pdl_launch("copy_bytes_kernel", copy_bytes_kernel, dim3(grid_for(std::max<long long>(nvec, 1), 256 * 4)), dim3(256),
+             0, s, static_cast<uint4*>(dst), static_cast<const uint4*>(src), nvec,
+             static_cast<unsigned char*>(dst) + nvec * 16, static_cast<const unsigned char*>(src) + nvec * 16, tail);
+}
+
 // ---- peer-memory flags ------------------------------------------------------
 
 __global__ void peer_epoch_kernel(unsigned* epoch) {

@@ -160,6 +160,9 @@ void launch_rowwise(int op, int dtype, const void* a, const void* b, void* out, 
                     float eps, cudaStream_t s);
 void launch_convert(int dtype_out, void* out, const float* in, std::int64_t count, cudaStream_t s);
 void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s);
+// Device-to-device copy on the SMs (16-byte vectors): keeps the copy engines
+// free for the host-link transfers running beside it (end-to-end mode).
+void launch_copy_bytes(void* dst, const void* src, std::int64_t bytes, cudaStream_t s);
 
 // Cross-rank ordering in peer-memory mode (program.hpp PeerSync). One
 // launch first publishes the step epoch (*epoch) to every `sig` flag

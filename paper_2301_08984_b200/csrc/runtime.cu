@@ -1039,7 +1039,7 @@ double Executor::run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_b
     ck(cudaStreamWaitEvent(origin_, ev_h2d_[slot], 0), "wait h2d");
     for (std::size_t i = 0; i < e2e_in_bufs_.size(); ++i) {
       const auto& b = prog_.buffers[e2e_in_bufs_[i]];
-      ck(cudaMemcpyAsync(buf_ptr(b.id), e2e_stage_in_[slot][i], b.bytes, cudaMemcpyDeviceToDevice, origin_), "in");
+      launch_copy_bytes(buf_ptr(b.id), e2e_stage_in_[slot][i], b.bytes, origin_);  // SMs: copy engines carry PCIe
     }
     ck(cudaEventRecord(ev_in_free_[slot], origin_), "record stage free");
     if (graph_exec_) ck(cudaGraphLaunch(graph_exec_, origin_), "graph launch");
@@ -1047,7 +1047,7 @@ double Executor::run_e2e(int iters, std::int64_t* h2d_bytes, std::int64_t* d2h_b
     ck(cudaStreamWaitEvent(origin_, ev_out_free_[slot], 0), "wait out free");
     for (std::size_t i = 0; i < e2e_out_bufs_.size(); ++i) {
       const auto& b = prog_.buffers[e2e_out_bufs_[i]];
-      ck(cudaMemcpyAsync(e2e_stage_out_[slot][i], buf_ptr(b.id), b.bytes, cudaMemcpyDeviceToDevice, origin_), "out");
+      launch_copy_bytes(e2e_stage_out_[slot][i], buf_ptr(b.id), b.bytes, origin_);
     }
     ck(cudaEventRecord(ev_out_ready_[slot], origin_), "record out ready");
   };
