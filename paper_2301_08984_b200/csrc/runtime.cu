@@ -189,7 +189,11 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   // recently used stream. Only data dependencies (and sync edges) then order
   // a lane's work, via events between streams.
   {
-    const int ns = std::max(1, std::min(opt_.streams_per_lane, kLaneStreams));
+    int want = opt_.streams_per_lane;
+    if (const char* e = std::getenv("PLANC_B200_STREAMS")) {
+      if (want > 1) want = std::atoi(e);  // A/B of the stream count (SERIAL_LANES keeps 1)
+    }
+    const int ns = std::max(1, std::min(want, kLaneStreams));
     exec_stream_.assign(prog_.instrs.size(), 0);
     std::vector<std::vector<int>> last(prog_.num_lanes, std::vector<int>(ns, -1));
     for (int id : prog_.issue_order) {

@@ -41,13 +41,13 @@ struct KernelStat {
 // Streams per lane. Instructions of a lane are spread over them so that only
 // true data dependencies (and sync edges) order work: independent GEMMs,
 // elementwise ops and adapters of one lane overlap on the GPU.
-constexpr int kLaneStreams = 4;
+constexpr int kLaneStreams = 8;  // capacity; streams used per lane: ExecOptions / PLANC_B200_STREAMS (default 4)
 
 struct ExecOptions {
   bool use_graph = true;       // capture one step into a CUDA graph
   bool allow_tensor_cores = true;
   bool value_split_extension = true;
-  int streams_per_lane = kLaneStreams;  // 1 = issue a lane strictly in plan order
+  int streams_per_lane = 4;             // 1 = issue a lane strictly in plan order
   bool fuse_epilogues = true;           // elementwise consumers computed in GEMM epilogues
   bool group_gemms = true;              // same-shape independent GEMMs in one grouped launch
   bool alias_copies = true;             // same-GPU whole-buffer copies (recv, identity) become aliases
