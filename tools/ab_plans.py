@@ -18,8 +18,7 @@ VARIANTS = [
     ("base", 0, {}),
     ("no_grouping", pb.NO_GROUPING, {}),
     ("no_occ2", 0, {"PLANC_B200_OCC2": "0"}),
-    ("streams8", 0, {"PLANC_B200_STREAMS": "8"}),
-    ("streams2", 0, {"PLANC_B200_STREAMS": "2"}),
+    ("no_sync_edges", 0, {"PLANC_B200_SYNC_EDGES": "0"}),
     ("no_fusion", pb.NO_FUSION, {}),
 ]
 
