@@ -171,11 +171,14 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   // launches with tiles >= 128 wide; 0 (default) leaves it off.
   const char* cenv = std::getenv("PLANC_B200_CLUSTER");
   const int cmode = cenv ? std::atoi(cenv) : 0;
-  if (cmode != 0 && best.occ == 1 && a.epi.n_ops == 0 && a.scatter == 0 && best.splits <= 1 && best.sk_ctas == 0 &&
-      best.half_items == 0 && best.bn >= 128 && cmode == 2) {
+  // PLANC_B200_2SM=2: the pair runs one 256-row tcgen05 MMA (cta_group::2).
+  const char* senv = std::getenv("PLANC_B200_2SM");
+  const int smode = senv ? std::atoi(senv) : 0;
+  if ((cmode == 2 || smode == 2) && best.occ == 1 && a.epi.n_ops == 0 && a.scatter == 0 && best.splits <= 1 &&
+      best.sk_ctas == 0 && best.half_items == 0 && best.bn >= 128) {
     const std::int64_t pairs =
         ((a.m + 2 * BM - 1) / (2 * BM)) * ((a.n + best.bn - 1) / best.bn) * std::max(a.group, 1);
-    best.occ = 4;
+    best.occ = smode == 2 ? 5 : 4;
     best.grid = static_cast<int>(2 * std::min<std::int64_t>(pairs, sms / 2));
   }
   return best;

@@ -71,7 +71,7 @@ struct Cfg {
   static constexpr int BN = BN_;
   static constexpr int B_STAGE_BYTES = BN * BK * 2;
   static constexpr int STAGES_RAW =
-      ((OCC == 1 || OCC == 4 ? 200 : OCC == 2 ? 76 : 159) * 1024) / (A_STAGE_BYTES + B_STAGE_BYTES);
+      ((OCC == 1 || OCC >= 4 ? 200 : OCC == 2 ? 76 : 159) * 1024) / (A_STAGE_BYTES + B_STAGE_BYTES);
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   // + epilogue staging: 4 warps x 2 buffers x (32 rows x 32 cols, <= 4 B);
   // FUSE (bf16): 4 warps x 2 x {C, fused result} 2 KB chunks — same size.
@@ -257,6 +257,46 @@ __device__ __forceinline__ void tc_commit_mc(std::uint64_t* bar, std::uint16_t m
                : "memory");
 }
 
+// 2-SM variant: TMA load whose completion is counted on the pair leader's
+// mbarrier (shared::cluster address), and the leader's MMA commit.
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                std::uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_commit_2sm_mc(std::uint64_t* bar, std::uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_2sm(std::uint32_t tmem_d, std::uint64_t adesc, std::uint64_t bdesc,
+                                           std::uint32_t idesc, std::uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// shared::cluster address of `p` in CTA `rank` of the cluster.
+__device__ __forceinline__ std::uint32_t cluster_addr(const void* p, std::uint32_t rank) {
+  std::uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(std::uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -306,7 +346,7 @@ __device__ __forceinline__ std::uint64_t smem_desc(std::uint32_t addr, std::uint
 }
 
 // Instruction descriptor: kind::f16, A/B bf16, D f32, M=128, N=BN.
-template <int BN>
+template <int BN, int M = BM>
 __host__ __device__ constexpr std::uint32_t make_idesc(bool a_mn, bool b_mn) {
   return (1u << 4)                              // D format f32
          | (1u << 7)                            // A bf16
@@ -314,7 +354,7 @@ __host__ __device__ constexpr std::uint32_t make_idesc(bool a_mn, bool b_mn) {
          | ((a_mn ? 1u : 0u) << 15)             // A major
          | ((b_mn ? 1u : 0u) << 16)             // B major
          | (static_cast<std::uint32_t>(BN >> 3) << 17)  // N
-         | (static_cast<std::uint32_t>(BM >> 4) << 24); // M
+         | (static_cast<std::uint32_t>(M >> 4) << 24);  // M
 }
 
 // tcgen05.ld without the wait: the registers are valid after tmem_wait_ld()
@@ -378,8 +418,10 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
                    const __grid_constant__ EpiParams epi, const __grid_constant__ EpiMaps maps,
                    const __grid_constant__ SkParams sk) {
   static_assert(OCC == 1 || (!FUSE && (OCC >= 3 || BN <= 128)), "two CTAs per SM: no fusion, <= 256 TMEM columns");
-  static_assert(OCC != 4 || BN >= 128, "cluster pairs split B tiles in 64-wide halves");
-  constexpr bool CL = OCC == 4;
+  static_assert(OCC < 4 || BN >= 128, "cluster pairs split B tiles in 64-wide halves");
+  constexpr bool CL = OCC == 4;   // pair sharing B by multicast, one MMA per CTA
+  constexpr bool SM2 = OCC == 5;  // pair running one 256-row MMA (tcgen05 cta_group::2)
+  constexpr bool PAIR = CL || SM2;
   constexpr int EPI_WARPS = epi_warps(OCC);
   extern __shared__ std::uint8_t smem_raw[];
   using CF = Cfg<BN, FUSE, OCC>;
@@ -407,7 +449,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
   const int num_k = (k + BK - 1) / BK;
   // Tile t of the launch: member t / per_gemm, its tile t % per_gemm.
   auto coords = [&](int t, int& p, int& mb, int& nb) {
-    if constexpr (CL) {
+    if constexpr (PAIR) {
       // t = 2 * pair + rank: pairs of vertically adjacent tiles sharing nb
       const int tiles_m2 = (tiles_m + 1) / 2;
       const int per_pair = tiles_m2 * tiles_n;
@@ -423,7 +465,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
   };
   // Work items: for_each_work, or — cluster pairs — pair tiles in lockstep.
   auto work = [&](auto&& f) {
-    if constexpr (CL) {
+    if constexpr (PAIR) {
       const int pairs = ((tiles_m + 1) / 2) * tiles_n * ng;
       const int rank = static_cast<int>(cluster_rank());
       for (int pr = blockIdx.x / 2; pr < pairs; pr += gridDim.x / 2) f(2 * pr + rank, 0, num_k, -1);
@@ -443,19 +485,25 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_WARPS);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], SM2 ? 2 * EPI_WARPS : EPI_WARPS);  // one arrive per epilogue warp (2-SM: both CTAs')
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (SM2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CL) cluster_sync();  // peer barriers initialised before any multicast / remote arrive
+  if constexpr (PAIR) cluster_sync();  // peer barriers initialised before any multicast / remote arrive
   tc_fence_after();
   const std::uint32_t tmem = *tmem_slot;
   // Prologue done (barriers, TMEM, descriptor prefetch): from here on the
@@ -473,6 +521,35 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
         // A half tile loads the B rows from its own first column (the box's
         // upper half is unused, and zero-filled past the tensor edge).
         const int m0 = mb * BM, n0 = nb * BN + (half > 0 ? BN / 2 : 0);
+        if constexpr (SM2) {
+          // 2-SM: this CTA's 128 rows of A and its half of B's columns land
+          // in its own smem; both CTAs' bytes are counted on the leader's
+          // full barrier, which only the leader arms (with both CTAs' bytes).
+          const int r = t & 1;
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            const int s = it % STAGES;
+            const std::uint32_t phase = (it / STAGES) & 1;
+            mbar_wait(&empty[s], phase ^ 1);
+            if (r == 0) mbar_expect_tx(&full[s], 2 * (A_STAGE_BYTES + B_STAGE_BYTES / 2));
+            const std::uint32_t lb = cluster_addr(&full[s], 0);
+            std::uint8_t* a = sA + s * A_STAGE_BYTES;
+            std::uint8_t* b = sB + s * B_STAGE_BYTES;
+            if (A_MN) {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d_2sm(a + j * (64 * BK * 2), tmA, m0 + 64 * j, kb * BK, lb);
+            } else {
+              tma_load_2d_2sm(a, tmA, kb * BK, m0, lb);
+            }
+            if (B_MN) {
+#pragma unroll
+              for (int j = 0; j < BN / 128; ++j)
+                tma_load_2d_2sm(b + j * (64 * BK * 2), tmB, n0 + r * (BN / 2) + 64 * j, kb * BK, lb);
+            } else {
+              tma_load_2d_2sm(b, tmB, kb * BK, n0 + r * (BN / 2), lb);
+            }
+          }
+          return;
+        }
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const std::uint32_t phase = (it / STAGES) & 1;
@@ -506,8 +583,10 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       });
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr std::uint32_t idesc_full = make_idesc<BN>(A_MN, B_MN);
+    if (SM2 && cluster_rank() != 0) {
+      // 2-SM: the pair leader issues every MMA for both CTAs.
+    } else if (lane == 0) {
+      constexpr std::uint32_t idesc_full = make_idesc<BN, SM2 ? 2 * BM : BM>(A_MN, B_MN);
       constexpr std::uint32_t idesc_half = make_idesc<(BN >= 128 ? BN / 2 : BN)>(A_MN, B_MN);
       int it = 0, local = 0;
       work([&](int, int kb0, int kb1, int half) {
@@ -534,12 +613,15 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
                                     : smem_desc(a_base + kk * 32, 16, 1024);
             std::uint64_t bd = B_MN ? smem_desc(b_base + kk * 2048, 64 * BK * 2, 1024)
                                     : smem_desc(b_base + kk * 32, 16, 1024);
-            tc_mma(d, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
+            if constexpr (SM2) tc_mma_2sm(d, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
+            else tc_mma(d, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
           }
-          if constexpr (CL) tc_commit_mc(&empty[s], 0x3);  // both CTAs' producers refill the stage
+          if constexpr (SM2) tc_commit_2sm_mc(&empty[s], 0x3);   // both CTAs' stages free
+          else if constexpr (CL) tc_commit_mc(&empty[s], 0x3);  // both CTAs' producers refill the stage
           else tc_commit(&empty[s]);  // smem stage free once these MMAs retire
         }
-        tc_commit(&tfull[acc]);  // accumulator complete
+        if constexpr (SM2) tc_commit_2sm_mc(&tfull[acc], 0x3);  // both CTAs' accumulator halves complete
+        else tc_commit(&tfull[acc]);  // accumulator complete
         ++local;
       });
       pdl_trigger();  // every MMA issued: the next kernel may start its prologue
@@ -641,7 +723,10 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
         auto release = [&] {  // every TMEM read of this accumulator has completed
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if constexpr (SM2) mbar_arrive_cluster(cluster_addr(&tempty[acc], 0));  // the leader's MMA waits
+            else mbar_arrive(&tempty[acc]);
+          }
         };
         std::uint32_t ra[32], rb[32];
         tmem_ld32_issue(base + c_lo * 32, ra);
@@ -844,10 +929,13 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CL) cluster_sync();  // no CTA leaves while its peer may still multicast / arrive into it
+  if constexpr (PAIR) cluster_sync();  // no CTA leaves while its peer may still multicast / arrive into it
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+    if constexpr (SM2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
   }
 }
 
@@ -989,7 +1077,7 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
     const void* B = ng > 1 ? a.gB[i] : a.B;
     void* C = ng > 1 ? a.gC[i] : a.C;
     gm.a[i] = A_MN ? make_map(A, a.k, a.m, BK) : make_map(A, a.m, a.k, BM);
-    gm.b[i] = B_MN ? make_map(B, a.k, a.n, BK) : make_map(B, a.n, a.k, OCC == 4 ? BN / 2 : BN);
+    gm.b[i] = B_MN ? make_map(B, a.k, a.n, BK) : make_map(B, a.n, a.k, OCC >= 4 ? BN / 2 : BN);
     gm.c[i] = make_store_map(a.scatter > 0 ? a.gC[0] : C, a.scatter > 0 ? a.scatter_rows : a.m, a.n, C_BF16);
   }
   if (a.scatter > 0) {
@@ -1017,7 +1105,7 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
     sk.counters = reinterpret_cast<int*>(ws);
     sk.partials = reinterpret_cast<float*>(ws + sc.counter_bytes);
   }
-  pdl_launch_cluster("gemm_tc_kernel", kern, dim3(sc.grid), dim3(cta_threads(OCC)), SMEM_BYTES, s, OCC == 4 ? 2 : 1,
+  pdl_launch_cluster("gemm_tc_kernel", kern, dim3(sc.grid), dim3(cta_threads(OCC)), SMEM_BYTES, s, OCC >= 4 ? 2 : 1,
              gm, ng, static_cast<int>(a.m),
              static_cast<int>(a.n), static_cast<int>(a.k), a.epi, maps, sk);
   if (sc.splits > 1) {
@@ -1035,9 +1123,12 @@ template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
   if constexpr (FUSE) {
     launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
-  } else if (sc.occ == 4) {
+  } else if (sc.occ == 4 || sc.occ == 5) {
     if constexpr (BN >= 128) {
-      if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup, 4>(a, sc, s);
+      if (sc.occ == 5) {
+        if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup, 5>(a, sc, s);
+        else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1, 5>(a, sc, s);
+      } else if (a.group > 1) launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, kMaxGemmGroup, 4>(a, sc, s);
       else launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1, 4>(a, sc, s);
     } else {
       throw std::runtime_error("gemm_tc: cluster pairs need BN >= 128");

@@ -18,7 +18,7 @@ VARIANTS = [
     ("base", 0, {}),
     ("no_grouping", pb.NO_GROUPING, {}),
     ("no_occ2", 0, {"PLANC_B200_OCC2": "0"}),
-    ("no_sync_edges", 0, {"PLANC_B200_SYNC_EDGES": "0"}),
+    ("two_sm", 0, {"PLANC_B200_2SM": "2"}),
     ("no_fusion", pb.NO_FUSION, {}),
 ]
 
