@@ -183,12 +183,13 @@ int planc_b200_gemm_config(int64_t m, int64_t n, int64_t k, int ta, int tb, int 
  * waves) followed by half_items half-width tiles (the last partial wave,
  * 128 x tile_n/2 each) or by the CTAs sharing the remaining tiles by k-range
  * (stream-K), or the number of k-splits per tile (split-K: fp32 partials + a
- * reduce kernel); with the workspace either needs (0 without); ctas_per_sm is 2
- * for the short-k variant (two CTAs share an SM, grid up to 2 x sms). bf16
- * operands. */
+ * reduce kernel); with the workspace either needs (0 without). `variant` is
+ * the kernel variant: 1 one CTA per SM, 2 two CTAs per SM (short k, grid up
+ * to 2 x sms), 3 eight epilogue warps (short k), 4 cluster pairs sharing B by
+ * multicast, 5 2-SM pairs (one 256-row tcgen05 MMA per pair). bf16 operands. */
 int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, int c_bf16, int sms, int group,
                              int* tile_n, int* grid, int* dp_tiles, int* sk_ctas, int* splits, int* half_items,
-                             int* ctas_per_sm, int64_t* ws_bytes);
+                             int* variant, int64_t* ws_bytes);
 
 /* Host-only lowering (no GPU needed): the executor's device program for a
  * plan as JSON — buffers, instructions, box cells, issue order. */

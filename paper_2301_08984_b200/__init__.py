@@ -174,7 +174,8 @@ def gemm_schedule(m: int, n: int, k: int, ta: bool = False, tb: bool = False, c_
                                       ctypes.byref(grid), ctypes.byref(dp), ctypes.byref(sk), ctypes.byref(sp),
                                       ctypes.byref(hf), ctypes.byref(occ), ctypes.byref(ws)))
     return {"tile_n": bn.value, "grid": grid.value, "dp_tiles": dp.value, "sk_ctas": sk.value, "splits": sp.value,
-            "half_items": hf.value, "ctas_per_sm": occ.value, "ws_bytes": ws.value}
+            "half_items": hf.value, "variant": occ.value, "ctas_per_sm": 2 if occ.value == 2 else 1,
+            "ws_bytes": ws.value}
 
 
 def nccl_unique_id() -> bytes:

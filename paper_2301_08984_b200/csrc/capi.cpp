@@ -336,7 +336,7 @@ int planc_b200_gemm_config(int64_t m, int64_t n, int64_t k, int ta, int tb, int 
 
 int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, int c_bf16, int sms, int group,
                              int* tile_n, int* grid, int* dp_tiles, int* sk_ctas, int* splits, int* half_items,
-                             int* ctas_per_sm, int64_t* ws_bytes) {
+                             int* variant, int64_t* ws_bytes) {
   return guarded([&] {
     if (sms <= 0) throw UsageError("sms must be positive");
     if (group < 1 || group > kMaxGemmGroup) throw UsageError("group must be in [1, 8]");
@@ -358,7 +358,7 @@ int planc_b200_gemm_schedule(int64_t m, int64_t n, int64_t k, int ta, int tb, in
     if (sk_ctas) *sk_ctas = sc.sk_ctas;
     if (splits) *splits = sc.splits;
     if (half_items) *half_items = sc.half_items;
-    if (ctas_per_sm) *ctas_per_sm = sc.occ;
+    if (variant) *variant = sc.occ;
     if (ws_bytes) *ws_bytes = sc.ws_bytes;
   });
 }

@@ -171,14 +171,19 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   // launches with tiles >= 128 wide; 0 (default) leaves it off.
   const char* cenv = std::getenv("PLANC_B200_CLUSTER");
   const int cmode = cenv ? std::atoi(cenv) : 0;
-  // PLANC_B200_2SM=2: the pair runs one 256-row tcgen05 MMA (cta_group::2).
+  // 2-SM pairs (one 256-row tcgen05 MMA per pair, cta_group::2) for
+  // medium-k data-parallel launches (16 < k-blocks <= 32, i.e. k <= 2048):
+  // C2x 1.921 -> 1.875 ms, C2 1.724 -> 1.714 ms; longer k measured neutral
+  // to slightly slower (C1-L), so it stays off there
+  // (profiles/r01/ab_2sm.jsonl). PLANC_B200_2SM=0 disables, =2 forces.
   const char* senv = std::getenv("PLANC_B200_2SM");
-  const int smode = senv ? std::atoi(senv) : 0;
-  if ((cmode == 2 || smode == 2) && best.occ == 1 && a.epi.n_ops == 0 && a.scatter == 0 && best.splits <= 1 &&
+  const int smode = senv ? std::atoi(senv) : 1;
+  const bool sm2 = smode == 2 || (smode == 1 && num_k > 16 && num_k <= 32);
+  if ((cmode == 2 || sm2) && best.occ == 1 && a.epi.n_ops == 0 && a.scatter == 0 && best.splits <= 1 &&
       best.sk_ctas == 0 && best.half_items == 0 && best.bn >= 128) {
     const std::int64_t pairs =
         ((a.m + 2 * BM - 1) / (2 * BM)) * ((a.n + best.bn - 1) / best.bn) * std::max(a.group, 1);
-    best.occ = smode == 2 ? 5 : 4;
+    best.occ = sm2 ? 5 : 4;
     best.grid = static_cast<int>(2 * std::min<std::int64_t>(pairs, sms / 2));
   }
   return best;
