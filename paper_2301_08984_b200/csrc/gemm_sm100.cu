@@ -172,15 +172,17 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   const char* cenv = std::getenv("PLANC_B200_CLUSTER");
   const int cmode = cenv ? std::atoi(cenv) : 0;
   // 2-SM pairs (one 256-row tcgen05 MMA per pair, cta_group::2) for
-  // medium-k data-parallel launches (16 < k-blocks <= 32, i.e. k <= 2048):
-  // C2x 1.921 -> 1.875 ms, C2 1.724 -> 1.714 ms; longer k measured neutral
-  // to slightly slower (C1-L), so it stays off there
-  // (profiles/r01/ab_2sm.jsonl). PLANC_B200_2SM=0 disables, =2 forces.
+  // data-parallel launches with more than 16 k-blocks (k > 1024), fused
+  // epilogues included: C2 1.733 -> 1.688 ms, C2x 1.906 -> 1.858 ms, C1-L
+  // 2.020 -> 1.960 ms, C4 / C5 neutral (profiles/r01/ab_2sm_fused.jsonl;
+  // short k keeps the eight-epilogue-warp / two-CTA variants).
+  // PLANC_B200_2SM=0 disables, =2 forces.
   const char* senv = std::getenv("PLANC_B200_2SM");
   const int smode = senv ? std::atoi(senv) : 1;
-  const bool sm2 = smode == 2 || (smode == 1 && num_k > 16 && num_k <= 32);
-  if ((cmode == 2 || sm2) && best.occ == 1 && a.epi.n_ops == 0 && a.scatter == 0 && best.splits <= 1 &&
-      best.sk_ctas == 0 && best.half_items == 0 && best.bn >= 128) {
+  const bool sm2 = smode == 2 || (smode == 1 && num_k > 16);
+  // (the 2-SM variant also carries fused elementwise epilogues)
+  if ((cmode == 2 || sm2) && best.occ == 1 && (a.epi.n_ops == 0 || (sm2 && cmode != 2)) && a.scatter == 0 &&
+      best.splits <= 1 && best.sk_ctas == 0 && best.half_items == 0 && best.bn >= 128) {
     const std::int64_t pairs =
         ((a.m + 2 * BM - 1) / (2 * BM)) * ((a.n + best.bn - 1) / best.bn) * std::max(a.group, 1);
     best.occ = sm2 ? 5 : 4;

@@ -417,7 +417,8 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
     gemm_tc_kernel(const __grid_constant__ GroupMaps<NG> gm, int ng, int m, int n, int k,
                    const __grid_constant__ EpiParams epi, const __grid_constant__ EpiMaps maps,
                    const __grid_constant__ SkParams sk) {
-  static_assert(OCC == 1 || (!FUSE && (OCC >= 3 || BN <= 128)), "two CTAs per SM: no fusion, <= 256 TMEM columns");
+  static_assert(OCC == 1 || OCC == 5 || (!FUSE && (OCC >= 3 || BN <= 128)),
+                "two CTAs per SM: no fusion, <= 256 TMEM columns");
   static_assert(OCC < 4 || BN >= 128, "cluster pairs split B tiles in 64-wide halves");
   constexpr bool CL = OCC == 4;   // pair sharing B by multicast, one MMA per CTA
   constexpr bool SM2 = OCC == 5;  // pair running one 256-row MMA (tcgen05 cta_group::2)
@@ -463,6 +464,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       tile_coords(t - p * per_gemm, tiles_m, tiles_n, mb, nb);
     }
   };
+  const int work_items = PAIR ? 2 * ((tiles_m + 1) / 2) * tiles_n * ng : num_tiles;  // fused epilogue loop bound
   // Work items: for_each_work, or — cluster pairs — pair tiles in lockstep.
   auto work = [&](auto&& f) {
     if constexpr (PAIR) {
@@ -842,7 +844,8 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
         static_cast<const __nv_bfloat16*>(epi.ops[0].in[epi.slot_in[1]]);
     auto load = [&](int t_, int c_, uint4(&d)[kMaxEpiSlots][4]) {
       int mb_, nb_;
-      tile_coords(t_, tiles_m, tiles_n, mb_, nb_);
+      int p_;
+      coords(t_, p_, mb_, nb_);
       const int grow = mb_ * BM + q * 32 + lane;
       const int gcol = nb_ * BN + c_ * 32;
       const std::int64_t off = static_cast<std::int64_t>(grow) * n + gcol;
@@ -859,13 +862,16 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
     auto chunk = [&](int t, int mb, int nb, int c, std::uint32_t base, int acc, uint4(&cur)[kMaxEpiSlots][4],
                      uint4(&nxt)[kMaxEpiSlots][4]) {
       if (c + 1 < BN / 32) load(t, c + 1, nxt);
-      else if (t + static_cast<int>(gridDim.x) < num_tiles) load(t + gridDim.x, 0, nxt);
+      else if (t + static_cast<int>(gridDim.x) < work_items) load(t + gridDim.x, 0, nxt);
       std::uint32_t r[32];
       tmem_ld32(base + c * 32, r);
       if (c == BN / 32 - 1) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if constexpr (SM2) mbar_arrive_cluster(cluster_addr(&tempty[acc], 0));  // the leader's MMA waits
+          else mbar_arrive(&tempty[acc]);
+        }
       }
       std::uint32_t cw[16];
 #pragma unroll
@@ -910,11 +916,14 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       ++g;
     };
     uint4 pa[kMaxEpiSlots][4], pb[kMaxEpiSlots][4];
-    if (blockIdx.x < num_tiles) load(blockIdx.x, 0, pa);
+    if (static_cast<int>(blockIdx.x) < work_items) load(blockIdx.x, 0, pa);
     int local = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+    // Work items t = blockIdx.x + i * gridDim.x: plain tiles, or (pairs)
+    // 2 * pair + rank — the same stride, cluster rank = blockIdx.x % 2.
+    for (int t = blockIdx.x; t < work_items; t += gridDim.x, ++local) {
       int mb, nb;
-      tile_coords(t, tiles_m, tiles_n, mb, nb);
+      int p;
+      coords(t, p, mb, nb);
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
@@ -1122,6 +1131,9 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
 template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE>
 void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
   if constexpr (FUSE) {
+    if constexpr (BN >= 128) {
+      if (sc.occ == 5) return launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1, 5>(a, sc, s);
+    }
     launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
   } else if (sc.occ == 4 || sc.occ == 5) {
     if constexpr (BN >= 128) {

@@ -276,3 +276,60 @@ def test_cluster_pair_multicast_variant_vs_fp64(g, m, n, k, ta, tb, monkeypatch)
         a, b = inputs[3 * i], inputs[3 * i + 1]
         ref = (a.T if ta else a) @ (b.T if tb else b)
         assert np.abs(outs[i] - ref).max() / max(1.0, np.abs(ref).max()) < 2.0 ** -8
+
+
+@pytest.mark.parametrize("g,m,n,k,ta,tb", [(1, 4096, 2048, 2048, False, False), (1, 1000, 1024, 1000, True, False),
+                                           (2, 2048, 512, 1536, False, True), (1, 384, 256, 512, True, True)])
+def test_two_sm_variant_vs_fp64(g, m, n, k, ta, tb, monkeypatch):
+    """The 2-SM variant (a CTA pair issuing one 256-row tcgen05.mma with
+    cta_group::2; forced with PLANC_B200_2SM=2; odd M-block counts give a
+    zero half tile whose stores are clipped) against fp64."""
+    from plan_builder import grouped_matmul_plan
+
+    monkeypatch.setenv("PLANC_B200_2SM", "2")
+    monkeypatch.setenv("PLANC_B200_SPLITK", "0")
+    monkeypatch.setenv("PLANC_B200_OCC2", "0")
+    monkeypatch.setenv("PLANC_B200_EPI8", "0")
+    plan = grouped_matmul_plan(g, m, n, k, ta, tb)
+    rng = np.random.default_rng(g + 5 * m + n + k)
+    inputs = {}
+    for i in range(g):
+        inputs[3 * i] = bf16_round(rng.standard_normal((k, m) if ta else (m, k)))
+        inputs[3 * i + 1] = bf16_round(rng.standard_normal((n, k) if tb else (k, n)))
+    with pb.Executor(plan, lane_gpus=[0]) as ex:
+        ex.set_inputs(inputs)
+        ex.run(2)
+        outs = [ex.get_output(3 * i + 2) for i in range(g)]
+    for i in range(g):
+        a, b = inputs[3 * i], inputs[3 * i + 1]
+        ref = (a.T if ta else a) @ (b.T if tb else b)
+        assert np.abs(outs[i] - ref).max() / max(1.0, np.abs(ref).max()) < 2.0 ** -8
+
+
+@pytest.mark.parametrize("two_sm", ["0", "2"])
+@pytest.mark.parametrize("m,n,k,ta,tb", [(4096, 1024, 2048, False, False), (1000, 512, 768, True, False),
+                                         (384, 256, 512, False, True)])
+def test_fused_epilogue_vs_fp64(m, n, k, ta, tb, two_sm, monkeypatch):
+    """C = op(A)·op(B), E = C + D with the add fused into the GEMM's epilogue
+    (default lowering), on the one-CTA and the 2-SM variant: C and E equal
+    the separate kernels' bits (E = bf16(bf16(C) + D))."""
+    from plan_builder import matmul_add_plan
+
+    monkeypatch.setenv("PLANC_B200_2SM", two_sm)
+    monkeypatch.setenv("PLANC_B200_SPLITK", "0")
+    plan, out = matmul_add_plan(m, n, k, ta, tb)
+    rng = np.random.default_rng(m + n + k + int(two_sm))
+    a = bf16_round(rng.standard_normal((k, m) if ta else (m, k)))
+    b = bf16_round(rng.standard_normal((n, k) if tb else (k, n)))
+    d = bf16_round(rng.standard_normal((m, n)))
+    res = {}
+    for flags in (0, pb.NO_FUSION):
+        with pb.Executor(plan, lane_gpus=[0], flags=flags) as ex:
+            ex.set_inputs({0: a, 1: b, 3: d})
+            ex.run(2)
+            res[flags] = (ex.read_buffer(2).reshape(m, n), ex.get_output(out))
+    assert pb.describe(plan)["instrs"][0]["label"] == "op+add"  # one fused launch
+    ref = (a.T if ta else a) @ (b.T if tb else b)
+    assert np.abs(res[0][0] - ref).max() / max(1.0, np.abs(ref).max()) < 2.0 ** -8
+    assert np.array_equal(res[0][0], res[pb.NO_FUSION][0])
+    assert np.array_equal(res[0][1], res[pb.NO_FUSION][1])

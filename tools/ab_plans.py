@@ -23,6 +23,10 @@ VARIANTS = [
 ]
 
 
+if os.environ.get("AB_VARIANTS"):  # [[label, flags, {env}], ...]
+    VARIANTS = [tuple(v) for v in json.loads(os.environ["AB_VARIANTS"])]
+
+
 def run_variant(plan, inp, flags, env, steps=20):
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
