@@ -34,9 +34,11 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #pragma once
 
+#include "gelu.cuh"
 #include "kernels.cuh"
 #include "launch.cuh"
 
@@ -398,8 +400,19 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nb = r / gm;
 }
 
+// Fold step of a fused epilogue op (program.hpp EwOp): add / mul / max; ACT
+// (compile-time, so the plain ops carry no activation code) 4 = GELU's
+// gradient gelu'(a) * b (a = x, b = incoming gradient), 3 = GELU, unary,
+// applied after the fold (epi_finish).
+template <int ACT>
 __device__ __forceinline__ float epi_apply(int op, float a, float b) {
+  if constexpr (ACT == 4) return gelu_grad_f(a, b);
   return op == 0 ? a + b : op == 1 ? a * b : fmaxf(a, b);
+}
+template <int ACT>
+__device__ __forceinline__ float epi_finish(float a) {
+  if constexpr (ACT == 3) return gelu_f(a);
+  return a;
 }
 
 __device__ __forceinline__ std::uint32_t bf16_pair(float lo, float hi) {
@@ -879,29 +892,40 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // ring entry g&1 is free
       __syncwarp();
       std::uint8_t* buf = stg + (g & 1) * 4096;
+      // Fold + store, specialised on the activation so the plain ops'
+      // loop carries no GELU code (a runtime select would evaluate both).
+      auto fold_store = [&](auto act) {
+        constexpr int ACT = decltype(act)::value;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        *reinterpret_cast<uint4*>(buf + lane * 64 + ((v ^ swz) << 4)) =
-            make_uint4(cw[4 * v], cw[4 * v + 1], cw[4 * v + 2], cw[4 * v + 3]);
-        float accv[8];
+        for (int v = 0; v < 4; ++v) {
+          *reinterpret_cast<uint4*>(buf + lane * 64 + ((v ^ swz) << 4)) =
+              make_uint4(cw[4 * v], cw[4 * v + 1], cw[4 * v + 2], cw[4 * v + 3]);
+          float accv[8];
 #pragma unroll
-        for (int i = 0; i < kMaxEpiIn; ++i) {
-          if (i >= epi.ops[0].n_in) break;
-          const uint4 w = i == epi.ops[0].gemm_pos ? make_uint4(cw[4 * v], cw[4 * v + 1], cw[4 * v + 2], cw[4 * v + 3])
-                          : (nst > 1 && epi.slot_in[1] == i) ? cur[1][v]
-                                                             : cur[0][v];
-          float x[8];
-          bf16_unpair(w.x, x[0], x[1]);
-          bf16_unpair(w.y, x[2], x[3]);
-          bf16_unpair(w.z, x[4], x[5]);
-          bf16_unpair(w.w, x[6], x[7]);
+          for (int i = 0; i < kMaxEpiIn; ++i) {
+            if (i >= epi.ops[0].n_in) break;
+            const uint4 w = i == epi.ops[0].gemm_pos ? make_uint4(cw[4 * v], cw[4 * v + 1], cw[4 * v + 2], cw[4 * v + 3])
+                            : (nst > 1 && epi.slot_in[1] == i) ? cur[1][v]
+                                                               : cur[0][v];
+            float x[8];
+            bf16_unpair(w.x, x[0], x[1]);
+            bf16_unpair(w.y, x[2], x[3]);
+            bf16_unpair(w.z, x[4], x[5]);
+            bf16_unpair(w.w, x[6], x[7]);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) accv[e] = i == 0 ? x[e] : epi_apply(epi.ops[0].op, accv[e], x[e]);
+            for (int e = 0; e < 8; ++e) accv[e] = i == 0 ? x[e] : epi_apply<ACT>(epi.ops[0].op, accv[e], x[e]);
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) accv[e] = epi_finish<ACT>(accv[e]);
+          *reinterpret_cast<uint4*>(buf + 2048 + lane * 64 + ((v ^ swz) << 4)) =
+              make_uint4(bf16_pair(accv[0], accv[1]), bf16_pair(accv[2], accv[3]), bf16_pair(accv[4], accv[5]),
+                         bf16_pair(accv[6], accv[7]));
         }
-        *reinterpret_cast<uint4*>(buf + 2048 + lane * 64 + ((v ^ swz) << 4)) =
-            make_uint4(bf16_pair(accv[0], accv[1]), bf16_pair(accv[2], accv[3]), bf16_pair(accv[4], accv[5]),
-                       bf16_pair(accv[6], accv[7]));
-      }
+      };
+      const int eop = epi.ops[0].op;
+      if (eop == 3) fold_store(std::integral_constant<int, 3>{});
+      else if (eop == 4) fold_store(std::integral_constant<int, 4>{});
+      else fold_store(std::integral_constant<int, 0>{});
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) {

@@ -57,7 +57,7 @@ struct DevChunk {
 constexpr int kMaxEpiOps = 1;
 constexpr int kMaxEpiIn = 4;
 struct EpiOp {
-  int op = 0;  // 0 add, 1 mul, 2 max
+  int op = 0;  // 0 add, 1 mul, 2 max, 3 gelu (unary), 4 gelu-grad (x, dy)
   int n_in = 0;
   int gemm_pos = 0;
   const void* in[kMaxEpiIn] = {};

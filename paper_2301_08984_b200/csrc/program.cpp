@@ -1,6 +1,7 @@
 #include "program.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <set>
 #include <sstream>
@@ -881,8 +882,17 @@ void group_gemms(Program& P, const ProgramOptions& opt) {
 
 void fuse_gemm_epilogues(Program& P, const ProgramOptions& opt) {
   std::vector<int> redirect(P.instrs.size(), -1);  // fused ew -> its GEMM
+  const char* act_env = std::getenv("PLANC_B200_FUSE_ACT");
+  const bool act_fusion = act_env && std::atoi(act_env) == 1;
   for (auto& e : P.instrs) {
-    if (e.kind != InstrKind::ew || e.in_bufs.size() > 4 || e.out_bufs.size() != 1) continue;
+    // Elementwise ops, and GELU / GELU-grad (row-wise instructions with no
+    // row structure) — the epilogue applies them to the bf16-rounded C.
+    // Opt-in (PLANC_B200_FUSE_ACT=1): correct and bit-identical, but on C2x
+    // the GELU epilogue outweighs the saved pass (1.833 -> 1.954 ms,
+    // profiles/r01/ab_fuse_gelu.jsonl).
+    const bool act = act_fusion && e.kind == InstrKind::rowwise &&
+                     (e.row_op == RowOp::gelu || e.row_op == RowOp::gelu_grad);
+    if ((e.kind != InstrKind::ew && !act) || e.in_bufs.size() > 4 || e.out_bufs.size() != 1) continue;
     if (P.buffers[e.out_bufs[0]].dtype != DType::bf16) continue;
     // The latest-issued GEMM among the operands' producers, same lane, bf16.
     int g = -1, pos = -1;
@@ -935,7 +945,7 @@ void fuse_gemm_epilogues(Program& P, const ProgramOptions& opt) {
     if (!ready) continue;
     Instr::FusedEw f;
     f.ew_instr = e.id;
-    f.op = e.ew;
+    f.op = !act ? e.ew : e.row_op == RowOp::gelu ? EwOp::gelu : EwOp::gelu_grad;
     f.in_bufs = e.in_bufs;
     f.gemm_pos = pos;
     f.out_buf = e.out_bufs[0];

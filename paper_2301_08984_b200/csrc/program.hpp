@@ -93,7 +93,9 @@ struct Xfer {
 };
 const char* instr_kind_name(InstrKind k);
 
-enum class EwOp { add = 0, mul = 1, max = 2 };
+// gelu / gelu_grad occur only as fused GEMM epilogue ops (Instr::FusedEw),
+// taken over from RowOp::gelu / gelu_grad instructions.
+enum class EwOp { add = 0, mul = 1, max = 2, gelu = 3, gelu_grad = 4 };
 
 struct Instr {
   int id = 0;

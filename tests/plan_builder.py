@@ -81,3 +81,20 @@ def grouped_matmul_plan(g, m, n, k, ta=False, tb=False, out_elem=2):
         doc["assignment"][f"op{i}"] = 0
         doc["lanes"][0]["tasks"].append({"kind": "compute", "op": f"op{i}", "duration": 0.0, "bytes": 0})
     return json.dumps(doc)
+
+
+def matmul_gelu_plan(m, n, k, ta=False, tb=False):
+    """C = op(A)·op(B); G = gelu(C) (bf16; schema-extension kind): a GEMM
+    whose activation runs in its epilogue."""
+    doc = json.loads(matmul_plan(m, n, k, ta, tb)[0])
+    doc["ptensors"].append({"id": 3, "shape": [m, n], "elem_size": 2, "kind": "activation"})
+    full = [[0, m], [0, n]]
+    doc["vtensors"] += [
+        {"id": 201, "ptensor": 2, "region": full, "value": [0, 1], "replica": [0, 1], "side": "in", "owner": "act"},
+        {"id": 203, "ptensor": 3, "region": full, "value": [0, 1], "replica": [0, 1], "side": "out", "owner": "act"}]
+    doc["ops"].append({"id": "act", "kind": "gelu", "inputs": [201], "outputs": [203], "direction": "forward",
+                       "flops": 0.0, "doc_order": 1, "inserted": False})
+    doc["assignment"]["act"] = 0
+    doc["feeds"].append([201, 200])
+    doc["lanes"][0]["tasks"].append({"kind": "compute", "op": "act", "duration": 0.0, "bytes": 0})
+    return json.dumps(doc), 3

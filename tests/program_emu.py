@@ -42,6 +42,12 @@ def exec_instr(ins: dict, data: dict, shape: dict):
             else:
                 data[ins["out"][g]] = c.reshape(-1)
         for f in ins.get("fused", []):  # elementwise consumers run in the GEMM epilogue
+            if f["ew"] >= 3:  # GELU (3) / GELU-grad (4, operands x, dy)
+                from oracle import planc_oracle as po
+
+                xs = [data[x].reshape(-1, 1) for x in f["in"]]
+                data[f["out"]] = po.eval_ext(("gelu", "gelu-grad")[f["ew"] - 3], xs, 1, 0.0).reshape(-1)
+                continue
             out = data[f["in"][0]].copy()
             for x in f["in"][1:]:
                 out = (out + data[x], out * data[x], np.maximum(out, data[x]))[f["ew"]]

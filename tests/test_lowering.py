@@ -328,3 +328,17 @@ def test_gemm_schedule_covers_every_k_block_once(m, n, k, ta, sk_mode, monkeypat
         assert owners == list(range(owners[0], owners[-1] + 1))
     if sk_mode == "2" and tiles % sms:
         assert sc["sk_ctas"] > 0 or (tiles - sc["dp_tiles"]) * num_k < 8
+
+
+def test_opt_in_gelu_epilogue_fusion(monkeypatch):
+    """PLANC_B200_FUSE_ACT=1 moves GELU into its GEMM's epilogue (fused op
+    ew 3); the lowered program still computes the same values."""
+    g = golden_cases.load("ext_block_fwd_tp2_mma")
+    plan = json.loads(g["plan"])
+    base = run_program(pb.describe(g["plan"]), plan, g["inputs"])
+    monkeypatch.setenv("PLANC_B200_FUSE_ACT", "1")
+    desc = pb.describe(g["plan"])
+    assert any(f["ew"] == 3 for i in desc["instrs"] for f in i["fused"])
+    out = run_program(desc, plan, g["inputs"])
+    ok, msg = pb.compare_outputs(base, out, 0.0, normwise=True)
+    assert ok, msg
