@@ -47,6 +47,8 @@ extern "C" {
 #define PLANC_B200_FUSE_EPILOGUES 0x10u /* (default, kept for compatibility) an elementwise op consuming a
                                            fresh bf16 GEMM output on the same lane runs in that GEMM's
                                            epilogue — same bits as the separate kernel */
+#define PLANC_B200_FUSE_ACT 0x400u      /* also run GELU / GELU-grad in the producing GEMM's epilogue
+                                           (opt-in: same bits, measured slower on C2x) */
 #define PLANC_B200_NO_FUSION 0x80u      /* every elementwise op its own kernel (no epilogue fusion) */
 #define PLANC_B200_NO_SCATTER 0x200u    /* all-reduce partials stored whole by their GEMM and pulled by the
                                            reduce-scatter phase (default: a GEMM whose output only feeds an

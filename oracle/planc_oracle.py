@@ -74,18 +74,26 @@ def _sl(region, origin):
 
 
 def reconstruct(target, pieces, ctx="", vv=False):
-    """refexec.cpp:102-140. target/pieces masks are dicts with region, vi, vc."""
+    """refexec.cpp:102-140. target/pieces masks are dicts with region, vi, vc.
+
+    With ``vv``, value sub-parts (vc = m * target vc) are summed only into
+    elements no exact-match piece covers: where the reference's own copy
+    rule (refexec.cpp:110-112) applies, its result stands and the sub-parts
+    are skipped as in refexec.cpp:115-117, whatever the piece order."""
     treg = target["region"]
     out = np.zeros([hi - lo for lo, hi in treg], dtype=np.float64)
+    sub = np.zeros_like(out) if vv else None
+    copied = np.zeros(out.shape, dtype=bool) if vv else None
     touched = 0
     for mask, value in pieces:
+        part = False
         if mask["vc"] == target["vc"] and mask["vi"] == target["vi"]:
             copy = True
         elif target["vc"] == 1 and mask["vc"] > 1:
             copy = False
         elif (vv and mask["vc"] > target["vc"] and mask["vc"] % target["vc"] == 0
               and mask["vi"] // (mask["vc"] // target["vc"]) == target["vi"]):
-            copy = False
+            copy, part = False, True
         else:
             continue
         ov = _region_intersect(mask["region"], treg)
@@ -93,13 +101,19 @@ def reconstruct(target, pieces, ctx="", vv=False):
             continue
         dst = _sl(ov, treg)
         src = value[_sl(ov, mask["region"])]
-        if copy:
+        if part:
+            sub[dst] += src
+        elif copy:
             out[dst] = src
+            if vv:
+                copied[dst] = True
         else:
             out[dst] += src
         touched += _vol(ov)
     if touched < _vol(treg):
         raise InternalError(f"reconstruct: region {treg} not fully covered ({ctx})")
+    if vv:
+        out = np.where(copied, out, out + sub)
     return out
 
 
@@ -271,20 +285,44 @@ class Plan:
         self.graph_inputs = {p for p in self.ptensors if p not in produced}
 
 
-def run_plan(plan, inputs, vv=False, return_vtensors=False):
-    """refexec.cpp:361-557 restated. ``plan`` is a Plan or plan.json text."""
+class InexactBf16(RuntimeError):
+    """round_bf16 emulation left the range where fp32 accumulation is exact."""
+
+
+def run_plan(plan, inputs, vv=False, return_vtensors=False, round_bf16=False):
+    """refexec.cpp:361-557 restated. ``plan`` is a Plan or plan.json text.
+
+    ``round_bf16``: every vTensor of a 2-byte pTensor is rounded to bfloat16
+    where the B200 executor stores it (op outputs, every reconstruct / adapter
+    output, graph-input placement); the final reassembly of produced pTensors
+    stays in float64 (the executor reassembles on the host in double,
+    refexec.cpp:532-556). On integer inputs every stored bf16 value is an
+    integer, so when every matmul's |A|·|B| stays below 2^24 each fp32
+    accumulation on the GPU is exact in ANY summation order and the
+    executor's bf16 results must equal this emulation bit for bit; the run
+    raises ``InexactBf16`` otherwise (the golden generator then rejects the
+    case)."""
     if not isinstance(plan, Plan):
         plan = Plan(plan)
     g = plan
     vt_values = {}
     channel_values = {}
+    half = {p for p, d in g.ptensors.items() if d["elem_size"] == 2} if round_bf16 else set()
+
+    def store(v, val):
+        if g.vtensors[v]["pt"] in half:
+            if val.size and (np.abs(val).max() >= 2.0 ** 24 or not np.all(val == np.round(val))):
+                raise InexactBf16(f"vtensor {v}: value outside the exact fp32 integer range")
+            val = bf16_round(val)
+        vt_values[v] = val
 
     def input_value(vt):
         if vt["pt"] not in inputs:
             raise UsageError(f"run_plan: missing input tensor {vt['pt']}")
         if vt["vc"] != 1:
             raise UsageError("run_plan: graph input consumed as partial value")
-        return np.asarray(inputs[vt["pt"]], dtype=np.float64)[_sl(vt["region"], [(0, 0)] * len(vt["region"]))].copy()
+        val = np.asarray(inputs[vt["pt"]], dtype=np.float64)[_sl(vt["region"], [(0, 0)] * len(vt["region"]))].copy()
+        return bf16_round(val) if vt["pt"] in half else val
 
     def feed_ready(cvt):
         vt = g.vtensors[cvt]
@@ -321,17 +359,23 @@ def run_plan(plan, inputs, vv=False, return_vtensors=False):
             channel_values[op["channel"]] = feed_value(op["inputs"][0])
             return
         if k == "recv":
-            vt_values[op["outputs"][0]] = channel_values[op["channel"]]
+            store(op["outputs"][0], channel_values[op["channel"]])
             return
         if k in ("split", "concat", "reduce-assemble"):
             pieces = [(mask(v), feed_value(v)) for v in op["inputs"]]
             for out in op["outputs"]:
-                vt_values[out] = reconstruct(mask(out), pieces, "op " + op["id"], vv)
+                store(out, reconstruct(mask(out), pieces, "op " + op["id"], vv))
             return
         ins = [feed_value(v) for v in op["inputs"]]
+        if round_bf16 and k == "matmul":
+            a = ins[0].T if op.get("transpose_a") else ins[0]
+            b = ins[1].T if op.get("transpose_b") else ins[1]
+            bound = float((np.abs(a) @ np.abs(b)).max()) if a.size and b.size else 0.0
+            if bound >= 2.0 ** 24 or not (np.all(a == np.round(a)) and np.all(b == np.round(b))):
+                raise InexactBf16(f"matmul {op['id']}: |A|.|B| reaches {bound} (fp32 sums not exact)")
         outs = eval_compute(op, ins, [mask(v) for v in op["inputs"]], [mask(v) for v in op["outputs"]])
         for v, val in zip(op["outputs"], outs):
-            vt_values[v] = val
+            store(v, val)
 
     def exec_collective(grp):
         pieces = []
@@ -340,7 +384,7 @@ def run_plan(plan, inputs, vv=False, return_vtensors=False):
                 pieces.append((mask(v), feed_value(v)))
         for oid in grp["ops"]:
             for out in g.op[oid]["outputs"]:
-                vt_values[out] = reconstruct(mask(out), pieces, "collective " + oid, vv)
+                store(out, reconstruct(mask(out), pieces, "collective " + oid, vv))
 
     progress = True
     while progress:

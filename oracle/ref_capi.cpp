@@ -168,7 +168,9 @@ StrategyInfo megatron_tp(PlanGraph& g, const ClusterSpec& env,
 // (test_refexec.cpp:100-140, test_commplan.cpp:303-366): target_ops lists
 // "op@algo[@offset[@count]]" with algo v (value split), sD (split output dim
 // D), r (replica) or e (vocabulary-sharded embedding), fanned out `count`
-// ways (default: devices); replacement i goes to device offset + i.
+// ways (default: devices); replacement i goes to device offset + i. An algo
+// "sD:n/sE:m" splits a forward op on dim D n ways, then each part on dim E m
+// ways (a 2-D tiling, e.g. the D(2,2) consumer of SURVEY fact 6).
 // Paired backward ops follow through adapt_backward. Unlisted ops stay whole
 // on device 0.
 StrategyInfo manual(PlanGraph& g, const ClusterSpec& env,
@@ -198,6 +200,27 @@ StrategyInfo manual(PlanGraph& g, const ClusterSpec& env,
     if (it == algo_of.end()) continue;
     const std::string& a = it->second.algo;
     int cnt = it->second.count, off = it->second.offset;
+    if (a.find('/') != std::string::npos) {
+      // Nested splits "sD:n/sE:m" (forward ops without a backward pair):
+      // op_trans by the first algo, then every replacement by the next;
+      // replacement i (row-major over the levels) goes to device off + i.
+      std::vector<std::string> ids{oid};
+      std::stringstream ls(a);
+      std::string lvl;
+      while (std::getline(ls, lvl, '/')) {
+        auto c = lvl.find(':');
+        if (lvl.empty() || lvl[0] != 's' || c == std::string::npos) throw UsageError("manual: bad level " + lvl);
+        TransformAlgo la = split_algo(std::stoi(lvl.substr(1, c - 1)), std::stoi(lvl.substr(c + 1)));
+        std::vector<std::string> next;
+        for (const auto& id : ids) {
+          auto r = op_trans(g, id, la);
+          next.insert(next.end(), r.begin(), r.end());
+        }
+        ids = next;
+      }
+      for (std::size_t i = 0; i < ids.size(); ++i) op_assign(g, env, ids[i], off + static_cast<int>(i));
+      continue;
+    }
     TransformAlgo algo = replica_algo(cnt);
     if (a == "v") algo = value_split_algo(cnt);
     else if (a == "e") algo = shard_embed_algo(cnt);

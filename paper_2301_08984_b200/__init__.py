@@ -42,6 +42,7 @@ NO_GROUPING = 0x40
 NO_FUSION = 0x80
 NO_ALIAS = 0x100
 NO_SCATTER = 0x200
+FUSE_ACT = 0x400
 
 
 class PlancError(RuntimeError):

@@ -52,6 +52,33 @@ char* dup(const std::string& s) {
 
 }  // namespace
 
+// One translation of the open flags, shared by every entry point, so that
+// every rank of a multi-process run lowers the same program from the same
+// flags (no lowering switch is read from the environment).
+ExecOptions exec_options(uint32_t flags) {
+  ExecOptions opt;
+  opt.use_graph = (flags & PLANC_B200_NO_GRAPH) == 0;
+  opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
+  opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
+  if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
+  opt.fuse_epilogues = (flags & PLANC_B200_NO_FUSION) == 0;
+  opt.fuse_act = (flags & PLANC_B200_FUSE_ACT) != 0;
+  opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
+  opt.alias_copies = (flags & PLANC_B200_NO_ALIAS) == 0;
+  opt.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0;
+  return opt;
+}
+
+ProgramOptions describe_options(uint32_t flags) {
+  const bool tc = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
+  ProgramOptions po = program_options((flags & PLANC_B200_STRICT_VALUE) == 0,
+                                      (flags & PLANC_B200_NO_FUSION) == 0 && tc);
+  po.fuse_act = (flags & PLANC_B200_FUSE_ACT) != 0;
+  po.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0 && tc;
+  po.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0 && tc;
+  return po;
+}
+
 extern "C" {
 
 const char* planc_b200_last_error(void) { return g_last_error.c_str(); }
@@ -64,15 +91,7 @@ int planc_b200_open(const char* plan_json, const int* lane_gpu, int num_lane_gpu
                     planc_b200_exec** out) {
   return guarded([&] {
     if (!plan_json || !out) throw UsageError("planc_b200_open: null argument");
-    ExecOptions opt;
-    opt.use_graph = (flags & PLANC_B200_NO_GRAPH) == 0;
-    opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
-    opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
-    if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
-    opt.fuse_epilogues = (flags & PLANC_B200_NO_FUSION) == 0;
-    opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
-    opt.alias_copies = (flags & PLANC_B200_NO_ALIAS) == 0;
-    opt.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0;
+    const ExecOptions opt = exec_options(flags);
     std::vector<int> lanes;
     for (int i = 0; lane_gpu && i < num_lane_gpu; ++i) lanes.push_back(lane_gpu[i]);
     auto* h = new planc_b200_exec;
@@ -101,15 +120,7 @@ int planc_b200_open_rank(const char* plan_json, int rank, int world, const int* 
     const bool peer = (flags & PLANC_B200_PEER_MEMORY) != 0;
     if (!plan_json || !out || !lane_rank || (!nccl_id && !peer)) throw UsageError("planc_b200_open_rank: null argument");
     if (num_lanes < 1) throw UsageError("planc_b200_open_rank: the plan's lanes need owners");
-    ExecOptions opt;
-    opt.use_graph = (flags & PLANC_B200_NO_GRAPH) == 0;
-    opt.allow_tensor_cores = (flags & PLANC_B200_NO_TENSOR_CORES) == 0;
-    opt.value_split_extension = (flags & PLANC_B200_STRICT_VALUE) == 0;
-    if (flags & PLANC_B200_SERIAL_LANES) opt.streams_per_lane = 1;
-    opt.fuse_epilogues = (flags & PLANC_B200_NO_FUSION) == 0;
-    opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
-    opt.alias_copies = (flags & PLANC_B200_NO_ALIAS) == 0;
-    opt.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0;
+    const ExecOptions opt = exec_options(flags);
     RankConfig rc;
     rc.rank = rank;
     rc.world = world;
@@ -132,11 +143,7 @@ int planc_b200_describe_rank(const char* plan_json, const int* lane_rank, int nu
                              char** json_out) {
   return guarded([&] {
     if (!plan_json || !json_out || !lane_rank) throw UsageError("null argument");
-    ProgramOptions po = program_options((flags & PLANC_B200_STRICT_VALUE) == 0,
-                                        (flags & PLANC_B200_NO_FUSION) == 0 &&
-                                            (flags & PLANC_B200_NO_TENSOR_CORES) == 0);
-    po.group_gemms = (flags & (PLANC_B200_NO_GROUPING | PLANC_B200_NO_TENSOR_CORES)) == 0;
-    po.scatter_allreduce = (flags & (PLANC_B200_NO_SCATTER | PLANC_B200_NO_TENSOR_CORES)) == 0;
+    ProgramOptions po = describe_options(flags);
     ExecutionPlan plan = load_plan(plan_json);
     const std::vector<int> lr(lane_rank, lane_rank + num_lanes);
     if ((flags & PLANC_B200_PEER_MEMORY) == 0) {
@@ -373,11 +380,7 @@ int planc_b200_timeline(planc_b200_exec* h, char** json_out) {
 int planc_b200_describe(const char* plan_json, uint32_t flags, char** json_out) {
   return guarded([&] {
     if (!plan_json || !json_out) throw UsageError("null argument");
-    ProgramOptions po = program_options((flags & PLANC_B200_STRICT_VALUE) == 0,
-                                        (flags & PLANC_B200_NO_FUSION) == 0 &&
-                                            (flags & PLANC_B200_NO_TENSOR_CORES) == 0);
-    po.group_gemms = (flags & (PLANC_B200_NO_GROUPING | PLANC_B200_NO_TENSOR_CORES)) == 0;
-    po.scatter_allreduce = (flags & (PLANC_B200_NO_SCATTER | PLANC_B200_NO_TENSOR_CORES)) == 0;
+    ProgramOptions po = describe_options(flags);
     ExecutionPlan plan = load_plan(plan_json);
     Program p = build_program(plan, po);
     *json_out = dup(p.describe_json());

@@ -106,7 +106,8 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   const int forced = env ? std::atoi(env) : 0;
   const char* skenv = std::getenv("PLANC_B200_STREAMK");
   const int skmode = skenv ? std::atoi(skenv) : 1;
-  const bool allow_sk = skmode != 0 && a.epi.n_ops == 0 && a.scatter == 0 && (a.allow_streamk || skmode == 2);
+  const bool allow_sk =
+      skmode != 0 && !a.no_workspace && a.epi.n_ops == 0 && a.scatter == 0 && (a.allow_streamk || skmode == 2);
   // PLANC_B200_SPLITK=0 disables split-K, =2 takes it whenever it applies.
   const char* spenv = std::getenv("PLANC_B200_SPLITK");
   const int splitmode = spenv ? std::atoi(spenv) : 1;
@@ -114,7 +115,7 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   // when the lane has it to itself, over at most a quarter of the SMs when
   // co-resident lanes share it (their concurrent work keeps the rest; C5's
   // 256 x 256 x 8192 weight gradients: 4 CTAs for ~40 us -> 36 CTAs).
-  const bool allow_split = splitmode != 0 && a.epi.n_ops == 0 && a.scatter == 0;
+  const bool allow_split = splitmode != 0 && !a.no_workspace && a.epi.n_ops == 0 && a.scatter == 0;
   const int split_sms = (a.allow_streamk || splitmode == 2) ? sms : std::max(1, sms / 4);
   GemmSchedule best;
   bool have = false;
@@ -217,8 +218,11 @@ void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
   const bool a_mn = a.ta, b_mn = !a.tb, cb = a.dc == DT_BF16;
   GemmSchedule sc = gemm_sm100_schedule(a, device_sms());
   if ((sc.sk_ctas > 0 || sc.splits > 1) && (a.ws == nullptr || a.ws_bytes < sc.ws_bytes)) {
-    sc = schedule_for(a.m, a.n, a.k, sc.bn, false, device_sms(), false, a.group,
-                      a.epi.n_ops == 0);  // no workspace: data-parallel
+    // No (or too small a) workspace: the same selection among the
+    // data-parallel variants (2-SM, eight epilogue warps, two CTAs per SM).
+    GemmArgs b = a;
+    b.no_workspace = true;
+    sc = gemm_sm100_schedule(b, device_sms());
   }
   if (a.epi.n_ops > 0) {
     if (!cb) throw std::runtime_error("fused GEMM epilogue needs a bf16 output");

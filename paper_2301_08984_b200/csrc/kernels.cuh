@@ -107,6 +107,9 @@ struct GemmArgs {
   // path: worth it when the GPU has nothing else to run (one lane per GPU),
   // not when co-resident lanes fill the idle SMs with their own work.
   bool allow_streamk = true;
+  // No workspace at all: the schedule is chosen among data-parallel
+  // variants only (no stream-K, no split-K).
+  bool no_workspace = false;
 };
 
 // Launch schedule of the tcgen05 GEMM: tile width, persistent grid, and the

@@ -99,12 +99,13 @@ std::vector<Cell> reconstruct_cells(const Mask& target, const std::vector<std::i
     const Mask* mask;
     int buffer;
     bool add;
+    bool part;  // V(m*v) -> V(v) sub-part (extension)
     Region ov;
   };
   std::vector<Used> used;
   std::int64_t touched = 0;
   for (const auto& [m, buf] : pieces) {
-    bool add;
+    bool add, part = false;
     if (m->value_count == target.value_count && m->value_index == target.value_index) {
       add = false;  // refexec.cpp:110-112 copy
     } else if (target.value_count == 1 && m->value_count > 1) {
@@ -112,14 +113,14 @@ std::vector<Cell> reconstruct_cells(const Mask& target, const std::vector<std::i
     } else if (vv_extension && m->value_count > target.value_count &&
                m->value_count % target.value_count == 0 &&
                m->value_index / (m->value_count / target.value_count) == target.value_index) {
-      add = true;  // V(m*v) -> V(v): sub-parts of the target's value part
+      add = part = true;  // V(m*v) -> V(v): sub-parts of the target's value part
     } else {
       continue;  // refexec.cpp:115-117
     }
     Region ov;
     if (!region_intersect(m->region, treg, &ov)) continue;
     touched += region_volume(ov);
-    used.push_back({m, buf, add, ov});
+    used.push_back({m, buf, add, part, ov});
   }
   if (touched < region_volume(treg)) {
     throw InternalError("reconstruct: region " + region_to_string(treg) + " not fully covered (" + ctx + ")");
@@ -149,10 +150,19 @@ std::vector<Cell> reconstruct_cells(const Mask& target, const std::vector<std::i
       c.dst_strides[d] = tstr[d];
       c.dst_offset += (box[d].lo - treg[d].lo) * tstr[d];
     }
+    // Sub-parts only fill cells no exact-match piece covers: where the
+    // reference's copy rule applies its result stands and the sub-parts are
+    // skipped (refexec.cpp:115-117), whatever the piece order.
+    bool has_copy = false;
     for (const auto& u : used) {
       bool inside = true;
       for (int d = 0; d < rank; ++d) inside = inside && u.ov[d].lo <= box[d].lo && box[d].hi <= u.ov[d].hi;
-      if (!inside) continue;
+      has_copy = has_copy || (inside && !u.add);
+    }
+    for (const auto& u : used) {
+      bool inside = true;
+      for (int d = 0; d < rank; ++d) inside = inside && u.ov[d].lo <= box[d].lo && box[d].hi <= u.ov[d].hi;
+      if (!inside || (u.part && has_copy)) continue;
       const BufferDesc& src = buffers[u.buffer];
       auto sstr = row_major_strides(src.shape);
       Term t;
@@ -819,7 +829,9 @@ void group_gemms(Program& P, const ProgramOptions& opt) {
   for (std::size_t i = 0; i < P.issue_order.size(); ++i) pos[P.issue_order[i]] = static_cast<int>(i);
   for (int id : P.issue_order) {
     Instr& g = P.instrs[id];
-    if (g.kind != InstrKind::gemm || !g.fused.empty() || g.group != 1) continue;
+    // Reduce-scatter GEMMs (scatter > 0) carry k receive slices as their
+    // outputs: a grouped launch holds one output per member, so they never join.
+    if (g.kind != InstrKind::gemm || !g.fused.empty() || g.group != 1 || g.scatter > 0) continue;
     const DType da = P.buffers[g.in_bufs[0]].dtype, db = P.buffers[g.in_bufs[1]].dtype,
                 dc = P.buffers[g.out_bufs[0]].dtype;
     if (!opt.gemm_groupable(g, da, db, dc)) continue;
@@ -882,18 +894,21 @@ void group_gemms(Program& P, const ProgramOptions& opt) {
 
 void fuse_gemm_epilogues(Program& P, const ProgramOptions& opt) {
   std::vector<int> redirect(P.instrs.size(), -1);  // fused ew -> its GEMM
-  const char* act_env = std::getenv("PLANC_B200_FUSE_ACT");
-  const bool act_fusion = act_env && std::atoi(act_env) == 1;
+  const bool act_fusion = opt.fuse_act;
   for (auto& e : P.instrs) {
     // Elementwise ops, and GELU / GELU-grad (row-wise instructions with no
     // row structure) — the epilogue applies them to the bf16-rounded C.
-    // Opt-in (PLANC_B200_FUSE_ACT=1): correct and bit-identical, but on C2x
+    // Opt-in (ProgramOptions::fuse_act, flag PLANC_B200_FUSE_ACT): correct and bit-identical, but on C2x
     // the GELU epilogue outweighs the saved pass (1.833 -> 1.954 ms,
     // profiles/r01/ab_fuse_gelu.jsonl).
     const bool act = act_fusion && e.kind == InstrKind::rowwise &&
                      (e.row_op == RowOp::gelu || e.row_op == RowOp::gelu_grad);
     if ((e.kind != InstrKind::ew && !act) || e.in_bufs.size() > 4 || e.out_bufs.size() != 1) continue;
     if (P.buffers[e.out_bufs[0]].dtype != DType::bf16) continue;
+    // The fused epilogue reads every operand as bf16.
+    bool all_bf16 = true;
+    for (int b : e.in_bufs) all_bf16 = all_bf16 && P.buffers[b].dtype == DType::bf16;
+    if (!all_bf16) continue;
     // The latest-issued GEMM among the operands' producers, same lane, bf16.
     int g = -1, pos = -1;
     for (std::size_t i = 0; i < e.in_bufs.size(); ++i) {
@@ -1521,6 +1536,8 @@ std::string Program::describe_json() const {
     for (std::size_t j = 0; j < outputs[i].second.size(); ++j) os << (j ? "," : "") << outputs[i].second[j];
     os << "]]";
   }
+  os << "],\"vt_buffer\":[";
+  for (std::size_t i = 0; i < vt_buffer.size(); ++i) os << (i ? "," : "") << vt_buffer[i];
   os << "],\"lane_arena_bytes\":[";
   for (std::size_t i = 0; i < lane_arena_bytes.size(); ++i) os << (i ? "," : "") << lane_arena_bytes[i];
   os << "],\"total_flops\":" << total_flops << ",\"total_bytes\":" << total_bytes

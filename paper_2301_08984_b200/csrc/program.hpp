@@ -161,6 +161,9 @@ struct ProgramOptions {
   // into that GEMM's epilogue (local form), for GEMMs the
   // predicate accepts (the tensor-core path implements the fused epilogue).
   bool fuse_epilogues = false;
+  // ...GELU / GELU-grad too (opt-in: bit-identical, but measured slower than
+  // the separate pass on C2x, profiles/r01/ab_fuse_gelu.jsonl).
+  bool fuse_act = false;
   // All-reduce groups (every member output = the sum of the same k whole
   // member inputs) as two box phases: member j sums slice j of all inputs
   // (reduce-scatter), then copies the other members' reduced slices

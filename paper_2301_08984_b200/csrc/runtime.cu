@@ -131,6 +131,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   plan_ = load_plan(plan_json);
   ProgramOptions po = program_options(opt.value_split_extension, opt.fuse_epilogues && opt.allow_tensor_cores);
   po.group_gemms = opt.group_gemms && opt.allow_tensor_cores;
+  po.fuse_act = opt.fuse_act;
   if (const char* e = std::getenv("PLANC_B200_SYNC_EDGES")) po.honor_sync_edges = e[0] != '0';  // A/B only
   // NCCL exchange steps lower whole-buffer all-reduce groups to
   // ncclAllReduce; every other mode runs them as two box phases.

@@ -49,6 +49,7 @@ struct ExecOptions {
   bool value_split_extension = true;
   int streams_per_lane = 4;             // 1 = issue a lane strictly in plan order
   bool fuse_epilogues = true;           // elementwise consumers computed in GEMM epilogues
+  bool fuse_act = false;                // ...GELU / GELU-grad as well (PLANC_B200_FUSE_ACT)
   bool group_gemms = true;              // same-shape independent GEMMs in one grouped launch
   bool alias_copies = true;             // same-GPU whole-buffer copies (recv, identity) become aliases
   bool scatter_allreduce = true;        // all-reduce partials leave the GEMM epilogue as reduce-scatter slices

@@ -8,6 +8,10 @@ Every case is produced by the UNMODIFIED reference (oracle/_ref, built from
               simulate.cpp:492) — the executor's input
   io.npz      in_<pt>: random_integer_inputs(graph, seed) (refexec.cpp:559)
               exp_<pt>: run_reference(graph, inputs)     (refexec.cpp:264)
+              emu_<pt>: bf16 plans only — the plan run by the numpy
+                        restatement with bf16 rounding at every store
+                        (planc_oracle.run_plan(round_bf16=True)), present
+                        when that emulation is exact (meta bf16_exact)
               ref_<pt>: run_plan(plan, inputs)            (refexec.cpp:361),
                         absent when the reference executor throws
   meta.json   seed, tolerance, provenance (reference test file:line)
@@ -26,7 +30,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
-from oracle import docs, refpy  # noqa: E402
+from oracle import docs, planc_oracle, refpy  # noqa: E402
 
 TP_TEST_DOC = json.dumps({
     "ptensors": [
@@ -72,6 +76,23 @@ def chain2(rows, cols, mid, elem=4):
              "flops": 2.0 * rows * cols * mid},
             {"id": "mm2", "kind": "matmul", "inputs": [2, 3], "outputs": [4], "direction": "forward",
              "flops": 2.0 * rows * cols * cols}]})
+
+
+def matmul_max(rows, cols, mid, elem=4):
+    """T = A[rows,mid]·W1[mid,cols]; U = max(T, Z): an elementwise consumer
+    that can be tiled on both dims (the D(2,2) / D(2,4) targets of fact 6)."""
+    return json.dumps({
+        "ptensors": [
+            {"id": 0, "shape": [rows, mid], "elem_size": elem, "kind": "activation"},
+            {"id": 1, "shape": [mid, cols], "elem_size": elem, "kind": "weight"},
+            {"id": 2, "shape": [rows, cols], "elem_size": elem, "kind": "activation"},
+            {"id": 3, "shape": [rows, cols], "elem_size": elem, "kind": "activation"},
+            {"id": 4, "shape": [rows, cols], "elem_size": elem, "kind": "activation"}],
+        "ops": [
+            {"id": "mm1", "kind": "matmul", "inputs": [0, 1], "outputs": [2], "direction": "forward",
+             "flops": 2.0 * rows * cols * mid},
+            {"id": "act", "kind": "max", "inputs": [2, 3], "outputs": [4], "direction": "forward",
+             "flops": rows * cols}]})
 
 
 def cases():
@@ -121,7 +142,16 @@ def cases():
         ("adapt_v_to_d8", chain2(16, 16, 16), dict(strategy="manual", devices=8, target_ops="mm1@v,mm2@s0"), 106,
          0.0, "V->D on 8 devices"),
         ("adapt_vv_gap", chain2(256, 256, 8), dict(strategy="manual", devices=4, target_ops="mm1@v,mm2@s1"), 107,
-         0.0, "large V(4)->D plan: Dijkstra may pick multi-step V->V (SURVEY fact 6)"),
+         0.0, "large V(4)->D(1,4) plan (Dijkstra picks one k=4 all-reduce + local split here)"),
+        # Dijkstra chains k=2 reduce-scatters (V(4)->V(2)->D),
+        # the reference run_plan throws on the V(4)->V(2) step; parity comes
+        # from run_reference on the graph (meta: reference_run_plan "throws").
+        ("adapt_vv_rs2x2", matmul_max(256, 256, 8),
+         dict(strategy="manual", devices=4, target_ops="mm1@v,act@s0:2/s1:2", testutil_cluster=1), 111, 0.0,
+         "SURVEY fact 6 / probe3: V(4)->D(2,2) at 256x256 fp32 = two chained k=2 reduce-scatters"),
+        ("adapt_vv_rs2x4", matmul_max(256, 512, 8),
+         dict(strategy="manual", devices=8, target_ops="mm1@v,act@s0:2/s1:4", testutil_cluster=1), 112, 0.0,
+         "SURVEY fact 6 on 8 devices: V(8)->D(2,4) through partial-value intermediates"),
         ("cross_group_copy", chain2(8, 8, 8),
          dict(strategy="manual", devices=4, target_ops="mm1@s0@0@2,mm2@s0@2@2", testutil_cluster=1,
               group_size=2), 108, 0.0, "disjoint device groups: group-copy (rvd.cpp:328-382)"),
@@ -145,6 +175,16 @@ def cases():
     out.append(("gpt_stack2_1f1b_bf16", docs.dumps(docs.gpt_stack_doc(2, 32, 16, elem_size=2)),
                 dict(strategy="1f1b", devices=4, stages=2, micro_batches=2, inner_dp=2), 72, 2e-2,
                 "C3 shape: stacked GPT blocks, 1F1B pipeline x inner DP (P2P + naive gradient sync), bf16"))
+    # bf16 train steps at tcgen05 shapes (every GEMM, forward and backward,
+    # above the SIMT threshold m*n*k >= 2^20): pinned bit for bit against the
+    # bf16 plan emulation (planc_oracle.run_plan(round_bf16=True)).
+    for k in (1, 2):
+        out.append((f"gpt_block_train_tp{k}_mma", docs.dumps(docs.gpt_block_doc(256, 128, elem_size=2, train=True)),
+                    dict(strategy="megatron_tp", devices=k), 80 + k, 2e-2,
+                    "C2 train step (fwd + bwd + optimizer) at tensor-core shapes, bf16"))
+    out.append(("c2_cpu_tp1", docs.dumps(docs.gpt_block_doc(128, 128, elem_size=2, train=True)),
+                dict(strategy="megatron_tp", devices=1), 1, 2e-2,
+                "plans/c2_tp1_cpu (the bench's reduced-shape C2 plan, T=H=128), bf16 train step"))
     out.append(("gpt_block_fwd_tp2_mma", docs.dumps(docs.gpt_block_doc(256, 128, elem_size=2, train=False)),
                 dict(strategy="megatron_tp", devices=2), 71, 2e-2,
                 "C2 forward at tensor-core-eligible shapes (bf16)"))
@@ -159,7 +199,8 @@ def main():
         plan = refpy.compile_plan(doc, **spec)
         # Small-magnitude inputs keep every fp32 partial sum below 2^24 so
         # fp32 plans are bit-exact against the double-precision oracle.
-        inputs = refpy.random_integer_inputs(doc, seed, 1 if name.startswith("gpt_block") else 4)
+        magnitude = 1 if name.startswith(("gpt_", "c2_")) else 4
+        inputs = refpy.random_integer_inputs(doc, seed, magnitude)
         expected = refpy.run_reference(doc, inputs)
         peak = max(float(np.abs(v).max()) for v in expected.values())
         if tol == 0.0 and peak >= 2.0 ** 24:
@@ -174,6 +215,18 @@ def main():
             arrays.update({f"ref_{k}": v for k, v in ref_out.items()})
         except refpy.RefError as e:
             ref_status = "throws: " + str(e)
+        # bf16 plans: the plan emulated with bf16 rounding wherever the
+        # executor stores a value; exact (any fp32 summation order) when every
+        # stored value is an integer below 2^24 -> the GPU must match it bit
+        # for bit. Cases outside that range keep only the tolerance bar.
+        bf16_exact = False
+        if any(p["elem_size"] == 2 for p in json.loads(doc)["ptensors"]):
+            try:
+                emu = planc_oracle.run_plan(plan, inputs, vv=True, round_bf16=True)
+                arrays.update({f"emu_{k}": v for k, v in emu.items()})
+                bf16_exact = True
+            except planc_oracle.InexactBf16:
+                pass
         with open(os.path.join(d, "graph.json"), "w") as f:
             f.write(doc)
         with open(os.path.join(d, "plan.json"), "w") as f:
@@ -181,7 +234,7 @@ def main():
         np.savez_compressed(os.path.join(d, "io.npz"), **arrays)
         pj = json.loads(plan)
         meta = dict(name=name, seed=seed, rel_tol=tol, provenance=prov, spec=spec, max_abs=peak,
-                    magnitude=1 if name.startswith("gpt_block") else 4,
+                    magnitude=magnitude, bf16_exact=bf16_exact,
                     reference_run_plan=ref_status, lanes=len(pj["lanes"]),
                     tasks=sum(len(l["tasks"]) for l in pj["lanes"]),
                     collectives=sorted({g["primitive"] for g in pj["coll_groups"]}),
@@ -189,7 +242,7 @@ def main():
         with open(os.path.join(d, "meta.json"), "w") as f:
             json.dump(meta, f, indent=1)
         index.append(name)
-        print(f"{name:24s} lanes={meta['lanes']} tasks={meta['tasks']:4d} ref={ref_status[:60]} "
+        print(f"{name:24s} bf16x={int(bf16_exact)} lanes={meta['lanes']} tasks={meta['tasks']:4d} ref={ref_status[:60]} "
               f"coll={meta['collectives']} kinds={meta['op_kinds']}")
     with open(os.path.join(HERE, "index.json"), "w") as f:
         json.dump(index, f, indent=1)

@@ -23,4 +23,4 @@ def load(name):
     io = np.load(os.path.join(d, "io.npz"))
     pick = lambda p: {int(k[len(p):]): io[k] for k in io.files if k.startswith(p)}  # noqa: E731
     return dict(name=name, plan=plan, graph=graph, meta=meta, inputs=pick("in_"), expected=pick("exp_"),
-                ref_plan=pick("ref_"))
+                ref_plan=pick("ref_"), emulated=pick("emu_"))

@@ -41,3 +41,22 @@ def test_verify_reports_input_errors_like_the_cli(tmp_path):
     r = subprocess.run([BIN, "--plan", str(bad), "--graph", os.path.join(d, "graph.json")], capture_output=True,
                        text=True, timeout=120)
     assert r.returncode == 4
+
+
+ACC = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
+
+
+@pytest.mark.skipif(not os.path.exists(ACC), reason="oracle/_ref/acceptance_b200 not built")
+def test_reference_acceptance_suite_with_b200_run_plan():
+    """The reference's own acceptance suite (acceptance.cpp, unmodified) with
+    every planc::run_plan call routed to the B200 (oracle/refexec_b200.cpp,
+    linker --wrap): criterion 1 is the 220-plan randomized corpus
+    (acceptance.cpp:36-71) — every plan bit-exact against the sequential
+    reference through testutil::oracle_ok; criteria 7 and 9 run their plans
+    on the GPU too. All nine criteria must pass."""
+    r = subprocess.run([ACC], capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert "PASS criterion 1: 220/220" in out, out
+    assert r.returncode == 0 and "FAIL" not in out, out
+    for c in range(1, 10):
+        assert f"PASS criterion {c}:" in out, out

@@ -347,20 +347,19 @@ def test_fused_gelu_epilogue(m, n, k, two_sm, monkeypatch):
     from plan_builder import matmul_gelu_plan
 
     monkeypatch.setenv("PLANC_B200_2SM", two_sm)
-    monkeypatch.setenv("PLANC_B200_FUSE_ACT", "1")  # opt-in fusion
     plan, out = matmul_gelu_plan(m, n, k)
-    assert pb.describe(plan)["instrs"][0]["label"] == "op+act"
+    assert pb.describe(plan, flags=pb.FUSE_ACT)["instrs"][0]["label"] == "op+act"
     rng = np.random.default_rng(m + n + k + 7 * int(two_sm))
     a = bf16_round(rng.standard_normal((m, k)) / 16)
     b = bf16_round(rng.standard_normal((k, n)))
     res = {}
-    for flags in (0, pb.NO_FUSION):
+    for flags in (pb.FUSE_ACT, pb.NO_FUSION):
         with pb.Executor(plan, lane_gpus=[0], flags=flags) as ex:
             ex.set_inputs({0: a, 1: b})
             ex.run(2)
             res[flags] = (ex.read_buffer(2).reshape(m, n), ex.get_output(out))
-    assert np.array_equal(res[0][0], res[pb.NO_FUSION][0])
-    assert np.array_equal(res[0][1], res[pb.NO_FUSION][1])
-    c = res[0][0]
+    assert np.array_equal(res[pb.FUSE_ACT][0], res[pb.NO_FUSION][0])
+    assert np.array_equal(res[pb.FUSE_ACT][1], res[pb.NO_FUSION][1])
+    c = res[pb.FUSE_ACT][0]
     ref = c * 0.5 * (1 + np.vectorize(erf)(c / np.sqrt(2)))
-    assert np.abs(res[0][1] - ref).max() <= 2.0 ** -7 * max(1.0, np.abs(ref).max())
+    assert np.abs(res[pb.FUSE_ACT][1] - ref).max() <= 2.0 ** -7 * max(1.0, np.abs(ref).max())

@@ -17,6 +17,7 @@ import pytest
 import golden_cases
 import paper_2301_08984_b200 as pb
 from oracle import planc_oracle as po
+from oracle import refpy
 from program_emu import run_program
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -166,13 +167,69 @@ def test_allgather_cells_copy_each_slice():
         assert all(len(c["terms"]) == 1 and not c["terms"][0]["add"] for c in i["cells"])
 
 
-def test_strict_value_mode_matches_reference_rule():
-    # With the reference rule the V(4)->V(2) extension is off; golden plans
-    # never need it, so both modes lower identically.
-    g = golden_cases.load("mlp_dp2")
-    a = pb.describe(g["plan"])
-    b = pb.describe(g["plan"], strict_value=True)
-    assert a["instrs"] == b["instrs"]
+@pytest.mark.parametrize("name", golden_cases.names())
+def test_strict_value_mode_matches_reference_rule(name):
+    """With the reference rule (STRICT_VALUE) the V(m*v)->V(v) extension is
+    off. Plans the reference executor runs lower identically in both modes;
+    the fact-6 plans (reference run_plan throws) fail to lower strictly with
+    the reference's InternalError and lower with the extension."""
+    g = golden_cases.load(name)
+    if g["meta"]["reference_run_plan"] == "ok":
+        assert pb.describe(g["plan"])["instrs"] == pb.describe(g["plan"], strict_value=True)["instrs"]
+    else:
+        with pytest.raises(pb.InternalError, match="not fully covered"):
+            pb.describe(g["plan"], strict_value=True)
+        desc = pb.describe(g["plan"])
+        # the chained reduce-scatters sum value sub-parts
+        assert any(t["add"] for i in desc["instrs"] for c in i["cells"] for t in c["terms"])
+
+
+def _two_row_parallel_doc(T=256, H=128):
+    """Two independent row-parallel (value-split) GEMMs of one shape whose
+    all-reduced outputs meet in an add (group_gemms must not merge
+    reduce-scatter GEMMs)."""
+    pts = [{"id": 0, "shape": [T, H], "elem_size": 2, "kind": "activation"},
+           {"id": 1, "shape": [H, H], "elem_size": 2, "kind": "weight"},
+           {"id": 2, "shape": [H, H], "elem_size": 2, "kind": "weight"},
+           {"id": 3, "shape": [T, H], "elem_size": 2, "kind": "activation"},
+           {"id": 4, "shape": [T, H], "elem_size": 2, "kind": "activation"},
+           {"id": 5, "shape": [T, H], "elem_size": 2, "kind": "activation"}]
+    ops = [{"id": "rowa", "kind": "matmul", "inputs": [0, 1], "outputs": [3], "direction": "forward",
+            "flops": 2.0 * T * H * H},
+           {"id": "rowb", "kind": "matmul", "inputs": [0, 2], "outputs": [4], "direction": "forward",
+            "flops": 2.0 * T * H * H},
+           {"id": "res", "kind": "add", "inputs": [3, 4], "outputs": [5], "direction": "forward", "flops": T * H}]
+    return json.dumps({"ptensors": pts, "ops": ops})
+
+
+@pytest.mark.skipif(not refpy.available(), reason="oracle/_ref not built")
+def test_reduce_scatter_gemms_are_never_grouped():
+    doc = _two_row_parallel_doc()
+    plan = refpy.compile_plan(doc, strategy="megatron_tp", devices=2)
+    desc = pb.describe(plan, lane_rank=[0, 1], flags=pb.PEER_MEMORY)
+    scat = [i for i in desc["instrs"] if i["kind"] == "gemm" and i["scatter"]]
+    assert len(scat) == 4  # two GEMMs x two lanes, each its own launch
+    for i in scat:
+        assert i["group"] == 1 and len(i["out"]) == i["scatter"]
+    inputs = refpy.random_integer_inputs(doc, 3, 1)
+    out = run_program(desc, json.loads(plan), inputs)
+    ok, msg = pb.compare_outputs(refpy.run_reference(doc, inputs), out, 2e-2, normwise=True)
+    assert ok, msg
+
+
+def test_fusion_requires_bf16_operands():
+    """an elementwise consumer with an fp32 operand is not fused
+    into a bf16 GEMM epilogue (which reads every operand as bf16)."""
+    from plan_builder import matmul_add_plan
+
+    plan, _ = matmul_add_plan(256, 256, 256)
+    p = json.loads(plan)
+    assert any(f for i in pb.describe(plan)["instrs"] for f in i["fused"])
+    for pt in p["ptensors"]:
+        if pt["id"] == 3:
+            pt["elem_size"] = 4
+    desc = pb.describe(json.dumps(p))
+    assert not any(f for i in desc["instrs"] for f in i["fused"])
 
 
 def test_malformed_plan_is_schema_error():
@@ -330,14 +387,14 @@ def test_gemm_schedule_covers_every_k_block_once(m, n, k, ta, sk_mode, monkeypat
         assert sc["sk_ctas"] > 0 or (tiles - sc["dp_tiles"]) * num_k < 8
 
 
-def test_opt_in_gelu_epilogue_fusion(monkeypatch):
-    """PLANC_B200_FUSE_ACT=1 moves GELU into its GEMM's epilogue (fused op
+def test_opt_in_gelu_epilogue_fusion():
+    """The FUSE_ACT flag moves GELU into its GEMM's epilogue (fused op
     ew 3); the lowered program still computes the same values."""
     g = golden_cases.load("ext_block_fwd_tp2_mma")
     plan = json.loads(g["plan"])
     base = run_program(pb.describe(g["plan"]), plan, g["inputs"])
-    monkeypatch.setenv("PLANC_B200_FUSE_ACT", "1")
-    desc = pb.describe(g["plan"])
+    assert not any(f["ew"] == 3 for i in pb.describe(g["plan"])["instrs"] for f in i["fused"])
+    desc = pb.describe(g["plan"], flags=pb.FUSE_ACT)
     assert any(f["ew"] == 3 for i in desc["instrs"] for f in i["fused"])
     out = run_program(desc, plan, g["inputs"])
     ok, msg = pb.compare_outputs(base, out, 0.0, normwise=True)

@@ -32,6 +32,61 @@ def test_golden_plan_parity(name):
     ok, msg = pb.compare_outputs(g["expected"], out, g["meta"]["rel_tol"], normwise=True)
     assert ok, msg
     assert st["kernels_per_step"] > 0
+    if g["emulated"]:
+        # bf16 plans in the exact-integer regime: bit for bit the plan's bf16
+        # emulation (rounding wherever the executor stores; tests/golden
+        # make_golden.py), whatever the kernels' fp32 summation order.
+        ok, msg = pb.compare_outputs(g["emulated"], out, 0.0)
+        assert ok, "bf16 emulation: " + msg
+
+
+REF_OK = [n for n in golden_cases.names() if golden_cases.load(n)["meta"]["reference_run_plan"] == "ok"]
+REF_THROWS = [n for n in golden_cases.names() if golden_cases.load(n)["meta"]["reference_run_plan"] != "ok"]
+
+
+@pytest.mark.parametrize("name", REF_OK)
+def test_value_split_extension_is_inert_where_the_reference_runs(name):
+    """The V(m*v)->V(v) extension (default on) changes nothing on any plan
+    the reference executor itself runs: bit-identical to STRICT_VALUE (the
+    reference's refexec.cpp:110-117 rule)."""
+    g = golden_cases.load(name)
+    out, _ = _run(g["plan"], g["inputs"])
+    strict, _ = _run(g["plan"], g["inputs"], flags=pb.STRICT_VALUE)
+    assert sorted(out) == sorted(strict)
+    for k in out:
+        assert np.array_equal(out[k], strict[k]), k
+
+
+@pytest.mark.parametrize("name", REF_THROWS)
+def test_fact6_plans_match_the_graph_reference(name):
+    """SURVEY fact 6: Dijkstra chains k=2 reduce-scatters (V(4)->V(2)->D);
+    the reference run_plan throws (meta), STRICT_VALUE throws the same
+    InternalError, the default executes the plan and equals run_reference on
+    the graph bit for bit (fp32, integer inputs)."""
+    g = golden_cases.load(name)
+    assert g["meta"]["reference_run_plan"].startswith("throws: reconstruct")
+    with pytest.raises(pb.InternalError, match="not fully covered"):
+        _run(g["plan"], g["inputs"], flags=pb.STRICT_VALUE)
+    out, _ = _run(g["plan"], g["inputs"])
+    ok, msg = pb.compare_outputs(g["expected"], out, 0.0)
+    assert ok, msg
+    ok, msg = po.compare_outputs(po.run_plan(g["plan"], g["inputs"], vv=True), out, 0.0)
+    assert ok, msg
+
+
+@pytest.mark.parametrize("name", ["gpt_block_train_tp1_mma", "gpt_block_train_tp2_mma", "c2_cpu_tp1"])
+def test_train_step_gemms_take_tensor_cores(name):
+    """Every GEMM of the bf16 train step — forward, the transposed-operand
+    dX / dW GEMMs of the backward, fused optimizer epilogues — runs on the
+    tcgen05 path, and the step equals the bf16 emulation bit for bit."""
+    g = golden_cases.load(name)
+    desc = pb.describe(g["plan"])
+    gemms = [i for i in desc["instrs"] if i["kind"] == "gemm"]
+    assert any(i["ta"] for i in gemms) and any(i["tb"] for i in gemms)  # dW / dX shapes present
+    out, st = _run(g["plan"], g["inputs"])
+    assert st["gemm_tc_per_step"] == len(gemms), (st["gemm_tc_per_step"], len(gemms))
+    ok, msg = pb.compare_outputs(g["emulated"], out, 0.0)
+    assert ok, msg
 
 
 @pytest.mark.parametrize("name", ["mlp_dp2", "gpt_block_tp2", "embed_shard2", "adapt_d1_to_d0_4",
@@ -62,11 +117,33 @@ def test_repeated_steps_are_idempotent():
     assert ok, msg
 
 
-def test_gpu_matches_numpy_oracle_vtensor_level():
+def test_gpu_matches_numpy_oracle_ptensor_level():
     g = golden_cases.load("mlp_1f1b_dp2")
     out, _ = _run(g["plan"], g["inputs"])
     ok, msg = po.compare_outputs(po.run_plan(g["plan"], g["inputs"]), out, 0.0)
     assert ok, msg
+
+
+@pytest.mark.parametrize("name", ["mlp_1f1b_dp2", "gpt_block_tp2", "adapt_vv_rs2x2", "embed_shard2"])
+def test_gpu_matches_numpy_oracle_vtensor_level(name):
+    """Every produced vTensor (every piece every lane holds, adapters'
+    intermediate results included) read back from its device buffer equals
+    the restatement's per-vTensor value (planc_oracle return_vtensors)."""
+    g = golden_cases.load(name)
+    _, vts = po.run_plan(g["plan"], g["inputs"], vv=True, return_vtensors=True)
+    desc = pb.describe(g["plan"])
+    n = len(json.loads(g["plan"])["lanes"])
+    checked = 0
+    with pb.Executor(g["plan"], lane_gpus=[0] * n, flags=pb.NO_ALIAS) as ex:
+        ex.set_inputs(g["inputs"])
+        ex.run(0)
+        for vt, buf in enumerate(desc["vt_buffer"]):
+            if buf < 0 or vt not in vts or desc["buffers"][buf]["dead"]:
+                continue
+            got = ex.read_buffer(buf).reshape(vts[vt].shape)
+            assert np.array_equal(got, vts[vt]), f"vtensor {vt} (buffer {buf})"
+            checked += 1
+    assert checked >= len(vts) // 2
 
 
 def test_missing_input_is_usage_error():
