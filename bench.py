@@ -44,10 +44,11 @@ PLANS = os.path.join(ROOT, "plans")
 
 def plan_name(config: str, n: int) -> str:
     """c2 / c1l plans are compiled per GPU count (TP / DP degree n); the
-    pipeline (c3: 8 lanes), co-shard (c4: 1 lane) and 3F1B (c5: 2 lanes)
-    plans have a fixed lane count — with fewer GPUs, lanes share GPUs."""
-    return {"c2": f"c2_tp{n}", "c2x": f"c2x_tp{n}", "c1l": f"c1l_dp{n}", "c3": "c3_pp4dp2", "c4": "c4_coshard4",
-            "c5": "c5_3f1b"}[config]
+    pipeline (c3: pp4 x dp2), co-shard x DP (c4: dp8 x co-shard 4) and 3F1B
+    x DAP (c5: 4 stages x dap 2) plans have 8 lanes — with fewer GPUs, lanes
+    share GPUs (round robin)."""
+    return {"c2": f"c2_tp{n}", "c2x": f"c2x_tp{n}", "c1l": f"c1l_dp{n}", "c3": "c3_pp4dp2", "c4": "c4_coshard4_dp8",
+            "c5": "c5_3f1b_dap"}[config]
 
 
 def load_plan(name):
@@ -406,9 +407,11 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (integer-valued inputs in {-1,0,1})",
             "config": {"workload": name, "config": args.config, "plan": f"plans/{name}.plan.json",
-                       "shape": {k: meta[k] for k in ("tokens", "batch", "hidden", "middle", "layers", "head") if k in meta},
+                       "shape": {k: meta[k] for k in ("tokens", "batch", "hidden", "middle", "layers", "head", "msa", "pair",
+                                                                  "micro_batches") if k in meta},
                        "parallelism": {"c2": f"tp{n}", "c2x": f"tp{n}", "c1l": f"dp{n}", "c3": "pp4 x dp2 (1F1B, K=8)",
-                                       "c4": "co-shard x4", "c5": "3F1B pp2 (K=4)"}[args.config],
+                                       "c4": "dp8 x co-shard 4 (FFN)",
+                                       "c5": "3F1B pp4 x dap2 (K=4)"}[args.config],
                        "lanes_per_gpu": nlanes / max(n, 1),
                        "sample": meta["sample"], "l2": "step working set " +
                        f"{st['device_bytes'] / 2**30:.1f} GiB > 126 MB L2 (no flush needed)",

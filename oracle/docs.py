@@ -271,3 +271,121 @@ def rewrite_plan(plan_json: str, doc: dict) -> str:
     if n == 0:
         raise ValueError("rewrite_plan: no extended op found in the plan")
     return json.dumps(p)
+
+
+# ---- C4 / C5 benchmark documents ------------------------------------
+
+
+def swin_stage_doc(tokens: int, hidden: int, elem_size: int = 2) -> dict:
+    """Swin-Transformer stage block proxy (config C4): the
+    GPT-style block of ``gpt_block_doc`` (window-attention proxy Q / K / S /
+    O, FFN 4H with ReLU proxy) as a train step, plus one ``agw*`` identity op
+    per updated weight — the parameter publication of a sharded (ZeRO-style)
+    optimizer: every data-parallel rank updates a row slice of each weight
+    and the next step's replicas read the whole updated weight. Under the
+    ``coshard_dp`` sProgram the weight gradients therefore leave each rank as
+    reduce-scatters (V(dp) -> D(dp)) and the updates come back as
+    all-gathers (D(dp) -> R(dp)), the adapters Dijkstra picks for sharded
+    weight updates (reference rvd.cpp:194-284)."""
+    d = gpt_block_doc(tokens, hidden, elem_size, train=True)
+    pts, ops = d["ptensors"], d["ops"]
+    H, F = hidden, 4 * hidden
+    for v, (w, shp) in enumerate((("wq", (H, H)), ("wk", (H, H)), ("wo", (H, H)), ("w1", (H, F)), ("w2", (F, H)))):
+        pts.append(_pt(140 + v, shp, "weight", elem_size))
+        ops.append(_op("agw" + w, "identity", [130 + v], [140 + v], "optimizer", 0, {"layer": 0}))
+    return {"ptensors": pts, "ops": ops}
+
+
+def evoformer_doc(layers: int, msa: tuple, pair: tuple, micro_batches: int = 1, elem_size: int = 2) -> dict:
+    """AlphaFold2 Evoformer proxy (config C5) in the
+    three-forward-passes-plus-one-backward shape of the reference's
+    ``three_pass_doc`` (proj/tests/testutil.cpp:298-368: passes 1-3 with
+    their own weights, gradients only through pass 3), with two streams per
+    layer: the MSA representation M [Nm, Cm] and the pair representation
+    Z [Np, Cz]. Each stream, per layer, pass and micro-batch:
+
+      R = X·Wr       row-attention proxy    (``row*``: DAP splits rows, dim 0)
+      C = max(R, G)  column-attention proxy (``col*``: DAP splits channels, dim 1)
+      X' = C·Wt      transition             (``row*``: rows again)
+
+    so DAP (``threef1b_dap``) switches the layout D(2,1) -> D(1,2) -> D(2,1)
+    twice per stream and layer: the all-to-all layout adapters of
+    rvd.cpp:286-326. Micro-batches are explicit in the document (op ids end
+    in ``#k``; activations of micro-batch k are their own pTensors of Nr/K
+    rows; weights are shared): the reference's collective pattern matching
+    works per pTensor family (rvd.cpp:785-870) and only finds collectives
+    when one family is one micro-batch. Backward (pass 3, reverse layer
+    order, per micro-batch) declares dX / dW GEMMs (transposed operands) and
+    the gate gradient mul(dC, G); the K weight gradients of a pass-3 weight
+    are accumulated by one ``gacc`` add and applied by one optimizer add."""
+    e = elem_size
+    L, K = layers, micro_batches
+    pts, ops = [], []
+    for s, (Nr, Cc), base in (("m", msa, 0), ("z", pair, 500000)):
+        if Nr % K:
+            raise ValueError("rows must divide into micro-batches")
+        rows = Nr // K
+        # activations of micro-batch k: base + 10000*k + 100*p + 10*l + {0: X_in, 1: R, 2: C, 3: X'}
+        act = lambda k, p, l, j, base=base: base + 10000 * k + 100 * p + 10 * l + j  # noqa: E731
+        wt = lambda p, l, j, base=base: base + 100000 + 100 * p + 10 * l + j  # noqa: E731  (0 Wr, 1 Wt, 2 G)
+        gx = lambda k, l, base=base: base + 200000 + 10000 * k + 10 * l  # noqa: E731  (+0 dX_in, +1 dR, +2 dC)
+        gw = lambda k, l, j, base=base: base + 300000 + 1000 * k + 10 * l + j  # noqa: E731
+        for p in (1, 2, 3):
+            for l in range(L):
+                for j in (0, 1):
+                    pts.append(_pt(wt(p, l, j), (Cc, Cc), "weight", e))
+                pts.append(_pt(wt(p, l, 2), (rows, Cc), "activation", e))  # gate, shared by the micro-batches
+        for l in range(L):
+            for j in (0, 1):
+                pts.append(_pt(gw(K, l, j), (Cc, Cc), "gradient", e, wt(3, l, j)))  # accumulated
+                pts.append(_pt(gw(K + 1, l, j), (Cc, Cc), "weight", e))  # updated
+        mm = 2.0 * rows * Cc * Cc
+        for k in range(K):
+            pts.append(_pt(act(k, 1, 0, 0), (rows, Cc), "activation", e))
+            for p in (1, 2, 3):
+                for l in range(L):
+                    for j in (1, 2, 3):
+                        pts.append(_pt(act(k, p, l, j), (rows, Cc), "activation", e))
+            for p in (1, 2, 3):
+                for l in range(L):
+                    x_in = act(k, 1, 0, 0) if (p == 1 and l == 0) else (
+                        act(k, p - 1, L - 1, 3) if l == 0 else act(k, p, l - 1, 3))
+                    A = {"layer": l, "batch_dim": 0, "pass": p}
+                    f = f"{s}{p}_{l}"
+                    ops.append(_op(f"{f}.rowr#{k}", "matmul", [x_in, wt(p, l, 0)], [act(k, p, l, 1)], "forward", mm, A))
+                    ops.append(_op(f"{f}.colg#{k}", "max", [act(k, p, l, 1), wt(p, l, 2)], [act(k, p, l, 2)],
+                                   "forward", rows * Cc, A))
+                    ops.append(_op(f"{f}.rowt#{k}", "matmul", [act(k, p, l, 2), wt(p, l, 1)], [act(k, p, l, 3)],
+                                   "forward", mm, A))
+            for l in range(L):
+                x_in = act(k, 2, L - 1, 3) if l == 0 else act(k, 3, l - 1, 3)
+                pts.append(_pt(gx(k, l), (rows, Cc), "gradient", e, x_in))
+                pts.append(_pt(gx(k, l) + 1, (rows, Cc), "gradient", e, act(k, 3, l, 1)))
+                pts.append(_pt(gx(k, l) + 2, (rows, Cc), "gradient", e, act(k, 3, l, 2)))
+                for j in (0, 1):
+                    pts.append(_pt(gw(k, l, j), (Cc, Cc), "gradient", e, wt(3, l, j)))
+            pts.append(_pt(gx(k, L), (rows, Cc), "gradient", e, act(k, 3, L - 1, 3)))
+            for l in reversed(range(L)):
+                x_in = act(k, 2, L - 1, 3) if l == 0 else act(k, 3, l - 1, 3)
+                B = {"layer": l}
+                TA, TB = dict(B, transpose_a=True), dict(B, transpose_b=True)
+                f = f"{s}3_{l}"
+                ops += [
+                    _op(f"{f}.growt#{k}", "matmul", [gx(k, l + 1), wt(3, l, 1)], [gx(k, l) + 2], "backward", mm, TB,
+                        f"{f}.rowt#{k}"),
+                    _op(f"{f}.growtw#{k}", "matmul", [act(k, 3, l, 2), gx(k, l + 1)], [gw(k, l, 1)], "backward", mm,
+                        TA, f"{f}.rowt#{k}"),
+                    _op(f"{f}.gcolg#{k}", "mul", [gx(k, l) + 2, wt(3, l, 2)], [gx(k, l) + 1], "backward", rows * Cc,
+                        B, f"{f}.colg#{k}"),
+                    _op(f"{f}.growr#{k}", "matmul", [gx(k, l) + 1, wt(3, l, 0)], [gx(k, l)], "backward", mm, TB,
+                        f"{f}.rowr#{k}"),
+                    _op(f"{f}.growrw#{k}", "matmul", [x_in, gx(k, l) + 1], [gw(k, l, 0)], "backward", mm, TA,
+                        f"{f}.rowr#{k}"),
+                ]
+        for l in range(L):
+            for j in (0, 1):
+                ops.append(_op(f"{s}3_{l}.gacc{j}", "add", [gw(k, l, j) for k in range(K)], [gw(K, l, j)],
+                               "optimizer", K * Cc * Cc, {"layer": l}))
+                ops.append(_op(f"{s}3_{l}.opt{j}", "add", [wt(3, l, j), gw(K, l, j)], [gw(K + 1, l, j)],
+                               "optimizer", Cc * Cc, {"layer": l}))
+    return {"ptensors": pts, "ops": ops}

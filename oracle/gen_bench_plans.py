@@ -9,6 +9,10 @@ box has no reference. Shapes follow SURVEY.md §8d:
        T=8192 tokens (4 seq x 2048), H=2048, FFN=4H, bf16,
        Megatron TP = 1/2/4/8 (megatron_tp sProgram)
   c1l  2-layer MLP (reference mlp_doc) B=16384, H=4096, bf16, DP = 1/2/4/8
+  c4   Swin stage block (docs.swin_stage_doc), 8-way DP x co-shard 4
+       (coshard_dp sProgram), 131072 tokens, H=512, bf16
+  c5   Evoformer proxy (docs.evoformer_doc), MSA [32768,256] + pair
+       [65536,128], 3F1B over 4 stages x 2-way DAP (threef1b_dap), bf16
   c2x  the schema-extension transformer block (docs.gpt_block_ext_doc: LN,
        per-head softmax, GELU and their gradients), T=8192, H=2048, 16 heads
        of 128, bf16, Megatron TP = 1/2/4/8 — compiled by the reference front
@@ -70,12 +74,63 @@ def gen_c2x():
                 write(f"c2x_tp{k}{tag}_standin", stand, plan, dict(meta, tp=k, standin=True))
 
 
+# C4: Swin stage block (H=512, FFN 2048) as a train step, 16384 tokens per GPU
+# x 8-way data parallelism = 131072 tokens; co-shard x4 of the FFN chain on
+# every rank (coshard_dp, oracle/ref_capi.cpp). Weight gradients leave the
+# ranks as reduce-scatters (attention weights; Dijkstra's pick) or naive
+# send/recv + reduce-assemble chains (the co-sharded FFN weights: the
+# reference's RVD matcher skips families whose ranks hold several pieces,
+# rvd.cpp:825-846); the updated weights come back as all-gathers.
+C4_SHAPE = (8 * 16384, 512)
+C4_SPEC = dict(strategy="coshard_dp", devices=8, shards=4, target_ops="colf1+tprelu+roww2")
+# C5: Evoformer proxy, MSA [32768, 256] + pair [65536, 128], 4 layers, three
+# forward passes + one backward, K=4 micro-batches, 3F1B over 4 stages x
+# 2-way DAP (threef1b_dap): all-to-all layout switches, reduce-scatter weight
+# gradients inside each DAP pair, P2P between stages.
+C5_SHAPE = (4, (32768, 256), (65536, 128), 4)
+C5_SPEC = dict(strategy="threef1b_dap", devices=8, stages=4, micro_batches=4, inner_dp=2)
+
+
+def gen_c4():
+    for T, H, tag in (C4_SHAPE + ("",), (8 * 32, 64, "_cpu")):
+        g = docs.dumps(docs.swin_stage_doc(T, H))
+        plan = refpy.compile_plan(g, **C4_SPEC)
+        write(f"c4_coshard4_dp8{tag}", g, plan,
+              dict(config="c4", tokens=T, hidden=H, middle=4 * H, shards=4, dp=8, dtype="bf16",
+                   samples_per_step=T, sample="token (row of the stage input)", spec=C4_SPEC))
+
+
+def gen_c5():
+    for shape, tag in ((C5_SHAPE, ""), ((4, (512, 32), (1024, 16), 4), "_cpu")):
+        L, msa, pair, K = shape
+        g = docs.dumps(docs.evoformer_doc(L, msa, pair, K))
+        plan = refpy.compile_plan(g, **C5_SPEC)
+        write(f"c5_3f1b_dap{tag}", g, plan,
+              dict(config="c5", layers=L, msa=list(msa), pair=list(pair), batch=msa[0], hidden=msa[1],
+                   micro_batches=K, stages=4, dap=2, dtype="bf16", samples_per_step=msa[0],
+                   sample="MSA row (sequence x residue) of the batch", spec=C5_SPEC))
+
+
+def gen_ref1():
+    # Unpartitioned single-lane plans of the C3/C4/C5 graphs at full size: the
+    # partition-invariance property tests compare the partitioned plans
+    # against them (tests/test_fullsize_gpu.py).
+    for name, g in (("c3_ref1", docs.dumps(docs.gpt_stack_doc(8, 32768, 2048, elem_size=2))),
+                    ("c4_ref1", docs.dumps(docs.swin_stage_doc(*C4_SHAPE))),
+                    ("c5_ref1", docs.dumps(docs.evoformer_doc(*C5_SHAPE)))):
+        plan = refpy.compile_plan(g, strategy="none", devices=1)
+        write(name, g, plan, dict(config=name[:2], strategy="none", dtype="bf16"))
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     only = set(sys.argv[1:])
     if only:
-        if "c2x" in only:
-            gen_c2x()
+        for name, fn in (("c2x", gen_c2x), ("c4", gen_c4), ("c5", gen_c5)):
+            if name in only:
+                fn()
+        if "ref1" in only:
+            gen_ref1()
         return
     gen_c2x()
     for T, H, tag in ((8192, 2048, ""), (128, 128, "_cpu")):
@@ -94,26 +149,9 @@ def main():
         write(f"c3_pp4dp2{tag}", g, plan, dict(config="c3", layers=L, tokens=T, hidden=H, stages=4, inner_dp=2,
                                                 micro_batches=8, dtype="bf16", samples_per_step=T,
                                                 sample="token (row of X)"))
-    # C4: co-shard x4 of the FFN-like pair (op1, op2) on one device (Swin stage proxy).
-    for B, H, M, tag in ((16384, 512, 2048, ""), (128, 64, 256, "_cpu")):
-        g = refpy.with_elem_size(refpy.coshard_doc(batch=B, hidden=H, middle=M), 2)
-        plan = refpy.compile_plan(g, strategy="coshard", devices=1, shards=4, target_ops="op1,op2")
-        write(f"c4_coshard4{tag}", g, plan, dict(config="c4", batch=B, hidden=H, middle=M, shards=4, dtype="bf16",
-                                                  samples_per_step=B, sample="row of the batch"))
-    # C5: three chained forward passes + one backward (Evoformer proxy), 3F1B S=2.
-    for B, H, tag in ((32768, 256, ""), (128, 32, "_cpu")):
-        g = refpy.with_elem_size(refpy.three_pass_doc(layers=4, batch=B, hidden=H), 2)
-        plan = refpy.compile_plan(g, strategy="3f1b", devices=2, stages=2, micro_batches=4)
-        write(f"c5_3f1b{tag}", g, plan, dict(config="c5", batch=B, hidden=H, stages=2, micro_batches=4,
-                                              dtype="bf16", samples_per_step=B, sample="row of the MSA batch"))
-    # Unpartitioned single-lane plans of the C3/C4/C5 graphs at full size: the
-    # partition-invariance property tests compare the partitioned plans
-    # against them (tests/test_fullsize_gpu.py).
-    for name, g in (("c3_ref1", docs.dumps(docs.gpt_stack_doc(8, 32768, 2048, elem_size=2))),
-                    ("c4_ref1", refpy.with_elem_size(refpy.coshard_doc(batch=16384, hidden=512, middle=2048), 2)),
-                    ("c5_ref1", refpy.with_elem_size(refpy.three_pass_doc(layers=4, batch=32768, hidden=256), 2))):
-        plan = refpy.compile_plan(g, strategy="none", devices=1)
-        write(name, g, plan, dict(config=name[:2], strategy="none", dtype="bf16"))
+    gen_c4()
+    gen_c5()
+    gen_ref1()
     for B, H, tag in ((16384, 4096, ""), (128, 128, "_cpu")):
         g = refpy.with_elem_size(refpy.mlp_doc(layers=2, batch=B, hidden=H), 2)
         for k in (1, 2, 4, 8):

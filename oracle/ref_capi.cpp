@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -245,10 +246,204 @@ StrategyInfo manual(PlanGraph& g, const ClusterSpec& env,
   return {};
 }
 
+bool has_backward_pair(const PlanGraph& g, const std::string& fwd) {
+  for (const auto& o : g.ops) {
+    if (o.backward_of && *o.backward_of == fwd) return true;
+  }
+  return false;
+}
+
+// op_trans preceded by adapt_backward when the op has declared backward
+// pairs (the composition the reference's own strategies use,
+// strategies.cpp:43-53); backward replacement i of every backward op is
+// appended to *bwd in op order.
+std::vector<std::string> trans_with_backward(PlanGraph& g, const std::string& oid, const TransformAlgo& algo,
+                                             std::vector<std::string>* bwd) {
+  if (has_backward_pair(g, oid)) {
+    auto b = adapt_backward(g, oid, algo);
+    bwd->insert(bwd->end(), b.begin(), b.end());
+  }
+  return op_trans(g, oid, algo);
+}
+
+std::string role_of(const std::string& oid) {
+  auto dot = oid.rfind('.');
+  return dot == std::string::npos ? oid : oid.substr(dot + 1);
+}
+
+// Config C4: co-shard x `shards` composed with `devices`-way
+// data parallelism. Forward ops split their batch dim across the DP ranks
+// (plan_data_parallel, strategies.cpp:120-146); optimizer adds split dim 0
+// across the ranks (a sharded, ZeRO-style optimizer: rank i updates rows
+// slice i), "agw*" publication ops stay replicated; then on every rank the
+// `target_ops` replacements are co-sharded with the reference's own
+// plan_coshard (strategies.cpp:278-396: time-multiplexed sub-operators with
+// recompute, chained split choice, shard i before shard i+1).
+StrategyInfo coshard_dp(PlanGraph& g, const ClusterSpec& env, const StrategyConfig& cfg) {
+  const int n = cfg.devices;
+  std::map<std::string, std::vector<std::string>> dp_ids;
+  std::vector<std::string> snapshot;
+  for (const auto& op : g.ops) snapshot.push_back(op.id);
+  for (const auto& oid : snapshot) {
+    if (!g.has_op(oid)) continue;
+    const OpNode& op = g.op(oid);
+    if (op.direction == OpDirection::backward) continue;
+    TransformAlgo algo = replica_algo(n);
+    if (op.direction == OpDirection::forward) {
+      if (!op.attrs.batch_dim) throw UsageError("coshard_dp: forward op " + oid + " has no batch_dim");
+      algo = split_algo(*op.attrs.batch_dim, n);
+    } else if (role_of(oid).rfind("agw", 0) != 0) {
+      algo = split_algo(0, n);
+    }
+    std::vector<std::string> bwd;
+    auto ids = trans_with_backward(g, oid, algo, &bwd);
+    for (std::size_t i = 0; i < ids.size(); ++i) op_assign(g, env, ids[i], static_cast<int>(i % n));
+    for (std::size_t i = 0; i < bwd.size(); ++i) op_assign(g, env, bwd[i], static_cast<int>(i % n));
+    dp_ids[oid] = ids;
+  }
+  // Each target_ops entry is one co-shard group ("a+b+c": a chain of ops
+  // sharded together, shard i of the group before shard i+1); groups are
+  // co-sharded independently, so a whole op between two chains (a residual
+  // add) never sits inside one group's shard order.
+  if (cfg.shards > 1) {
+    for (int d = 0; d < n; ++d) {
+      for (const auto& entry : cfg.target_ops) {
+        std::vector<std::string> targets;
+        std::stringstream ss(entry);
+        std::string t;
+        while (std::getline(ss, t, '+')) {
+          auto it = dp_ids.find(t);
+          if (it == dp_ids.end()) throw UsageError("coshard_dp: unknown target op " + t);
+          targets.push_back(it->second.at(static_cast<std::size_t>(d)));
+        }
+        plan_coshard(g, env, targets, cfg.shards, d);
+      }
+    }
+  }
+  return {};
+}
+
+// Config C5: the 3F1B schedule (plan_3f1b, strategies.cpp:
+// 524-653) over `stages` pipeline stages of `dap` devices each, with the
+// micro-batches declared by the document (op id suffix "#k"), every
+// micro-batch sub-operator split DAP-style inside its stage (Dynamic Axial
+// Parallelism): "row*" ops on dim 0 (rows), "col*" ops on dim 1 (channels),
+// so consecutive row / column ops switch layout D(dap,1) <-> D(1,dap) — the
+// all-to-all adapters (rvd.cpp:286-326). Optimizer adds split dim 0 over
+// the stage's DAP group. Stage of a layer: contiguous equal count (as
+// stage_of_layer, strategies.cpp:72-103). Per stage the task order is the
+// 3F1B priority list (backward first, then forward passes 3, 2, 1, lowest
+// micro-batch first), enforced with op_order between consecutive groups.
+StrategyInfo threef1b_dap(PlanGraph& g, const ClusterSpec& env, const StrategyConfig& cfg) {
+  const int S = cfg.stages, K = cfg.micro_batches;
+  const int dap = cfg.inner_dp > 0 ? cfg.inner_dp : 1;
+  if (S * dap != cfg.devices) throw UsageError("threef1b_dap: devices must equal stages x dap");
+  std::set<int> layer_set;
+  for (const auto& op : g.ops) {
+    if (op.direction == OpDirection::forward && op.attrs.layer) layer_set.insert(*op.attrs.layer);
+  }
+  std::vector<int> layers(layer_set.begin(), layer_set.end());
+  if (static_cast<int>(layers.size()) < S) throw UsageError("threef1b_dap: fewer layers than stages");
+  std::map<int, int> stage_of;
+  for (std::size_t i = 0; i < layers.size(); ++i)
+    stage_of[layers[i]] = static_cast<int>(i * static_cast<std::size_t>(S) / layers.size());
+  auto layer = [&](const OpNode& op) {
+    if (!op.attrs.layer) throw UsageError("threef1b_dap: op " + op.id + " has no layer");
+    return *op.attrs.layer;
+  };
+  // 1. micro-batches are explicit in the document: op ids end in "#k"
+  // (docs.evoformer_doc) — one pTensor family per micro-batch, so the
+  // collective pattern matching (rvd.cpp:785-870) sees whole families.
+  for (auto& op : g.ops) {
+    if (op.direction == OpDirection::optimizer || op.is_reserved_kind()) continue;
+    auto h = op.id.rfind('#');
+    if (h == std::string::npos) throw UsageError("threef1b_dap: op " + op.id + " lacks a #micro-batch suffix");
+    op.micro_batch = std::stoi(op.id.substr(h + 1));
+    if (*op.micro_batch >= K) throw UsageError("threef1b_dap: micro-batch of " + op.id + " >= micro_batches");
+    if (op.direction == OpDirection::forward && !op.attrs.pass_index) throw UsageError("threef1b_dap: no pass on " + op.id);
+  }
+  // 2. per-stage 3F1B order over (pass, micro-batch) groups; pass 0 = backward
+  using Task = std::pair<int, int>;
+  std::vector<std::set<Task>> done(S);
+  std::vector<std::vector<Task>> seq(S);
+  auto ready = [&](int s, Task t) {
+    if (t.first == 0) return (s + 1 == S || done[s + 1].count(t)) && done[s].count({3, t.second}) > 0;
+    if (s > 0) return done[s - 1].count(t) > 0;
+    return t.first == 1 || done[S - 1].count({t.first - 1, t.second}) > 0;
+  };
+  for (int total = 0, guard = 0; total < 4 * S * K; ++guard) {
+    if (guard > 16 * S * K + 16) throw InternalError("threef1b_dap: schedule stalled");
+    std::vector<Task> pick(S, {-1, -1});
+    for (int s = 0; s < S; ++s) {
+      for (int pass : {0, 3, 2, 1}) {
+        for (int mb = 0; mb < K && pick[s].first < 0; ++mb) {
+          if (!done[s].count({pass, mb}) && ready(s, {pass, mb})) pick[s] = {pass, mb};
+        }
+        if (pick[s].first >= 0) break;
+      }
+    }
+    for (int s = 0; s < S; ++s) {
+      if (pick[s].first < 0) continue;
+      done[s].insert(pick[s]);
+      seq[s].push_back(pick[s]);
+      ++total;
+    }
+  }
+  auto group = [&](int s, Task t) {
+    std::vector<std::string> out;
+    for (const auto& op : g.ops) {
+      if (op.is_reserved_kind() || !op.micro_batch || *op.micro_batch != t.second) continue;
+      if (op.direction == OpDirection::optimizer || stage_of.at(layer(op)) != s) continue;
+      const bool b = op.direction == OpDirection::backward;
+      if (t.first == 0 ? !b : (b || op.attrs.pass_index.value_or(-1) != t.first)) continue;
+      out.push_back(op.id);
+    }
+    return out;
+  };
+  StrategyInfo info;
+  info.stage_task_sequences.resize(S);
+  for (int s = 0; s < S; ++s) {
+    std::vector<std::string> prev;
+    for (const auto& t : seq[s]) {
+      auto ops = group(s, t);
+      if (ops.empty()) throw InternalError("threef1b_dap: empty group");
+      for (const auto& a : prev)
+        for (const auto& b : ops) op_order(g, a, b);
+      prev = ops;
+      info.stage_task_sequences[s].push_back(ops);
+    }
+  }
+  // 3. DAP inside each stage (happen-before edges follow the replacements)
+  std::vector<std::string> snapshot;
+  for (const auto& op : g.ops) snapshot.push_back(op.id);
+  for (const auto& oid : snapshot) {
+    if (!g.has_op(oid)) continue;
+    const OpNode& op = g.op(oid);
+    if (op.direction == OpDirection::backward || op.is_reserved_kind()) continue;
+    const int s = stage_of.at(layer(op));
+    const std::string r = role_of(oid.substr(0, oid.find('#')));
+    TransformAlgo algo = split_algo(0, dap);
+    if (op.direction == OpDirection::forward && r.rfind("col", 0) == 0) algo = split_algo(1, dap);
+    std::vector<std::string> bwd;
+    std::vector<std::string> ids{oid};
+    if (dap > 1) ids = trans_with_backward(g, oid, algo, &bwd);
+    for (std::size_t i = 0; i < ids.size(); ++i) op_assign(g, env, ids[i], s * dap + static_cast<int>(i % dap));
+    for (std::size_t i = 0; i < bwd.size(); ++i) op_assign(g, env, bwd[i], s * dap + static_cast<int>(i % dap));
+  }
+  for (const auto& op : g.ops) {
+    if (!g.assignment.count(op.id) && !op.is_reserved_kind()) op_assign(g, env, op.id, stage_of.at(layer(op)) * dap);
+  }
+  // stage sequences are reported at micro-batch granularity (pre-DAP ids)
+  info.stage_task_sequences.clear();
+  return info;
+}
+
 struct Registrar {
   Registrar() {
     register_strategy("megatron_tp", megatron_tp);
     register_strategy("manual", manual);
+    register_strategy("coshard_dp", coshard_dp);
+    register_strategy("threef1b_dap", threef1b_dap);
   }
 } registrar;
 

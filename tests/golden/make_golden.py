@@ -185,6 +185,19 @@ def cases():
     out.append(("c2_cpu_tp1", docs.dumps(docs.gpt_block_doc(128, 128, elem_size=2, train=True)),
                 dict(strategy="megatron_tp", devices=1), 1, 2e-2,
                 "plans/c2_tp1_cpu (the bench's reduced-shape C2 plan, T=H=128), bf16 train step"))
+    # C4 / C5 as BASELINE.json states them, at small shapes (8 lanes each):
+    # Swin stage x 8-way DP x co-shard 4 (reduce-scatter / all-gather weight
+    # adapters) and the Evoformer proxy under 3F1B x 2-way DAP (all-to-all).
+    c4 = dict(strategy="coshard_dp", devices=8, shards=4, target_ops="colf1+tprelu+roww2")
+    c5 = dict(strategy="threef1b_dap", devices=8, stages=4, micro_batches=2, inner_dp=2)
+    out.append(("c4_coshard_dp8", docs.dumps(docs.swin_stage_doc(256, 16, elem_size=4)), c4, 401, 0.0,
+                "C4: Swin stage block, coshard_dp (DP 8 x co-shard 4 of the FFN), fp32"))
+    out.append(("c4_coshard_dp8_bf16", docs.dumps(docs.swin_stage_doc(256, 64, elem_size=2)), c4, 402, 2e-2,
+                "C4: Swin stage block, coshard_dp, bf16"))
+    out.append(("c5_3f1b_dap", docs.dumps(docs.evoformer_doc(4, (128, 4), (256, 4), 2, elem_size=4)), c5, 501,
+                0.0, "C5: Evoformer proxy (MSA + pair), 3F1B x DAP 2 (all-to-all), fp32"))
+    out.append(("c5_3f1b_dap_bf16", docs.dumps(docs.evoformer_doc(4, (256, 4), (512, 4), 2, elem_size=2)), c5,
+                682, 2e-2, "C5: Evoformer proxy (MSA + pair), 3F1B x DAP 2 (all-to-all), bf16"))
     out.append(("gpt_block_fwd_tp2_mma", docs.dumps(docs.gpt_block_doc(256, 128, elem_size=2, train=False)),
                 dict(strategy="megatron_tp", devices=2), 71, 2e-2,
                 "C2 forward at tensor-core-eligible shapes (bf16)"))
@@ -199,7 +212,7 @@ def main():
         plan = refpy.compile_plan(doc, **spec)
         # Small-magnitude inputs keep every fp32 partial sum below 2^24 so
         # fp32 plans are bit-exact against the double-precision oracle.
-        magnitude = 1 if name.startswith(("gpt_", "c2_")) else 4
+        magnitude = 1 if name.startswith(("gpt_", "c2_", "c4_", "c5_")) else 4
         inputs = refpy.random_integer_inputs(doc, seed, magnitude)
         expected = refpy.run_reference(doc, inputs)
         peak = max(float(np.abs(v).max()) for v in expected.values())

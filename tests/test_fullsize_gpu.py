@@ -62,7 +62,7 @@ def run(plan_json, inputs, ids):
 
 @pytest.mark.parametrize("base,parts", [("c2_tp1", ["c2_tp2", "c2_tp4"]), ("c2x_tp1", ["c2x_tp2", "c2x_tp8"]),
                                         ("c1l_dp1", ["c1l_dp2"]),
-                                        ("c4_ref1", ["c4_coshard4"]), ("c5_ref1", ["c5_3f1b"]),
+                                        ("c4_ref1", ["c4_coshard4_dp8"]), ("c5_ref1", ["c5_3f1b_dap"]),
                                         ("c3_ref1", ["c3_pp4dp2"])])
 def test_partition_invariance_at_full_size(base, parts):
     plan0, _ = bench.load_plan(base)
