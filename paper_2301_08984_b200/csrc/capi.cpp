@@ -263,9 +263,7 @@ int planc_b200_ptensor_shape(planc_b200_exec* h, int ptensor, int64_t* shape, in
 int planc_b200_get_output(planc_b200_exec* h, int ptensor, double* out, int64_t capacity) {
   return guarded([&] {
     if (!h || !out) throw UsageError("planc_b200_get_output: null argument");
-    HostTensor t = h->ex->get_output(ptensor);
-    if (static_cast<std::int64_t>(t.data.size()) > capacity) throw UsageError("output buffer too small");
-    std::memcpy(out, t.data.data(), t.data.size() * sizeof(double));
+    h->ex->get_output_into(ptensor, out, capacity);
   });
 }
 

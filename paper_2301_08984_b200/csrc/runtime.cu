@@ -7,6 +7,7 @@
 #include <set>
 #include <sstream>
 #include <stdexcept>
+#include <thread>
 
 #include "nccl_api.hpp"
 
@@ -85,6 +86,47 @@ struct DeviceGuard {
   }
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
+
+// Host-side parallel loop over [0, n) in contiguous chunks (the float64 <->
+// device-type conversions of the drop-in TensorMap path): one chunk per
+// hardware thread, inline below `min_work` items.
+template <class F>
+void parallel_for(std::int64_t n, std::int64_t work_per_item, F&& f) {
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const std::int64_t T = std::min<std::int64_t>(hw, n);
+  if (T <= 1 || n * work_per_item < (std::int64_t(1) << 16)) {
+    f(std::int64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const std::int64_t chunk = (n + T - 1) / T;
+  for (std::int64_t t = 0; t < T; ++t) {
+    const std::int64_t lo = t * chunk, hi = std::min(n, lo + chunk);
+    if (lo < hi) th.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  for (auto& x : th) x.join();
+}
+
+inline double load_elem(const char* base, DType d, std::int64_t i) {
+  switch (d) {
+    case DType::f32: {
+      float f;
+      std::memcpy(&f, base + 4 * i, 4);
+      return f;
+    }
+    case DType::bf16: {
+      std::uint16_t h;
+      std::memcpy(&h, base + 2 * i, 2);
+      return bf16_to_f32(h);
+    }
+    case DType::i32: {
+      std::int32_t v;
+      std::memcpy(&v, base + 4 * i, 4);
+      return v;
+    }
+  }
+  return 0;
+}
 
 }  // namespace
 
@@ -386,6 +428,7 @@ Executor::~Executor() {
   for (auto e : lane_join_)
     if (e) cudaEventDestroy(e);
   if (comm_) nccl().comm_destroy(static_cast<ncclComm_t>(comm_));
+  if (host_stage_) cudaFreeHost(host_stage_);
   for (void* p : pinned_in_) cudaFreeHost(p);
   for (void* p : pinned_out_) cudaFreeHost(p);
   for (int k = 0; k < 2; ++k) {
@@ -707,46 +750,65 @@ void Executor::build_box_tables() {
   }
 }
 
-void Executor::set_input(int ptensor, const double* data, const std::vector<std::int64_t>& shape) {
-  HostTensor t;
-  t.shape = shape;
-  std::int64_t vol = 1;
-  for (auto e : shape) vol *= e;
-  t.data.assign(data, data + vol);
-  inputs_[ptensor] = std::move(t);
-  inputs_dirty_ = true;
+char* Executor::host_stage(std::int64_t bytes) {
+  if (bytes > host_stage_bytes_) {
+    if (host_stage_) cudaFreeHost(host_stage_);
+    host_stage_ = nullptr;
+    host_stage_bytes_ = 0;
+    ck(cudaMallocHost(&host_stage_, static_cast<std::size_t>(bytes)), "cudaMallocHost (staging)");
+    host_stage_bytes_ = bytes;
+  }
+  return static_cast<char*>(host_stage_);
 }
 
-// Graph-input placement (refexec.cpp:366-376): each view's region of the
-// host pTensor, converted to the device element type.
-void Executor::place_inputs() {
-  if (!inputs_dirty_) return;
+// Graph-input placement (refexec.cpp:366-376 + ConcreteTensor::extract
+// :75-83): each placement buffer of the pTensor receives its view's region,
+// converted to the device element type — rows of the region converted in
+// parallel into pinned staging, one H2D copy per buffer. Placed at once (the
+// caller keeps ownership of `data`); run() checks every input was placed.
+void Executor::set_input(int ptensor, const double* data, const std::vector<std::int64_t>& shape) {
+  bool synced = false;
   for (const auto& b : prog_.buffers) {
-    if (!b.graph_input || !owned_[b.lane]) continue;
-    auto it = inputs_.find(b.ptensor);
-    if (it == inputs_.end()) throw UsageError("run_plan: missing input tensor " + std::to_string(b.ptensor));
+    if (!b.graph_input || !owned_[b.lane] || b.ptensor != ptensor) continue;
     const PTensor& pt = plan_.pt(b.ptensor);
-    if (it->second.shape != pt.shape) {
-      throw UsageError("input tensor " + std::to_string(b.ptensor) + " has the wrong shape");
+    if (shape != pt.shape) throw UsageError("input tensor " + std::to_string(ptensor) + " has the wrong shape");
+    if (!synced) {  // no step in flight may still read the old values
+      for (int g : gpus_) {
+        DeviceGuard dg(g);
+        ck(cudaDeviceSynchronize(), "sync before input placement");
+      }
+      synced = true;
     }
-    std::vector<char> host(b.bytes);
     const int rank = static_cast<int>(b.shape.size());
     std::vector<std::int64_t> gstr(rank, 1);
     for (int d = rank - 2; d >= 0; --d) gstr[d] = gstr[d + 1] * pt.shape[d + 1];
-    std::vector<std::int64_t> idx(rank, 0);
-    for (std::int64_t e = 0; e < b.elems; ++e) {
-      std::int64_t g = 0;
-      for (int d = 0; d < rank; ++d) g += (b.mask.region[d].lo + idx[d]) * gstr[d];
-      put_elem(host.data(), b.dtype, e, it->second.data[g]);
-      for (int d = rank - 1; d >= 0; --d) {
-        if (++idx[d] < b.shape[d]) break;
-        idx[d] = 0;
+    const std::int64_t inner = rank ? b.shape[rank - 1] : 1;
+    const std::int64_t rows = inner ? b.elems / inner : 0;
+    char* host = host_stage(std::max<std::int64_t>(b.bytes, 1));
+    parallel_for(rows, inner, [&](std::int64_t lo, std::int64_t hi) {
+      for (std::int64_t r = lo; r < hi; ++r) {
+        std::int64_t rem = r, g = 0;
+        for (int d = rank - 2; d >= 0; --d) {
+          g += (b.mask.region[d].lo + rem % b.shape[d]) * gstr[d];
+          rem /= b.shape[d];
+        }
+        if (rank) g += b.mask.region[rank - 1].lo;
+        const double* src = data + g;
+        const std::int64_t e0 = r * inner;
+        for (std::int64_t j = 0; j < inner; ++j) put_elem(host, b.dtype, e0 + j, src[j]);
       }
-    }
+    });
     DeviceGuard dg(lanes_[b.lane].gpu);
-    ck(cudaMemcpy(buf_ptr(b.id), host.data(), b.bytes, cudaMemcpyHostToDevice), "input placement");
+    ck(cudaMemcpy(buf_ptr(b.id), host, b.bytes, cudaMemcpyHostToDevice), "input placement");
   }
-  inputs_dirty_ = false;
+  placed_.insert(ptensor);
+}
+
+void Executor::place_inputs() {
+  for (const auto& b : prog_.buffers) {
+    if (b.graph_input && owned_[b.lane] && !placed_.count(b.ptensor))
+      throw UsageError("run_plan: missing input tensor " + std::to_string(b.ptensor));
+  }
 }
 
 void Executor::launch_instr(const Instr& in, cudaStream_t s) {
@@ -1302,56 +1364,79 @@ std::vector<int> Executor::output_ids() const {
 // producer pieces are read back and reconstructed into the full tensor on
 // the host in double, like the reference returns them.
 HostTensor Executor::get_output(int ptensor) {
-  const std::vector<int>* bufs = nullptr;
-  for (const auto& o : prog_.outputs)
-    if (o.first == ptensor) bufs = &o.second;
-  if (!bufs) throw UsageError("ptensor " + std::to_string(ptensor) + " is not a plan output");
-  for (auto& l : lanes_) {
-    DeviceGuard dg(l.gpu);
-    ck(cudaDeviceSynchronize(), "sync before readback");
-  }
   const PTensor& pt = plan_.pt(ptensor);
   HostTensor out;
   out.shape = pt.shape;
   out.data.assign(pt.volume(), 0.0);
+  get_output_into(ptensor, out.data.data(), static_cast<std::int64_t>(out.data.size()));
+  return out;
+}
+
+// The pieces are read back through pinned staging and reconstructed (same
+// cells as every adapter, reconstruct_cells) in parallel over cell rows.
+void Executor::get_output_into(int ptensor, double* out, std::int64_t capacity) {
+  const std::vector<int>* bufs = nullptr;
+  for (const auto& o : prog_.outputs)
+    if (o.first == ptensor) bufs = &o.second;
+  if (!bufs) throw UsageError("ptensor " + std::to_string(ptensor) + " is not a plan output");
+  const PTensor& pt = plan_.pt(ptensor);
+  if (pt.volume() > capacity) throw UsageError("output buffer too small");
+  for (auto& l : lanes_) {
+    DeviceGuard dg(l.gpu);
+    ck(cudaDeviceSynchronize(), "sync before readback");
+  }
   Mask full;
   for (auto e : pt.shape) full.region.push_back({0, e});
   std::vector<std::pair<const Mask*, int>> pieces;
-  std::map<int, std::vector<char>> raw;
+  std::map<int, std::int64_t> off;
+  std::int64_t total = 0;
   for (int b : *bufs) {
     const BufferDesc& bd = prog_.buffers[b];
     if (!readable(bd.lane)) {
       throw UsageError("ptensor " + std::to_string(ptensor) + " has pieces on another rank; read buffers instead");
     }
     pieces.push_back({&bd.mask, b});
-    std::vector<char> r(bd.bytes);
+    off[b] = total;
+    total += (bd.bytes + 255) / 256 * 256;
+  }
+  char* stage = host_stage(std::max<std::int64_t>(total, 1));
+  for (int b : *bufs) {
+    const BufferDesc& bd = prog_.buffers[b];
     DeviceGuard dg(lanes_[bd.lane].gpu);
-    ck(cudaMemcpy(r.data(), buf_ptr(b), bd.bytes, cudaMemcpyDeviceToHost), "readback");
-    raw[b] = std::move(r);
+    ck(cudaMemcpy(stage + off[b], buf_ptr(b), bd.bytes, cudaMemcpyDeviceToHost), "readback");
   }
   auto cells = reconstruct_cells(full, pt.shape, pieces, prog_.buffers, opt_.value_split_extension,
                                  "output " + std::to_string(ptensor));
   for (const auto& c : cells) {
-    std::int64_t n = c.elems();
-    std::vector<std::int64_t> idx(c.rank, 0);
-    for (std::int64_t e = 0; e < n; ++e) {
-      std::int64_t doff = c.dst_offset;
-      for (int d = 0; d < c.rank; ++d) doff += idx[d] * c.dst_strides[d];
-      double v = 0;
-      for (const auto& t : c.terms) {
-        std::int64_t so = t.offset;
-        for (int d = 0; d < c.rank; ++d) so += idx[d] * t.strides[d];
-        double x = host_elem(raw[t.buffer], prog_.buffers[t.buffer].dtype, so);
-        v = t.add ? v + x : x;
+    const int rank = c.rank;
+    const std::int64_t inner = rank ? c.extents[rank - 1] : 1;
+    const std::int64_t rows = inner ? c.elems() / inner : 0;
+    parallel_for(rows, inner * static_cast<std::int64_t>(c.terms.size()), [&](std::int64_t lo, std::int64_t hi) {
+      for (std::int64_t r = lo; r < hi; ++r) {
+        std::int64_t rem = r, doff = c.dst_offset;
+        std::int64_t idx[kMaxCellRank] = {};
+        for (int d = rank - 2; d >= 0; --d) {
+          idx[d] = rem % c.extents[d];
+          rem /= c.extents[d];
+          doff += idx[d] * c.dst_strides[d];
+        }
+        const std::int64_t dstep = rank ? c.dst_strides[rank - 1] : 1;
+        for (std::int64_t j = 0; j < inner; ++j) out[doff + j * dstep] = 0.0;
+        for (const auto& t : c.terms) {
+          std::int64_t so = t.offset;
+          for (int d = 0; d + 1 < rank; ++d) so += idx[d] * t.strides[d];
+          const std::int64_t sstep = rank ? t.strides[rank - 1] : 1;
+          const char* base = stage + off.at(t.buffer);
+          const DType dt = prog_.buffers[t.buffer].dtype;
+          for (std::int64_t j = 0; j < inner; ++j) {
+            const double x = load_elem(base, dt, so + j * sstep);
+            double& v = out[doff + j * dstep];
+            v = t.add ? v + x : x;
+          }
+        }
       }
-      out.data[doff] = v;
-      for (int d = c.rank - 1; d >= 0; --d) {
-        if (++idx[d] < c.extents[d]) break;
-        idx[d] = 0;
-      }
-    }
+    });
   }
-  return out;
 }
 
 }  // namespace planc_b200

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <set>
 #include <memory>
 #include <string>
 #include <vector>
@@ -117,6 +118,8 @@ class Executor {
   // (simulate.cpp:373-383): [{device, op, kind, start, end}] in seconds.
   std::string timeline_json();
   HostTensor get_output(int ptensor);
+  // Reassembles a produced pTensor straight into `out` (volume elements).
+  void get_output_into(int ptensor, double* out, std::int64_t capacity);
   // Raw value of one device buffer (a vTensor piece) as doubles.
   std::vector<double> read_buffer(int buffer);
   std::vector<int> output_ids() const;
@@ -205,8 +208,10 @@ class Executor {
   std::vector<int> alias_;  // per buffer: -1, or the buffer whose memory it shares
   std::vector<int> gpus_;  // distinct devices
   std::vector<void*> table_allocs_;
-  std::map<int, HostTensor> inputs_;
-  bool inputs_dirty_ = true;
+  std::set<int> placed_;                // graph inputs placed by set_input
+  void* host_stage_ = nullptr;          // pinned staging for set_input / get_output conversions
+  std::int64_t host_stage_bytes_ = 0;
+  char* host_stage(std::int64_t bytes);
   cudaStream_t origin_ = nullptr;
   cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr;
   std::vector<cudaEvent_t> lane_join_;
