@@ -47,8 +47,18 @@ def plan_name(config: str, n: int) -> str:
     pipeline (c3: pp4 x dp2), co-shard x DP (c4: dp8 x co-shard 4) and 3F1B
     x DAP (c5: 4 stages x dap 2) plans have 8 lanes — with fewer GPUs, lanes
     share GPUs (round robin)."""
-    return {"c2": f"c2_tp{n}", "c2x": f"c2x_tp{n}", "c1l": f"c1l_dp{n}", "c3": "c3_pp4dp2", "c4": "c4_coshard4_dp8",
+    return {"c2": f"c2_tp{n}", "c2x": f"c2x_tp{n}", "c1l": f"c1l_dp{n}", "c3": "c3_pp4dp2_l24", "c4": "c4_coshard4_dp8",
             "c5": "c5_3f1b_dap"}[config]
+
+
+def cpu_plan_name(config: str) -> str:
+    """Reduced-shape twin of the config's plan for the reference CPU executor
+    (SURVEY §8d). c3's 24-layer plan has none (the reference needs ~1 min per
+    step for its 26704 tasks at any shape): the 4-layer stack under the same
+    1F1B pp4 x dp2 strategy stands in."""
+    if config == "c3":
+        return "c3_pp4dp2_cpu"
+    return plan_name(config, 1) + "_cpu" + ("_standin" if config == "c2x" else "")
 
 
 def load_plan(name):
@@ -196,13 +206,14 @@ def cpu_baseline(config: str, budget_s: float = 20.0):
     reduced-shape plan of the same graph, bounded in time."""
     from oracle import refpy  # checker / baseline only
 
-    name = plan_name(config, 1) + "_cpu"
+    name = cpu_plan_name(config)
     note = ""
     if config == "c2x":
         # The reference executor has no layernorm / softmax / GELU: it runs the
         # stand-in plan (identity / mul in their place, same data flow).
-        name += "_standin"
         note = "; stand-in plan: identity/mul where the extension has LN/softmax/GELU"
+    if config == "c3":
+        note = "; 4-layer stack (the 24-layer plan takes the reference ~1 min per step)"
     plan, meta = load_plan(name)
     inputs = synthetic_inputs(plan, 1)
     _, secs = refpy.run_plan(plan, inputs, iters=1)
@@ -231,7 +242,7 @@ def run_reference_arm(args, rank, world):
 
     from oracle import refpy  # reference arm only
 
-    name = plan_name(args.config, 1) + "_cpu" + ("_standin" if args.config == "c2x" else "")
+    name = cpu_plan_name(args.config)
     plan, meta = load_plan(name)
     inputs = synthetic_inputs(plan, 1)
     threads = os.cpu_count() or 1
@@ -326,6 +337,10 @@ def main():
     peaks = measured_peaks()
     nlanes = len(json.loads(plan)["lanes"])
     transport = None
+    # C3 at 24 layers holds ~190 GiB of step buffers when nothing is freed:
+    # one process driving every lane runs it honouring the plan's frees
+    # (REUSE_MEMORY, ~80 GiB). One process per GPU holds 1/N of the lanes.
+    reuse_flags = pb.REUSE_MEMORY if (args.config == "c3" and not dist) else 0
     if dist:
         # One process per GPU: this rank runs lanes l with l % world == rank
         # on its local GPU; cross-rank pieces move over NVLink (peer memory or
@@ -361,7 +376,7 @@ def main():
             dist.broadcast_object_list(box, src=0)
             ex = pb.Executor(plan, rank=rank, world=world, lane_rank=lane_rank, local_gpu=local, nccl_id=box[0])
     else:
-        ex = pb.Executor(plan, lane_gpus=list(range(n)))
+        ex = pb.Executor(plan, lane_gpus=list(range(n)), flags=reuse_flags)
     # each rank generates and binds only the inputs its lanes place
     inputs = synthetic_inputs(plan, only=set(ex.input_ids()))
     ex.set_inputs(inputs)
@@ -396,7 +411,7 @@ def main():
     sustained = {"ms_per_step": sus_ms, "steps": sus_iters, "seconds": sus_ms * sus_iters / 1e3,
                  "value": meta["samples_per_step"] / (sus_ms / 1e3), "clocks": clk2.summary()}
     dropin = None
-    if not dist:  # one process owns every lane: the whole TensorMap round trip
+    if not dist and not reuse_flags:  # one process owns every lane: the whole TensorMap round trip
         dropin = dropin_e2e(ex, inputs, meta["samples_per_step"])
     prof = [ex.profile() for _ in range(3)]  # every rank: exchange steps pair up
     if dist:
@@ -500,6 +515,8 @@ def main():
                        f"{st['device_bytes'] / 2**30:.1f} GiB > 126 MB L2 (no flush needed)",
                        "transport": (("peer memory (CUDA IPC over NVLink, device flags)" if transport == "peer"
                                       else transport) if dist else "single process"),
+                       "memory": ("timed-mode reuse of freed buffers (REUSE_MEMORY)" if reuse_flags
+                                  else "every buffer resident for the step"),
                        "lanes": st["num_lanes"], "tasks": st["num_tasks"], "launch": (
                            "CUDA graph" if st["graph_captured"] else "eager")},
             "roofline": roof,
@@ -527,7 +544,7 @@ def main():
         if not args.no_cpu_baseline and n == 1:
             try:
                 cb, _ = cpu_baseline(args.config)
-                small, smeta = load_plan(plan_name(args.config, 1) + "_cpu")
+                small, smeta = load_plan(cpu_plan_name(args.config).replace("_standin", ""))
                 with pb.Executor(small, lane_gpus=[0]) as sx:
                     sx.set_inputs(synthetic_inputs(small, 1))
                     sx.run(3)

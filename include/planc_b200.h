@@ -49,6 +49,10 @@ extern "C" {
                                            epilogue — same bits as the separate kernel */
 #define PLANC_B200_FUSE_ACT 0x400u      /* also run GELU / GELU-grad in the producing GEMM's epilogue
                                            (opt-in: same bits, measured slower on C2x) */
+#define PLANC_B200_REUSE_MEMORY 0x800u  /* timed mode: the bytes of every buffer the plan frees (free tasks,
+                                           refexec.cpp:416-417) are reused within the step once all its uses
+                                           are ordered before the new writer; outputs whose bytes were reused
+                                           are unavailable (UsageError). Single-process executor only */
 #define PLANC_B200_NO_FUSION 0x80u      /* every elementwise op its own kernel (no epilogue fusion) */
 #define PLANC_B200_NO_SCATTER 0x200u    /* all-reduce partials stored whole by their GEMM and pulled by the
                                            reduce-scatter phase (default: a GEMM whose output only feeds an

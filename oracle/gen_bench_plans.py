@@ -91,6 +91,22 @@ C5_SHAPE = (4, (32768, 256), (65536, 128), 4)
 C5_SPEC = dict(strategy="threef1b_dap", devices=8, stages=4, micro_batches=4, inner_dp=2)
 
 
+def gen_c3_l24():
+    """C3 at the GPT-3 1.3B shape: 24 layers (6 per stage), H=2048, 16 x 2048
+    tokens, 1F1B S=4 x inner DP 2, K=8. Its step holds ~190 GiB of buffers
+    when nothing is freed; the bench runs it with REUSE_MEMORY (the plan's
+    free tasks honoured: ~80 GiB)."""
+    # (no reduced-shape twin: the reference executor needs ~1 min per step
+    # for the 26704-task plan at any shape — per-task lookups, SURVEY fact 10;
+    # the CPU baseline of c3 runs c3_pp4dp2_cpu)
+    for L, T, H, tag in ((24, 32768, 2048, ""),):
+        g = docs.dumps(docs.gpt_stack_doc(L, T, H, elem_size=2))
+        plan = refpy.compile_plan(g, strategy="1f1b", devices=8, stages=4, micro_batches=8, inner_dp=2)
+        write(f"c3_pp4dp2_l24{tag}", g, plan, dict(config="c3", layers=L, tokens=T, hidden=H, stages=4, inner_dp=2,
+                                                    micro_batches=8, dtype="bf16", samples_per_step=T,
+                                                    sample="token (row of X)"))
+
+
 def gen_c4():
     for T, H, tag in (C4_SHAPE + ("",), (8 * 32, 64, "_cpu")):
         g = docs.dumps(docs.swin_stage_doc(T, H))
@@ -126,7 +142,7 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     only = set(sys.argv[1:])
     if only:
-        for name, fn in (("c2x", gen_c2x), ("c4", gen_c4), ("c5", gen_c5)):
+        for name, fn in (("c2x", gen_c2x), ("c3l24", gen_c3_l24), ("c4", gen_c4), ("c5", gen_c5)):
             if name in only:
                 fn()
         if "ref1" in only:
@@ -149,6 +165,7 @@ def main():
         write(f"c3_pp4dp2{tag}", g, plan, dict(config="c3", layers=L, tokens=T, hidden=H, stages=4, inner_dp=2,
                                                 micro_batches=8, dtype="bf16", samples_per_step=T,
                                                 sample="token (row of X)"))
+    gen_c3_l24()
     gen_c4()
     gen_c5()
     gen_ref1()

@@ -43,6 +43,7 @@ NO_FUSION = 0x80
 NO_ALIAS = 0x100
 NO_SCATTER = 0x200
 FUSE_ACT = 0x400
+REUSE_MEMORY = 0x800
 
 
 class PlancError(RuntimeError):

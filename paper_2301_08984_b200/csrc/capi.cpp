@@ -66,6 +66,7 @@ ExecOptions exec_options(uint32_t flags) {
   opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
   opt.alias_copies = (flags & PLANC_B200_NO_ALIAS) == 0;
   opt.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0;
+  opt.reuse_memory = (flags & PLANC_B200_REUSE_MEMORY) != 0;
   return opt;
 }
 
@@ -381,7 +382,29 @@ int planc_b200_describe(const char* plan_json, uint32_t flags, char** json_out) 
     ProgramOptions po = describe_options(flags);
     ExecutionPlan plan = load_plan(plan_json);
     Program p = build_program(plan, po);
-    *json_out = dup(p.describe_json());
+    std::string js = p.describe_json();
+    if (flags & PLANC_B200_REUSE_MEMORY) {
+      // The timed-mode memory plan with every lane in this process, 4
+      // streams per lane, no same-GPU aliases.
+      std::vector<int> lane(p.instrs.size());
+      for (const auto& in : p.instrs) lane[in.id] = in.lane;
+      const std::vector<int> streams = assign_streams(p, lane, 4);
+      MemoryPlan mp = plan_memory(p, plan, lane, streams, 4, {});
+      std::ostringstream os;
+      os << ",\"memory_plan\":{\"bytes_before\":" << mp.bytes_before << ",\"bytes_after\":" << mp.bytes_after
+         << ",\"reused\":" << mp.reused << ",\"streams\":[";
+      for (std::size_t i = 0; i < streams.size(); ++i) os << (i ? "," : "") << streams[i];
+      os << "],\"offset\":[";
+      for (std::size_t i = 0; i < mp.offset.size(); ++i) os << (i ? "," : "") << mp.offset[i];
+      os << "],\"lane_bytes\":[";
+      for (std::size_t i = 0; i < mp.lane_bytes.size(); ++i) os << (i ? "," : "") << mp.lane_bytes[i];
+      os << "],\"overwritten\":[";
+      for (std::size_t i = 0; i < mp.overwritten.size(); ++i) os << (i ? "," : "") << (mp.overwritten[i] ? 1 : 0);
+      os << "]}}";
+      js.pop_back();
+      js += os.str();
+    }
+    *json_out = dup(js);
   });
 }
 

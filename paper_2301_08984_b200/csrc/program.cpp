@@ -1546,3 +1546,206 @@ std::string Program::describe_json() const {
 }
 
 }  // namespace planc_b200
+
+namespace planc_b200 {
+
+std::vector<int> assign_streams(const Program& p, const std::vector<int>& exec_lane, int ns) {
+  ns = std::max(1, ns);
+  std::vector<int> stream(p.instrs.size(), 0);
+  std::vector<std::vector<int>> last(p.num_lanes, std::vector<int>(ns, -1));
+  for (int id : p.issue_order) {
+    const int el = exec_lane[id];
+    if (el < 0) continue;
+    const Instr& in = p.instrs[id];
+    int pick = -1, best_dep = -1;
+    for (int s = 0; s < ns; ++s) {
+      const int l = last[el][s];
+      if (l >= 0 && l > best_dep && std::find(in.deps.begin(), in.deps.end(), l) != in.deps.end()) {
+        best_dep = l;
+        pick = s;
+      }
+    }
+    if (pick < 0) {
+      pick = 0;
+      for (int s = 1; s < ns; ++s)
+        if (last[el][s] < last[el][pick]) pick = s;
+    }
+    stream[id] = pick;
+    last[el][pick] = id;
+  }
+  return stream;
+}
+
+namespace {
+
+// Every buffer an instruction touches: (buffer, is_write).
+template <class F>
+void for_each_use(const Instr& in, F&& f) {
+  for (int b : in.in_bufs) f(b, false);
+  for (int b : in.out_bufs) f(b, true);
+  for (const auto& c : in.cells)
+    for (const auto& t : c.terms) f(t.buffer, false);
+  for (const auto& fe : in.fused) {
+    for (int b : fe.in_bufs) f(b, false);
+    if (fe.out_buf >= 0) f(fe.out_buf, true);
+  }
+  for (const auto& x : in.xfers) {
+    f(x.src, false);
+    f(x.dst, true);
+  }
+}
+
+constexpr std::int64_t kAlign = 256;
+std::int64_t aligned(std::int64_t b) { return (std::max<std::int64_t>(b, 1) + kAlign - 1) / kAlign * kAlign; }
+
+}  // namespace
+
+MemoryPlan plan_memory(const Program& p, const ExecutionPlan& plan, const std::vector<int>& exec_lane,
+                       const std::vector<int>& exec_stream, int ns, const std::vector<int>& alias) {
+  const int nb = static_cast<int>(p.buffers.size());
+  const int ni = static_cast<int>(p.instrs.size());
+  ns = std::max(1, ns);
+  const int S = p.num_lanes * ns;
+  auto root = [&](int b) {
+    while (!alias.empty() && alias[b] >= 0) b = alias[b];
+    return b;
+  };
+  MemoryPlan mp;
+  mp.offset.assign(nb, 0);
+  for (int b = 0; b < nb; ++b) mp.offset[b] = p.buffers[b].offset;
+  mp.lane_bytes = p.lane_arena_bytes;
+  mp.overwritten.assign(nb, false);
+  for (auto v : p.lane_arena_bytes) mp.bytes_before += v;
+
+  // Vector clocks: done[i][s] = highest stream-s sequence number known
+  // complete when instruction i completes.
+  std::vector<int> sid(ni, -1), seq(ni, -1), prev(ni, -1);
+  {
+    std::vector<int> count(S, 0), last(S, -1);
+    for (int id : p.issue_order) {
+      if (exec_lane[id] < 0) continue;
+      sid[id] = exec_lane[id] * ns + exec_stream[id];
+      seq[id] = count[sid[id]]++;
+      prev[id] = last[sid[id]];
+      last[sid[id]] = id;
+    }
+  }
+  std::vector<std::int32_t> done(static_cast<std::size_t>(ni) * S, -1);
+  auto start_clock = [&](int id, std::vector<std::int32_t>& vc) {
+    vc.assign(S, -1);
+    auto merge = [&](int d) {
+      if (d < 0 || sid[d] < 0) return;
+      const std::int32_t* v = &done[static_cast<std::size_t>(d) * S];
+      for (int s = 0; s < S; ++s) vc[s] = std::max(vc[s], v[s]);
+    };
+    merge(prev[id]);
+    for (int d : p.instrs[id].deps) merge(d);
+  };
+  std::vector<std::int32_t> vc;
+  for (int id : p.issue_order) {
+    if (sid[id] < 0) continue;
+    start_clock(id, vc);
+    vc[sid[id]] = seq[id];
+    std::copy(vc.begin(), vc.end(), done.begin() + static_cast<std::size_t>(id) * S);
+  }
+
+  // Which buffers may release their bytes.
+  std::vector<bool> freed(nb, false);
+  for (const auto& op : plan.ops) {
+    if (op.kind != OpKind::free_buffer) continue;
+    const int vt = op.free_vtensor;
+    if (vt >= 0 && vt < static_cast<int>(p.vt_buffer.size()) && p.vt_buffer[vt] >= 0) freed[root(p.vt_buffer[vt])] = true;
+  }
+  std::set<int> consumed;
+  for (const auto& op : plan.ops)
+    for (int v : op.inputs) consumed.insert(plan.vt(v).ptensor);
+  std::vector<bool> keep(nb, false);
+  for (const auto& [pt, bufs] : p.outputs) {
+    if (consumed.count(pt)) continue;
+    for (int b : bufs) keep[root(b)] = true;  // terminal results survive the step
+  }
+  // Uses and writers per root buffer; release vector = last use per stream.
+  std::vector<std::vector<int>> writers(nb);
+  std::vector<std::map<int, int>> release(nb);
+  std::vector<bool> used(nb, false);
+  for (int id = 0; id < ni; ++id) {
+    if (sid[id] < 0) continue;
+    for_each_use(p.instrs[id], [&](int b, bool w) {
+      const int r = root(b);
+      used[r] = true;
+      if (w && r == b) writers[r].push_back(id);
+      int& q = release[r][sid[id]];
+      q = std::max(q, seq[id] + 1) ;
+    });
+  }
+  auto planned = [&](int b) {
+    const BufferDesc& d = p.buffers[b];
+    return root(b) == b && !d.dead && !d.graph_input && !keep[b] && used[b] &&
+           !writers[b].empty() && (freed[b] || d.vt < 0);
+  };
+  // Lay out: permanent buffers first (graph inputs, kept / never-freed
+  // results), then planned buffers by first write in issue order, best fit
+  // among blocks whose occupant is released before every writer.
+  struct Block {
+    std::int64_t off, size;
+    int occupant;
+  };
+  std::vector<std::vector<Block>> blocks(p.num_lanes);
+  std::vector<std::int64_t> top(p.num_lanes, 0);
+  for (int b = 0; b < nb; ++b) {
+    const BufferDesc& d = p.buffers[b];
+    if (root(b) != b || d.dead || planned(b)) continue;
+    mp.offset[b] = top[d.lane];
+    top[d.lane] += aligned(d.bytes);
+  }
+  std::vector<bool> placed(nb, false);
+  std::vector<std::vector<std::int32_t>> wclock;
+  for (int id : p.issue_order) {
+    if (sid[id] < 0) continue;
+    std::vector<int> outs;
+    for_each_use(p.instrs[id], [&](int b, bool w) {
+      if (w && b == root(b) && planned(b) && !placed[b]) outs.push_back(b);
+    });
+    for (int c : outs) {
+      if (placed[c]) continue;
+      placed[c] = true;
+      const BufferDesc& d = p.buffers[c];
+      const std::int64_t need = aligned(d.bytes);
+      wclock.clear();
+      for (int w : writers[c]) {
+        start_clock(w, vc);
+        wclock.push_back(vc);
+      }
+      int best = -1;
+      for (int k = 0; k < static_cast<int>(blocks[d.lane].size()); ++k) {
+        const Block& bl = blocks[d.lane][k];
+        if (bl.size < need || (best >= 0 && bl.size >= blocks[d.lane][best].size)) continue;
+        bool ok = true;
+        for (const auto& [s, q] : release[bl.occupant]) {
+          for (const auto& wc : wclock) ok = ok && wc[s] >= q - 1;
+          if (!ok) break;
+        }
+        if (ok) best = k;
+      }
+      if (best >= 0) {
+        Block& bl = blocks[d.lane][best];
+        mp.overwritten[bl.occupant] = true;
+        mp.offset[c] = bl.off;
+        if (bl.size - need >= kAlign) blocks[d.lane].push_back({bl.off + need, bl.size - need, bl.occupant});
+        Block& nbk = blocks[d.lane][best];  // (push_back may have moved it)
+        nbk.size = need;
+        nbk.occupant = c;
+        ++mp.reused;
+      } else {
+        mp.offset[c] = top[d.lane];
+        blocks[d.lane].push_back({top[d.lane], need, c});
+        top[d.lane] += need;
+      }
+    }
+  }
+  for (int l = 0; l < p.num_lanes; ++l) mp.lane_bytes[l] = top[l];
+  for (auto v : mp.lane_bytes) mp.bytes_after += v;
+  return mp;
+}
+
+}  // namespace planc_b200

@@ -252,6 +252,29 @@ PeerSync peer_sync_schedule(const Program& p, const std::vector<int>& lane_rank)
 // lanes other ranks own stay in the program (the caller skips them).
 Program localize(const Program& global, const std::vector<int>& lane_rank);
 
+// Stream of each instruction within its lane (exec_lane[i] < 0: not run in
+// this process): continue the stream of the most recent dependency that
+// ended a stream's chain, else take the least recently used of `ns` streams.
+std::vector<int> assign_streams(const Program& p, const std::vector<int>& exec_lane, int ns);
+
+// Static memory plan of one step for timed mode (the plan's `free` tasks,
+// refexec.cpp:416-417 / insert_frees materialize.cpp:340-465, made real):
+// a buffer the plan frees (or an executor-internal buffer) may hand its
+// arena bytes to a later buffer once every use of it — reads and writes,
+// through aliases, on any lane's stream — is ordered before every write of
+// the newcomer by the step's dependency edges and stream order (vector
+// clocks over the (lane, stream) queues). Graph inputs, terminal outputs
+// and buffers the plan never frees keep their own bytes.
+struct MemoryPlan {
+  std::vector<std::int64_t> offset;      // per buffer: byte offset in its lane arena
+  std::vector<std::int64_t> lane_bytes;  // per lane: arena size
+  std::vector<bool> overwritten;         // per buffer: its bytes are reused later in the step
+  std::int64_t bytes_before = 0, bytes_after = 0;
+  int reused = 0;                        // buffers placed in released bytes
+};
+MemoryPlan plan_memory(const Program& p, const ExecutionPlan& plan, const std::vector<int>& exec_lane,
+                       const std::vector<int>& exec_stream, int ns, const std::vector<int>& alias);
+
 // Reconstruct-as-cells (refexec.cpp:102-140): target buffer box from ordered
 // pieces. Exposed for tests.
 std::vector<Cell> reconstruct_cells(const Mask& target, const std::vector<std::int64_t>& target_shape,

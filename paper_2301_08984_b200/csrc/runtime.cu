@@ -232,34 +232,14 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   // most recent dependency that ended a stream's chain, else take the least
   // recently used stream. Only data dependencies (and sync edges) then order
   // a lane's work, via events between streams.
+  int nstreams = 1;
   {
     int want = opt_.streams_per_lane;
     if (const char* e = std::getenv("PLANC_B200_STREAMS")) {
       if (want > 1) want = std::atoi(e);  // A/B of the stream count (SERIAL_LANES keeps 1)
     }
-    const int ns = std::max(1, std::min(want, kLaneStreams));
-    exec_stream_.assign(prog_.instrs.size(), 0);
-    std::vector<std::vector<int>> last(prog_.num_lanes, std::vector<int>(ns, -1));
-    for (int id : prog_.issue_order) {
-      const int el = exec_lane_[id];
-      if (el < 0) continue;
-      const Instr& in = prog_.instrs[id];
-      int pick = -1, best_dep = -1;
-      for (int s = 0; s < ns; ++s) {
-        const int l = last[el][s];
-        if (l >= 0 && l > best_dep && std::find(in.deps.begin(), in.deps.end(), l) != in.deps.end()) {
-          best_dep = l;
-          pick = s;
-        }
-      }
-      if (pick < 0) {
-        pick = 0;
-        for (int s = 1; s < ns; ++s)
-          if (last[el][s] < last[el][pick]) pick = s;
-      }
-      exec_stream_[id] = pick;
-      last[el][pick] = id;
-    }
+    nstreams = std::max(1, std::min(want, kLaneStreams));
+    exec_stream_ = assign_streams(prog_, exec_lane_, nstreams);
   }
   if (rank_mode_ && !peer_) {
     DeviceGuard dg(rc_.local_gpu);
@@ -282,6 +262,17 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
       else ck(e, "cudaDeviceEnablePeerAccess");
     }
+  }
+  irt_.resize(prog_.instrs.size());
+  if (!peer_) plan_aliases();  // (before the memory plan: an alias extends its source's lifetime)
+  if (opt_.reuse_memory) {
+    // Timed mode honouring the plan's frees: released bytes are reused
+    // within the step (single process: every reader's stream is ours).
+    if (rank_mode_) throw UsageError("REUSE_MEMORY needs the single-process executor");
+    MemoryPlan mp = plan_memory(prog_, plan_, exec_lane_, exec_stream_, nstreams, alias_);
+    for (std::size_t b = 0; b < prog_.buffers.size(); ++b) prog_.buffers[b].offset = mp.offset[b];
+    prog_.lane_arena_bytes = mp.lane_bytes;
+    overwritten_ = mp.overwritten;
   }
   for (int l = 0; l < prog_.num_lanes; ++l) {
     if (!owned_[l]) continue;
@@ -356,7 +347,6 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
     lane_mapped_.assign(prog_.num_lanes, false);
     // Box tables need every rank's arena: built by peer_import.
   } else {
-    plan_aliases();
     build_box_tables();
   }
   kernels_per_step_ = 0;
@@ -451,6 +441,11 @@ bool Executor::gemm_streamk_ok(int lane) const {
   for (int l = 0; l < prog_.num_lanes; ++l)
     if (owned_[l] && lanes_[l].gpu == lanes_[lane].gpu) ++sharing;
   return sharing == 1;
+}
+
+bool Executor::released(int b) const {
+  while (!alias_.empty() && alias_[b] >= 0) b = alias_[b];
+  return !overwritten_.empty() && overwritten_[b];
 }
 
 void* Executor::buf_ptr(int b) const {
@@ -1334,6 +1329,7 @@ std::vector<double> Executor::read_buffer(int buffer) {
   const BufferDesc& bd = prog_.buffers[buffer];
   peer_check_ready();
   if (!readable(bd.lane)) throw UsageError("buffer " + std::to_string(buffer) + " lives on another rank");
+  if (released(buffer)) throw UsageError("buffer " + std::to_string(buffer) + " was reused in the step (REUSE_MEMORY)");
   DeviceGuard dg(lanes_[bd.lane].gpu);
   for (int g : gpus_) {
     cudaSetDevice(g);
@@ -1394,6 +1390,10 @@ void Executor::get_output_into(int ptensor, double* out, std::int64_t capacity) 
     const BufferDesc& bd = prog_.buffers[b];
     if (!readable(bd.lane)) {
       throw UsageError("ptensor " + std::to_string(ptensor) + " has pieces on another rank; read buffers instead");
+    }
+    if (released(b)) {
+      throw UsageError("ptensor " + std::to_string(ptensor) +
+                       " was freed by the plan and its bytes reused in the step (REUSE_MEMORY)");
     }
     pieces.push_back({&bd.mask, b});
     off[b] = total;

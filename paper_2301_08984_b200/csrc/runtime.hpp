@@ -54,6 +54,7 @@ struct ExecOptions {
   bool group_gemms = true;              // same-shape independent GEMMs in one grouped launch
   bool alias_copies = true;             // same-GPU whole-buffer copies (recv, identity) become aliases
   bool scatter_allreduce = true;        // all-reduce partials leave the GEMM epilogue as reduce-scatter slices
+  bool reuse_memory = false;            // timed mode: bytes the plan frees are reused within the step
 };
 
 // ProgramOptions as the executor uses them: epilogue fusion only for GEMMs
@@ -158,6 +159,7 @@ class Executor {
   };
 
   void* buf_ptr(int b) const;
+  bool released(int b) const;  // REUSE_MEMORY: bytes taken over by a later buffer
   void plan_aliases();
   bool gemm_streamk_ok(int lane) const;  // the lane has its GPU to itself
   cudaStream_t stream_of(const Instr& in) const;
@@ -208,6 +210,7 @@ class Executor {
   std::vector<int> alias_;  // per buffer: -1, or the buffer whose memory it shares
   std::vector<int> gpus_;  // distinct devices
   std::vector<void*> table_allocs_;
+  std::vector<bool> overwritten_;       // REUSE_MEMORY: buffers whose bytes a later buffer takes
   std::set<int> placed_;                // graph inputs placed by set_input
   void* host_stage_ = nullptr;          // pinned staging for set_input / get_output conversions
   std::int64_t host_stage_bytes_ = 0;

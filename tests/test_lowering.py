@@ -399,3 +399,105 @@ def test_opt_in_gelu_epilogue_fusion():
     out = run_program(desc, plan, g["inputs"])
     ok, msg = pb.compare_outputs(base, out, 0.0, normwise=True)
     assert ok, msg
+
+
+def _happens_before_clocks(desc, ns=4):
+    """Vector clocks of the executed step, recomputed here from the lowered
+    program: stream FIFO order (describe's stream assignment) plus every
+    dependency edge. done[i][s] = last sequence number of stream s complete
+    when instruction i completes."""
+    instrs = desc["instrs"]
+    streams = desc["memory_plan"]["streams"]
+    S = desc["num_lanes"] * ns
+    sid = {}
+    seq = {}
+    count = [0] * S
+    last = [-1] * S
+    prev = {}
+    for i in desc["issue_order"]:
+        s = instrs[i]["lane"] * ns + streams[i]
+        sid[i], seq[i], prev[i] = s, count[s], last[s]
+        count[s] += 1
+        last[s] = i
+    done = np.full((len(instrs), S), -1, dtype=np.int64)
+    for i in desc["issue_order"]:
+        v = np.full(S, -1, dtype=np.int64)
+        for d in instrs[i]["deps"] + ([prev[i]] if prev[i] >= 0 else []):
+            v = np.maximum(v, done[d])
+        v[sid[i]] = seq[i]
+        done[i] = v
+    return sid, seq, done, prev
+
+
+def _uses(ins):
+    for b in ins["in"]:
+        yield b, False
+    for b in ins["out"]:
+        yield b, True
+    for c in ins["cells"]:
+        for t in c["terms"]:
+            yield t["buf"], False
+    for f in ins["fused"]:
+        for b in f["in"]:
+            yield b, False
+        yield f["out"], True
+
+
+@pytest.mark.parametrize("name", ["c5_3f1b_dap", "c4_coshard4_dp8", "c2_tp1"])
+def test_timed_memory_plan_never_overlaps_live_buffers(name):
+    """REUSE_MEMORY (the plan's free tasks made real): two buffers sharing
+    arena bytes must be ordered — every use of one happens before every write
+    of the other, by dependency edges and stream order — and terminal
+    results / graph inputs are never overwritten. Checked independently of
+    the C++ planner from the lowered program."""
+    import bench
+
+    plan, _ = bench.load_plan(name)
+    desc = pb.describe(plan, flags=pb.REUSE_MEMORY)
+    mp = desc["memory_plan"]
+    assert mp["reused"] > 0 and mp["bytes_after"] < mp["bytes_before"]
+    sid, seq, done, prev = _happens_before_clocks(desc)
+    uses, writes = {}, {}
+    for ins in desc["instrs"]:
+        for b, w in _uses(ins):
+            uses.setdefault(b, []).append(ins["id"])
+            if w:
+                writes.setdefault(b, []).append(ins["id"])
+
+    def start_clock(i):
+        ins = desc["instrs"][i]
+        v = np.full(done.shape[1], -1, dtype=np.int64)
+        for d in ins["deps"] + ([prev[i]] if prev[i] >= 0 else []):
+            v = np.maximum(v, done[d])
+        return v
+
+    def before(x, y):  # every use of x completes before every write of y starts
+        clocks = [start_clock(w) for w in writes.get(y, [])]
+        return all(c[sid[u]] >= seq[u] for u in uses.get(x, []) for c in clocks)
+
+    bufs = desc["buffers"]
+    off = mp["offset"]
+    by_lane = {}
+    for b in bufs:
+        if b["dead"] or b["id"] not in uses:
+            continue
+        by_lane.setdefault(b["lane"], []).append(b["id"])
+    checked = 0
+    for lane, ids in by_lane.items():
+        ids.sort(key=lambda b: off[b])
+        for i, x in enumerate(ids):
+            xend = off[x] + bufs[x]["bytes"]
+            for y in ids[i + 1:]:
+                if off[y] >= xend:
+                    break
+                checked += 1
+                assert before(x, y) or before(y, x), (name, x, y)
+                assert not (bufs[x]["graph_input"] or bufs[y]["graph_input"])
+    assert checked >= mp["reused"] // 2
+    # results the step hands back keep their bytes
+    consumed = {v["ptensor"] for o in json.loads(plan)["ops"] for vid in o["inputs"]
+                for v in [next(vv for vv in json.loads(plan)["vtensors"] if vv["id"] == vid)]} if name == "c2_tp1" else None
+    if consumed is not None:
+        for pt, pieces in desc["outputs"]:
+            if pt not in consumed:
+                assert not any(mp["overwritten"][b] for b in pieces)

@@ -239,3 +239,28 @@ def test_reduce_scatter_gemm_epilogue(name):
         assert ok, msg
     for k in outs[0]:
         assert np.array_equal(outs[0][k], outs[pb.NO_SCATTER][k]), k
+
+
+@pytest.mark.parametrize("name", [n for n in golden_cases.names() if golden_cases.load(n)["meta"]["lanes"] > 1])
+def test_timed_mode_memory_reuse(name):
+    """REUSE_MEMORY (the plan's frees honoured within the step): every output
+    whose bytes survive the step is bit-identical to the resident run, the
+    rest raise UsageError instead of returning reused bytes; a second step
+    gives the same bits (released bytes are rewritten before they are read)."""
+    g = golden_cases.load(name)
+    n = len(json.loads(g["plan"])["lanes"])
+    ref, _ = _run(g["plan"], g["inputs"])
+    with pb.Executor(g["plan"], lane_gpus=[0] * n, flags=pb.REUSE_MEMORY) as ex:
+        ex.set_inputs(g["inputs"])
+        for steps in (0, 3):
+            ex.run(steps)
+            kept = 0
+            for pt in ex.output_ids():
+                try:
+                    v = ex.get_output(pt)
+                except pb.UsageError as e:
+                    assert "REUSE_MEMORY" in str(e)
+                    continue
+                assert np.array_equal(v, ref[pt]), pt
+                kept += 1
+            assert kept > 0
