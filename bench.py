@@ -281,11 +281,13 @@ def dropin_e2e(ex, inputs, samples_per_step, steps=2):
     (planc_b200_get_output). Timed on the host clock around whole calls."""
     ids = ex.output_ids()
     h2d = sum(v.nbytes for v in inputs.values())
+    # the caller's TensorMap storage, allocated (and first touched) once
+    outs = {i: np.zeros(ex.shape(i), dtype=np.float64) for i in ids}
 
     def once():
         ex.set_inputs(inputs)
         ex.run(0)
-        return sum(ex.get_output(i).nbytes for i in ids)
+        return sum(ex.get_output(i, outs[i]).nbytes for i in ids)
 
     once()
     t0 = time.perf_counter()
@@ -295,7 +297,8 @@ def dropin_e2e(ex, inputs, samples_per_step, steps=2):
     return {"value": samples_per_step / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms, "steps": steps,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "via": "planc_b200_set_input (float64 TensorMap) -> planc_b200_run -> planc_b200_get_output "
-                   "(every produced pTensor, float64): the reference run_plan contract"}
+                   "(every produced pTensor, float64, into the caller's reused arrays): the reference "
+                   "run_plan contract"}
 
 
 def main():

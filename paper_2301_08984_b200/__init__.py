@@ -275,9 +275,15 @@ class Executor:
         for pid, v in inputs.items():
             self.set_input(int(pid), v)
 
-    def get_output(self, ptensor: int) -> np.ndarray:
+    def get_output(self, ptensor: int, out: np.ndarray = None) -> np.ndarray:
+        """Reassembled value of a produced pTensor (float64). ``out``: a
+        C-contiguous float64 array of the pTensor's shape to fill instead of
+        allocating one (a caller reusing its TensorMap storage across steps)."""
         shp = self.shape(ptensor)
-        out = np.empty(shp, dtype=np.float64)
+        if out is None:
+            out = np.empty(shp, dtype=np.float64)
+        elif out.dtype != np.float64 or out.shape != tuple(shp) or not out.flags.c_contiguous:
+            raise UsageError("get_output: out must be a C-contiguous float64 array of shape %s" % (shp,))
         _check(_load().planc_b200_get_output(self._h, ptensor, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                              out.size))
         return out
