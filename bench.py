@@ -284,18 +284,28 @@ def dropin_e2e(ex, inputs, samples_per_step, steps=2):
     # the caller's TensorMap storage, allocated (and first touched) once
     outs = {i: np.zeros(ex.shape(i), dtype=np.float64) for i in ids}
 
+    split = {"set_input_ms": 0.0, "run_ms": 0.0, "get_output_ms": 0.0}
+
     def once():
+        t0 = time.perf_counter()
         ex.set_inputs(inputs)
+        t1 = time.perf_counter()
         ex.run(0)
-        return sum(ex.get_output(i, outs[i]).nbytes for i in ids)
+        t2 = time.perf_counter()
+        n = sum(ex.get_output(i, outs[i]).nbytes for i in ids)
+        t3 = time.perf_counter()
+        for k, v in zip(split, (t1 - t0, t2 - t1, t3 - t2)):
+            split[k] += v * 1e3 / steps
+        return n
 
     once()
+    split = dict.fromkeys(split, 0.0)
     t0 = time.perf_counter()
     for _ in range(steps):
         d2h = once()
     ms = (time.perf_counter() - t0) / steps * 1e3
     return {"value": samples_per_step / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms, "steps": steps,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "split": split,
             "via": "planc_b200_set_input (float64 TensorMap) -> planc_b200_run -> planc_b200_get_output "
                    "(every produced pTensor, float64, into the caller's reused arrays): the reference "
                    "run_plan contract"}

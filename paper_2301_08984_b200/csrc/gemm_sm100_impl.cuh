@@ -127,6 +127,12 @@ struct SkParams {
   // plain 16-byte stores from registers, valid for NVLink peer memory.
   int scatter_rows = 0;
   void* scatter_dst[kMaxGemmGroup] = {};
+  // Raster: M-blocks (pair rows for 2-SM launches) per group (tiles_coords).
+  int group_m = GROUP_M;
+  // L2 eviction priority of the A / B operand loads (0: default, 1:
+  // evict_first — streamed once, 2: evict_last — re-read across raster
+  // groups while the other operand streams past it).
+  int hint_a = 0, hint_b = 0;
   long long sk_iters = 0;
   float* partials = nullptr;  // [sk_ctas][2 slots][4 quarters][BN/32 chunks][8][32] float4
   int* counters = nullptr;    // [(tiles - dp_tiles) * 4], zero between launches
@@ -216,6 +222,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// Same, with an L2 eviction-priority policy (createpolicy).
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1, std::uint64_t* bar,
+                                                 std::uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// L2 policy for operand loads: 1 = evict_first, 2 = evict_last, else normal.
+__device__ __forceinline__ std::uint64_t l2_policy(int hint) {
+  std::uint64_t p;
+  if (hint == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else if (hint == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // Bulk tensor store smem -> global (clips rows / cols outside the tensor).
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
@@ -267,6 +292,15 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
       "[%4];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_2sm_hint(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                     std::uint32_t bar_cluster, std::uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(policy)
       : "memory");
 }
 
@@ -390,11 +424,11 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&r
 
 // ---- kernel --------------------------------------------------------------------
 
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
-  const int per_group = GROUP_M * tiles_n;
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb, int group_m = GROUP_M) {
+  const int per_group = group_m * tiles_n;
   const int group = t / per_group;
-  const int first_m = group * GROUP_M;
-  const int gm = min(tiles_m - first_m, GROUP_M);
+  const int first_m = group * group_m;
+  const int gm = min(tiles_m - first_m, group_m);
   const int r = t % per_group;
   mb = first_m + r % gm;
   nb = r / gm;
@@ -470,11 +504,11 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       const int pr = t >> 1;
       p = pr / per_pair;
       int mb2;
-      tile_coords(pr - p * per_pair, tiles_m2, tiles_n, mb2, nb);
+      tile_coords(pr - p * per_pair, tiles_m2, tiles_n, mb2, nb, sk.group_m);
       mb = 2 * mb2 + (t & 1);  // may pass tiles_m: a zero tile whose stores are clipped
     } else {
       p = t / per_gemm;
-      tile_coords(t - p * per_gemm, tiles_m, tiles_n, mb, nb);
+      tile_coords(t - p * per_gemm, tiles_m, tiles_n, mb, nb, sk.group_m);
     }
   };
   const int work_items = PAIR ? 2 * ((tiles_m + 1) / 2) * tiles_n * ng : num_tiles;  // fused epilogue loop bound
@@ -528,6 +562,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;  // global k-block counter across work items (ring position)
+      const std::uint64_t pol_a = l2_policy(sk.hint_a), pol_b = l2_policy(sk.hint_b);
       work([&](int t, int kb0, int kb1, int half) {
         int p, mb, nb;
         coords(t, p, mb, nb);
@@ -551,16 +586,17 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
             std::uint8_t* b = sB + s * B_STAGE_BYTES;
             if (A_MN) {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j) tma_load_2d_2sm(a + j * (64 * BK * 2), tmA, m0 + 64 * j, kb * BK, lb);
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_2d_2sm_hint(a + j * (64 * BK * 2), tmA, m0 + 64 * j, kb * BK, lb, pol_a);
             } else {
-              tma_load_2d_2sm(a, tmA, kb * BK, m0, lb);
+              tma_load_2d_2sm_hint(a, tmA, kb * BK, m0, lb, pol_a);
             }
             if (B_MN) {
 #pragma unroll
               for (int j = 0; j < BN / 128; ++j)
-                tma_load_2d_2sm(b + j * (64 * BK * 2), tmB, n0 + r * (BN / 2) + 64 * j, kb * BK, lb);
+                tma_load_2d_2sm_hint(b + j * (64 * BK * 2), tmB, n0 + r * (BN / 2) + 64 * j, kb * BK, lb, pol_b);
             } else {
-              tma_load_2d_2sm(b, tmB, kb * BK, n0 + r * (BN / 2), lb);
+              tma_load_2d_2sm_hint(b, tmB, kb * BK, n0 + r * (BN / 2), lb, pol_b);
             }
           }
           return;
@@ -574,9 +610,10 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
           std::uint8_t* b = sB + s * B_STAGE_BYTES;
           if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * (64 * BK * 2), tmA, m0 + 64 * j, kb * BK, &full[s]);
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d_hint(a + j * (64 * BK * 2), tmA, m0 + 64 * j, kb * BK, &full[s], pol_a);
           } else {
-            tma_load_2d(a, tmA, kb * BK, m0, &full[s]);
+            tma_load_2d_hint(a, tmA, kb * BK, m0, &full[s], pol_a);
           }
           if constexpr (CL) {
             // this CTA's half of the B tile, multicast to both CTAs of the pair
@@ -590,9 +627,10 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
             }
           } else if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * (64 * BK * 2), tmB, n0 + 64 * j, kb * BK, &full[s]);
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d_hint(b + j * (64 * BK * 2), tmB, n0 + 64 * j, kb * BK, &full[s], pol_b);
           } else {
-            tma_load_2d(b, tmB, kb * BK, n0, &full[s]);
+            tma_load_2d_hint(b, tmB, kb * BK, n0, &full[s], pol_b);
           }
         }
       });
@@ -1086,6 +1124,37 @@ int device_sms() {
   return num_sms[dev & 31];
 }
 
+// L2 residency of the operands. The grouped raster (GROUP_M rows of tiles,
+// N slow) streams each A row-panel through L2 once, shared by the group's
+// concurrently running N-tiles, while every group re-reads all of B (and,
+// for tall-k shapes, a wide B re-reads A across N-tiles). When the operands
+// together outgrow L2 (126 MB), the smaller one (<= 48 MB) is loaded
+// evict_last so it survives the other's stream between raster groups — the
+// re-reads of it otherwise come from HBM (C2's k = 8192 launches read
+// ~2x their algorithmic bytes, profiles/r01/ncu_gemm_dram_c2_tp1_v10.csv).
+// PLANC_B200_L2HINT=0 disables, =2 also marks the large operand evict_first;
+// PLANC_B200_GROUP_M sets the raster group height.
+inline void l2_plan(const GemmArgs& a, SkParams& sk) {
+  static const int mode = [] {
+    const char* e = std::getenv("PLANC_B200_L2HINT");
+    return e ? std::atoi(e) : 1;
+  }();
+  static const int group_m = [] {
+    const char* e = std::getenv("PLANC_B200_GROUP_M");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : GROUP_M;
+  }();
+  sk.group_m = group_m;
+  sk.hint_a = sk.hint_b = 0;
+  if (mode == 0) return;
+  const double g = std::max(a.group, 1);
+  const double bytes_a = g * a.m * a.k * 2.0, bytes_b = g * a.k * a.n * 2.0;
+  const double small = std::min(bytes_a, bytes_b), big = std::max(bytes_a, bytes_b);
+  if (small + big <= 96e6 || small > 48e6) return;
+  const bool a_small = bytes_a <= bytes_b;
+  (a_small ? sk.hint_a : sk.hint_b) = 2;
+  if (mode == 2) (a_small ? sk.hint_b : sk.hint_a) = 1;
+}
+
 template <bool A_MN, bool B_MN, bool C_BF16, int BN, bool FUSE, int NG, int OCC = 1>
 void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
   static unsigned attr_set_mask = 0;  // per device ordinal
@@ -1128,6 +1197,7 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
   sk.splits = sc.splits;
   sk.half_items = sc.half_items;
   sk.scatter_rows = a.scatter > 0 ? static_cast<int>(a.scatter_rows) : 0;
+  l2_plan(a, sk);
   for (int i = 0; i < a.scatter; ++i) sk.scatter_dst[i] = a.gC[i];
   const std::int64_t m_pad = (a.m + BM - 1) / BM * BM, n_pad = (a.n + BN - 1) / BN * BN;
   if (sc.splits > 1) {
