@@ -57,7 +57,11 @@ constexpr int NUM_THREADS = 192;
 // 4 = one CTA per SM in clusters of two along M: the pair shares each B
 // tile — every CTA loads half of it and multicasts to both (TMA
 // .multicast::cluster), halving B's L2 -> SM traffic.
-__host__ __device__ constexpr int epi_warps(int occ) { return occ == 3 ? 8 : 4; }
+// Eight epilogue warps (two per TMEM lane quarter, each taking half of a
+// tile's columns) for short-k launches (OCC 3) and for the 2-SM variant
+// (OCC 5), whose fused elementwise epilogues otherwise outlast the pair's
+// MMAs (C2's FFN GEMM with its fused ReLU: 250 us vs 169 us plain, r01).
+__host__ __device__ constexpr int epi_warps(int occ) { return occ == 3 || occ == 5 ? 8 : 4; }
 __host__ __device__ constexpr int cta_threads(int occ) { return 64 + 32 * epi_warps(occ); }
 constexpr int GROUP_M = 8;
 constexpr int kSkDepth = 2;  // stream-K partials loaded per round trip
@@ -71,13 +75,15 @@ constexpr int kSkDepth = 2;  // stream-K partials loaded per round trip
 template <int BN_, bool FUSE = false, int OCC = 1>
 struct Cfg {
   static constexpr int BN = BN_;
-  static constexpr int B_STAGE_BYTES = BN * BK * 2;
-  static constexpr int STAGES_RAW =
-      ((OCC == 1 || OCC >= 4 ? 200 : OCC == 2 ? 76 : 159) * 1024) / (A_STAGE_BYTES + B_STAGE_BYTES);
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  // + epilogue staging: 4 warps x 2 buffers x (32 rows x 32 cols, <= 4 B);
-  // FUSE (bf16): 4 warps x 2 x {C, fused result} 2 KB chunks — same size.
+  // 2-SM pairs (OCC 5): each CTA holds only its BN/2 columns of the B tile.
+  static constexpr int B_STAGE_BYTES = (OCC == 5 ? BN / 2 : BN) * BK * 2;
+  // + epilogue staging: 4 (8) warps x 2 buffers x (32 rows x 32 cols, <= 4 B);
+  // FUSE (bf16): warps x 2 x {C, fused result} 2 KB chunks — same size.
   static constexpr int STAGING_BYTES = epi_warps(OCC) * 2 * 4096;
+  static constexpr int RING_BYTES =
+      OCC == 5 ? 227 * 1024 - STAGING_BYTES - 3 * 1024 : (OCC == 1 || OCC >= 4 ? 200 : OCC == 2 ? 76 : 159) * 1024;
+  static constexpr int STAGES_RAW = RING_BYTES / (A_STAGE_BYTES + B_STAGE_BYTES);
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int SMEM_BYTES =
       STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + STAGING_BYTES + 1024 /*align*/ + 1024 /*barriers + align*/;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
@@ -580,7 +586,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
             const int s = it % STAGES;
             const std::uint32_t phase = (it / STAGES) & 1;
             mbar_wait(&empty[s], phase ^ 1);
-            if (r == 0) mbar_expect_tx(&full[s], 2 * (A_STAGE_BYTES + B_STAGE_BYTES / 2));
+            if (r == 0) mbar_expect_tx(&full[s], 2 * (A_STAGE_BYTES + B_STAGE_BYTES));  // (B_STAGE: BN/2 columns)
             const std::uint32_t lb = cluster_addr(&full[s], 0);
             std::uint8_t* a = sA + s * A_STAGE_BYTES;
             std::uint8_t* b = sB + s * B_STAGE_BYTES;
@@ -887,6 +893,11 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
     // in order, reading the GEMM's bf16-rounded C.
     const int q = warp % 4;
     std::uint8_t* stg = staging + (warp - 2) * 2 * 4096;  // [2][C 2 KB | result 2 KB]
+    // 8 epilogue warps: warps q and q + 4 share TMEM lane quarter q, each
+    // taking half of the tile's 32-column chunks.
+    constexpr int NCH = BN / 32;
+    const int c_lo = EPI_WARPS == 8 ? ((warp - 2) / 4) * (NCH / 2) : 0;
+    const int c_hi = EPI_WARPS == 8 ? c_lo + NCH / 2 : NCH;
     const int swz = (lane >> 1) & 3;
     const int nst = epi.n_slots;
     const __nv_bfloat16* src0 =
@@ -912,11 +923,11 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
     int g = 0;  // chunk counter of this warp (staging ring position)
     auto chunk = [&](int t, int mb, int nb, int c, std::uint32_t base, int acc, uint4(&cur)[kMaxEpiSlots][4],
                      uint4(&nxt)[kMaxEpiSlots][4]) {
-      if (c + 1 < BN / 32) load(t, c + 1, nxt);
-      else if (t + static_cast<int>(gridDim.x) < work_items) load(t + gridDim.x, 0, nxt);
+      if (c + 1 < c_hi) load(t, c + 1, nxt);
+      else if (t + static_cast<int>(gridDim.x) < work_items) load(t + gridDim.x, c_lo, nxt);
       std::uint32_t r[32];
       tmem_ld32(base + c * 32, r);
-      if (c == BN / 32 - 1) {
+      if (c == c_hi - 1) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -978,7 +989,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       ++g;
     };
     uint4 pa[kMaxEpiSlots][4], pb[kMaxEpiSlots][4];
-    if (static_cast<int>(blockIdx.x) < work_items) load(blockIdx.x, 0, pa);
+    if (static_cast<int>(blockIdx.x) < work_items) load(blockIdx.x, c_lo, pa);
     int local = 0;
     // Work items t = blockIdx.x + i * gridDim.x: plain tiles, or (pairs)
     // 2 * pair + rank — the same stride, cluster rank = blockIdx.x % 2.
@@ -991,7 +1002,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       tc_fence_after();
       const std::uint32_t base = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; c += 2) {
+      for (int c = c_lo; c < c_hi; c += 2) {
         chunk(t, mb, nb, c, base, acc, pa, pb);
         chunk(t, mb, nb, c + 1, base, acc, pb, pa);
       }
@@ -1132,12 +1143,14 @@ int device_sms() {
 // evict_last so it survives the other's stream between raster groups — the
 // re-reads of it otherwise come from HBM (C2's k = 8192 launches read
 // ~2x their algorithmic bytes, profiles/r01/ncu_gemm_dram_c2_tp1_v10.csv).
-// PLANC_B200_L2HINT=0 disables, =2 also marks the large operand evict_first;
+// The large operand streams evict_first (C2's k = 8192 launches 336 -> 264 MB
+// of DRAM reads and 190 -> 184 us, gpurun_out/l2hint r02). PLANC_B200_L2HINT
+// =0 disables, =1 marks only the small operand;
 // PLANC_B200_GROUP_M sets the raster group height.
 inline void l2_plan(const GemmArgs& a, SkParams& sk) {
   static const int mode = [] {
     const char* e = std::getenv("PLANC_B200_L2HINT");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
   static const int group_m = [] {
     const char* e = std::getenv("PLANC_B200_GROUP_M");

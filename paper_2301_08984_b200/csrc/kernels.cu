@@ -389,18 +389,146 @@ __global__ void emb_lookup_kernel(const int* __restrict__ idx, const T* __restri
   }
 }
 
+// embedding-grad (refexec.cpp:233-250: out[idx[j] - lo] += gout[j] in
+// ascending j), deterministic: no float atomics. Kernel 1 takes 1024
+// consecutive indices per block, sorts (row, j) keys in shared memory
+// (bitonic, unique keys) and sums each row's gout rows in ascending j into a
+// per-block partial; kernel 2 gives each output row one warp that adds the
+// blocks' partials in block order (binary search of the block's sorted
+// segment rows). Same bits on every run, the reference's j order inside a
+// block.
+constexpr int kEmbBlock = 1024;
+
 template <typename T>
-__global__ void emb_grad_kernel(const int* __restrict__ idx, const T* __restrict__ gout, float* __restrict__ acc,
-                                std::int64_t n, std::int64_t rows, std::int64_t h, std::int64_t lo) {
+__global__ void __launch_bounds__(512) emb_grad_block_kernel(const int* __restrict__ idx, const T* __restrict__ gout,
+                                                             float* __restrict__ partial, int* __restrict__ seg_row,
+                                                             int* __restrict__ nseg, std::int64_t n, std::int64_t rows,
+                                                             std::int64_t h, std::int64_t lo) {
   pdl_wait();  // launch.cuh: inputs of the previous kernel visible
   pdl_trigger();
-  std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / 32;
-  int lane = threadIdx.x & 31;
-  std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * blockDim.x / 32;
-  for (std::int64_t j = warp; j < n; j += nwarps) {
-    std::int64_t id = idx[j];
-    if (id < lo || id >= lo + rows) continue;
-    for (std::int64_t c = lane; c < h; c += 32) atomicAdd(acc + (id - lo) * h + c, to_acc<T>(gout[j * h + c]));
+  __shared__ unsigned long long key[kEmbBlock];
+  __shared__ int start[kEmbBlock + 1];
+  __shared__ int head_scan[kEmbBlock];
+  const std::int64_t base = static_cast<std::int64_t>(blockIdx.x) * kEmbBlock;
+  for (int i = threadIdx.x; i < kEmbBlock; i += blockDim.x) {
+    const std::int64_t j = base + i;
+    unsigned long long r = static_cast<unsigned long long>(rows);  // sentinel: not in this shard / padding
+    if (j < n) {
+      const std::int64_t id = idx[j];
+      if (id >= lo && id < lo + rows) r = static_cast<unsigned long long>(id - lo);
+    }
+    key[i] = (r << 10) | static_cast<unsigned long long>(i);
+  }
+  __syncthreads();
+  for (int k = 2; k <= kEmbBlock; k <<= 1) {
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int i = threadIdx.x; i < kEmbBlock; i += blockDim.x) {
+        const int p = i ^ jj;
+        if (p > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long a = key[i], b = key[p];
+          if ((a > b) == up) {
+            key[i] = b;
+            key[p] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // segment heads (valid rows only) -> inclusive scan -> segment ids
+  for (int i = threadIdx.x; i < kEmbBlock; i += blockDim.x) {
+    const unsigned long long r = key[i] >> 10;
+    head_scan[i] = (r < static_cast<unsigned long long>(rows) && (i == 0 || (key[i - 1] >> 10) != r)) ? 1 : 0;
+  }
+  __syncthreads();
+  for (int off = 1; off < kEmbBlock; off <<= 1) {
+    int v[2];
+    for (int q = 0; q < 2; ++q) {
+      const int i = threadIdx.x + q * blockDim.x;
+      v[q] = (i < kEmbBlock && i >= off) ? head_scan[i - off] : 0;
+    }
+    __syncthreads();
+    for (int q = 0; q < 2; ++q) {
+      const int i = threadIdx.x + q * blockDim.x;
+      if (i < kEmbBlock) head_scan[i] += v[q];
+    }
+    __syncthreads();
+  }
+  const int segs = head_scan[kEmbBlock - 1];
+  for (int i = threadIdx.x; i < kEmbBlock; i += blockDim.x) {
+    const unsigned long long r = key[i] >> 10;
+    const bool head = r < static_cast<unsigned long long>(rows) && (i == 0 || (key[i - 1] >> 10) != r);
+    if (head) {
+      start[head_scan[i] - 1] = i;
+      seg_row[base + head_scan[i] - 1] = static_cast<int>(r);
+    }
+    // end of the last valid segment: the first sentinel (or the block end)
+    if (r >= static_cast<unsigned long long>(rows) && (i == 0 || (key[i - 1] >> 10) < static_cast<unsigned long long>(rows)))
+      start[segs] = i;
+  }
+  if (threadIdx.x == 0) {
+    nseg[blockIdx.x] = segs;
+    if ((key[kEmbBlock - 1] >> 10) < static_cast<unsigned long long>(rows)) start[segs] = kEmbBlock;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int sg = warp; sg < segs; sg += nw) {
+    const int s0 = start[sg], s1 = start[sg + 1];
+    float* dst = partial + (base + sg) * h;
+    for (std::int64_t c = lane; c < h; c += 32) {
+      float acc = 0.f;
+      for (int i = s0; i < s1; ++i) acc += to_acc<T>(gout[(base + static_cast<int>(key[i] & 1023)) * h + c]);
+      dst[c] = acc;
+    }
+  }
+}
+
+template <typename T>
+__global__ void emb_grad_combine_kernel(const float* __restrict__ partial, const int* __restrict__ seg_row,
+                                        const int* __restrict__ nseg, T* __restrict__ out, int nblocks,
+                                        std::int64_t rows, std::int64_t h) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / 32;
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * blockDim.x / 32;
+  for (std::int64_t r = warp; r < rows; r += nwarps) {
+    for (std::int64_t c0 = 0; c0 < h; c0 += 128) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int b0 = 0; b0 < nblocks; b0 += 32) {
+        // lane l looks row r up among block (b0 + l)'s sorted segment rows
+        int seg = -1;
+        const int b = b0 + lane;
+        if (b < nblocks) {
+          int lo_i = 0, hi_i = nseg[b];
+          const int* rowsb = seg_row + static_cast<std::int64_t>(b) * kEmbBlock;
+          while (lo_i < hi_i) {
+            const int mid = (lo_i + hi_i) / 2;
+            if (rowsb[mid] < r) lo_i = mid + 1;
+            else hi_i = mid;
+          }
+          if (lo_i < nseg[b] && rowsb[lo_i] == r) seg = lo_i;
+        }
+        unsigned found = __ballot_sync(0xffffffffu, seg >= 0);
+        while (found) {  // blocks in ascending order
+          const int l = __ffs(found) - 1;
+          found &= found - 1;
+          const int sg = __shfl_sync(0xffffffffu, seg, l);
+          const float* src = partial + (static_cast<std::int64_t>(b0 + l) * kEmbBlock + sg) * h;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const std::int64_t c = c0 + lane + 32 * v;
+            if (c < h) acc[v] += src[c];
+          }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const std::int64_t c = c0 + lane + 32 * v;
+        if (c < h) out[r * h + c] = from_acc<T>(acc[v]);
+      }
+    }
   }
 }
 
@@ -563,19 +691,33 @@ void launch_emb_lookup(int dtype, const int* idx, const void* table, void* out, 
   check_launch("emb_lookup_kernel");
 }
 
-void launch_emb_grad(int dtype, const int* idx, const void* gout, void* out, float* scratch, std::int64_t n,
+std::int64_t emb_grad_scratch_bytes(std::int64_t n, std::int64_t h) {
+  const std::int64_t nb = (n + kEmbBlock - 1) / kEmbBlock;
+  return nb * kEmbBlock * h * 4 + nb * kEmbBlock * 4 + nb * 4 + 256;
+}
+
+void launch_emb_grad(int dtype, const int* idx, const void* gout, void* out, void* scratch, std::int64_t n,
                      std::int64_t rows, std::int64_t h, std::int64_t lo, cudaStream_t s) {
-  float* acc = dtype == DT_F32 ? static_cast<float*>(out) : scratch;
-  pdl_launch("zero_kernel", zero_kernel, dim3(grid_for(rows * h, 256)), dim3(256), 0, s, acc, rows * h);
-  int g = grid_for(n * 32, 256);
+  if (dtype != DT_F32 && dtype != DT_BF16) throw std::runtime_error("embedding-grad: unsupported dtype");
+  const std::int64_t nb = (n + kEmbBlock - 1) / kEmbBlock;
+  float* partial = static_cast<float*>(scratch);
+  int* seg_row = reinterpret_cast<int*>(partial + nb * kEmbBlock * h);
+  int* nseg = seg_row + nb * kEmbBlock;
+  if (nb > 0) {
+    if (dtype == DT_F32)
+      pdl_launch("emb_grad_block_kernel", emb_grad_block_kernel<float>, dim3(static_cast<unsigned>(nb)), dim3(512), 0, s,
+                 idx, static_cast<const float*>(gout), partial, seg_row, nseg, n, rows, h, lo);
+    else
+      pdl_launch("emb_grad_block_kernel", emb_grad_block_kernel<__nv_bfloat16>, dim3(static_cast<unsigned>(nb)),
+                 dim3(512), 0, s, idx, static_cast<const __nv_bfloat16*>(gout), partial, seg_row, nseg, n, rows, h, lo);
+  }
+  const int g = grid_for(rows * 32, 256);
   if (dtype == DT_F32)
-    pdl_launch("emb_grad_kernel", emb_grad_kernel<float>, dim3(g), dim3(256), 0, s, idx, static_cast<const float*>(gout), acc, n, rows, h, lo);
-  else if (dtype == DT_BF16)
-    pdl_launch("emb_grad_kernel", emb_grad_kernel<__nv_bfloat16>, dim3(g), dim3(256), 0, s, idx, static_cast<const __nv_bfloat16*>(gout), acc, n, rows,
-                                                      h, lo);
+    pdl_launch("emb_grad_combine_kernel", emb_grad_combine_kernel<float>, dim3(g), dim3(256), 0, s, partial, seg_row,
+               nseg, static_cast<float*>(out), static_cast<int>(nb), rows, h);
   else
-    throw std::runtime_error("embedding-grad: unsupported dtype");
-  if (dtype != DT_F32) pdl_launch("convert_kernel", convert_kernel, dim3(grid_for(rows * h, 256)), dim3(256), 0, s, dtype, out, acc, rows * h);
+    pdl_launch("emb_grad_combine_kernel", emb_grad_combine_kernel<__nv_bfloat16>, dim3(g), dim3(256), 0, s, partial,
+               seg_row, nseg, static_cast<__nv_bfloat16*>(out), static_cast<int>(nb), rows, h);
   check_launch("emb_grad_kernel");
 }
 

@@ -152,7 +152,10 @@ void launch_reduce(int dtype, const void* in, void* out, std::int64_t outer, std
                    std::int64_t inner, cudaStream_t s);
 void launch_emb_lookup(int dtype, const int* idx, const void* table, void* out, std::int64_t n, std::int64_t rows,
                        std::int64_t h, std::int64_t lo, cudaStream_t s);
-void launch_emb_grad(int dtype, const int* idx, const void* gout, void* out, float* scratch, std::int64_t n,
+// Deterministic embedding-grad: per-block sorted segment sums, then one warp
+// per output row adds the blocks' partials in block order (no atomics).
+std::int64_t emb_grad_scratch_bytes(std::int64_t n, std::int64_t h);
+void launch_emb_grad(int dtype, const int* idx, const void* gout, void* out, void* scratch, std::int64_t n,
                      std::int64_t rows, std::int64_t h, std::int64_t lo, cudaStream_t s);
 void launch_gemm_simt(const GemmArgs& a, cudaStream_t s);
 // Schema extension (program.hpp RowOp): softmax / softmax_grad / layernorm /

@@ -328,9 +328,9 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
         ck(cudaEventCreateWithFlags(&irt_[d].done, cudaEventDisableTiming), "event");
       }
     }
-    if (in.kind == InstrKind::emb_grad && prog_.buffers[in.out_bufs[0]].dtype != DType::f32) {
+    if (in.kind == InstrKind::emb_grad) {
       DeviceGuard dg(lanes_[in.lane].gpu);
-      ck(cudaMalloc(&irt_[in.id].scratch, sizeof(float) * in.rows * in.h), "cudaMalloc(scratch)");
+      ck(cudaMalloc(&irt_[in.id].scratch, emb_grad_scratch_bytes(in.n_idx, in.h)), "cudaMalloc(scratch)");
     }
   }
   if (peer_) {
@@ -359,7 +359,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
     switch (in.kind) {
       case InstrKind::nop: break;
       case InstrKind::box: kernels_per_step_ += static_cast<int>(irt_[in.id].box.size()); break;  // peer: at import
-      case InstrKind::emb_grad: kernels_per_step_ += prog_.buffers[in.out_bufs[0]].dtype == DType::f32 ? 2 : 3; break;
+      case InstrKind::emb_grad: kernels_per_step_ += in.n_idx > 0 ? 2 : 1; break;
       case InstrKind::ew: kernels_per_step_ += 1 + (in.count % 8 != 0 ? 1 : 0); break;
       default: kernels_per_step_ += 1;
     }
