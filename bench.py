@@ -51,6 +51,42 @@ def plan_name(config: str, n: int) -> str:
             "c5": "c5_3f1b_dap"}[config]
 
 
+def nvlink_peer_bandwidth(nbytes: int = 512 << 20, reps: int = 5):
+    """Peer copy bandwidth GPU 0 -> GPU 1 (and both directions at once) over
+    NVLink with CUDA events: the measured ceiling beside the nominal 900 GB/s
+    per direction that adapter_bus_gbs is reported against. None with fewer
+    than two visible GPUs."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        return {"value": None, "note": "fewer than two visible GPUs"}
+    a0 = torch.empty(nbytes, dtype=torch.uint8, device="cuda:0")
+    b1 = torch.empty(nbytes, dtype=torch.uint8, device="cuda:1")
+    a1 = torch.empty(nbytes, dtype=torch.uint8, device="cuda:1")
+    b0 = torch.empty(nbytes, dtype=torch.uint8, device="cuda:0")
+    s1 = torch.cuda.Stream(device="cuda:1")
+    out = {}
+    for name in ("uni", "bidir"):
+        best = 0.0
+        for _ in range(reps):
+            torch.cuda.synchronize(0)
+            torch.cuda.synchronize(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.current_stream(0))
+            b1.copy_(a0, non_blocking=True)
+            if name == "bidir":
+                with torch.cuda.stream(s1):
+                    b0.copy_(a1, non_blocking=True)
+                torch.cuda.current_stream(0).wait_stream(s1)
+            e1.record(torch.cuda.current_stream(0))
+            e1.synchronize()
+            moved = nbytes * (2 if name == "bidir" else 1)
+            best = max(best, moved / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        out[name] = round(best, 1)
+    return {"value": out["uni"], "bidir_gbs": out["bidir"], "unit": "GB/s", "nbytes": nbytes,
+            "via": "torch peer copy cuda:0 -> cuda:1 (CUDA events, best of %d)" % reps}
+
+
 def cpu_plan_name(config: str) -> str:
     """Reduced-shape twin of the config's plan for the reference CPU executor
     (SURVEY §8d). c3's 24-layer plan has none (the reference needs ~1 min per
@@ -542,6 +578,7 @@ def main():
                                         "nvlink_gbs": NVLINK_GBS, "source": peaks["src"] + " (sustained bf16)"}},
             "adapter_bus_gbs": (None if not coll or coll["wire"] == 0 else
                                 {"value": coll["wire"] / (coll["ms"] / 1e3) / 1e9, "vs_nvlink_gbs": NVLINK_GBS}),
+            "nvlink_peer_copy": nvlink_peer_bandwidth() if n > 1 else None,
             "kernel_families": families,
             "e2e": {"value": meta["samples_per_step"] / (e2e_ms / 1e3), "unit": "samples/s",
                     "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -1409,10 +1409,17 @@ void Executor::get_output_into(int ptensor, double* out, std::int64_t capacity) 
                                  "output " + std::to_string(ptensor));
   for (const auto& c : cells) {
     const int rank = c.rank;
-    const std::int64_t inner = rank ? c.extents[rank - 1] : 1;
-    const std::int64_t rows = inner ? c.elems() / inner : 0;
-    parallel_for(rows, inner * static_cast<std::int64_t>(c.terms.size()), [&](std::int64_t lo, std::int64_t hi) {
-      for (std::int64_t r = lo; r < hi; ++r) {
+    const std::int64_t inner_all = rank ? c.extents[rank - 1] : 1;
+    const std::int64_t rows = inner_all ? c.elems() / inner_all : 0;
+    // work item = (row, 64 Ki-element piece of it): collapsed cells are often
+    // one long row
+    constexpr std::int64_t kPiece = 1 << 16;
+    const std::int64_t pieces_per_row = std::max<std::int64_t>(1, (inner_all + kPiece - 1) / kPiece);
+    parallel_for(rows * pieces_per_row, std::min(inner_all, kPiece) * static_cast<std::int64_t>(c.terms.size()),
+                 [&](std::int64_t lo, std::int64_t hi) {
+      for (std::int64_t item = lo; item < hi; ++item) {
+        const std::int64_t r = item / pieces_per_row, j0 = (item % pieces_per_row) * kPiece;
+        const std::int64_t inner = std::min(kPiece, inner_all - j0);
         std::int64_t rem = r, doff = c.dst_offset;
         std::int64_t idx[kMaxCellRank] = {};
         for (int d = rank - 2; d >= 0; --d) {
@@ -1421,11 +1428,13 @@ void Executor::get_output_into(int ptensor, double* out, std::int64_t capacity) 
           doff += idx[d] * c.dst_strides[d];
         }
         const std::int64_t dstep = rank ? c.dst_strides[rank - 1] : 1;
+        doff += j0 * dstep;
         for (std::int64_t j = 0; j < inner; ++j) out[doff + j * dstep] = 0.0;
         for (const auto& t : c.terms) {
           std::int64_t so = t.offset;
           for (int d = 0; d + 1 < rank; ++d) so += idx[d] * t.strides[d];
           const std::int64_t sstep = rank ? t.strides[rank - 1] : 1;
+          so += j0 * sstep;
           const char* base = stage + off.at(t.buffer);
           const DType dt = prog_.buffers[t.buffer].dtype;
           for (std::int64_t j = 0; j < inner; ++j) {
