@@ -179,7 +179,9 @@ int planc_b200_profile(planc_b200_exec* h, char** json_out);
 int planc_b200_timeline(planc_b200_exec* h, char** json_out);
 
 /* Host-only: which GEMM path a matmul of this shape takes — tcgen05 tensor
- * cores (1) or the SIMT kernel (0) — and the tensor-core tile width. */
+ * cores (1: kind::f16 for bf16 operands, 3xTF32 kind::tf32 when operands and
+ * output are all fp32) or the SIMT kernel (0) — and the tensor-core tile
+ * width. */
 int planc_b200_gemm_config(int64_t m, int64_t n, int64_t k, int ta, int tb, int a_bf16, int b_bf16, int c_bf16,
                            int* tensor_cores, int* tile_n);
 

@@ -123,6 +123,7 @@ def _load():
     L.planc_b200_peer_import.argtypes = [vp, ctypes.c_char_p, c_i64]
     L.planc_b200_gemm_schedule.argtypes = [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_int, P(c_int),
                                            P(c_int), P(c_int), P(c_int), P(c_int), P(c_int), P(c_int), P(c_i64)]
+    L.planc_b200_gemm_config.argtypes = [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_int, P(c_int), P(c_int)]
     L.planc_b200_free.argtypes = [vp]
     _lib = L
     return L
@@ -178,6 +179,18 @@ def gemm_schedule(m: int, n: int, k: int, ta: bool = False, tb: bool = False, c_
     return {"tile_n": bn.value, "grid": grid.value, "dp_tiles": dp.value, "sk_ctas": sk.value, "splits": sp.value,
             "half_items": hf.value, "variant": occ.value, "ctas_per_sm": 2 if occ.value == 2 else 1,
             "ws_bytes": ws.value}
+
+
+def gemm_config(m: int, n: int, k: int, ta: bool = False, tb: bool = False, a_bf16: bool = True,
+                b_bf16: bool = True, c_bf16: bool = True) -> dict:
+    """Host-only: whether a matmul of this shape and these element types
+    takes the tensor cores (bf16: tcgen05 kind::f16; fp32 operands and
+    output: 3xTF32 kind::tf32) and the tile width."""
+    L = _load()
+    tc, bn = ctypes.c_int(), ctypes.c_int()
+    _check(L.planc_b200_gemm_config(m, n, k, int(ta), int(tb), int(a_bf16), int(b_bf16), int(c_bf16),
+                                    ctypes.byref(tc), ctypes.byref(bn)))
+    return {"tensor_cores": bool(tc.value), "tile_n": bn.value}
 
 
 def nccl_unique_id() -> bytes:

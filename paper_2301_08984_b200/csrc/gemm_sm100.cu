@@ -102,6 +102,7 @@ GemmSchedule splitk_for(std::int64_t m, std::int64_t n, std::int64_t k, int bn, 
 // unless narrower ones are). PLANC_B200_GEMM_BN=256|128|64 forces a width,
 // PLANC_B200_STREAMK=0 disables stream-K, =2 takes it whenever it applies.
 GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
+  if (gemm_x3_eligible(a)) return gemm_x3_schedule(a, sms);
   const char* env = std::getenv("PLANC_B200_GEMM_BN");
   const int forced = env ? std::atoi(env) : 0;
   const char* skenv = std::getenv("PLANC_B200_STREAMK");
@@ -192,7 +193,10 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   return best;
 }
 
-int gemm_sm100_launches(const GemmArgs& a) { return gemm_sm100_schedule(a, device_sms()).splits > 1 ? 2 : 1; }
+int gemm_sm100_launches(const GemmArgs& a) {
+  if (gemm_x3_eligible(a)) return 2;  // hi / lo split + GEMM
+  return gemm_sm100_schedule(a, device_sms()).splits > 1 ? 2 : 1;
+}
 
 int gemm_sm100_tile_n(const GemmArgs& a) { return gemm_sm100_schedule(a, 148).bn; }
 
@@ -202,6 +206,7 @@ std::int64_t gemm_sm100_workspace_bytes(const GemmArgs& a) {
 }
 
 bool gemm_sm100_eligible(const GemmArgs& a) {
+  if (gemm_x3_eligible(a)) return true;  // fp32: 3xTF32 (gemm_x3.cu)
   if (a.da != DT_BF16 || a.db != DT_BF16 || (a.dc != DT_BF16 && a.dc != DT_F32)) return false;
   if (a.m <= 0 || a.n <= 0 || a.k <= 0) return false;
   if (a.m > (1 << 30) || a.n > (1 << 30) || a.k > (1 << 30)) return false;
@@ -215,6 +220,7 @@ bool gemm_sm100_eligible(const GemmArgs& a) {
 }
 
 void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s) {
+  if (gemm_x3_eligible(a)) return launch_gemm_x3(a, s);
   const bool a_mn = a.ta, b_mn = !a.tb, cb = a.dc == DT_BF16;
   GemmSchedule sc = gemm_sm100_schedule(a, device_sms());
   if ((sc.sk_ctas > 0 || sc.splits > 1) && (a.ws == nullptr || a.ws_bytes < sc.ws_bytes)) {

@@ -197,6 +197,11 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms);
 std::int64_t gemm_sm100_workspace_bytes(const GemmArgs& a);  // on the current device
 int gemm_sm100_launches(const GemmArgs& a);                   // kernels per GEMM (2 with split-K)
 void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s);
+// 3xTF32 tcgen05 GEMM for fp32 operands and output (gemm_x3.cu); reached
+// through the gemm_sm100_* entry points above.
+bool gemm_x3_eligible(const GemmArgs& a);
+GemmSchedule gemm_x3_schedule(const GemmArgs& a, int sms);
+void launch_gemm_x3(const GemmArgs& a, cudaStream_t s);
 
 // Dispatch: tcgen05 path when eligible, SIMT tile kernel otherwise (a
 // group then runs member by member).

@@ -145,6 +145,9 @@ bool tc_fusable(const Instr& g, DType a, DType b, DType c) {
 }
 bool tc_groupable(const Instr& g, DType a, DType b, DType c) {
   static_assert(kMaxGemmGroupInstr == kMaxGemmGroup, "group size limits differ");
+  // Grouped launches and the reduce-scatter epilogue are bf16-operand
+  // variants (fp32 GEMMs take the single-launch 3xTF32 kernel).
+  if (a != DType::bf16 || b != DType::bf16) return false;
   GemmArgs x{};
   x.m = g.m;
   x.n = g.n;
