@@ -336,45 +336,113 @@ void ew_typed(const void* const* ins, int nin, void* out, std::int64_t count, cu
 // ---- reduce-sum --------------------------------------------------------------
 
 // inner == 1: one warp per output row, lanes stride the reduced axis.
-template <typename T>
-__global__ void reduce_rows_kernel(const T* __restrict__ in, T* __restrict__ out, std::int64_t outer,
-                                   std::int64_t axis_len) {
+// V > 1: 16-byte vectors (axis_len % V == 0, 16-byte aligned rows), four
+// loads in flight per lane.
+template <typename T, int V>
+__global__ void __launch_bounds__(256) reduce_rows_kernel(const T* __restrict__ in, T* __restrict__ out,
+                                                          std::int64_t outer, std::int64_t axis_len) {
   pdl_wait();  // launch.cuh: inputs of the previous kernel visible
   pdl_trigger();
   std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / 32;
   int lane = threadIdx.x & 31;
   std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * blockDim.x / 32;
+  const std::int64_t nv = axis_len / V;
+  constexpr int U = V > 1 ? 4 : 1;
   for (std::int64_t r = warp; r < outer; r += nwarps) {
+    const T* row = in + r * axis_len;
     float acc = 0.f;
-    for (std::int64_t a = lane; a < axis_len; a += 32) acc += to_acc<T>(in[r * axis_len + a]);
+    for (std::int64_t a0 = lane; a0 < nv; a0 += 32 * U) {
+      float v[U][V];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (a0 + 32 * u < nv) load_vec<T, V>(row + (a0 + 32 * u) * V, v[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (a0 + 32 * u < nv) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc += v[u][j];
+        }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) out[r] = from_acc<T>(acc);
   }
 }
 
-// inner > 1: one thread per (outer, inner) column, coalesced along inner.
-template <typename T>
-__global__ void reduce_cols_kernel(const T* __restrict__ in, T* __restrict__ out, std::int64_t outer,
-                                   std::int64_t axis_len, std::int64_t inner) {
+// inner > 1: a block owns 32 * V consecutive inner columns of one outer
+// index (each lane V of them, 16-byte vectors when inner % V == 0) and a
+// range of the reduced axis, split over its 8 warps (interleaved rows, 4
+// loads in flight); the warps' sums are combined in shared memory in warp
+// order. When the axis is split over S > 1 blocks (grid.z), each writes an
+// fp32 partial [outer][S][inner] to scratch and reduce_cols_finish adds the
+// S partials in order — no atomics, the same bits every run.
+constexpr int kRedWarps = 8;
+template <typename T, int V>
+__global__ void __launch_bounds__(kRedWarps * 32) reduce_cols_kernel(const T* __restrict__ in, T* __restrict__ out,
+                                                                    float* __restrict__ partial, std::int64_t outer,
+                                                                    std::int64_t axis_len, std::int64_t inner) {
   pdl_wait();  // launch.cuh: inputs of the previous kernel visible
   pdl_trigger();
-  std::int64_t total = outer * inner;
-  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < total;
+  __shared__ float red[kRedWarps][32 * V];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const std::int64_t o = blockIdx.y;
+  const std::int64_t c0 = (static_cast<std::int64_t>(blockIdx.x) * 32 + lane) * V;
+  const int S = gridDim.z;
+  const std::int64_t a_lo = axis_len * blockIdx.z / S, a_hi = axis_len * (blockIdx.z + 1) / S;
+  const bool live = c0 < inner;  // inner % V == 0 when V > 1
+  const T* base = in + o * axis_len * inner + c0;
+  float acc[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) acc[j] = 0.f;
+  constexpr int U = 4;
+  for (std::int64_t a = a_lo + warp; a < a_hi; a += kRedWarps * U) {
+    float v[U][V];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (live && a + kRedWarps * u < a_hi) load_vec<T, V>(base + (a + kRedWarps * u) * inner, v[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (live && a + kRedWarps * u < a_hi) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] += v[u][j];
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < V; ++j) red[warp][lane * V + j] = acc[j];
+  __syncthreads();
+  for (int i = threadIdx.x; i < 32 * V; i += blockDim.x) {
+    const std::int64_t c = static_cast<std::int64_t>(blockIdx.x) * 32 * V + i;
+    if (c >= inner) continue;
+    float sum = red[0][i];
+#pragma unroll
+    for (int w = 1; w < kRedWarps; ++w) sum += red[w][i];
+    if (S == 1) out[o * inner + c] = from_acc<T>(sum);
+    else partial[(o * S + blockIdx.z) * inner + c] = sum;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_cols_finish(const float* __restrict__ partial, T* __restrict__ out,
+                                                          std::int64_t outer, int S, std::int64_t inner) {
+  pdl_wait();
+  pdl_trigger();
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < outer * inner;
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-    std::int64_t o = i / inner, c = i % inner;
-    const T* p = in + o * axis_len * inner + c;
-    float acc = 0.f;
-    for (std::int64_t a = 0; a < axis_len; ++a) acc += to_acc<T>(p[a * inner]);
-    out[i] = from_acc<T>(acc);
+    const std::int64_t o = i / inner, c = i - o * inner;
+    const float* p = partial + o * S * inner + c;
+    float sum = p[0];
+    for (int s = 1; s < S; ++s) sum += p[s * inner];
+    out[i] = from_acc<T>(sum);
   }
 }
 
 // ---- embedding ---------------------------------------------------------------
 
-template <typename T>
-__global__ void emb_lookup_kernel(const int* __restrict__ idx, const T* __restrict__ table, T* __restrict__ out,
-                                  std::int64_t n, std::int64_t rows, std::int64_t h, std::int64_t lo) {
+// One warp per index; V > 1 copies 16-byte vectors (h % V == 0, aligned).
+template <typename T, int V>
+__global__ void __launch_bounds__(256) emb_lookup_kernel(const int* __restrict__ idx, const T* __restrict__ table,
+                                                         T* __restrict__ out, std::int64_t n, std::int64_t rows,
+                                                         std::int64_t h, std::int64_t lo) {
   pdl_wait();  // launch.cuh: inputs of the previous kernel visible
   pdl_trigger();
   std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / 32;
@@ -383,8 +451,12 @@ __global__ void emb_lookup_kernel(const int* __restrict__ idx, const T* __restri
   for (std::int64_t j = warp; j < n; j += nwarps) {
     std::int64_t id = idx[j];
     bool in_shard = id >= lo && id < lo + rows;
-    for (std::int64_t c = lane; c < h; c += 32) {
-      out[j * h + c] = in_shard ? table[(id - lo) * h + c] : from_acc<T>(0.f);
+    if constexpr (V > 1) {
+      const uint4* src = reinterpret_cast<const uint4*>(table + (id - lo) * h);
+      uint4* dst = reinterpret_cast<uint4*>(out + j * h);
+      for (std::int64_t c = lane; c < h / V; c += 32) dst[c] = in_shard ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+    } else {
+      for (std::int64_t c = lane; c < h; c += 32) out[j * h + c] = in_shard ? table[(id - lo) * h + c] : from_acc<T>(0.f);
     }
   }
 }
@@ -654,40 +726,93 @@ void launch_ew(int op, int dtype, const void* const* ins, int nin, void* out, st
   check_launch("ew_kernel");
 }
 
-void launch_reduce(int dtype, const void* in, void* out, std::int64_t outer, std::int64_t axis_len,
-                   std::int64_t inner, cudaStream_t s) {
-  if (dtype == DT_F32) {
-    if (inner == 1)
-      pdl_launch("reduce_rows_kernel", reduce_rows_kernel<float>, dim3(grid_for(outer * 32, 256)), dim3(256), 0, s, static_cast<const float*>(in),
-                                                                           static_cast<float*>(out), outer, axis_len);
+namespace {
+bool aligned16(const void* p) { return reinterpret_cast<std::uintptr_t>(p) % 16 == 0; }
+
+// Axis splits of a column reduction: enough blocks for ~2 waves, at least
+// 64 rows per split.
+int reduce_splits(std::int64_t outer, std::int64_t axis_len, std::int64_t inner, int vec) {
+  const std::int64_t tiles = outer * ((inner + 32 * vec - 1) / (32 * vec));
+  std::int64_t S = (2 * 148 + tiles - 1) / tiles;
+  S = std::min<std::int64_t>(S, std::max<std::int64_t>(1, axis_len / 64));
+  return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(S, 1024)));
+}
+
+template <typename T>
+void reduce_typed(const void* in_, void* out_, void* scratch, std::int64_t outer, std::int64_t axis_len,
+                  std::int64_t inner, cudaStream_t s) {
+  constexpr int VV = 16 / sizeof(T);
+  const T* in = static_cast<const T*>(in_);
+  T* out = static_cast<T*>(out_);
+  if (inner == 1) {
+    if (aligned16(in) && axis_len % VV == 0)
+      pdl_launch("reduce_rows_kernel", reduce_rows_kernel<T, VV>, dim3(grid_for(outer * 32, 256)), dim3(256), 0, s, in,
+                 out, outer, axis_len);
     else
-      pdl_launch("reduce_cols_kernel", reduce_cols_kernel<float>, dim3(grid_for(outer * inner, 256)), dim3(256), 0, s, 
-          static_cast<const float*>(in), static_cast<float*>(out), outer, axis_len, inner);
-  } else if (dtype == DT_BF16) {
-    using B = __nv_bfloat16;
-    if (inner == 1)
-      pdl_launch("reduce_rows_kernel", reduce_rows_kernel<B>, dim3(grid_for(outer * 32, 256)), dim3(256), 0, s, static_cast<const B*>(in),
-                                                                       static_cast<B*>(out), outer, axis_len);
-    else
-      pdl_launch("reduce_cols_kernel", reduce_cols_kernel<B>, dim3(grid_for(outer * inner, 256)), dim3(256), 0, s, static_cast<const B*>(in),
-                                                                         static_cast<B*>(out), outer, axis_len, inner);
-  } else {
-    throw std::runtime_error("reduce: unsupported dtype");
+      pdl_launch("reduce_rows_kernel", reduce_rows_kernel<T, 1>, dim3(grid_for(outer * 32, 256)), dim3(256), 0, s, in,
+                 out, outer, axis_len);
+    return;
   }
+  const bool vec = aligned16(in) && inner % VV == 0;
+  const int v = vec ? VV : 1;
+  const int S = scratch ? reduce_splits(outer, axis_len, inner, v) : 1;
+  if (outer > 65535) throw std::runtime_error("reduce: more than 65535 outer rows with a column reduction");
+  dim3 grid(static_cast<unsigned>((inner + 32 * v - 1) / (32 * v)), static_cast<unsigned>(outer),
+            static_cast<unsigned>(S));
+  float* part = static_cast<float*>(scratch);
+  if (vec)
+    pdl_launch("reduce_cols_kernel", reduce_cols_kernel<T, VV>, grid, dim3(kRedWarps * 32), 0, s, in, out, part,
+               outer, axis_len, inner);
+  else
+    pdl_launch("reduce_cols_kernel", reduce_cols_kernel<T, 1>, grid, dim3(kRedWarps * 32), 0, s, in, out, part, outer,
+               axis_len, inner);
+  if (S > 1)
+    pdl_launch("reduce_cols_finish", reduce_cols_finish<T>, dim3(grid_for(outer * inner, 256)), dim3(256), 0, s,
+               static_cast<const float*>(part), out, outer, S, inner);
+}
+}  // namespace
+
+std::int64_t reduce_scratch_bytes(std::int64_t outer, std::int64_t axis_len, std::int64_t inner, int dtype) {
+  if (inner == 1) return 0;
+  const int v = dtype == DT_BF16 ? 8 : 4;
+  const int S = reduce_splits(outer, axis_len, inner, v);
+  return S > 1 ? static_cast<std::int64_t>(S) * outer * inner * 4 : 0;
+}
+
+int reduce_launches(std::int64_t outer, std::int64_t axis_len, std::int64_t inner, int dtype) {
+  return reduce_scratch_bytes(outer, axis_len, inner, dtype) > 0 ? 2 : 1;
+}
+
+void launch_reduce(int dtype, const void* in, void* out, void* scratch, std::int64_t outer, std::int64_t axis_len,
+                   std::int64_t inner, cudaStream_t s) {
+  if (dtype == DT_F32) reduce_typed<float>(in, out, scratch, outer, axis_len, inner, s);
+  else if (dtype == DT_BF16) reduce_typed<__nv_bfloat16>(in, out, scratch, outer, axis_len, inner, s);
+  else throw std::runtime_error("reduce: unsupported dtype");
   check_launch("reduce_kernel");
 }
 
 void launch_emb_lookup(int dtype, const int* idx, const void* table, void* out, std::int64_t n, std::int64_t rows,
                        std::int64_t h, std::int64_t lo, cudaStream_t s) {
   int g = grid_for(n * 32, 256);
-  if (dtype == DT_F32)
-    pdl_launch("emb_lookup_kernel", emb_lookup_kernel<float>, dim3(g), dim3(256), 0, s, idx, static_cast<const float*>(table), static_cast<float*>(out), n,
-                                                rows, h, lo);
-  else if (dtype == DT_BF16)
-    pdl_launch("emb_lookup_kernel", emb_lookup_kernel<__nv_bfloat16>, dim3(g), dim3(256), 0, s, idx, static_cast<const __nv_bfloat16*>(table),
-                                                        static_cast<__nv_bfloat16*>(out), n, rows, h, lo);
-  else
+  const bool vec = aligned16(table) && aligned16(out);
+  if (dtype == DT_F32) {
+    const float* t = static_cast<const float*>(table);
+    float* o = static_cast<float*>(out);
+    if (vec && h % 4 == 0)
+      pdl_launch("emb_lookup_kernel", emb_lookup_kernel<float, 4>, dim3(g), dim3(256), 0, s, idx, t, o, n, rows, h, lo);
+    else
+      pdl_launch("emb_lookup_kernel", emb_lookup_kernel<float, 1>, dim3(g), dim3(256), 0, s, idx, t, o, n, rows, h, lo);
+  } else if (dtype == DT_BF16) {
+    using B = __nv_bfloat16;
+    const B* t = static_cast<const B*>(table);
+    B* o = static_cast<B*>(out);
+    if (vec && h % 8 == 0)
+      pdl_launch("emb_lookup_kernel", emb_lookup_kernel<B, 8>, dim3(g), dim3(256), 0, s, idx, t, o, n, rows, h, lo);
+    else
+      pdl_launch("emb_lookup_kernel", emb_lookup_kernel<B, 1>, dim3(g), dim3(256), 0, s, idx, t, o, n, rows, h, lo);
+  } else {
     throw std::runtime_error("embedding: unsupported dtype");
+  }
   check_launch("emb_lookup_kernel");
 }
 

@@ -148,7 +148,12 @@ constexpr int kBoxChunkUnits = 1024;
 void launch_box(void* dst, int dtype, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks,
                 int nchunks, int vec, int max_rank, cudaStream_t s);
 void launch_ew(int op, int dtype, const void* const* ins, int nin, void* out, std::int64_t count, cudaStream_t s);
-void launch_reduce(int dtype, const void* in, void* out, std::int64_t outer, std::int64_t axis_len,
+// reduce-sum over the middle axis of [outer][axis_len][inner]; column
+// reductions (inner > 1) split the axis over blocks with fp32 partials in
+// `scratch` (reduce_scratch_bytes; null = no split), summed in split order.
+std::int64_t reduce_scratch_bytes(std::int64_t outer, std::int64_t axis_len, std::int64_t inner, int dtype);
+int reduce_launches(std::int64_t outer, std::int64_t axis_len, std::int64_t inner, int dtype);
+void launch_reduce(int dtype, const void* in, void* out, void* scratch, std::int64_t outer, std::int64_t axis_len,
                    std::int64_t inner, cudaStream_t s);
 void launch_emb_lookup(int dtype, const int* idx, const void* table, void* out, std::int64_t n, std::int64_t rows,
                        std::int64_t h, std::int64_t lo, cudaStream_t s);

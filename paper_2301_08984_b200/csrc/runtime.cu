@@ -335,6 +335,14 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       DeviceGuard dg(lanes_[in.lane].gpu);
       ck(cudaMalloc(&irt_[in.id].scratch, emb_grad_scratch_bytes(in.n_idx, in.h)), "cudaMalloc(scratch)");
     }
+    if (in.kind == InstrKind::reduce) {
+      const std::int64_t b =
+          reduce_scratch_bytes(in.outer, in.axis_len, in.inner, dt_of(prog_.buffers[in.out_bufs[0]].dtype));
+      if (b > 0) {
+        DeviceGuard dg(lanes_[in.lane].gpu);
+        ck(cudaMalloc(&irt_[in.id].scratch, b), "cudaMalloc(reduce scratch)");
+      }
+    }
   }
   if (peer_) {
     // This rank's flag block: epoch, step barrier slots, ready slots.
@@ -363,6 +371,9 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       case InstrKind::nop: break;
       case InstrKind::box: kernels_per_step_ += static_cast<int>(irt_[in.id].box.size()); break;  // peer: at import
       case InstrKind::emb_grad: kernels_per_step_ += in.n_idx > 0 ? 2 : 1; break;
+      case InstrKind::reduce:
+        kernels_per_step_ += reduce_launches(in.outer, in.axis_len, in.inner, dt_of(prog_.buffers[in.out_bufs[0]].dtype));
+        break;
       case InstrKind::ew: kernels_per_step_ += 1 + (in.count % 8 != 0 ? 1 : 0); break;
       default: kernels_per_step_ += 1;
     }
@@ -896,7 +907,7 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
     }
     case InstrKind::reduce:
       launch_reduce(dt_of(prog_.buffers[in.out_bufs[0]].dtype), buf_ptr(in.in_bufs[0]), buf_ptr(in.out_bufs[0]),
-                    in.outer, in.axis_len, in.inner, s);
+                    irt_[in.id].scratch, in.outer, in.axis_len, in.inner, s);
       return;
     case InstrKind::emb_lookup:
       launch_emb_lookup(dt_of(prog_.buffers[in.out_bufs[0]].dtype), static_cast<const int*>(buf_ptr(in.in_bufs[0])),

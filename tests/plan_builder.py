@@ -98,3 +98,12 @@ def matmul_gelu_plan(m, n, k, ta=False, tb=False):
     doc["feeds"].append([201, 200])
     doc["lanes"][0]["tasks"].append({"kind": "compute", "op": "act", "duration": 0.0, "bytes": 0})
     return json.dumps(doc), 3
+
+
+def embedding_plan(n, vocab, h, lo, rows, elem=2):
+    """out[j] = table[idx[j]] for idx in the shard [lo, lo + rows) of a
+    [vocab, h] table, else 0 (refexec.cpp:216-232): one lane holding table
+    rows [lo, lo + rows)."""
+    doc = json.loads(single_op_plan("embedding-lookup", [(n,), (vocab, h)], (n, h), [4, elem], elem)[0])
+    doc["vtensors"][1]["region"] = [[lo, lo + rows], [0, h]]
+    return json.dumps(doc), 2

@@ -164,6 +164,43 @@ def test_reduce_sum(shape, axis):
     assert np.array_equal(out.reshape(-1), x.sum(axis=axis).reshape(-1))
 
 
+# Column reductions split the axis over blocks (fp32 partials, summed in
+# split order) and vectorise along the kept inner axis; row reductions load
+# 16-byte vectors. Exact on integer data; same bits on every run.
+@pytest.mark.parametrize("shape,axis,elem", [((8192, 2048), 0, 4), ((3, 4096, 520), 1, 4), ((64, 300, 40), 1, 4),
+                                             ((200, 2048), 0, 2), ((7, 130, 33), 1, 2), ((4096, 1000), 1, 2),
+                                             ((1000, 4096), 1, 4), ((65536, 8), 0, 4)])
+def test_reduce_sum_vectorised(shape, axis, elem):
+    rng = np.random.default_rng(sum(shape))
+    out_shape = tuple(e for i, e in enumerate(shape) if i != axis) or (1,)
+    plan, out_pt = single_op_plan("reduce-sum", [shape], out_shape, elem, elem, {"axis": axis})
+    x = rng.integers(-1, 2, size=shape).astype(np.float64)
+    with pb.Executor(plan, lane_gpus=[0]) as ex:
+        ex.set_inputs({0: x})
+        ex.run(2)
+        out = ex.get_output(out_pt)
+        ex.run(1)
+        again = ex.get_output(out_pt)
+    assert np.array_equal(out.reshape(-1), x.sum(axis=axis).reshape(-1))
+    assert np.array_equal(out, again)
+
+
+@pytest.mark.parametrize("h,elem", [(2048, 2), (100, 2), (512, 4), (33, 4)])
+def test_embedding_lookup_vectorised(h, elem):
+    """Gather of table rows (16-byte vectors when h allows), out-of-shard
+    indices give zero rows (refexec.cpp:216-232)."""
+    from plan_builder import embedding_plan
+
+    vocab, n, lo, rows = 1000, 4096, 200, 500
+    plan, out_pt = embedding_plan(n, vocab, h, lo, rows, elem)
+    rng = np.random.default_rng(h)
+    idx = rng.integers(0, vocab, size=n).astype(np.float64)
+    table = rng.integers(-4, 5, size=(vocab, h)).astype(np.float64)
+    out, _ = run_single(plan, {0: idx, 1: table}, out_pt)
+    ref = np.where(((idx >= lo) & (idx < lo + rows))[:, None], table[idx.astype(int)], 0.0)
+    assert np.array_equal(out, ref)
+
+
 @pytest.mark.parametrize("g,m,n,k,ta,tb", [(4, 16384, 512, 512, False, False), (3, 304, 520, 200, False, True),
                                            (4, 512, 512, 16384, True, False), (8, 1024, 256, 256, False, False),
                                            (2, 8192, 2048, 2048, False, True)])
