@@ -65,6 +65,9 @@ extern "C" {
 #define PLANC_B200_NO_GROUPING 0x40u    /* every GEMM its own launch (default: independent same-shape
                                            GEMMs of a lane that become ready together share one grouped
                                            tensor-core launch) */
+#define PLANC_B200_NO_BATCH 0x1000u     /* every adapter (box) instruction its own launch (default: box
+                                           instructions of one GPU pending together in issue order —
+                                           pairwise independent — share one launch per element type) */
 #define PLANC_B200_SERIAL_LANES 0x8u    /* one stream per lane: a lane's tasks run strictly in plan
                                            order (default: only data dependencies and sync edges order
                                            a lane's work, spread over several streams) */

@@ -44,6 +44,7 @@ NO_ALIAS = 0x100
 NO_SCATTER = 0x200
 FUSE_ACT = 0x400
 REUSE_MEMORY = 0x800
+NO_BATCH = 0x1000
 
 
 class PlancError(RuntimeError):

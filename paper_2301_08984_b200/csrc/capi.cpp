@@ -67,6 +67,7 @@ ExecOptions exec_options(uint32_t flags) {
   opt.alias_copies = (flags & PLANC_B200_NO_ALIAS) == 0;
   opt.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0;
   opt.reuse_memory = (flags & PLANC_B200_REUSE_MEMORY) != 0;
+  opt.batch_boxes = (flags & PLANC_B200_NO_BATCH) == 0;
   return opt;
 }
 

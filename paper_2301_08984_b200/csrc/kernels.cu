@@ -129,7 +129,7 @@ constexpr int kBoxThreads = 256;
 constexpr int kBoxUnroll = 4;
 
 template <typename T, int V, int R>
-__global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, const DevCell* __restrict__ cells,
+__global__ void __launch_bounds__(kBoxThreads) box_kernel(const DevCell* __restrict__ cells,
                                                            const DevTerm* __restrict__ terms,
                                                            const DevChunk* __restrict__ chunks) {
   pdl_wait();  // launch.cuh: inputs of the previous kernel visible
@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, c
     dstr[d] = __ldg(&c->dst_str[d]);
   }
   const std::int64_t dst_off = __ldg(&c->dst_off);
+  T* dst = reinterpret_cast<T*>(__ldg(reinterpret_cast<const unsigned long long*>(&c->dst)));
   const std::uint32_t inner_vecs = ext[R - 1] / V;
   std::int64_t coord[U][R];
   bool live[U];
@@ -216,20 +217,19 @@ __global__ void __launch_bounds__(kBoxThreads) box_kernel(T* __restrict__ dst, c
 }
 
 template <typename T, int V>
-void box_rank_dispatch(void* dst, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks,
-                       int max_rank, cudaStream_t s) {
-  T* d = static_cast<T*>(dst);
-  if (max_rank <= 1) pdl_launch("box_kernel", box_kernel<T, V, 1>, dim3(nchunks), dim3(kBoxThreads), 0, s, d, cells, terms, chunks);
-  else if (max_rank == 2) pdl_launch("box_kernel", box_kernel<T, V, 2>, dim3(nchunks), dim3(kBoxThreads), 0, s, d, cells, terms, chunks);
-  else pdl_launch("box_kernel", box_kernel<T, V, kBoxRank>, dim3(nchunks), dim3(kBoxThreads), 0, s, d, cells, terms, chunks);
+void box_rank_dispatch(const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks, int max_rank,
+                       cudaStream_t s) {
+  if (max_rank <= 1) pdl_launch("box_kernel", box_kernel<T, V, 1>, dim3(nchunks), dim3(kBoxThreads), 0, s, cells, terms, chunks);
+  else if (max_rank == 2) pdl_launch("box_kernel", box_kernel<T, V, 2>, dim3(nchunks), dim3(kBoxThreads), 0, s, cells, terms, chunks);
+  else pdl_launch("box_kernel", box_kernel<T, V, kBoxRank>, dim3(nchunks), dim3(kBoxThreads), 0, s, cells, terms, chunks);
 }
 
 template <typename T>
-void box_dispatch(void* dst, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks, int vec,
+void box_dispatch(const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks, int vec,
                   int max_rank, cudaStream_t s) {
   constexpr int VV = 16 / sizeof(T);
-  if (vec) box_rank_dispatch<T, VV>(dst, cells, terms, chunks, nchunks, max_rank, s);
-  else box_rank_dispatch<T, 1>(dst, cells, terms, chunks, nchunks, max_rank, s);
+  if (vec) box_rank_dispatch<T, VV>(cells, terms, chunks, nchunks, max_rank, s);
+  else box_rank_dispatch<T, 1>(cells, terms, chunks, nchunks, max_rank, s);
 }
 
 // ---- elementwise -----------------------------------------------------------
@@ -694,13 +694,13 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs a) {
 
 }  // namespace
 
-void launch_box(void* dst, int dtype, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks,
-                int vec, int max_rank, cudaStream_t s) {
+void launch_box(int dtype, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks, int nchunks, int vec,
+                int max_rank, cudaStream_t s) {
   if (nchunks == 0) return;
   switch (dtype) {
-    case DT_F32: box_dispatch<float>(dst, cells, terms, chunks, nchunks, vec, max_rank, s); break;
-    case DT_BF16: box_dispatch<__nv_bfloat16>(dst, cells, terms, chunks, nchunks, vec, max_rank, s); break;
-    case DT_I32: box_dispatch<int>(dst, cells, terms, chunks, nchunks, vec, max_rank, s); break;
+    case DT_F32: box_dispatch<float>(cells, terms, chunks, nchunks, vec, max_rank, s); break;
+    case DT_BF16: box_dispatch<__nv_bfloat16>(cells, terms, chunks, nchunks, vec, max_rank, s); break;
+    case DT_I32: box_dispatch<int>(cells, terms, chunks, nchunks, vec, max_rank, s); break;
     default: throw std::runtime_error("box: bad dtype");
   }
   check_launch("box_kernel");

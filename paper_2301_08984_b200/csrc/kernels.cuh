@@ -33,6 +33,7 @@ struct DevTerm {
 };
 
 struct DevCell {
+  void* dst;  // destination buffer (cells of a batched launch write different buffers)
   std::int64_t ext[kBoxRank];
   std::int64_t dst_str[kBoxRank];
   std::int64_t dst_off;
@@ -145,7 +146,7 @@ struct GemmSchedule {
 // `max_rank` is the highest cell rank in the launch; every chunk covers at
 // most kBoxChunkUnits vector units of one cell.
 constexpr int kBoxChunkUnits = 1024;
-void launch_box(void* dst, int dtype, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks,
+void launch_box(int dtype, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks,
                 int nchunks, int vec, int max_rank, cudaStream_t s);
 void launch_ew(int op, int dtype, const void* const* ins, int nin, void* out, std::int64_t count, cudaStream_t s);
 // reduce-sum over the middle axis of [outer][axis_len][inner]; column

@@ -359,8 +359,10 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
     // Box tables need every rank's arena: built by peer_import.
   } else {
     build_box_tables();
+    plan_box_batches();
   }
   kernels_per_step_ = 0;
+  for (const auto& b : batches_) kernels_per_step_ += static_cast<int>(b.launches.size());
   for (const auto& in : prog_.instrs) {
     if (exec_lane_[in.id] < 0) continue;
     if (peer_) {
@@ -369,7 +371,9 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
     }
     switch (in.kind) {
       case InstrKind::nop: break;
-      case InstrKind::box: kernels_per_step_ += static_cast<int>(irt_[in.id].box.size()); break;  // peer: at import
+      case InstrKind::box:  // peer: at import; batched: counted with the batch
+        if (batch_of_.empty() || batch_of_[in.id] < 0) kernels_per_step_ += static_cast<int>(irt_[in.id].box.size());
+        break;
       case InstrKind::emb_grad: kernels_per_step_ += in.n_idx > 0 ? 2 : 1; break;
       case InstrKind::reduce:
         kernels_per_step_ += reduce_launches(in.outer, in.axis_len, in.inner, dt_of(prog_.buffers[in.out_bufs[0]].dtype));
@@ -445,6 +449,11 @@ Executor::~Executor() {
   if (d2h_stream_) cudaStreamDestroy(d2h_stream_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
+  for (auto& b : batches_)
+    if (b.done) cudaEventDestroy(b.done);
+  for (auto e : batch_join_) cudaEventDestroy(e);
+  for (auto& kv : batch_streams_)
+    for (auto st : kv.second) cudaStreamDestroy(st);
   if (ev_begin_) cudaEventDestroy(ev_begin_);
   if (ev_end_) cudaEventDestroy(ev_end_);
   if (origin_) cudaStreamDestroy(origin_);
@@ -712,6 +721,7 @@ void Executor::build_box_tables() {
           dc.ext[d] = d < pad ? 1 : c->extents[d - pad];
           dc.dst_str[d] = d < pad ? 0 : c->dst_strides[d - pad];
         }
+        dc.dst = buf_ptr(in.out_bufs[0]);
         dc.dst_off = c->dst_offset;
         dc.elems = c->elems();
         dc.nterms = static_cast<int>(c->terms.size());
@@ -738,25 +748,148 @@ void Executor::build_box_tables() {
         }
       }
       if (chunks.empty()) continue;
-      DeviceGuard dg(lanes_[in.lane].gpu);
-      std::size_t cb = cells.size() * sizeof(DevCell), tb = terms.size() * sizeof(DevTerm),
-                  hb = chunks.size() * sizeof(DevChunk);
-      char* mem = nullptr;
-      ck(cudaMalloc(&mem, cb + tb + hb + 64), "cudaMalloc(box table)");
-      table_allocs_.push_back(mem);
-      ck(cudaMemcpy(mem, cells.data(), cb, cudaMemcpyHostToDevice), "box table");
-      if (tb) ck(cudaMemcpy(mem + cb, terms.data(), tb, cudaMemcpyHostToDevice), "box table");
-      ck(cudaMemcpy(mem + cb + tb, chunks.data(), hb, cudaMemcpyHostToDevice), "box table");
       BoxLaunch bl;
-      bl.cells = reinterpret_cast<DevCell*>(mem);
-      bl.terms = reinterpret_cast<DevTerm*>(mem + cb);
-      bl.chunks = reinterpret_cast<DevChunk*>(mem + cb + tb);
       bl.nchunks = static_cast<int>(chunks.size());
       bl.vec = g;
       bl.max_rank = max_rank;
+      bl.dtype = dt_of(ob.dtype);
+      bl.h_cells = std::move(cells);
+      bl.h_terms = std::move(terms);
+      bl.h_chunks = std::move(chunks);
+      upload_box(bl, lanes_[in.lane].gpu);
       irt_[in.id].box.push_back(bl);
     }
   }
+}
+
+void Executor::upload_box(BoxLaunch& bl, int gpu) {
+  DeviceGuard dg(gpu);
+  const std::size_t cb = bl.h_cells.size() * sizeof(DevCell), tb = bl.h_terms.size() * sizeof(DevTerm),
+                    hb = bl.h_chunks.size() * sizeof(DevChunk);
+  char* mem = nullptr;
+  ck(cudaMalloc(&mem, cb + tb + hb + 64), "cudaMalloc(box table)");
+  table_allocs_.push_back(mem);
+  ck(cudaMemcpy(mem, bl.h_cells.data(), cb, cudaMemcpyHostToDevice), "box table");
+  if (tb) ck(cudaMemcpy(mem + cb, bl.h_terms.data(), tb, cudaMemcpyHostToDevice), "box table");
+  ck(cudaMemcpy(mem + cb + tb, bl.h_chunks.data(), hb, cudaMemcpyHostToDevice), "box table");
+  bl.cells = reinterpret_cast<DevCell*>(mem);
+  bl.terms = reinterpret_cast<DevTerm*>(mem + cb);
+  bl.chunks = reinterpret_cast<DevChunk*>(mem + cb + tb);
+  bl.nchunks = static_cast<int>(bl.h_chunks.size());
+}
+
+// Greedy over the issue order, one open batch per GPU: a box instruction
+// joins its GPU's open batch; an instruction that depends on a member first
+// closes (launches) that batch. Members are therefore pairwise independent
+// and every consumer is issued after its batch.
+void Executor::plan_box_batches() {
+  const std::size_t n = prog_.instrs.size();
+  batch_of_.assign(n, -1);
+  flush_before_.assign(prog_.issue_order.size(), {});
+  flush_end_.clear();
+  batches_.clear();
+  const char* env = std::getenv("PLANC_B200_BATCH");
+  if (!opt_.batch_boxes || (env && env[0] == '0') || rank_mode_ || peer_ || opt_.reuse_memory) return;
+  std::map<int, std::vector<int>> open;  // gpu -> members
+  std::vector<char> pending(n, 0);
+  auto close = [&](int gpu, std::vector<int>* where) {
+    auto& mem = open[gpu];
+    if (mem.empty()) return;
+    BoxBatch b;
+    b.members = mem;
+    b.gpu = gpu;
+    for (int m : mem) {
+      batch_of_[m] = static_cast<int>(batches_.size());
+      pending[m] = 0;
+    }
+    where->push_back(static_cast<int>(batches_.size()));
+    batches_.push_back(std::move(b));
+    mem.clear();
+  };
+  for (std::size_t pos = 0; pos < prog_.issue_order.size(); ++pos) {
+    const int id = prog_.issue_order[pos];
+    if (exec_lane_[id] < 0) continue;
+    const Instr& in = prog_.instrs[id];
+    for (int d : in.deps)
+      if (d >= 0 && pending[d]) close(lanes_[exec_lane_[d]].gpu, &flush_before_[pos]);
+    if (in.kind == InstrKind::box && !irt_[id].aliased && !irt_[id].box.empty()) {
+      open[lanes_[exec_lane_[id]].gpu].push_back(id);
+      pending[id] = 1;
+    }
+  }
+  for (auto& kv : open) close(kv.first, &flush_end_);
+  // Merged tables per (element type, vector width, rank); streams; events.
+  constexpr int kBatchStreams = 4;
+  std::map<int, int> next_stream;
+  for (auto& b : batches_) {
+    DeviceGuard dg(b.gpu);
+    auto& pool = batch_streams_[b.gpu];
+    if (pool.empty()) {
+      pool.resize(kBatchStreams);
+      for (auto& st : pool) ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "batch stream");
+      for (std::size_t k = 0; k < pool.size(); ++k) {
+        cudaEvent_t e = nullptr;
+        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        batch_join_.push_back(e);
+      }
+    }
+    b.stream = pool[next_stream[b.gpu]++ % kBatchStreams];
+    ck(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming), "event");
+    std::map<std::tuple<int, int, int>, BoxLaunch> merged;
+    for (int m : b.members) {
+      for (const BoxLaunch& bl : irt_[m].box) {
+        BoxLaunch& t = merged[{bl.dtype, bl.vec, bl.max_rank}];
+        t.dtype = bl.dtype;
+        t.vec = bl.vec;
+        t.max_rank = bl.max_rank;
+        const int cell0 = static_cast<int>(t.h_cells.size()), term0 = static_cast<int>(t.h_terms.size());
+        for (DevCell c : bl.h_cells) {
+          c.term0 += term0;
+          t.h_cells.push_back(c);
+        }
+        t.h_terms.insert(t.h_terms.end(), bl.h_terms.begin(), bl.h_terms.end());
+        for (DevChunk ch : bl.h_chunks) {
+          ch.cell += cell0;
+          t.h_chunks.push_back(ch);
+        }
+      }
+      // the member's dependencies are awaited by events from the batch stream
+      for (int d : prog_.instrs[m].deps) {
+        if (d < 0 || exec_lane_[d] < 0 || batch_of_[d] >= 0 || irt_[d].done) continue;
+        DeviceGuard dg2(lanes_[exec_lane_[d]].gpu);
+        ck(cudaEventCreateWithFlags(&irt_[d].done, cudaEventDisableTiming), "event");
+      }
+    }
+    for (auto& kv : merged) {
+      if (b.members.size() == 1) {
+        b.launches = irt_[b.members[0]].box;  // the member's own tables
+        break;
+      }
+      upload_box(kv.second, b.gpu);
+      b.launches.push_back(std::move(kv.second));
+    }
+  }
+  // Non-members whose consumers moved to a batch keep their events; a
+  // member's consumer waits for the batch event.
+}
+
+cudaStream_t Executor::issued_stream(int id) const {
+  return batch_of_.empty() || batch_of_[id] < 0 ? stream_of(prog_.instrs[id]) : batches_[batch_of_[id]].stream;
+}
+
+cudaEvent_t Executor::done_event(int id) const {
+  return batch_of_.empty() || batch_of_[id] < 0 ? irt_[id].done : batches_[batch_of_[id]].done;
+}
+
+void Executor::launch_batch(int bi) {
+  BoxBatch& b = batches_[bi];
+  if (gpus_.size() > 1) ck(cudaSetDevice(b.gpu), "cudaSetDevice");
+  for (int m : b.members)
+    for (int d : prog_.instrs[m].deps)
+      if (d >= 0 && exec_lane_[d] >= 0 && issued_stream(d) != b.stream)
+        ck(cudaStreamWaitEvent(b.stream, done_event(d), 0), "wait dep (batch)");
+  for (const auto& bl : b.launches) launch_box(bl.dtype, bl.cells, bl.terms, bl.chunks, bl.nchunks, bl.vec, bl.max_rank, b.stream);
+  ck(cudaEventRecord(b.done, b.stream), "record batch");
 }
 
 char* Executor::host_stage(std::int64_t bytes) {
@@ -924,9 +1057,8 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
                      static_cast<float>(in.eps), s);
       return;
     case InstrKind::box: {
-      int dt = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
       for (const auto& bl : irt_[in.id].box) {
-        launch_box(buf_ptr(in.out_bufs[0]), dt, bl.cells, bl.terms, bl.chunks, bl.nchunks, bl.vec, bl.max_rank, s);
+        launch_box(bl.dtype, bl.cells, bl.terms, bl.chunks, bl.nchunks, bl.vec, bl.max_rank, s);
       }
       return;
     }
@@ -947,24 +1079,31 @@ void Executor::issue_step(bool, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>
   for (int l = 0; l < prog_.num_lanes; ++l)
     if (owned_[l])
       for (auto s : lanes_[l].stream) ck(cudaStreamWaitEvent(s, ev_begin_, 0), "wait begin");
-  for (int id : prog_.issue_order) {
+  for (auto& kv : batch_streams_)
+    for (auto s : kv.second) ck(cudaStreamWaitEvent(s, ev_begin_, 0), "wait begin");
+  for (std::size_t pos = 0; pos < prog_.issue_order.size(); ++pos) {
+    if (!flush_before_.empty())
+      for (int b : flush_before_[pos]) {
+        launch_batch(b);
+        cur = batches_[b].gpu;
+      }
+    const int id = prog_.issue_order[pos];
     const int el = exec_lane_[id];
     if (el < 0) continue;  // another rank's instruction
+    if (!batch_of_.empty() && batch_of_[id] >= 0) continue;  // launched with its batch
     const Instr& in = prog_.instrs[id];
     cudaStream_t s = stream_of(in);
     set_dev(lanes_[el].gpu);
     for (int d : in.deps) {
       if (exec_lane_[d] < 0) continue;
-      const Instr& p = prog_.instrs[d];
-      (void)p;
-      if (exec_lane_[d] != el || exec_stream_[d] != exec_stream_[id])
-        ck(cudaStreamWaitEvent(s, irt_[d].done, 0), "wait dep");
+      if (issued_stream(d) != s) ck(cudaStreamWaitEvent(s, done_event(d), 0), "wait dep");
     }
     peer_wait(id, s);
     launch_instr(in, s);
     peer_signal(id, s);
     if (irt_[id].done) ck(cudaEventRecord(irt_[id].done, s), "record done");
   }
+  for (int b : flush_end_) launch_batch(b);
   join_lanes();
   peer_step_end(origin_);
 }
@@ -977,9 +1116,15 @@ void Executor::join_lanes() {
     for (int k = 0; k < kLaneStreams; ++k)
       ck(cudaEventRecord(lane_join_[kLaneStreams * l + k], lanes_[l].stream[k]), "record join");
   }
+  std::size_t j = 0;
+  for (auto& kv : batch_streams_) {
+    if (gpus_.size() > 1) ck(cudaSetDevice(kv.first), "cudaSetDevice");
+    for (auto st : kv.second) ck(cudaEventRecord(batch_join_[j++], st), "record join");
+  }
   ck(cudaSetDevice(lanes_[first_lane_].gpu), "cudaSetDevice");
   for (auto e : lane_join_)
     if (e) ck(cudaStreamWaitEvent(origin_, e, 0), "wait join");
+  for (auto e : batch_join_) ck(cudaStreamWaitEvent(origin_, e, 0), "wait join");
 }
 
 void Executor::ensure_graph() {

@@ -55,6 +55,7 @@ struct ExecOptions {
   bool alias_copies = true;             // same-GPU whole-buffer copies (recv, identity) become aliases
   bool scatter_allreduce = true;        // all-reduce partials leave the GEMM epilogue as reduce-scatter slices
   bool reuse_memory = false;            // timed mode: bytes the plan frees are reused within the step
+  bool batch_boxes = true;              // independent adapter (box) instructions of one GPU in shared launches
 };
 
 // ProgramOptions as the executor uses them: epilogue fusion only for GEMMs
@@ -150,6 +151,26 @@ class Executor {
     int nchunks = 0;
     int vec = 0;
     int max_rank = 1;
+    int dtype = 0;
+    // host copies (merged into batched launches)
+    std::vector<DevCell> h_cells;
+    std::vector<DevTerm> h_terms;
+    std::vector<DevChunk> h_chunks;
+  };
+  // Adapter batching (ExecOptions::batch_boxes): box instructions of one GPU
+  // that are pending together in issue order — none depends on another,
+  // nothing issued so far consumes them — run as one launch per (element
+  // type, vector width, cell rank): their cell tables concatenated, each
+  // cell writing its own destination. The batch runs on one of the GPU's
+  // batch streams after every member's dependencies; its event orders every
+  // member's consumers. Many small adapter launches (split / concat /
+  // all-to-all pieces of co-sharded and pipelined plans) become a few.
+  struct BoxBatch {
+    std::vector<int> members;
+    int gpu = 0;
+    cudaStream_t stream = nullptr;
+    std::vector<BoxLaunch> launches;
+    cudaEvent_t done = nullptr;
   };
   struct InstrRt {
     std::vector<BoxLaunch> box;
@@ -164,6 +185,11 @@ class Executor {
   bool gemm_streamk_ok(int lane) const;  // the lane has its GPU to itself
   cudaStream_t stream_of(const Instr& in) const;
   void build_box_tables();
+  void plan_box_batches();
+  void upload_box(BoxLaunch& bl, int gpu);
+  void launch_batch(int b);
+  cudaStream_t issued_stream(int id) const;
+  cudaEvent_t done_event(int id) const;
   void place_inputs();
   void issue_step(bool timing_events, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* ev);
   void launch_instr(const Instr& in, cudaStream_t s);
@@ -210,6 +236,12 @@ class Executor {
   std::vector<int> alias_;  // per buffer: -1, or the buffer whose memory it shares
   std::vector<int> gpus_;  // distinct devices
   std::vector<void*> table_allocs_;
+  std::vector<BoxBatch> batches_;
+  std::vector<int> batch_of_;                    // per instruction: its batch, or -1
+  std::vector<std::vector<int>> flush_before_;   // per issue position: batches launched before it
+  std::vector<int> flush_end_;                   // batches launched after the last instruction
+  std::map<int, std::vector<cudaStream_t>> batch_streams_;  // per GPU
+  std::vector<cudaEvent_t> batch_join_;
   std::vector<bool> overwritten_;       // REUSE_MEMORY: buffers whose bytes a later buffer takes
   std::set<int> placed_;                // graph inputs placed by set_input
   void* host_stage_ = nullptr;          // pinned staging for set_input / get_output conversions
