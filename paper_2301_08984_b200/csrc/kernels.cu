@@ -125,6 +125,9 @@ __device__ __forceinline__ void store_any(void* p, int dt, std::int64_t i, float
 // are read through the read-only path (warp-uniform broadcasts); no smem,
 // no barriers.
 
+__device__ __forceinline__ float box_max(float a, float b) { return fmaxf(a, b); }  // = ew_kernel's max
+__device__ __forceinline__ int box_max(int a, int b) { return a > b ? a : b; }
+
 constexpr int kBoxThreads = 256;
 constexpr int kBoxUnroll = 4;
 
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(kBoxThreads) box_kernel(const DevCell* __restr
     const DevTerm* tm = terms + term0 + t;
     const T* src = reinterpret_cast<const T*>(__ldg(reinterpret_cast<const unsigned long long*>(&tm->src)));
     const std::int64_t toff = __ldg(&tm->offset);
-    const int add = __ldg(&tm->add);
+    const int op = __ldg(&tm->op);
     std::int64_t tstr[R];
 #pragma unroll
     for (int d = 0; d < R; ++d) tstr[d] = __ldg(&tm->str[d]);
@@ -197,12 +200,18 @@ __global__ void __launch_bounds__(kBoxThreads) box_kernel(const DevCell* __restr
     }
 #pragma unroll
     for (int x = 0; x < U; ++x) {
-      if (add) {
+      if (op == 1) {
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[x][i] += v[x][i];
-      } else {
+      } else if (op == 0) {
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[x][i] = v[x][i];
+      } else if (op == 2) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[x][i] *= v[x][i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[x][i] = box_max(acc[x][i], v[x][i]);
       }
     }
   }

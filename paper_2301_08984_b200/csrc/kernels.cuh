@@ -28,7 +28,7 @@ struct DevTerm {
   const void* src;
   std::int64_t offset;
   std::int64_t str[kBoxRank];
-  int add;
+  int op;  // 0 copy, 1 add, 2 mul, 3 max (elementwise instructions run as box cells)
   int pad;
 };
 

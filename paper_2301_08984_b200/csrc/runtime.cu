@@ -378,7 +378,13 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       case InstrKind::reduce:
         kernels_per_step_ += reduce_launches(in.outer, in.axis_len, in.inner, dt_of(prog_.buffers[in.out_bufs[0]].dtype));
         break;
-      case InstrKind::ew: kernels_per_step_ += 1 + (in.count % 8 != 0 ? 1 : 0); break;
+      case InstrKind::ew:
+        if (!irt_[in.id].box.empty()) {
+          if (batch_of_.empty() || batch_of_[in.id] < 0) kernels_per_step_ += static_cast<int>(irt_[in.id].box.size());
+        } else {
+          kernels_per_step_ += 1 + (in.count % 8 != 0 ? 1 : 0);
+        }
+        break;
       default: kernels_per_step_ += 1;
     }
     if (in.kind == InstrKind::gemm) {
@@ -732,7 +738,7 @@ void Executor::build_box_tables() {
           dt.src = buf_ptr(t.buffer);
           dt.offset = t.offset;
           for (int d = 0; d < R; ++d) dt.str[d] = d < pad ? 0 : t.strides[d - pad];
-          dt.add = t.add ? 1 : 0;
+          dt.op = t.add ? 1 : 0;
           terms.push_back(dt);
         }
         int ci = static_cast<int>(cells.size());
@@ -758,6 +764,64 @@ void Executor::build_box_tables() {
       bl.h_chunks = std::move(chunks);
       upload_box(bl, lanes_[in.lane].gpu);
       irt_[in.id].box.push_back(bl);
+    }
+  }
+}
+
+// Elementwise instructions as box cells (with batching on): one rank-1
+// cell per instruction, terms = the operands in fold order (copy, then the
+// op) — the same fp32 fold and single rounding as ew_kernel, so the same
+// bits; 16-byte vectors for the aligned body, a scalar cell for the tail.
+// (More than 8 operands keep ew_kernel: it rounds every 8-operand chunk.)
+void Executor::build_ew_tables() {
+  for (const auto& in : prog_.instrs) {
+    if (in.kind != InstrKind::ew || exec_lane_[in.id] < 0 || in.in_bufs.empty() || in.in_bufs.size() > 8) continue;
+    if (in.ew != EwOp::add && in.ew != EwOp::mul && in.ew != EwOp::max) continue;
+    const BufferDesc& ob = prog_.buffers[in.out_bufs[0]];
+    if (ob.dtype == DType::i32) continue;
+    const std::int64_t V = 16 / dtype_size(ob.dtype);
+    const int opc = in.ew == EwOp::add ? 1 : in.ew == EwOp::mul ? 2 : 3;
+    bool aligned = reinterpret_cast<std::uintptr_t>(buf_ptr(in.out_bufs[0])) % 16 == 0;
+    for (int b : in.in_bufs) aligned = aligned && reinterpret_cast<std::uintptr_t>(buf_ptr(b)) % 16 == 0;
+    const std::int64_t body = aligned ? in.count / V * V : 0;
+    for (int g = 1; g >= 0; --g) {
+      const std::int64_t lo = g ? 0 : body, n = g ? body : in.count - body;
+      if (n <= 0) continue;
+      const std::int64_t width = g ? V : 1;
+      BoxLaunch bl;
+      bl.vec = g;
+      bl.max_rank = 1;
+      bl.dtype = dt_of(ob.dtype);
+      DevCell dc{};
+      dc.dst = buf_ptr(in.out_bufs[0]);
+      dc.rank = 1;
+      dc.ext[0] = n;
+      dc.dst_str[0] = 1;
+      dc.dst_off = lo;
+      dc.elems = n;
+      dc.nterms = static_cast<int>(in.in_bufs.size());
+      dc.term0 = 0;
+      dc.vec = static_cast<int>(width);
+      for (std::size_t t = 0; t < in.in_bufs.size(); ++t) {
+        DevTerm dt{};
+        dt.src = buf_ptr(in.in_bufs[t]);
+        dt.offset = lo;
+        dt.str[0] = 1;
+        dt.op = t == 0 ? 0 : opc;
+        bl.h_terms.push_back(dt);
+      }
+      bl.h_cells.push_back(dc);
+      const std::int64_t units = n / width;
+      if (units >= (std::int64_t(1) << 32)) continue;
+      for (std::int64_t b = 0; b < units; b += kBoxChunkUnits) {
+        DevChunk ch{};
+        ch.cell = 0;
+        ch.begin = b;
+        ch.count = std::min<std::int64_t>(kBoxChunkUnits, units - b);
+        bl.h_chunks.push_back(ch);
+      }
+      upload_box(bl, lanes_[in.lane].gpu);
+      irt_[in.id].box.push_back(std::move(bl));
     }
   }
 }
@@ -790,6 +854,7 @@ void Executor::plan_box_batches() {
   batches_.clear();
   const char* env = std::getenv("PLANC_B200_BATCH");
   if (!opt_.batch_boxes || (env && env[0] == '0') || rank_mode_ || peer_ || opt_.reuse_memory) return;
+  build_ew_tables();
   std::map<int, std::vector<int>> open;  // gpu -> members
   std::vector<char> pending(n, 0);
   auto close = [&](int gpu, std::vector<int>* where) {
@@ -812,7 +877,7 @@ void Executor::plan_box_batches() {
     const Instr& in = prog_.instrs[id];
     for (int d : in.deps)
       if (d >= 0 && pending[d]) close(lanes_[exec_lane_[d]].gpu, &flush_before_[pos]);
-    if (in.kind == InstrKind::box && !irt_[id].aliased && !irt_[id].box.empty()) {
+    if ((in.kind == InstrKind::box || in.kind == InstrKind::ew) && !irt_[id].aliased && !irt_[id].box.empty()) {
       open[lanes_[exec_lane_[id]].gpu].push_back(id);
       pending[id] = 1;
     }
@@ -1024,6 +1089,11 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
       return;
     }
     case InstrKind::ew: {
+      if (!irt_[in.id].box.empty()) {  // as box cells (build_ew_tables)
+        for (const auto& bl : irt_[in.id].box)
+          launch_box(bl.dtype, bl.cells, bl.terms, bl.chunks, bl.nchunks, bl.vec, bl.max_rank, s);
+        return;
+      }
       int dt = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
       std::vector<const void*> ptrs;
       for (int b : in.in_bufs) ptrs.push_back(buf_ptr(b));

@@ -186,6 +186,7 @@ class Executor {
   cudaStream_t stream_of(const Instr& in) const;
   void build_box_tables();
   void plan_box_batches();
+  void build_ew_tables();
   void upload_box(BoxLaunch& bl, int gpu);
   void launch_batch(int b);
   cudaStream_t issued_stream(int id) const;
