@@ -57,7 +57,8 @@ def gpt_stack_doc(layers: int, tokens: int, hidden: int, elem_size: int = 2) -> 
 
 
 def gpt_block_doc(tokens: int, hidden: int, elem_size: int = 2, train: bool = True,
-                  layer: int = 0, prefix: str = "", base: int = 0, x_in=None, g_out=None) -> dict:
+                  layer: int = 0, prefix: str = "", base: int = 0, x_in=None, g_out=None,
+                  seq_parallel: bool = False) -> dict:
     """GPT-3-style transformer block proxy.
 
     Forward: Q = X·Wq, K = X·Wk (column-parallel), S = Q*K (attention proxy),
@@ -65,6 +66,10 @@ def gpt_block_doc(tokens: int, hidden: int, elem_size: int = 2, train: bool = Tr
     F = max(F1, Z) (ReLU proxy), Y = F·W2 [4H,H] (row-parallel), OUT = Y + X2.
     ``train`` adds the mlp_doc-style backward (transposed GEMMs; reference
     proj/tests/testutil.cpp:55-154) and one optimizer add per weight.
+    ``seq_parallel`` names the residual adds "spres1" / "spres2" so the
+    megatron_tp sProgram splits them on the token dim (Megatron sequence
+    parallelism: reduce-scatter after the row-parallel GEMMs, all-gather
+    before the column-parallel ones).
     """
     T, H, F = tokens, hidden, 4 * hidden
     e = elem_size
@@ -81,6 +86,7 @@ def gpt_block_doc(tokens: int, hidden: int, elem_size: int = 2, train: bool = Tr
                    ("F1", (T, F)), ("Z", (T, F)), ("Fa", (T, F)), ("Y", (T, H)), ("OUT", (T, H))):
         pts.append(_pt(ids[a], shp, "activation", e))
     p = prefix
+    r1, r2 = ("spres1", "spres2") if seq_parallel else ("res1", "res2")
     A = {"layer": layer, "batch_dim": 0}
     mm = lambda m, n, k: 2.0 * m * n * k  # noqa: E731
     ops = [
@@ -88,11 +94,11 @@ def gpt_block_doc(tokens: int, hidden: int, elem_size: int = 2, train: bool = Tr
         _op(p + "colk", "matmul", [X, ids["Wk"]], [ids["K"]], "forward", mm(T, H, H), A),
         _op(p + "tpmul", "mul", [ids["Q"], ids["K"]], [ids["S"]], "forward", T * H, A),
         _op(p + "rowo", "matmul", [ids["S"], ids["Wo"]], [ids["O"]], "forward", mm(T, H, H), A),
-        _op(p + "res1", "add", [ids["O"], X], [ids["X2"]], "forward", T * H, A),
+        _op(p + r1, "add", [ids["O"], X], [ids["X2"]], "forward", T * H, A),
         _op(p + "colf1", "matmul", [ids["X2"], ids["W1"]], [ids["F1"]], "forward", mm(T, F, H), A),
         _op(p + "tprelu", "max", [ids["F1"], ids["Z"]], [ids["Fa"]], "forward", T * F, A),
         _op(p + "roww2", "matmul", [ids["Fa"], ids["W2"]], [ids["Y"]], "forward", mm(T, H, F), A),
-        _op(p + "res2", "add", [ids["Y"], ids["X2"]], [ids["OUT"]], "forward", T * H, A),
+        _op(p + r2, "add", [ids["Y"], ids["X2"]], [ids["OUT"]], "forward", T * H, A),
     ]
     if train:
         g = {k: b + 100 + v for k, v in dict(OUT=0, Y=1, Fa=2, F1=3, X2a=4, X2=5, O=6, S=7, Q=8,
@@ -118,14 +124,14 @@ def gpt_block_doc(tokens: int, hidden: int, elem_size: int = 2, train: bool = Tr
         TA = dict(B, transpose_a=True)
         TB = dict(B, transpose_b=True)
         ops += [
-            _op(p + "gres2", "identity", [g["OUT"]], [g["Y"]], "backward", 0, B, p + "res2"),
+            _op(p + "gres2", "identity", [g["OUT"]], [g["Y"]], "backward", 0, B, p + r2),
             _op(p + "gw2a", "matmul", [g["Y"], ids["W2"]], [g["Fa"]], "backward", mm(T, F, H), TB, p + "roww2"),
             _op(p + "gw2w", "matmul", [ids["Fa"], g["Y"]], [gw["W2"]], "backward", mm(F, H, T), TA, p + "roww2"),
             _op(p + "grelu", "mul", [g["Fa"], ids["Z"]], [g["F1"]], "backward", T * F, B, p + "tprelu"),
             _op(p + "gf1a", "matmul", [g["F1"], ids["W1"]], [g["X2a"]], "backward", mm(T, H, F), TB, p + "colf1"),
             _op(p + "gf1w", "matmul", [ids["X2"], g["F1"]], [gw["W1"]], "backward", mm(H, F, T), TA, p + "colf1"),
-            _op(p + "gres2x", "add", [g["X2a"], g["OUT"]], [g["X2"]], "backward", T * H, B, p + "res2"),
-            _op(p + "gres1", "identity", [g["X2"]], [g["O"]], "backward", 0, B, p + "res1"),
+            _op(p + "gres2x", "add", [g["X2a"], g["OUT"]], [g["X2"]], "backward", T * H, B, p + r2),
+            _op(p + "gres1", "identity", [g["X2"]], [g["O"]], "backward", 0, B, p + r1),
             _op(p + "gwoa", "matmul", [g["O"], ids["Wo"]], [g["S"]], "backward", mm(T, H, H), TB, p + "rowo"),
             _op(p + "gwow", "matmul", [ids["S"], g["O"]], [gw["Wo"]], "backward", mm(H, H, T), TA, p + "rowo"),
             _op(p + "gmulq", "mul", [g["S"], ids["K"]], [g["Q"]], "backward", T * H, B, p + "tpmul"),
@@ -134,7 +140,7 @@ def gpt_block_doc(tokens: int, hidden: int, elem_size: int = 2, train: bool = Tr
             _op(p + "gqw", "matmul", [X, g["Q"]], [gw["Wq"]], "backward", mm(H, H, T), TA, p + "colq"),
             _op(p + "gka", "matmul", [g["K"], ids["Wk"]], [g["Xk"]], "backward", mm(T, H, H), TB, p + "colk"),
             _op(p + "gkw", "matmul", [X, g["K"]], [gw["Wk"]], "backward", mm(H, H, T), TA, p + "colk"),
-            _op(p + "gres1x", "add", [g["Xq"], g["Xk"], g["X2"]], [g["X"]], "backward", 2 * T * H, B, p + "res1"),
+            _op(p + "gres1x", "add", [g["Xq"], g["Xk"], g["X2"]], [g["X"]], "backward", 2 * T * H, B, p + r1),
         ]
         for w, kind in (("Wq", "optc"), ("Wk", "optc"), ("W1", "optc"), ("Wo", "optr"), ("W2", "optr")):
             shp = next(q["shape"] for q in pts if q["id"] == ids[w])

@@ -118,7 +118,11 @@ char* blob_out(const TensorMap& m, std::int64_t* nbytes) {
 // forward ops whose id starts with "col" split output dim 1 (column-parallel
 // GEMM), "row" value-split (row-parallel GEMM -> partial sums), "tp" split
 // output dim 1 (elementwise ops between the column- and row-parallel GEMMs),
-// everything else is replicated. Backward ops follow their forward op through
+// "sp" split output dim 0 (sequence parallelism: the residual ops between
+// the row- and column-parallel GEMMs hold a slice of the tokens, so the
+// front end materialises reduce-scatter after row-parallel GEMMs and
+// all-gather before column-parallel ones — Megatron-SP), everything else is
+// replicated. Backward ops follow their forward op through
 // adapt_backward (transform.cpp:503); optimizer ops "optc" / "optr" split like
 // their column- / row-parallel weight (dim 1 / dim 0), others are replicated.
 StrategyInfo megatron_tp(PlanGraph& g, const ClusterSpec& env,
@@ -145,6 +149,8 @@ StrategyInfo megatron_tp(PlanGraph& g, const ClusterSpec& env,
     if (op.direction == OpDirection::forward) {
       if (is("col") || is("tp")) {
         algo = split_algo(1, n);
+      } else if (is("sp")) {
+        algo = split_algo(0, n);
       } else if (is("row")) {
         algo = value_split_algo(n);
       }

@@ -20,11 +20,19 @@
 //                    into the GEMM's workspace (HBM-bound, 12 B per element).
 //   gemm_x3_kernel   persistent, one CTA per SM, 128 x 128 output tiles in
 //                    grouped raster order, 6 warps: TMA producer (four planes
-//                    per k-block: A_hi, A_lo, B_hi, B_lo, 128B-swizzled, a
-//                    3-stage 64 KB ring), single-thread MMA issuer (3 MMAs
-//                    of 128x128x8 per 32-byte k-step, two 128-column fp32
-//                    TMEM accumulators), 4 epilogue warps (tcgen05.ld ->
-//                    swizzled smem -> TMA bulk store of fp32 C).
+//                    per k-block: A_hi, A_lo, B_hi, B_lo, a 3-stage 64 KB
+//                    ring; K-major operands 128B-swizzled, MN-major ones in
+//                    the 128B / 32-byte-atom swizzle UMMA requires for 32-bit
+//                    MN-major operands), single-thread MMA issuer (3 MMAs of
+//                    128x128x8 per 32-byte k-step), 4 epilogue warps.
+//
+// Promotion: the tensor core adds each MMA's products into the fp32 TMEM
+// accumulator without round-to-nearest (the error grows ~linearly with the
+// number of MMAs: 7e-6 normwise at k = 1000, 3e-5 at k = 4096 measured with
+// one accumulator per tile), so every X3_CHUNK_KB k-blocks the MMA warp
+// switches to a fresh TMEM accumulator (a ring of four 128-column slots)
+// and the epilogue warps add the finished chunk into fp32 registers with
+// ordinary (round-to-nearest) adds, storing the tile after its last chunk.
 #include "gemm_sm100_impl.cuh"
 
 namespace planc_b200 {
@@ -37,10 +45,26 @@ constexpr int X3_A_BYTES = BM * 128;             // one plane of the A tile, 16 
 constexpr int X3_B_BYTES = X3_BN * 128;          // one plane of the B tile, 16 KB
 constexpr int X3_STAGE_BYTES = 2 * (X3_A_BYTES + X3_B_BYTES);
 constexpr int X3_STAGES = 3;
-constexpr int X3_STAGING = 4 * 2 * 4096;         // 4 warps x 2 buffers x 32x32 fp32
+constexpr int X3_EPI_WARPS = 8;                  // two per TMEM lane quarter, 64 columns each
+constexpr int X3_THREADS = 64 + 32 * X3_EPI_WARPS;
+constexpr int X3_STAGING = X3_EPI_WARPS * 4096;  // one 32x32 fp32 staging buffer per warp
 constexpr int X3_SMEM = X3_STAGES * X3_STAGE_BYTES + X3_STAGING + 1024 + 1024;
-constexpr int X3_TMEM_COLS = 2 * X3_BN;
+constexpr int X3_SLOTS = 4;       // TMEM accumulator ring (chunk partials)
+constexpr int X3_TMEM_COLS = X3_SLOTS * X3_BN;
+constexpr int X3_CHUNK_KB = 8;    // k-blocks (256 k) accumulated in TMEM before promotion
 static_assert(X3_SMEM <= 227 * 1024, "3xTF32 ring above the shared memory limit");
+
+// 32-bit MN-major operands: SWIZZLE_128B_BASE32B (32-byte atoms, 4-row
+// groups; descriptor layout type 1), the only UMMA layout for MN-major tf32.
+__device__ __forceinline__ std::uint64_t smem_desc_b32(std::uint32_t addr, std::uint32_t lbo, std::uint32_t sbo) {
+  std::uint64_t d = 0;
+  d |= static_cast<std::uint64_t>((addr >> 4) & 0x3FFFu);
+  d |= static_cast<std::uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<std::uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;  // version
+  d |= 1ull << 61;  // SWIZZLE_128B_BASE32B
+  return d;
+}
 
 struct X3Maps {
   CUtensorMap ah, al, bh, bl, c;
@@ -124,7 +148,7 @@ __global__ void __launch_bounds__(kX3SplitThreads) x3_split_kernel(const __grid_
 }
 
 template <bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(X3_THREADS, 1)
     gemm_x3_kernel(const __grid_constant__ X3Maps mp, int m, int n, int k, int group_m) {
   extern __shared__ std::uint8_t smem_raw[];
   std::uint8_t* smem =
@@ -135,8 +159,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(staging + X3_STAGING);
   std::uint64_t* empty = full + X3_STAGES;
   std::uint64_t* tfull = empty + X3_STAGES;
-  std::uint64_t* tempty = tfull + 2;
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  std::uint64_t* tempty = tfull + X3_SLOTS;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + X3_SLOTS);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -154,9 +178,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < X3_SLOTS; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], X3_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -212,13 +236,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr std::uint32_t idesc = x3_idesc(A_MN, B_MN);
-      int it = 0, local = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
-        const int acc = local & 1;
-        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const std::uint32_t d = tmem + static_cast<std::uint32_t>(acc * X3_BN);
+      int it = 0, q = 0;  // ring position, chunk counter
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        std::uint32_t d = 0;
         for (int kb = 0; kb < num_k; ++kb, ++it) {
+          const int slot = q % X3_SLOTS;
+          if (kb % X3_CHUNK_KB == 0) {  // a fresh accumulator for this chunk
+            mbar_wait(&tempty[slot], ((q / X3_SLOTS) & 1) ^ 1);
+            tc_fence_after();
+            d = tmem + static_cast<std::uint32_t>(slot * X3_BN);
+          }
           const int s = it % X3_STAGES;
           mbar_wait(&full[s], (it / X3_STAGES) & 1);
           tc_fence_after();
@@ -227,59 +254,85 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const std::uint32_t bh = base + 2 * X3_A_BYTES, bl = bh + X3_B_BYTES;
 #pragma unroll
           for (int kk = 0; kk < X3_BK / 8; ++kk) {
-            // k-step of 8 fp32 = 32 bytes: K-major advances 32 B along the
-            // swizzled row (8-row groups 1024 B apart); MN-major advances 8
-            // k-rows = 1024 B, 32-element MN blocks 4 KB apart (LBO).
+            // k-step of 8 fp32: K-major advances 32 B along the 128B-swizzled
+            // row (8-row groups 1024 B apart); MN-major advances 8 k-rows =
+            // 1024 B in the 32B-atom layout (4-row groups 512 B apart,
+            // 32-element MN blocks 4 KB apart).
             auto desc = [&](std::uint32_t b, bool mn) {
-              return mn ? smem_desc(b + kk * 1024, 4096, 1024) : smem_desc(b + kk * 32, 16, 1024);
+              return mn ? smem_desc_b32(b + kk * 1024, 4096, 512) : smem_desc(b + kk * 32, 16, 1024);
             };
             const std::uint64_t dah = desc(ah, A_MN), dal = desc(al, A_MN);
             const std::uint64_t dbh = desc(bh, B_MN), dbl = desc(bl, B_MN);
+            const std::uint32_t first = (kb % X3_CHUNK_KB != 0 || kk != 0) ? 1u : 0u;
             // small terms first
-            tc_mma_tf32(d, dah, dbl, idesc, (kb != 0 || kk != 0) ? 1u : 0u);
+            tc_mma_tf32(d, dah, dbl, idesc, first);
             tc_mma_tf32(d, dal, dbh, idesc, 1u);
             tc_mma_tf32(d, dah, dbh, idesc, 1u);
           }
           tc_commit(&empty[s]);
+          if (kb % X3_CHUNK_KB == X3_CHUNK_KB - 1 || kb == num_k - 1) {
+            tc_commit(&tfull[slot]);  // chunk partial complete
+            ++q;
+          }
         }
-        tc_commit(&tfull[acc]);
       }
       pdl_trigger();
     }
   } else {
-    // Epilogue warps 2..5: TMEM lane quarter q = warp % 4; each 32x32 fp32
-    // chunk: tcgen05.ld -> 128B-swizzled staging -> TMA store.
-    const int q = warp % 4;
-    std::uint8_t* stg = staging + (warp - 2) * 2 * 4096;
-    int sb = 0, local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    // Epilogue warps 2..9: TMEM lane quarter qr = warp % 4, column half
+    // (warp - 2) / 4, one output row per lane: every chunk partial of the
+    // tile is added into 64 fp32 registers (round-to-nearest), then the row
+    // half leaves in 32-column pieces through 128B-swizzled staging and TMA
+    // stores.
+    constexpr int HC = X3_BN / 2;
+    const int qr = warp % 4;
+    const int c0 = ((warp - 2) / 4) * HC;
+    std::uint8_t* stg = staging + (warp - 2) * 4096;
+    int q = 0;
+    const int nch = (num_k + X3_CHUNK_KB - 1) / X3_CHUNK_KB;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(t, tiles_m, tiles_n, mb, nb, group_m);
-      const int acc = local & 1;
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
-      tc_fence_after();
-      const std::uint32_t base =
-          tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(acc * X3_BN);
+      float acc[HC];
 #pragma unroll 1
-      for (int c = 0; c < X3_BN / 32; ++c) {
-        std::uint32_t r[32];
-        tmem_ld32(base + c * 32, r);
-        if (c == X3_BN / 32 - 1) {  // accumulator drained: the MMA warp may refill it
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+      for (int c = 0; c < nch; ++c, ++q) {
+        const int slot = q % X3_SLOTS;
+        mbar_wait(&tfull[slot], (q / X3_SLOTS) & 1);
+        tc_fence_after();
+        const std::uint32_t base = tmem + (static_cast<std::uint32_t>(qr * 32) << 16) +
+                                   static_cast<std::uint32_t>(slot * X3_BN + c0);
+        if (c == 0) {
+#pragma unroll
+          for (int j = 0; j < HC / 32; ++j) {
+            std::uint32_t r[32];
+            tmem_ld32(base + j * 32, r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[j * 32 + i] = __uint_as_float(r[i]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < HC / 32; ++j) {
+            std::uint32_t r[32];
+            tmem_ld32(base + j * 32, r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[j * 32 + i] += __uint_as_float(r[i]);
+          }
         }
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        tc_fence_before();
         __syncwarp();
-        std::uint8_t* buf = stg + sb * 4096;
+        if (lane == 0) mbar_arrive(&tempty[slot]);  // the MMA warp may refill this slot
+      }
+#pragma unroll
+      for (int j = 0; j < HC / 32; ++j) {
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+        __syncwarp();
 #pragma unroll
         for (int v = 0; v < 8; ++v)
-          *reinterpret_cast<uint4*>(buf + lane * 128 + ((v ^ (lane & 7)) << 4)) =
-              make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+          *reinterpret_cast<float4*>(stg + lane * 128 + ((v ^ (lane & 7)) << 4)) =
+              make_float4(acc[j * 32 + 4 * v], acc[j * 32 + 4 * v + 1], acc[j * 32 + 4 * v + 2], acc[j * 32 + 4 * v + 3]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) tma_store_2d(&mp.c, buf, nb * X3_BN + c * 32, mb * BM + q * 32);
-        sb ^= 1;
+        if (lane == 0) tma_store_2d(&mp.c, stg, nb * X3_BN + c0 + j * 32, mb * BM + qr * 32);
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -292,8 +345,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-// fp32 row-major [rows][cols], box {32 cols (128 B), box_rows}, 128B swizzle.
-CUtensorMap make_map_f32(const void* base, std::int64_t rows, std::int64_t cols, int box_rows) {
+// fp32 row-major [rows][cols], box {32 cols (128 B), box_rows}: 128B swizzle
+// (K-major operand) or 128B with 32-byte atoms (MN-major operand, `mn`).
+CUtensorMap make_map_f32(const void* base, std::int64_t rows, std::int64_t cols, int box_rows, bool mn = false) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -301,7 +355,8 @@ CUtensorMap make_map_f32(const void* base, std::int64_t rows, std::int64_t cols,
   cuuint32_t box[2] = {32, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (fp32) failed: " + std::to_string(r));
   return m;
@@ -324,12 +379,12 @@ void launch_x3_typed(const GemmArgs& a, const GemmSchedule& sc, float* ah, float
   X3Maps mp;
   std::memset(&mp, 0, sizeof(mp));
   // A: [m][k] (K-major) or [k][m] (MN-major); B: [k][n] (MN-major) or [n][k].
-  mp.ah = A_MN ? make_map_f32(ah, a.k, a.m, X3_BK) : make_map_f32(ah, a.m, a.k, BM);
-  mp.al = A_MN ? make_map_f32(al, a.k, a.m, X3_BK) : make_map_f32(al, a.m, a.k, BM);
-  mp.bh = B_MN ? make_map_f32(bh, a.k, a.n, X3_BK) : make_map_f32(bh, a.n, a.k, X3_BN);
-  mp.bl = B_MN ? make_map_f32(bl, a.k, a.n, X3_BK) : make_map_f32(bl, a.n, a.k, X3_BN);
+  mp.ah = A_MN ? make_map_f32(ah, a.k, a.m, X3_BK, true) : make_map_f32(ah, a.m, a.k, BM);
+  mp.al = A_MN ? make_map_f32(al, a.k, a.m, X3_BK, true) : make_map_f32(al, a.m, a.k, BM);
+  mp.bh = B_MN ? make_map_f32(bh, a.k, a.n, X3_BK, true) : make_map_f32(bh, a.n, a.k, X3_BN);
+  mp.bl = B_MN ? make_map_f32(bl, a.k, a.n, X3_BK, true) : make_map_f32(bl, a.n, a.k, X3_BN);
   mp.c = make_store_map(a.C, a.m, a.n, false);
-  pdl_launch("gemm_x3_kernel", kern, dim3(sc.grid), dim3(NUM_THREADS), X3_SMEM, s, mp, static_cast<int>(a.m),
+  pdl_launch("gemm_x3_kernel", kern, dim3(sc.grid), dim3(X3_THREADS), X3_SMEM, s, mp, static_cast<int>(a.m),
              static_cast<int>(a.n), static_cast<int>(a.k), GROUP_M);
 }
 
