@@ -65,9 +65,12 @@ extern "C" {
 #define PLANC_B200_NO_GROUPING 0x40u    /* every GEMM its own launch (default: independent same-shape
                                            GEMMs of a lane that become ready together share one grouped
                                            tensor-core launch) */
-#define PLANC_B200_NO_BATCH 0x1000u     /* every adapter (box) instruction its own launch (default: box
-                                           instructions of one GPU pending together in issue order —
-                                           pairwise independent — share one launch per element type) */
+#define PLANC_B200_BATCH 0x1000u        /* box and elementwise instructions of one GPU pending together in issue
+                                           order (pairwise independent) share one launch per element type
+                                           (default off: measured slower — it couples the lanes of a GPU) */
+#define PLANC_B200_NO_GATHER 0x2000u    /* materialise every concat / all-gather (default: one whose output only
+                                           feeds tensor-core GEMMs as an operand is dropped and the GEMMs' TMA
+                                           loads read the row pieces in place — the all-gather -> GEMM prologue) */
 #define PLANC_B200_SERIAL_LANES 0x8u    /* one stream per lane: a lane's tasks run strictly in plan
                                            order (default: only data dependencies and sync edges order
                                            a lane's work, spread over several streams) */

@@ -44,7 +44,8 @@ NO_ALIAS = 0x100
 NO_SCATTER = 0x200
 FUSE_ACT = 0x400
 REUSE_MEMORY = 0x800
-NO_BATCH = 0x1000
+BATCH = 0x1000
+NO_GATHER = 0x2000
 
 
 class PlancError(RuntimeError):

@@ -67,7 +67,8 @@ ExecOptions exec_options(uint32_t flags) {
   opt.alias_copies = (flags & PLANC_B200_NO_ALIAS) == 0;
   opt.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0;
   opt.reuse_memory = (flags & PLANC_B200_REUSE_MEMORY) != 0;
-  opt.batch_boxes = (flags & PLANC_B200_NO_BATCH) == 0;
+  opt.batch_boxes = (flags & PLANC_B200_BATCH) != 0;
+  opt.gather_operands = (flags & PLANC_B200_NO_GATHER) == 0;
   return opt;
 }
 
@@ -78,6 +79,7 @@ ProgramOptions describe_options(uint32_t flags) {
   po.fuse_act = (flags & PLANC_B200_FUSE_ACT) != 0;
   po.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0 && tc;
   po.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0 && tc;
+  po.gather_operands = (flags & PLANC_B200_NO_GATHER) == 0 && tc;
   return po;
 }
 
@@ -150,6 +152,7 @@ int planc_b200_describe_rank(const char* plan_json, const int* lane_rank, int nu
     const std::vector<int> lr(lane_rank, lane_rank + num_lanes);
     if ((flags & PLANC_B200_PEER_MEMORY) == 0) {
       po.two_phase_allreduce = false;  // NCCL exchange steps: whole-buffer ncclAllReduce
+      po.gather_operands = false;      // pieces on other ranks are not addressable
       *json_out = dup(localize(build_program(plan, po), lr).describe_json());
       return;
     }

@@ -198,6 +198,19 @@ int gemm_sm100_launches(const GemmArgs& a) {
   return gemm_sm100_schedule(a, device_sms()).splits > 1 ? 2 : 1;
 }
 
+void gemm_sm100_gather_maps(const GemmArgs& a, void* host_out) {
+  static_assert(sizeof(CUtensorMap) == kTensorMapBytes, "tensor map size");
+  GemmSchedule sc = gemm_sm100_schedule(a, device_sms());
+  if ((sc.sk_ctas > 0 || sc.splits > 1) && (a.ws == nullptr || a.ws_bytes < sc.ws_bytes)) {
+    GemmArgs b = a;
+    b.no_workspace = true;
+    sc = gemm_sm100_schedule(b, device_sms());
+  }
+  CUtensorMap* out = static_cast<CUtensorMap*>(host_out);
+  std::memset(out, 0, kGatherMapSlots * sizeof(CUtensorMap));
+  encode_gather_maps(a, sc, out);
+}
+
 int gemm_sm100_tile_n(const GemmArgs& a) { return gemm_sm100_schedule(a, 148).bn; }
 
 std::int64_t gemm_sm100_workspace_bytes(const GemmArgs& a) {

@@ -139,6 +139,15 @@ struct SkParams {
   // evict_first — streamed once, 2: evict_last — re-read across raster
   // groups while the other operand streams past it).
   int hint_a = 0, hint_b = 0;
+  // Gathered operands (all-gather / concat -> GEMM prologue): operand A (B)
+  // is the row-wise concatenation of pieces of gather_rows_a (_b) rows each,
+  // stored row-major wherever their producers left them (this lane, another
+  // lane, NVLink peer memory). Their tensor maps live in global memory
+  // (gather_maps: A pieces [0, 8), B pieces [8, 16)); a TMA box at stored
+  // row r reads piece r / gather_rows at row r % gather_rows (pieces are
+  // whole multiples of every box height).
+  int gather_rows_a = 0, gather_rows_b = 0;
+  const CUtensorMap* gather_maps = nullptr;
   long long sk_iters = 0;
   float* partials = nullptr;  // [sk_ctas][2 slots][4 quarters][BN/32 chunks][8][32] float4
   int* counters = nullptr;    // [(tiles - dp_tiles) * 4], zero between launches
@@ -569,6 +578,19 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
     if (lane == 0) {
       int it = 0;  // global k-block counter across work items (ring position)
       const std::uint64_t pol_a = l2_policy(sk.hint_a), pol_b = l2_policy(sk.hint_b);
+      // Gathered operand: the piece holding stored row `row` (made piece-local).
+      auto pick_a = [&](const CUtensorMap* dflt, int& row) -> const CUtensorMap* {
+        if (sk.gather_rows_a == 0) return dflt;
+        const int q = row / sk.gather_rows_a;
+        row -= q * sk.gather_rows_a;
+        return sk.gather_maps + q;
+      };
+      auto pick_b = [&](const CUtensorMap* dflt, int& row) -> const CUtensorMap* {
+        if (sk.gather_rows_b == 0) return dflt;
+        const int q = row / sk.gather_rows_b;
+        row -= q * sk.gather_rows_b;
+        return sk.gather_maps + kMaxGemmGroup + q;
+      };
       work([&](int t, int kb0, int kb1, int half) {
         int p, mb, nb;
         coords(t, p, mb, nb);
@@ -590,19 +612,22 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
             const std::uint32_t lb = cluster_addr(&full[s], 0);
             std::uint8_t* a = sA + s * A_STAGE_BYTES;
             std::uint8_t* b = sB + s * B_STAGE_BYTES;
+            int ra = A_MN ? kb * BK : m0, rb = B_MN ? kb * BK : n0 + r * (BN / 2);
+            const CUtensorMap* mA = pick_a(tmA, ra);
+            const CUtensorMap* mB = pick_b(tmB, rb);
             if (A_MN) {
 #pragma unroll
               for (int j = 0; j < BM / 64; ++j)
-                tma_load_2d_2sm_hint(a + j * (64 * BK * 2), tmA, m0 + 64 * j, kb * BK, lb, pol_a);
+                tma_load_2d_2sm_hint(a + j * (64 * BK * 2), mA, m0 + 64 * j, ra, lb, pol_a);
             } else {
-              tma_load_2d_2sm_hint(a, tmA, kb * BK, m0, lb, pol_a);
+              tma_load_2d_2sm_hint(a, mA, kb * BK, ra, lb, pol_a);
             }
             if (B_MN) {
 #pragma unroll
               for (int j = 0; j < BN / 128; ++j)
-                tma_load_2d_2sm_hint(b + j * (64 * BK * 2), tmB, n0 + r * (BN / 2) + 64 * j, kb * BK, lb, pol_b);
+                tma_load_2d_2sm_hint(b + j * (64 * BK * 2), mB, n0 + r * (BN / 2) + 64 * j, rb, lb, pol_b);
             } else {
-              tma_load_2d_2sm_hint(b, tmB, kb * BK, n0 + r * (BN / 2), lb, pol_b);
+              tma_load_2d_2sm_hint(b, mB, kb * BK, rb, lb, pol_b);
             }
           }
           return;
@@ -614,29 +639,37 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
           mbar_expect_tx(&full[s], A_STAGE_BYTES + B_STAGE_BYTES);
           std::uint8_t* a = sA + s * A_STAGE_BYTES;
           std::uint8_t* b = sB + s * B_STAGE_BYTES;
+          int ra = A_MN ? kb * BK : m0;
+          const CUtensorMap* mA = pick_a(tmA, ra);
           if (A_MN) {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d_hint(a + j * (64 * BK * 2), tmA, m0 + 64 * j, kb * BK, &full[s], pol_a);
+              tma_load_2d_hint(a + j * (64 * BK * 2), mA, m0 + 64 * j, ra, &full[s], pol_a);
           } else {
-            tma_load_2d_hint(a, tmA, kb * BK, m0, &full[s], pol_a);
+            tma_load_2d_hint(a, mA, kb * BK, ra, &full[s], pol_a);
           }
           if constexpr (CL) {
             // this CTA's half of the B tile, multicast to both CTAs of the pair
             const int r = t & 1;
+            int rb = B_MN ? kb * BK : n0 + r * (BN / 2);
+            const CUtensorMap* mB = pick_b(tmB, rb);
             if (B_MN) {
 #pragma unroll
               for (int j = r * (BN / 128); j < (r + 1) * (BN / 128); ++j)
-                tma_load_2d_mc(b + j * (64 * BK * 2), tmB, n0 + 64 * j, kb * BK, &full[s], 0x3);
+                tma_load_2d_mc(b + j * (64 * BK * 2), mB, n0 + 64 * j, rb, &full[s], 0x3);
             } else {
-              tma_load_2d_mc(b + r * (BN / 2) * 128, tmB, kb * BK, n0 + r * (BN / 2), &full[s], 0x3);
+              tma_load_2d_mc(b + r * (BN / 2) * 128, mB, kb * BK, rb, &full[s], 0x3);
             }
-          } else if (B_MN) {
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d_hint(b + j * (64 * BK * 2), tmB, n0 + 64 * j, kb * BK, &full[s], pol_b);
           } else {
-            tma_load_2d_hint(b, tmB, kb * BK, n0, &full[s], pol_b);
+            int rb = B_MN ? kb * BK : n0;
+            const CUtensorMap* mB = pick_b(tmB, rb);
+            if (B_MN) {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_2d_hint(b + j * (64 * BK * 2), mB, n0 + 64 * j, rb, &full[s], pol_b);
+            } else {
+              tma_load_2d_hint(b, mB, kb * BK, rb, &full[s], pol_b);
+            }
           }
         }
       });
@@ -1212,6 +1245,11 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
   sk.scatter_rows = a.scatter > 0 ? static_cast<int>(a.scatter_rows) : 0;
   l2_plan(a, sk);
   for (int i = 0; i < a.scatter; ++i) sk.scatter_dst[i] = a.gC[i];
+  if (a.gather_maps) {
+    sk.gather_rows_a = static_cast<int>(a.gather_rows_a);
+    sk.gather_rows_b = static_cast<int>(a.gather_rows_b);
+    sk.gather_maps = static_cast<const CUtensorMap*>(a.gather_maps);
+  }
   const std::int64_t m_pad = (a.m + BM - 1) / BM * BM, n_pad = (a.n + BN - 1) / BN * BN;
   if (sc.splits > 1) {
     // Partials: fp32 [ng * splits * m_pad][n_pad], stored like an fp32 C.
@@ -1232,6 +1270,22 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
     pdl_launch("splitk_reduce_kernel", splitk_reduce_kernel<C_BF16>, dim3(blocks), dim3(256), 0, s,
                static_cast<const float4*>(a.ws), out, sc.splits, static_cast<int>(a.m), static_cast<int>(a.n),
                static_cast<int>(m_pad), static_cast<int>(n_pad), ng);
+  }
+}
+
+// Tensor maps of a gathered operand's pieces with the box the launch of
+// schedule `sc` loads (gemm_sm100_gather_maps).
+inline void encode_gather_maps(const GemmArgs& a, const GemmSchedule& sc, CUtensorMap* out) {
+  const bool a_mn = a.ta, b_mn = !a.tb;
+  for (int i = 0; i < a.gather_a; ++i) {
+    // A: K-major [m][k] boxes of BM rows; MN-major [k][m] boxes of BK rows
+    out[i] = a_mn ? make_map(a.gather_a_ptr[i], a.gather_rows_a, a.m, BK)
+                  : make_map(a.gather_a_ptr[i], a.gather_rows_a, a.k, BM);
+  }
+  for (int i = 0; i < a.gather_b; ++i) {
+    // B: MN-major [k][n] boxes of BK rows; K-major [n][k] boxes of BN (pairs: BN/2) rows
+    out[kMaxGemmGroup + i] = b_mn ? make_map(a.gather_b_ptr[i], a.gather_rows_b, a.n, BK)
+                                  : make_map(a.gather_b_ptr[i], a.gather_rows_b, a.k, sc.occ >= 4 ? sc.bn / 2 : sc.bn);
   }
 }
 

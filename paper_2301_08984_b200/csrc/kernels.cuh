@@ -111,6 +111,15 @@ struct GemmArgs {
   // No workspace at all: the schedule is chosen among data-parallel
   // variants only (no stream-K, no split-K).
   bool no_workspace = false;
+  // Gathered operands (all-gather / concat -> GEMM prologue, group == 1):
+  // A (B) is the row-wise concatenation, in stored layout, of gather_a
+  // (gather_b) pieces of gather_rows_a (_b) rows each; gather_maps = device
+  // copy of their tensor maps (gemm_sm100_gather_maps; 16 slots).
+  int gather_a = 0, gather_b = 0;
+  std::int64_t gather_rows_a = 0, gather_rows_b = 0;
+  const void* gather_a_ptr[kMaxGemmGroup] = {};
+  const void* gather_b_ptr[kMaxGemmGroup] = {};
+  const void* gather_maps = nullptr;
 };
 
 // Launch schedule of the tcgen05 GEMM: tile width, persistent grid, and the
@@ -203,6 +212,12 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms);
 std::int64_t gemm_sm100_workspace_bytes(const GemmArgs& a);  // on the current device
 int gemm_sm100_launches(const GemmArgs& a);                   // kernels per GEMM (2 with split-K)
 void launch_gemm_sm100(const GemmArgs& a, cudaStream_t s);
+// Host: the 16 tensor maps (A pieces, then B pieces at slot 8) of a GEMM
+// with gathered operands, boxed for the launch the schedule will choose;
+// the caller copies them to device memory and passes it as gather_maps.
+constexpr int kGatherMapSlots = 2 * kMaxGemmGroup;
+constexpr std::size_t kTensorMapBytes = 128;
+void gemm_sm100_gather_maps(const GemmArgs& a, void* host_out /* kGatherMapSlots * 128 bytes */);
 // 3xTF32 tcgen05 GEMM for fp32 operands and output (gemm_x3.cu); reached
 // through the gemm_sm100_* entry points above.
 bool gemm_x3_eligible(const GemmArgs& a);

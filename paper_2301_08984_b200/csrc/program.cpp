@@ -782,6 +782,7 @@ Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt) {
   b.run();
   if (opt.two_phase_allreduce) two_phase_allreduce(b.P, opt);
   if (opt.fuse_epilogues) fuse_gemm_epilogues(b.P, opt);
+  if (opt.gather_operands && opt.gemm_groupable) gather_gemm_operands(b.P, opt);
   if (opt.group_gemms && opt.gemm_groupable) group_gemms(b.P, opt);
   return std::move(b.P);
 }
@@ -831,7 +832,9 @@ void group_gemms(Program& P, const ProgramOptions& opt) {
     Instr& g = P.instrs[id];
     // Reduce-scatter GEMMs (scatter > 0) carry k receive slices as their
     // outputs: a grouped launch holds one output per member, so they never join.
-    if (g.kind != InstrKind::gemm || !g.fused.empty() || g.group != 1 || g.scatter > 0) continue;
+    if (g.kind != InstrKind::gemm || !g.fused.empty() || g.group != 1 || g.scatter > 0 || !g.gather[0].empty() ||
+        !g.gather[1].empty())
+      continue;
     const DType da = P.buffers[g.in_bufs[0]].dtype, db = P.buffers[g.in_bufs[1]].dtype,
                 dc = P.buffers[g.out_bufs[0]].dtype;
     if (!opt.gemm_groupable(g, da, db, dc)) continue;
@@ -889,6 +892,102 @@ void group_gemms(Program& P, const ProgramOptions& opt) {
       in.deps.erase(std::unique(in.deps.begin(), in.deps.end()), in.deps.end());
       in.deps.erase(std::remove(in.deps.begin(), in.deps.end(), in.id), in.deps.end());
     }
+  }
+}
+
+void gather_gemm_operands(Program& P, const ProgramOptions& opt) {
+  const int nb = static_cast<int>(P.buffers.size());
+  std::vector<std::vector<int>> readers(nb);
+  for (const auto& in : P.instrs) {
+    if (in.kind == InstrKind::nop) continue;
+    std::set<int> r;
+    for (int b : in.in_bufs) r.insert(b);
+    for (const auto& c : in.cells)
+      for (const auto& t : c.terms) r.insert(t.buffer);
+    for (const auto& fe : in.fused)
+      for (int b : fe.in_bufs) r.insert(b);
+    for (const auto& x : in.xfers) r.insert(x.src);
+    for (int b : r) readers[b].push_back(in.id);
+  }
+  std::set<int> outputs;
+  for (const auto& o : P.outputs)
+    for (int b : o.second) outputs.insert(b);
+  // Piece rows must be whole multiples of every TMA box height the GEMM may
+  // load (BM = 128 rows, BK = 64 k-rows, BN <= 256 columns-as-rows).
+  constexpr std::int64_t kPieceRowAlign = 256;
+  for (auto& bx : P.instrs) {
+    if (bx.kind != InstrKind::box || bx.out_bufs.size() != 1 || bx.cells.empty() ||
+        bx.cells.size() > static_cast<std::size_t>(kMaxGemmGroupInstr))
+      continue;
+    const int O = bx.out_bufs[0];
+    const BufferDesc& ob = P.buffers[O];
+    if (ob.shape.size() != 2 || ob.graph_input || outputs.count(O) || ob.dtype != DType::bf16) continue;
+    const std::int64_t R = ob.shape[0], C = ob.shape[1];
+    // Cells: whole row blocks, one plain copy of a dense piece each.
+    std::vector<std::pair<std::int64_t, int>> pieces;  // (first row, source buffer)
+    bool ok = true;
+    std::int64_t rows = -1;
+    for (const auto& c : bx.cells) {
+      if (c.terms.size() != 1 || c.terms[0].add || c.terms[0].offset != 0 || c.dst_offset % C != 0) {
+        ok = false;
+        break;
+      }
+      const Term& t = c.terms[0];
+      const BufferDesc& sb = P.buffers[t.buffer];
+      const std::int64_t e = c.elems();
+      bool dense = false;
+      if (c.rank == 1) dense = c.dst_strides[0] == 1 && t.strides[0] == 1;
+      if (c.rank == 2)
+        dense = c.extents[1] == C && c.dst_strides[0] == C && c.dst_strides[1] == 1 && t.strides[0] == C &&
+                t.strides[1] == 1;
+      if (!dense || e % C != 0 || sb.elems != e || sb.dtype != ob.dtype || sb.dead) {
+        ok = false;
+        break;
+      }
+      if (rows < 0) rows = e / C;
+      ok = ok && e / C == rows;
+      pieces.push_back({c.dst_offset / C, t.buffer});
+    }
+    if (!ok || rows <= 0 || rows % kPieceRowAlign != 0 || static_cast<std::int64_t>(pieces.size()) * rows != R) continue;
+    std::sort(pieces.begin(), pieces.end());
+    for (std::size_t i = 0; i < pieces.size(); ++i) ok = ok && pieces[i].first == static_cast<std::int64_t>(i) * rows;
+    // Readers: tensor-core GEMMs only, O as one plain operand.
+    std::vector<std::pair<int, int>> uses;  // (gemm, operand index)
+    for (int r : readers[O]) {
+      const Instr& g = P.instrs[r];
+      const bool gem = g.kind == InstrKind::gemm && g.group == 1 && g.scatter == 0 && g.in_bufs.size() == 2 &&
+                       (g.in_bufs[0] == O) != (g.in_bufs[1] == O);
+      bool fused_reads = false;
+      for (const auto& fe : g.fused)
+        for (int b : fe.in_bufs) fused_reads = fused_reads || b == O;
+      if (!ok || !gem || fused_reads || g.lane != bx.lane ||
+          !opt.gemm_groupable(g, P.buffers[g.in_bufs[0]].dtype, P.buffers[g.in_bufs[1]].dtype,
+                              P.buffers[g.out_bufs[0]].dtype)) {
+        ok = false;
+        break;
+      }
+      uses.push_back({r, g.in_bufs[0] == O ? 0 : 1});
+    }
+    if (!ok || uses.empty()) continue;
+    for (auto [r, j] : uses) {
+      Instr& g = P.instrs[r];
+      for (const auto& pc : pieces) g.gather[j].push_back(pc.second);
+      g.gather_rows[j] = rows;
+      g.in_bufs[j] = pieces[0].second;  // (O is dead: never written nor read)
+      // The GEMM waits for the pieces' producers (bx's dependencies).
+      for (int d : bx.deps) g.deps.push_back(d);
+      g.deps.erase(std::remove(g.deps.begin(), g.deps.end(), bx.id), g.deps.end());
+      std::sort(g.deps.begin(), g.deps.end());
+      g.deps.erase(std::unique(g.deps.begin(), g.deps.end()), g.deps.end());
+      g.label += "<gather:" + bx.label + ">";
+    }
+    // bx stays as a nop (its deps still order anything a sync edge hangs on it).
+    bx.kind = InstrKind::nop;
+    bx.cells.clear();
+    bx.out_bufs.clear();
+    bx.bytes = 0;
+    P.buffers[O].dead = true;
+    P.buffers[O].producer = -1;
   }
 }
 
@@ -1494,7 +1593,13 @@ std::string Program::describe_json() const {
        << static_cast<int>(in.row_op) << ",\"seg\":" << in.seg << ",\"eps\":" << in.eps << ",\"flops\":" << in.flops
        << ",\"bytes\":" << in.bytes << ",\"wire_bytes\":" << in.wire_bytes << ",\"coll_group\":" << in.coll_group
        << ",\"allreduce\":" << (in.allreduce ? "true" : "false") << ",\"group\":" << in.group
-       << ",\"scatter\":" << in.scatter << ",\"scatter_rows\":" << in.scatter_rows << ",\"fused\":[";
+       << ",\"scatter\":" << in.scatter << ",\"scatter_rows\":" << in.scatter_rows << ",\"gather\":[";
+    for (int j = 0; j < 2; ++j) {
+      os << (j ? "," : "") << "{\"rows\":" << in.gather_rows[j] << ",\"pieces\":[";
+      for (std::size_t q = 0; q < in.gather[j].size(); ++q) os << (q ? "," : "") << in.gather[j][q];
+      os << "]}";
+    }
+    os << "],\"fused\":[";
     for (std::size_t f = 0; f < in.fused.size(); ++f) {
       const auto& fe = in.fused[f];
       os << (f ? "," : "") << "{\"ew_instr\":" << fe.ew_instr << ",\"ew\":" << static_cast<int>(fe.op)
@@ -1582,6 +1687,8 @@ namespace {
 template <class F>
 void for_each_use(const Instr& in, F&& f) {
   for (int b : in.in_bufs) f(b, false);
+  for (int j = 0; j < 2; ++j)
+    for (int b : in.gather[j]) f(b, false);
   for (int b : in.out_bufs) f(b, true);
   for (const auto& c : in.cells)
     for (const auto& t : c.terms) f(t.buffer, false);

@@ -147,6 +147,15 @@ struct Instr {
     int out_buf = -1;
   };
   std::vector<FusedEw> fused;
+  // gemm operand gathered in place (all-gather / concat -> GEMM prologue,
+  // SURVEY §8f rank 1): operand j (0 = A, 1 = B) is the row-wise
+  // concatenation, in its stored layout, of gather[j] (pieces of
+  // gather_rows[j] rows each, in order) — the concatenating box instruction
+  // is gone (a nop), its output buffer is dead and in_bufs[j] names the
+  // first piece; the GEMM's TMA loads read each piece where its producer
+  // left it.
+  std::vector<int> gather[2];
+  std::int64_t gather_rows[2] = {0, 0};
   // accounting (algorithmic, from masks)
   double flops = 0;
   double bytes = 0;       // HBM bytes read + written
@@ -183,6 +192,12 @@ struct ProgramOptions {
   // grouped tensor-core launch (one tile space: no per-GEMM wave tail, one
   // launch instead of several) — for GEMMs the predicate accepts.
   bool group_gemms = true;
+  // A box instruction that only concatenates whole row blocks of its pieces
+  // into a buffer read by nothing but tensor-core GEMMs (as an operand) is
+  // dropped: those GEMMs read the pieces in place (Instr::gather) — the
+  // all-gather / concat -> GEMM prologue. Single-process and peer-memory
+  // modes (the pieces must be addressable by the GEMM's lane).
+  bool gather_operands = true;
   bool (*gemm_groupable)(const Instr& gemm, DType a, DType b, DType c) = nullptr;
   bool (*gemm_fusable)(const Instr& gemm, DType a, DType b, DType c) = nullptr;
 };
@@ -220,6 +235,10 @@ void fuse_gemm_epilogues(Program& p, const ProgramOptions& opt);
 // opt.group_gemms): members become nops, the first member of each group
 // carries every member's operands and results.
 void group_gemms(Program& p, const ProgramOptions& opt);
+
+// Gather-prologue pass (opt.gather_operands; run after epilogue fusion,
+// before grouping): see ProgramOptions::gather_operands.
+void gather_gemm_operands(Program& p, const ProgramOptions& opt);
 
 // The two-phase all-reduce pass (ProgramOptions::two_phase_allreduce), run
 // by build_program before epilogue fusion. Rebuilds the program in issue

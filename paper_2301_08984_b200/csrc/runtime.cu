@@ -181,6 +181,8 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   // NCCL exchange steps lower whole-buffer all-reduce groups to
   // ncclAllReduce; every other mode runs them as two box phases.
   po.two_phase_allreduce = !(rank && !rank->peer_memory);
+  // Gathered operands read pieces in place: not across NCCL ranks.
+  po.gather_operands = opt.gather_operands && opt.allow_tensor_cores && !(rank && !rank->peer_memory);
   // The scatter epilogue pays when the slices cross GPUs (the transfer rides
   // in the GEMM); with every lane on one GPU it only trades TMA stores for
   // plain ones (measured ~2 % slower, profiles/r01/ab_scatter.jsonl).
@@ -419,6 +421,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       ck(cudaMemset(lr.gemm_ws[k], 0, lr.gemm_ws_bytes[k]), "memset(gemm workspace)");  // stream-K counters
     }
   }
+  if (!peer_) build_gather_maps();  // peer mode: at import (pieces may live on other ranks)
 }
 
 Executor::~Executor() {
@@ -606,6 +609,7 @@ void Executor::peer_import(const unsigned char* blobs, std::int64_t blob_bytes) 
   }
   peer_ready_ = true;
   build_box_tables();
+  build_gather_maps();
   for (const auto& in : prog_.instrs)
     if (in.kind == InstrKind::box && exec_lane_[in.id] >= 0) kernels_per_step_ += static_cast<int>(irt_[in.id].box.size());
   kernels_per_step_ += 1 + (rc_.world > 1 ? 1 : 0);  // epoch + step barrier
@@ -852,17 +856,22 @@ void Executor::plan_box_batches() {
   flush_before_.assign(prog_.issue_order.size(), {});
   flush_end_.clear();
   batches_.clear();
+  // PLANC_B200_BATCH: 1 = one open batch per GPU (lanes sharing it are
+  // batched together), 2 = one per lane; unset / 0 = ExecOptions.
   const char* env = std::getenv("PLANC_B200_BATCH");
-  if (!opt_.batch_boxes || (env && env[0] == '0') || rank_mode_ || peer_ || opt_.reuse_memory) return;
+  const int mode = env ? std::atoi(env) : (opt_.batch_boxes ? 1 : 0);
+  if (mode == 0 || rank_mode_ || peer_ || opt_.reuse_memory) return;
   build_ew_tables();
-  std::map<int, std::vector<int>> open;  // gpu -> members
+  const bool per_lane = mode == 2;
+  std::map<int, std::vector<int>> open;  // gpu (or lane) -> members
   std::vector<char> pending(n, 0);
-  auto close = [&](int gpu, std::vector<int>* where) {
-    auto& mem = open[gpu];
+  auto key_of = [&](int id) { return per_lane ? exec_lane_[id] : lanes_[exec_lane_[id]].gpu; };
+  auto close = [&](int key, std::vector<int>* where) {
+    auto& mem = open[key];
     if (mem.empty()) return;
     BoxBatch b;
     b.members = mem;
-    b.gpu = gpu;
+    b.gpu = lanes_[exec_lane_[mem[0]]].gpu;
     for (int m : mem) {
       batch_of_[m] = static_cast<int>(batches_.size());
       pending[m] = 0;
@@ -876,9 +885,9 @@ void Executor::plan_box_batches() {
     if (exec_lane_[id] < 0) continue;
     const Instr& in = prog_.instrs[id];
     for (int d : in.deps)
-      if (d >= 0 && pending[d]) close(lanes_[exec_lane_[d]].gpu, &flush_before_[pos]);
+      if (d >= 0 && pending[d]) close(key_of(d), &flush_before_[pos]);
     if ((in.kind == InstrKind::box || in.kind == InstrKind::ew) && !irt_[id].aliased && !irt_[id].box.empty()) {
-      open[lanes_[exec_lane_[id]].gpu].push_back(id);
+      open[key_of(id)].push_back(id);
       pending[id] = 1;
     }
   }
@@ -898,7 +907,8 @@ void Executor::plan_box_batches() {
         batch_join_.push_back(e);
       }
     }
-    b.stream = pool[next_stream[b.gpu]++ % kBatchStreams];
+    // per lane: the first member's own stream (no cross-lane coupling)
+    b.stream = per_lane ? stream_of(prog_.instrs[b.members[0]]) : pool[next_stream[b.gpu]++ % kBatchStreams];
     ck(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming), "event");
     std::map<std::tuple<int, int, int>, BoxLaunch> merged;
     for (int m : b.members) {
@@ -1018,6 +1028,95 @@ void Executor::place_inputs() {
   }
 }
 
+GemmArgs Executor::gemm_args(const Instr& in) const {
+  GemmArgs a{};
+  a.A = buf_ptr(in.in_bufs[0]);
+  a.B = buf_ptr(in.in_bufs[1]);
+  a.C = buf_ptr(in.out_bufs[0]);
+  a.m = in.m;
+  a.n = in.n;
+  a.k = in.k;
+  a.ta = in.ta;
+  a.tb = in.tb;
+  a.da = dt_of(prog_.buffers[in.in_bufs[0]].dtype);
+  a.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
+  a.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
+  a.group = in.group;
+  if (in.scatter > 0) {
+    if (in.scatter > kMaxGemmGroup || static_cast<int>(in.out_bufs.size()) != in.scatter || !in.fused.empty())
+      throw InternalError("malformed reduce-scatter GEMM instruction");
+    a.scatter = in.scatter;
+    a.scatter_rows = in.scatter_rows;
+    for (int i = 0; i < in.scatter; ++i) a.gC[i] = buf_ptr(in.out_bufs[i]);
+    a.C = a.gC[0];
+  }
+  if (in.group > 1) {
+    if (in.group > kMaxGemmGroup || static_cast<int>(in.in_bufs.size()) != 2 * in.group ||
+        static_cast<int>(in.out_bufs.size()) != in.group || !in.fused.empty()) {
+      throw InternalError("malformed grouped GEMM instruction");
+    }
+    for (int i = 0; i < in.group; ++i) {
+      a.gA[i] = buf_ptr(in.in_bufs[2 * i]);
+      a.gB[i] = buf_ptr(in.in_bufs[2 * i + 1]);
+      a.gC[i] = buf_ptr(in.out_bufs[i]);
+    }
+  }
+  a.epi.n_ops = static_cast<int>(in.fused.size());
+  for (std::size_t f = 0; f < in.fused.size(); ++f) {
+    const auto& fe = in.fused[f];
+    EpiOp& o = a.epi.ops[f];
+    o.op = static_cast<int>(fe.op);
+    o.n_in = static_cast<int>(fe.in_bufs.size());
+    o.gemm_pos = fe.gemm_pos;
+    for (std::size_t j = 0; j < fe.in_bufs.size(); ++j) {
+      o.in[j] = buf_ptr(fe.in_bufs[j]);
+      if (static_cast<int>(j) != fe.gemm_pos) {
+        if (a.epi.n_slots >= kMaxEpiSlots) throw InternalError("fused epilogue needs more than 2 operands");
+        a.epi.slot_op[a.epi.n_slots] = static_cast<int>(f);
+        a.epi.slot_in[a.epi.n_slots] = static_cast<int>(j);
+        ++a.epi.n_slots;
+      }
+    }
+    o.out = buf_ptr(fe.out_buf);
+  }
+  {
+    const LaneRt& lr = lanes_[exec_lane_[in.id]];
+    a.ws = lr.gemm_ws[exec_stream_[in.id]];
+    a.ws_bytes = lr.gemm_ws_bytes[exec_stream_[in.id]];
+    a.allow_streamk = gemm_streamk_ok(exec_lane_[in.id]);
+  }
+  if (!in.gather[0].empty() || !in.gather[1].empty()) {
+    if (in.group != 1 || in.scatter > 0) throw InternalError("malformed gathered-operand GEMM instruction");
+    a.gather_a = static_cast<int>(in.gather[0].size());
+    a.gather_b = static_cast<int>(in.gather[1].size());
+    a.gather_rows_a = in.gather_rows[0];
+    a.gather_rows_b = in.gather_rows[1];
+    for (int i = 0; i < a.gather_a; ++i) a.gather_a_ptr[i] = buf_ptr(in.gather[0][i]);
+    for (int i = 0; i < a.gather_b; ++i) a.gather_b_ptr[i] = buf_ptr(in.gather[1][i]);
+    a.gather_maps = irt_[in.id].gather_maps;
+  }
+  return a;
+}
+
+// Tensor maps of every gathered-operand GEMM's pieces (buffers are placed
+// and workspaces sized by now), copied to device memory once.
+void Executor::build_gather_maps() {
+  std::vector<unsigned char> host(kGatherMapSlots * kTensorMapBytes);
+  for (const auto& in : prog_.instrs) {
+    if (in.kind != InstrKind::gemm || exec_lane_[in.id] < 0 || (in.gather[0].empty() && in.gather[1].empty())) continue;
+    const GemmArgs a = gemm_args(in);
+    if (!opt_.allow_tensor_cores || !gemm_sm100_eligible(a))
+      throw InternalError("gathered-operand GEMM " + in.label + " off the tensor-core path");
+    gemm_sm100_gather_maps(a, host.data());
+    DeviceGuard dg(lanes_[exec_lane_[in.id]].gpu);
+    if (!irt_[in.id].gather_maps) {
+      ck(cudaMalloc(&irt_[in.id].gather_maps, host.size()), "cudaMalloc(gather maps)");
+      table_allocs_.push_back(irt_[in.id].gather_maps);
+    }
+    ck(cudaMemcpy(irt_[in.id].gather_maps, host.data(), host.size(), cudaMemcpyHostToDevice), "gather maps");
+  }
+}
+
 void Executor::launch_instr(const Instr& in, cudaStream_t s) {
   switch (in.kind) {
     case InstrKind::nop:
@@ -1026,62 +1125,7 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
       launch_xfer(in, s);
       return;
     case InstrKind::gemm: {
-      GemmArgs a{};
-      a.A = buf_ptr(in.in_bufs[0]);
-      a.B = buf_ptr(in.in_bufs[1]);
-      a.C = buf_ptr(in.out_bufs[0]);
-      a.m = in.m;
-      a.n = in.n;
-      a.k = in.k;
-      a.ta = in.ta;
-      a.tb = in.tb;
-      a.da = dt_of(prog_.buffers[in.in_bufs[0]].dtype);
-      a.db = dt_of(prog_.buffers[in.in_bufs[1]].dtype);
-      a.dc = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
-      a.group = in.group;
-      if (in.scatter > 0) {
-        if (in.scatter > kMaxGemmGroup || static_cast<int>(in.out_bufs.size()) != in.scatter || !in.fused.empty())
-          throw InternalError("malformed reduce-scatter GEMM instruction");
-        a.scatter = in.scatter;
-        a.scatter_rows = in.scatter_rows;
-        for (int i = 0; i < in.scatter; ++i) a.gC[i] = buf_ptr(in.out_bufs[i]);
-        a.C = a.gC[0];
-      }
-      if (in.group > 1) {
-        if (in.group > kMaxGemmGroup || static_cast<int>(in.in_bufs.size()) != 2 * in.group ||
-            static_cast<int>(in.out_bufs.size()) != in.group || !in.fused.empty()) {
-          throw InternalError("malformed grouped GEMM instruction");
-        }
-        for (int i = 0; i < in.group; ++i) {
-          a.gA[i] = buf_ptr(in.in_bufs[2 * i]);
-          a.gB[i] = buf_ptr(in.in_bufs[2 * i + 1]);
-          a.gC[i] = buf_ptr(in.out_bufs[i]);
-        }
-      }
-      a.epi.n_ops = static_cast<int>(in.fused.size());
-      for (std::size_t f = 0; f < in.fused.size(); ++f) {
-        const auto& fe = in.fused[f];
-        EpiOp& o = a.epi.ops[f];
-        o.op = static_cast<int>(fe.op);
-        o.n_in = static_cast<int>(fe.in_bufs.size());
-        o.gemm_pos = fe.gemm_pos;
-        for (std::size_t j = 0; j < fe.in_bufs.size(); ++j) {
-          o.in[j] = buf_ptr(fe.in_bufs[j]);
-          if (static_cast<int>(j) != fe.gemm_pos) {
-            if (a.epi.n_slots >= kMaxEpiSlots) throw InternalError("fused epilogue needs more than 2 operands");
-            a.epi.slot_op[a.epi.n_slots] = static_cast<int>(f);
-            a.epi.slot_in[a.epi.n_slots] = static_cast<int>(j);
-            ++a.epi.n_slots;
-          }
-        }
-        o.out = buf_ptr(fe.out_buf);
-      }
-      {
-        const LaneRt& lr = lanes_[exec_lane_[in.id]];
-        a.ws = lr.gemm_ws[exec_stream_[in.id]];
-        a.ws_bytes = lr.gemm_ws_bytes[exec_stream_[in.id]];
-        a.allow_streamk = gemm_streamk_ok(exec_lane_[in.id]);
-      }
+      GemmArgs a = gemm_args(in);
       if (a.epi.n_ops > 0 && !(opt_.allow_tensor_cores && gemm_sm100_eligible(a))) {
         throw InternalError("fused epilogue on a GEMM the tensor-core path does not take");
       }

@@ -55,7 +55,12 @@ struct ExecOptions {
   bool alias_copies = true;             // same-GPU whole-buffer copies (recv, identity) become aliases
   bool scatter_allreduce = true;        // all-reduce partials leave the GEMM epilogue as reduce-scatter slices
   bool reuse_memory = false;            // timed mode: bytes the plan frees are reused within the step
-  bool batch_boxes = true;              // independent adapter (box) instructions of one GPU in shared launches
+  // Independent adapter (box) and elementwise instructions of one GPU in
+  // shared launches. Off by default: it couples the lanes sharing a GPU
+  // (C4 5.55 -> 7.19 ms, C5 2.68 -> 4.48 ms per step measured,
+  // profiles/r02/ab_batch.jsonl); PLANC_B200_BATCH=1 / 2 (per lane) for A/B.
+  bool batch_boxes = false;
+  bool gather_operands = true;          // concat / all-gather feeding only GEMMs: GEMMs read the pieces in place
 };
 
 // ProgramOptions as the executor uses them: epilogue fusion only for GEMMs
@@ -177,6 +182,7 @@ class Executor {
     bool aliased = false;        // whole-buffer copy on one GPU: output shares the source's memory
     cudaEvent_t done = nullptr;  // recorded when a later instruction on another stream depends on it
     float* scratch = nullptr;
+    void* gather_maps = nullptr;  // device tensor maps of a gathered-operand GEMM's pieces
   };
 
   void* buf_ptr(int b) const;
@@ -194,6 +200,8 @@ class Executor {
   void place_inputs();
   void issue_step(bool timing_events, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* ev);
   void launch_instr(const Instr& in, cudaStream_t s);
+  GemmArgs gemm_args(const Instr& in) const;
+  void build_gather_maps();
   void ensure_graph();
 
   bool local(int buffer) const { return owned_[prog_.buffers[buffer].lane]; }

@@ -29,9 +29,17 @@ def exec_instr(ins: dict, data: dict, shape: dict):
     (results are assigned to data[out]; a box writes only its cells)."""
     k = ins["kind"]
     if k == "gemm":
+        gathered = ins.get("gather", [{"pieces": []}, {"pieces": []}])
+
+        def operand(j, buf):
+            # all-gather / concat -> GEMM prologue: the row pieces in order
+            if gathered[j]["pieces"]:
+                return np.concatenate([data[p].reshape(shape[p]) for p in gathered[j]["pieces"]], axis=0)
+            return data[buf].reshape(shape[buf])
+
         for g in range(ins.get("group", 1)):  # grouped launch: member g = (in[2g], in[2g+1]) -> out[g]
-            a = data[ins["in"][2 * g]].reshape(shape[ins["in"][2 * g]])
-            b = data[ins["in"][2 * g + 1]].reshape(shape[ins["in"][2 * g + 1]])
+            a = operand(0, ins["in"][2 * g])
+            b = operand(1, ins["in"][2 * g + 1])
             a = a.T if ins["ta"] else a
             b = b.T if ins["tb"] else b
             c = a @ b

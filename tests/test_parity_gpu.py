@@ -93,7 +93,7 @@ def test_train_step_gemms_take_tensor_cores(name):
                                   "three_pass_3f1b", "gpt_block_fwd_tp2_mma"])
 @pytest.mark.parametrize("flags", [pb.NO_GRAPH, pb.NO_TENSOR_CORES, pb.SERIAL_LANES, pb.NO_GRAPH | pb.SERIAL_LANES,
                                    pb.NO_FUSION, pb.NO_FUSION | pb.NO_GRAPH, pb.NO_ALIAS, pb.NO_GROUPING,
-                                   pb.NO_SCATTER, pb.NO_BATCH, pb.NO_BATCH | pb.NO_GRAPH])
+                                   pb.NO_SCATTER, pb.BATCH, pb.BATCH | pb.NO_GRAPH, pb.NO_GATHER])
 def test_parity_across_launch_modes(name, flags):
     g = golden_cases.load(name)
     out, _ = _run(g["plan"], g["inputs"], flags=flags)
@@ -198,18 +198,18 @@ def test_profile_reports_kernel_families():
 @pytest.mark.parametrize("name", ["mlp_1f1b_dp2", "three_pass_3f1b", "adapt_d1_to_d0_4", "gpt_stack2_1f1b_bf16",
                                   "cross_group_scatter", "mlp_dp2_naive", "c4_coshard_dp8_bf16", "c5_3f1b_dap_bf16"])
 def test_box_batching_same_bits_fewer_launches(name):
-    """Adapter instructions pending together in issue order share launches
-    (ExecOptions::batch_boxes): the same bits as one launch per
-    instruction, and no more kernels per step."""
+    """Adapter / elementwise instructions pending together in issue order
+    share launches (BATCH, ExecOptions::batch_boxes; off by default): the
+    same bits as one launch per instruction, and no more kernels per step."""
     g = golden_cases.load(name)
     outs, kernels = {}, {}
-    for flags in (0, pb.NO_BATCH):
+    for flags in (0, pb.BATCH):
         out, st = _run(g["plan"], g["inputs"], flags=flags)
         outs[flags], kernels[flags] = out, st["kernels_per_step"]
-    assert kernels[0] <= kernels[pb.NO_BATCH]
+    assert kernels[pb.BATCH] <= kernels[0]
     for k in outs[0]:
-        assert np.array_equal(outs[0][k], outs[pb.NO_BATCH][k]), k
-    ok, msg = pb.compare_outputs(g["expected"], outs[0], g["meta"]["rel_tol"], normwise=True)
+        assert np.array_equal(outs[0][k], outs[pb.BATCH][k]), k
+    ok, msg = pb.compare_outputs(g["expected"], outs[pb.BATCH], g["meta"]["rel_tol"], normwise=True)
     assert ok, msg
 
 
