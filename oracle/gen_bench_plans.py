@@ -13,6 +13,10 @@ box has no reference. Shapes follow SURVEY.md §8d:
        (coshard_dp sProgram), 131072 tokens, H=512, bf16
   c5   Evoformer proxy (docs.evoformer_doc), MSA [32768,256] + pair
        [65536,128], 3F1B over 4 stages x 2-way DAP (threef1b_dap), bf16
+  c2sp the C2 block under Megatron TP + sequence parallelism (megatron_tp
+       "sp" role: residual adds split on the token dim -> reduce-scatter
+       after the row-parallel GEMMs, all-gather (send/recv + concat) before
+       the column-parallel ones), TP = 2/4/8
   c2x  the schema-extension transformer block (docs.gpt_block_ext_doc: LN,
        per-head softmax, GELU and their gradients), T=8192, H=2048, 16 heads
        of 128, bf16, Megatron TP = 1/2/4/8 — compiled by the reference front
@@ -138,17 +142,27 @@ def gen_ref1():
         write(name, g, plan, dict(config=name[:2], strategy="none", dtype="bf16"))
 
 
+def gen_c2sp():
+    g = docs.dumps(docs.gpt_block_doc(8192, 2048, elem_size=2, train=True, seq_parallel=True))
+    for k in (2, 4, 8):
+        plan = refpy.compile_plan(g, strategy="megatron_tp", devices=k)
+        write(f"c2sp_tp{k}", g, plan, dict(config="c2sp", tokens=8192, hidden=2048, tp=k, dtype="bf16",
+                                            samples_per_step=8192, sample="token (row of X)",
+                                            parallelism="Megatron TP + sequence parallel"))
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     only = set(sys.argv[1:])
     if only:
-        for name, fn in (("c2x", gen_c2x), ("c3l24", gen_c3_l24), ("c4", gen_c4), ("c5", gen_c5)):
+        for name, fn in (("c2x", gen_c2x), ("c2sp", gen_c2sp), ("c3l24", gen_c3_l24), ("c4", gen_c4), ("c5", gen_c5)):
             if name in only:
                 fn()
         if "ref1" in only:
             gen_ref1()
         return
     gen_c2x()
+    gen_c2sp()
     for T, H, tag in ((8192, 2048, ""), (128, 128, "_cpu")):
         g = docs.dumps(docs.gpt_block_doc(T, H, elem_size=2, train=True))
         for k in (1, 2, 4, 8):

@@ -201,12 +201,27 @@ def cases():
     out.append(("gpt_block_fwd_tp2_mma", docs.dumps(docs.gpt_block_doc(256, 128, elem_size=2, train=False)),
                 dict(strategy="megatron_tp", devices=2), 71, 2e-2,
                 "C2 forward at tensor-core-eligible shapes (bf16)"))
+    # Megatron sequence parallelism (megatron_tp "sp" role: residual ops split
+    # on the token dim): reduce-scatter after the row-parallel GEMMs,
+    # send/recv + concat (an all-gather) before the column-parallel ones —
+    # at tensor-core shapes the concat feeds the GEMMs' gather prologue.
+    out.append(("gpt_block_sp_tp2", docs.dumps(docs.gpt_block_doc(16, 8, elem_size=4, train=True, seq_parallel=True)),
+                dict(strategy="megatron_tp", devices=2), 90, 0.0, "C2 Megatron TP + sequence parallel (train), fp32"))
+    for k, T, H in ((2, 512, 128), (4, 1024, 64)):  # token pieces of 256 rows: the gather prologue applies
+        out.append((f"gpt_block_sp_tp{k}_mma",
+                    docs.dumps(docs.gpt_block_doc(T, H, elem_size=2, train=True, seq_parallel=True)),
+                    dict(strategy="megatron_tp", devices=k), 90 + k, 2e-2,
+                    "C2 Megatron TP + sequence parallel train step at tensor-core shapes (gathered GEMM operands), bf16"))
     return out
 
 
 def main():
     index = []
+    only = set(sys.argv[1:])  # regenerate just these cases (the index always lists all)
     for name, doc, spec, seed, tol, prov in cases():
+        if only and name not in only:
+            index.append(name)
+            continue
         d = os.path.join(HERE, name)
         os.makedirs(d, exist_ok=True)
         plan = refpy.compile_plan(doc, **spec)

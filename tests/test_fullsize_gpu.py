@@ -60,7 +60,8 @@ def run(plan_json, inputs, ids):
         return {i: ex.get_output(i) for i in ids}
 
 
-@pytest.mark.parametrize("base,parts", [("c2_tp1", ["c2_tp2", "c2_tp4"]), ("c2x_tp1", ["c2x_tp2", "c2x_tp8"]),
+@pytest.mark.parametrize("base,parts", [("c2_tp1", ["c2_tp2", "c2_tp4"]), ("c2_tp1", ["c2sp_tp2", "c2sp_tp8"]),
+                                        ("c2x_tp1", ["c2x_tp2", "c2x_tp8"]),
                                         ("c1l_dp1", ["c1l_dp2"]),
                                         ("c4_ref1", ["c4_coshard4_dp8"]), ("c5_ref1", ["c5_3f1b_dap"]),
                                         ("c3_ref1", ["c3_pp4dp2"])])

@@ -213,6 +213,30 @@ def test_box_batching_same_bits_fewer_launches(name):
     assert ok, msg
 
 
+@pytest.mark.parametrize("name", ["gpt_block_sp_tp2_mma", "gpt_block_sp_tp4_mma", "gpt_block_train_tp2_mma"])
+def test_gathered_gemm_operands(name):
+    """All-gather / concat -> GEMM prologue: a concat of
+    row pieces feeding only tensor-core GEMMs is dropped and the GEMMs' TMA
+    loads read the pieces in place. Same operands, same bits as the
+    materialised concat (NO_GATHER), and the bf16 plan emulation's bits."""
+    g = golden_cases.load(name)
+    desc = pb.describe(g["plan"])
+    gathers = [i for i in desc["instrs"] if i["kind"] == "gemm" and any(x["pieces"] for x in i["gather"])]
+    assert gathers, "the plan has no gathered GEMM operand"
+    outs, kernels = {}, {}
+    for flags in (0, pb.NO_GATHER):
+        out, st = _run(g["plan"], g["inputs"], flags=flags)
+        outs[flags], kernels[flags] = out, st["kernels_per_step"]
+    assert kernels[0] < kernels[pb.NO_GATHER]
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[pb.NO_GATHER][k]), k
+    ok, msg = pb.compare_outputs(g["expected"], outs[0], g["meta"]["rel_tol"], normwise=True)
+    assert ok, msg
+    if g["meta"].get("bf16_exact"):
+        for k, v in g["emulated"].items():
+            assert np.array_equal(outs[0][k], v), k
+
+
 def test_same_gpu_copies_become_aliases():
     """A recv whose send lane shares the GPU and identity ops launch nothing
     (the output aliases the source); results unchanged; NO_ALIAS copies."""
