@@ -392,6 +392,7 @@ def main():
     # one process driving every lane runs it honouring the plan's frees
     # (REUSE_MEMORY, ~80 GiB). One process per GPU holds 1/N of the lanes.
     reuse_flags = pb.REUSE_MEMORY if (args.config == "c3" and not dist) else 0
+    reuse_flags |= int(os.environ.get("PLANC_B200_BENCH_FLAGS", "0"), 0)  # A/B experiments only
     if dist:
         # One process per GPU: this rank runs lanes l with l % world == rank
         # on its local GPU; cross-rank pieces move over NVLink (peer memory or
