@@ -378,55 +378,69 @@ __global__ void __launch_bounds__(256) reduce_rows_kernel(const T* __restrict__ 
   }
 }
 
-// inner > 1: a block owns 32 * V consecutive inner columns of one outer
-// index (each lane V of them, 16-byte vectors when inner % V == 0) and a
-// range of the reduced axis, split over its 8 warps (interleaved rows, 4
-// loads in flight); the warps' sums are combined in shared memory in warp
-// order. When the axis is split over S > 1 blocks (grid.z), each writes an
-// fp32 partial [outer][S][inner] to scratch and reduce_cols_finish adds the
-// S partials in order — no atomics, the same bits every run.
+// inner > 1: a block owns 32 * V * CV consecutive inner columns of one outer
+// index (lane l holds vectors l, l + 32, ... of V elements: a warp reads
+// CV * 512 contiguous bytes of every row it visits, DRAM-page friendly) and a
+// range of the reduced axis, split over its 8 warps (interleaved rows, two
+// rows of loads in flight); the warps' sums are combined in shared memory in
+// warp order. When the axis is split over S > 1 blocks (grid.z), each writes
+// an fp32 partial [outer][S][inner] to scratch and reduce_cols_finish adds
+// the S partials in order — no atomics, the same bits every run.
 constexpr int kRedWarps = 8;
+constexpr int kRedCV = 4;  // vectors per lane along the kept axis
 template <typename T, int V>
 __global__ void __launch_bounds__(kRedWarps * 32) reduce_cols_kernel(const T* __restrict__ in, T* __restrict__ out,
                                                                     float* __restrict__ partial, std::int64_t outer,
                                                                     std::int64_t axis_len, std::int64_t inner) {
   pdl_wait();  // launch.cuh: inputs of the previous kernel visible
   pdl_trigger();
-  __shared__ float red[kRedWarps][32 * V];
+  constexpr int TW = 32 * V * kRedCV;  // columns per block
+  __shared__ float red[kRedWarps][TW];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const std::int64_t o = blockIdx.y;
-  const std::int64_t c0 = (static_cast<std::int64_t>(blockIdx.x) * 32 + lane) * V;
+  const std::int64_t col0 = static_cast<std::int64_t>(blockIdx.x) * TW;
   const int S = gridDim.z;
   const std::int64_t a_lo = axis_len * blockIdx.z / S, a_hi = axis_len * (blockIdx.z + 1) / S;
-  const bool live = c0 < inner;  // inner % V == 0 when V > 1
-  const T* base = in + o * axis_len * inner + c0;
-  float acc[V];
+  const T* base = in + o * axis_len * inner + col0;
+  float acc[kRedCV][V];
 #pragma unroll
-  for (int j = 0; j < V; ++j) acc[j] = 0.f;
-  constexpr int U = 4;
+  for (int c = 0; c < kRedCV; ++c)
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[c][j] = 0.f;
+  bool live[kRedCV];
+#pragma unroll
+  for (int c = 0; c < kRedCV; ++c) live[c] = col0 + (c * 32 + lane) * V < inner;  // inner % V == 0 when V > 1
+  constexpr int U = 2;
   for (std::int64_t a = a_lo + warp; a < a_hi; a += kRedWarps * U) {
-    float v[U][V];
+    float v[U][kRedCV][V];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (live && a + kRedWarps * u < a_hi) load_vec<T, V>(base + (a + kRedWarps * u) * inner, v[u]);
+#pragma unroll
+      for (int c = 0; c < kRedCV; ++c)
+        if (live[c] && a + kRedWarps * u < a_hi)
+          load_vec<T, V>(base + (a + kRedWarps * u) * inner + (c * 32 + lane) * V, v[u][c]);
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (live && a + kRedWarps * u < a_hi) {
 #pragma unroll
-        for (int j = 0; j < V; ++j) acc[j] += v[u][j];
-      }
+      for (int c = 0; c < kRedCV; ++c)
+        if (live[c] && a + kRedWarps * u < a_hi) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc[c][j] += v[u][c][j];
+        }
   }
 #pragma unroll
-  for (int j = 0; j < V; ++j) red[warp][lane * V + j] = acc[j];
+  for (int c = 0; c < kRedCV; ++c)
+#pragma unroll
+    for (int j = 0; j < V; ++j) red[warp][(c * 32 + lane) * V + j] = acc[c][j];
   __syncthreads();
-  for (int i = threadIdx.x; i < 32 * V; i += blockDim.x) {
-    const std::int64_t c = static_cast<std::int64_t>(blockIdx.x) * 32 * V + i;
-    if (c >= inner) continue;
+  for (int i = threadIdx.x; i < TW; i += blockDim.x) {
+    const std::int64_t col = col0 + i;
+    if (col >= inner) continue;
     float sum = red[0][i];
 #pragma unroll
     for (int w = 1; w < kRedWarps; ++w) sum += red[w][i];
-    if (S == 1) out[o * inner + c] = from_acc<T>(sum);
-    else partial[(o * S + blockIdx.z) * inner + c] = sum;
+    if (S == 1) out[o * inner + col] = from_acc<T>(sum);
+    else partial[(o * S + blockIdx.z) * inner + col] = sum;
   }
 }
 
@@ -741,7 +755,7 @@ bool aligned16(const void* p) { return reinterpret_cast<std::uintptr_t>(p) % 16 
 // Axis splits of a column reduction: enough blocks for ~2 waves, at least
 // 64 rows per split.
 int reduce_splits(std::int64_t outer, std::int64_t axis_len, std::int64_t inner, int vec) {
-  const std::int64_t tiles = outer * ((inner + 32 * vec - 1) / (32 * vec));
+  const std::int64_t tiles = outer * ((inner + 32 * vec * kRedCV - 1) / (32 * vec * kRedCV));
   std::int64_t S = (2 * 148 + tiles - 1) / tiles;
   S = std::min<std::int64_t>(S, std::max<std::int64_t>(1, axis_len / 64));
   return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(S, 1024)));
@@ -766,7 +780,7 @@ void reduce_typed(const void* in_, void* out_, void* scratch, std::int64_t outer
   const int v = vec ? VV : 1;
   const int S = scratch ? reduce_splits(outer, axis_len, inner, v) : 1;
   if (outer > 65535) throw std::runtime_error("reduce: more than 65535 outer rows with a column reduction");
-  dim3 grid(static_cast<unsigned>((inner + 32 * v - 1) / (32 * v)), static_cast<unsigned>(outer),
+  dim3 grid(static_cast<unsigned>((inner + 32 * v * kRedCV - 1) / (32 * v * kRedCV)), static_cast<unsigned>(outer),
             static_cast<unsigned>(S));
   float* part = static_cast<float*>(scratch);
   if (vec)

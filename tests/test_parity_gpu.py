@@ -227,7 +227,11 @@ def test_gathered_gemm_operands(name):
     for flags in (0, pb.NO_GATHER):
         out, st = _run(g["plan"], g["inputs"], flags=flags)
         outs[flags], kernels[flags] = out, st["kernels_per_step"]
-    assert kernels[0] < kernels[pb.NO_GATHER]
+    # (a single-piece "gather" reads an identity's source: on one GPU that
+    # copy is already an alias, so no kernel is saved there)
+    assert kernels[0] <= kernels[pb.NO_GATHER]
+    if "_sp_" in name:
+        assert kernels[0] < kernels[pb.NO_GATHER]
     for k in outs[0]:
         assert np.array_equal(outs[0][k], outs[pb.NO_GATHER][k]), k
     ok, msg = pb.compare_outputs(g["expected"], outs[0], g["meta"]["rel_tol"], normwise=True)
