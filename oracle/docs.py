@@ -160,7 +160,12 @@ def dumps(doc: dict) -> str:
 # compiled plan by rewrite_plan (op ids are preserved by op-trans as
 # "<id>/<i>" and "<id>~rc").
 EXT_STANDIN = {"softmax": "identity", "layernorm": "identity", "gelu": "identity",
-               "softmax-grad": "mul", "layernorm-grad": "mul", "gelu-grad": "mul"}
+               "softmax-grad": "mul", "layernorm-grad": "mul", "gelu-grad": "mul",
+               # attention(Q, K, V) partitions like a 3-operand elementwise op:
+               # head (column) and sequence (row) splits carry over; the
+               # executor rejects pieces that cut a sequence or a head
+               "attention": "add"}
+EXT_ATTRS = ("segment", "eps", "head_dim", "seq", "causal")
 
 
 def gpt_block_ext_doc(tokens: int, hidden: int, head: int, elem_size: int = 2, train: bool = True) -> dict:
@@ -253,7 +258,8 @@ def standin_doc(doc: dict) -> dict:
     for op in out["ops"]:
         if op["kind"] in EXT_STANDIN:
             op["kind"] = EXT_STANDIN[op["kind"]]
-            op.get("attrs", {}).pop("segment", None)
+            for a in ("segment", "head_dim", "seq", "causal"):
+                op.get("attrs", {}).pop(a, None)
     return out
 
 
@@ -271,12 +277,25 @@ def rewrite_plan(plan_json: str, doc: dict) -> str:
             attrs = src.get("attrs", {})
             if attrs.get("segment"):
                 op["segment"] = attrs["segment"]
-            if "eps" in attrs:
-                op["eps"] = attrs["eps"]
+            for a in ("eps", "head_dim", "seq", "causal"):
+                if a in attrs:
+                    op[a] = attrs[a]
             n += 1
     if n == 0:
         raise ValueError("rewrite_plan: no extended op found in the plan")
     return json.dumps(p)
+
+
+def attention_doc(tokens: int, heads: int, head_dim: int, seq: int, causal: bool = False, elem_size: int = 2,
+                  prefix: str = "tp") -> dict:
+    """One fused attention op O = attention(Q, K, V) over [tokens, heads x
+    head_dim] operands (sequences of ``seq`` tokens). ``prefix`` "tp" makes
+    megatron_tp split it by heads (dim 1)."""
+    T, D = tokens, heads * head_dim
+    pts = [_pt(i, (T, D), "activation", elem_size) for i in range(4)]
+    ops = [_op(prefix + "attn", "attention", [0, 1, 2], [3], "forward", 4.0 * T * seq * D,
+               {"batch_dim": 0, "head_dim": head_dim, "seq": seq, "causal": causal})]
+    return {"ptensors": pts, "ops": ops}
 
 
 # ---- C4 / C5 benchmark documents (SURVEY §8d) ------------------------------------

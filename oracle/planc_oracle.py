@@ -166,12 +166,40 @@ def eval_compute(op, ins, in_masks, out_masks):
         return [out]
     if kind == "identity":
         return [ins[0].copy()]
+    if kind == "attention":
+        return [attention(ins[0], ins[1], ins[2], op.get("head_dim", 0), op.get("seq", 0), op.get("causal", False),
+                          in_masks)]
     if kind in EXT_KINDS:
         return [eval_ext(kind, ins, op.get("segment", 0), op.get("eps", 1e-5), in_masks)]
     raise UsageError(f"refexec: unsupported op kind {kind} ({op['id']})")
 
 
 EXT_KINDS = ("softmax", "softmax-grad", "layernorm", "layernorm-grad", "gelu", "gelu-grad")
+
+
+def attention(q, k, v, head_dim, seq, causal=False, in_masks=None):
+    """Schema extension (not in the reference): O = softmax(Q·Kᵀ/sqrt(d) [+
+    causal mask])·V per sequence of ``seq`` rows and head of ``head_dim``
+    columns of the [T, D] operands, in float64. The executor's rule for a
+    piece: whole sequences and whole heads, Q/K/V/O on the same region."""
+    q, k, v = (np.asarray(x, dtype=np.float64) for x in (q, k, v))
+    T, D = q.shape
+    if head_dim <= 0 or seq <= 0 or T % seq or D % head_dim:
+        raise UsageError(f"attention: piece [{T}, {D}] does not hold whole sequences of {seq} / heads of {head_dim}")
+    if in_masks is not None:
+        r = in_masks[0]["region"]
+        if r[0][0] % seq or r[1][0] % head_dim or any(m["region"] != r for m in in_masks):
+            raise UsageError("attention: pieces not aligned to whole sequences / heads or not the same region")
+    nb, nh = T // seq, D // head_dim
+    qs = q.reshape(nb, seq, nh, head_dim).transpose(0, 2, 1, 3)
+    ks = k.reshape(nb, seq, nh, head_dim).transpose(0, 2, 1, 3)
+    vs = v.reshape(nb, seq, nh, head_dim).transpose(0, 2, 1, 3)
+    s = qs @ ks.transpose(0, 1, 3, 2) / np.sqrt(head_dim)
+    if causal:
+        s = np.where(np.tril(np.ones((seq, seq), dtype=bool)), s, -np.inf)
+    p = np.exp(s - s.max(axis=-1, keepdims=True))
+    p /= p.sum(axis=-1, keepdims=True)
+    return (p @ vs).transpose(0, 2, 1, 3).reshape(T, D)
 
 
 def _erf(x):

@@ -1,0 +1,327 @@
+// Fused attention (schema extension): O = softmax(Q·Kᵀ·s)·V
+// per (sequence, head) on tcgen05 tensor cores — one kernel, S and P never
+// leave the SM (flash-attention structure: online softmax, rescaled
+// accumulation).
+//
+// Layout: Q, K, V, O are a piece's [rows, cols] bf16 tensors (row-major):
+// rows = whole sequences of `seq` tokens, cols = whole heads of `dh`
+// features. CTA (qb, h, b) computes the 128 query rows qb of head h of
+// sequence b.
+//
+// Warps: 0 TMA producer (Q once; K_j / V_j 128-row tiles through a 2-stage
+//          ring), 1 single-thread MMA issuer, 2..5 softmax / accumulation
+//          (thread = query row = TMEM lane).
+// Per key block j:
+//   MMA      S_j = Q·K_jᵀ  -> TMEM S[j%2]   (M=128, N=128, K=dh; both K-major)
+//   softmax  row max over S_j (scaled, base 2; causal mask on the diagonal
+//            block) -> m_j; P_j = exp2(S_j - m_j) -> bf16 smem P[j%2] in the
+//            128B-swizzled K-major layout of an MMA A operand; row sum
+//   MMA      O_j = P_j·V_j  -> TMEM O[j%2]   (N=dh; V MN-major)
+//   softmax  acc = acc·exp2(m_{j-1} - m_j) + O_j in fp32 registers
+// so the tensor core runs S_{j+1} and P_j·V_j while the softmax warps work
+// on block j (TMEM: S0 S1 O0 O1 = 512 columns at dh = 128). End: O = acc / l.
+#include "gemm_sm100_impl.cuh"
+
+namespace planc_b200 {
+
+namespace {
+
+constexpr int kAttnThreads = 192;
+constexpr int kAttnBlock = 128;  // query / key rows per tile
+
+template <int DH>
+struct AttnCfg {
+  static constexpr int Q_BYTES = kAttnBlock * DH * 2;   // DH/64 K-major chunks of 16 KB
+  static constexpr int K_BYTES = kAttnBlock * DH * 2;
+  static constexpr int V_BYTES = kAttnBlock * DH * 2;   // 2 kv chunks x DH/64 n-blocks of 8 KB
+  static constexpr int P_BYTES = kAttnBlock * kAttnBlock * 2;  // 2 kv chunks of 16 KB
+  static constexpr int SMEM = Q_BYTES + 2 * (K_BYTES + V_BYTES) + 2 * P_BYTES + 1024 + 1024;
+  static_assert(SMEM <= 227 * 1024, "attention tiles above the shared memory limit");
+};
+
+struct AttnMaps {
+  CUtensorMap q, k, v;
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int DH, bool CAUSAL>
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ AttnMaps mp, __nv_bfloat16* __restrict__ out, int seq, int ld,
+                    float scale_log2) {
+  using CF = AttnCfg<DH>;
+  extern __shared__ std::uint8_t smem_raw[];
+  std::uint8_t* smem =
+      reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  std::uint8_t* sQ = smem;
+  std::uint8_t* sK = sQ + CF::Q_BYTES;                 // [2][K_BYTES]
+  std::uint8_t* sV = sK + 2 * CF::K_BYTES;             // [2][V_BYTES]
+  std::uint8_t* sP = sV + 2 * CF::V_BYTES;             // [2][P_BYTES]
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sP + 2 * CF::P_BYTES);
+  std::uint64_t* q_full = bars;
+  std::uint64_t* kv_full = bars + 1;   // [2]
+  std::uint64_t* kv_empty = bars + 3;  // [2]
+  std::uint64_t* s_full = bars + 5;    // [2]
+  std::uint64_t* s_empty = bars + 7;   // [2]
+  std::uint64_t* p_full = bars + 9;    // [2]
+  std::uint64_t* p_empty = bars + 11;  // [2]
+  std::uint64_t* o_full = bars + 13;   // [2]
+  std::uint64_t* o_empty = bars + 15;  // [2]
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 17);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int row0 = b * seq + qb * kAttnBlock;  // first query row of the tile
+  const int col0 = h * DH;
+  const int nkv = CAUSAL ? qb + 1 : seq / kAttnBlock;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&mp.q)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&mp.k)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&mp.v)) : "memory");
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_empty[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, CF::Q_BYTES);
+#pragma unroll
+      for (int c = 0; c < DH / 64; ++c) tma_load_2d(sQ + c * 16384, &mp.q, col0 + 64 * c, row0, q_full);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], CF::K_BYTES + CF::V_BYTES);
+        const int kr = b * seq + j * kAttnBlock;
+        std::uint8_t* k = sK + st * CF::K_BYTES;
+        std::uint8_t* v = sV + st * CF::V_BYTES;
+#pragma unroll
+        for (int c = 0; c < DH / 64; ++c) tma_load_2d(k + c * 16384, &mp.k, col0 + 64 * c, kr, &kv_full[st]);
+        // V as an MN-major B operand: per 64-key chunk, DH/64 blocks of 64 features
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc)
+#pragma unroll
+          for (int nb = 0; nb < DH / 64; ++nb)
+            tma_load_2d(v + kc * (DH / 64) * 8192 + nb * 8192, &mp.v, col0 + 64 * nb, kr + 64 * kc, &kv_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr std::uint32_t idesc_s = make_idesc<kAttnBlock>(false, false);
+      constexpr std::uint32_t idesc_o = make_idesc<DH>(false, true);
+      mbar_wait(q_full, 0);
+      auto pv = [&](int i) {  // O[i%2] = P[i%2] · V[i%2]
+        const int st = i & 1;
+        mbar_wait(&p_full[st], (i >> 1) & 1);
+        mbar_wait(&o_empty[st], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const std::uint32_t p = smem_u32(sP + st * CF::P_BYTES), v = smem_u32(sV + st * CF::V_BYTES);
+        const std::uint32_t d = tmem + 256 + st * DH;
+#pragma unroll
+        for (int s = 0; s < kAttnBlock / 16; ++s) {
+          const int kc = s / 4, kk = s % 4;
+          tc_mma(d, smem_desc(p + kc * 16384 + kk * 32, 16, 1024),
+                 smem_desc(v + kc * (DH / 64) * 8192 + kk * 2048, 8192, 1024), idesc_o, s > 0 ? 1u : 0u);
+        }
+        tc_commit(&o_full[st]);
+        tc_commit(&kv_empty[st]);  // K_i / V_i consumed (S_i issued earlier)
+        tc_commit(&p_empty[st]);
+      };
+      const std::uint32_t q = smem_u32(sQ);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const std::uint32_t k = smem_u32(sK + st * CF::K_BYTES);
+        const std::uint32_t d = tmem + st * kAttnBlock;
+#pragma unroll
+        for (int s = 0; s < DH / 16; ++s) {
+          const int c = s / 4, kk = s % 4;
+          tc_mma(d, smem_desc(q + c * 16384 + kk * 32, 16, 1024), smem_desc(k + c * 16384 + kk * 32, 16, 1024),
+                 idesc_s, s > 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[st]);
+        if (j > 0) pv(j - 1);
+      }
+      pv(nkv - 1);
+      pdl_trigger();
+    }
+  } else {
+    // Softmax warps: row r of the tile = TMEM lane r.
+    const int qr = warp % 4;
+    const int r = qr * 32 + lane;
+    const std::uint32_t lane_base = tmem + (static_cast<std::uint32_t>(qr * 32) << 16);
+    float acc[DH];
+#pragma unroll
+    for (int i = 0; i < DH; ++i) acc[i] = 0.f;
+    float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
+    auto accumulate = [&](int i, float alpha) {  // acc = acc * alpha + O[i%2]
+      const int st = i & 1;
+      mbar_wait(&o_full[st], (i >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < DH / 32; ++c) {
+        std::uint32_t v[32];
+        tmem_ld32(lane_base + 256 + st * DH + c * 32, v);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc[c * 32 + e] = acc[c * 32 + e] * alpha + __uint_as_float(v[e]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[st]);
+    };
+    for (int j = 0; j < nkv; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      const std::uint32_t sb = lane_base + st * kAttnBlock;
+      const bool diag = CAUSAL && j == qb;  // keys above the query row are masked
+      // pass 1: row max (base-2 scaled scores)
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kAttnBlock / 32; ++c) {
+        std::uint32_t v[32];
+        tmem_ld32(sb + c * 32, v);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float s = __uint_as_float(v[e]) * scale_log2;
+          if (!diag || c * 32 + e <= r) mx = fmaxf(mx, s);
+        }
+      }
+      const float m_new = fmaxf(m, mx);
+      // pass 2: P = exp2(s - m_new) as bf16 into the swizzled A-operand tile
+      mbar_wait(&p_empty[st], ((j >> 1) & 1) ^ 1);
+      std::uint8_t* prow = sP + st * CF::P_BYTES + r * 128;
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < kAttnBlock / 32; ++c) {
+        std::uint32_t v[32];
+        tmem_ld32(sb + c * 32, v);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          std::uint32_t w[4];
+#pragma unroll
+          for (int h2 = 0; h2 < 4; ++h2) {
+            const int e = 8 * g + 2 * h2;
+            const float s0 = __uint_as_float(v[e]) * scale_log2, s1 = __uint_as_float(v[e + 1]) * scale_log2;
+            const float p0 = (!diag || c * 32 + e <= r) ? ex2(s0 - m_new) : 0.f;
+            const float p1 = (!diag || c * 32 + e + 1 <= r) ? ex2(s1 - m_new) : 0.f;
+            w[h2] = bf16_pair(p0, p1);
+            // the MMA consumes bf16 P: sum the rounded values it multiplies
+            float lo, hi;
+            bf16_unpair(w[h2], lo, hi);
+            sum += lo + hi;
+          }
+          // 16-byte chunk (c * 4 + g) of the row: chunks 0-7 in the first
+          // 64-key atom, 8-15 in the second; 128B swizzle: chunk ^ (row & 7)
+          const int chunk = c * 4 + g;
+          const int atom = chunk >> 3, cw = chunk & 7;
+          *reinterpret_cast<uint4*>(prow + atom * 16384 + ((cw ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&p_full[st]);
+        mbar_arrive(&s_empty[st]);
+      }
+      const float alpha = ex2(m - m_new);  // (m = -inf on the first block: alpha = 0, acc is 0)
+      l = l * alpha + sum;
+      m = m_new;
+      if (j > 0) accumulate(j - 1, alpha_prev);
+      alpha_prev = alpha;
+    }
+    accumulate(nkv - 1, alpha_prev);
+    // acc holds sum_j exp2(m_final...) weighted rows: every accumulate step
+    // rescaled the running sum to the block's max before adding O_j, which
+    // was computed against that same max.
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = out + static_cast<std::int64_t>(row0 + r) * ld + col0;
+#pragma unroll
+    for (int g = 0; g < DH / 8; ++g)
+      reinterpret_cast<uint4*>(orow)[g] =
+          make_uint4(bf16_pair(acc[8 * g] * inv, acc[8 * g + 1] * inv), bf16_pair(acc[8 * g + 2] * inv, acc[8 * g + 3] * inv),
+                     bf16_pair(acc[8 * g + 4] * inv, acc[8 * g + 5] * inv), bf16_pair(acc[8 * g + 6] * inv, acc[8 * g + 7] * inv));
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// bf16 row-major [rows][cols], box {64 cols, box_rows}, 128B swizzle (make_map).
+template <int DH, bool CAUSAL>
+void attn_launch(const void* q, const void* k, const void* v, void* o, std::int64_t rows, std::int64_t cols,
+                 std::int64_t seq, cudaStream_t s) {
+  static unsigned attr_set_mask = 0;
+  auto kern = attn_fwd_kernel<DH, CAUSAL>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_set_mask & (1u << dev))) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnCfg<DH>::SMEM);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("attention smem attribute: ") + cudaGetErrorString(e));
+    attr_set_mask |= 1u << dev;
+  }
+  AttnMaps mp;
+  mp.q = make_map(q, rows, cols, kAttnBlock);
+  mp.k = make_map(k, rows, cols, kAttnBlock);
+  mp.v = make_map(v, rows, cols, 64);
+  const float scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(DH));
+  dim3 grid(static_cast<unsigned>(seq / kAttnBlock), static_cast<unsigned>(cols / DH), static_cast<unsigned>(rows / seq));
+  pdl_launch("attn_fwd_kernel", kern, grid, dim3(kAttnThreads), AttnCfg<DH>::SMEM, s, mp,
+             static_cast<__nv_bfloat16*>(o), static_cast<int>(seq), static_cast<int>(cols), scale_log2);
+}
+
+}  // namespace
+
+const char* attention_unsupported(std::int64_t rows, std::int64_t cols, std::int64_t seq, std::int64_t head_dim,
+                                  int dtype) {
+  if (dtype != DT_BF16) return "fused attention needs bf16 tensors";
+  if (head_dim != 64 && head_dim != 128) return "fused attention supports head_dim 64 or 128";
+  if (seq <= 0 || seq % kAttnBlock != 0) return "fused attention needs seq a multiple of 128";
+  if (rows % seq != 0 || cols % head_dim != 0) return "attention piece does not hold whole sequences and heads";
+  if (rows / seq > 65535 || cols / head_dim > 65535) return "attention piece above the grid limits";
+  return nullptr;
+}
+
+void launch_attention(const void* q, const void* k, const void* v, void* o, std::int64_t rows, std::int64_t cols,
+                      std::int64_t seq, std::int64_t head_dim, bool causal, int dtype, cudaStream_t s) {
+  if (const char* why = attention_unsupported(rows, cols, seq, head_dim, dtype)) throw std::runtime_error(why);
+  if (head_dim == 128) {
+    if (causal) attn_launch<128, true>(q, k, v, o, rows, cols, seq, s);
+    else attn_launch<128, false>(q, k, v, o, rows, cols, seq, s);
+  } else {
+    if (causal) attn_launch<64, true>(q, k, v, o, rows, cols, seq, s);
+    else attn_launch<64, false>(q, k, v, o, rows, cols, seq, s);
+  }
+}
+
+}  // namespace planc_b200

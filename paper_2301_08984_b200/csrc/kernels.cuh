@@ -180,6 +180,14 @@ void launch_gemm_simt(const GemmArgs& a, cudaStream_t s);
 void launch_rowwise(int op, int dtype, const void* a, const void* b, void* out, std::int64_t count, std::int64_t seg,
                     float eps, cudaStream_t s);
 void launch_convert(int dtype_out, void* out, const float* in, std::int64_t count, cudaStream_t s);
+// Fused attention (attention.cu; schema extension): O = softmax(Q·Kᵀ/sqrt(dh)
+// [+ causal mask])·V per (sequence of `seq` rows, head of `head_dim` cols)
+// of a [rows, cols] bf16 piece. attention_unsupported: why a shape cannot
+// run (nullptr when it can).
+const char* attention_unsupported(std::int64_t rows, std::int64_t cols, std::int64_t seq, std::int64_t head_dim,
+                                  int dtype);
+void launch_attention(const void* q, const void* k, const void* v, void* o, std::int64_t rows, std::int64_t cols,
+                      std::int64_t seq, std::int64_t head_dim, bool causal, int dtype, cudaStream_t s);
 void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s);
 // Device-to-device copy on the SMs (16-byte vectors): keeps the copy engines
 // free for the host-link transfers running beside it (end-to-end mode).

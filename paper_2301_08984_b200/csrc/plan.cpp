@@ -51,6 +51,7 @@ const char* op_kind_name(OpKind k) {
     case OpKind::recv: return "recv";
     case OpKind::collective: return "collective";
     case OpKind::free_buffer: return "free";
+    case OpKind::attention: return "attention";
     case OpKind::softmax: return "softmax";
     case OpKind::softmax_grad: return "softmax-grad";
     case OpKind::layernorm: return "layernorm";
@@ -74,7 +75,8 @@ OpKind op_kind_from_doc(const std::string& s) {
       {"collective", OpKind::collective}, {"free", OpKind::free_buffer},
       // schema extension (oracle/planc_oracle.py eval_ext)
       {"softmax", OpKind::softmax}, {"softmax-grad", OpKind::softmax_grad}, {"layernorm", OpKind::layernorm},
-      {"layernorm-grad", OpKind::layernorm_grad}, {"gelu", OpKind::gelu}, {"gelu-grad", OpKind::gelu_grad}};
+      {"layernorm-grad", OpKind::layernorm_grad}, {"gelu", OpKind::gelu}, {"gelu-grad", OpKind::gelu_grad},
+      {"attention", OpKind::attention}};
   auto it = m.find(s);
   if (it == m.end()) throw SchemaError("plan document: unknown op kind " + s);
   return it->second;
@@ -199,6 +201,9 @@ ExecutionPlan load_plan(const std::string& document) {
       if (o.contains("primitive")) op.primitive = o.at("primitive").as_string();
       if (o.contains("segment")) op.segment = o.at("segment").as_int();
       if (o.contains("eps")) op.eps = o.at("eps").as_double();
+      if (o.contains("head_dim")) op.head_dim = o.at("head_dim").as_int();
+      if (o.contains("seq")) op.seq = o.at("seq").as_int();
+      if (o.contains("causal")) op.causal = o.at("causal").as_bool();
       if (op.segment < 0 || !(op.eps >= 0)) throw SchemaError("plan document: bad segment / eps on op " + op.id);
       plan.ops.push_back(std::move(op));
     }

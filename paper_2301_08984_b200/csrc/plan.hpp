@@ -82,6 +82,9 @@ enum class OpKind {
   // them): row-wise transformer sub-operators over the last axis in
   // segments of `segment` elements (0 = the whole axis), and GELU.
   softmax, softmax_grad, layernorm, layernorm_grad, gelu, gelu_grad,
+  // O = softmax(Q·Kᵀ/sqrt(head_dim) [causal])·V per sequence of `seq` rows
+  // and head of `head_dim` columns (inputs Q, K, V; output O, all [T, D]).
+  attention,
 };
 const char* op_kind_name(OpKind k);
 
@@ -104,6 +107,9 @@ struct OpNode {
   std::string primitive;
   std::int64_t segment = 0;  // extension: row-wise segment width (0 = whole last axis)
   double eps = 1e-5;         // extension: layernorm epsilon
+  std::int64_t head_dim = 0;  // extension: attention head width
+  std::int64_t seq = 0;       // extension: attention rows per sequence
+  bool causal = false;        // extension: attention causal mask
 
   bool is_elementwise() const {
     return kind == OpKind::ew_add || kind == OpKind::ew_mul || kind == OpKind::ew_max;

@@ -31,6 +31,7 @@ const char* instr_kind_name(InstrKind k) {
     case InstrKind::xfer: return "xfer";
     case InstrKind::nop: return "nop";
     case InstrKind::rowwise: return "rowwise";
+    case InstrKind::attention: return "attention";
   }
   return "?";
 }
@@ -515,6 +516,41 @@ struct Builder {
         const std::int64_t es = dtype_size(P.buffers[ob].dtype);
         in.bytes = static_cast<double>(in.count) * es * (ib.size() + 1);
         in.flops = static_cast<double>(in.count) * 8;
+        finish_deps(in);
+        break;
+      }
+      case OpKind::attention: {
+        // Schema extension (oracle/planc_oracle.py eval_ext): a piece must
+        // hold whole sequences and whole heads, and Q, K, V, O the same
+        // region — a split inside a sequence or a head is rejected.
+        if (ib.size() != 3 || op.outputs.size() != 1) throw InternalError("attention arity in " + op.id);
+        int ob = out_buffer(op.outputs[0], lane);
+        const auto sh = shape_of(ob);
+        for (int b : ib)
+          if (shape_of(b) != sh) throw InternalError("attention operand shape mismatch in " + op.id);
+        const Region& ro = plan.vt(op.outputs[0]).mask.region;
+        for (int v : op.inputs) {
+          if (!(plan.vt(v).mask.region == ro))
+            throw UsageError("attention " + op.id + ": Q, K, V and O pieces must cover the same region");
+        }
+        if (sh.size() != 2 || op.head_dim <= 0 || op.seq <= 0)
+          throw UsageError("attention " + op.id + ": needs rank-2 [tokens, heads x head_dim] tensors, head_dim and seq");
+        if (ro[0].lo % op.seq != 0 || sh[0] % op.seq != 0 || ro[1].lo % op.head_dim != 0 || sh[1] % op.head_dim != 0)
+          throw UsageError("attention " + op.id + ": the piece does not hold whole sequences of " +
+                           std::to_string(op.seq) + " rows and whole heads of " + std::to_string(op.head_dim));
+        Instr& in = emit(InstrKind::attention, lane, 0, op_idx, op.id);
+        in.in_bufs = ib;
+        in.out_bufs = {ob};
+        in.att_rows = sh[0];
+        in.att_cols = sh[1];
+        in.att_seq = op.seq;
+        in.att_dh = op.head_dim;
+        in.causal = op.causal;
+        const std::int64_t es = dtype_size(P.buffers[ob].dtype);
+        in.bytes = static_cast<double>(sh[0] * sh[1]) * es * 4;
+        // QK^T and PV per (sequence, head): 4 * seq^2 * dh (half with a causal mask)
+        in.flops = 4.0 * static_cast<double>(sh[0]) * static_cast<double>(op.seq) * static_cast<double>(sh[1]) *
+                   (op.causal ? 0.5 : 1.0);
         finish_deps(in);
         break;
       }
@@ -1593,7 +1629,9 @@ std::string Program::describe_json() const {
        << static_cast<int>(in.row_op) << ",\"seg\":" << in.seg << ",\"eps\":" << in.eps << ",\"flops\":" << in.flops
        << ",\"bytes\":" << in.bytes << ",\"wire_bytes\":" << in.wire_bytes << ",\"coll_group\":" << in.coll_group
        << ",\"allreduce\":" << (in.allreduce ? "true" : "false") << ",\"group\":" << in.group
-       << ",\"scatter\":" << in.scatter << ",\"scatter_rows\":" << in.scatter_rows << ",\"gather\":[";
+       << ",\"scatter\":" << in.scatter << ",\"scatter_rows\":" << in.scatter_rows << ",\"att\":{\"rows\":"
+       << in.att_rows << ",\"cols\":" << in.att_cols << ",\"seq\":" << in.att_seq << ",\"head_dim\":" << in.att_dh
+       << ",\"causal\":" << (in.causal ? "true" : "false") << "},\"gather\":[";
     for (int j = 0; j < 2; ++j) {
       os << (j ? "," : "") << "{\"rows\":" << in.gather_rows[j] << ",\"pieces\":[";
       for (std::size_t q = 0; q < in.gather[j].size(); ++q) os << (q ? "," : "") << in.gather[j][q];

@@ -76,7 +76,7 @@ struct Cell {
 
 constexpr int kMaxGemmGroupInstr = 8;  // members of one grouped GEMM launch (kernels.cuh kMaxGemmGroup)
 
-enum class InstrKind { gemm, ew, reduce, emb_lookup, emb_grad, box, xfer, nop, rowwise };
+enum class InstrKind { gemm, ew, reduce, emb_lookup, emb_grad, box, xfer, nop, rowwise, attention };
 
 // Row-wise / activation sub-operators of the schema extension.
 enum class RowOp { softmax = 0, softmax_grad = 1, layernorm = 2, layernorm_grad = 3, gelu = 4, gelu_grad = 5 };
@@ -127,6 +127,10 @@ struct Instr {
   RowOp row_op = RowOp::softmax;
   std::int64_t seg = 0;
   double eps = 0;
+  // attention: in_bufs = Q, K, V, out_bufs = O, each a [rows, cols] piece of
+  // whole sequences (att_seq rows) and whole heads (att_dh columns)
+  std::int64_t att_rows = 0, att_cols = 0, att_seq = 0, att_dh = 0;
+  bool causal = false;
   // box
   std::vector<Cell> cells;
   int coll_group = -1;  // collective group a box instruction belongs to

@@ -306,8 +306,17 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       lane_join_.push_back(e);
     }
   }
-  // Element types must agree across an elementwise op's operands.
+  // Element types must agree across an elementwise op's operands; fused
+  // attention shapes the kernel supports (bf16, head_dim 64 / 128, seq % 128).
   for (const auto& in : prog_.instrs) {
+    if (in.kind == InstrKind::attention) {
+      const int dt = dt_of(prog_.buffers[in.out_bufs[0]].dtype);
+      for (int b : in.in_bufs)
+        if (prog_.buffers[b].dtype != prog_.buffers[in.out_bufs[0]].dtype)
+          throw UsageError("attention " + plan_.ops[in.op].id + " mixes element sizes");
+      if (const char* why = attention_unsupported(in.att_rows, in.att_cols, in.att_seq, in.att_dh, dt))
+        throw UsageError("attention " + plan_.ops[in.op].id + ": " + why);
+    }
     if (in.kind == InstrKind::ew || in.kind == InstrKind::rowwise) {
       DType d = prog_.buffers[in.out_bufs[0]].dtype;
       if (in.kind == InstrKind::rowwise && d == DType::i32) {
@@ -1165,6 +1174,11 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
                       buf_ptr(in.in_bufs[1]), buf_ptr(in.out_bufs[0]), irt_[in.id].scratch, in.n_idx, in.rows, in.h,
                       in.lo, s);
       return;
+    case InstrKind::attention:
+      launch_attention(buf_ptr(in.in_bufs[0]), buf_ptr(in.in_bufs[1]), buf_ptr(in.in_bufs[2]), buf_ptr(in.out_bufs[0]),
+                       in.att_rows, in.att_cols, in.att_seq, in.att_dh, in.causal,
+                       dt_of(prog_.buffers[in.out_bufs[0]].dtype), s);
+      return;
     case InstrKind::rowwise:
       launch_rowwise(static_cast<int>(in.row_op), dt_of(prog_.buffers[in.out_bufs[0]].dtype), buf_ptr(in.in_bufs[0]),
                      in.in_bufs.size() > 1 ? buf_ptr(in.in_bufs[1]) : nullptr, buf_ptr(in.out_bufs[0]), in.count, in.seg,
@@ -1552,6 +1566,7 @@ std::vector<KernelStat> Executor::profile() {
       }
       case InstrKind::ew: kind = "ew"; break;
       case InstrKind::rowwise: kind = "rowwise"; break;
+      case InstrKind::attention: kind = "attention"; break;
       case InstrKind::reduce: kind = "reduce"; break;
       case InstrKind::emb_lookup:
       case InstrKind::emb_grad: kind = "embedding"; break;

@@ -43,12 +43,33 @@ CASES = [
 ]
 
 
+# Fused attention (bf16): name, (tokens, heads, head_dim, seq, causal), strategy spec, seed, rel_tol
+ATTN_CASES = [
+    ("attn_heads_tp2_bf16", (512, 4, 64, 256, False), dict(strategy="megatron_tp", devices=2), 91, 2e-2),
+    ("attn_causal_tp2_bf16", (512, 2, 128, 256, True), dict(strategy="megatron_tp", devices=2), 92, 2e-2),
+    ("attn_seq_split2_bf16", (1024, 2, 128, 512, True), dict(strategy="manual", devices=2, target_ops="tpattn@s0"),
+     93, 2e-2),
+]
+
+
+def cases():
+    for name, (T, H, hd, e, train), k, seed, tol in CASES:
+        yield name, docs.gpt_block_ext_doc(T, H, hd, elem_size=e, train=train), dict(strategy="megatron_tp", devices=k), \
+            seed, tol, e, dict(tokens=T, hidden=H, head=hd, elem_size=e, train=train)
+    for name, (T, nh, hd, seq, causal), spec, seed, tol in ATTN_CASES:
+        yield name, docs.attention_doc(T, nh, hd, seq, causal), spec, seed, tol, 2, \
+            dict(tokens=T, heads=nh, head_dim=hd, seq=seq, causal=causal, elem_size=2)
+
+
 def main():
     index = []
-    for name, (T, H, hd, e, train), k, seed, tol in CASES:
-        doc = docs.gpt_block_ext_doc(T, H, hd, elem_size=e, train=train)
+    only = set(sys.argv[1:])
+    for name, doc, spec, seed, tol, e, shape in cases():
+        if only and name not in only:
+            index.append(name)
+            continue
         stand = docs.dumps(docs.standin_doc(doc))
-        plan = docs.rewrite_plan(refpy.compile_plan(stand, strategy="megatron_tp", devices=k), doc)
+        plan = docs.rewrite_plan(refpy.compile_plan(stand, **spec), doc)
         inputs = refpy.random_integer_inputs(stand, seed, 1)
         got = planc_oracle.run_plan(plan, inputs)
         ok, msg = planc_oracle.compare_outputs(planc_oracle.run_graph(doc, inputs), got, 1e-9)
@@ -71,8 +92,7 @@ def main():
         meta = dict(name=name, seed=seed, rel_tol=tol, normwise=True, extension=True,
                     provenance="schema extension: reference front end on stand-ins + rewrite_plan; "
                                "expected = planc_oracle.run_graph (float64, torch-pinned)",
-                    spec=dict(strategy="megatron_tp", devices=k, tokens=T, hidden=H, head=hd, elem_size=e,
-                              train=train),
+                    spec=dict(spec, **shape),
                     max_abs=max(float(np.abs(v).max()) for v in expected.values()),
                     lanes=len(pj["lanes"]), tasks=sum(len(lane["tasks"]) for lane in pj["lanes"]),
                     collectives=sorted({g["primitive"] for g in pj["coll_groups"]}),

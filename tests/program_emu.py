@@ -90,6 +90,12 @@ def exec_instr(ins: dict, data: dict, shape: dict):
         seg = ins["seg"] if ins["row_op"] < 4 else 1
         xs = [data[b].reshape(-1, seg) for b in ins["in"]]
         data[ins["out"][0]] = po.eval_ext(names[ins["row_op"]], xs, seg, ins["eps"]).reshape(-1)
+    elif k == "attention":  # schema extension: fused attention
+        from oracle import planc_oracle as po
+
+        a = ins["att"]
+        q, kk, v = (data[b].reshape(a["rows"], a["cols"]) for b in ins["in"])
+        data[ins["out"][0]] = po.attention(q, kk, v, a["head_dim"], a["seq"], a["causal"]).reshape(-1)
     elif k == "box":
         ob = ins["out"][0]
         out = data[ob].copy()  # a box writes only its cells (two-phase all-reduce: two boxes per output)

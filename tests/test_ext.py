@@ -79,3 +79,32 @@ def test_ext_unknown_kind_is_schema_error():
     p["ops"][0]["kind"] = "attention"
     with pytest.raises(pb.SchemaError):
         pb.describe(json.dumps(p))
+
+
+def test_attention_lowering_and_piece_rules():
+    """Fused attention (schema extension): head (TP) and sequence splits lower
+    to one attention instruction per lane; a piece cutting a sequence is a
+    UsageError at lowering; the lowered program interpreted in numpy equals
+    the float64 graph oracle."""
+    import json
+
+    import numpy as np
+
+    from oracle import docs, planc_oracle, refpy
+    from program_emu import run_program
+
+    doc = docs.attention_doc(512, 2, 128, 256, causal=True)
+    stand = docs.dumps(docs.standin_doc(doc))
+    for spec in (dict(strategy="megatron_tp", devices=2), dict(strategy="manual", devices=2, target_ops="tpattn@s0")):
+        plan = docs.rewrite_plan(refpy.compile_plan(stand, **spec), doc)
+        d = pb.describe(plan)
+        att = [i for i in d["instrs"] if i["kind"] == "attention"]
+        assert len(att) == 2 and all(i["att"]["causal"] for i in att)
+        rng = np.random.default_rng(1)
+        inputs = {i: rng.standard_normal((512, 256)) for i in range(3)}
+        out = run_program(d, json.loads(plan), inputs)
+        ref = planc_oracle.run_graph(docs.dumps(doc), inputs)
+        assert np.abs(out[3] - ref[3]).max() < 1e-12
+    bad = docs.rewrite_plan(refpy.compile_plan(stand, strategy="manual", devices=4, target_ops="tpattn@s0"), doc)
+    with pytest.raises(pb.UsageError, match="whole sequences"):
+        pb.describe(bad)
