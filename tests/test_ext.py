@@ -76,7 +76,7 @@ def test_ext_layernorm_on_split_rows_is_usage_error():
 def test_ext_unknown_kind_is_schema_error():
     g = golden_cases.load("ext_block_tp1")
     p = json.loads(g["plan"])
-    p["ops"][0]["kind"] = "attention"
+    p["ops"][0]["kind"] = "rotary-embedding"
     with pytest.raises(pb.SchemaError):
         pb.describe(json.dumps(p))
 
