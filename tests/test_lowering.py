@@ -238,7 +238,7 @@ def test_malformed_plan_is_schema_error():
     with pytest.raises(pb.SchemaError):
         pb.describe(json.dumps({"ptensors": []}))
     plan = json.loads(golden_cases.load("mlp_dp2")["plan"])
-    plan["ops"][0]["kind"] = "attention"  # not a kind (softmax is the schema extension, tests/test_ext.py)
+    plan["ops"][0]["kind"] = "rotary-embedding"  # not a kind (softmax, attention are the schema extension, tests/test_ext.py)
     with pytest.raises(pb.SchemaError):
         pb.describe(json.dumps(plan))
 
