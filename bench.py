@@ -48,7 +48,7 @@ def plan_name(config: str, n: int) -> str:
     x DAP (c5: 4 stages x dap 2) plans have 8 lanes — with fewer GPUs, lanes
     share GPUs (round robin)."""
     return {"c2": f"c2_tp{n}", "c2x": f"c2x_tp{n}", "c1l": f"c1l_dp{n}", "c3": "c3_pp4dp2_l24", "c4": "c4_coshard4_dp8",
-            "c5": "c5_3f1b_dap", "c2sp": f"c2sp_tp{max(n, 2)}"}[config]
+            "c5": "c5_3f1b_dap", "c2sp": f"c2sp_tp{max(n, 2)}", "c2a": f"c2a_tp{n}"}[config]
 
 
 def nvlink_peer_bandwidth(nbytes: int = 512 << 20, reps: int = 5):
@@ -96,7 +96,7 @@ def cpu_plan_name(config: str) -> str:
         return "c3_pp4dp2_cpu"
     if config == "c2sp":
         return "c2_tp1_cpu"  # the same graph (sequence parallelism only renames the residual ops' split)
-    return plan_name(config, 1) + "_cpu" + ("_standin" if config == "c2x" else "")
+    return plan_name(config, 1) + "_cpu" + ("_standin" if config in ("c2x", "c2a") else "")
 
 
 def load_plan(name):
@@ -246,10 +246,10 @@ def cpu_baseline(config: str, budget_s: float = 20.0):
 
     name = cpu_plan_name(config)
     note = ""
-    if config == "c2x":
-        # The reference executor has no layernorm / softmax / GELU: it runs the
-        # stand-in plan (identity / mul in their place, same data flow).
-        note = "; stand-in plan: identity/mul where the extension has LN/softmax/GELU"
+    if config in ("c2x", "c2a"):
+        # The reference executor has no layernorm / softmax / GELU / attention:
+        # it runs the stand-in plan (identity / mul / add in their place, same data flow).
+        note = "; stand-in plan: identity/mul/add where the extension has LN/softmax/GELU/attention"
     if config == "c3":
         note = "; 4-layer stack (the 24-layer plan takes the reference ~1 min per step)"
     plan, meta = load_plan(name)
@@ -354,7 +354,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c2", "c2x", "c1l", "c3", "c4", "c5", "c2sp"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c2x", "c1l", "c3", "c4", "c5", "c2sp", "c2a"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sustain-s", type=float, default=3.0, help="seconds of the sustained timed region")
@@ -503,7 +503,7 @@ def main():
                 traffic, traffic_src = tj[top]["mean"], tj["source"]
         except Exception:
             pass
-        if top.startswith("gemm"):
+        if top.startswith("gemm") or top == "attention":
             achieved = t["flops"] / (t["ms"] / 1e3) / 1e12
             # fused elementwise epilogues add their operand / result bytes at
             # HBM speed to the tensor-bound time (0 without fusion)
@@ -533,8 +533,10 @@ def main():
         F, M, W = [0.0] * n, [0.0] * n, [0.0] * n
         for ins in desc["instrs"]:
             gidx = gpu_of[ins["lane"]]
-            if ins["kind"] == "gemm":
+            if ins["kind"] in ("gemm", "attention"):  # tensor-core work (attention: QK^T and PV)
                 F[gidx] += ins["flops"]
+                if ins["kind"] == "attention":
+                    M[gidx] += ins["bytes"]
             else:
                 M[gidx] += ins["bytes"]
             if n > 1:
@@ -542,8 +544,8 @@ def main():
         t_roof = max(max(F[i] / (peaks["bf16_sus"] * 1e12) + M[i] / (peaks["hbm"] * 1e9),
                          W[i] / (NVLINK_GBS * 1e9)) for i in range(n))
         families = {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
-                        "tflops" if k.startswith("gemm") else "gbs":
-                            round((v["flops"] / 1e12 if k.startswith("gemm") else v["bytes"] / 1e9)
+                        "tflops" if k.startswith("gemm") or k == "attention" else "gbs":
+                            round((v["flops"] / 1e12 if k.startswith("gemm") or k == "attention" else v["bytes"] / 1e9)
                                   / max(v["ms"] / 1e3, 1e-12), 2)} for k, v in fam.items()}
         # Adapter bus bandwidth: wire bytes (NCCL bus-bandwidth convention) of
         # the cross-GPU adapter launches over their device time.
@@ -560,7 +562,7 @@ def main():
                        "shape": {k: meta[k] for k in ("tokens", "batch", "hidden", "middle", "layers", "head", "msa", "pair",
                                                                   "micro_batches") if k in meta},
                        "parallelism": {"c2": f"tp{n}", "c2x": f"tp{n}", "c1l": f"dp{n}", "c3": "pp4 x dp2 (1F1B, K=8)",
-                                       "c2sp": f"tp{max(n, 2)} + sequence parallel",
+                                       "c2sp": f"tp{max(n, 2)} + sequence parallel", "c2a": f"tp{n} (forward)",
                                        "c4": "dp8 x co-shard 4 (FFN)",
                                        "c5": "3F1B pp4 x dap2 (K=4)"}[args.config],
                        "lanes_per_gpu": nlanes / max(n, 1),

@@ -286,6 +286,43 @@ def rewrite_plan(plan_json: str, doc: dict) -> str:
     return json.dumps(p)
 
 
+def gpt_block_attn_doc(tokens: int, hidden: int, head_dim: int, seq: int, elem_size: int = 2) -> dict:
+    """Transformer block forward with real attention (config C2a, inference
+    prefill): N1 = LN(X); Q, K, V = N1·Wq, N1·Wk, N1·Wv (column-parallel);
+    A = attention(Q, K, V) (causal, per head, split with the heads); O = A·Wo
+    (row-parallel); X2 = O + X; N2 = LN(X2); F1 = N2·W1 (column-parallel);
+    Fa = GELU(F1); Y = Fa·W2 (row-parallel); OUT = Y + X2."""
+    T, H, Fd = tokens, hidden, 4 * hidden
+    e = elem_size
+    ids = dict(X=0, Wq=1, Wk=2, Wv=3, Wo=4, W1=5, W2=6, N1=10, Q=11, K=12, V=13, A=14, O=15, X2=16, N2=17, F1=18,
+               Fa=19, Y=20, OUT=21)
+    pts = [_pt(ids["X"], (T, H), "activation", e)]
+    for w, shp in (("Wq", (H, H)), ("Wk", (H, H)), ("Wv", (H, H)), ("Wo", (H, H)), ("W1", (H, Fd)), ("W2", (Fd, H))):
+        pts.append(_pt(ids[w], shp, "weight", e))
+    for a, shp in (("N1", (T, H)), ("Q", (T, H)), ("K", (T, H)), ("V", (T, H)), ("A", (T, H)), ("O", (T, H)),
+                   ("X2", (T, H)), ("N2", (T, H)), ("F1", (T, Fd)), ("Fa", (T, Fd)), ("Y", (T, H)),
+                   ("OUT", (T, H))):
+        pts.append(_pt(ids[a], shp, "activation", e))
+    A = {"layer": 0, "batch_dim": 0}
+    mm = lambda m, n, k: 2.0 * m * n * k  # noqa: E731
+    ops = [
+        _op("ln1", "layernorm", [ids["X"]], [ids["N1"]], "forward", 8 * T * H, A),
+        _op("colq", "matmul", [ids["N1"], ids["Wq"]], [ids["Q"]], "forward", mm(T, H, H), A),
+        _op("colk", "matmul", [ids["N1"], ids["Wk"]], [ids["K"]], "forward", mm(T, H, H), A),
+        _op("colv", "matmul", [ids["N1"], ids["Wv"]], [ids["V"]], "forward", mm(T, H, H), A),
+        _op("tpattn", "attention", [ids["Q"], ids["K"], ids["V"]], [ids["A"]], "forward", 2.0 * T * seq * H,
+            dict(A, head_dim=head_dim, seq=seq, causal=True)),
+        _op("rowo", "matmul", [ids["A"], ids["Wo"]], [ids["O"]], "forward", mm(T, H, H), A),
+        _op("res1", "add", [ids["O"], ids["X"]], [ids["X2"]], "forward", T * H, A),
+        _op("ln2", "layernorm", [ids["X2"]], [ids["N2"]], "forward", 8 * T * H, A),
+        _op("colf1", "matmul", [ids["N2"], ids["W1"]], [ids["F1"]], "forward", mm(T, Fd, H), A),
+        _op("tpgelu", "gelu", [ids["F1"]], [ids["Fa"]], "forward", 8 * T * Fd, A),
+        _op("roww2", "matmul", [ids["Fa"], ids["W2"]], [ids["Y"]], "forward", mm(T, H, Fd), A),
+        _op("res2", "add", [ids["Y"], ids["X2"]], [ids["OUT"]], "forward", T * H, A),
+    ]
+    return {"ptensors": pts, "ops": ops}
+
+
 def attention_doc(tokens: int, heads: int, head_dim: int, seq: int, causal: bool = False, elem_size: int = 2,
                   prefix: str = "tp") -> dict:
     """One fused attention op O = attention(Q, K, V) over [tokens, heads x

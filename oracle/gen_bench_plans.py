@@ -142,6 +142,25 @@ def gen_ref1():
         write(name, g, plan, dict(config=name[:2], strategy="none", dtype="bf16"))
 
 
+def gen_c2a():
+    """C2a: the block forward with real (fused, causal) attention — 4
+    sequences of 2048 tokens, 16 heads of 128 — Megatron TP 1/2/4/8; the
+    *_cpu twin (T=256: 2 sequences of 128, H=128, 1 head) and its stand-in
+    plan for the reference CPU executor."""
+    for T, H, hd, seq, tag in ((8192, 2048, 128, 2048, ""), (256, 128, 128, 128, "_cpu")):
+        doc = docs.gpt_block_attn_doc(T, H, hd, seq)
+        stand = docs.dumps(docs.standin_doc(doc))
+        meta = dict(config="c2a", tokens=T, hidden=H, head=hd, seq=seq, dtype="bf16", samples_per_step=T,
+                    sample="token (row of X)", extension=True, note="forward only (inference prefill)")
+        for k in (1, 2, 4, 8):
+            if tag and k > 1:
+                continue
+            plan = refpy.compile_plan(stand, strategy="megatron_tp", devices=k)
+            write(f"c2a_tp{k}{tag}", docs.dumps(doc), docs.rewrite_plan(plan, doc), dict(meta, tp=k))
+            if tag:
+                write(f"c2a_tp{k}{tag}_standin", stand, plan, dict(meta, tp=k, standin=True))
+
+
 def gen_c2sp():
     g = docs.dumps(docs.gpt_block_doc(8192, 2048, elem_size=2, train=True, seq_parallel=True))
     for k in (2, 4, 8):
@@ -155,7 +174,7 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     only = set(sys.argv[1:])
     if only:
-        for name, fn in (("c2x", gen_c2x), ("c2sp", gen_c2sp), ("c3l24", gen_c3_l24), ("c4", gen_c4), ("c5", gen_c5)):
+        for name, fn in (("c2x", gen_c2x), ("c2sp", gen_c2sp), ("c2a", gen_c2a), ("c3l24", gen_c3_l24), ("c4", gen_c4), ("c5", gen_c5)):
             if name in only:
                 fn()
         if "ref1" in only:
@@ -163,6 +182,7 @@ def main():
         return
     gen_c2x()
     gen_c2sp()
+    gen_c2a()
     for T, H, tag in ((8192, 2048, ""), (128, 128, "_cpu")):
         g = docs.dumps(docs.gpt_block_doc(T, H, elem_size=2, train=True))
         for k in (1, 2, 4, 8):
