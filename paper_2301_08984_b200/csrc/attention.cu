@@ -26,7 +26,7 @@ namespace planc_b200 {
 
 namespace {
 
-constexpr int kAttnThreads = 192;
+constexpr int kAttnThreads = 64 + 8 * 32;  // producer, MMA, 8 softmax warps
 constexpr int kAttnBlock = 128;  // query / key rows per tile
 
 template <int DH>
@@ -35,7 +35,8 @@ struct AttnCfg {
   static constexpr int K_BYTES = kAttnBlock * DH * 2;
   static constexpr int V_BYTES = kAttnBlock * DH * 2;   // 2 kv chunks x DH/64 n-blocks of 8 KB
   static constexpr int P_BYTES = kAttnBlock * kAttnBlock * 2;  // 2 kv chunks of 16 KB
-  static constexpr int SMEM = Q_BYTES + 2 * (K_BYTES + V_BYTES) + 2 * P_BYTES + 1024 + 1024;
+  // + 1024-byte alignment slack, barriers / TMEM slot (256 B), pair-exchange rows (2 x 128 floats)
+  static constexpr int SMEM = Q_BYTES + 2 * (K_BYTES + V_BYTES) + 2 * P_BYTES + 1024 + 256 + 1024;
   static_assert(SMEM <= 227 * 1024, "attention tiles above the shared memory limit");
 };
 
@@ -74,7 +75,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  // causal: the longest query blocks (most keys) are scheduled first
+  const int qb = CAUSAL ? static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+  const int h = blockIdx.y, b = blockIdx.z;
   const int row0 = b * seq + qb * kAttnBlock;  // first query row of the tile
   const int col0 = h * DH;
   const int nkv = CAUSAL ? qb + 1 : seq / kAttnBlock;
@@ -88,11 +91,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&s_empty[i], 8);
+      mbar_init(&p_full[i], 8);
       mbar_init(&p_empty[i], 1);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 4);
+      mbar_init(&o_empty[i], 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -172,24 +175,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       pdl_trigger();
     }
   } else {
-    // Softmax warps: row r of the tile = TMEM lane r.
-    const int qr = warp % 4;
+    // Softmax warps 2..9: row r of the tile = TMEM lane r; the two warps of a
+    // lane quarter split its columns (scores: 64 keys each; output: DH/2
+    // features each) and exchange row maxima / sums through shared memory
+    // under a 64-thread named barrier (one per quarter).
+    const int qr = warp % 4, half = (warp - 2) / 4;
     const int r = qr * 32 + lane;
     const std::uint32_t lane_base = tmem + (static_cast<std::uint32_t>(qr * 32) << 16);
-    float acc[DH];
+    float* xch = reinterpret_cast<float*>(bars + 32);  // [2 halves][128 rows]
+    auto pair_sync = [&] { asm volatile("bar.sync %0, 64;" ::"r"(1 + qr) : "memory"); };
+    constexpr int HD = DH / 2;
+    float acc[HD];
 #pragma unroll
-    for (int i = 0; i < DH; ++i) acc[i] = 0.f;
+    for (int i = 0; i < HD; ++i) acc[i] = 0.f;
     float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
-    auto accumulate = [&](int i, float alpha) {  // acc = acc * alpha + O[i%2]
+    auto accumulate = [&](int i, float alpha) {  // acc = acc * alpha + O[i%2] (this warp's features)
       const int st = i & 1;
       mbar_wait(&o_full[st], (i >> 1) & 1);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < DH / 32; ++c) {
+      for (int c = 0; c < HD / 32; ++c) {
         std::uint32_t v[32];
-        tmem_ld32(lane_base + 256 + st * DH + c * 32, v);
+        tmem_ld32(lane_base + 256 + st * DH + half * HD + c * 32, v);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) acc[c * 32 + e] = acc[c * 32 + e] * alpha + __uint_as_float(v[e]);
+        for (int e = 0; e < 32; ++e) acc[c * 32 + e] = fmaf(acc[c * 32 + e], alpha, __uint_as_float(v[e]));
       }
       tc_fence_before();
       __syncwarp();
@@ -199,27 +208,31 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const int st = j & 1;
       mbar_wait(&s_full[st], (j >> 1) & 1);
       tc_fence_after();
-      const std::uint32_t sb = lane_base + st * kAttnBlock;
+      const std::uint32_t sb = lane_base + st * kAttnBlock + half * 64;
       const bool diag = CAUSAL && j == qb;  // keys above the query row are masked
-      // pass 1: row max (base-2 scaled scores)
+      const int key0 = half * 64;
+      // pass 1: row max of the raw scores (the scale is positive), pair-combined
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < kAttnBlock / 32; ++c) {
+      for (int c = 0; c < 2; ++c) {
         std::uint32_t v[32];
         tmem_ld32(sb + c * 32, v);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float s = __uint_as_float(v[e]) * scale_log2;
-          if (!diag || c * 32 + e <= r) mx = fmaxf(mx, s);
-        }
+        for (int e = 0; e < 32; ++e)
+          if (!diag || key0 + c * 32 + e <= r) mx = fmaxf(mx, __uint_as_float(v[e]));
       }
-      const float m_new = fmaxf(m, mx);
-      // pass 2: P = exp2(s - m_new) as bf16 into the swizzled A-operand tile
+      xch[half * 128 + r] = mx;
+      pair_sync();
+      mx = fmaxf(xch[r], xch[128 + r]);
+      pair_sync();  // both halves read before the next block's maxima land
+      const float m_new = fmaxf(m, mx * scale_log2);
+      // pass 2: P = exp2(s * scale - m_new) as bf16 into this warp's 64-key
+      // atom of the swizzled A-operand tile
       mbar_wait(&p_empty[st], ((j >> 1) & 1) ^ 1);
-      std::uint8_t* prow = sP + st * CF::P_BYTES + r * 128;
+      std::uint8_t* prow = sP + st * CF::P_BYTES + half * 16384 + r * 128;
       float sum = 0.f;
 #pragma unroll
-      for (int c = 0; c < kAttnBlock / 32; ++c) {
+      for (int c = 0; c < 2; ++c) {
         std::uint32_t v[32];
         tmem_ld32(sb + c * 32, v);
 #pragma unroll
@@ -228,20 +241,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
           for (int h2 = 0; h2 < 4; ++h2) {
             const int e = 8 * g + 2 * h2;
-            const float s0 = __uint_as_float(v[e]) * scale_log2, s1 = __uint_as_float(v[e + 1]) * scale_log2;
-            const float p0 = (!diag || c * 32 + e <= r) ? ex2(s0 - m_new) : 0.f;
-            const float p1 = (!diag || c * 32 + e + 1 <= r) ? ex2(s1 - m_new) : 0.f;
+            const float p0 = (!diag || key0 + c * 32 + e <= r) ? ex2(fmaf(__uint_as_float(v[e]), scale_log2, -m_new)) : 0.f;
+            const float p1 =
+                (!diag || key0 + c * 32 + e + 1 <= r) ? ex2(fmaf(__uint_as_float(v[e + 1]), scale_log2, -m_new)) : 0.f;
+            sum += p0 + p1;
             w[h2] = bf16_pair(p0, p1);
-            // the MMA consumes bf16 P: sum the rounded values it multiplies
-            float lo, hi;
-            bf16_unpair(w[h2], lo, hi);
-            sum += lo + hi;
           }
-          // 16-byte chunk (c * 4 + g) of the row: chunks 0-7 in the first
-          // 64-key atom, 8-15 in the second; 128B swizzle: chunk ^ (row & 7)
-          const int chunk = c * 4 + g;
-          const int atom = chunk >> 3, cw = chunk & 7;
-          *reinterpret_cast<uint4*>(prow + atom * 16384 + ((cw ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+          const int cw = c * 4 + g;  // 16-byte chunk of the 128-byte row; 128B swizzle: chunk ^ (row & 7)
+          *reinterpret_cast<uint4*>(prow + ((cw ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
@@ -252,19 +259,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mbar_arrive(&s_empty[st]);
       }
       const float alpha = ex2(m - m_new);  // (m = -inf on the first block: alpha = 0, acc is 0)
-      l = l * alpha + sum;
+      l = l * alpha + sum;                  // this warp's keys only; halves added at the end
       m = m_new;
       if (j > 0) accumulate(j - 1, alpha_prev);
       alpha_prev = alpha;
     }
     accumulate(nkv - 1, alpha_prev);
-    // acc holds sum_j exp2(m_final...) weighted rows: every accumulate step
-    // rescaled the running sum to the block's max before adding O_j, which
-    // was computed against that same max.
-    const float inv = 1.f / l;
-    __nv_bfloat16* orow = out + static_cast<std::int64_t>(row0 + r) * ld + col0;
+    // acc: sum over blocks of P_j·V_j, each rescaled to the running max;
+    // l: this warp's share of the row sum (same maxima) — add the pair's.
+    xch[half * 128 + r] = l;
+    pair_sync();
+    const float inv = 1.f / (xch[r] + xch[128 + r]);
+    __nv_bfloat16* orow = out + static_cast<std::int64_t>(row0 + r) * ld + col0 + half * HD;
 #pragma unroll
-    for (int g = 0; g < DH / 8; ++g)
+    for (int g = 0; g < HD / 8; ++g)
       reinterpret_cast<uint4*>(orow)[g] =
           make_uint4(bf16_pair(acc[8 * g] * inv, acc[8 * g + 1] * inv), bf16_pair(acc[8 * g + 2] * inv, acc[8 * g + 3] * inv),
                      bf16_pair(acc[8 * g + 4] * inv, acc[8 * g + 5] * inv), bf16_pair(acc[8 * g + 6] * inv, acc[8 * g + 7] * inv));
