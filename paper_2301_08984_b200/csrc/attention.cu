@@ -44,6 +44,28 @@ struct AttnMaps {
   CUtensorMap q, k, v;
 };
 
+// tcgen05.ld 32x32b.x64: 64 consecutive TMEM columns of this thread's lane,
+// one wait (tcgen05.wait::ld) for all of them.
+__device__ __forceinline__ void tmem_ld64(std::uint32_t taddr, std::uint32_t (&r)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+      "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+      "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]),
+        "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]),
+        "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+        "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]),
+        "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -193,12 +215,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const int st = i & 1;
       mbar_wait(&o_full[st], (i >> 1) & 1);
       tc_fence_after();
+      if constexpr (HD == 64) {
+        std::uint32_t v[64];
+        tmem_ld64(lane_base + 256 + st * DH + half * HD, v);
 #pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
+        for (int e = 0; e < 64; ++e) acc[e] = fmaf(acc[e], alpha, __uint_as_float(v[e]));
+      } else {
         std::uint32_t v[32];
-        tmem_ld32(lane_base + 256 + st * DH + half * HD + c * 32, v);
+        tmem_ld32(lane_base + 256 + st * DH + half * HD, v);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) acc[c * 32 + e] = fmaf(acc[c * 32 + e], alpha, __uint_as_float(v[e]));
+        for (int e = 0; e < 32; ++e) acc[e] = fmaf(acc[e], alpha, __uint_as_float(v[e]));
       }
       tc_fence_before();
       __syncwarp();
@@ -211,16 +237,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const std::uint32_t sb = lane_base + st * kAttnBlock + half * 64;
       const bool diag = CAUSAL && j == qb;  // keys above the query row are masked
       const int key0 = half * 64;
+      // this warp's 64 scores of the row stay in registers for both passes
+      std::uint32_t v[64];
+      tmem_ld64(sb, v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[st]);  // S[st] may be overwritten (S_{j+2})
       // pass 1: row max of the raw scores (the scale is positive), pair-combined
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        std::uint32_t v[32];
-        tmem_ld32(sb + c * 32, v);
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (!diag || key0 + c * 32 + e <= r) mx = fmaxf(mx, __uint_as_float(v[e]));
-      }
+      for (int e = 0; e < 64; ++e)
+        if (!diag || key0 + e <= r) mx = fmaxf(mx, __uint_as_float(v[e]));
       xch[half * 128 + r] = mx;
       pair_sync();
       mx = fmaxf(xch[r], xch[128 + r]);
@@ -232,32 +259,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       std::uint8_t* prow = sP + st * CF::P_BYTES + half * 16384 + r * 128;
       float sum = 0.f;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        std::uint32_t v[32];
-        tmem_ld32(sb + c * 32, v);
+      for (int cw = 0; cw < 8; ++cw) {  // 16-byte chunk of the 128-byte row; 128B swizzle: chunk ^ (row & 7)
+        std::uint32_t w[4];
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          std::uint32_t w[4];
-#pragma unroll
-          for (int h2 = 0; h2 < 4; ++h2) {
-            const int e = 8 * g + 2 * h2;
-            const float p0 = (!diag || key0 + c * 32 + e <= r) ? ex2(fmaf(__uint_as_float(v[e]), scale_log2, -m_new)) : 0.f;
-            const float p1 =
-                (!diag || key0 + c * 32 + e + 1 <= r) ? ex2(fmaf(__uint_as_float(v[e + 1]), scale_log2, -m_new)) : 0.f;
-            sum += p0 + p1;
-            w[h2] = bf16_pair(p0, p1);
-          }
-          const int cw = c * 4 + g;  // 16-byte chunk of the 128-byte row; 128B swizzle: chunk ^ (row & 7)
-          *reinterpret_cast<uint4*>(prow + ((cw ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        for (int h2 = 0; h2 < 4; ++h2) {
+          const int e = 8 * cw + 2 * h2;
+          const float p0 = (!diag || key0 + e <= r) ? ex2(fmaf(__uint_as_float(v[e]), scale_log2, -m_new)) : 0.f;
+          const float p1 = (!diag || key0 + e + 1 <= r) ? ex2(fmaf(__uint_as_float(v[e + 1]), scale_log2, -m_new)) : 0.f;
+          sum += p0 + p1;
+          w[h2] = bf16_pair(p0, p1);
         }
+        *reinterpret_cast<uint4*>(prow + ((cw ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&p_full[st]);
-        mbar_arrive(&s_empty[st]);
-      }
+      if (lane == 0) mbar_arrive(&p_full[st]);
       const float alpha = ex2(m - m_new);  // (m = -inf on the first block: alpha = 0, acc is 0)
       l = l * alpha + sum;                  // this warp's keys only; halves added at the end
       m = m_new;
