@@ -86,15 +86,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   std::uint8_t* sP = sV + 2 * CF::V_BYTES;             // [2][P_BYTES]
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sP + 2 * CF::P_BYTES);
   std::uint64_t* q_full = bars;
-  std::uint64_t* kv_full = bars + 1;   // [2]
-  std::uint64_t* kv_empty = bars + 3;  // [2]
+  std::uint64_t* k_full = bars + 1;    // [2]
+  std::uint64_t* k_empty = bars + 3;   // [2]
   std::uint64_t* s_full = bars + 5;    // [2]
   std::uint64_t* s_empty = bars + 7;   // [2]
   std::uint64_t* p_full = bars + 9;    // [2]
   std::uint64_t* p_empty = bars + 11;  // [2]
   std::uint64_t* o_full = bars + 13;   // [2]
   std::uint64_t* o_empty = bars + 15;  // [2]
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 17);
+  std::uint64_t* v_full = bars + 17;   // [2]
+  std::uint64_t* v_empty = bars + 19;  // [2]
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 21);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // causal: the longest query blocks (most keys) are scheduled first
@@ -110,8 +112,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&mp.v)) : "memory");
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 8);
       mbar_init(&p_full[i], 8);
@@ -137,21 +141,33 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_expect_tx(q_full, CF::Q_BYTES);
 #pragma unroll
       for (int c = 0; c < DH / 64; ++c) tma_load_2d(sQ + c * 16384, &mp.q, col0 + 64 * c, row0, q_full);
-      for (int j = 0; j < nkv; ++j) {
+      // K_j is freed by S_j, V_j only by P_j·V_j: K runs one block ahead of V
+      // so the next score tile never waits for a value tile's release.
+      auto load_k = [&](int j) {
         const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], CF::K_BYTES + CF::V_BYTES);
-        const int kr = b * seq + j * kAttnBlock;
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], CF::K_BYTES);
         std::uint8_t* k = sK + st * CF::K_BYTES;
-        std::uint8_t* v = sV + st * CF::V_BYTES;
 #pragma unroll
-        for (int c = 0; c < DH / 64; ++c) tma_load_2d(k + c * 16384, &mp.k, col0 + 64 * c, kr, &kv_full[st]);
-        // V as an MN-major B operand: per 64-key chunk, DH/64 blocks of 64 features
+        for (int c = 0; c < DH / 64; ++c)
+          tma_load_2d(k + c * 16384, &mp.k, col0 + 64 * c, b * seq + j * kAttnBlock, &k_full[st]);
+      };
+      auto load_v = [&](int j) {  // V as an MN-major B operand: per 64-key chunk, DH/64 blocks of 64 features
+        const int st = j & 1;
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], CF::V_BYTES);
+        std::uint8_t* v = sV + st * CF::V_BYTES;
 #pragma unroll
         for (int kc = 0; kc < 2; ++kc)
 #pragma unroll
           for (int nb = 0; nb < DH / 64; ++nb)
-            tma_load_2d(v + kc * (DH / 64) * 8192 + nb * 8192, &mp.v, col0 + 64 * nb, kr + 64 * kc, &kv_full[st]);
+            tma_load_2d(v + kc * (DH / 64) * 8192 + nb * 8192, &mp.v, col0 + 64 * nb,
+                        b * seq + j * kAttnBlock + 64 * kc, &v_full[st]);
+      };
+      load_k(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) load_k(j + 1);
+        load_v(j);
       }
     }
   } else if (warp == 1) {
@@ -161,6 +177,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_wait(q_full, 0);
       auto pv = [&](int i) {  // O[i%2] = P[i%2] · V[i%2]
         const int st = i & 1;
+        mbar_wait(&v_full[st], (i >> 1) & 1);
         mbar_wait(&p_full[st], (i >> 1) & 1);
         mbar_wait(&o_empty[st], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -173,13 +190,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                  smem_desc(v + kc * (DH / 64) * 8192 + kk * 2048, 8192, 1024), idesc_o, s > 0 ? 1u : 0u);
         }
         tc_commit(&o_full[st]);
-        tc_commit(&kv_empty[st]);  // K_i / V_i consumed (S_i issued earlier)
+        tc_commit(&v_empty[st]);  // V_i consumed
         tc_commit(&p_empty[st]);
       };
       const std::uint32_t q = smem_u32(sQ);
       for (int j = 0; j < nkv; ++j) {
         const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(&k_full[st], (j >> 1) & 1);
         mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const std::uint32_t k = smem_u32(sK + st * CF::K_BYTES);
@@ -191,6 +208,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                  idesc_s, s > 0 ? 1u : 0u);
         }
         tc_commit(&s_full[st]);
+        tc_commit(&k_empty[st]);  // K_j consumed
         if (j > 0) pv(j - 1);
       }
       pv(nkv - 1);
@@ -204,7 +222,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int qr = warp % 4, half = (warp - 2) / 4;
     const int r = qr * 32 + lane;
     const std::uint32_t lane_base = tmem + (static_cast<std::uint32_t>(qr * 32) << 16);
-    float* xch = reinterpret_cast<float*>(bars + 32);  // [2 halves][128 rows]
+    float* xch = reinterpret_cast<float*>(bars + 32);  // [2 halves][128 rows] (bars: 22 words used)
     auto pair_sync = [&] { asm volatile("bar.sync %0, 64;" ::"r"(1 + qr) : "memory"); };
     constexpr int HD = DH / 2;
     float acc[HD];
@@ -267,7 +285,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           const float p0 = (!diag || key0 + e <= r) ? ex2(fmaf(__uint_as_float(v[e]), scale_log2, -m_new)) : 0.f;
           const float p1 = (!diag || key0 + e + 1 <= r) ? ex2(fmaf(__uint_as_float(v[e + 1]), scale_log2, -m_new)) : 0.f;
           sum += p0 + p1;
-          w[h2] = bf16_pair(p0, p1);
+          const __nv_bfloat162 pk = __floats2bfloat162_rn(p0, p1);  // one packed convert (FMA pipe, not XU)
+          w[h2] = *reinterpret_cast<const std::uint32_t*>(&pk);
         }
         *reinterpret_cast<uint4*>(prow + ((cw ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
