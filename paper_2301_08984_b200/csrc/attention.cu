@@ -5,7 +5,7 @@
 //
 // Layout: Q, K, V, O are a piece's [rows, cols] bf16 tensors (row-major):
 // rows = whole sequences of `seq` tokens, cols = whole heads of `dh`
-// features. CTA (qb, h, b) computes the 128 query rows qb of head h of
+// features. CTA (h, b, qb) computes the 128 query rows qb of head h of
 // sequence b.
 //
 // Warps: 0 TMA producer (Q once; K_j / V_j 128-row tiles through a 2-stage
@@ -99,9 +99,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 21);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // causal: the longest query blocks (most keys) are scheduled first
-  const int qb = CAUSAL ? static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
-  const int h = blockIdx.y, b = blockIdx.z;
+  // grid (head, sequence, query block), query blocks slowest: with a causal
+  // mask the longest blocks (most keys) are dispatched first (LPT order)
+  const int qb = CAUSAL ? static_cast<int>(gridDim.z) - 1 - static_cast<int>(blockIdx.z) : static_cast<int>(blockIdx.z);
+  const int h = blockIdx.x, b = blockIdx.y;
   const int row0 = b * seq + qb * kAttnBlock;  // first query row of the tile
   const int col0 = h * DH;
   const int nkv = CAUSAL ? qb + 1 : seq / kAttnBlock;
@@ -339,7 +340,7 @@ void attn_launch(const void* q, const void* k, const void* v, void* o, std::int6
   mp.k = make_map(k, rows, cols, kAttnBlock);
   mp.v = make_map(v, rows, cols, 64);
   const float scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(DH));
-  dim3 grid(static_cast<unsigned>(seq / kAttnBlock), static_cast<unsigned>(cols / DH), static_cast<unsigned>(rows / seq));
+  dim3 grid(static_cast<unsigned>(cols / DH), static_cast<unsigned>(rows / seq), static_cast<unsigned>(seq / kAttnBlock));
   pdl_launch("attn_fwd_kernel", kern, grid, dim3(kAttnThreads), AttnCfg<DH>::SMEM, s, mp,
              static_cast<__nv_bfloat16*>(o), static_cast<int>(seq), static_cast<int>(cols), scale_log2);
 }
@@ -352,7 +353,7 @@ const char* attention_unsupported(std::int64_t rows, std::int64_t cols, std::int
   if (head_dim != 64 && head_dim != 128) return "fused attention supports head_dim 64 or 128";
   if (seq <= 0 || seq % kAttnBlock != 0) return "fused attention needs seq a multiple of 128";
   if (rows % seq != 0 || cols % head_dim != 0) return "attention piece does not hold whole sequences and heads";
-  if (rows / seq > 65535 || cols / head_dim > 65535) return "attention piece above the grid limits";
+  if (rows / seq > 65535 || seq / kAttnBlock > 65535) return "attention piece above the grid limits";
   return nullptr;
 }
 
