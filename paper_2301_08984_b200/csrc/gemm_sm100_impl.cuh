@@ -1195,6 +1195,22 @@ inline void l2_plan(const GemmArgs& a, SkParams& sk) {
   const double g = std::max(a.group, 1);
   const double bytes_a = g * a.m * a.k * 2.0, bytes_b = g * a.k * a.n * 2.0;
   const double small = std::min(bytes_a, bytes_b), big = std::max(bytes_a, bytes_b);
+  // Launches that stream a large output (and, fused, as large an operand
+  // and result) through L2 evict the operand every raster group re-reads —
+  // all of B, once per group of M-blocks — even when A and B fit together:
+  // C2's fused 8192x8192x2048 launches read 356 MB for 201 MB of operands
+  // (profiles/r02/l2hint). There B is kept (evict_last) and A streams.
+  // PLANC_B200_L2HINT_STREAM=0 disables this case.
+  static const bool stream_rule = [] {
+    const char* e = std::getenv("PLANC_B200_L2HINT_STREAM");
+    return !(e && e[0] == '0');
+  }();
+  const double out_bytes = g * a.m * a.n * (a.dc == DT_BF16 ? 2.0 : 4.0) * (a.epi.n_ops > 0 ? 3.0 : 1.0);
+  if (stream_rule && small + big <= 96e6 && out_bytes >= 64e6 && bytes_b <= 48e6) {
+    sk.hint_b = 2;
+    if (mode == 2) sk.hint_a = 1;
+    return;
+  }
   if (small + big <= 96e6 || small > 48e6) return;
   const bool a_small = bytes_a <= bytes_b;
   (a_small ? sk.hint_a : sk.hint_b) = 2;
