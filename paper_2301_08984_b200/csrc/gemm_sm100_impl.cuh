@@ -1199,11 +1199,13 @@ inline void l2_plan(const GemmArgs& a, SkParams& sk) {
   // and result) through L2 evict the operand every raster group re-reads —
   // all of B, once per group of M-blocks — even when A and B fit together:
   // C2's fused 8192x8192x2048 launches read 356 MB for 201 MB of operands
-  // (profiles/r02/l2hint). There B is kept (evict_last) and A streams.
-  // PLANC_B200_L2HINT_STREAM=0 disables this case.
+  // (profiles/r02/l2hint). Keeping B (evict_last) with A streaming was
+  // measured worse (C2's fused 8192x8192x2048 launch 228 -> 237 us, 353 ->
+  // 473 MB read; profiles/r02/ab_l2_stream.jsonl): opt-in only,
+  // PLANC_B200_L2HINT_STREAM=1.
   static const bool stream_rule = [] {
     const char* e = std::getenv("PLANC_B200_L2HINT_STREAM");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   const double out_bytes = g * a.m * a.n * (a.dc == DT_BF16 ? 2.0 : 4.0) * (a.epi.n_ops > 0 ? 3.0 : 1.0);
   if (stream_rule && small + big <= 96e6 && out_bytes >= 64e6 && bytes_b <= 48e6) {
