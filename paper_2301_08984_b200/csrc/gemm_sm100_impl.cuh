@@ -344,8 +344,15 @@ __device__ __forceinline__ std::uint32_t cluster_addr(const void* p, std::uint32
   return r;
 }
 
+// Remote arrive on a pair CTA's mbarrier releasing an accumulator: relaxed.
+// It only has to follow this thread's TMEM reads, which have completed
+// (tcgen05.wait::ld returned them; tcgen05.fence::before_thread_sync orders
+// them) before the peer's MMA warp reuses the columns. A release arrive
+// compiles to MEMBAR.ALL.CTA / .GPU, which also wait for the epilogue's
+// in-flight operand prefetch loads — the top stall of the fused 2-SM launch
+// (~1/5 of its samples; profiles/r02/ncu_fused_gemm_*).
 __device__ __forceinline__ void mbar_arrive_cluster(std::uint32_t bar_cluster) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
 __device__ __forceinline__ void cluster_sync() {
@@ -464,9 +471,11 @@ __device__ __forceinline__ float epi_finish(float a) {
   return a;
 }
 
+// Two floats -> packed bf16x2 (round to nearest even): one F2FP pack on the
+// FMA / ALU pipes instead of two F2F conversions on the XU pipe.
 __device__ __forceinline__ std::uint32_t bf16_pair(float lo, float hi) {
-  return static_cast<std::uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(lo))) |
-         (static_cast<std::uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(hi))) << 16);
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const std::uint32_t*>(&v);
 }
 
 __device__ __forceinline__ void bf16_unpair(std::uint32_t w, float& lo, float& hi) {

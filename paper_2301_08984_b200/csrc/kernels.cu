@@ -61,9 +61,9 @@ __device__ __forceinline__ void unpack_word(std::uint32_t w, float& lo, float& h
   lo = __uint_as_float(w << 16);
   hi = __uint_as_float(w & 0xffff0000u);
 }
-__device__ __forceinline__ std::uint32_t pack_word(float lo, float hi) {
-  return static_cast<std::uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(lo))) |
-         (static_cast<std::uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(hi))) << 16);
+__device__ __forceinline__ std::uint32_t pack_word(float lo, float hi) {  // one F2FP pack (RNE)
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const std::uint32_t*>(&v);
 }
 
 template <typename T, int V>
