@@ -164,7 +164,9 @@ EXT_STANDIN = {"softmax": "identity", "layernorm": "identity", "gelu": "identity
                # attention(Q, K, V) partitions like a 3-operand elementwise op:
                # head (column) and sequence (row) splits carry over; the
                # executor rejects pieces that cut a sequence or a head
-               "attention": "add"}
+               "attention": "add",
+               # attention-grad(Q, K, V, O, dO) -> dQ | dK | dV ("wrt"): a 5-operand add
+               "attention-grad": "add"}
 EXT_ATTRS = ("segment", "eps", "head_dim", "seq", "causal")
 
 
@@ -258,7 +260,7 @@ def standin_doc(doc: dict) -> dict:
     for op in out["ops"]:
         if op["kind"] in EXT_STANDIN:
             op["kind"] = EXT_STANDIN[op["kind"]]
-            for a in ("segment", "head_dim", "seq", "causal"):
+            for a in ("segment", "head_dim", "seq", "causal", "wrt"):
                 op.get("attrs", {}).pop(a, None)
     return out
 
@@ -277,7 +279,7 @@ def rewrite_plan(plan_json: str, doc: dict) -> str:
             attrs = src.get("attrs", {})
             if attrs.get("segment"):
                 op["segment"] = attrs["segment"]
-            for a in ("eps", "head_dim", "seq", "causal"):
+            for a in ("eps", "head_dim", "seq", "causal", "wrt"):
                 if a in attrs:
                     op[a] = attrs[a]
             n += 1

@@ -169,6 +169,9 @@ def eval_compute(op, ins, in_masks, out_masks):
     if kind == "attention":
         return [attention(ins[0], ins[1], ins[2], op.get("head_dim", 0), op.get("seq", 0), op.get("causal", False),
                           in_masks)]
+    if kind == "attention-grad":
+        return [attention_grad(*ins[:5], op.get("head_dim", 0), op.get("seq", 0), op.get("causal", False),
+                               op.get("wrt", "q"), in_masks)]
     if kind in EXT_KINDS:
         return [eval_ext(kind, ins, op.get("segment", 0), op.get("eps", 1e-5), in_masks)]
     raise UsageError(f"refexec: unsupported op kind {kind} ({op['id']})")
@@ -200,6 +203,38 @@ def attention(q, k, v, head_dim, seq, causal=False, in_masks=None):
     p = np.exp(s - s.max(axis=-1, keepdims=True))
     p /= p.sum(axis=-1, keepdims=True)
     return (p @ vs).transpose(0, 2, 1, 3).reshape(T, D)
+
+
+def attention_grad(q, k, v, o, do, head_dim, seq, causal=False, wrt="q", in_masks=None):
+    """Gradient of attention (schema extension) with respect to Q, K or V,
+    given the forward output O and its incoming gradient dO, in float64:
+    P = softmax(Q·Kᵀ/sqrt(d) [causal]); D = rowsum(dO ∘ O);
+    dV = Pᵀ·dO; dS = P ∘ (dO·Vᵀ − D); dQ = dS·K/sqrt(d); dK = dSᵀ·Q/sqrt(d).
+    (D uses the supplied O, as the executor's kernels do.)"""
+    q, k, v, o, do = (np.asarray(x, dtype=np.float64) for x in (q, k, v, o, do))
+    T, D = q.shape
+    if head_dim <= 0 or seq <= 0 or T % seq or D % head_dim:
+        raise UsageError(f"attention-grad: piece [{T}, {D}] does not hold whole sequences / heads")
+    if in_masks is not None:
+        r = in_masks[0]["region"]
+        if r[0][0] % seq or r[1][0] % head_dim or any(m["region"] != r for m in in_masks):
+            raise UsageError("attention-grad: pieces not aligned to whole sequences / heads or not the same region")
+    nb, nh = T // seq, D // head_dim
+    sh = lambda x: x.reshape(nb, seq, nh, head_dim).transpose(0, 2, 1, 3)  # noqa: E731
+    qs, ks, vs, os_, dos = sh(q), sh(k), sh(v), sh(o), sh(do)
+    sc = 1.0 / np.sqrt(head_dim)
+    s = qs @ ks.transpose(0, 1, 3, 2) * sc
+    if causal:
+        s = np.where(np.tril(np.ones((seq, seq), dtype=bool)), s, -np.inf)
+    p = np.exp(s - s.max(axis=-1, keepdims=True))
+    p /= p.sum(axis=-1, keepdims=True)
+    if wrt == "v":
+        g = p.transpose(0, 1, 3, 2) @ dos
+    else:
+        dd = (dos * os_).sum(axis=-1, keepdims=True)
+        ds = p * (dos @ vs.transpose(0, 1, 3, 2) - dd)
+        g = (ds @ ks if wrt == "q" else ds.transpose(0, 1, 3, 2) @ qs) * sc
+    return g.transpose(0, 2, 1, 3).reshape(T, D)
 
 
 def _erf(x):

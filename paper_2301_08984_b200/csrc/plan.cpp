@@ -52,6 +52,7 @@ const char* op_kind_name(OpKind k) {
     case OpKind::collective: return "collective";
     case OpKind::free_buffer: return "free";
     case OpKind::attention: return "attention";
+    case OpKind::attention_grad: return "attention-grad";
     case OpKind::softmax: return "softmax";
     case OpKind::softmax_grad: return "softmax-grad";
     case OpKind::layernorm: return "layernorm";
@@ -76,7 +77,7 @@ OpKind op_kind_from_doc(const std::string& s) {
       // schema extension (oracle/planc_oracle.py eval_ext)
       {"softmax", OpKind::softmax}, {"softmax-grad", OpKind::softmax_grad}, {"layernorm", OpKind::layernorm},
       {"layernorm-grad", OpKind::layernorm_grad}, {"gelu", OpKind::gelu}, {"gelu-grad", OpKind::gelu_grad},
-      {"attention", OpKind::attention}};
+      {"attention", OpKind::attention}, {"attention-grad", OpKind::attention_grad}};
   auto it = m.find(s);
   if (it == m.end()) throw SchemaError("plan document: unknown op kind " + s);
   return it->second;
@@ -204,6 +205,11 @@ ExecutionPlan load_plan(const std::string& document) {
       if (o.contains("head_dim")) op.head_dim = o.at("head_dim").as_int();
       if (o.contains("seq")) op.seq = o.at("seq").as_int();
       if (o.contains("causal")) op.causal = o.at("causal").as_bool();
+      if (o.contains("wrt")) {
+        const std::string w = o.at("wrt").as_string();
+        if (w != "q" && w != "k" && w != "v") throw SchemaError("attention-grad wrt must be q, k or v");
+        op.wrt = w[0];
+      }
       if (op.segment < 0 || !(op.eps >= 0)) throw SchemaError("plan document: bad segment / eps on op " + op.id);
       plan.ops.push_back(std::move(op));
     }

@@ -85,6 +85,8 @@ enum class OpKind {
   // O = softmax(Q·Kᵀ/sqrt(head_dim) [causal])·V per sequence of `seq` rows
   // and head of `head_dim` columns (inputs Q, K, V; output O, all [T, D]).
   attention,
+  // its gradient with respect to Q, K or V (`wrt`): inputs Q, K, V, O, dO
+  attention_grad,
 };
 const char* op_kind_name(OpKind k);
 
@@ -110,6 +112,7 @@ struct OpNode {
   std::int64_t head_dim = 0;  // extension: attention head width
   std::int64_t seq = 0;       // extension: attention rows per sequence
   bool causal = false;        // extension: attention causal mask
+  char wrt = 'q';             // extension: attention-grad output ('q', 'k' or 'v')
 
   bool is_elementwise() const {
     return kind == OpKind::ew_add || kind == OpKind::ew_mul || kind == OpKind::ew_max;

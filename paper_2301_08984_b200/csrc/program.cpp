@@ -519,11 +519,14 @@ struct Builder {
         finish_deps(in);
         break;
       }
-      case OpKind::attention: {
+      case OpKind::attention:
+      case OpKind::attention_grad: {
         // Schema extension (oracle/planc_oracle.py eval_ext): a piece must
         // hold whole sequences and whole heads, and Q, K, V, O the same
         // region — a split inside a sequence or a head is rejected.
-        if (ib.size() != 3 || op.outputs.size() != 1) throw InternalError("attention arity in " + op.id);
+        const bool grad = op.kind == OpKind::attention_grad;
+        if (ib.size() != (grad ? 5u : 3u) || op.outputs.size() != 1)
+          throw InternalError(std::string(op_kind_name(op.kind)) + " arity in " + op.id);
         int ob = out_buffer(op.outputs[0], lane);
         const auto sh = shape_of(ob);
         for (int b : ib)
@@ -538,17 +541,46 @@ struct Builder {
         if (ro[0].lo % op.seq != 0 || sh[0] % op.seq != 0 || ro[1].lo % op.head_dim != 0 || sh[1] % op.head_dim != 0)
           throw UsageError("attention " + op.id + ": the piece does not hold whole sequences of " +
                            std::to_string(op.seq) + " rows and whole heads of " + std::to_string(op.head_dim));
+        const int wi = op.wrt == 'q' ? 0 : op.wrt == 'k' ? 1 : 2;
+        if (grad) {
+          // Join an earlier attention-grad instruction of this lane on the
+          // same operands (dQ, dK, dV share the statistics pass and the
+          // recomputed scores).
+          for (auto it = P.instrs.rbegin(); it != P.instrs.rend(); ++it) {
+            Instr& g = *it;
+            if (g.kind != InstrKind::attention || g.att_grad == 0 || g.lane != lane || g.in_bufs != ib ||
+                g.att_seq != op.seq || g.att_dh != op.head_dim || g.causal != op.causal || g.att_out[wi] >= 0)
+              continue;
+            g.att_out[wi] = ob;
+            g.att_grad |= 1 << wi;
+            g.out_bufs.push_back(ob);
+            g.label += "+" + op.id;
+            P.buffers[ob].producer = g.id;
+            g.flops += 4.0 * static_cast<double>(sh[0]) * static_cast<double>(op.seq) *
+                       static_cast<double>(sh[1]) * (op.causal ? 0.5 : 1.0);
+            g.bytes += static_cast<double>(sh[0] * sh[1]) * dtype_size(P.buffers[ob].dtype);
+            ob = -1;
+            break;
+          }
+          if (ob < 0) break;  // joined
+        }
         Instr& in = emit(InstrKind::attention, lane, 0, op_idx, op.id);
         in.in_bufs = ib;
         in.out_bufs = {ob};
+        if (grad) {
+          in.att_grad = 1 << wi;
+          in.att_out[wi] = ob;
+        }
         in.att_rows = sh[0];
         in.att_cols = sh[1];
         in.att_seq = op.seq;
         in.att_dh = op.head_dim;
         in.causal = op.causal;
         const std::int64_t es = dtype_size(P.buffers[ob].dtype);
-        in.bytes = static_cast<double>(sh[0] * sh[1]) * es * 4;
-        // QK^T and PV per (sequence, head): 4 * seq^2 * dh (half with a causal mask)
+        in.bytes = static_cast<double>(sh[0] * sh[1]) * es * (grad ? 6 : 4);
+        // forward: QK^T and PV per (sequence, head): 4 * seq^2 * dh (half with a
+        // causal mask); each gradient adds two such products (the algorithmic
+        // dQ, dK, dV work; the executor recomputes scores on top)
         in.flops = 4.0 * static_cast<double>(sh[0]) * static_cast<double>(op.seq) * static_cast<double>(sh[1]) *
                    (op.causal ? 0.5 : 1.0);
         finish_deps(in);
@@ -1631,7 +1663,8 @@ std::string Program::describe_json() const {
        << ",\"allreduce\":" << (in.allreduce ? "true" : "false") << ",\"group\":" << in.group
        << ",\"scatter\":" << in.scatter << ",\"scatter_rows\":" << in.scatter_rows << ",\"att\":{\"rows\":"
        << in.att_rows << ",\"cols\":" << in.att_cols << ",\"seq\":" << in.att_seq << ",\"head_dim\":" << in.att_dh
-       << ",\"causal\":" << (in.causal ? "true" : "false") << "},\"gather\":[";
+       << ",\"causal\":" << (in.causal ? "true" : "false") << ",\"grad\":" << in.att_grad << ",\"grad_out\":["
+       << in.att_out[0] << "," << in.att_out[1] << "," << in.att_out[2] << "]},\"gather\":[";
     for (int j = 0; j < 2; ++j) {
       os << (j ? "," : "") << "{\"rows\":" << in.gather_rows[j] << ",\"pieces\":[";
       for (std::size_t q = 0; q < in.gather[j].size(); ++q) os << (q ? "," : "") << in.gather[j][q];

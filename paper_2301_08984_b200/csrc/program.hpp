@@ -128,9 +128,15 @@ struct Instr {
   std::int64_t seg = 0;
   double eps = 0;
   // attention: in_bufs = Q, K, V, out_bufs = O, each a [rows, cols] piece of
-  // whole sequences (att_seq rows) and whole heads (att_dh columns)
+  // whole sequences (att_seq rows) and whole heads (att_dh columns).
+  // attention gradient (att_grad != 0): in_bufs = Q, K, V, O, dO; att_out[0..2]
+  // = the dQ / dK / dV buffers it writes (-1: not requested) — the
+  // attention-grad ops of one lane with the same operands share one
+  // instruction (one statistics pass); out_bufs lists the written ones.
   std::int64_t att_rows = 0, att_cols = 0, att_seq = 0, att_dh = 0;
   bool causal = false;
+  int att_grad = 0;
+  int att_out[3] = {-1, -1, -1};
   // box
   std::vector<Cell> cells;
   int coll_group = -1;  // collective group a box instruction belongs to

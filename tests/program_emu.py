@@ -94,8 +94,13 @@ def exec_instr(ins: dict, data: dict, shape: dict):
         from oracle import planc_oracle as po
 
         a = ins["att"]
-        q, kk, v = (data[b].reshape(a["rows"], a["cols"]) for b in ins["in"])
-        data[ins["out"][0]] = po.attention(q, kk, v, a["head_dim"], a["seq"], a["causal"]).reshape(-1)
+        ops = [data[b].reshape(a["rows"], a["cols"]) for b in ins["in"]]
+        if not a.get("grad"):
+            data[ins["out"][0]] = po.attention(*ops, a["head_dim"], a["seq"], a["causal"]).reshape(-1)
+        else:  # attention gradient: dQ / dK / dV into grad_out[0..2]
+            for w, ob in zip("qkv", a["grad_out"]):
+                if ob >= 0:
+                    data[ob] = po.attention_grad(*ops, a["head_dim"], a["seq"], a["causal"], w).reshape(-1)
     elif k == "box":
         ob = ins["out"][0]
         out = data[ob].copy()  # a box writes only its cells (two-phase all-reduce: two boxes per output)
