@@ -337,6 +337,22 @@ def attention_doc(tokens: int, heads: int, head_dim: int, seq: int, causal: bool
     return {"ptensors": pts, "ops": ops}
 
 
+def attention_train_doc(tokens: int, heads: int, head_dim: int, seq: int, causal: bool = True,
+                        elem_size: int = 2) -> dict:
+    """O = attention(Q, K, V) and its three gradients dQ, dK, dV from dO
+    (attention-grad with wrt = q / k / v, each the backward of the forward
+    op): the executor merges the three per lane into one instruction."""
+    T, D = tokens, heads * head_dim
+    pts = [_pt(i, (T, D), "activation", elem_size) for i in range(4)] + [_pt(4, (T, D), "gradient", elem_size, 3)]
+    pts += [_pt(5 + i, (T, D), "gradient", elem_size, i) for i in range(3)]
+    A = {"batch_dim": 0, "head_dim": head_dim, "seq": seq, "causal": causal}
+    fl = 4.0 * T * seq * D * (0.5 if causal else 1.0)
+    ops = [_op("tpattn", "attention", [0, 1, 2], [3], "forward", fl, A)]
+    for i, w in enumerate("qkv"):
+        ops.append(_op("tpg" + w, "attention-grad", [0, 1, 2, 3, 4], [5 + i], "backward", fl, dict(A, wrt=w), "tpattn"))
+    return {"ptensors": pts, "ops": ops}
+
+
 # ---- C4 / C5 benchmark documents (SURVEY §8d) ------------------------------------
 
 

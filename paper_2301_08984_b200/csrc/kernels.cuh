@@ -188,6 +188,13 @@ const char* attention_unsupported(std::int64_t rows, std::int64_t cols, std::int
                                   int dtype);
 void launch_attention(const void* q, const void* k, const void* v, void* o, std::int64_t rows, std::int64_t cols,
                       std::int64_t seq, std::int64_t head_dim, bool causal, int dtype, cudaStream_t s);
+// Its gradient: a statistics pass (per-row log-sum-exp of the scores and
+// D = rowsum(dO ∘ O) into `scratch`), then dQ (query-block CTAs) and dK / dV
+// (key-block CTAs) — any of dq / dk / dv may be null.
+std::int64_t attention_grad_scratch_bytes(std::int64_t rows, std::int64_t cols, std::int64_t head_dim);
+void launch_attention_grad(const void* q, const void* k, const void* v, const void* o, const void* dout, void* dq,
+                           void* dk, void* dv, void* scratch, std::int64_t rows, std::int64_t cols, std::int64_t seq,
+                           std::int64_t head_dim, bool causal, int dtype, cudaStream_t s);
 void launch_fill_zero_f32(float* p, std::int64_t count, cudaStream_t s);
 // Device-to-device copy on the SMs (16-byte vectors): keeps the copy engines
 // free for the host-link transfers running beside it (end-to-end mode).

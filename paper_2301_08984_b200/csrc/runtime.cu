@@ -346,6 +346,11 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       DeviceGuard dg(lanes_[in.lane].gpu);
       ck(cudaMalloc(&irt_[in.id].scratch, emb_grad_scratch_bytes(in.n_idx, in.h)), "cudaMalloc(scratch)");
     }
+    if (in.kind == InstrKind::attention && in.att_grad) {
+      DeviceGuard dg(lanes_[in.lane].gpu);
+      ck(cudaMalloc(&irt_[in.id].scratch, attention_grad_scratch_bytes(in.att_rows, in.att_cols, in.att_dh)),
+         "cudaMalloc(attention statistics)");
+    }
     if (in.kind == InstrKind::reduce) {
       const std::int64_t b =
           reduce_scratch_bytes(in.outer, in.axis_len, in.inner, dt_of(prog_.buffers[in.out_bufs[0]].dtype));
@@ -386,6 +391,9 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
         if (batch_of_.empty() || batch_of_[in.id] < 0) kernels_per_step_ += static_cast<int>(irt_[in.id].box.size());
         break;
       case InstrKind::emb_grad: kernels_per_step_ += in.n_idx > 0 ? 2 : 1; break;
+      case InstrKind::attention:
+        kernels_per_step_ += in.att_grad ? 1 + (in.att_out[0] >= 0 ? 1 : 0) + (in.att_out[1] >= 0 || in.att_out[2] >= 0 ? 1 : 0) : 1;
+        break;
       case InstrKind::reduce:
         kernels_per_step_ += reduce_launches(in.outer, in.axis_len, in.inner, dt_of(prog_.buffers[in.out_bufs[0]].dtype));
         break;
@@ -1175,6 +1183,14 @@ void Executor::launch_instr(const Instr& in, cudaStream_t s) {
                       in.lo, s);
       return;
     case InstrKind::attention:
+      if (in.att_grad) {
+        auto out = [&](int w) { return in.att_out[w] >= 0 ? buf_ptr(in.att_out[w]) : nullptr; };
+        launch_attention_grad(buf_ptr(in.in_bufs[0]), buf_ptr(in.in_bufs[1]), buf_ptr(in.in_bufs[2]),
+                              buf_ptr(in.in_bufs[3]), buf_ptr(in.in_bufs[4]), out(0), out(1), out(2),
+                              irt_[in.id].scratch, in.att_rows, in.att_cols, in.att_seq, in.att_dh, in.causal,
+                              dt_of(prog_.buffers[in.out_bufs[0]].dtype), s);
+        return;
+      }
       launch_attention(buf_ptr(in.in_bufs[0]), buf_ptr(in.in_bufs[1]), buf_ptr(in.in_bufs[2]), buf_ptr(in.out_bufs[0]),
                        in.att_rows, in.att_cols, in.att_seq, in.att_dh, in.causal,
                        dt_of(prog_.buffers[in.out_bufs[0]].dtype), s);
@@ -1566,7 +1582,7 @@ std::vector<KernelStat> Executor::profile() {
       }
       case InstrKind::ew: kind = "ew"; break;
       case InstrKind::rowwise: kind = "rowwise"; break;
-      case InstrKind::attention: kind = "attention"; break;
+      case InstrKind::attention: kind = in.att_grad ? "attention_grad" : "attention"; break;
       case InstrKind::reduce: kind = "reduce"; break;
       case InstrKind::emb_lookup:
       case InstrKind::emb_grad: kind = "embedding"; break;

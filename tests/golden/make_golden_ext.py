@@ -59,6 +59,9 @@ def cases():
     for name, (T, nh, hd, seq, causal), spec, seed, tol in ATTN_CASES:
         yield name, docs.attention_doc(T, nh, hd, seq, causal), spec, seed, tol, 2, \
             dict(tokens=T, heads=nh, head_dim=hd, seq=seq, causal=causal, elem_size=2)
+    # fused attention forward + backward (dQ, dK, dV merged per lane), heads split over 2 lanes
+    yield "attn_train_tp2_bf16", docs.attention_train_doc(512, 2, 128, 256, True), \
+        dict(strategy="megatron_tp", devices=2), 95, 2e-2, 2, dict(tokens=512, heads=2, head_dim=128, seq=256, elem_size=2)
     # C2a: the transformer block forward with fused causal attention, Megatron TP 2
     yield "attn_block_fwd_tp2_mma", docs.gpt_block_attn_doc(512, 256, 128, 256), \
         dict(strategy="megatron_tp", devices=2), 94, 2e-2, 2, dict(tokens=512, hidden=256, head_dim=128, seq=256, elem_size=2)

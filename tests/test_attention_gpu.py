@@ -68,3 +68,27 @@ def test_attention_unsupported_shapes(T, D, dh, seq, elem, why):
     plan, _ = attention_plan(T, D, dh, seq, False, elem)
     with pytest.raises(pb.PlancError, match=why):
         pb.Executor(plan, lane_gpus=[0])
+
+
+@pytest.mark.parametrize("T,heads,dh,seq,causal", [(256, 2, 128, 256, False), (512, 2, 64, 256, True),
+                                                   (1024, 2, 128, 512, True), (768, 1, 128, 384, False)])
+@pytest.mark.parametrize("wrt", ["q", "k", "v"])
+def test_attention_grad_vs_fp64(T, heads, dh, seq, causal, wrt):
+    """attention-grad (statistics pass, then the dQ or dK / dV kernel) against
+    the float64 gradient (pinned against torch autograd in
+    tests/test_ext_oracle.py) — normwise <= 2e-2 (bf16 P and dS operands)."""
+    rng = np.random.default_rng(T + heads + dh + ord(wrt))
+    D = heads * dh
+    q, k, v, do = (bf16_round(rng.standard_normal((T, D))) for _ in range(4))
+    o = bf16_round(planc_oracle.attention(q, k, v, dh, seq, causal))
+    plan, out_pt = single_op_plan("attention-grad", [(T, D)] * 5, (T, D), 2, 2,
+                                  {"head_dim": dh, "seq": seq, "causal": causal, "wrt": wrt})
+    with pb.Executor(plan, lane_gpus=[0]) as ex:
+        ex.set_inputs({0: q, 1: k, 2: v, 3: o, 4: do})
+        ex.run(2)
+        out = ex.get_output(out_pt)
+        prof = ex.profile()
+    ref = planc_oracle.attention_grad(q, k, v, o, do, dh, seq, causal, wrt)
+    err = np.abs(out - ref).max() / np.abs(ref).max()
+    assert err <= 2e-2, err
+    assert any(p["kind"] == "attention_grad" for p in prof)

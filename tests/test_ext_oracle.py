@@ -56,3 +56,26 @@ def test_segment_alignment_is_enforced():
         po.eval_ext("softmax", [np.zeros((2, 6))], 4)
     with pytest.raises(po.UsageError):
         po.eval_ext("softmax", [np.zeros((2, 8))], 4, in_masks=[{"region": [[0, 2], [2, 10]]}])
+
+
+def test_attention_oracle_vs_torch():
+    """The float64 attention restatement and its gradients against torch's
+    scaled_dot_product_attention and autograd (causal and not)."""
+    import numpy as np
+    import torch
+
+    from oracle import planc_oracle as po
+
+    rng = np.random.default_rng(0)
+    T, nh, dh, seq = 256, 2, 32, 128
+    q, k, v, do = (rng.standard_normal((T, nh * dh)) for _ in range(4))
+    sh = lambda x: x.reshape(T // seq, seq, nh, dh).transpose(0, 2, 1, 3)  # noqa: E731
+    for causal in (False, True):
+        o = po.attention(q, k, v, dh, seq, causal)
+        tq, tk, tv = (torch.tensor(sh(x), requires_grad=True) for x in (q, k, v))
+        out = torch.nn.functional.scaled_dot_product_attention(tq, tk, tv, is_causal=causal)
+        assert np.abs(out.detach().numpy().transpose(0, 2, 1, 3).reshape(T, -1) - o).max() < 1e-12
+        out.backward(torch.tensor(sh(do)))
+        for w, t in (("q", tq), ("k", tk), ("v", tv)):
+            g = po.attention_grad(q, k, v, o, do, dh, seq, causal, w)
+            assert np.abs(g - t.grad.numpy().transpose(0, 2, 1, 3).reshape(T, -1)).max() < 1e-12, (causal, w)
