@@ -48,7 +48,8 @@ def plan_name(config: str, n: int) -> str:
     x DAP (c5: 4 stages x dap 2) plans have 8 lanes — with fewer GPUs, lanes
     share GPUs (round robin)."""
     return {"c2": f"c2_tp{n}", "c2x": f"c2x_tp{n}", "c1l": f"c1l_dp{n}", "c3": "c3_pp4dp2_l24", "c4": "c4_coshard4_dp8",
-            "c5": "c5_3f1b_dap", "c2sp": f"c2sp_tp{max(n, 2)}", "c2a": f"c2a_tp{n}"}[config]
+            "c5": "c5_3f1b_dap", "c2sp": f"c2sp_tp{max(n, 2)}", "c2a": f"c2a_tp{n}",
+            "c2at": f"c2at_tp{n}"}[config]
 
 
 def nvlink_peer_bandwidth(nbytes: int = 512 << 20, reps: int = 5):
@@ -96,7 +97,7 @@ def cpu_plan_name(config: str) -> str:
         return "c3_pp4dp2_cpu"
     if config == "c2sp":
         return "c2_tp1_cpu"  # the same graph (sequence parallelism only renames the residual ops' split)
-    return plan_name(config, 1) + "_cpu" + ("_standin" if config in ("c2x", "c2a") else "")
+    return plan_name(config, 1) + "_cpu" + ("_standin" if config in ("c2x", "c2a", "c2at") else "")
 
 
 def load_plan(name):
@@ -246,7 +247,7 @@ def cpu_baseline(config: str, budget_s: float = 20.0):
 
     name = cpu_plan_name(config)
     note = ""
-    if config in ("c2x", "c2a"):
+    if config in ("c2x", "c2a", "c2at"):
         # The reference executor has no layernorm / softmax / GELU / attention:
         # it runs the stand-in plan (identity / mul / add in their place, same data flow).
         note = "; stand-in plan: identity/mul/add where the extension has LN/softmax/GELU/attention"
@@ -354,7 +355,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c2", "c2x", "c1l", "c3", "c4", "c5", "c2sp", "c2a"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c2x", "c1l", "c3", "c4", "c5", "c2sp", "c2a", "c2at"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sustain-s", type=float, default=3.0, help="seconds of the sustained timed region")
@@ -563,6 +564,7 @@ def main():
                                                                   "micro_batches") if k in meta},
                        "parallelism": {"c2": f"tp{n}", "c2x": f"tp{n}", "c1l": f"dp{n}", "c3": "pp4 x dp2 (1F1B, K=8)",
                                        "c2sp": f"tp{max(n, 2)} + sequence parallel", "c2a": f"tp{n} (forward)",
+                                       "c2at": f"tp{n}",
                                        "c4": "dp8 x co-shard 4 (FFN)",
                                        "c5": "3F1B pp4 x dap2 (K=4)"}[args.config],
                        "lanes_per_gpu": nlanes / max(n, 1),

@@ -325,6 +325,70 @@ def gpt_block_attn_doc(tokens: int, hidden: int, head_dim: int, seq: int, elem_s
     return {"ptensors": pts, "ops": ops}
 
 
+def gpt_block_attn_train_doc(tokens: int, hidden: int, head_dim: int, seq: int, elem_size: int = 2) -> dict:
+    """The C2a block (LayerNorm, Q/K/V projections, fused causal attention,
+    Wo, GELU MLP) as a train step (config C2at): forward, the backward with
+    attention-grad (dQ, dK, dV) and the other extended gradients, and one
+    optimizer add per weight. Megatron TP: Q/K/V/W1 column-parallel (split
+    with the heads), Wo/W2 row-parallel, LayerNorms replicated."""
+    T, H, Fd = tokens, hidden, 4 * hidden
+    e = elem_size
+    doc = gpt_block_attn_doc(tokens, hidden, head_dim, seq, elem_size)
+    pts, ops = doc["ptensors"], doc["ops"]
+    ids = dict(X=0, Wq=1, Wk=2, Wv=3, Wo=4, W1=5, W2=6, N1=10, Q=11, K=12, V=13, A=14, O=15, X2=16, N2=17, F1=18,
+               Fa=19, Y=20, OUT=21)
+    names = ["OUT", "Y", "Fa", "F1", "N2", "X2a", "X2", "O", "A", "Q", "K", "V", "N1q", "N1k", "N1v", "N1", "X1", "X"]
+    g = {n: 100 + i for i, n in enumerate(names)}
+    of = dict(OUT="OUT", Y="Y", Fa="Fa", F1="F1", N2="N2", X2a="X2", X2="X2", O="O", A="A", Q="Q", K="K", V="V",
+              N1q="N1", N1k="N1", N1v="N1", N1="N1", X1="X", X="X")
+    for n, src in of.items():
+        shp = next(q["shape"] for q in pts if q["id"] == ids[src])
+        pts.append(_pt(g[n], shp, "gradient", e, ids[src]))
+    W = {"Wq": (H, H), "Wk": (H, H), "Wv": (H, H), "Wo": (H, H), "W1": (H, Fd), "W2": (Fd, H)}
+    gw = {w: 130 + i for i, w in enumerate(W)}
+    nw = {w: 140 + i for i, w in enumerate(W)}
+    for w, shp in W.items():
+        pts.append(_pt(gw[w], shp, "gradient", e, ids[w]))
+        pts.append(_pt(nw[w], shp, "weight", e))
+    B = {"layer": 0}
+    TA = dict(B, transpose_a=True)
+    TB = dict(B, transpose_b=True)
+    AT = dict(B, head_dim=head_dim, seq=seq, causal=True)
+    mm = lambda m, n, k: 2.0 * m * n * k  # noqa: E731
+    fa = 2.0 * T * seq * H
+    ops += [
+        _op("gres2", "identity", [g["OUT"]], [g["Y"]], "backward", 0, B, "res2"),
+        _op("gw2a", "matmul", [g["Y"], ids["W2"]], [g["Fa"]], "backward", mm(T, Fd, H), TB, "roww2"),
+        _op("gw2w", "matmul", [ids["Fa"], g["Y"]], [gw["W2"]], "backward", mm(Fd, H, T), TA, "roww2"),
+        _op("ggelu", "gelu-grad", [ids["F1"], g["Fa"]], [g["F1"]], "backward", 8 * T * Fd, B, "tpgelu"),
+        _op("gf1a", "matmul", [g["F1"], ids["W1"]], [g["N2"]], "backward", mm(T, H, Fd), TB, "colf1"),
+        _op("gf1w", "matmul", [ids["N2"], g["F1"]], [gw["W1"]], "backward", mm(H, Fd, T), TA, "colf1"),
+        _op("gln2", "layernorm-grad", [ids["X2"], g["N2"]], [g["X2a"]], "backward", 8 * T * H, B, "ln2"),
+        _op("gres2x", "add", [g["X2a"], g["OUT"]], [g["X2"]], "backward", T * H, B, "res2"),
+        _op("gres1", "identity", [g["X2"]], [g["O"]], "backward", 0, B, "res1"),
+        _op("gwoa", "matmul", [g["O"], ids["Wo"]], [g["A"]], "backward", mm(T, H, H), TB, "rowo"),
+        _op("gwow", "matmul", [ids["A"], g["O"]], [gw["Wo"]], "backward", mm(H, H, T), TA, "rowo"),
+    ]
+    for w in "qkv":
+        ops.append(_op("gattn" + w, "attention-grad", [ids["Q"], ids["K"], ids["V"], ids["A"], g["A"]],
+                       [g[w.upper()]], "backward", fa, dict(AT, wrt=w), "tpattn"))
+    for w, n in (("q", "N1q"), ("k", "N1k"), ("v", "N1v")):
+        W_ = "W" + w
+        ops.append(_op("g" + w + "a", "matmul", [g[w.upper()], ids[W_]], [g[n]], "backward", mm(T, H, H), TB,
+                       "col" + w))
+        ops.append(_op("g" + w + "w", "matmul", [ids["N1"], g[w.upper()]], [gw[W_]], "backward", mm(H, H, T), TA,
+                       "col" + w))
+    ops += [
+        _op("gln1s", "add", [g["N1q"], g["N1k"], g["N1v"]], [g["N1"]], "backward", 2 * T * H, B, "ln1"),
+        _op("gln1", "layernorm-grad", [ids["X"], g["N1"]], [g["X1"]], "backward", 8 * T * H, B, "ln1"),
+        _op("gres1x", "add", [g["X1"], g["X2"]], [g["X"]], "backward", T * H, B, "res1"),
+    ]
+    for w, kind in (("Wq", "optc"), ("Wk", "optc"), ("Wv", "optc"), ("W1", "optc"), ("Wo", "optr"), ("W2", "optr")):
+        shp = W[w]
+        ops.append(_op(kind + w.lower(), "add", [ids[w], gw[w]], [nw[w]], "optimizer", shp[0] * shp[1], B))
+    return {"ptensors": pts, "ops": ops}
+
+
 def attention_doc(tokens: int, heads: int, head_dim: int, seq: int, causal: bool = False, elem_size: int = 2,
                   prefix: str = "tp") -> dict:
     """One fused attention op O = attention(Q, K, V) over [tokens, heads x

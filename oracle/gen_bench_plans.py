@@ -161,6 +161,24 @@ def gen_c2a():
                 write(f"c2a_tp{k}{tag}_standin", stand, plan, dict(meta, tp=k, standin=True))
 
 
+def gen_c2at():
+    """C2at: the C2a block as a train step (fused attention forward and
+    attention-grad, LN / GELU gradients, optimizer), Megatron TP 1/2/4/8, and
+    its reduced-shape stand-in twin for the reference CPU executor."""
+    for T, H, hd, seq, tag in ((8192, 2048, 128, 2048, ""), (256, 128, 128, 128, "_cpu")):
+        doc = docs.gpt_block_attn_train_doc(T, H, hd, seq)
+        stand = docs.dumps(docs.standin_doc(doc))
+        meta = dict(config="c2at", tokens=T, hidden=H, head=hd, seq=seq, dtype="bf16", samples_per_step=T,
+                    sample="token (row of X)", extension=True, note="train step with fused attention and its gradient")
+        for k in (1, 2, 4, 8):
+            if tag and k > 1:
+                continue
+            plan = refpy.compile_plan(stand, strategy="megatron_tp", devices=k)
+            write(f"c2at_tp{k}{tag}", docs.dumps(doc), docs.rewrite_plan(plan, doc), dict(meta, tp=k))
+            if tag:
+                write(f"c2at_tp{k}{tag}_standin", stand, plan, dict(meta, tp=k, standin=True))
+
+
 def gen_c2sp():
     g = docs.dumps(docs.gpt_block_doc(8192, 2048, elem_size=2, train=True, seq_parallel=True))
     for k in (2, 4, 8):
@@ -174,7 +192,7 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     only = set(sys.argv[1:])
     if only:
-        for name, fn in (("c2x", gen_c2x), ("c2sp", gen_c2sp), ("c2a", gen_c2a), ("c3l24", gen_c3_l24), ("c4", gen_c4), ("c5", gen_c5)):
+        for name, fn in (("c2x", gen_c2x), ("c2sp", gen_c2sp), ("c2a", gen_c2a), ("c2at", gen_c2at), ("c3l24", gen_c3_l24), ("c4", gen_c4), ("c5", gen_c5)):
             if name in only:
                 fn()
         if "ref1" in only:
@@ -183,6 +201,7 @@ def main():
     gen_c2x()
     gen_c2sp()
     gen_c2a()
+    gen_c2at()
     for T, H, tag in ((8192, 2048, ""), (128, 128, "_cpu")):
         g = docs.dumps(docs.gpt_block_doc(T, H, elem_size=2, train=True))
         for k in (1, 2, 4, 8):

@@ -62,6 +62,9 @@ def cases():
     # fused attention forward + backward (dQ, dK, dV merged per lane), heads split over 2 lanes
     yield "attn_train_tp2_bf16", docs.attention_train_doc(512, 2, 128, 256, True), \
         dict(strategy="megatron_tp", devices=2), 95, 2e-2, 2, dict(tokens=512, heads=2, head_dim=128, seq=256, elem_size=2)
+    # C2at: the block train step with fused attention and attention-grad, Megatron TP 2
+    yield "attn_block_train_tp2_mma", docs.gpt_block_attn_train_doc(256, 256, 128, 128), \
+        dict(strategy="megatron_tp", devices=2), 96, 2e-2, 2, dict(tokens=256, hidden=256, head_dim=128, seq=128, elem_size=2)
     # C2a: the transformer block forward with fused causal attention, Megatron TP 2
     yield "attn_block_fwd_tp2_mma", docs.gpt_block_attn_doc(512, 256, 128, 256), \
         dict(strategy="megatron_tp", devices=2), 94, 2e-2, 2, dict(tokens=512, hidden=256, head_dim=128, seq=256, elem_size=2)
