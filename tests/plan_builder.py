@@ -107,3 +107,30 @@ def embedding_plan(n, vocab, h, lo, rows, elem=2):
     doc = json.loads(single_op_plan("embedding-lookup", [(n,), (vocab, h)], (n, h), [4, elem], elem)[0])
     doc["vtensors"][1]["region"] = [[lo, lo + rows], [0, h]]
     return json.dumps(doc), 2
+
+
+def attention_grad_plan(T, D, head_dim, seq, causal):
+    """dQ, dK, dV = attention-grad(Q, K, V, O, dO) on one lane (three ops the
+    executor merges into one instruction): pTensors 0..4 in, 5, 6, 7 out."""
+    attrs = {"head_dim": head_dim, "seq": seq, "causal": causal, "wrt": "q"}
+    doc = json.loads(single_op_plan("attention-grad", [(T, D)] * 5, (T, D), 2, 2, attrs)[0])
+    full = [[0, T], [0, D]]
+    for i, w in ((1, "k"), (2, "v")):
+        pt = 5 + i
+        doc["ptensors"].append({"id": pt, "shape": [T, D], "elem_size": 2, "kind": "activation"})
+        ins = []
+        for j in range(5):
+            vid = 300 + 10 * i + j
+            doc["vtensors"].append({"id": vid, "ptensor": j, "region": full, "value": [0, 1], "replica": [0, 1],
+                                    "side": "in", "owner": "op" + w})
+            ins.append(vid)
+        oid = 300 + 10 * i + 9
+        doc["vtensors"].append({"id": oid, "ptensor": pt, "region": full, "value": [0, 1], "replica": [0, 1],
+                                "side": "out", "owner": "op" + w})
+        op = {"id": "op" + w, "kind": "attention-grad", "inputs": ins, "outputs": [oid], "direction": "backward",
+              "flops": 0.0, "doc_order": i, "inserted": False}
+        op.update(dict(attrs, wrt=w))
+        doc["ops"].append(op)
+        doc["assignment"]["op" + w] = 0
+        doc["lanes"][0]["tasks"].append({"kind": "compute", "op": "op" + w, "duration": 0.0, "bytes": 0})
+    return json.dumps(doc), (5, 6, 7)
