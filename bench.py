@@ -504,7 +504,7 @@ def main():
                 traffic, traffic_src = tj[top]["mean"], tj["source"]
         except Exception:
             pass
-        if top.startswith("gemm") or top == "attention":
+        if top.startswith("gemm") or top.startswith("attention"):
             achieved = t["flops"] / (t["ms"] / 1e3) / 1e12
             # fused elementwise epilogues add their operand / result bytes at
             # HBM speed to the tensor-bound time (0 without fusion)
@@ -534,7 +534,7 @@ def main():
         F, M, W = [0.0] * n, [0.0] * n, [0.0] * n
         for ins in desc["instrs"]:
             gidx = gpu_of[ins["lane"]]
-            if ins["kind"] in ("gemm", "attention"):  # tensor-core work (attention: QK^T and PV)
+            if ins["kind"] in ("gemm", "attention"):  # tensor-core work (attention: QK^T and PV, and its gradient)
                 F[gidx] += ins["flops"]
                 if ins["kind"] == "attention":
                     M[gidx] += ins["bytes"]
@@ -545,8 +545,8 @@ def main():
         t_roof = max(max(F[i] / (peaks["bf16_sus"] * 1e12) + M[i] / (peaks["hbm"] * 1e9),
                          W[i] / (NVLINK_GBS * 1e9)) for i in range(n))
         families = {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
-                        "tflops" if k.startswith("gemm") or k == "attention" else "gbs":
-                            round((v["flops"] / 1e12 if k.startswith("gemm") or k == "attention" else v["bytes"] / 1e9)
+                        "tflops" if k.startswith(("gemm", "attention")) else "gbs":
+                            round((v["flops"] / 1e12 if k.startswith(("gemm", "attention")) else v["bytes"] / 1e9)
                                   / max(v["ms"] / 1e3, 1e-12), 2)} for k, v in fam.items()}
         # Adapter bus bandwidth: wire bytes (NCCL bus-bandwidth convention) of
         # the cross-GPU adapter launches over their device time.

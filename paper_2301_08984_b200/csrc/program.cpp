@@ -556,7 +556,7 @@ struct Builder {
             g.out_bufs.push_back(ob);
             g.label += "+" + op.id;
             P.buffers[ob].producer = g.id;
-            g.flops += 4.0 * static_cast<double>(sh[0]) * static_cast<double>(op.seq) *
+            g.flops += (wi == 0 ? 1.0 : 0.5) * 4.0 * static_cast<double>(sh[0]) * static_cast<double>(op.seq) *
                        static_cast<double>(sh[1]) * (op.causal ? 0.5 : 1.0);
             g.bytes += static_cast<double>(sh[0] * sh[1]) * dtype_size(P.buffers[ob].dtype);
             ob = -1;
@@ -579,10 +579,11 @@ struct Builder {
         const std::int64_t es = dtype_size(P.buffers[ob].dtype);
         in.bytes = static_cast<double>(sh[0] * sh[1]) * es * (grad ? 6 : 4);
         // forward: QK^T and PV per (sequence, head): 4 * seq^2 * dh (half with a
-        // causal mask); each gradient adds two such products (the algorithmic
-        // dQ, dK, dV work; the executor recomputes scores on top)
-        in.flops = 4.0 * static_cast<double>(sh[0]) * static_cast<double>(op.seq) * static_cast<double>(sh[1]) *
-                   (op.causal ? 0.5 : 1.0);
+        // causal mask). Gradient (algorithmic, no recomputed scores): dP and
+        // dQ for wrt = q (one forward's worth), dK or dV (half each) — 2x the
+        // forward for all three.
+        in.flops = (grad && wi > 0 ? 0.5 : 1.0) * 4.0 * static_cast<double>(sh[0]) * static_cast<double>(op.seq) *
+                   static_cast<double>(sh[1]) * (op.causal ? 0.5 : 1.0);
         finish_deps(in);
         break;
       }

@@ -79,7 +79,21 @@ def main():
             continue
         stand = docs.dumps(docs.standin_doc(doc))
         plan = docs.rewrite_plan(refpy.compile_plan(stand, **spec), doc)
-        inputs = refpy.random_integer_inputs(stand, seed, 1)
+        if name.startswith("attn_block"):
+            # full blocks at tensor-core widths: integer inputs would grow past
+            # bf16's exact range through the GEMM chain (one-ulp rounding
+            # differences become percent-level); standard init instead —
+            # weights N(0, 1/fan_in), activations / incoming gradients N(0, 1)
+            rng = np.random.default_rng(seed)
+            produced = {o for op in doc["ops"] for o in op["outputs"]}
+            inputs = {}
+            for p_ in doc["ptensors"]:
+                if p_["id"] in produced:
+                    continue
+                x = rng.standard_normal(p_["shape"])
+                inputs[p_["id"]] = x / np.sqrt(p_["shape"][0]) if p_["kind"] == "weight" else x
+        else:
+            inputs = refpy.random_integer_inputs(stand, seed, 1)
         got = planc_oracle.run_plan(plan, inputs)
         ok, msg = planc_oracle.compare_outputs(planc_oracle.run_graph(doc, inputs), got, 1e-9)
         if not ok:
