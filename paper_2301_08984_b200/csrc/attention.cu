@@ -492,7 +492,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       constexpr std::uint32_t idesc_q = make_idesc<DH>(false, true);
       const std::uint32_t q = smem_u32(sQ), o = smem_u32(sO), ds = smem_u32(sS);
       mbar_wait(q_full, 0);
-      for (int j = 0; j < nkv; ++j) {
+      // S_j / dP_j are issued as soon as the softmax warps have read the
+      // previous block's scores (registers), i.e. before dQ += dS_{j-1}·K_{j-1}:
+      // the tensor core computes block j while the softmax warps work on j-1.
+      auto scores = [&](int j) {
         const int st = j & 1;
         const std::uint32_t k = smem_u32(sK + st * CF::T_BYTES), v = smem_u32(sV + st * CF::T_BYTES);
         mbar_wait(&k_full[st], (j >> 1) & 1);
@@ -505,7 +508,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int s = 0; s < DH / 16; ++s) tc_mma(tmem + 128, kdesc(o, s), kdesc(v, s), idesc_s, s > 0 ? 1u : 0u);
         tc_commit(s_full);
         tc_commit(&v_empty[st]);  // V_j consumed (dP only)
-        // dQ += dS_j · K_j
+      };
+      auto grad = [&](int j) {  // dQ += dS_j · K_j
+        const int st = j & 1;
+        const std::uint32_t k = smem_u32(sK + st * CF::T_BYTES);
         mbar_wait(ds_full, j & 1);
         tc_fence_after();
 #pragma unroll
@@ -513,7 +519,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           tc_mma(tmem + 256, kdesc(ds, s), mndesc(k, s), idesc_q, (j > 0 || s > 0) ? 1u : 0u);
         tc_commit(ds_empty);
         tc_commit(&k_empty[st]);
+      };
+      scores(0);
+      for (int j = 1; j < nkv; ++j) {
+        scores(j);
+        grad(j - 1);
       }
+      grad(nkv - 1);
       tc_commit(acc_full);
       pdl_trigger();
     }
@@ -666,18 +678,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       constexpr std::uint32_t idesc_g = make_idesc<DH>(false, true);
       const std::uint32_t k = smem_u32(sK), v = smem_u32(sV), p = smem_u32(sP);
       mbar_wait(kv_full, 0);
-      for (int i = i0; i < nq; ++i) {
+      // Sᵀ / dPᵀ of block i+1 are issued once the softmax warps have read
+      // block i's (registers) — before dV / dK of block i.
+      auto scores = [&](int i) {  // Sᵀ = K·Q_iᵀ, dPᵀ = V·dO_iᵀ  (keys x queries)
         const int n = i - i0, st = n & 1;
         const std::uint32_t q = smem_u32(sQ + st * CF::T_BYTES), o = smem_u32(sO + st * CF::T_BYTES);
         mbar_wait(&q_full[st], (n >> 1) & 1);
         mbar_wait(s_empty, (n & 1) ^ 1);
         tc_fence_after();
-        // Sᵀ = K·Q_iᵀ, dPᵀ = V·dO_iᵀ  (keys x queries)
 #pragma unroll
         for (int s = 0; s < DH / 16; ++s) tc_mma(tmem, kdesc(k, s), kdesc(q, s), idesc_s, s > 0 ? 1u : 0u);
 #pragma unroll
         for (int s = 0; s < DH / 16; ++s) tc_mma(tmem + 128, kdesc(v, s), kdesc(o, s), idesc_s, s > 0 ? 1u : 0u);
         tc_commit(s_full);
+      };
+      scores(i0);
+      for (int i = i0; i < nq; ++i) {
+        const int n = i - i0, st = n & 1;
+        const std::uint32_t q = smem_u32(sQ + st * CF::T_BYTES), o = smem_u32(sO + st * CF::T_BYTES);
+        if (i + 1 < nq) scores(i + 1);
         // dV += Pᵀ · dO_i
         mbar_wait(p_full, n & 1);
         tc_fence_after();
