@@ -1093,6 +1093,8 @@ void fuse_gemm_epilogues(Program& P, const ProgramOptions& opt) {
     }
     if (g < 0) continue;
     Instr& G = P.instrs[g];
+    if (((G.m + 127) / 128) * ((G.n + 255) / 256) <= opt.fuse_min_tiles && G.m * G.n * G.k >= (std::int64_t(1) << 34))
+      continue;  // a long single-wave GEMM: its epilogue would be exposed
     // The epilogue prefetches at most two non-GEMM operands per chunk.
     std::size_t slots = e.in_bufs.size() - 1;
     for (const auto& f : G.fused) slots += f.in_bufs.size() - 1;

@@ -183,6 +183,12 @@ struct ProgramOptions {
   // ...GELU / GELU-grad too (opt-in: bit-identical, but measured slower than
   // the separate pass on C2x, profiles/r01/ab_fuse_gelu.jsonl).
   bool fuse_act = false;
+  // ...not into long GEMMs (m·n·k >= 2^34) of at most this many 128x256
+  // output tiles (one wave: every CTA has a single tile, so the fused
+  // epilogue cannot overlap a next tile's MMAs and is exposed; the separate
+  // elementwise pass runs beside other work instead, and the GEMM may take
+  // split-K / stream-K). 0 = fuse regardless.
+  int fuse_min_tiles = 148;
   // All-reduce groups (every member output = the sum of the same k whole
   // member inputs) as two box phases: member j sums slice j of all inputs
   // (reduce-scatter), then copies the other members' reduced slices

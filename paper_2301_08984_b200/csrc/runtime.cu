@@ -167,6 +167,13 @@ ProgramOptions program_options(bool value_split_extension, bool fuse_epilogues) 
   po.fuse_epilogues = fuse_epilogues;
   po.gemm_fusable = &tc_fusable;
   po.gemm_groupable = &tc_groupable;
+  // A/B knob, read once per process (every rank of a run shares its env):
+  // PLANC_B200_FUSE_MIN_TILES=0 fuses single-wave GEMMs too.
+  static const int min_tiles = [] {
+    const char* e = std::getenv("PLANC_B200_FUSE_MIN_TILES");
+    return e ? std::atoi(e) : 148;
+  }();
+  po.fuse_min_tiles = min_tiles;
   return po;
 }
 
