@@ -72,21 +72,9 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x for x <= 0 on the FMA / ALU pipes (Cody-Waite split + degree-4
-// polynomial on [-0.5, 0.5], relative error < 1e-4 — below bf16's 2^-9):
-// half of each row's exponentials take this path so the XU pipe (MUFU ex2),
-// the softmax warps' bound, carries only the other half.
-__device__ __forceinline__ float ex2_fma(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;           // 1.5 * 2^23: round to the nearest integer
-  const float f = x - (t - 12582912.f);     // in [-0.5, 0.5]
-  float p = fmaf(f, 0.0096181291f, 0.0555041087f);
-  p = fmaf(p, f, 0.2402265070f);
-  p = fmaf(p, f, 0.6931471806f);
-  p = fmaf(p, f, 1.0f);
-  const int j = __float_as_int(t) - 0x4B400000;  // the integer part
-  return __int_as_float(__float_as_int(p) + (j << 23));
-}
+// (Splitting the exponentials between MUFU ex2 and an FMA-pipe polynomial —
+// FA4's balance — measured slower here: forward 794 -> 712 TFLOP/s, causal
+// 436 -> 308; the softmax warps are issue / latency bound, not XU bound.)
 
 // STATS (the backward's statistics pass): no V, no P·V — every query row's
 // base-2 log-sum-exp lse2 = m + log2(l) of its scaled scores, and
@@ -317,8 +305,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int h2 = 0; h2 < 4; ++h2) {
           const int e = 8 * cw + 2 * h2;
           const float p0 = (!diag || key0 + e <= r) ? ex2(fmaf(__uint_as_float(v[e]), scale_log2, -m_new)) : 0.f;
-          const float p1 =
-              (!diag || key0 + e + 1 <= r) ? ex2_fma(fmaf(__uint_as_float(v[e + 1]), scale_log2, -m_new)) : 0.f;
+          const float p1 = (!diag || key0 + e + 1 <= r) ? ex2(fmaf(__uint_as_float(v[e + 1]), scale_log2, -m_new)) : 0.f;
           sum += p0 + p1;
           const __nv_bfloat162 pk = __floats2bfloat162_rn(p0, p1);  // one packed convert (FMA pipe, not XU)
           w[h2] = *reinterpret_cast<const std::uint32_t*>(&pk);
@@ -572,7 +559,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int h2 = 0; h2 < 4; ++h2) {
           const int e = 8 * cw + 2 * h2;
           const float p0 = (!diag || key0 + e <= r) ? ex2(fmaf(__uint_as_float(sv[e]), scale_log2, -l2)) : 0.f;
-          const float p1 = (!diag || key0 + e + 1 <= r) ? ex2_fma(fmaf(__uint_as_float(sv[e + 1]), scale_log2, -l2)) : 0.f;
+          const float p1 = (!diag || key0 + e + 1 <= r) ? ex2(fmaf(__uint_as_float(sv[e + 1]), scale_log2, -l2)) : 0.f;
           w[h2] = bf16_pair(p0 * (__uint_as_float(pv[e]) - dd), p1 * (__uint_as_float(pv[e + 1]) - dd));
         }
         *reinterpret_cast<uint4*>(drow + ((cw ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -760,10 +747,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       float pf[64];
 #pragma unroll
       for (int e = 0; e < 64; ++e)
-        pf[e] = (!diag || r <= q0 + e)
-                    ? ((e & 1) ? ex2_fma(fmaf(__uint_as_float(sv[e]), scale_log2, -st[q0 + e]))
-                               : ex2(fmaf(__uint_as_float(sv[e]), scale_log2, -st[q0 + e])))
-                    : 0.f;
+        pf[e] = (!diag || r <= q0 + e) ? ex2(fmaf(__uint_as_float(sv[e]), scale_log2, -st[q0 + e])) : 0.f;
       std::uint8_t* prow = sP + half * 16384 + r * 128;
       mbar_wait(ds_empty, (n & 1) ^ 1);  // the previous block's dSᵀ consumed
 #pragma unroll
