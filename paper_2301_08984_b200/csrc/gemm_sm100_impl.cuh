@@ -963,10 +963,10 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       }
     };
     int g = 0;  // chunk counter of this warp (staging ring position)
-    // One 32x32 chunk: TMEM -> bf16 C, fold with the prefetched operands,
-    // both to swizzled staging, two TMA stores.
-    auto chunk_body = [&](int mb, int nb, int c, std::uint32_t base, int acc, const uint4(&op0)[4],
-                          const uint4(&op1)[4]) {
+    auto chunk = [&](int t, int mb, int nb, int c, std::uint32_t base, int acc, uint4(&cur)[kMaxEpiSlots][4],
+                     uint4(&nxt)[kMaxEpiSlots][4]) {
+      if (c + 1 < c_hi) load(t, c + 1, nxt);
+      else if (t + static_cast<int>(gridDim.x) < work_items) load(t + gridDim.x, c_lo, nxt);
       std::uint32_t r[32];
       tmem_ld32(base + c * 32, r);
       if (c == c_hi - 1) {
@@ -996,8 +996,8 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
           for (int i = 0; i < kMaxEpiIn; ++i) {
             if (i >= epi.ops[0].n_in) break;
             const uint4 w = i == epi.ops[0].gemm_pos ? make_uint4(cw[4 * v], cw[4 * v + 1], cw[4 * v + 2], cw[4 * v + 3])
-                            : (nst > 1 && epi.slot_in[1] == i) ? op1[v]
-                                                               : op0[v];
+                            : (nst > 1 && epi.slot_in[1] == i) ? cur[1][v]
+                                                               : cur[0][v];
             float x[8];
             bf16_unpair(w.x, x[0], x[1]);
             bf16_unpair(w.y, x[2], x[3]);
@@ -1030,13 +1030,6 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       }
       ++g;
     };
-    // Two operand slots: each chunk's operands are loaded one chunk ahead.
-    auto chunk = [&](int t, int mb, int nb, int c, std::uint32_t base, int acc, uint4(&cur)[kMaxEpiSlots][4],
-                     uint4(&nxt)[kMaxEpiSlots][4]) {
-      if (c + 1 < c_hi) load(t, c + 1, nxt);
-      else if (t + static_cast<int>(gridDim.x) < work_items) load(t + gridDim.x, c_lo, nxt);
-      chunk_body(mb, nb, c, base, acc, cur[0], cur[1]);
-    };
     uint4 pa[kMaxEpiSlots][4], pb[kMaxEpiSlots][4];
     if (static_cast<int>(blockIdx.x) < work_items) load(blockIdx.x, c_lo, pa);
     int local = 0;
@@ -1050,23 +1043,6 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
       const std::uint32_t base = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(acc * BN);
-      // The next tile's operand rows of this warp -> L2 now (one bulk
-      // prefetch per lane and slot, no registers or shared memory): its
-      // chunk loads, issued one chunk ahead, then hit L2 instead of HBM
-      // (their latency was the fused launch's top stall).
-      if (t + static_cast<int>(gridDim.x) < work_items) {
-        int pn, mbn, nbn;
-        coords(t + gridDim.x, pn, mbn, nbn);
-        const int grow = mbn * BM + q * 32 + lane;
-        const int gcol = nbn * BN + c_lo * 32;
-        const int bytes = min(c_hi - c_lo, (n - gcol + 31) / 32) * 64;
-        if (grow < m && bytes > 0) {
-          const std::int64_t off = static_cast<std::int64_t>(grow) * n + gcol;
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src0 + off), "r"(bytes) : "memory");
-          if (nst > 1)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src1 + off), "r"(bytes) : "memory");
-        }
-      }
 #pragma unroll 1
       for (int c = c_lo; c < c_hi; c += 2) {
         chunk(t, mb, nb, c, base, acc, pa, pb);
