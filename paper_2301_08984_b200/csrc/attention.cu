@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   using CF = AttnCfg<DH>;
   extern __shared__ std::uint8_t smem_raw[];
   std::uint8_t* smem =
-      reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+      smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer (STS / LDS)
   std::uint8_t* sQ = smem;
   std::uint8_t* sK = sQ + CF::Q_BYTES;                 // [2][K_BYTES]
   std::uint8_t* sV = sK + 2 * CF::K_BYTES;             // [2][V_BYTES]
@@ -415,8 +415,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   using CF = AttnBwdCfg<DH>;
   extern __shared__ std::uint8_t smem_raw[];
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem_raw);
-  std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
-      (reinterpret_cast<std::uintptr_t>(smem_raw) + 2304 + 1023) & ~std::uintptr_t(1023));
+  std::uint8_t* smem = smem_raw + 2304 + ((1024u - ((smem_u32(smem_raw) + 2304u) & 1023u)) & 1023u);
   std::uint8_t* sQ = smem;
   std::uint8_t* sO = sQ + CF::T_BYTES;       // dO
   std::uint8_t* sK = sO + CF::T_BYTES;       // [2]
@@ -602,8 +601,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   using CF = AttnBwdCfg<DH>;
   extern __shared__ std::uint8_t smem_raw[];
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem_raw);
-  std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
-      (reinterpret_cast<std::uintptr_t>(smem_raw) + 2304 + 1023) & ~std::uintptr_t(1023));
+  std::uint8_t* smem = smem_raw + 2304 + ((1024u - ((smem_u32(smem_raw) + 2304u) & 1023u)) & 1023u);
   std::uint8_t* sK = smem;
   std::uint8_t* sV = sK + CF::T_BYTES;
   std::uint8_t* sQ = sV + CF::T_BYTES;       // [2]

@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
   constexpr int B_STAGE_BYTES = CF::B_STAGE_BYTES;
   constexpr int TMEM_COLS = CF::TMEM_COLS;
   std::uint8_t* smem =
-      reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+      smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer (STS / LDS)
   std::uint8_t* sA = smem;
   std::uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
   // Epilogue staging (1024-aligned: the 64B / 128B swizzle atoms of the C map).

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
     gemm_x3_kernel(const __grid_constant__ X3Maps mp, int m, int n, int k, int group_m) {
   extern __shared__ std::uint8_t smem_raw[];
   std::uint8_t* smem =
-      reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+      smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer (STS / LDS)
   // Stage s: [A_hi | A_lo | B_hi | B_lo]
   std::uint8_t* ring = smem;
   std::uint8_t* staging = ring + X3_STAGES * X3_STAGE_BYTES;
