@@ -112,12 +112,15 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   // PLANC_B200_SPLITK=0 disables split-K, =2 takes it whenever it applies.
   const char* spenv = std::getenv("PLANC_B200_SPLITK");
   const int splitmode = spenv ? std::atoi(spenv) : 1;
-  // Like stream-K, split-K trades SM-time for latency: over the whole GPU
-  // when the lane has it to itself, over at most a quarter of the SMs when
-  // co-resident lanes share it (their concurrent work keeps the rest; C5's
-  // 256 x 256 x 8192 weight gradients: 4 CTAs for ~40 us -> 36 CTAs).
-  const bool allow_split = splitmode != 0 && !a.no_workspace && a.epi.n_ops == 0 && a.scatter == 0;
-  const int split_sms = (a.allow_streamk || splitmode == 2) ? sms : std::max(1, sms / 4);
+  // Like stream-K, split-K trades SM-time (and a reduce launch) for
+  // latency: only when the lane has the GPU to itself. With co-resident
+  // lanes (C4 / C5 at N=1: 8 lanes) the reduce launch lengthens every
+  // lane's dependency chain and their concurrent work fills the SMs anyway
+  // (C5 2.57 -> 2.35 ms, C4 5.34 -> 5.26 ms without it;
+  // profiles/r02/ab_knobs_c4_c5.jsonl). =2 forces it.
+  const bool allow_split = splitmode != 0 && !a.no_workspace && a.epi.n_ops == 0 && a.scatter == 0 &&
+                           (a.allow_streamk || splitmode == 2);
+  const int split_sms = sms;
   GemmSchedule best;
   bool have = false;
   for (int bn : {256, 128, 64}) {
