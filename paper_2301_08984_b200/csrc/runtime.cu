@@ -719,7 +719,6 @@ void Executor::check_sync(cudaError_t e, const char* what) const {
 }
 
 void Executor::build_box_tables() {
-  constexpr std::int64_t kChunkUnits = kBoxChunkUnits;
   if (alias_.empty()) alias_.assign(prog_.buffers.size(), -1);
   for (const auto& in : prog_.instrs) {
     if (in.kind != InstrKind::box || exec_lane_[in.id] < 0 || irt_[in.id].aliased) continue;
@@ -738,6 +737,13 @@ void Executor::build_box_tables() {
     for (int g = 0; g < 2; ++g) {
       if (groups[g].empty()) continue;
       std::int64_t width = g ? V : 1;
+      // Chunk size: a block owns up to kBoxChunkUnits vector units; launches
+      // moving a few MB (C5's all-to-all / split pieces) use smaller chunks
+      // so they spread over ~2 waves of blocks instead of a few dozen SMs.
+      std::int64_t total = 0;
+      for (const Cell* c : groups[g]) total += c->elems() / width;
+      const std::int64_t kChunkUnits = std::max<std::int64_t>(
+          256, std::min<std::int64_t>(kBoxChunkUnits, (total / (2 * 148) + 255) / 256 * 256));
       std::vector<DevCell> cells;
       std::vector<DevTerm> terms;
       std::vector<DevChunk> chunks;
