@@ -118,9 +118,13 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   // lane's dependency chain and their concurrent work fills the SMs anyway
   // (C5 2.57 -> 2.35 ms, C4 5.34 -> 5.26 ms without it;
   // profiles/r02/ab_knobs_c4_c5.jsonl). =2 forces it.
+  // PLANC_B200_SPLITK_SHARED=1: co-resident lanes split long-k GEMMs too,
+  // within their share of the SMs (sms / lanes on the GPU).
+  const char* shenv = std::getenv("PLANC_B200_SPLITK_SHARED");
+  const bool shared_split = shenv && shenv[0] == '1' && a.gpu_share > 1;
   const bool allow_split = splitmode != 0 && !a.no_workspace && a.epi.n_ops == 0 && a.scatter == 0 &&
-                           (a.allow_streamk || splitmode == 2);
-  const int split_sms = sms;
+                           (a.allow_streamk || splitmode == 2 || shared_split);
+  const int split_sms = a.allow_streamk ? sms : std::max(2, sms / std::max(a.gpu_share, 1));
   GemmSchedule best;
   bool have = false;
   for (int bn : {256, 128, 64}) {

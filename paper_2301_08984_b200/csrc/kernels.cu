@@ -1081,11 +1081,12 @@ __global__ void __launch_bounds__(kRowWarps * 32) row_reg_kernel(const T* __rest
         for (int e = 0; e < V; ++e) m = fmaxf(m, x[r][e]);
     m = group_max<LPS>(m);
     float sm = 0.f;
+    const float ml = m * 1.4426950408889634f;  // exp(x - m) = 2^(x log2 e - m log2 e)
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        x[r][e] = valid(r) ? exp2f((x[r][e] - m) * 1.4426950408889634f) : 0.f;
+        x[r][e] = valid(r) ? ex2_ftz(fmaf(x[r][e], 1.4426950408889634f, -ml)) : 0.f;
         sm += x[r][e];
       }
     const float inv = __fdividef(1.f, group_sum<LPS>(sm));
@@ -1141,6 +1142,119 @@ __global__ void __launch_bounds__(kRowWarps * 32) row_reg_kernel(const T* __rest
 #pragma unroll
   for (int r = 0; r < R; ++r)
     if (valid(r)) store_vec<T, V>(out + base + (j + r * LPS) * V, x[r]);
+}
+
+// Wide segments (more than one warp's registers hold): one CTA per segment,
+// every thread R vectors of the segment in registers — one global read per
+// operand, exact two-pass statistics, CTA-wide reductions through shared
+// memory in warp order (the same bits every run).
+template <bool MAX>
+__device__ __forceinline__ float cta_reduce(float v, float* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = MAX ? fmaxf(v, w) : v + w;
+  }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  __syncthreads();  // the previous reduction's readers are done with sh
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  float r = MAX ? -INFINITY : 0.f;
+  for (int w = 0; w < nw; ++w) r = MAX ? fmaxf(r, sh[w]) : r + sh[w];
+  return r;
+}
+
+template <typename T, int OP, int V, int R>
+__global__ void __launch_bounds__(512) row_cta_kernel(const T* __restrict__ a, const T* __restrict__ b,
+                                                       T* __restrict__ out, int seg, float eps) {
+  pdl_wait();  // launch.cuh: inputs of the previous kernel visible
+  pdl_trigger();
+  __shared__ float sh[32];
+  const int nv = seg / V;
+  const long long base = static_cast<long long>(blockIdx.x) * seg;
+  float x[R][V], g[R][V];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int vi = threadIdx.x + r * blockDim.x;
+#pragma unroll
+    for (int e = 0; e < V; ++e) x[r][e] = g[r][e] = 0.f;
+    if (vi < nv) {
+      load_vec<T, V>(a + base + vi * V, x[r]);
+      if constexpr (OP == 1 || OP == 3) load_vec<T, V>(b + base + vi * V, g[r]);
+    }
+  }
+  auto valid = [&](int r) { return static_cast<int>(threadIdx.x + r * blockDim.x) < nv; };
+  const float inv_n = __fdividef(1.f, static_cast<float>(seg));
+  if constexpr (OP == 0) {  // softmax
+    float m = -INFINITY;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (valid(r))
+#pragma unroll
+        for (int e = 0; e < V; ++e) m = fmaxf(m, x[r][e]);
+    m = cta_reduce<true>(m, sh);
+    float sm = 0.f;
+    const float ml = m * 1.4426950408889634f;  // exp(x - m) = 2^(x log2 e - m log2 e)
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        x[r][e] = valid(r) ? ex2_ftz(fmaf(x[r][e], 1.4426950408889634f, -ml)) : 0.f;
+        sm += x[r][e];
+      }
+    const float inv = __fdividef(1.f, cta_reduce<false>(sm, sh));
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) x[r][e] *= inv;
+  } else if constexpr (OP == 1) {  // softmax-grad
+    float dot = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) dot += x[r][e] * g[r][e];
+    dot = cta_reduce<false>(dot, sh);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) x[r][e] = x[r][e] * (g[r][e] - dot);
+  } else {  // layernorm / layernorm-grad
+    float sx = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) sx += x[r][e];
+    const float mean = cta_reduce<false>(sx, sh) * inv_n;
+    float sq = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (valid(r))
+#pragma unroll
+        for (int e = 0; e < V; ++e) sq += (x[r][e] - mean) * (x[r][e] - mean);
+    const float rstd = rsqrtf(cta_reduce<false>(sq, sh) * inv_n + eps);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) x[r][e] = (x[r][e] - mean) * rstd;
+    if constexpr (OP == 3) {
+      float sdy = 0.f, sdx = 0.f;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          sdy += g[r][e];
+          sdx += g[r][e] * x[r][e];
+        }
+      const float mdy = cta_reduce<false>(sdy, sh) * inv_n, mdx = cta_reduce<false>(sdx, sh) * inv_n;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int e = 0; e < V; ++e) x[r][e] = rstd * (g[r][e] - mdy - x[r][e] * mdx);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (valid(r)) store_vec<T, V>(out + base + (threadIdx.x + r * blockDim.x) * V, x[r]);
 }
 
 template <typename T, int OP, int V>
@@ -1224,6 +1338,25 @@ void rowwise_typed(int op, const void* a, const void* b, void* out, std::int64_t
 #undef PLANC_RR_L
 #undef PLANC_RR_R
 #undef PLANC_RR
+    }
+  }
+  // CTA-per-segment path: up to 512 threads x R vectors (R = 8 only for the
+  // one-operand kinds: two operands of 8 vectors would spill).
+  if (vec && nseg <= 0x7fffffffLL) {
+    const long long nv = seg / VV;
+    const int R = nv <= 4 * 512 ? 4 : (nv <= 8 * 512 && (op == 0 || op == 2)) ? 8 : 0;
+    if (R) {
+      const long long th = std::max<long long>(64, ((nv + R - 1) / R + 31) / 32 * 32);
+      const dim3 gc(static_cast<unsigned>(nseg)), bc(static_cast<unsigned>(th));
+#define PLANC_RC(OPV, RR) \
+  return pdl_launch("row_cta_kernel", row_cta_kernel<T, OPV, VV, RR>, gc, bc, 0, s, A, B, O, sg, eps)
+      switch (op) {
+        case 0: if (R == 4) PLANC_RC(0, 4); else PLANC_RC(0, 8);
+        case 1: PLANC_RC(1, 4);
+        case 2: if (R == 4) PLANC_RC(2, 4); else PLANC_RC(2, 8);
+        default: PLANC_RC(3, 4);
+      }
+#undef PLANC_RC
     }
   }
 #define PLANC_ROW(OPV, V) pdl_launch("row_kernel", row_kernel<T, OPV, V>, g, blk, 0, s, A, B, O, nseg, sg, eps)

@@ -108,6 +108,7 @@ struct GemmArgs {
   // path: worth it when the GPU has nothing else to run (one lane per GPU),
   // not when co-resident lanes fill the idle SMs with their own work.
   bool allow_streamk = true;
+  int gpu_share = 1;  // lanes co-resident on this GPU (their launches run concurrently)
   // No workspace at all: the schedule is chosen among data-parallel
   // variants only (no stream-K, no split-K).
   bool no_workspace = false;

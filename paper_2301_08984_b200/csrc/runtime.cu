@@ -427,6 +427,8 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
       a.scatter = in.scatter;
       a.scatter_rows = in.scatter_rows;
       a.allow_streamk = gemm_streamk_ok(exec_lane_[in.id]);
+    a.gpu_share = gpu_share(exec_lane_[in.id]);
+      a.gpu_share = gpu_share(exec_lane_[in.id]);
       if (opt_.allow_tensor_cores && gemm_sm100_eligible(a)) {
         ++gemm_tc_per_step_;
         kernels_per_step_ += gemm_sm100_launches(a) - 1;  // split-K reduce kernel
@@ -492,12 +494,14 @@ Executor::~Executor() {
   if (origin_) cudaStreamDestroy(origin_);
 }
 
-bool Executor::gemm_streamk_ok(int lane) const {
+int Executor::gpu_share(int lane) const {
   int sharing = 0;
   for (int l = 0; l < prog_.num_lanes; ++l)
     if (owned_[l] && lanes_[l].gpu == lanes_[lane].gpu) ++sharing;
-  return sharing == 1;
+  return std::max(sharing, 1);
 }
+
+bool Executor::gemm_streamk_ok(int lane) const { return gpu_share(lane) == 1; }
 
 bool Executor::released(int b) const {
   while (!alias_.empty() && alias_[b] >= 0) b = alias_[b];
@@ -742,8 +746,11 @@ void Executor::build_box_tables() {
       // so they spread over ~2 waves of blocks instead of a few dozen SMs.
       std::int64_t total = 0;
       for (const Cell* c : groups[g]) total += c->elems() / width;
-      const std::int64_t kChunkUnits = std::max<std::int64_t>(
-          256, std::min<std::int64_t>(kBoxChunkUnits, (total / (2 * 148) + 255) / 256 * 256));
+      static const char* fixed = std::getenv("PLANC_B200_BOX_CHUNK");  // A/B: a fixed chunk size
+      const std::int64_t kChunkUnits =
+          fixed ? std::max<std::int64_t>(1, std::min<std::int64_t>(kBoxChunkUnits, std::atoll(fixed)))
+                : std::max<std::int64_t>(
+                      256, std::min<std::int64_t>(kBoxChunkUnits, (total / (2 * 148) + 255) / 256 * 256));
       std::vector<DevCell> cells;
       std::vector<DevTerm> terms;
       std::vector<DevChunk> chunks;
@@ -1114,6 +1121,7 @@ GemmArgs Executor::gemm_args(const Instr& in) const {
     a.ws = lr.gemm_ws[exec_stream_[in.id]];
     a.ws_bytes = lr.gemm_ws_bytes[exec_stream_[in.id]];
     a.allow_streamk = gemm_streamk_ok(exec_lane_[in.id]);
+    a.gpu_share = gpu_share(exec_lane_[in.id]);
   }
   if (!in.gather[0].empty() || !in.gather[1].empty()) {
     if (in.group != 1 || in.scatter > 0) throw InternalError("malformed gathered-operand GEMM instruction");

@@ -188,7 +188,8 @@ class Executor {
   void* buf_ptr(int b) const;
   bool released(int b) const;  // REUSE_MEMORY: bytes taken over by a later buffer
   void plan_aliases();
-  bool gemm_streamk_ok(int lane) const;  // the lane has its GPU to itself
+  bool gemm_streamk_ok(int lane) const;
+  int gpu_share(int lane) const;  // the lane has its GPU to itself
   cudaStream_t stream_of(const Instr& in) const;
   void build_box_tables();
   void plan_box_batches();

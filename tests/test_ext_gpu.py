@@ -42,7 +42,8 @@ def bf16_round(x):
 
 @pytest.mark.parametrize("kind", ["softmax", "softmax-grad", "layernorm", "layernorm-grad", "gelu", "gelu-grad"])
 @pytest.mark.parametrize("shape,seg", [((33, 128), 0), ((7, 2048), 0), ((5, 96), 32), ((9, 7), 0), ((3, 4096), 0),
-                                       ((2, 6000), 1000)])
+                                       ((2, 6000), 1000), ((4, 2056), 0), ((3, 8192), 0), ((2, 24576), 0),
+                                       ((2, 40000), 0)])
 @pytest.mark.parametrize("elem", [4, 2])
 def test_rowwise_kernels_vs_fp64(kind, shape, seg, elem):
     binary = kind.endswith("-grad")
