@@ -105,6 +105,29 @@ __device__ __forceinline__ void store_vec(T* p, const typename Acc<T>::type (&v)
   }
 }
 
+// Raw 16-byte vector loads, unpacked only after every load of a thread is in
+// flight (unpacking at each load lets the compiler recycle one destination
+// register set and serialise the loads).
+template <typename T>
+__device__ __forceinline__ uint4 ld16(const T* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+template <typename T, int V>
+__device__ __forceinline__ void unpack16(const uint4& r, float (&o)[V]) {
+  static_assert(V == 16 / sizeof(T), "one 16-byte vector");
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    unpack_word(r.x, o[0], o[1]);
+    unpack_word(r.y, o[2], o[3]);
+    unpack_word(r.z, o[4], o[5]);
+    unpack_word(r.w, o[6], o[7]);
+  } else {
+    o[0] = __uint_as_float(r.x);
+    o[1] = __uint_as_float(r.y);
+    o[2] = __uint_as_float(r.z);
+    o[3] = __uint_as_float(r.w);
+  }
+}
+
 __device__ __forceinline__ float load_any(const void* p, int dt, std::int64_t i) {
   if (dt == DT_BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
   if (dt == DT_I32) return static_cast<float>(reinterpret_cast<const int*>(p)[i]);
@@ -362,12 +385,20 @@ __global__ void __launch_bounds__(256) reduce_rows_kernel(const T* __restrict__ 
     float acc = 0.f;
     for (std::int64_t a0 = lane; a0 < nv; a0 += 32 * U) {
       float v[U][V];
+      if constexpr (V > 1) {  // raw loads first: all U in flight
+        uint4 raw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) raw[u] = a0 + 32 * u < nv ? ld16(row + (a0 + 32 * u) * V) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) unpack16<T, V>(raw[u], v[u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (a0 + 32 * u < nv) load_vec<T, V>(row + (a0 + 32 * u) * V, v[u]);
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (a0 + 32 * u < nv) load_vec<T, V>(row + (a0 + 32 * u) * V, v[u]);
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (a0 + 32 * u < nv) {
+        if (V > 1 || a0 + 32 * u < nv) {  // V > 1: dead vectors loaded as zeros
 #pragma unroll
           for (int j = 0; j < V; ++j) acc += v[u][j];
         }
@@ -413,17 +444,32 @@ __global__ void __launch_bounds__(kRedWarps * 32) reduce_cols_kernel(const T* __
   constexpr int U = 2;
   for (std::int64_t a = a_lo + warp; a < a_hi; a += kRedWarps * U) {
     float v[U][kRedCV][V];
+    if constexpr (V > 1) {  // raw loads first: all U x CV in flight
+      uint4 raw[U][kRedCV];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int c = 0; c < kRedCV; ++c)
+          raw[u][c] = live[c] && a + kRedWarps * u < a_hi
+                          ? ld16(base + (a + kRedWarps * u) * inner + (c * 32 + lane) * V)
+                          : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int c = 0; c < kRedCV; ++c) unpack16<T, V>(raw[u][c], v[u][c]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int c = 0; c < kRedCV; ++c)
+          if (live[c] && a + kRedWarps * u < a_hi)
+            load_vec<T, V>(base + (a + kRedWarps * u) * inner + (c * 32 + lane) * V, v[u][c]);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int c = 0; c < kRedCV; ++c)
-        if (live[c] && a + kRedWarps * u < a_hi)
-          load_vec<T, V>(base + (a + kRedWarps * u) * inner + (c * 32 + lane) * V, v[u][c]);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int c = 0; c < kRedCV; ++c)
-        if (live[c] && a + kRedWarps * u < a_hi) {
+        if (V > 1 || (live[c] && a + kRedWarps * u < a_hi)) {  // V > 1: dead vectors loaded as zeros
 #pragma unroll
           for (int j = 0; j < V; ++j) acc[c][j] += v[u][c][j];
         }
@@ -453,8 +499,17 @@ __global__ void __launch_bounds__(256) reduce_cols_finish(const float* __restric
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     const std::int64_t o = i / inner, c = i - o * inner;
     const float* p = partial + o * S * inner + c;
-    float sum = p[0];
-    for (int s = 1; s < S; ++s) sum += p[s * inner];
+    // Partials folded in split order; loaded 8 at a time so the chain of S
+    // loads costs S / 8 memory round trips, not S.
+    float sum = 0.f;
+    for (int s0 = 0; s0 < S; s0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int d = 0; d < 8; ++d) v[d] = s0 + d < S ? __ldcg(p + static_cast<std::int64_t>(s0 + d) * inner) : 0.f;
+#pragma unroll
+      for (int d = 0; d < 8; ++d)
+        if (s0 + d < S) sum = s0 + d == 0 ? v[d] : sum + v[d];
+    }
     out[i] = from_acc<T>(sum);
   }
 }
@@ -752,12 +807,13 @@ void launch_ew(int op, int dtype, const void* const* ins, int nin, void* out, st
 namespace {
 bool aligned16(const void* p) { return reinterpret_cast<std::uintptr_t>(p) % 16 == 0; }
 
-// Axis splits of a column reduction: enough blocks for ~2 waves, at least
-// 64 rows per split.
+// Axis splits of a column reduction: enough blocks for ~4 resident per SM,
+// at least 128 rows per split (the finishing pass reads S partials per
+// column).
 int reduce_splits(std::int64_t outer, std::int64_t axis_len, std::int64_t inner, int vec) {
   const std::int64_t tiles = outer * ((inner + 32 * vec * kRedCV - 1) / (32 * vec * kRedCV));
-  std::int64_t S = (2 * 148 + tiles - 1) / tiles;
-  S = std::min<std::int64_t>(S, std::max<std::int64_t>(1, axis_len / 64));
+  std::int64_t S = (4 * 148 + tiles - 1) / tiles;
+  S = std::min<std::int64_t>(S, std::max<std::int64_t>(1, axis_len / 128));
   return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(S, 1024)));
 }
 
@@ -1059,15 +1115,21 @@ __global__ void __launch_bounds__(kRowWarps * 32) row_reg_kernel(const T* __rest
   const int nv = seg / V;
   const long long base = (live_seg ? sidx : 0) * seg;
   float x[R][V], g[R][V];
+  {
+    uint4 ra[R], rb[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int vi = j + r * LPS;
-    const bool ok = live_seg && vi < nv;
+    for (int r = 0; r < R; ++r) {
+      const int vi = j + r * LPS;
+      ra[r] = rb[r] = make_uint4(0, 0, 0, 0);
+      if (live_seg && vi < nv) {
+        ra[r] = ld16(a + base + vi * V);
+        if constexpr (OP == 1 || OP == 3) rb[r] = ld16(b + base + vi * V);
+      }
+    }
 #pragma unroll
-    for (int e = 0; e < V; ++e) x[r][e] = g[r][e] = 0.f;
-    if (ok) {
-      load_vec<T, V>(a + base + vi * V, x[r]);
-      if constexpr (OP == 1 || OP == 3) load_vec<T, V>(b + base + vi * V, g[r]);
+    for (int r = 0; r < R; ++r) {
+      unpack16<T, V>(ra[r], x[r]);
+      unpack16<T, V>(rb[r], g[r]);
     }
   }
   auto valid = [&](int r) { return live_seg && j + r * LPS < nv; };
@@ -1173,14 +1235,21 @@ __global__ void __launch_bounds__(512) row_cta_kernel(const T* __restrict__ a, c
   const int nv = seg / V;
   const long long base = static_cast<long long>(blockIdx.x) * seg;
   float x[R][V], g[R][V];
+  {
+    uint4 ra[R], rb[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int vi = threadIdx.x + r * blockDim.x;
+    for (int r = 0; r < R; ++r) {
+      const int vi = threadIdx.x + r * blockDim.x;
+      ra[r] = rb[r] = make_uint4(0, 0, 0, 0);
+      if (vi < nv) {
+        ra[r] = ld16(a + base + vi * V);
+        if constexpr (OP == 1 || OP == 3) rb[r] = ld16(b + base + vi * V);
+      }
+    }
 #pragma unroll
-    for (int e = 0; e < V; ++e) x[r][e] = g[r][e] = 0.f;
-    if (vi < nv) {
-      load_vec<T, V>(a + base + vi * V, x[r]);
-      if constexpr (OP == 1 || OP == 3) load_vec<T, V>(b + base + vi * V, g[r]);
+    for (int r = 0; r < R; ++r) {
+      unpack16<T, V>(ra[r], x[r]);
+      unpack16<T, V>(rb[r], g[r]);
     }
   }
   auto valid = [&](int r) { return static_cast<int>(threadIdx.x + r * blockDim.x) < nv; };

@@ -741,16 +741,13 @@ void Executor::build_box_tables() {
     for (int g = 0; g < 2; ++g) {
       if (groups[g].empty()) continue;
       std::int64_t width = g ? V : 1;
-      // Chunk size: a block owns up to kBoxChunkUnits vector units; launches
-      // moving a few MB (C5's all-to-all / split pieces) use smaller chunks
-      // so they spread over ~2 waves of blocks instead of a few dozen SMs.
-      std::int64_t total = 0;
-      for (const Cell* c : groups[g]) total += c->elems() / width;
-      static const char* fixed = std::getenv("PLANC_B200_BOX_CHUNK");  // A/B: a fixed chunk size
+      // A block owns up to kBoxChunkUnits vector units of one cell. Smaller
+      // chunks for small boxes (>= 2 waves of blocks) measured slower (C5
+      // 2.33 -> 3.10 ms: the lanes' concurrent launches already fill the
+      // SMs); PLANC_B200_BOX_CHUNK=<units> sets a fixed size for A/B.
+      static const char* fixed = std::getenv("PLANC_B200_BOX_CHUNK");
       const std::int64_t kChunkUnits =
-          fixed ? std::max<std::int64_t>(1, std::min<std::int64_t>(kBoxChunkUnits, std::atoll(fixed)))
-                : std::max<std::int64_t>(
-                      256, std::min<std::int64_t>(kBoxChunkUnits, (total / (2 * 148) + 255) / 256 * 256));
+          fixed ? std::max<std::int64_t>(1, std::min<std::int64_t>(kBoxChunkUnits, std::atoll(fixed))) : kBoxChunkUnits;
       std::vector<DevCell> cells;
       std::vector<DevTerm> terms;
       std::vector<DevChunk> chunks;
