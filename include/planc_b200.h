@@ -71,6 +71,11 @@ extern "C" {
 #define PLANC_B200_NO_GATHER 0x2000u    /* materialise every concat / all-gather (default: one whose output only
                                            feeds tensor-core GEMMs as an operand is dropped and the GEMMs' TMA
                                            loads read the row pieces in place — the all-gather -> GEMM prologue) */
+#define PLANC_B200_NO_BOX_EW 0x4000u    /* keep an add / mul / max on a pure-copy adapter output (all-to-all,
+                                           all-gather, layout change) as its own kernel (default: it runs inside
+                                           the adapter's box launch as fold terms — same bits) */
+#define PLANC_B200_NO_ALIAS_VIEWS 0x8000u /* copy contiguous sub-ranges (splits) instead of aliasing them as views
+                                           of their source on the same GPU (NO_ALIAS turns off every alias) */
 #define PLANC_B200_SERIAL_LANES 0x8u    /* one stream per lane: a lane's tasks run strictly in plan
                                            order (default: only data dependencies and sync edges order
                                            a lane's work, spread over several streams) */

@@ -46,6 +46,8 @@ FUSE_ACT = 0x400
 REUSE_MEMORY = 0x800
 BATCH = 0x1000
 NO_GATHER = 0x2000
+NO_BOX_EW = 0x4000
+NO_ALIAS_VIEWS = 0x8000
 
 
 class PlancError(RuntimeError):

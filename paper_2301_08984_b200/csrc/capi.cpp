@@ -65,10 +65,12 @@ ExecOptions exec_options(uint32_t flags) {
   opt.fuse_act = (flags & PLANC_B200_FUSE_ACT) != 0;
   opt.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0;
   opt.alias_copies = (flags & PLANC_B200_NO_ALIAS) == 0;
+  opt.alias_views = (flags & PLANC_B200_NO_ALIAS_VIEWS) == 0;
   opt.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0;
   opt.reuse_memory = (flags & PLANC_B200_REUSE_MEMORY) != 0;
   opt.batch_boxes = (flags & PLANC_B200_BATCH) != 0;
   opt.gather_operands = (flags & PLANC_B200_NO_GATHER) == 0;
+  opt.fuse_box_ew = (flags & PLANC_B200_NO_BOX_EW) == 0;
   return opt;
 }
 
@@ -80,6 +82,7 @@ ProgramOptions describe_options(uint32_t flags) {
   po.group_gemms = (flags & PLANC_B200_NO_GROUPING) == 0 && tc;
   po.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0 && tc;
   po.gather_operands = (flags & PLANC_B200_NO_GATHER) == 0 && tc;
+  po.fuse_box_ew = (flags & PLANC_B200_NO_BOX_EW) == 0;
   return po;
 }
 
@@ -153,6 +156,7 @@ int planc_b200_describe_rank(const char* plan_json, const int* lane_rank, int nu
     if ((flags & PLANC_B200_PEER_MEMORY) == 0) {
       po.two_phase_allreduce = false;  // NCCL exchange steps: whole-buffer ncclAllReduce
       po.gather_operands = false;      // pieces on other ranks are not addressable
+      po.fuse_box_ew = false;          // as in Executor (NCCL exchange steps)
       *json_out = dup(localize(build_program(plan, po), lr).describe_json());
       return;
     }

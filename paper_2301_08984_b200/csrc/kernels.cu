@@ -807,12 +807,33 @@ void launch_ew(int op, int dtype, const void* const* ins, int nin, void* out, st
 namespace {
 bool aligned16(const void* p) { return reinterpret_cast<std::uintptr_t>(p) % 16 == 0; }
 
-// Axis splits of a column reduction: enough blocks for ~4 resident per SM,
-// at least 128 rows per split (the finishing pass reads S partials per
-// column).
+// Axis splits of a column reduction: one full wave of resident blocks
+// (occupancy x SMs — a second, partial wave doubled the kernel's time:
+// 512 blocks on 444 slots measured 61 us for 134 MB), at least 128 rows per
+// split (the finishing pass reads S partials per column).
+int reduce_resident_blocks(int vec) {
+  static int cached[2] = {0, 0};
+  int& c = cached[vec > 4 ? 1 : 0];
+  if (c == 0) {
+    int per_sm = 0;
+    const cudaError_t e =
+        vec > 4 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reduce_cols_kernel<__nv_bfloat16, 8>,
+                                                                kRedWarps * 32, 0)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reduce_cols_kernel<float, 4>, kRedWarps * 32, 0);
+    if (e != cudaSuccess || per_sm <= 0) {
+      (void)cudaGetLastError();
+      per_sm = 3;
+    }
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    c = per_sm * std::max(sms, 1);
+  }
+  return c;
+}
+
 int reduce_splits(std::int64_t outer, std::int64_t axis_len, std::int64_t inner, int vec) {
   const std::int64_t tiles = outer * ((inner + 32 * vec * kRedCV - 1) / (32 * vec * kRedCV));
-  std::int64_t S = (4 * 148 + tiles - 1) / tiles;
+  std::int64_t S = std::max<std::int64_t>(1, reduce_resident_blocks(vec) / tiles);
   S = std::min<std::int64_t>(S, std::max<std::int64_t>(1, axis_len / 128));
   return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(S, 1024)));
 }

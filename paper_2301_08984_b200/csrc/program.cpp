@@ -851,6 +851,7 @@ Program build_program(const ExecutionPlan& plan, const ProgramOptions& opt) {
   b.run();
   if (opt.two_phase_allreduce) two_phase_allreduce(b.P, opt);
   if (opt.fuse_epilogues) fuse_gemm_epilogues(b.P, opt);
+  if (opt.fuse_epilogues && opt.fuse_box_ew) fuse_box_elementwise(b.P, opt);
   if (opt.gather_operands && opt.gemm_groupable) gather_gemm_operands(b.P, opt);
   if (opt.group_gemms && opt.gemm_groupable) group_gemms(b.P, opt);
   return std::move(b.P);
@@ -1057,6 +1058,125 @@ void gather_gemm_operands(Program& P, const ProgramOptions& opt) {
     bx.bytes = 0;
     P.buffers[O].dead = true;
     P.buffers[O].producer = -1;
+  }
+}
+
+void fuse_box_elementwise(Program& P, const ProgramOptions&) {
+  const int nb = static_cast<int>(P.buffers.size());
+  std::vector<int> nreaders(nb, 0), nwriters(nb, 0);
+  for (const auto& in : P.instrs) {
+    if (in.kind == InstrKind::nop) continue;
+    std::set<int> r;
+    for (int b : in.in_bufs) r.insert(b);
+    for (const auto& c : in.cells)
+      for (const auto& t : c.terms) r.insert(t.buffer);
+    for (const auto& fe : in.fused)
+      for (int b : fe.in_bufs) r.insert(b);
+    for (const auto& x : in.xfers) r.insert(x.src);
+    for (int b : r) ++nreaders[b];
+    for (int b : in.out_bufs) ++nwriters[b];
+  }
+  std::set<int> outputs;
+  for (const auto& o : P.outputs)
+    for (int b : o.second) outputs.insert(b);
+  std::vector<int> pos(P.instrs.size(), 0);
+  for (std::size_t i = 0; i < P.issue_order.size(); ++i) pos[P.issue_order[i]] = static_cast<int>(i);
+  std::vector<int> redirect(P.instrs.size(), -1);  // fused ew -> its box
+  for (auto& e : P.instrs) {
+    if (e.kind != InstrKind::ew || e.out_bufs.size() != 1 || e.in_bufs.size() < 2 ||
+        e.in_bufs.size() > 8 ||
+        !(e.ew == EwOp::add || e.ew == EwOp::mul || e.ew == EwOp::max))
+      continue;
+    const DType dt = P.buffers[e.out_bufs[0]].dtype;
+    bool same = true;
+    for (int b : e.in_bufs) same = same && P.buffers[b].dtype == dt && P.buffers[b].elems == e.count;
+    if (!same) continue;
+    // The box operand: produced by a pure-copy box of this lane, read only here.
+    int bi = -1;
+    for (std::size_t i = 0; i < e.in_bufs.size() && bi < 0; ++i) {
+      const int O = e.in_bufs[i];
+      const BufferDesc& ob = P.buffers[O];
+      if (ob.producer < 0 || ob.graph_input || outputs.count(O) || nreaders[O] != 1 || nwriters[O] != 1) continue;
+      if (std::count(e.in_bufs.begin(), e.in_bufs.end(), O) != 1) continue;
+      const Instr& bx = P.instrs[ob.producer];
+      if (bx.kind != InstrKind::box || bx.lane != e.lane || bx.out_bufs.size() != 1 || bx.out_bufs[0] != O ||
+          bx.cells.empty() || redirect[bx.id] >= 0)
+        continue;
+      std::int64_t covered = 0;
+      bool copies = true;
+      for (const auto& c : bx.cells) {
+        copies = copies && c.terms.size() == 1 && !c.terms[0].add && c.terms[0].fold < 0 &&
+                 P.buffers[c.terms[0].buffer].dtype == dt;
+        covered += c.elems();
+      }
+      if (copies && covered == ob.elems) bi = static_cast<int>(i);
+    }
+    if (bi < 0) continue;
+    const int O = e.in_bufs[bi];
+    Instr& bx = P.instrs[P.buffers[O].producer];
+    // The other operands' producers must be issued before the box (it gains
+    // them as dependencies).
+    bool ready = true;
+    std::set<int> extra;
+    for (std::size_t i = 0; i < e.in_bufs.size(); ++i) {
+      if (static_cast<int>(i) == bi) continue;
+      const int pr = P.buffers[e.in_bufs[i]].producer;
+      if (pr < 0) continue;
+      const int pe = redirect[pr] >= 0 ? redirect[pr] : pr;
+      if (pos[pe] >= pos[bx.id]) ready = false;
+      extra.insert(pe);
+    }
+    if (!ready) continue;
+    const int fold = static_cast<int>(e.ew);
+    for (auto& c : bx.cells) {
+      const Term bt = c.terms[0];
+      std::vector<Term> terms;
+      for (std::size_t i = 0; i < e.in_bufs.size(); ++i) {
+        Term t;
+        if (static_cast<int>(i) == bi) {
+          t = bt;
+        } else {  // operand i: the same element positions as the cell's destination
+          t.buffer = e.in_bufs[i];
+          t.offset = c.dst_offset;
+          for (int d = 0; d < kMaxCellRank; ++d) t.strides[d] = c.dst_strides[d];
+        }
+        t.add = false;
+        t.fold = i == 0 ? -1 : fold;
+        terms.push_back(t);
+      }
+      c.terms = std::move(terms);
+    }
+    for (int d : extra)
+      if (d != bx.id) bx.deps.push_back(d);
+    std::sort(bx.deps.begin(), bx.deps.end());
+    bx.deps.erase(std::unique(bx.deps.begin(), bx.deps.end()), bx.deps.end());
+    const double ob_bytes = static_cast<double>(P.buffers[O].bytes);
+    bx.bytes += e.bytes - 2 * ob_bytes;  // O is neither written nor re-read
+    bx.out_bufs = e.out_bufs;
+    bx.label += "+" + e.label;
+    P.buffers[e.out_bufs[0]].producer = bx.id;
+    P.buffers[O].dead = true;
+    P.buffers[O].producer = -1;
+    redirect[e.id] = bx.id;
+    e.kind = InstrKind::nop;
+    e.deps.clear();
+    e.in_bufs.clear();
+    e.out_bufs.clear();
+    e.bytes = 0;
+  }
+  for (auto& in : P.instrs) {
+    bool changed = false;
+    for (int& d : in.deps) {
+      if (redirect[d] >= 0) {
+        d = redirect[d];
+        changed = true;
+      }
+    }
+    if (changed) {
+      std::sort(in.deps.begin(), in.deps.end());
+      in.deps.erase(std::unique(in.deps.begin(), in.deps.end()), in.deps.end());
+      in.deps.erase(std::remove(in.deps.begin(), in.deps.end(), in.id), in.deps.end());
+    }
   }
 }
 
@@ -1699,6 +1819,7 @@ std::string Program::describe_json() const {
       for (std::size_t t = 0; t < cl.terms.size(); ++t) {
         const auto& tm = cl.terms[t];
         os << (t ? "," : "") << "{\"buf\":" << tm.buffer << ",\"off\":" << tm.offset << ",\"add\":" << tm.add
+           << ",\"fold\":" << tm.fold
            << ",\"str\":[";
         for (int d = 0; d < cl.rank; ++d) os << (d ? "," : "") << tm.strides[d];
         os << "]}";

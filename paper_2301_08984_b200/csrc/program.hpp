@@ -57,10 +57,14 @@ struct Term {
   std::int64_t offset = 0;  // element offset of the cell origin in the source
   std::int64_t strides[kMaxCellRank] = {0};
   bool add = false;
+  // >= 0: an elementwise op folded into the box (fuse_box_elementwise):
+  // value = value (EwOp add | mul | max) term, in the ew kernel's fp32 fold.
+  int fold = -1;
 };
 
 // Destination box of an adapter output with its ordered source terms.
-// value = 0; for term in terms: value = term (copy) | value += term (add).
+// value = 0; for term in terms: value = term (copy) | value += term (add)
+// | value = value fold term.
 struct Cell {
   int rank = 0;
   std::int64_t extents[kMaxCellRank] = {0};
@@ -214,6 +218,13 @@ struct ProgramOptions {
   // all-gather / concat -> GEMM prologue. Single-process and peer-memory
   // modes (the pieces must be addressable by the GEMM's lane).
   bool gather_operands = true;
+  // An elementwise op (add / mul / max) whose operand is the output of a
+  // pure-copy box instruction (an all-to-all / all-gather / layout adapter)
+  // read by nothing else runs inside that box: the other operands become
+  // fold terms of every cell and the box writes the op's output — one launch
+  // and one HBM round trip of the adapter output fewer, the same bits (the
+  // copy is exact, the fold is the ew kernel's fp32 fold in operand order).
+  bool fuse_box_ew = true;
   bool (*gemm_groupable)(const Instr& gemm, DType a, DType b, DType c) = nullptr;
   bool (*gemm_fusable)(const Instr& gemm, DType a, DType b, DType c) = nullptr;
 };
@@ -255,6 +266,8 @@ void group_gemms(Program& p, const ProgramOptions& opt);
 // Gather-prologue pass (opt.gather_operands; run after epilogue fusion,
 // before grouping): see ProgramOptions::gather_operands.
 void gather_gemm_operands(Program& p, const ProgramOptions& opt);
+// Box -> elementwise fusion pass (opt.fuse_box_ew; after epilogue fusion).
+void fuse_box_elementwise(Program& p, const ProgramOptions& opt);
 
 // The two-phase all-reduce pass (ProgramOptions::two_phase_allreduce), run
 // by build_program before epilogue fusion. Rebuilds the program in issue

@@ -190,6 +190,13 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   po.two_phase_allreduce = !(rank && !rank->peer_memory);
   // Gathered operands read pieces in place: not across NCCL ranks.
   po.gather_operands = opt.gather_operands && opt.allow_tensor_cores && !(rank && !rank->peer_memory);
+  // Box -> elementwise fusion: single-process and peer-memory modes
+  // (PLANC_B200_BOX_EW=0 for A/B).
+  static const bool box_ew_env = [] {
+    const char* e = std::getenv("PLANC_B200_BOX_EW");
+    return !(e && e[0] == '0');
+  }();
+  po.fuse_box_ew = opt.fuse_box_ew && box_ew_env && !(rank && !rank->peer_memory);
   // The scatter epilogue pays when the slices cross GPUs (the transfer rides
   // in the GEMM); with every lane on one GPU it only trades TMA stores for
   // plain ones (measured ~2 % slower, profiles/r01/ab_scatter.jsonl).
@@ -509,35 +516,52 @@ bool Executor::released(int b) const {
 }
 
 void* Executor::buf_ptr(int b) const {
-  while (!alias_.empty() && alias_[b] >= 0) b = alias_[b];
+  std::int64_t off = 0;  // bytes into the aliased source (a view of a sub-range)
+  while (!alias_.empty() && alias_[b] >= 0) {
+    off += alias_off_[b];
+    b = alias_[b];
+  }
   const BufferDesc& d = prog_.buffers[b];
-  return lanes_[d.lane].arena + d.offset;
+  return lanes_[d.lane].arena + d.offset + off;
 }
 
-// A box instruction that copies one whole buffer into another of the same
-// dense layout (a recv whose send lane shares the GPU, an identity op) moves
-// no data when both lanes' arenas sit in the same HBM: the output becomes an
-// alias of the source (single assignment: neither is rewritten within the
-// step) and the instruction launches nothing — its events still order its
-// consumers after its producers. Across GPUs or ranks the copy stays.
+// A box instruction that copies one whole buffer — or one contiguous
+// sub-range of it (a split along the outermost dimension) — into another
+// buffer of the same dense layout (a recv whose send lane shares the GPU, an
+// identity op, C5's DAP splits) moves no data when both lanes' arenas sit in
+// the same HBM: the output becomes an alias of the source range (single
+// assignment: neither is rewritten within the step; sub-ranges start on a
+// 256-byte boundary, as arena buffers do) and the instruction launches
+// nothing — its events still order its consumers after its producers.
+// Across GPUs or ranks the copy stays.
 void Executor::plan_aliases() {
   alias_.assign(prog_.buffers.size(), -1);
+  alias_off_.assign(prog_.buffers.size(), 0);
   if (rank_mode_ || !opt_.alias_copies) return;
+  static const bool views_env = [] {  // A/B: PLANC_B200_ALIAS_VIEWS=0 keeps sub-range copies
+    const char* e = std::getenv("PLANC_B200_ALIAS_VIEWS");
+    return !(e && e[0] == '0');
+  }();
+  const bool views = opt_.alias_views && views_env;
   std::vector<int> writers(prog_.buffers.size(), 0);
   for (const auto& in : prog_.instrs)
     for (int b : in.out_bufs) ++writers[b];
   for (const auto& in : prog_.instrs) {
     if (in.kind != InstrKind::box || exec_lane_[in.id] < 0 || in.out_bufs.size() != 1 || in.cells.size() != 1) continue;
     const Cell& c = in.cells[0];
-    if (c.terms.size() != 1 || c.terms[0].add || c.rank != 1 || c.dst_offset != 0 || c.dst_strides[0] != 1 ||
-        c.terms[0].offset != 0 || c.terms[0].strides[0] != 1)
+    if (c.terms.size() != 1 || c.terms[0].add || c.terms[0].fold >= 0 || c.rank != 1 || c.dst_offset != 0 ||
+        c.dst_strides[0] != 1 || c.terms[0].strides[0] != 1)
       continue;
     const BufferDesc& ob = prog_.buffers[in.out_bufs[0]];
     const BufferDesc& sb = prog_.buffers[c.terms[0].buffer];
-    if (ob.graph_input || writers[ob.id] != 1 || ob.dtype != sb.dtype || ob.elems != sb.elems || c.elems() != ob.elems)
+    const std::int64_t off = c.terms[0].offset;
+    const std::int64_t off_bytes = off * static_cast<std::int64_t>(dtype_size(sb.dtype));
+    if (ob.graph_input || writers[ob.id] != 1 || ob.dtype != sb.dtype || c.elems() != ob.elems || off < 0 ||
+        off + ob.elems > sb.elems || off_bytes % 256 != 0 || (off != 0 && !views))
       continue;
     if (!owned_[sb.lane] || lanes_[ob.lane].gpu != lanes_[sb.lane].gpu) continue;
     alias_[ob.id] = sb.id;
+    alias_off_[ob.id] = off_bytes;
     irt_[in.id].aliased = true;
   }
 }
@@ -723,7 +747,10 @@ void Executor::check_sync(cudaError_t e, const char* what) const {
 }
 
 void Executor::build_box_tables() {
-  if (alias_.empty()) alias_.assign(prog_.buffers.size(), -1);
+  if (alias_.empty()) {
+    alias_.assign(prog_.buffers.size(), -1);
+    alias_off_.assign(prog_.buffers.size(), 0);
+  }
   for (const auto& in : prog_.instrs) {
     if (in.kind != InstrKind::box || exec_lane_[in.id] < 0 || irt_[in.id].aliased) continue;
     const BufferDesc& ob = prog_.buffers[in.out_bufs[0]];
@@ -776,7 +803,7 @@ void Executor::build_box_tables() {
           dt.src = buf_ptr(t.buffer);
           dt.offset = t.offset;
           for (int d = 0; d < R; ++d) dt.str[d] = d < pad ? 0 : t.strides[d - pad];
-          dt.op = t.add ? 1 : 0;
+          dt.op = t.fold >= 0 ? t.fold + 1 : t.add ? 1 : 0;  // EwOp add / mul / max -> box 1 / 2 / 3
           terms.push_back(dt);
         }
         int ci = static_cast<int>(cells.size());
@@ -1762,7 +1789,7 @@ void Executor::get_output_into(int ptensor, double* out, std::int64_t capacity) 
           for (std::int64_t j = 0; j < inner; ++j) {
             const double x = load_elem(base, dt, so + j * sstep);
             double& v = out[doff + j * dstep];
-            v = t.add ? v + x : x;
+            v = t.fold == 0 ? v + x : t.fold == 1 ? v * x : t.fold == 2 ? std::max(v, x) : t.add ? v + x : x;
           }
         }
       }

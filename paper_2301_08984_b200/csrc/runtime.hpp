@@ -53,6 +53,7 @@ struct ExecOptions {
   bool fuse_act = false;                // ...GELU / GELU-grad as well (PLANC_B200_FUSE_ACT)
   bool group_gemms = true;              // same-shape independent GEMMs in one grouped launch
   bool alias_copies = true;             // same-GPU whole-buffer copies (recv, identity) become aliases
+  bool alias_views = true;              // ...and contiguous sub-range copies (splits) views of their source
   bool scatter_allreduce = true;        // all-reduce partials leave the GEMM epilogue as reduce-scatter slices
   bool reuse_memory = false;            // timed mode: bytes the plan frees are reused within the step
   // Independent adapter (box) and elementwise instructions of one GPU in
@@ -61,6 +62,7 @@ struct ExecOptions {
   // profiles/r02/ab_batch.jsonl); PLANC_B200_BATCH=1 / 2 (per lane) for A/B.
   bool batch_boxes = false;
   bool gather_operands = true;          // concat / all-gather feeding only GEMMs: GEMMs read the pieces in place
+  bool fuse_box_ew = true;              // elementwise ops on a pure-copy adapter output run inside the box
 };
 
 // ProgramOptions as the executor uses them: epilogue fusion only for GEMMs
@@ -244,6 +246,7 @@ class Executor {
   std::vector<LaneRt> lanes_;
   std::vector<InstrRt> irt_;
   std::vector<int> alias_;  // per buffer: -1, or the buffer whose memory it shares
+  std::vector<std::int64_t> alias_off_;  // per aliased buffer: byte offset into its source
   std::vector<int> gpus_;  // distinct devices
   std::vector<void*> table_allocs_;
   std::vector<BoxBatch> batches_;

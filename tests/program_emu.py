@@ -24,6 +24,10 @@ def buffer_shapes(desc: dict) -> dict:
     return {b["id"]: [hi - lo for lo, hi in b["region"]] for b in desc["buffers"]}
 
 
+def _fold(op, v, x):
+    return (v + x, v * x, np.maximum(v, x))[op]
+
+
 def exec_instr(ins: dict, data: dict, shape: dict):
     """One compute / box instruction on the flat float64 buffers in ``data``
     (results are assigned to data[out]; a box writes only its cells)."""
@@ -109,7 +113,12 @@ def exec_instr(ins: dict, data: dict, shape: dict):
             v = np.zeros(di.shape)
             for t in c["terms"]:
                 si = _strided_view(data[t["buf"]], t["off"], t["str"], c["ext"])
-                v = v + data[t["buf"]][si] if t["add"] else data[t["buf"]][si].copy()
+                x = data[t["buf"]][si]
+                f = t.get("fold", -1)
+                if f >= 0:  # an elementwise op folded into the box (fuse_box_elementwise)
+                    v = _fold(f, v, x)
+                else:
+                    v = v + x if t["add"] else x.copy()
             out[di] = v
         data[ob] = out
 

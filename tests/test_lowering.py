@@ -501,3 +501,29 @@ def test_timed_memory_plan_never_overlaps_live_buffers(name):
         for pt, pieces in desc["outputs"]:
             if pt not in consumed:
                 assert not any(mp["overwritten"][b] for b in pieces)
+
+
+def test_box_elementwise_fusion_lowering():
+    """C5's all-to-all -> max gate: the max runs as fold terms of the
+    all-to-all's box (operand order kept, the adapter output buffer dead),
+    and the lowered program still reproduces the reference bit for bit."""
+    g = golden_cases.load("c5_3f1b_dap")
+    fused = pb.describe(g["plan"])
+    plain = pb.describe(g["plan"], flags=pb.NO_BOX_EW)
+    n_ew = lambda d: sum(1 for i in d["instrs"] if i["kind"] == "ew")  # noqa: E731
+    boxes = [i for i in fused["instrs"] if i["kind"] == "box" and
+             any(t["fold"] >= 0 for c in i["cells"] for t in c["terms"])]
+    assert boxes and n_ew(fused) == n_ew(plain) - len(boxes)
+    for b in boxes:
+        for c in b["cells"]:
+            assert c["terms"][0]["fold"] == -1 and all(t["fold"] >= 0 for t in c["terms"][1:])
+    dead = {b["id"] for b in fused["buffers"] if b.get("dead")}
+    assert dead
+    for ins in fused["instrs"]:
+        assert not dead & set(ins["in"]) and not dead & set(ins["out"])
+    a = run_program(fused, json.loads(g["plan"]), g["inputs"])
+    b = run_program(plain, json.loads(g["plan"]), g["inputs"])
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+    ok, msg = pb.compare_outputs(g["expected"], a, 0.0)
+    assert ok, msg

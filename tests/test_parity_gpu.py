@@ -310,3 +310,42 @@ def test_timed_mode_memory_reuse(name):
                 assert np.array_equal(v, ref[pt]), pt
                 kept += 1
             assert kept > 0
+
+
+@pytest.mark.parametrize("name", ["c5_3f1b_dap", "c5_3f1b_dap_bf16", "c4_coshard_dp8_bf16", "embed_shard2"])
+def test_box_elementwise_fusion(name):
+    """An add / mul / max on a pure-copy adapter output (C5's all-to-all ->
+    max gate) runs inside the adapter's box launch as fold terms: fewer
+    kernels, and the same bits as the separate elementwise kernel
+    (NO_BOX_EW) and as the reference."""
+    g = golden_cases.load(name)
+    desc = pb.describe(g["plan"])
+    fused = [i for i in desc["instrs"] if i["kind"] == "box" and
+             any(t["fold"] >= 0 for c in i["cells"] for t in c["terms"])]
+    assert fused, "the plan has no box -> elementwise pattern"
+    outs, kernels = {}, {}
+    for flags in (0, pb.NO_BOX_EW):
+        out, st = _run(g["plan"], g["inputs"], flags=flags)
+        outs[flags], kernels[flags] = out, st["kernels_per_step"]
+    assert kernels[0] < kernels[pb.NO_BOX_EW]
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[pb.NO_BOX_EW][k]), k
+    ok, msg = pb.compare_outputs(g["expected"], outs[0], g["meta"]["rel_tol"], normwise=True)
+    assert ok, msg
+
+
+@pytest.mark.parametrize("name", ["c5_3f1b_dap", "c5_3f1b_dap_bf16"])
+def test_same_gpu_splits_become_views(name):
+    """A copy of a contiguous sub-range (C5's DAP splits feeding the
+    all-to-all) launches nothing on one GPU: the output is a view of the
+    source range. Same bits as copying it (NO_ALIAS_VIEWS)."""
+    g = golden_cases.load(name)
+    outs, kernels = {}, {}
+    for flags in (0, pb.NO_ALIAS_VIEWS):
+        out, st = _run(g["plan"], g["inputs"], flags=flags)
+        outs[flags], kernels[flags] = out, st["kernels_per_step"]
+    assert kernels[0] < kernels[pb.NO_ALIAS_VIEWS]
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[pb.NO_ALIAS_VIEWS][k]), k
+    ok, msg = pb.compare_outputs(g["expected"], outs[0], g["meta"]["rel_tol"], normwise=True)
+    assert ok, msg
