@@ -147,6 +147,7 @@ struct SkParams {
   // row r reads piece r / gather_rows at row r % gather_rows (pieces are
   // whole multiples of every box height).
   int gather_rows_a = 0, gather_rows_b = 0;
+  int gather_cols_a = 0, gather_cols_b = 0;  // column pieces: a box at stored column x reads piece x / cols
   const CUtensorMap* gather_maps = nullptr;
   long long sk_iters = 0;
   float* partials = nullptr;  // [sk_ctas][2 slots][4 quarters][BN/32 chunks][8][32] float4
@@ -587,18 +588,33 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
     if (lane == 0) {
       int it = 0;  // global k-block counter across work items (ring position)
       const std::uint64_t pol_a = l2_policy(sk.hint_a), pol_b = l2_policy(sk.hint_b);
-      // Gathered operand: the piece holding stored row `row` (made piece-local).
-      auto pick_a = [&](const CUtensorMap* dflt, int& row) -> const CUtensorMap* {
-        if (sk.gather_rows_a == 0) return dflt;
-        const int q = row / sk.gather_rows_a;
-        row -= q * sk.gather_rows_a;
-        return sk.gather_maps + q;
+      // Gathered operand: the piece holding stored row `row` (row pieces)
+      // or stored column `x` (column pieces), coordinates made piece-local.
+      auto pick_a = [&](const CUtensorMap* dflt, int& x, int& row) -> const CUtensorMap* {
+        if (sk.gather_rows_a != 0) {
+          const int q = row / sk.gather_rows_a;
+          row -= q * sk.gather_rows_a;
+          return sk.gather_maps + q;
+        }
+        if (sk.gather_cols_a != 0) {
+          const int q = x / sk.gather_cols_a;
+          x -= q * sk.gather_cols_a;
+          return sk.gather_maps + q;
+        }
+        return dflt;
       };
-      auto pick_b = [&](const CUtensorMap* dflt, int& row) -> const CUtensorMap* {
-        if (sk.gather_rows_b == 0) return dflt;
-        const int q = row / sk.gather_rows_b;
-        row -= q * sk.gather_rows_b;
-        return sk.gather_maps + kMaxGemmGroup + q;
+      auto pick_b = [&](const CUtensorMap* dflt, int& x, int& row) -> const CUtensorMap* {
+        if (sk.gather_rows_b != 0) {
+          const int q = row / sk.gather_rows_b;
+          row -= q * sk.gather_rows_b;
+          return sk.gather_maps + kMaxGemmGroup + q;
+        }
+        if (sk.gather_cols_b != 0) {
+          const int q = x / sk.gather_cols_b;
+          x -= q * sk.gather_cols_b;
+          return sk.gather_maps + kMaxGemmGroup + q;
+        }
+        return dflt;
       };
       work([&](int t, int kb0, int kb1, int half) {
         int p, mb, nb;
@@ -621,22 +637,29 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
             const std::uint32_t lb = cluster_addr(&full[s], 0);
             std::uint8_t* a = sA + s * A_STAGE_BYTES;
             std::uint8_t* b = sB + s * B_STAGE_BYTES;
-            int ra = A_MN ? kb * BK : m0, rb = B_MN ? kb * BK : n0 + r * (BN / 2);
-            const CUtensorMap* mA = pick_a(tmA, ra);
-            const CUtensorMap* mB = pick_b(tmB, rb);
             if (A_MN) {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j)
-                tma_load_2d_2sm_hint(a + j * (64 * BK * 2), mA, m0 + 64 * j, ra, lb, pol_a);
+              for (int j = 0; j < BM / 64; ++j) {
+                int x = m0 + 64 * j, ra = kb * BK;
+                const CUtensorMap* mA = pick_a(tmA, x, ra);
+                tma_load_2d_2sm_hint(a + j * (64 * BK * 2), mA, x, ra, lb, pol_a);
+              }
             } else {
-              tma_load_2d_2sm_hint(a, mA, kb * BK, ra, lb, pol_a);
+              int x = kb * BK, ra = m0;
+              const CUtensorMap* mA = pick_a(tmA, x, ra);
+              tma_load_2d_2sm_hint(a, mA, x, ra, lb, pol_a);
             }
             if (B_MN) {
 #pragma unroll
-              for (int j = 0; j < BN / 128; ++j)
-                tma_load_2d_2sm_hint(b + j * (64 * BK * 2), mB, n0 + r * (BN / 2) + 64 * j, rb, lb, pol_b);
+              for (int j = 0; j < BN / 128; ++j) {
+                int x = n0 + r * (BN / 2) + 64 * j, rb = kb * BK;
+                const CUtensorMap* mB = pick_b(tmB, x, rb);
+                tma_load_2d_2sm_hint(b + j * (64 * BK * 2), mB, x, rb, lb, pol_b);
+              }
             } else {
-              tma_load_2d_2sm_hint(b, mB, kb * BK, rb, lb, pol_b);
+              int x = kb * BK, rb = n0 + r * (BN / 2);
+              const CUtensorMap* mB = pick_b(tmB, x, rb);
+              tma_load_2d_2sm_hint(b, mB, x, rb, lb, pol_b);
             }
           }
           return;
@@ -648,36 +671,45 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
           mbar_expect_tx(&full[s], A_STAGE_BYTES + B_STAGE_BYTES);
           std::uint8_t* a = sA + s * A_STAGE_BYTES;
           std::uint8_t* b = sB + s * B_STAGE_BYTES;
-          int ra = A_MN ? kb * BK : m0;
-          const CUtensorMap* mA = pick_a(tmA, ra);
           if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d_hint(a + j * (64 * BK * 2), mA, m0 + 64 * j, ra, &full[s], pol_a);
+            for (int j = 0; j < BM / 64; ++j) {
+              int x = m0 + 64 * j, ra = kb * BK;
+              const CUtensorMap* mA = pick_a(tmA, x, ra);
+              tma_load_2d_hint(a + j * (64 * BK * 2), mA, x, ra, &full[s], pol_a);
+            }
           } else {
-            tma_load_2d_hint(a, mA, kb * BK, ra, &full[s], pol_a);
+            int x = kb * BK, ra = m0;
+            const CUtensorMap* mA = pick_a(tmA, x, ra);
+            tma_load_2d_hint(a, mA, x, ra, &full[s], pol_a);
           }
           if constexpr (CL) {
             // this CTA's half of the B tile, multicast to both CTAs of the pair
             const int r = t & 1;
-            int rb = B_MN ? kb * BK : n0 + r * (BN / 2);
-            const CUtensorMap* mB = pick_b(tmB, rb);
             if (B_MN) {
 #pragma unroll
-              for (int j = r * (BN / 128); j < (r + 1) * (BN / 128); ++j)
-                tma_load_2d_mc(b + j * (64 * BK * 2), mB, n0 + 64 * j, rb, &full[s], 0x3);
+              for (int j = r * (BN / 128); j < (r + 1) * (BN / 128); ++j) {
+                int x = n0 + 64 * j, rb = kb * BK;
+                const CUtensorMap* mB = pick_b(tmB, x, rb);
+                tma_load_2d_mc(b + j * (64 * BK * 2), mB, x, rb, &full[s], 0x3);
+              }
             } else {
-              tma_load_2d_mc(b + r * (BN / 2) * 128, mB, kb * BK, rb, &full[s], 0x3);
+              int x = kb * BK, rb = n0 + r * (BN / 2);
+              const CUtensorMap* mB = pick_b(tmB, x, rb);
+              tma_load_2d_mc(b + r * (BN / 2) * 128, mB, x, rb, &full[s], 0x3);
             }
           } else {
-            int rb = B_MN ? kb * BK : n0;
-            const CUtensorMap* mB = pick_b(tmB, rb);
             if (B_MN) {
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_load_2d_hint(b + j * (64 * BK * 2), mB, n0 + 64 * j, rb, &full[s], pol_b);
+              for (int j = 0; j < BN / 64; ++j) {
+                int x = n0 + 64 * j, rb = kb * BK;
+                const CUtensorMap* mB = pick_b(tmB, x, rb);
+                tma_load_2d_hint(b + j * (64 * BK * 2), mB, x, rb, &full[s], pol_b);
+              }
             } else {
-              tma_load_2d_hint(b, mB, kb * BK, rb, &full[s], pol_b);
+              int x = kb * BK, rb = n0;
+              const CUtensorMap* mB = pick_b(tmB, x, rb);
+              tma_load_2d_hint(b, mB, x, rb, &full[s], pol_b);
             }
           }
         }
@@ -1275,6 +1307,8 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
   if (a.gather_maps) {
     sk.gather_rows_a = static_cast<int>(a.gather_rows_a);
     sk.gather_rows_b = static_cast<int>(a.gather_rows_b);
+    sk.gather_cols_a = static_cast<int>(a.gather_cols_a);
+    sk.gather_cols_b = static_cast<int>(a.gather_cols_b);
     sk.gather_maps = static_cast<const CUtensorMap*>(a.gather_maps);
   }
   const std::int64_t m_pad = (a.m + BM - 1) / BM * BM, n_pad = (a.n + BN - 1) / BN * BN;
@@ -1304,15 +1338,19 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
 // schedule `sc` loads (gemm_sm100_gather_maps).
 inline void encode_gather_maps(const GemmArgs& a, const GemmSchedule& sc, CUtensorMap* out) {
   const bool a_mn = a.ta, b_mn = !a.tb;
+  // Row pieces: (piece rows) x (full stored width); column pieces: (full
+  // stored rows) x (piece columns).
   for (int i = 0; i < a.gather_a; ++i) {
     // A: K-major [m][k] boxes of BM rows; MN-major [k][m] boxes of BK rows
-    out[i] = a_mn ? make_map(a.gather_a_ptr[i], a.gather_rows_a, a.m, BK)
-                  : make_map(a.gather_a_ptr[i], a.gather_rows_a, a.k, BM);
+    const std::int64_t rows = a.gather_cols_a ? (a_mn ? a.k : a.m) : a.gather_rows_a;
+    const std::int64_t cols = a.gather_cols_a ? a.gather_cols_a : (a_mn ? a.m : a.k);
+    out[i] = make_map(a.gather_a_ptr[i], rows, cols, a_mn ? BK : BM);
   }
   for (int i = 0; i < a.gather_b; ++i) {
     // B: MN-major [k][n] boxes of BK rows; K-major [n][k] boxes of BN (pairs: BN/2) rows
-    out[kMaxGemmGroup + i] = b_mn ? make_map(a.gather_b_ptr[i], a.gather_rows_b, a.n, BK)
-                                  : make_map(a.gather_b_ptr[i], a.gather_rows_b, a.k, sc.occ >= 4 ? sc.bn / 2 : sc.bn);
+    const std::int64_t rows = a.gather_cols_b ? (b_mn ? a.k : a.n) : a.gather_rows_b;
+    const std::int64_t cols = a.gather_cols_b ? a.gather_cols_b : (b_mn ? a.n : a.k);
+    out[kMaxGemmGroup + i] = make_map(a.gather_b_ptr[i], rows, cols, b_mn ? BK : (sc.occ >= 4 ? sc.bn / 2 : sc.bn));
   }
 }
 

@@ -116,8 +116,11 @@ struct GemmArgs {
   // A (B) is the row-wise concatenation, in stored layout, of gather_a
   // (gather_b) pieces of gather_rows_a (_b) rows each; gather_maps = device
   // copy of their tensor maps (gemm_sm100_gather_maps; 16 slots).
+  // With gather_cols_a (_b) > 0 the pieces are column blocks of that many
+  // stored columns instead (gather_rows_* = 0).
   int gather_a = 0, gather_b = 0;
   std::int64_t gather_rows_a = 0, gather_rows_b = 0;
+  std::int64_t gather_cols_a = 0, gather_cols_b = 0;
   const void* gather_a_ptr[kMaxGemmGroup] = {};
   const void* gather_b_ptr[kMaxGemmGroup] = {};
   const void* gather_maps = nullptr;

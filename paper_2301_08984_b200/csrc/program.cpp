@@ -993,34 +993,57 @@ void gather_gemm_operands(Program& P, const ProgramOptions& opt) {
     const BufferDesc& ob = P.buffers[O];
     if (ob.shape.size() != 2 || ob.graph_input || outputs.count(O) || ob.dtype != DType::bf16) continue;
     const std::int64_t R = ob.shape[0], C = ob.shape[1];
-    // Cells: whole row blocks, one plain copy of a dense piece each.
-    std::vector<std::pair<std::int64_t, int>> pieces;  // (first row, source buffer)
-    bool ok = true;
-    std::int64_t rows = -1;
+    // Cells: whole row blocks (or whole column blocks), one plain copy of a
+    // dense piece each.
+    std::vector<std::pair<std::int64_t, int>> pieces;  // (first row / column, source buffer)
+    bool ok = true, by_cols = false;
+    std::int64_t rows = -1, cols = -1;
     for (const auto& c : bx.cells) {
-      if (c.terms.size() != 1 || c.terms[0].add || c.terms[0].offset != 0 || c.dst_offset % C != 0) {
+      if (c.terms.size() != 1 || c.terms[0].add || c.terms[0].fold >= 0 || c.terms[0].offset != 0) {
         ok = false;
         break;
       }
       const Term& t = c.terms[0];
       const BufferDesc& sb = P.buffers[t.buffer];
       const std::int64_t e = c.elems();
-      bool dense = false;
-      if (c.rank == 1) dense = c.dst_strides[0] == 1 && t.strides[0] == 1;
-      if (c.rank == 2)
-        dense = c.extents[1] == C && c.dst_strides[0] == C && c.dst_strides[1] == 1 && t.strides[0] == C &&
-                t.strides[1] == 1;
-      if (!dense || e % C != 0 || sb.elems != e || sb.dtype != ob.dtype || sb.dead) {
+      if (sb.elems != e || sb.dtype != ob.dtype || sb.dead) {
         ok = false;
         break;
       }
-      if (rows < 0) rows = e / C;
-      ok = ok && e / C == rows;
-      pieces.push_back({c.dst_offset / C, t.buffer});
+      bool dense_rows = false, dense_cols = false;
+      if (c.rank == 1) dense_rows = c.dst_strides[0] == 1 && t.strides[0] == 1 && e % C == 0 && c.dst_offset % C == 0;
+      if (c.rank == 2) {
+        dense_rows = c.extents[1] == C && c.dst_strides[0] == C && c.dst_strides[1] == 1 && t.strides[0] == C &&
+                     t.strides[1] == 1 && c.dst_offset % C == 0;
+        // a column block: all R rows, extents[1] columns starting at dst_offset
+        dense_cols = c.extents[0] == R && c.extents[1] < C && c.dst_strides[0] == C && c.dst_strides[1] == 1 &&
+                     t.strides[0] == c.extents[1] && t.strides[1] == 1 && c.dst_offset < C;
+      }
+      if (pieces.empty()) by_cols = dense_cols && !dense_rows;
+      if (by_cols ? !dense_cols : !dense_rows) {
+        ok = false;
+        break;
+      }
+      if (by_cols) {
+        if (cols < 0) cols = c.extents[1];
+        ok = ok && c.extents[1] == cols;
+        pieces.push_back({c.dst_offset, t.buffer});
+      } else {
+        if (rows < 0) rows = e / C;
+        ok = ok && e / C == rows;
+        pieces.push_back({c.dst_offset / C, t.buffer});
+      }
     }
-    if (!ok || rows <= 0 || rows % kPieceRowAlign != 0 || static_cast<std::int64_t>(pieces.size()) * rows != R) continue;
+    // Piece columns: whole 64-element TMA boxes (a box never straddles two
+    // pieces along the stored inner dimension).
+    constexpr std::int64_t kPieceColAlign = 64;
+    if (!ok || pieces.empty()) continue;
+    if (by_cols ? (cols <= 0 || cols % kPieceColAlign != 0 || static_cast<std::int64_t>(pieces.size()) * cols != C)
+                : (rows <= 0 || rows % kPieceRowAlign != 0 || static_cast<std::int64_t>(pieces.size()) * rows != R))
+      continue;
     std::sort(pieces.begin(), pieces.end());
-    for (std::size_t i = 0; i < pieces.size(); ++i) ok = ok && pieces[i].first == static_cast<std::int64_t>(i) * rows;
+    const std::int64_t ext = by_cols ? cols : rows;
+    for (std::size_t i = 0; i < pieces.size(); ++i) ok = ok && pieces[i].first == static_cast<std::int64_t>(i) * ext;
     // Readers: tensor-core GEMMs only, O as one plain operand.
     std::vector<std::pair<int, int>> uses;  // (gemm, operand index)
     for (int r : readers[O]) {
@@ -1042,7 +1065,8 @@ void gather_gemm_operands(Program& P, const ProgramOptions& opt) {
     for (auto [r, j] : uses) {
       Instr& g = P.instrs[r];
       for (const auto& pc : pieces) g.gather[j].push_back(pc.second);
-      g.gather_rows[j] = rows;
+      g.gather_rows[j] = by_cols ? 0 : rows;
+      g.gather_cols[j] = by_cols ? cols : 0;
       g.in_bufs[j] = pieces[0].second;  // (O is dead: never written nor read)
       // The GEMM waits for the pieces' producers (bx's dependencies).
       for (int d : bx.deps) g.deps.push_back(d);
@@ -1789,7 +1813,8 @@ std::string Program::describe_json() const {
        << ",\"causal\":" << (in.causal ? "true" : "false") << ",\"grad\":" << in.att_grad << ",\"grad_out\":["
        << in.att_out[0] << "," << in.att_out[1] << "," << in.att_out[2] << "]},\"gather\":[";
     for (int j = 0; j < 2; ++j) {
-      os << (j ? "," : "") << "{\"rows\":" << in.gather_rows[j] << ",\"pieces\":[";
+      os << (j ? "," : "") << "{\"rows\":" << in.gather_rows[j] << ",\"cols\":" << in.gather_cols[j]
+         << ",\"pieces\":[";
       for (std::size_t q = 0; q < in.gather[j].size(); ++q) os << (q ? "," : "") << in.gather[j][q];
       os << "]}";
     }

@@ -168,8 +168,12 @@ struct Instr {
   // is gone (a nop), its output buffer is dead and in_bufs[j] names the
   // first piece; the GEMM's TMA loads read each piece where its producer
   // left it.
+  // ...or, with gather_cols[j] > 0, the column-wise concatenation of pieces
+  // of gather_cols[j] stored columns each (DAP's column halves -> GEMM: a
+  // K- or N-split of the operand); gather_rows[j] is then 0.
   std::vector<int> gather[2];
   std::int64_t gather_rows[2] = {0, 0};
+  std::int64_t gather_cols[2] = {0, 0};
   // accounting (algorithmic, from masks)
   double flops = 0;
   double bytes = 0;       // HBM bytes read + written

@@ -1153,6 +1153,8 @@ GemmArgs Executor::gemm_args(const Instr& in) const {
     a.gather_b = static_cast<int>(in.gather[1].size());
     a.gather_rows_a = in.gather_rows[0];
     a.gather_rows_b = in.gather_rows[1];
+    a.gather_cols_a = in.gather_cols[0];
+    a.gather_cols_b = in.gather_cols[1];
     for (int i = 0; i < a.gather_a; ++i) a.gather_a_ptr[i] = buf_ptr(in.gather[0][i]);
     for (int i = 0; i < a.gather_b; ++i) a.gather_b_ptr[i] = buf_ptr(in.gather[1][i]);
     a.gather_maps = irt_[in.id].gather_maps;

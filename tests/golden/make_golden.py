@@ -198,6 +198,11 @@ def cases():
                 0.0, "C5: Evoformer proxy (MSA + pair), 3F1B x DAP 2 (all-to-all), fp32"))
     out.append(("c5_3f1b_dap_bf16", docs.dumps(docs.evoformer_doc(4, (256, 4), (512, 4), 2, elem_size=2)), c5,
                 682, 2e-2, "C5: Evoformer proxy (MSA + pair), 3F1B x DAP 2 (all-to-all), bf16"))
+    # C5 at tensor-core shapes: DAP's column halves (128 channels) feed the
+    # GEMMs through the column-gather prologue, all-to-all -> max gates run
+    # inside the adapter box, the row splits are views.
+    out.append(("c5_3f1b_dap_mma", docs.dumps(docs.evoformer_doc(4, (128, 256), (256, 128), 2, elem_size=2)), c5,
+                683, 2e-2, "C5: Evoformer proxy, 3F1B x DAP 2 at tensor-core shapes (column-gathered GEMM operands), bf16"))
     out.append(("gpt_block_fwd_tp2_mma", docs.dumps(docs.gpt_block_doc(256, 128, elem_size=2, train=False)),
                 dict(strategy="megatron_tp", devices=2), 71, 2e-2,
                 "C2 forward at tensor-core-eligible shapes (bf16)"))
@@ -213,6 +218,9 @@ def cases():
                     dict(strategy="megatron_tp", devices=k), 90 + k, 2e-2,
                     "C2 Megatron TP + sequence parallel train step at tensor-core shapes (gathered GEMM operands), bf16"))
     return out
+
+
+COMPACT = {"c5_3f1b_dap_mma"}
 
 
 def main():
@@ -234,13 +242,22 @@ def main():
         if tol == 0.0 and peak >= 2.0 ** 24:
             raise SystemExit(f"{name}: |values| reach {peak}, beyond exact fp32 integers")
         arrays = {f"in_{k}": v for k, v in inputs.items()}
-        arrays.update({f"exp_{k}": v for k, v in expected.items()})
+        # Large cases (COMPACT): the reference run_plan outputs are not
+        # stored (their agreement is recorded in meta.reference_run_plan) and
+        # the expected values are a fixed subset: every 4th produced pTensor
+        # in id order.
+        compact = name in COMPACT
+        keep = sorted(expected)
+        if compact:
+            keep = keep[::4]
+        arrays.update({f"exp_{k}": expected[k] for k in keep})
         ref_status = "ok"
         try:
             ref_out, _ = refpy.run_plan(plan, inputs)
             ok, msg = refpy.compare_outputs(expected, ref_out, tol)
             ref_status = "ok" if ok else "mismatch: " + msg
-            arrays.update({f"ref_{k}": v for k, v in ref_out.items()})
+            if not compact:
+                arrays.update({f"ref_{k}": v for k, v in ref_out.items()})
         except refpy.RefError as e:
             ref_status = "throws: " + str(e)
         # bf16 plans: the plan emulated with bf16 rounding wherever the
@@ -262,7 +279,7 @@ def main():
         np.savez_compressed(os.path.join(d, "io.npz"), **arrays)
         pj = json.loads(plan)
         meta = dict(name=name, seed=seed, rel_tol=tol, provenance=prov, spec=spec, max_abs=peak,
-                    magnitude=magnitude, bf16_exact=bf16_exact,
+                    magnitude=magnitude, bf16_exact=bf16_exact, compact=compact,
                     reference_run_plan=ref_status, lanes=len(pj["lanes"]),
                     tasks=sum(len(l["tasks"]) for l in pj["lanes"]),
                     collectives=sorted({g["primitive"] for g in pj["coll_groups"]}),

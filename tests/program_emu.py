@@ -37,8 +37,9 @@ def exec_instr(ins: dict, data: dict, shape: dict):
 
         def operand(j, buf):
             # all-gather / concat -> GEMM prologue: the row pieces in order
-            if gathered[j]["pieces"]:
-                return np.concatenate([data[p].reshape(shape[p]) for p in gathered[j]["pieces"]], axis=0)
+            if gathered[j]["pieces"]:  # row pieces, or column pieces ("cols" > 0)
+                axis = 1 if gathered[j].get("cols", 0) else 0
+                return np.concatenate([data[p].reshape(shape[p]) for p in gathered[j]["pieces"]], axis=axis)
             return data[buf].reshape(shape[buf])
 
         for g in range(ins.get("group", 1)):  # grouped launch: member g = (in[2g], in[2g+1]) -> out[g]

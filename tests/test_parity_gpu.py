@@ -213,7 +213,8 @@ def test_box_batching_same_bits_fewer_launches(name):
     assert ok, msg
 
 
-@pytest.mark.parametrize("name", ["gpt_block_sp_tp2_mma", "gpt_block_sp_tp4_mma", "gpt_block_train_tp2_mma"])
+@pytest.mark.parametrize("name", ["gpt_block_sp_tp2_mma", "gpt_block_sp_tp4_mma", "gpt_block_train_tp2_mma",
+                                  "c5_3f1b_dap_mma"])
 def test_gathered_gemm_operands(name):
     """All-gather / concat -> GEMM prologue: a concat of
     row pieces feeding only tensor-core GEMMs is dropped and the GEMMs' TMA
@@ -312,7 +313,8 @@ def test_timed_mode_memory_reuse(name):
             assert kept > 0
 
 
-@pytest.mark.parametrize("name", ["c5_3f1b_dap", "c5_3f1b_dap_bf16", "c4_coshard_dp8_bf16", "embed_shard2"])
+@pytest.mark.parametrize("name", ["c5_3f1b_dap", "c5_3f1b_dap_bf16", "c5_3f1b_dap_mma", "c4_coshard_dp8_bf16",
+                                  "embed_shard2"])
 def test_box_elementwise_fusion(name):
     """An add / mul / max on a pure-copy adapter output (C5's all-to-all ->
     max gate) runs inside the adapter's box launch as fold terms: fewer
