@@ -529,7 +529,7 @@ def main():
         # a GPU add up; their adapter bytes then stay in HBM (no NVLink).
         # algorithmic work of the PLAN (every elementwise op and copy counted,
         # whatever the executor fuses, groups or aliases)
-        desc = pb.describe(plan, flags=pb.NO_FUSION | pb.NO_GROUPING)
+        desc = pb.describe(plan, flags=pb.NO_FUSION | pb.NO_GROUPING | pb.NO_GATHER)
         gpu_of = [lane % n for lane in range(nlanes)]
         F, M, W = [0.0] * n, [0.0] * n, [0.0] * n
         for ins in desc["instrs"]:

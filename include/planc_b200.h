@@ -74,6 +74,8 @@ extern "C" {
 #define PLANC_B200_NO_BOX_EW 0x4000u    /* keep an add / mul / max on a pure-copy adapter output (all-to-all,
                                            all-gather, layout change) as its own kernel (default: it runs inside
                                            the adapter's box launch as fold terms — same bits) */
+#define PLANC_B200_GATHER_COLS 0x10000u  /* the gather prologue also takes concats of column blocks along K
+                                           (opt-in: measured ~3 % slower on C5 than the materialised concat) */
 #define PLANC_B200_NO_ALIAS_VIEWS 0x8000u /* copy contiguous sub-ranges (splits) instead of aliasing them as views
                                            of their source on the same GPU (NO_ALIAS turns off every alias) */
 #define PLANC_B200_SERIAL_LANES 0x8u    /* one stream per lane: a lane's tasks run strictly in plan

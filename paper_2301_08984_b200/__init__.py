@@ -48,6 +48,7 @@ BATCH = 0x1000
 NO_GATHER = 0x2000
 NO_BOX_EW = 0x4000
 NO_ALIAS_VIEWS = 0x8000
+GATHER_COLS = 0x10000
 
 
 class PlancError(RuntimeError):

@@ -71,6 +71,7 @@ ExecOptions exec_options(uint32_t flags) {
   opt.batch_boxes = (flags & PLANC_B200_BATCH) != 0;
   opt.gather_operands = (flags & PLANC_B200_NO_GATHER) == 0;
   opt.fuse_box_ew = (flags & PLANC_B200_NO_BOX_EW) == 0;
+  opt.gather_cols = (flags & PLANC_B200_GATHER_COLS) != 0;
   return opt;
 }
 
@@ -83,6 +84,7 @@ ProgramOptions describe_options(uint32_t flags) {
   po.scatter_allreduce = (flags & PLANC_B200_NO_SCATTER) == 0 && tc;
   po.gather_operands = (flags & PLANC_B200_NO_GATHER) == 0 && tc;
   po.fuse_box_ew = (flags & PLANC_B200_NO_BOX_EW) == 0;
+  po.gather_cols = (flags & PLANC_B200_GATHER_COLS) != 0;
   return po;
 }
 

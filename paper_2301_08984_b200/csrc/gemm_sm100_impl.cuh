@@ -148,6 +148,7 @@ struct SkParams {
   // whole multiples of every box height).
   int gather_rows_a = 0, gather_rows_b = 0;
   int gather_cols_a = 0, gather_cols_b = 0;  // column pieces: a box at stored column x reads piece x / cols
+  int gather_na = 0, gather_nb = 0;          // piece counts (boxes past the last piece stay in it, out of bounds)
   const CUtensorMap* gather_maps = nullptr;
   long long sk_iters = 0;
   float* partials = nullptr;  // [sk_ctas][2 slots][4 quarters][BN/32 chunks][8][32] float4
@@ -553,6 +554,12 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&gm.a[p])) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&gm.b[p])) : "memory");
     }
+    // Gathered operands' piece maps (global memory, written at open).
+    for (int i = 0; i < sk.gather_na; ++i)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(sk.gather_maps + i)) : "memory");
+    for (int i = 0; i < sk.gather_nb; ++i)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(sk.gather_maps + kMaxGemmGroup + i))
+                   : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CL ? 2 : 1);  // cluster pairs: both CTAs' MMAs free a stage
@@ -590,14 +597,17 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       const std::uint64_t pol_a = l2_policy(sk.hint_a), pol_b = l2_policy(sk.hint_b);
       // Gathered operand: the piece holding stored row `row` (row pieces)
       // or stored column `x` (column pieces), coordinates made piece-local.
+      // A box past the operand's end (the zero tile of a 2-SM pair, a
+      // partial tile) stays in the last piece, out of bounds there: TMA
+      // zero-fills it as it would past the concatenated operand.
       auto pick_a = [&](const CUtensorMap* dflt, int& x, int& row) -> const CUtensorMap* {
         if (sk.gather_rows_a != 0) {
-          const int q = row / sk.gather_rows_a;
+          const int q = min(row / sk.gather_rows_a, sk.gather_na - 1);
           row -= q * sk.gather_rows_a;
           return sk.gather_maps + q;
         }
         if (sk.gather_cols_a != 0) {
-          const int q = x / sk.gather_cols_a;
+          const int q = min(x / sk.gather_cols_a, sk.gather_na - 1);
           x -= q * sk.gather_cols_a;
           return sk.gather_maps + q;
         }
@@ -605,12 +615,12 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
       };
       auto pick_b = [&](const CUtensorMap* dflt, int& x, int& row) -> const CUtensorMap* {
         if (sk.gather_rows_b != 0) {
-          const int q = row / sk.gather_rows_b;
+          const int q = min(row / sk.gather_rows_b, sk.gather_nb - 1);
           row -= q * sk.gather_rows_b;
           return sk.gather_maps + kMaxGemmGroup + q;
         }
         if (sk.gather_cols_b != 0) {
-          const int q = x / sk.gather_cols_b;
+          const int q = min(x / sk.gather_cols_b, sk.gather_nb - 1);
           x -= q * sk.gather_cols_b;
           return sk.gather_maps + kMaxGemmGroup + q;
         }
@@ -1309,6 +1319,8 @@ void launch_typed_ng(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) 
     sk.gather_rows_b = static_cast<int>(a.gather_rows_b);
     sk.gather_cols_a = static_cast<int>(a.gather_cols_a);
     sk.gather_cols_b = static_cast<int>(a.gather_cols_b);
+    sk.gather_na = a.gather_a;
+    sk.gather_nb = a.gather_b;
     sk.gather_maps = static_cast<const CUtensorMap*>(a.gather_maps);
   }
   const std::int64_t m_pad = (a.m + BM - 1) / BM * BM, n_pad = (a.n + BN - 1) / BN * BN;

@@ -1037,7 +1037,7 @@ void gather_gemm_operands(Program& P, const ProgramOptions& opt) {
     // Piece columns: whole 64-element TMA boxes (a box never straddles two
     // pieces along the stored inner dimension).
     constexpr std::int64_t kPieceColAlign = 64;
-    if (!ok || pieces.empty()) continue;
+    if (!ok || pieces.empty() || (by_cols && !opt.gather_cols)) continue;
     if (by_cols ? (cols <= 0 || cols % kPieceColAlign != 0 || static_cast<std::int64_t>(pieces.size()) * cols != C)
                 : (rows <= 0 || rows % kPieceRowAlign != 0 || static_cast<std::int64_t>(pieces.size()) * rows != R))
       continue;
@@ -1059,7 +1059,17 @@ void gather_gemm_operands(Program& P, const ProgramOptions& opt) {
         ok = false;
         break;
       }
-      uses.push_back({r, g.in_bufs[0] == O ? 0 : 1});
+      const int j = g.in_bufs[0] == O ? 0 : 1;
+      // Column pieces only along K (A stored [m][k], B stored [n][k]): the
+      // piece then changes every cols / BK k-blocks. Along M or N every
+      // k-block's boxes alternate between the pieces' tensor maps, which
+      // measured ~1.8x slower on C5's 2-SM dW GEMMs (TMA descriptor
+      // switches; profiles/r02/ab_col_gather.jsonl).
+      if (by_cols && (j == 0 ? g.ta : !g.tb)) {
+        ok = false;
+        break;
+      }
+      uses.push_back({r, j});
     }
     if (!ok || uses.empty()) continue;
     for (auto [r, j] : uses) {

@@ -222,6 +222,9 @@ struct ProgramOptions {
   // all-gather / concat -> GEMM prologue. Single-process and peer-memory
   // modes (the pieces must be addressable by the GEMM's lane).
   bool gather_operands = true;
+  // ...column pieces too (opt-in, flag GATHER_COLS): along K only; measured
+  // ~3 % slower on C5 than the materialised concat (profiles/r02/ab_col_gather.jsonl).
+  bool gather_cols = false;
   // An elementwise op (add / mul / max) whose operand is the output of a
   // pure-copy box instruction (an all-to-all / all-gather / layout adapter)
   // read by nothing else runs inside that box: the other operands become

@@ -190,6 +190,7 @@ Executor::Executor(const std::string& plan_json, const std::vector<int>& lane_gp
   po.two_phase_allreduce = !(rank && !rank->peer_memory);
   // Gathered operands read pieces in place: not across NCCL ranks.
   po.gather_operands = opt.gather_operands && opt.allow_tensor_cores && !(rank && !rank->peer_memory);
+  po.gather_cols = opt.gather_cols;
   // Box -> elementwise fusion: single-process and peer-memory modes
   // (PLANC_B200_BOX_EW=0 for A/B).
   static const bool box_ew_env = [] {

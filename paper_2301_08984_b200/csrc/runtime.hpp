@@ -63,6 +63,7 @@ struct ExecOptions {
   bool batch_boxes = false;
   bool gather_operands = true;          // concat / all-gather feeding only GEMMs: GEMMs read the pieces in place
   bool fuse_box_ew = true;              // elementwise ops on a pure-copy adapter output run inside the box
+  bool gather_cols = false;             // column-piece gathers too (opt-in)
 };
 
 // ProgramOptions as the executor uses them: epilogue fusion only for GEMMs

@@ -79,3 +79,4 @@ def test_partition_invariance_at_full_size(base, parts):
             assert np.isfinite(got[i]).all(), (name, i)
         ok, msg = pb.compare_outputs(ref, got, 2e-2, normwise=True)
         assert ok, f"{name} vs {base}: {msg}"
+

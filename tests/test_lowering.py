@@ -527,3 +527,24 @@ def test_box_elementwise_fusion_lowering():
         assert np.array_equal(a[k], b[k]), k
     ok, msg = pb.compare_outputs(g["expected"], a, 0.0)
     assert ok, msg
+
+
+def test_column_gather_lowering():
+    """GATHER_COLS: concats of column blocks along K feeding tensor-core GEMMs
+    become column-gathered operands (pieces of 64k stored columns, the concat
+    buffer dead); the lowered program still reproduces the reference."""
+    g = golden_cases.load("c5_3f1b_dap_mma")
+    desc = pb.describe(g["plan"], flags=pb.GATHER_COLS)
+    cols = [i for i in desc["instrs"] if i["kind"] == "gemm" and any(x["cols"] for x in i["gather"])]
+    assert cols
+    for i in cols:
+        for j, x in enumerate(i["gather"]):
+            if x["cols"]:
+                assert x["cols"] % 64 == 0 and x["rows"] == 0 and len(x["pieces"]) >= 2
+                assert (not i["ta"]) if j == 0 else i["tb"]  # K is the stored column axis
+    assert not any(any(x["cols"] for x in i["gather"]) for i in pb.describe(g["plan"])["instrs"]
+                   if i["kind"] == "gemm")  # opt-in
+    out = run_program(desc, json.loads(g["plan"]), g["inputs"])
+    tol = 0.0 if g["meta"].get("max_abs", 0) < 2.0 ** 53 else 1e-12
+    ok, msg = pb.compare_outputs(g["expected"], out, tol, normwise=True)
+    assert ok, msg

@@ -221,25 +221,26 @@ def test_gathered_gemm_operands(name):
     loads read the pieces in place. Same operands, same bits as the
     materialised concat (NO_GATHER), and the bf16 plan emulation's bits."""
     g = golden_cases.load(name)
-    desc = pb.describe(g["plan"])
+    on = pb.GATHER_COLS if name.startswith("c5_") else 0  # column pieces: opt-in
+    desc = pb.describe(g["plan"], flags=on)
     gathers = [i for i in desc["instrs"] if i["kind"] == "gemm" and any(x["pieces"] for x in i["gather"])]
     assert gathers, "the plan has no gathered GEMM operand"
     outs, kernels = {}, {}
-    for flags in (0, pb.NO_GATHER):
+    for flags in (on, pb.NO_GATHER):
         out, st = _run(g["plan"], g["inputs"], flags=flags)
         outs[flags], kernels[flags] = out, st["kernels_per_step"]
     # (a single-piece "gather" reads an identity's source: on one GPU that
     # copy is already an alias, so no kernel is saved there)
-    assert kernels[0] <= kernels[pb.NO_GATHER]
-    if "_sp_" in name:
-        assert kernels[0] < kernels[pb.NO_GATHER]
-    for k in outs[0]:
-        assert np.array_equal(outs[0][k], outs[pb.NO_GATHER][k]), k
-    ok, msg = pb.compare_outputs(g["expected"], outs[0], g["meta"]["rel_tol"], normwise=True)
+    assert kernels[on] <= kernels[pb.NO_GATHER]
+    if "_sp_" in name or on:
+        assert kernels[on] < kernels[pb.NO_GATHER]
+    for k in outs[on]:
+        assert np.array_equal(outs[on][k], outs[pb.NO_GATHER][k]), k
+    ok, msg = pb.compare_outputs(g["expected"], outs[on], g["meta"]["rel_tol"], normwise=True)
     assert ok, msg
     if g["meta"].get("bf16_exact"):
         for k, v in g["emulated"].items():
-            assert np.array_equal(outs[0][k], v), k
+            assert np.array_equal(outs[on][k], v), k
 
 
 def test_same_gpu_copies_become_aliases():
@@ -351,3 +352,29 @@ def test_same_gpu_splits_become_views(name):
         assert np.array_equal(outs[0][k], outs[pb.NO_ALIAS_VIEWS][k]), k
     ok, msg = pb.compare_outputs(g["expected"], outs[0], g["meta"]["rel_tol"], normwise=True)
     assert ok, msg
+
+
+@pytest.mark.parametrize("name", ["c5_3f1b_dap", "c2sp_tp2"])
+def test_gathered_operands_at_full_size(name):
+    """The gather prologue at the benchmark shapes (C5: column pieces of the
+    DAP channel halves, incl. the 2-SM dW GEMMs whose zero tile reads past
+    the last piece; C2-SP: row pieces): the terminal outputs are bit-equal
+    to the materialised concats' (NO_GATHER)."""
+    from test_fullsize_gpu import init_inputs, terminal_outputs  # (puts the repo root on sys.path)
+    import bench
+
+    plan, _ = bench.load_plan(name)
+    inputs = init_inputs(plan)
+    ids = terminal_outputs(plan)
+    nl = len(json.loads(plan)["lanes"])
+    on = pb.GATHER_COLS if name.startswith("c5_") else 0  # column pieces: opt-in
+    outs = {}
+    for flags in (on, pb.NO_GATHER):
+        with pb.Executor(plan, lane_gpus=[0] * nl, flags=flags) as ex:
+            ex.set_inputs(inputs)
+            ex.run(0)
+            outs[flags] = {i: ex.get_output(i) for i in ids}
+    for i in ids:
+        assert np.isfinite(outs[on][i]).all(), i
+        assert np.array_equal(outs[on][i], outs[pb.NO_GATHER][i]), i
+
