@@ -345,7 +345,10 @@ def test_two_sm_variant_vs_fp64(g, m, n, k, ta, tb, monkeypatch):
 
 @pytest.mark.parametrize("two_sm", ["0", "2"])
 @pytest.mark.parametrize("m,n,k,ta,tb", [(4096, 1024, 2048, False, False), (1000, 512, 768, True, False),
-                                         (384, 256, 512, False, True)])
+                                         (384, 256, 512, False, True),
+                                         # several tiles per CTA with a partial last wave (the
+                                         # epilogue's operand prefetch runs across tile boundaries)
+                                         (8192, 2048, 2048, False, False), (2000, 1536, 1024, False, True)])
 def test_fused_epilogue_vs_fp64(m, n, k, ta, tb, two_sm, monkeypatch):
     """C = op(A)·op(B), E = C + D with the add fused into the GEMM's epilogue
     (default lowering), on the one-CTA and the 2-SM variant: C and E equal
