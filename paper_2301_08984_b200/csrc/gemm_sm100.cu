@@ -118,10 +118,17 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   // lane's dependency chain and their concurrent work fills the SMs anyway
   // (C5 2.57 -> 2.35 ms, C4 5.34 -> 5.26 ms without it;
   // profiles/r02/ab_knobs_c4_c5.jsonl). =2 forces it.
-  // PLANC_B200_SPLITK_SHARED=1: co-resident lanes split long-k GEMMs too,
-  // within their share of the SMs (sms / lanes on the GPU).
+  // Exception: a long-k GEMM with a tiny output (C5's dW GEMMs: 128 x 128 x
+  // 8192 and 256 x 256 x 4096, one or two tiles — 2-4 SMs for 40-60 us, a
+  // link of its lane's chain) is split within the lane's share of the SMs
+  // (sms / lanes on the GPU) when that gives >= 4 splits: C5 2.42 -> 2.30
+  // ms. With 2 splits (C4's 512 x 512 x 16384 dW) the reduce launch costs
+  // more than it saves (C4 5.38 -> 5.52 ms; profiles/r02/ab_shared_split.json).
+  // PLANC_B200_SPLITK_SHARED=0 disables, =2 allows 2 splits as well.
   const char* shenv = std::getenv("PLANC_B200_SPLITK_SHARED");
-  const bool shared_split = shenv && shenv[0] == '1' && a.gpu_share > 1;
+  const int shmode = shenv ? std::atoi(shenv) : 1;
+  const bool shared_split = shmode != 0 && a.gpu_share > 1;
+  const int min_splits = a.allow_streamk || splitmode == 2 || shmode == 2 ? 2 : 4;
   const bool allow_split = splitmode != 0 && !a.no_workspace && a.epi.n_ops == 0 && a.scatter == 0 &&
                            (a.allow_streamk || splitmode == 2 || shared_split);
   const int split_sms = a.allow_streamk ? sms : std::max(2, sms / std::max(a.gpu_share, 1));
@@ -141,7 +148,7 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
     GemmSchedule c = (sk.sk_ctas > 0 && (skmode == 2 || sk.model_us < 0.9 * dp.model_us)) ? sk : dp;
     if (allow_split) {
       GemmSchedule sp = splitk_for(a.m, a.n, a.k, bn, split_sms, a.group, a.dc == DT_BF16 ? 2 : 4);
-      if (sp.splits > 1 && (splitmode == 2 || sp.model_us < 0.9 * c.model_us)) c = sp;
+      if (sp.splits >= min_splits && (splitmode == 2 || sp.model_us < 0.9 * c.model_us)) c = sp;
     }
     if (!have || c.model_us < best.model_us * 0.97) {
       best = c;

@@ -1552,4 +1552,26 @@ void launch_peer_flags(const unsigned* epoch, const PeerFlags& f, unsigned long 
   check_launch("peer_flags_kernel");
 }
 
+// Host gate (profiling): holds a stream until the host sets *flag, so the
+// instruction enqueued behind it starts right after the preceding event
+// record instead of after the host's launch latency — per-instruction event
+// times then measure the kernels, not the enqueue. Gives up after 2 s.
+namespace {
+__global__ void host_gate_kernel(const volatile unsigned* flag) {
+  std::uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*flag == 0) {
+    std::uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 2000000000ull) break;
+    __nanosleep(200);
+  }
+}
+}  // namespace
+
+void launch_host_gate(const unsigned* flag, cudaStream_t s) {
+  host_gate_kernel<<<1, 32, 0, s>>>(flag);
+  check_launch("host_gate_kernel");
+}
+
 }  // namespace planc_b200

@@ -161,6 +161,9 @@ struct GemmSchedule {
 constexpr int kBoxChunkUnits = 1024;
 void launch_box(int dtype, const DevCell* cells, const DevTerm* terms, const DevChunk* chunks,
                 int nchunks, int vec, int max_rank, cudaStream_t s);
+// Profiling: blocks stream s until the host writes a nonzero *flag
+// (mapped pinned memory), at most 2 s.
+void launch_host_gate(const unsigned* flag, cudaStream_t s);
 void launch_ew(int op, int dtype, const void* const* ins, int nin, void* out, std::int64_t count, cudaStream_t s);
 // reduce-sum over the middle axis of [outer][axis_len][inner]; column
 // reductions (inner > 1) split the axis over blocks with fp32 partials in

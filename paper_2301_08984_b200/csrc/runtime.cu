@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <set>
 #include <sstream>
@@ -1590,6 +1591,17 @@ std::vector<KernelStat> Executor::profile() {
   }
   std::map<std::string, KernelStat> acc;
   std::vector<std::string> order;
+  // Each instruction runs alone, enqueued behind a host gate: start event,
+  // launches, end event are all queued before the gate opens, so the
+  // interval holds the instruction's kernels back to back — not the host's
+  // launch latency (which would dominate a 2-us kernel's measurement).
+  unsigned* gate = nullptr;
+  ck(cudaHostAlloc(reinterpret_cast<void**>(&gate), sizeof(unsigned), cudaHostAllocMapped | cudaHostAllocPortable),
+     "cudaHostAlloc (profile gate)");
+  struct GateFree {
+    unsigned* p;
+    ~GateFree() { cudaFreeHost(p); }
+  } gate_free{gate};
   for (int id : prog_.issue_order) {
     const Instr& in = prog_.instrs[id];
     const int el = exec_lane_[id];
@@ -1602,9 +1614,15 @@ std::vector<KernelStat> Executor::profile() {
     ck(cudaEventCreate(&a), "event");
     ck(cudaEventCreate(&b), "event");
     peer_wait(id, s);
+    unsigned* gate_dev = nullptr;
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&gate_dev), gate, 0), "gate pointer");
+    *reinterpret_cast<volatile unsigned*>(gate) = 0;
+    launch_host_gate(gate_dev, s);
     ck(cudaEventRecord(a, s), "record");
     launch_instr(in, s);
     ck(cudaEventRecord(b, s), "record");
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    *reinterpret_cast<volatile unsigned*>(gate) = 1;
     peer_signal(id, s);
     check_sync(cudaEventSynchronize(b), "sync");
     float ms = 0;

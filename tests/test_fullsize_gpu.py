@@ -80,3 +80,29 @@ def test_partition_invariance_at_full_size(base, parts):
         ok, msg = pb.compare_outputs(ref, got, 2e-2, normwise=True)
         assert ok, f"{name} vs {base}: {msg}"
 
+
+
+def test_shared_gpu_split_k_at_full_size(monkeypatch):
+    """C5 at N=1 (8 lanes on one GPU): its tiny-output long-k dW GEMMs are
+    split-K'd within each lane's share of the SMs (gemm_sm100.cu) — more
+    launches, the same results within bf16 summation-order noise, and the
+    same bits on every run (splits summed in fixed order)."""
+    plan, _ = bench.load_plan("c5_3f1b_dap")
+    inputs = init_inputs(plan)
+    ids = terminal_outputs(plan)
+    nl = len(json.loads(plan)["lanes"])
+    res, kernels = {}, {}
+    for mode in ("1", "1", "0"):
+        monkeypatch.setenv("PLANC_B200_SPLITK_SHARED", mode)
+        with pb.Executor(plan, lane_gpus=[0] * nl) as ex:
+            ex.set_inputs(inputs)
+            ex.run(0)
+            out = {i: ex.get_output(i) for i in ids}
+            kernels.setdefault(mode, ex.stats()["kernels_per_step"])
+        if mode in res:
+            for i in ids:
+                assert np.array_equal(out[i], res[mode][i]), i  # deterministic
+        res[mode] = out
+    assert kernels["1"] > kernels["0"]  # split GEMMs + their reduce launches
+    ok, msg = pb.compare_outputs(res["0"], res["1"], 2e-2, normwise=True)
+    assert ok, msg
