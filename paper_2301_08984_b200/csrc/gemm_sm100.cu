@@ -176,9 +176,15 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   // (BN/32 TMEM chunks per warp) outlasts the tile's few k-blocks of MMAs,
   // so 8 epilogue warps split each tile's columns. PLANC_B200_EPI8=0
   // disables it, =2 forces it on plain data-parallel launches.
+  // Fused elementwise epilogues too (C4's 16384 x 512 x 512 GEMMs with their
+  // add / mul: the fold and the second store double the epilogue's work);
+  // PLANC_B200_EPI8_FUSED=0 keeps those on four epilogue warps.
   const char* e8 = std::getenv("PLANC_B200_EPI8");
   const int e8mode = e8 ? std::atoi(e8) : 1;
-  if (e8mode != 0 && best.occ == 1 && a.epi.n_ops == 0 && a.scatter == 0 && best.splits <= 1 && best.sk_ctas == 0 &&
+  const char* e8f = std::getenv("PLANC_B200_EPI8_FUSED");
+  const bool e8fused = !(e8f && e8f[0] == '0');
+  if (e8mode != 0 && best.occ == 1 && (a.epi.n_ops == 0 || e8fused) && a.scatter == 0 && best.splits <= 1 &&
+      best.sk_ctas == 0 &&
       best.half_items == 0 && (e8mode == 2 || num_k <= 16)) {
     best.occ = 3;
   }

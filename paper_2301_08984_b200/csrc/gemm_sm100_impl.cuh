@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(cta_threads(OCC), OCC == 2 ? 2 : 1)
     gemm_tc_kernel(const __grid_constant__ GroupMaps<NG> gm, int ng, int m, int n, int k,
                    const __grid_constant__ EpiParams epi, const __grid_constant__ EpiMaps maps,
                    const __grid_constant__ SkParams sk) {
-  static_assert(OCC == 1 || OCC == 5 || (!FUSE && (OCC >= 3 || BN <= 128)),
+  static_assert(OCC == 1 || OCC == 3 || OCC == 5 || (!FUSE && (OCC >= 3 || BN <= 128)),
                 "two CTAs per SM: no fusion, <= 256 TMEM columns");
   static_assert(OCC < 4 || BN >= 128, "cluster pairs split B tiles in 64-wide halves");
   constexpr bool CL = OCC == 4;   // pair sharing B by multicast, one MMA per CTA
@@ -1372,6 +1372,7 @@ void launch_typed(const GemmArgs& a, const GemmSchedule& sc, cudaStream_t s) {
     if constexpr (BN >= 128) {
       if (sc.occ == 5) return launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1, 5>(a, sc, s);
     }
+    if (sc.occ == 3) return launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1, 3>(a, sc, s);
     launch_typed_ng<A_MN, B_MN, C_BF16, BN, FUSE, 1>(a, sc, s);
   } else if (sc.occ == 4 || sc.occ == 5) {
     if constexpr (BN >= 128) {
