@@ -155,6 +155,20 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
       have = true;
     }
   }
+  // Fused short-k launches: a tile's epilogue (fold + two stores per chunk)
+  // outlasts its few k-blocks, and with ~1.7 tiles per CTA (C4's 16384 x 512
+  // x 512: 256 tiles of 128 x 256) it barely overlaps the next mainloop
+  // (profiles/r02/ncu_fused_shortk_c4.json): 128-wide tiles instead (twice
+  // the tiles per CTA, half-length epilogues) — C4 5.27 -> 5.15 ms, 64-wide
+  // 5.83 (profiles/r02/ab_fused_short_k_bn.json). PLANC_B200_FUSED_SHORTK_BN=0
+  // leaves the width to the model.
+  const std::int64_t nk_fs = (a.k + BK - 1) / BK;
+  static const int fused_bn = [] {
+    const char* e = std::getenv("PLANC_B200_FUSED_SHORTK_BN");
+    return e ? std::atoi(e) : 128;
+  }();
+  if (a.epi.n_ops > 0 && nk_fs <= 16 && !forced && fused_bn == 128 && fused_bn < best.bn)
+    best = schedule_for(a.m, a.n, a.k, fused_bn, false, sms, false, a.group, false);
   // Short-k GEMMs (<= 16 k-blocks: latency-bound tiles) that cannot fill
   // the GPU on their own (<= sms tiles of 128 x 128) take the two-CTAs-per-SM
   // variant (BN <= 128, a ~76 KB ring): a concurrent small GEMM of another
@@ -183,7 +197,10 @@ GemmSchedule gemm_sm100_schedule(const GemmArgs& a, int sms) {
   const int e8mode = e8 ? std::atoi(e8) : 1;
   const char* e8f = std::getenv("PLANC_B200_EPI8_FUSED");
   const bool e8fused = !(e8f && e8f[0] == '0');
-  if (e8mode != 0 && best.occ == 1 && (a.epi.n_ops == 0 || e8fused) && a.scatter == 0 && best.splits <= 1 &&
+  // (fused: >= 128-wide tiles — the fused chunk loop walks column chunks in
+  // pairs, and a 64-wide tile gives each of the eight warps a single chunk)
+  if (e8mode != 0 && best.occ == 1 && (a.epi.n_ops == 0 || (e8fused && best.bn >= 128)) && a.scatter == 0 &&
+      best.splits <= 1 &&
       best.sk_ctas == 0 &&
       best.half_items == 0 && (e8mode == 2 || num_k <= 16)) {
     best.occ = 3;

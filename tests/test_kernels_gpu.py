@@ -350,7 +350,8 @@ def test_two_sm_variant_vs_fp64(g, m, n, k, ta, tb, monkeypatch):
                                          # epilogue's operand prefetch runs across tile boundaries)
                                          (8192, 2048, 2048, False, False), (2000, 1536, 1024, False, True),
                                          # short k: eight epilogue warps (C4's shape)
-                                         (16384, 512, 512, False, False), (16384, 512, 512, False, True)])
+                                         (16384, 512, 512, False, False), (16384, 512, 512, False, True),
+                                         (8192, 64, 512, False, False)])
 def test_fused_epilogue_vs_fp64(m, n, k, ta, tb, two_sm, monkeypatch):
     """C = op(A)·op(B), E = C + D with the add fused into the GEMM's epilogue
     (default lowering), on the one-CTA and the 2-SM variant: C and E equal
